@@ -1,0 +1,295 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes wrapper around oracle/pbng_oracle.c (plain serial fp64 C).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may import
+this module.  It performs argument marshalling only; all arithmetic is in pbng_oracle.c.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "pbng_oracle.c")
+_SO = os.path.join(_HERE, "liborc.so")
+_lock = threading.Lock()
+_lib = None
+
+ACCEL = {"none": 0, "sor": 1, "chebyshev": 2}
+MODEL = {"nh": 0, "fcr": 1}
+ERR = {0: "ok", 1: "invalid argument", 2: "degenerate element", 3: "isolated vertex", 4: "out of memory"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, bad=-1):
+        super().__init__(f"oracle error {code} ({ERR.get(code, '?')}), index {bad}")
+        self.code = code
+        self.bad = bad
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile the oracle with gcc (serial, -O2, no FP contraction so the arithmetic is as written)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        tmp = _SO + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-std=c99", "-fPIC", "-shared",
+                               "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _SO)
+    return _SO
+
+
+class _Scene(C.Structure):
+    _fields_ = [
+        ("nv", C.c_int64), ("X", C.c_void_p), ("nt", C.c_int64), ("tets", C.c_void_p),
+        ("model", C.c_int32), ("E", C.c_void_p), ("nE", C.c_int64), ("nu", C.c_double),
+        ("density", C.c_double), ("gravity", C.c_double * 3), ("npin", C.c_int64), ("pinned", C.c_void_p),
+        ("nwc", C.c_int64), ("wc_n0", C.c_void_p), ("wc_n1", C.c_void_p), ("wc_idx0", C.c_void_p),
+        ("wc_idx1", C.c_void_p), ("wc_w0", C.c_void_p), ("wc_w1", C.c_void_p), ("wc_anchor", C.c_void_p),
+        ("wc_K", C.c_void_p),
+    ]
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            L = C.CDLL(build_oracle())
+            vp, d, i64, i32 = C.c_void_p, C.c_double, C.c_int64, C.c_int32
+            L.orc_cofactor.argtypes = [vp, vp]
+            L.orc_det.argtypes = [vp]
+            L.orc_det.restype = d
+            L.orc_lame.argtypes = [d, d, vp, vp]
+            L.orc_lame.restype = C.c_int
+            L.orc_polar.argtypes = [vp, vp]
+            L.orc_psi.argtypes = [C.c_int, d, d, vp, C.c_int]
+            L.orc_psi.restype = d
+            L.orc_piola.argtypes = [C.c_int, d, d, vp, vp]
+            L.orc_mod_hess_density.argtypes = [d, d, vp, vp]
+            L.orc_prepare.argtypes = [C.POINTER(_Scene), C.POINTER(vp), C.POINTER(i64)]
+            L.orc_prepare.restype = C.c_int
+            L.orc_free.argtypes = [vp]
+            L.orc_num_colours.argtypes = [vp]
+            L.orc_num_colours.restype = i32
+            L.orc_get_colour.argtypes = [vp, vp]
+            L.orc_get_rest.argtypes = [vp, vp, vp]
+            L.orc_get_fext.argtypes = [vp, vp]
+            L.orc_deformation_gradient.argtypes = [vp, vp, i64, vp]
+            L.orc_nodal.argtypes = [vp, vp, i64, vp, vp]
+            L.orc_sweep.argtypes = [vp, vp]
+            L.orc_sweep.restype = i64
+            L.orc_chebyshev_omega.argtypes = [i64, d]
+            L.orc_chebyshev_omega.restype = d
+            L.orc_iterate.argtypes = [vp, vp, vp, i64, i32, i32, d, d, d]
+            L.orc_iterate.restype = i64
+            L.orc_forces.argtypes = [vp, vp, vp]
+            L.orc_residual.argtypes = [vp, vp]
+            L.orc_residual.restype = d
+            L.orc_energy.argtypes = [vp, vp, vp]
+            L.orc_energy.restype = d
+            _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _mat(F):
+    return np.ascontiguousarray(np.asarray(F, dtype=np.float64).reshape(3, 3))
+
+
+def lame(E: float, nu: float):
+    mu, lam = C.c_double(), C.c_double()
+    st = lib().orc_lame(E, nu, C.byref(mu), C.byref(lam))
+    if st:
+        raise OracleError(st)
+    return mu.value, lam.value
+
+
+def cofactor(F):
+    F = _mat(F)
+    out = np.empty((3, 3))
+    lib().orc_cofactor(_p(F), _p(out))
+    return out
+
+
+def polar(F):
+    F = _mat(F)
+    out = np.empty((3, 3))
+    lib().orc_polar(_p(F), _p(out))
+    return out
+
+
+def psi(model: str, mu: float, lam: float, F, raw: bool = False) -> float:
+    F = _mat(F)
+    return lib().orc_psi(MODEL[model], mu, lam, _p(F), int(raw))
+
+
+def piola(model: str, mu: float, lam: float, F):
+    F = _mat(F)
+    out = np.empty((3, 3))
+    lib().orc_piola(MODEL[model], mu, lam, _p(F), _p(out))
+    return out
+
+
+def mod_hess_density(mu: float, lam: float, F):
+    """Ctilde as a 9x9 matrix, row (alpha,gamma) = 3*alpha+gamma, column (beta,delta) = 3*beta+delta."""
+    F = _mat(F)
+    out = np.empty((9, 9))
+    lib().orc_mod_hess_density(mu, lam, _p(F), _p(out))
+    return out
+
+
+def chebyshev_omega(m: int, rho: float) -> float:
+    return lib().orc_chebyshev_omega(m, rho)
+
+
+class Oracle:
+    """Prepared oracle for one sample of a scene (scenes.Scene)."""
+
+    def __init__(self, scene, sample: int = 0):
+        L = lib()
+        self.scene = scene
+        self.sample = sample
+        self._keep = []
+
+        def keep(a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            self._keep.append(a)
+            return _p(a)
+
+        s = _Scene()
+        s.nv = scene.n_vertices
+        s.X = keep(scene.X, np.float64)
+        s.nt = scene.n_tets
+        s.tets = keep(scene.tets if scene.n_tets else np.zeros((1, 4), np.int32), np.int32)
+        s.model = MODEL[scene.model]
+        s.E = keep(scene.E, np.float64)
+        s.nE = int(np.asarray(scene.E).size)
+        s.nu = scene.nu
+        s.density = scene.density
+        for k in range(3):
+            s.gravity[k] = float(scene.gravity[k])
+        s.npin = int(scene.pinned.size)
+        s.pinned = keep(scene.pinned if scene.pinned.size else np.zeros(1, np.int32), np.int32)
+        wc = scene.wc
+        if wc is None:
+            s.nwc = 0
+            z4 = np.zeros((1, 4), np.int32)
+            s.wc_n0 = keep(np.zeros(1, np.int32), np.int32)
+            s.wc_n1 = keep(np.zeros(1, np.int32), np.int32)
+            s.wc_idx0 = keep(z4, np.int32)
+            s.wc_idx1 = keep(z4, np.int32)
+            s.wc_w0 = keep(np.zeros((1, 4)), np.float64)
+            s.wc_w1 = keep(np.zeros((1, 4)), np.float64)
+            s.wc_anchor = keep(np.zeros((1, 3)), np.float64)
+            s.wc_K = keep(np.zeros((1, 6)), np.float64)
+        else:
+            s.nwc = int(wc["n0"].shape[0])
+            s.wc_n0 = keep(wc["n0"], np.int32)
+            s.wc_n1 = keep(wc["n1"], np.int32)
+            s.wc_idx0 = keep(wc["idx0"], np.int32)
+            s.wc_idx1 = keep(wc["idx1"], np.int32)
+            s.wc_w0 = keep(wc["w0"], np.float64)
+            s.wc_w1 = keep(wc["w1"], np.float64)
+            s.wc_anchor = keep(wc["anchor"], np.float64)
+            s.wc_K = keep(wc["K"], np.float64)
+        handle = C.c_void_p()
+        bad = C.c_int64(-1)
+        st = L.orc_prepare(C.byref(s), C.byref(handle), C.byref(bad))
+        self._keep = []
+        if st:
+            raise OracleError(st, bad.value)
+        self._h = handle
+        self.nv = scene.n_vertices
+        self.nt = scene.n_tets
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.orc_free(h)
+            self._h = None
+
+    # ---- precompute getters ------------------------------------------------------------------------
+    @property
+    def n_colours(self) -> int:
+        return int(lib().orc_num_colours(self._h))
+
+    def colours(self) -> np.ndarray:
+        out = np.empty(self.nv, np.int32)
+        lib().orc_get_colour(self._h, _p(out))
+        return out
+
+    def rest(self):
+        B = np.empty((max(self.nt, 1), 3, 3))
+        V = np.empty(max(self.nt, 1))
+        lib().orc_get_rest(self._h, _p(B), _p(V))
+        return B[:self.nt], V[:self.nt]
+
+    def fext(self) -> np.ndarray:
+        out = np.empty((self.nv, 3))
+        lib().orc_get_fext(self._h, _p(out))
+        return out
+
+    # ---- evaluation --------------------------------------------------------------------------------
+    def _x(self, x):
+        x = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(self.nv, 3))
+        return x
+
+    def deformation_gradient(self, x, e: int):
+        x = self._x(x)
+        F = np.empty((3, 3))
+        lib().orc_deformation_gradient(self._h, _p(x), e, _p(F))
+        return F
+
+    def nodal(self, x, i: int):
+        x = self._x(x)
+        f = np.empty(3)
+        A = np.empty((3, 3))
+        lib().orc_nodal(self._h, _p(x), int(i), _p(f), _p(A))
+        return f, A
+
+    def forces(self, x) -> np.ndarray:
+        x = self._x(x)
+        out = np.empty((self.nv, 3))
+        lib().orc_forces(self._h, _p(x), _p(out))
+        return out
+
+    def residual(self, x) -> float:
+        x = self._x(x)
+        return float(lib().orc_residual(self._h, _p(x)))
+
+    def energy(self, x, parts: bool = False):
+        x = self._x(x)
+        pr = np.empty(3)
+        e = float(lib().orc_energy(self._h, _p(x), _p(pr)))
+        return (e, pr) if parts else e
+
+    # ---- iteration ---------------------------------------------------------------------------------
+    def sweep(self, x) -> np.ndarray:
+        w = self._x(x).copy()
+        fails = lib().orc_sweep(self._h, _p(w))
+        if fails:
+            raise RuntimeError(f"{fails} nodal solves failed")
+        return w
+
+    def iterate(self, x, xm1, l0: int, n: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0,
+                gamma: float = 1.0):
+        """n accelerated PBNG iterations from iteration index l0; returns (x^{l0+n}, x^{l0+n-1})."""
+        x = self._x(x).copy()
+        xm1 = self._x(xm1).copy()
+        fails = lib().orc_iterate(self._h, _p(x), _p(xm1), int(l0), int(n), ACCEL[accel], float(omega),
+                                  float(rho), float(gamma))
+        if fails:
+            raise RuntimeError(f"{fails} nodal solves failed")
+        return x, xm1
+
+    def run(self, iterations=None, x0=None):
+        """The scene's full run from x^0 (x^{-1} = x^0): returns x^L."""
+        sc = self.scene
+        L = sc.iterations if iterations is None else iterations
+        x = sc.x0[self.sample] if x0 is None else x0
+        xL, _ = self.iterate(x, x, 0, L, sc.accel, sc.omega, sc.rho, sc.gamma)
+        return xL

@@ -1,0 +1,741 @@
+/*
+ * oracle/pbng_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, serial, fp64 CPU reference ("oracle") for the hot path of
+ *   Chen, Han, Chen, Teran, "Position-Based Nonlinear Gauss-Seidel for Quasistatic Hyperelasticity",
+ *   arXiv 2306.09021 (the paper text is PAPER.md; line numbers below are PAPER.md lines).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may load
+ * this file.  It shares no code, header, table or constant generator with the CUDA path
+ * (paper_2306_09021_b200/csrc) and neither side includes or links the other.
+ *
+ * Every function follows the paper's definitions in the paper's order and notation; nothing is fused,
+ * blocked or reordered.  Readings of silent / garbled passages:
+ *   Z1  Neo-Hookean energy shifted by a constant so that Psi(I) = 0 (forces unchanged).
+ *   Z2  the modified Hessian density uses the Lame lambda (not lambda-hat) for every model.
+ *   Z3  "J F^{-1}" in eq:mod_hess_dens is the cofactor matrix cof(F) = det(F) F^{-T}.
+ *   Z4  R(F) is the closest ROTATION (sign-corrected SVD, det R = +1), also for inverted F.
+ *   Z5  Chebyshev omega_1 = omega_2 = 1, omega_3 = 2/(2-rho^2), omega_{l+1} = 4/(4-rho^2 omega_l).
+ *   Z7  SOR blends against x^{l-1} exactly as printed.
+ *   Z8  x^{-1} := x^0.    Z9  Dirichlet rows keep their targets under blending.
+ *   Z13 the external-work term sums over all vertices.  Z14 residual = 2-norm over free vertices.
+ *   Weak constraint with an empty side 1 uses a fixed anchor point instead (rigid-plane contact).
+ *
+ * Matrices are row-major double[9]: M[3*a+b] = M_{ab}.  Fourth-order tensors are double[81] with
+ * T[(3*alpha+gamma)*9 + 3*beta+delta] = T_{alpha gamma beta delta}.
+ * Pinned by tests/test_oracle_*.py (materials, colouring, solver); no function is "parity unpinned".
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { ORC_OK = 0, ORC_E_ARG = 1, ORC_E_DEGENERATE = 2, ORC_E_ISOLATED = 3, ORC_E_NOMEM = 4 };
+enum { ORC_NH = 0, ORC_FCR = 1 };
+enum { ORC_ACCEL_NONE = 0, ORC_ACCEL_SOR = 1, ORC_ACCEL_CHEBYSHEV = 2 };
+
+/* ------------------------------------------------------------------------------------------------ */
+/* 3x3 helpers                                                                                      */
+/* ------------------------------------------------------------------------------------------------ */
+
+static double det3(const double *M) {
+    return M[0] * (M[4] * M[8] - M[5] * M[7]) - M[1] * (M[3] * M[8] - M[5] * M[6]) +
+           M[2] * (M[3] * M[7] - M[4] * M[6]);
+}
+
+/* cof(F)_{ab} = d det(F) / d F_{ab}  ("J F^{-T} ... the cofactor matrix", defined for all F) */
+void orc_cofactor(const double *F, double *C) {
+    C[0] = F[4] * F[8] - F[5] * F[7];
+    C[1] = F[5] * F[6] - F[3] * F[8];
+    C[2] = F[3] * F[7] - F[4] * F[6];
+    C[3] = F[2] * F[7] - F[1] * F[8];
+    C[4] = F[0] * F[8] - F[2] * F[6];
+    C[5] = F[1] * F[6] - F[0] * F[7];
+    C[6] = F[1] * F[5] - F[2] * F[4];
+    C[7] = F[2] * F[3] - F[0] * F[5];
+    C[8] = F[0] * F[4] - F[1] * F[3];
+}
+
+double orc_det(const double *F) { return det3(F); }
+
+/* eq:lame: mu = E / (2 (1 + nu)),  lambda = E nu / ((1 + nu)(1 - 2 nu)) */
+int orc_lame(double E, double nu, double *mu, double *lambda) {
+    if (!(E > 0.0) || !(nu >= 0.0) || !(nu < 0.5)) return ORC_E_ARG;
+    *mu = E / (2.0 * (1.0 + nu));
+    *lambda = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------------------------------ */
+/* Polar rotation R(F) of F = R S, reading Z4: closest rotation.                 */
+/* Cyclic Jacobi eigen-decomposition of S = F^T F (textbook), then U from F V by Gram-Schmidt,        */
+/* u3 = u1 x u2 (so det U = det V = +1 and the smallest singular value carries the sign of det F).   */
+/* ------------------------------------------------------------------------------------------------ */
+
+static void jacobi_eig_sym3(double *S, double *V) {
+    int p, q, k, sweep;
+    static const int P[3] = {0, 0, 1}, Q[3] = {1, 2, 2};
+    for (k = 0; k < 9; ++k) V[k] = (k % 4 == 0) ? 1.0 : 0.0;
+    for (sweep = 0; sweep < 64; ++sweep) {
+        double off = S[1] * S[1] + S[2] * S[2] + S[5] * S[5];
+        double diag = S[0] * S[0] + S[4] * S[4] + S[8] * S[8];
+        if (off == 0.0 || off <= 1e-40 * diag) break;
+        for (k = 0; k < 3; ++k) {
+            double apq, app, aqq, theta, t, c, s;
+            int r;
+            p = P[k];
+            q = Q[k];
+            apq = S[3 * p + q];
+            if (apq == 0.0) continue;
+            app = S[3 * p + p];
+            aqq = S[3 * q + q];
+            theta = (aqq - app) / (2.0 * apq);
+            t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+            /* S <- J^T S J with J the (p,q) Givens rotation [c s; -s c] */
+            for (r = 0; r < 3; ++r) { /* columns p,q */
+                double srp = S[3 * r + p], srq = S[3 * r + q];
+                S[3 * r + p] = c * srp - s * srq;
+                S[3 * r + q] = s * srp + c * srq;
+            }
+            for (r = 0; r < 3; ++r) { /* rows p,q */
+                double spr = S[3 * p + r], sqr = S[3 * q + r];
+                S[3 * p + r] = c * spr - s * sqr;
+                S[3 * q + r] = s * spr + c * sqr;
+            }
+            for (r = 0; r < 3; ++r) {
+                double vrp = V[3 * r + p], vrq = V[3 * r + q];
+                V[3 * r + p] = c * vrp - s * vrq;
+                V[3 * r + q] = s * vrp + c * vrq;
+            }
+        }
+    }
+}
+
+static void cross3(const double *a, const double *b, double *c) {
+    c[0] = a[1] * b[2] - a[2] * b[1];
+    c[1] = a[2] * b[0] - a[0] * b[2];
+    c[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+static double norm3(const double *a) { return sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]); }
+
+/* a unit vector perpendicular to unit u, chosen deterministically */
+static void perp_unit(const double *u, double *out) {
+    double e[3] = {0, 0, 0}, c[3], n;
+    int k = 0;
+    if (fabs(u[1]) < fabs(u[k])) k = 1;
+    if (fabs(u[2]) < fabs(u[k])) k = 2;
+    e[k] = 1.0;
+    cross3(u, e, c);
+    n = norm3(c);
+    out[0] = c[0] / n;
+    out[1] = c[1] / n;
+    out[2] = c[2] / n;
+}
+
+void orc_polar(const double *F, double *R) {
+    double S[9], V[9], ev[3], u[3][3], fv[3][3], n1, n2, d;
+    int a, b, k, order[3] = {0, 1, 2};
+    for (a = 0; a < 3; ++a)
+        for (b = 0; b < 3; ++b) {
+            S[3 * a + b] = 0.0;
+            for (k = 0; k < 3; ++k) S[3 * a + b] += F[3 * k + a] * F[3 * k + b];
+        }
+    jacobi_eig_sym3(S, V);
+    for (k = 0; k < 3; ++k) ev[k] = S[4 * k];
+    /* sort eigenpairs by decreasing eigenvalue (insertion sort of the index list) */
+    for (a = 1; a < 3; ++a)
+        for (b = a; b > 0 && ev[order[b]] > ev[order[b - 1]]; --b) {
+            int t = order[b];
+            order[b] = order[b - 1];
+            order[b - 1] = t;
+        }
+    {
+        double Vs[9];
+        for (a = 0; a < 3; ++a)
+            for (k = 0; k < 3; ++k) Vs[3 * a + k] = V[3 * a + order[k]];
+        memcpy(V, Vs, sizeof(Vs));
+    }
+    if (det3(V) < 0.0)
+        for (a = 0; a < 3; ++a) V[3 * a + 2] = -V[3 * a + 2];
+    /* F v_k */
+    for (k = 0; k < 3; ++k)
+        for (a = 0; a < 3; ++a) {
+            fv[k][a] = 0.0;
+            for (b = 0; b < 3; ++b) fv[k][a] += F[3 * a + b] * V[3 * b + k];
+        }
+    n1 = norm3(fv[0]);
+    if (n1 == 0.0) { /* F == 0: every rotation is closest; take R = I */
+        for (k = 0; k < 9; ++k) R[k] = (k % 4 == 0) ? 1.0 : 0.0;
+        return;
+    }
+    for (a = 0; a < 3; ++a) u[0][a] = fv[0][a] / n1;
+    d = u[0][0] * fv[1][0] + u[0][1] * fv[1][1] + u[0][2] * fv[1][2];
+    for (a = 0; a < 3; ++a) u[1][a] = fv[1][a] - d * u[0][a];
+    n2 = norm3(u[1]);
+    if (n2 <= 1e-13 * n1) {
+        perp_unit(u[0], u[1]);
+    } else {
+        for (a = 0; a < 3; ++a) u[1][a] /= n2;
+    }
+    cross3(u[0], u[1], u[2]);
+    /* R = U V^T */
+    for (a = 0; a < 3; ++a)
+        for (b = 0; b < 3; ++b) {
+            R[3 * a + b] = 0.0;
+            for (k = 0; k < 3; ++k) R[3 * a + b] += u[k][a] * V[3 * b + k];
+        }
+}
+
+/* ------------------------------------------------------------------------------------------------ */
+/* Constitutive models                                                           */
+/* ------------------------------------------------------------------------------------------------ */
+
+/* Psi(F).  FCR eq:cor: mu |F - R(F)|_F^2 + lambda/2 (det F - 1)^2.
+ * NH eq:nh: 1/2 mu |F|_F^2 + lambdahat/2 (det F - 1 - mu/lambdahat)^2, lambdahat = mu +
+ * lambda; with raw == 0 the constant 3/2 mu + mu^2/(2 lambdahat) is subtracted (reading Z1). */
+double orc_psi(int model, double mu, double lambda, const double *F, int raw) {
+    double J = det3(F);
+    int k;
+    if (model == ORC_FCR) {
+        double R[9], s = 0.0;
+        orc_polar(F, R);
+        for (k = 0; k < 9; ++k) s += (F[k] - R[k]) * (F[k] - R[k]);
+        return mu * s + 0.5 * lambda * (J - 1.0) * (J - 1.0);
+    } else {
+        double lh = mu + lambda, fro = 0.0, t, psi;
+        for (k = 0; k < 9; ++k) fro += F[k] * F[k];
+        t = J - 1.0 - mu / lh;
+        psi = 0.5 * mu * fro + 0.5 * lh * t * t;
+        if (!raw) psi -= 1.5 * mu + mu * mu / (2.0 * lh);
+        return psi;
+    }
+}
+
+/* P = dPsi/dF.  NH: mu F + lambdahat (J - 1 - mu/lambdahat) cof F.
+ * FCR: 2 mu (F - R) + lambda (J - 1) cof F. */
+void orc_piola(int model, double mu, double lambda, const double *F, double *P) {
+    double C[9], J = det3(F);
+    int k;
+    orc_cofactor(F, C);
+    if (model == ORC_FCR) {
+        double R[9];
+        orc_polar(F, R);
+        for (k = 0; k < 9; ++k) P[k] = 2.0 * mu * (F[k] - R[k]) + lambda * (J - 1.0) * C[k];
+    } else {
+        double lh = mu + lambda;
+        for (k = 0; k < 9; ++k) P[k] = mu * F[k] + lh * (J - 1.0 - mu / lh) * C[k];
+    }
+}
+
+/* eq:mod_hess_dens: Ctilde_{alpha gamma beta delta} = 2 mu delta_{alpha beta}
+ * delta_{gamma delta} + lambda cof(F)_{alpha gamma} cof(F)_{beta delta}   (readings Z2, Z3) */
+void orc_mod_hess_density(double mu, double lambda, const double *F, double *T) {
+    double C[9];
+    int al, ga, be, de;
+    orc_cofactor(F, C);
+    for (al = 0; al < 3; ++al)
+        for (ga = 0; ga < 3; ++ga)
+            for (be = 0; be < 3; ++be)
+                for (de = 0; de < 3; ++de)
+                    T[(3 * al + ga) * 9 + 3 * be + de] =
+                        2.0 * mu * (al == be ? 1.0 : 0.0) * (ga == de ? 1.0 : 0.0) +
+                        lambda * C[3 * al + ga] * C[3 * be + de];
+}
+
+/* ------------------------------------------------------------------------------------------------ */
+/* Scene and its plain precompute                                                */
+/* ------------------------------------------------------------------------------------------------ */
+
+typedef struct {
+    int64_t nv;
+    const double *X;
+    int64_t nt;
+    const int32_t *tets;
+    int32_t model;
+    const double *E;
+    int64_t nE;
+    double nu, density;
+    double gravity[3];
+    int64_t npin;
+    const int32_t *pinned;
+    int64_t nwc;
+    const int32_t *wc_n0, *wc_n1, *wc_idx0, *wc_idx1;
+    const double *wc_w0, *wc_w1, *wc_anchor, *wc_K;
+} orc_scene;
+
+typedef struct {
+    int64_t nv, nt, nwc;
+    int32_t model;
+    double nu, density, gravity[3];
+    double *X;
+    int32_t *tets;
+    double *B;      /* nt*9 : Dm^{-1}; row k-1 is dN_k/dX for local node k = 1..3 */
+    double *V;      /* nt   : rest measure V^0_e */
+    double *mu, *lambda;
+    double *fext;   /* nv*3 : consistent body force  f^ext_i = sum_e R^0 g V_e / 4 */
+    char *pinned;
+    int32_t *wc_n0, *wc_n1, *wc_idx0, *wc_idx1;
+    double *wc_w0, *wc_w1, *wc_anchor, *wc_K;
+    int64_t *vt_off; /* vertex -> incident tets, ascending tet index */
+    int32_t *vt;
+    int64_t *vc_off; /* vertex -> incident weak constraints, input order */
+    int32_t *vc;
+    int32_t *colour;
+    int32_t ncolours;
+} orc_prep;
+
+void orc_free(orc_prep *p) {
+    if (!p) return;
+    free(p->X); free(p->tets); free(p->B); free(p->V); free(p->mu); free(p->lambda); free(p->fext);
+    free(p->pinned); free(p->wc_n0); free(p->wc_n1); free(p->wc_idx0); free(p->wc_idx1);
+    free(p->wc_w0); free(p->wc_w1); free(p->wc_anchor); free(p->wc_K); free(p->vt_off); free(p->vt);
+    free(p->vc_off); free(p->vc); free(p->colour);
+    free(p);
+}
+
+static void *xdup(const void *src, size_t bytes) {
+    void *d = malloc(bytes ? bytes : 1);
+    if (d && bytes) memcpy(d, src, bytes);
+    return d;
+}
+
+/* gradient of the linear shape function of local node k in tet e: k >= 1 -> row k-1 of B,
+ * k = 0 -> minus the sum of the rows (the shape functions sum to one) */
+static void shape_grad(const orc_prep *p, int64_t e, int k, double *g) {
+    const double *B = p->B + 9 * e;
+    int b;
+    if (k > 0) {
+        for (b = 0; b < 3; ++b) g[b] = B[3 * (k - 1) + b];
+    } else {
+        for (b = 0; b < 3; ++b) g[b] = -(B[b] + B[3 + b] + B[6 + b]);
+    }
+}
+
+/* PBNG node colouring: visiting vertices in ascending index, colour(v) = least colour
+ * not in the union of S_c over the elements / weak constraints c incident to v; then register the
+ * colour in S_c for each of them.  S_c holds at most (#nodes of c) colours, so it is a short list. */
+static int colour_nodes(orc_prep *p) {
+    int64_t nt = p->nt, nwc = p->nwc, v, k;
+    int32_t *ts_n = calloc((size_t)(nt + nwc) + 1, sizeof(int32_t));
+    int32_t *ts = malloc(((size_t)(nt + nwc) * 8 + 1) * sizeof(int32_t)); /* <= 8 nodes per stencil */
+    char *used = NULL;
+    int32_t maxc = 0;
+    if (!ts_n || !ts) { free(ts_n); free(ts); return ORC_E_NOMEM; }
+    for (v = 0; v < p->nv; ++v) {
+        int32_t cap = 0, c;
+        /* count an upper bound for the forbidden set */
+        for (k = p->vt_off[v]; k < p->vt_off[v + 1]; ++k) cap += ts_n[p->vt[k]];
+        for (k = p->vc_off[v]; k < p->vc_off[v + 1]; ++k) cap += ts_n[nt + p->vc[k]];
+        used = realloc(used, (size_t)cap + 2);
+        memset(used, 0, (size_t)cap + 2);
+        for (k = p->vt_off[v]; k < p->vt_off[v + 1]; ++k) {
+            int64_t s = p->vt[k];
+            int32_t q;
+            for (q = 0; q < ts_n[s]; ++q)
+                if (ts[8 * s + q] <= cap) used[ts[8 * s + q]] = 1;
+        }
+        for (k = p->vc_off[v]; k < p->vc_off[v + 1]; ++k) {
+            int64_t s = nt + p->vc[k];
+            int32_t q;
+            for (q = 0; q < ts_n[s]; ++q)
+                if (ts[8 * s + q] <= cap) used[ts[8 * s + q]] = 1;
+        }
+        c = 0;
+        while (used[c]) ++c;
+        p->colour[v] = c;
+        if (c + 1 > maxc) maxc = c + 1;
+        for (k = p->vt_off[v]; k < p->vt_off[v + 1]; ++k) {
+            int64_t s = p->vt[k];
+            ts[8 * s + ts_n[s]++] = c;
+        }
+        for (k = p->vc_off[v]; k < p->vc_off[v + 1]; ++k) {
+            int64_t s = nt + p->vc[k];
+            if (ts_n[s] < 8) ts[8 * s + ts_n[s]++] = c;
+        }
+    }
+    p->ncolours = maxc;
+    free(used); free(ts_n); free(ts);
+    return ORC_OK;
+}
+
+/* builds vertex -> stencil lists; a weak constraint is listed once per distinct node */
+static int build_incidence(orc_prep *p) {
+    int64_t e, c, v, q;
+    int64_t *cnt;
+    p->vt_off = calloc((size_t)p->nv + 1, sizeof(int64_t));
+    p->vc_off = calloc((size_t)p->nv + 1, sizeof(int64_t));
+    cnt = calloc((size_t)p->nv + 1, sizeof(int64_t));
+    if (!p->vt_off || !p->vc_off || !cnt) { free(cnt); return ORC_E_NOMEM; }
+    for (e = 0; e < p->nt; ++e)
+        for (q = 0; q < 4; ++q) p->vt_off[p->tets[4 * e + q] + 1]++;
+    for (v = 0; v < p->nv; ++v) p->vt_off[v + 1] += p->vt_off[v];
+    p->vt = malloc((size_t)(4 * p->nt + 1) * sizeof(int32_t));
+    if (!p->vt) { free(cnt); return ORC_E_NOMEM; }
+    for (e = 0; e < p->nt; ++e) /* ascending e -> each list ascending */
+        for (q = 0; q < 4; ++q) {
+            v = p->tets[4 * e + q];
+            p->vt[p->vt_off[v] + cnt[v]++] = (int32_t)e;
+        }
+    memset(cnt, 0, (size_t)(p->nv + 1) * sizeof(int64_t));
+    /* weak constraints: node list = side-0 nodes then side-1 nodes, deduplicated per constraint */
+    for (c = 0; c < p->nwc; ++c) {
+        int32_t nodes[8], nn = 0, a, b;
+        for (a = 0; a < p->wc_n0[c]; ++a) nodes[nn++] = p->wc_idx0[4 * c + a];
+        for (a = 0; a < p->wc_n1[c]; ++a) nodes[nn++] = p->wc_idx1[4 * c + a];
+        for (a = 0; a < nn; ++a) {
+            int dup = 0;
+            for (b = 0; b < a; ++b) dup |= nodes[b] == nodes[a];
+            if (!dup) p->vc_off[nodes[a] + 1]++;
+        }
+    }
+    for (v = 0; v < p->nv; ++v) p->vc_off[v + 1] += p->vc_off[v];
+    p->vc = malloc((size_t)(p->vc_off[p->nv] + 1) * sizeof(int32_t));
+    if (!p->vc) { free(cnt); return ORC_E_NOMEM; }
+    for (c = 0; c < p->nwc; ++c) {
+        int32_t nodes[8], nn = 0, a, b;
+        for (a = 0; a < p->wc_n0[c]; ++a) nodes[nn++] = p->wc_idx0[4 * c + a];
+        for (a = 0; a < p->wc_n1[c]; ++a) nodes[nn++] = p->wc_idx1[4 * c + a];
+        for (a = 0; a < nn; ++a) {
+            int dup = 0;
+            for (b = 0; b < a; ++b) dup |= nodes[b] == nodes[a];
+            if (!dup) {
+                v = nodes[a];
+                p->vc[p->vc_off[v] + cnt[v]++] = (int32_t)c;
+            }
+        }
+    }
+    free(cnt);
+    return ORC_OK;
+}
+
+/* Set-up: copy the scene, rest precompute (Dm, Dm^{-1}, V^0_e), Lame per tet
+ * (eq:lame), body force, incidence and colouring.  *bad receives the offending index. */
+int orc_prepare(const orc_scene *s, orc_prep **out, int64_t *bad) {
+    orc_prep *p;
+    int64_t e, v, k, c;
+    int st;
+    *out = NULL;
+    if (bad) *bad = -1;
+    if (s->nv <= 0 || s->nt < 0 || (s->model != ORC_NH && s->model != ORC_FCR)) return ORC_E_ARG;
+    if (s->nE != 1 && s->nE != s->nt) return ORC_E_ARG;
+    if (!(s->nu >= 0.0 && s->nu < 0.5)) return ORC_E_ARG;
+    for (e = 0; e < s->nt * 4; ++e)
+        if (s->tets[e] < 0 || s->tets[e] >= s->nv) { if (bad) *bad = e / 4; return ORC_E_ARG; }
+    for (k = 0; k < s->npin; ++k)
+        if (s->pinned[k] < 0 || s->pinned[k] >= s->nv) { if (bad) *bad = k; return ORC_E_ARG; }
+    for (c = 0; c < s->nwc; ++c) {
+        int a;
+        if (s->wc_n0[c] < 1 || s->wc_n0[c] > 4 || s->wc_n1[c] < 0 || s->wc_n1[c] > 4) { if (bad) *bad = c; return ORC_E_ARG; }
+        for (a = 0; a < s->wc_n0[c]; ++a)
+            if (s->wc_idx0[4 * c + a] < 0 || s->wc_idx0[4 * c + a] >= s->nv) { if (bad) *bad = c; return ORC_E_ARG; }
+        for (a = 0; a < s->wc_n1[c]; ++a)
+            if (s->wc_idx1[4 * c + a] < 0 || s->wc_idx1[4 * c + a] >= s->nv) { if (bad) *bad = c; return ORC_E_ARG; }
+    }
+    p = calloc(1, sizeof(orc_prep));
+    if (!p) return ORC_E_NOMEM;
+    p->nv = s->nv; p->nt = s->nt; p->nwc = s->nwc; p->model = s->model; p->nu = s->nu;
+    p->density = s->density;
+    for (k = 0; k < 3; ++k) p->gravity[k] = s->gravity[k];
+    p->X = xdup(s->X, (size_t)s->nv * 3 * sizeof(double));
+    p->tets = xdup(s->tets, (size_t)s->nt * 4 * sizeof(int32_t));
+    p->wc_n0 = xdup(s->wc_n0, (size_t)s->nwc * sizeof(int32_t));
+    p->wc_n1 = xdup(s->wc_n1, (size_t)s->nwc * sizeof(int32_t));
+    p->wc_idx0 = xdup(s->wc_idx0, (size_t)s->nwc * 4 * sizeof(int32_t));
+    p->wc_idx1 = xdup(s->wc_idx1, (size_t)s->nwc * 4 * sizeof(int32_t));
+    p->wc_w0 = xdup(s->wc_w0, (size_t)s->nwc * 4 * sizeof(double));
+    p->wc_w1 = xdup(s->wc_w1, (size_t)s->nwc * 4 * sizeof(double));
+    p->wc_anchor = xdup(s->wc_anchor, (size_t)s->nwc * 3 * sizeof(double));
+    p->wc_K = xdup(s->wc_K, (size_t)s->nwc * 6 * sizeof(double));
+    p->B = malloc((size_t)(s->nt * 9 + 1) * sizeof(double));
+    p->V = malloc((size_t)(s->nt + 1) * sizeof(double));
+    p->mu = malloc((size_t)(s->nt + 1) * sizeof(double));
+    p->lambda = malloc((size_t)(s->nt + 1) * sizeof(double));
+    p->fext = calloc((size_t)s->nv * 3, sizeof(double));
+    p->pinned = calloc((size_t)s->nv, 1);
+    p->colour = malloc((size_t)s->nv * sizeof(int32_t));
+    if (!p->X || !p->tets || !p->B || !p->V || !p->mu || !p->lambda || !p->fext || !p->pinned || !p->colour) {
+        orc_free(p);
+        return ORC_E_NOMEM;
+    }
+    for (k = 0; k < s->npin; ++k) p->pinned[s->pinned[k]] = 1;
+    for (e = 0; e < s->nt; ++e) {
+        const int32_t *t = p->tets + 4 * e;
+        double Dm[9], adj[9], det, ell = 0.0;
+        int a, b;
+        int pa[6] = {0, 0, 0, 1, 1, 2}, pb[6] = {1, 2, 3, 2, 3, 3};
+        /* Dm = [X1 - X0, X2 - X0, X3 - X0] (columns) */
+        for (a = 0; a < 3; ++a)
+            for (b = 0; b < 3; ++b) Dm[3 * a + b] = p->X[3 * t[b + 1] + a] - p->X[3 * t[0] + a];
+        det = det3(Dm);
+        for (a = 0; a < 6; ++a) {
+            double d[3];
+            for (b = 0; b < 3; ++b) d[b] = p->X[3 * t[pa[a]] + b] - p->X[3 * t[pb[a]] + b];
+            ell += norm3(d) / 6.0;
+        }
+        if (!(fabs(det) > 1e-12 * ell * ell * ell)) {
+            if (bad) *bad = e;
+            orc_free(p);
+            return ORC_E_DEGENERATE;
+        }
+        /* B = Dm^{-1} = adj(Dm) / det = cof(Dm)^T / det */
+        orc_cofactor(Dm, adj);
+        for (a = 0; a < 3; ++a)
+            for (b = 0; b < 3; ++b) p->B[9 * e + 3 * a + b] = adj[3 * b + a] / det;
+        p->V[e] = fabs(det) / 6.0;
+        if (orc_lame(s->E[s->nE == 1 ? 0 : e], s->nu, &p->mu[e], &p->lambda[e]) != ORC_OK) {
+            if (bad) *bad = e;
+            orc_free(p);
+            return ORC_E_ARG;
+        }
+        for (a = 0; a < 4; ++a)
+            for (b = 0; b < 3; ++b) p->fext[3 * t[a] + b] += p->density * p->gravity[b] * p->V[e] / 4.0;
+    }
+    st = build_incidence(p);
+    if (st != ORC_OK) { orc_free(p); return st; }
+    for (v = 0; v < p->nv; ++v)
+        if (!p->pinned[v] && p->vt_off[v + 1] == p->vt_off[v] && p->vc_off[v + 1] == p->vc_off[v]) {
+            if (bad) *bad = v;
+            orc_free(p);
+            return ORC_E_ISOLATED;
+        }
+    st = colour_nodes(p);
+    if (st != ORC_OK) { orc_free(p); return st; }
+    *out = p;
+    return ORC_OK;
+}
+
+int32_t orc_num_colours(const orc_prep *p) { return p->ncolours; }
+void orc_get_colour(const orc_prep *p, int32_t *out) { memcpy(out, p->colour, (size_t)p->nv * sizeof(int32_t)); }
+void orc_get_rest(const orc_prep *p, double *B, double *V) {
+    memcpy(B, p->B, (size_t)p->nt * 9 * sizeof(double));
+    memcpy(V, p->V, (size_t)p->nt * sizeof(double));
+}
+void orc_get_fext(const orc_prep *p, double *out) { memcpy(out, p->fext, (size_t)p->nv * 3 * sizeof(double)); }
+
+/* deformation gradient of tet e (eq:disc_pe): F = sum_j y_j (dN_j/dX)^T */
+static void deformation_gradient(const orc_prep *p, const double *y, int64_t e, double *F) {
+    int j, a, b;
+    double g[3];
+    for (a = 0; a < 9; ++a) F[a] = 0.0;
+    for (j = 0; j < 4; ++j) {
+        const double *yj = y + 3 * (int64_t)p->tets[4 * e + j];
+        shape_grad(p, e, j, g);
+        for (a = 0; a < 3; ++a)
+            for (b = 0; b < 3; ++b) F[3 * a + b] += yj[a] * g[b];
+    }
+}
+
+void orc_deformation_gradient(const orc_prep *p, const double *y, int64_t e, double *F) {
+    deformation_gradient(p, y, e, F);
+}
+
+/* C_c(y) = sum_j w0_j y_j - sum_j w1_j y_j; side 1 empty -> fixed anchor point */
+static void constraint_value(const orc_prep *p, const double *y, int64_t c, double *C) {
+    int a, b;
+    for (b = 0; b < 3; ++b) C[b] = 0.0;
+    for (a = 0; a < p->wc_n0[c]; ++a)
+        for (b = 0; b < 3; ++b) C[b] += p->wc_w0[4 * c + a] * y[3 * (int64_t)p->wc_idx0[4 * c + a] + b];
+    if (p->wc_n1[c] == 0) {
+        for (b = 0; b < 3; ++b) C[b] -= p->wc_anchor[3 * c + b];
+    } else {
+        for (a = 0; a < p->wc_n1[c]; ++a)
+            for (b = 0; b < 3; ++b) C[b] -= p->wc_w1[4 * c + a] * y[3 * (int64_t)p->wc_idx1[4 * c + a] + b];
+    }
+}
+
+static void constraint_K(const orc_prep *p, int64_t c, double *K) {
+    const double *k = p->wc_K + 6 * c; /* xx yy zz xy yz xz */
+    K[0] = k[0]; K[1] = k[3]; K[2] = k[5];
+    K[3] = k[3]; K[4] = k[1]; K[5] = k[4];
+    K[6] = k[5]; K[7] = k[4]; K[8] = k[2];
+}
+
+/* w^c_{0i} - w^c_{1i} */
+static double constraint_weight_diff(const orc_prep *p, int64_t c, int64_t i) {
+    double d = 0.0;
+    int a;
+    for (a = 0; a < p->wc_n0[c]; ++a)
+        if (p->wc_idx0[4 * c + a] == i) d += p->wc_w0[4 * c + a];
+    for (a = 0; a < p->wc_n1[c]; ++a)
+        if (p->wc_idx1[4 * c + a] == i) d -= p->wc_w1[4 * c + a];
+    return d;
+}
+
+/* The right-hand side f_i(y) + f^ext_i of eq:pbgn_dx and the modified nodal Hessian A of eq:mod_hess,
+ * for node i at positions y:
+ *   f_i = - sum_e P_e(y) dN_i/dX V_e - sum_c (w0_ci - w1_ci) K_c C_c(y)
+ *   A_ab = sum_e sum_{gamma,delta} Ctilde_{a gamma b delta} (dN_i/dX)_gamma (dN_i/dX)_delta V_e
+ *          + sum_c (w0_ci - w1_ci)^2 K_c,ab                                                        */
+void orc_nodal(const orc_prep *p, const double *y, int64_t i, double *f, double *A) {
+    int64_t k;
+    int a, b, ga, de;
+    for (a = 0; a < 3; ++a) f[a] = p->fext[3 * i + a];
+    for (a = 0; a < 9; ++a) A[a] = 0.0;
+    for (k = p->vt_off[i]; k < p->vt_off[i + 1]; ++k) {
+        int64_t e = p->vt[k];
+        int slot = 0;
+        double F[9], P[9], T[81], g[3], Ve = p->V[e];
+        while (p->tets[4 * e + slot] != i) ++slot;
+        shape_grad(p, e, slot, g);
+        deformation_gradient(p, y, e, F);
+        orc_piola(p->model, p->mu[e], p->lambda[e], F, P);
+        for (a = 0; a < 3; ++a)
+            for (b = 0; b < 3; ++b) f[a] -= P[3 * a + b] * g[b] * Ve;
+        orc_mod_hess_density(p->mu[e], p->lambda[e], F, T);
+        for (a = 0; a < 3; ++a)
+            for (b = 0; b < 3; ++b) {
+                double s = 0.0;
+                for (ga = 0; ga < 3; ++ga)
+                    for (de = 0; de < 3; ++de) s += T[(3 * a + ga) * 9 + 3 * b + de] * g[ga] * g[de];
+                A[3 * a + b] += s * Ve;
+            }
+    }
+    for (k = p->vc_off[i]; k < p->vc_off[i + 1]; ++k) {
+        int64_t c = p->vc[k];
+        double C[3], K[9], d = constraint_weight_diff(p, c, i);
+        constraint_value(p, y, c, C);
+        constraint_K(p, c, K);
+        for (a = 0; a < 3; ++a)
+            for (b = 0; b < 3; ++b) {
+                f[a] -= d * K[3 * a + b] * C[b];
+                A[3 * a + b] += d * d * K[3 * a + b];
+            }
+    }
+}
+
+/* solve the 3x3 SPD system A dx = r by Cholesky (plain, fp64) */
+static int spd_solve3(const double *A, const double *r, double *x) {
+    double L[9] = {0}, z[3];
+    int i, j, k;
+    for (j = 0; j < 3; ++j) {
+        double s = A[3 * j + j];
+        for (k = 0; k < j; ++k) s -= L[3 * j + k] * L[3 * j + k];
+        if (!(s > 0.0)) return 1;
+        L[3 * j + j] = sqrt(s);
+        for (i = j + 1; i < 3; ++i) {
+            double t = A[3 * i + j];
+            for (k = 0; k < j; ++k) t -= L[3 * i + k] * L[3 * j + k];
+            L[3 * i + j] = t / L[3 * j + j];
+        }
+    }
+    for (i = 0; i < 3; ++i) {
+        double s = r[i];
+        for (k = 0; k < i; ++k) s -= L[3 * i + k] * z[k];
+        z[i] = s / L[3 * i + i];
+    }
+    for (i = 2; i >= 0; --i) {
+        double s = z[i];
+        for (k = i + 1; k < 3; ++k) s -= L[3 * k + i] * x[k];
+        x[i] = s / L[3 * i + i];
+    }
+    return 0;
+}
+
+/* One PBNG iteration in place: colours in ascending order; within a
+ * colour, free nodes in ascending index; each node takes ONE modified-Newton step from a zero initial
+ * guess, x_i += A^{-1} (f_i + f^ext_i), with no line search.  Returns the number of failed solves. */
+int64_t orc_sweep(const orc_prep *p, double *w) {
+    int32_t c;
+    int64_t i, fails = 0;
+    for (c = 0; c < p->ncolours; ++c)
+        for (i = 0; i < p->nv; ++i) {
+            double f[3], A[9], dx[3];
+            if (p->colour[i] != c || p->pinned[i]) continue;
+            orc_nodal(p, w, i, f, A);
+            if (spd_solve3(A, f, dx)) { ++fails; continue; }
+            w[3 * i + 0] += dx[0];
+            w[3 * i + 1] += dx[1];
+            w[3 * i + 2] += dx[2];
+        }
+    return fails;
+}
+
+/* Chebyshev weight omega_m (reading Z5): omega_m = 1 for m <= 2, omega_3 = 2/(2-rho^2),
+ * omega_m = 4/(4 - rho^2 omega_{m-1}) for m > 3. */
+double orc_chebyshev_omega(int64_t m, double rho) {
+    double om;
+    int64_t k;
+    if (m <= 2) return 1.0;
+    om = 2.0 / (2.0 - rho * rho);
+    for (k = 4; k <= m; ++k) om = 4.0 / (4.0 - rho * rho * om);
+    return om;
+}
+
+/* n accelerated iterations starting at iteration index l0.
+ *   x   : x^{l}   (in), x^{l0+n}   (out)
+ *   xm1 : x^{l-1} (in), x^{l0+n-1} (out)   (caller sets xm1 = x^0 when l0 == 0, reading Z8)
+ * none      : x^{l+1} = x_PBNG
+ * SOR       : x^{l+1} = omega (x_PBNG - x^{l-1}) + x^{l-1}
+ * Chebyshev : x^{l+1} = omega_{l+1} (gamma (x_PBNG - x^l) + x^l - x^{l-1}) + x^{l-1}
+ * Dirichlet rows are never updated (reading Z9).  Returns the number of failed nodal solves. */
+int64_t orc_iterate(const orc_prep *p, double *x, double *xm1, int64_t l0, int32_t n, int32_t accel,
+                    double omega, double rho, double gamma) {
+    int64_t N = p->nv * 3, l, k, fails = 0;
+    double *w = malloc((size_t)N * sizeof(double));
+    if (!w) return -1;
+    for (l = l0; l < l0 + n; ++l) {
+        double om = orc_chebyshev_omega(l + 1, rho);
+        memcpy(w, x, (size_t)N * sizeof(double));
+        fails += orc_sweep(p, w);
+        for (k = 0; k < N; ++k) {
+            double xl = x[k], xl1 = xm1[k], xn;
+            if (p->pinned[k / 3]) continue;
+            if (accel == ORC_ACCEL_SOR) {
+                xn = omega * (w[k] - xl1) + xl1;
+            } else if (accel == ORC_ACCEL_CHEBYSHEV) {
+                xn = om * (gamma * (w[k] - xl) + xl - xl1) + xl1;
+            } else {
+                xn = w[k];
+            }
+            xm1[k] = xl;
+            x[k] = xn;
+        }
+    }
+    free(w);
+    return fails;
+}
+
+/* r_i = f_i(y) + f^ext_i for every node (pinned included; the residual norm skips them) */
+void orc_forces(const orc_prep *p, const double *y, double *r) {
+    int64_t i;
+    double A[9];
+    for (i = 0; i < p->nv; ++i) orc_nodal(p, y, i, r + 3 * i, A);
+}
+
+/* Newton residual 2-norm over free nodes (Fig. 10 caption; reading Z14) */
+double orc_residual(const orc_prep *p, const double *y) {
+    int64_t i;
+    double s = 0.0, f[3], A[9];
+    for (i = 0; i < p->nv; ++i) {
+        if (p->pinned[i]) continue;
+        orc_nodal(p, y, i, f, A);
+        s += f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+    }
+    return sqrt(s);
+}
+
+/* total energy PE^Psi(y) + PE^wc(y) - y . f^ext (reading Z13);
+ * parts (optional): [elastic, weak-constraint, external-work] */
+double orc_energy(const orc_prep *p, const double *y, double *parts) {
+    int64_t e, c, i;
+    double el = 0.0, wc = 0.0, ext = 0.0;
+    for (e = 0; e < p->nt; ++e) {
+        double F[9];
+        deformation_gradient(p, y, e, F);
+        el += p->V[e] * orc_psi(p->model, p->mu[e], p->lambda[e], F, 0);
+    }
+    for (c = 0; c < p->nwc; ++c) {
+        double C[3], K[9];
+        int a, b;
+        constraint_value(p, y, c, C);
+        constraint_K(p, c, K);
+        for (a = 0; a < 3; ++a)
+            for (b = 0; b < 3; ++b) wc += 0.5 * C[a] * K[3 * a + b] * C[b];
+    }
+    for (i = 0; i < p->nv * 3; ++i) ext -= y[i] * p->fext[i];
+    if (parts) { parts[0] = el; parts[1] = wc; parts[2] = ext; }
+    return el + wc + ext;
+}
