@@ -1,0 +1,173 @@
+/*
+ * pbng.h -- C ABI of the B200-native Position-Based Nonlinear Gauss-Seidel (PBNG) hot path.
+ *
+ * Method: Chen, Han, Chen, Teran, "Position-Based Nonlinear Gauss-Seidel for Quasistatic
+ * Hyperelasticity", arXiv 2306.09021.  Citations "PAPER.md:N" are lines of the paper text.
+ *
+ * The calls follow the paper's problem statement: a tetrahedral FEM discretisation,
+ * hyperelastic materials, Dirichlet and weak constraints, a node
+ * colouring, PBNG iterations with SOR / Chebyshev acceleration
+ * (PAPER.md:598-618), and the energy / Newton residual used to judge convergence.
+ *
+ * Conventions (all functions):
+ *  - Every function returns a pbng_status; on failure pbng_last_error() gives a message (thread-local)
+ *    and the context is left unchanged (strong guarantee for the setters).  Nothing is thrown across
+ *    the ABI.
+ *  - Host arrays passed in are copied; the caller keeps ownership.  Device pointers are borrowed for the
+ *    duration of the call and used stream-ordered on the context's stream.
+ *  - The only device memory the library uses is the workspace the caller allocates and binds
+ *    (pbng_bind_workspace); the caller keeps it alive until pbng_destroy.
+ *  - Positions are [n_batch][n_vertices][3] in the context dtype (float or double) in the caller's
+ *    ORIGINAL vertex order.  Internally the library reorders vertices colour-major.
+ *  - Call order: create_mesh -> set_material -> set_constraints -> color -> workspace_bytes ->
+ *    bind_workspace -> set_positions -> iterate* / energy_residual / get_positions.  Out-of-order calls
+ *    return PBNG_E_BAD_ORDER.  set_material / set_constraints after color invalidate the colouring.
+ *  - Functions that return host values (pbng_color, pbng_energy_residual, pbng_synchronize,
+ *    pbng_get_positions into host memory) synchronise the stream; all others are asynchronous.
+ *  - A context created with device = -1 is host-only: everything up to and including pbng_color and
+ *    pbng_query works (CPU tests of the host logic); device calls return PBNG_E_NO_DEVICE.
+ */
+#ifndef PBNG_H
+#define PBNG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pbng_ctx pbng_ctx;
+
+typedef enum {
+    PBNG_OK = 0,
+    PBNG_E_INVALID_ARGUMENT = 1,   /* bad size, null pointer, nu not in [0, 0.5), E <= 0, omega not in (0,2) ... */
+    PBNG_E_INDEX_OUT_OF_RANGE = 2, /* a tet / pinned / constraint vertex index outside [0, n_vertices) */
+    PBNG_E_DEGENERATE_ELEMENT = 3, /* |det Dm| <= 1e-12 * (mean edge)^3; *bad_index = tet index */
+    PBNG_E_ISOLATED_VERTEX = 4,    /* a free vertex with no incident tet and no weak constraint (singular A) */
+    PBNG_E_BAD_ORDER = 5,          /* call sequence violated */
+    PBNG_E_NOT_COLORED = 6,        /* device call before pbng_color */
+    PBNG_E_NONFINITE = 7,          /* a non-finite position was produced (positions left as computed) */
+    PBNG_E_CUDA = 8,               /* CUDA runtime error (message in pbng_last_error) */
+    PBNG_E_NCCL = 9,               /* reserved for the domain-decomposed path */
+    PBNG_E_OUT_OF_MEMORY = 10,     /* host allocation failed or the bound workspace is too small */
+    PBNG_E_NO_DEVICE = 11          /* device call on a host-only context */
+} pbng_status;
+
+typedef enum { PBNG_F32 = 0, PBNG_F64 = 1 } pbng_dtype;
+
+/* PBNG_NEOHOOKEAN: eq:nh with lambdahat = mu + lambda.
+ * PBNG_FIXED_COROTATED: eq:cor, R(F) the closest rotation (polar decomposition). */
+typedef enum { PBNG_NEOHOOKEAN = 0, PBNG_FIXED_COROTATED = 1 } pbng_model;
+
+/* PAPER.md:603-618.  SOR: x^{l+1} = omega (x_PBNG - x^{l-1}) + x^{l-1}.
+ * Chebyshev: x^{l+1} = omega_{l+1} (gamma (x_PBNG - x^l) + x^l - x^{l-1}) + x^{l-1},
+ * omega_1 = omega_2 = 1, omega_3 = 2/(2 - rho^2), omega_{l+1} = 4/(4 - rho^2 omega_l). */
+typedef enum { PBNG_ACCEL_NONE = 0, PBNG_ACCEL_SOR = 1, PBNG_ACCEL_CHEBYSHEV = 2 } pbng_accel;
+
+/* Weak constraint: energy 1/2 C^T K C with C = sum_j w0_j y_{idx0_j} - sum_j w1_j
+ * y_{idx1_j}.  n0 in [1,4]; n1 in [0,4], n1 == 0 means side 1 is the fixed point `anchor` (e.g. a
+ * rigid-plane contact).  K symmetric PSD given as xx, yy, zz, xy, yz, xz.  176 bytes, no padding. */
+typedef struct {
+    int32_t n0, n1;
+    int32_t idx0[4], idx1[4];
+    double w0[4], w1[4];
+    double anchor[3];
+    double K[6];
+} pbng_weak_constraint;
+
+/* Sizes and counters of a coloured context (pbng_query). */
+typedef struct {
+    int64_t n_vertices, n_tets, n_free, n_pinned, n_weak_constraints;
+    int64_t n_pairs;          /* sum over free vertices of incident tets = per-sweep (vertex, tet) records */
+    int64_t n_pair_slots;     /* records stored including 32-vertex-chunk padding */
+    int32_t n_batch, n_colours;
+    int32_t dtype, model;
+    int64_t iteration;        /* l: iterations done since the last pbng_set_positions */
+    int64_t kernel_launches;  /* kernels this context launched since creation */
+    double sweep_bytes;       /* algorithmic HBM bytes of one non-accelerated iteration (all colours, samples) */
+    double accel_bytes;       /* extra algorithmic bytes of one SOR / Chebyshev iteration (blend traffic) */
+    double sweep_flops;       /* nominal flops of one iteration (per-pair counts) */
+} pbng_info;
+
+/* Create a mesh context: rest positions X (n_vertices*3 doubles), tets (n_tets*4
+ * int32, any orientation), n_batch >= 1 independent samples sharing mesh, material and colouring
+ * (only positions and Dirichlet targets differ), compute dtype, CUDA device ordinal (or -1 for a
+ * host-only context) and the cudaStream_t (as an integer; 0 = legacy default stream) used by every
+ * later call.  Precomputes Dm^{-1} and V^0_e in fp64.  On PBNG_E_DEGENERATE_ELEMENT or
+ * PBNG_E_INDEX_OUT_OF_RANGE *bad_index (optional) receives the offending tet. */
+pbng_status pbng_create_mesh(const double *rest_xyz, int64_t n_vertices, const int32_t *tets, int64_t n_tets,
+                             int32_t n_batch, pbng_dtype dtype, int device, uintptr_t cuda_stream,
+                             pbng_ctx **out, int64_t *bad_index);
+
+/* Material: model, Young's modulus per tet (n_E == n_tets) or uniform (n_E == 1),
+ * Poisson ratio nu in [0, 0.5), density R^0 >= 0 and gravity (3 doubles) for the consistent body force
+ * f^ext_i = sum_e R^0 g V_e / 4.  Lame parameters by eq:lame. */
+pbng_status pbng_set_material(pbng_ctx *ctx, pbng_model model, const double *E, int64_t n_E, double nu,
+                              double density, const double gravity[3]);
+
+/* Dirichlet set and weak constraints.  pinned: n_pinned distinct vertex ids;
+ * pinned_xyz: targets [n_batch][n_pinned][3] in the order of `pinned`.  wc may be NULL if n_wc == 0. */
+pbng_status pbng_set_constraints(pbng_ctx *ctx, const int32_t *pinned, int64_t n_pinned, const double *pinned_xyz,
+                                 const pbng_weak_constraint *wc, int64_t n_wc);
+
+/* Greedy node colouring over elements and weak constraints, vertices visited in
+ * ascending index, and the colour-sorted device layout it implies.  colour_out (optional, n_vertices
+ * int32) receives each vertex's colour, n_colours_out (optional) the number of colours.
+ * Fails with PBNG_E_ISOLATED_VERTEX for a free vertex with no incident stencil. */
+pbng_status pbng_color(pbng_ctx *ctx, int32_t *colour_out, int32_t *n_colours_out);
+
+/* Device bytes the caller must allocate for pbng_bind_workspace (256-byte aligned). */
+pbng_status pbng_workspace_bytes(pbng_ctx *ctx, uint64_t *bytes);
+
+/* Bind caller-owned device memory (>= pbng_workspace_bytes, 256-byte aligned) and upload the layout.
+ * Synchronises the stream once (set-up only). */
+pbng_status pbng_bind_workspace(pbng_ctx *ctx, void *device_ptr, uint64_t bytes);
+
+/* Set x^0 (host or device pointer, [n_batch][n_vertices][3] in the context dtype).  Pinned rows are
+ * overwritten by their targets.  Resets the acceleration state: l = 0, x^{-1} = x^0. */
+pbng_status pbng_set_positions(pbng_ctx *ctx, const void *x);
+
+/* Current positions x^l into `x_out` (host or device, [n_batch][n_vertices][3], context dtype).
+ * Synchronises when x_out is host memory. */
+pbng_status pbng_get_positions(pbng_ctx *ctx, void *x_out);
+
+/* n_iterations PBNG iterations: for each colour in order, every free vertex of the
+ * colour takes one modified-Newton step x_i += A^{-1}(f_i + f^ext_i) with A of eq:mod_hess; then the
+ * acceleration blend.  Continues the acceleration state (l, x^{l-1}) across calls.  omega in (0,2)
+ * (SOR), rho in [0,1), gamma in (0,2] (Chebyshev).  Switching from PBNG_ACCEL_NONE to an accelerated
+ * mode after l > 0 returns PBNG_E_BAD_ORDER (x^{l-1} was not kept).  Asynchronous. */
+pbng_status pbng_iterate(pbng_ctx *ctx, int32_t n_iterations, pbng_accel accel, double omega, double rho,
+                         double gamma);
+
+/* Total energy E = sum_e V_e Psi(F_e) + 1/2 sum_c C_c^T K_c C_c - sum_i x_i . f^ext_i (
+ * Neo-Hookean shifted so that Psi(I) = 0) and the Newton residual ||(f_i + f^ext_i)_{i free}||_2
+ * (PAPER.md:926), per sample, accumulated in fp64 in a fixed order (deterministic).  Either output may
+ * be NULL.  Synchronises; returns PBNG_E_NONFINITE if a non-finite position was produced. */
+pbng_status pbng_energy_residual(pbng_ctx *ctx, double *energy_out, double *residual_out);
+
+/* Wait for the context's stream; PBNG_E_NONFINITE if any iteration produced a non-finite position. */
+pbng_status pbng_synchronize(pbng_ctx *ctx);
+
+/* Sizes, byte / flop model and counters. */
+pbng_status pbng_query(pbng_ctx *ctx, pbng_info *info);
+
+/* Per-launch timing of the colour-sweep kernel with CUDA events on the context stream (bench.py's
+ * roofline).  enable != 0 starts recording; pbng_profile_read synchronises, returns the summed sweep
+ * kernel time (ms) and the number of timed launches since the last read, then clears them. */
+pbng_status pbng_profile_enable(pbng_ctx *ctx, int enable);
+pbng_status pbng_profile_read(pbng_ctx *ctx, double *sweep_ms, int64_t *sweep_launches);
+
+/* Release the context (not the workspace, which the caller owns). NULL is a no-op. */
+pbng_status pbng_destroy(pbng_ctx *ctx);
+
+/* Message for the last non-OK status returned on this thread (never NULL). */
+const char *pbng_last_error(void);
+
+/* ABI version (major * 10000 + minor * 100 + patch). */
+int32_t pbng_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PBNG_H */

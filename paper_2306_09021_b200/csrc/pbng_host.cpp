@@ -1,0 +1,967 @@
+// pbng_host.cpp -- host side of libpbng: the C ABI of include/pbng.h.
+//
+// Owns validation, the fp64 rest-state precompute, Lame conversion (eq:lame), the
+// greedy node colouring, the colour-sorted SELL-32 device layout, the workspace plan
+// and the launch sequence of PBNG iterations.  Every per-iteration arithmetic step
+// runs in the kernels of pbng_kernels.cu; there is no CPU fallback.
+#include "pbng.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "pbng_internal.h"
+
+using namespace pbng;
+
+namespace {
+
+thread_local std::string g_err = "no error";
+
+pbng_status fail(pbng_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+
+pbng_status cuda_fail(cudaError_t e, const char *where) {
+    return fail(PBNG_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define PBNG_CUDA(call, where)                          \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+    } while (0)
+
+struct DevGuard {
+    int prev = -1, dev = -1;
+    explicit DevGuard(int d) : dev(d) {
+        if (d >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != d) cudaSetDevice(d);
+    }
+    ~DevGuard() {
+        if (dev >= 0 && prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+double det3(const double *M) {
+    return M[0] * (M[4] * M[8] - M[5] * M[7]) - M[1] * (M[3] * M[8] - M[5] * M[6]) +
+           M[2] * (M[3] * M[7] - M[4] * M[6]);
+}
+
+// Chebyshev weights: omega_m = 1 (m <= 2), 2/(2-rho^2) (m = 3), 4/(4 - rho^2 omega_{m-1})
+double chebyshev_weight(int64_t m, double rho) {
+    if (m <= 2) return 1.0;
+    double w = 2.0 / (2.0 - rho * rho);
+    for (int64_t k = 4; k <= m; ++k) w = 4.0 / (4.0 - rho * rho * w);
+    return w;
+}
+
+struct Region {
+    size_t off = 0, bytes = 0;
+};
+
+}  // namespace
+
+struct pbng_ctx {
+    // mesh
+    int64_t nv = 0, nt = 0;
+    int32_t nb = 1;
+    int dtype = DT_F32;
+    int device = -1;
+    cudaStream_t stream = nullptr;
+    std::vector<double> X;
+    std::vector<int32_t> tets;
+    std::vector<double> Bm;  // per tet Dm^{-1} (row-major)
+    std::vector<double> V;   // per tet rest volume
+    // material
+    bool has_material = false;
+    int model = MODEL_NH;
+    std::vector<double> E;
+    double nu = 0, density = 0, grav[3] = {0, 0, 0};
+    // constraints
+    bool has_constraints = false;
+    std::vector<int32_t> pinned;   // ascending
+    std::vector<double> targets;   // [nb][npin][3] in ascending pinned order
+    std::vector<pbng_weak_constraint> wc;
+    // colouring + layout
+    bool colored = false;
+    std::vector<int32_t> colour;
+    int32_t ncol = 0;
+    std::vector<int32_t> orig2int, int2orig;
+    int64_t n_free = 0, n_pairs = 0, n_slots = 0, n_chunks = 0, n_vc = 0;
+    std::vector<int32_t> col_vbegin, col_nfree;
+    std::vector<int64_t> col_chunk;
+    // host images of the device arrays (uploaded by bind)
+    std::vector<int4> h_rec_id;
+    std::vector<unsigned char> h_rec_a, h_rec_b, h_rec_c, h_fext, h_wc_d, h_c_w, h_c_anchor, h_c_K, h_tet_a,
+        h_tet_b, h_tet_c, h_targets;
+    std::vector<int64_t> h_chunk_off;
+    std::vector<int2> h_chunk_v;
+    std::vector<int32_t> h_deg, h_wc_off, h_wc_cid, h_c_n, h_c_node;
+    std::vector<int4> h_tet_id;
+    Problem prob;
+    // workspace plan
+    Region r_rec_id, r_rec_a, r_rec_b, r_rec_c, r_chunk_off, r_chunk_v, r_deg, r_fext, r_wc_off, r_wc_cid, r_wc_d,
+        r_c_n, r_c_node, r_c_w, r_c_anchor, r_c_K, r_tet_id, r_tet_a, r_tet_b, r_tet_c, r_int2orig, r_targets,
+        r_x[3], r_stage, r_part_e, r_part_r, r_results, r_flag;
+    size_t ws_need = 0;
+    // bound device state
+    bool bound = false;
+    void *ws = nullptr;
+    Layout L;
+    bool positions_set = false;
+    int work = 0, out = 1, hist = 2;
+    int64_t l = 0;
+    bool hist_valid = true;
+    int64_t launches = 0;
+    // profiling
+    bool profiling = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
+
+    size_t real_size() const { return dtype == DT_F64 ? 8 : 4; }
+    size_t real4_size() const { return dtype == DT_F64 ? 32 : 16; }
+    bool on_device() const { return device >= 0; }
+
+    ~pbng_ctx() {
+        for (auto &e : ev_used) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+        for (auto &e : ev_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    }
+
+    void invalidate_colouring() {
+        colored = false;
+        bound = false;
+        positions_set = false;
+    }
+};
+
+namespace {
+
+// ------------------------------------------------------------------------------------------------
+// typed writers for the host images
+// ------------------------------------------------------------------------------------------------
+template <class R>
+void put4(std::vector<unsigned char> &buf, int64_t idx, double a, double b, double c, double d) {
+    R *p = reinterpret_cast<R *>(buf.data()) + 4 * idx;
+    p[0] = R(a); p[1] = R(b); p[2] = R(c); p[3] = R(d);
+}
+
+template <class R>
+void put1(std::vector<unsigned char> &buf, int64_t idx, double a) {
+    reinterpret_cast<R *>(buf.data())[idx] = R(a);
+}
+
+// gradient of local node k of tet e (k >= 1: row k-1 of Dm^{-1}; k = 0: minus the row sum)
+inline void shape_grad(const pbng_ctx *c, int64_t e, int k, double g[3]) {
+    const double *B = c->Bm.data() + 9 * e;
+    for (int b = 0; b < 3; ++b) g[b] = k > 0 ? B[3 * (k - 1) + b] : -(B[b] + B[3 + b] + B[6 + b]);
+}
+
+// ------------------------------------------------------------------------------------------------
+// greedy node colouring, PAPER.md:702-705 (library implementation: 64-bit used-colour masks per
+// stencil; vertices in ascending index; colour = least colour not used by any stencil of the vertex)
+// ------------------------------------------------------------------------------------------------
+pbng_status colour_greedy(pbng_ctx *c, const std::vector<int64_t> &vs_off, const std::vector<int64_t> &vs) {
+    const int64_t n_st = c->nt + (int64_t)c->wc.size();
+    for (int W = 1;; W *= 2) {
+        std::vector<uint64_t> used((size_t)n_st * W, 0ull);
+        std::vector<uint64_t> forb(W);
+        bool overflow = false;
+        int32_t maxc = 0;
+        for (int64_t v = 0; v < c->nv && !overflow; ++v) {
+            std::fill(forb.begin(), forb.end(), 0ull);
+            for (int64_t k = vs_off[v]; k < vs_off[v + 1]; ++k) {
+                const uint64_t *u = used.data() + (size_t)vs[k] * W;
+                for (int w = 0; w < W; ++w) forb[w] |= u[w];
+            }
+            int32_t col = -1;
+            for (int w = 0; w < W && col < 0; ++w)
+                if (~forb[w]) col = 64 * w + __builtin_ctzll(~forb[w]);
+            if (col < 0) { overflow = true; break; }
+            c->colour[v] = col;
+            maxc = std::max(maxc, col + 1);
+            for (int64_t k = vs_off[v]; k < vs_off[v + 1]; ++k)
+                used[(size_t)vs[k] * W + col / 64] |= 1ull << (col % 64);
+        }
+        if (!overflow) {
+            c->ncol = maxc;
+            return PBNG_OK;
+        }
+        if (W > 1024) return fail(PBNG_E_INVALID_ARGUMENT, "colouring needs more than 65536 colours");
+    }
+}
+
+template <class R>
+void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::vector<int32_t> &vt) {
+    const int64_t nv = c->nv, nt = c->nt, nb = c->nb;
+    const size_t s = sizeof(R), s4 = 4 * sizeof(R);
+    const double cmu = 1.0 / (2.0 * (1.0 + c->nu));
+    const double clam = c->nu / ((1.0 + c->nu) * (1.0 - 2.0 * c->nu));
+    auto Ee = [&](int64_t e) { return c->E.size() == 1 ? c->E[0] : c->E[(size_t)e]; };
+
+    // chunks and degrees
+    c->col_chunk.assign(c->ncol + 1, 0);
+    c->h_deg.assign(c->n_free, 0);
+    for (int64_t i = 0; i < c->n_free; ++i) {
+        const int32_t o = c->int2orig[i];
+        c->h_deg[i] = (int32_t)(vt_off[o + 1] - vt_off[o]);
+    }
+    c->h_chunk_off.clear();
+    c->h_chunk_v.clear();
+    c->h_chunk_off.push_back(0);
+    int64_t n_chunks = 0;
+    for (int32_t col = 0; col < c->ncol; ++col) {
+        c->col_chunk[col] = n_chunks;
+        const int32_t v0 = c->col_vbegin[col], nc = c->col_nfree[col];
+        for (int32_t k = 0; k < nc; k += kChunk) {
+            const int32_t cnt = std::min<int32_t>(kChunk, nc - k);
+            int32_t width = 0;
+            for (int32_t q = 0; q < cnt; ++q) width = std::max(width, c->h_deg[v0 + k + q]);
+            c->h_chunk_v.push_back(make_int2(v0 + k, cnt));
+            c->h_chunk_off.push_back(c->h_chunk_off.back() + (int64_t)width * kChunk);
+            ++n_chunks;
+        }
+    }
+    c->col_chunk[c->ncol] = n_chunks;
+    c->n_chunks = n_chunks;
+    c->n_slots = c->h_chunk_off.back();
+    c->n_pairs = 0;
+    for (int64_t i = 0; i < c->n_free; ++i) c->n_pairs += c->h_deg[i];
+
+    // pair records
+    const int64_t ns = std::max<int64_t>(c->n_slots, 1);
+    c->h_rec_id.assign((size_t)ns, make_int4(0, 0, 0, 0));
+    c->h_rec_a.assign((size_t)ns * s4, 0);
+    c->h_rec_b.assign((size_t)ns * s4, 0);
+    c->h_rec_c.assign((size_t)ns * (c->dtype == DT_F64 ? 2 * s : s), 0);
+    for (int64_t ch = 0; ch < n_chunks; ++ch) {
+        const int2 cv = c->h_chunk_v[ch];
+        for (int32_t lane = 0; lane < cv.y; ++lane) {
+            const int32_t vi = cv.x + lane, o = c->int2orig[vi];
+            int k = 0;
+            for (int64_t q = vt_off[o]; q < vt_off[o + 1]; ++q, ++k) {
+                const int64_t e = vt[q];
+                const int32_t *t = c->tets.data() + 4 * e;
+                int a = 0;
+                while (t[a] != o) ++a;
+                int ids[3], m = 0;
+                double g[3][3];
+                for (int sl = 0; sl < 4; ++sl) {
+                    if (sl == a) continue;
+                    ids[m] = c->orig2int[t[sl]];
+                    shape_grad(c, e, sl, g[m]);
+                    ++m;
+                }
+                const int64_t r = c->h_chunk_off[ch] + (int64_t)k * kChunk + lane;
+                const double VE = c->V[e] * Ee(e);
+                int4 id = make_int4(ids[0], ids[1], ids[2], 0);
+                if (c->dtype == DT_F32) {
+                    const float vf = (float)VE;
+                    std::memcpy(&id.w, &vf, 4);
+                }
+                c->h_rec_id[r] = id;
+                put4<R>(c->h_rec_a, r, g[0][0], g[0][1], g[0][2], g[1][0]);
+                put4<R>(c->h_rec_b, r, g[1][1], g[1][2], g[2][0], g[2][1]);
+                if (c->dtype == DT_F64) {
+                    put1<R>(c->h_rec_c, 2 * r, g[2][2]);
+                    put1<R>(c->h_rec_c, 2 * r + 1, VE);
+                } else {
+                    put1<R>(c->h_rec_c, r, g[2][2]);
+                }
+            }
+        }
+    }
+
+    // body force f^ext_i = sum_e R^0 g V_e / 4, free vertices
+    const bool has_fext = c->density > 0 && (c->grav[0] != 0 || c->grav[1] != 0 || c->grav[2] != 0);
+    c->h_fext.assign(has_fext ? (size_t)std::max<int64_t>(c->n_free, 1) * s4 : 0, 0);
+    if (has_fext)
+        for (int64_t i = 0; i < c->n_free; ++i) {
+            const int32_t o = c->int2orig[i];
+            double m = 0;
+            for (int64_t q = vt_off[o]; q < vt_off[o + 1]; ++q) m += c->density * c->V[vt[q]] / 4.0;
+            put4<R>(c->h_fext, i, m * c->grav[0], m * c->grav[1], m * c->grav[2], 0.0);
+        }
+
+    // weak constraints: distinct nodes with combined weights w0_j - w1_j; per free vertex CSR
+    const int64_t nwc = (int64_t)c->wc.size();
+    c->h_c_n.assign((size_t)std::max<int64_t>(nwc, 1), 0);
+    c->h_c_node.assign((size_t)std::max<int64_t>(nwc, 1) * kWcMaxNodes, 0);
+    c->h_c_w.assign((size_t)std::max<int64_t>(nwc, 1) * kWcMaxNodes * s, 0);
+    c->h_c_anchor.assign((size_t)std::max<int64_t>(nwc, 1) * s4, 0);
+    c->h_c_K.assign((size_t)std::max<int64_t>(nwc, 1) * kWcMaxNodes * s, 0);
+    std::vector<std::vector<std::pair<int32_t, double>>> per_v((size_t)c->n_free);
+    for (int64_t ci = 0; ci < nwc; ++ci) {
+        const pbng_weak_constraint &w = c->wc[ci];
+        int32_t nodes[kWcMaxNodes];
+        double wt[kWcMaxNodes];
+        int nn = 0;
+        auto add = [&](int32_t node, double weight) {
+            for (int q = 0; q < nn; ++q)
+                if (nodes[q] == node) { wt[q] += weight; return; }
+            nodes[nn] = node;
+            wt[nn] = weight;
+            ++nn;
+        };
+        for (int q = 0; q < w.n0; ++q) add(w.idx0[q], w.w0[q]);
+        for (int q = 0; q < w.n1; ++q) add(w.idx1[q], -w.w1[q]);
+        c->h_c_n[ci] = nn;
+        for (int q = 0; q < nn; ++q) {
+            c->h_c_node[kWcMaxNodes * ci + q] = c->orig2int[nodes[q]];
+            put1<R>(c->h_c_w, kWcMaxNodes * ci + q, wt[q]);
+            const int32_t vi = c->orig2int[nodes[q]];
+            if (vi < c->n_free) per_v[vi].push_back({(int32_t)ci, wt[q]});
+        }
+        if (w.n1 == 0) put4<R>(c->h_c_anchor, ci, w.anchor[0], w.anchor[1], w.anchor[2], 0.0);
+        for (int q = 0; q < 6; ++q) put1<R>(c->h_c_K, kWcMaxNodes * ci + q, w.K[q]);
+    }
+    c->h_wc_off.assign((size_t)c->n_free + 1, 0);
+    for (int64_t i = 0; i < c->n_free; ++i) c->h_wc_off[i + 1] = c->h_wc_off[i] + (int32_t)per_v[i].size();
+    c->n_vc = c->h_wc_off[c->n_free];
+    c->h_wc_cid.assign((size_t)std::max<int64_t>(c->n_vc, 1), 0);
+    c->h_wc_d.assign((size_t)std::max<int64_t>(c->n_vc, 1) * s, 0);
+    for (int64_t i = 0; i < c->n_free; ++i)
+        for (size_t q = 0; q < per_v[i].size(); ++q) {
+            c->h_wc_cid[c->h_wc_off[i] + q] = per_v[i][q].first;
+            put1<R>(c->h_wc_d, c->h_wc_off[i] + q, per_v[i][q].second);
+        }
+
+    // tet records for the energy pass
+    const int64_t ntr = std::max<int64_t>(nt, 1);
+    c->h_tet_id.assign((size_t)ntr, make_int4(0, 0, 0, 0));
+    c->h_tet_a.assign((size_t)ntr * s4, 0);
+    c->h_tet_b.assign((size_t)ntr * s4, 0);
+    c->h_tet_c.assign((size_t)ntr * s4, 0);
+    for (int64_t e = 0; e < nt; ++e) {
+        const int32_t *t = c->tets.data() + 4 * e;
+        const double *B = c->Bm.data() + 9 * e;
+        c->h_tet_id[e] = make_int4(c->orig2int[t[0]], c->orig2int[t[1]], c->orig2int[t[2]], c->orig2int[t[3]]);
+        put4<R>(c->h_tet_a, e, B[0], B[1], B[2], B[3]);
+        put4<R>(c->h_tet_b, e, B[4], B[5], B[6], B[7]);
+        put4<R>(c->h_tet_c, e, B[8], c->V[e] * Ee(e), c->V[e], 0.0);
+    }
+
+    // Dirichlet targets as Real4 [nb][npin]
+    const int64_t np = (int64_t)c->pinned.size();
+    c->h_targets.assign((size_t)std::max<int64_t>(nb * np, 1) * s4, 0);
+    for (int64_t b = 0; b < nb; ++b)
+        for (int64_t k = 0; k < np; ++k) {
+            const double *t = c->targets.data() + 3 * (b * np + k);
+            put4<R>(c->h_targets, b * np + k, t[0], t[1], t[2], 0.0);
+        }
+
+    // problem constants
+    Problem &p = c->prob;
+    p.dtype = c->dtype;
+    p.model = c->model;
+    p.n_vertices = nv;
+    p.n_free = c->n_free;
+    p.n_pinned = np;
+    p.n_tets = nt;
+    p.n_cons = nwc;
+    p.n_chunks = n_chunks;
+    p.n_batch = c->nb;
+    p.x_stride = (int64_t)align_up((size_t)nv, 64);
+    p.cmu = cmu;
+    p.clam = clam;
+    for (int k = 0; k < 3; ++k) p.rho_g[k] = c->density * c->grav[k];
+    p.has_fext = has_fext;
+    p.has_wc = c->n_vc > 0;
+    const int64_t items = nt + nwc;
+    p.ge = (int)std::max<int64_t>(1, std::min<int64_t>((items + kRedBlock - 1) / kRedBlock, 1184));
+    p.gr = (int)std::max<int64_t>(1, std::min<int64_t>((n_chunks * kChunk + kRedBlock - 1) / kRedBlock, 1184));
+}
+
+void plan_workspace(pbng_ctx *c) {
+    size_t off = 0;
+    auto take = [&](Region &r, size_t bytes) {
+        r.off = off;
+        r.bytes = std::max<size_t>(bytes, 1);
+        off = align_up(off + r.bytes, 256);
+    };
+    const Problem &p = c->prob;
+    const size_t s = c->real_size(), s4 = c->real4_size();
+    const int64_t ns = std::max<int64_t>(c->n_slots, 1);
+    take(c->r_rec_id, (size_t)ns * 16);
+    take(c->r_rec_a, (size_t)ns * s4);
+    take(c->r_rec_b, (size_t)ns * s4);
+    take(c->r_rec_c, c->h_rec_c.size());
+    take(c->r_chunk_off, c->h_chunk_off.size() * 8);
+    take(c->r_chunk_v, std::max<size_t>(c->h_chunk_v.size(), 1) * 8);
+    take(c->r_deg, std::max<size_t>(c->h_deg.size(), 1) * 4);
+    take(c->r_fext, c->h_fext.size());
+    take(c->r_wc_off, c->h_wc_off.size() * 4);
+    take(c->r_wc_cid, c->h_wc_cid.size() * 4);
+    take(c->r_wc_d, c->h_wc_d.size());
+    take(c->r_c_n, c->h_c_n.size() * 4);
+    take(c->r_c_node, c->h_c_node.size() * 4);
+    take(c->r_c_w, c->h_c_w.size());
+    take(c->r_c_anchor, c->h_c_anchor.size());
+    take(c->r_c_K, c->h_c_K.size());
+    take(c->r_tet_id, c->h_tet_id.size() * 16);
+    take(c->r_tet_a, c->h_tet_a.size());
+    take(c->r_tet_b, c->h_tet_b.size());
+    take(c->r_tet_c, c->h_tet_c.size());
+    take(c->r_int2orig, (size_t)c->nv * 4);
+    take(c->r_targets, c->h_targets.size());
+    for (int k = 0; k < 3; ++k) take(c->r_x[k], (size_t)c->nb * (size_t)p.x_stride * s4);
+    take(c->r_stage, (size_t)c->nb * (size_t)c->nv * 3 * s);
+    take(c->r_part_e, (size_t)c->nb * p.ge * 8);
+    take(c->r_part_r, (size_t)c->nb * p.gr * 8);
+    take(c->r_results, (size_t)c->nb * 2 * 8);
+    take(c->r_flag, 4);
+    c->ws_need = off;
+}
+
+double sweep_bytes_model(const pbng_ctx *c) {
+    // algorithmic HBM bytes of one iteration: pair records once (shared by the
+    // samples of a batch), chunk offsets, per free vertex and sample: degree, position write, blend
+    // traffic (x^{l-1} read, x^{l-1} and x^{l+1} writes) and body force; all positions read once.
+    const double s = (double)c->real_size();
+    const double rec = c->dtype == DT_F64 ? 96.0 : 52.0;
+    double b = (double)c->n_pairs * rec + (double)(c->n_chunks + 1) * 8.0 + (double)c->n_free * 4.0;
+    double per_v = 3 * s;  // write x_PBNG
+    per_v += (c->prob.has_fext ? 3 * s : 0);
+    b += (double)c->nb * ((double)c->n_free * per_v + (double)c->nv * 3 * s);
+    return b;
+}
+
+double accel_bytes_model(const pbng_ctx *c) {
+    return (double)c->nb * (double)c->n_free * 9.0 * (double)c->real_size();
+}
+
+pbng_status require_device(pbng_ctx *c) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    if (!c->on_device()) return fail(PBNG_E_NO_DEVICE, "host-only context (device = -1)");
+    return PBNG_OK;
+}
+
+cudaError_t timed_sweep(pbng_ctx *c, const SweepLaunch &s) {
+    if (!c->profiling) return launch_sweep(c->prob, c->L, s, c->stream);
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    if (!c->ev_free.empty()) {
+        ev = c->ev_free.back();
+        c->ev_free.pop_back();
+    } else {
+        cudaError_t e = cudaEventCreate(&ev.first);
+        if (e != cudaSuccess) return e;
+        e = cudaEventCreate(&ev.second);
+        if (e != cudaSuccess) return e;
+    }
+    cudaEventRecord(ev.first, c->stream);
+    cudaError_t e = launch_sweep(c->prob, c->L, s, c->stream);
+    cudaEventRecord(ev.second, c->stream);
+    c->ev_used.push_back(ev);
+    return e;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *pbng_last_error(void) { return g_err.c_str(); }
+
+int32_t pbng_version(void) { return 100; }
+
+pbng_status pbng_create_mesh(const double *rest_xyz, int64_t n_vertices, const int32_t *tets, int64_t n_tets,
+                             int32_t n_batch, pbng_dtype dtype, int device, uintptr_t cuda_stream, pbng_ctx **out,
+                             int64_t *bad_index) {
+    if (bad_index) *bad_index = -1;
+    if (!out) return fail(PBNG_E_INVALID_ARGUMENT, "out is null");
+    *out = nullptr;
+    if (!rest_xyz || n_vertices <= 0 || n_vertices > INT32_MAX - 64 || n_tets < 0 || (n_tets > 0 && !tets) ||
+        n_batch < 1 || (dtype != PBNG_F32 && dtype != PBNG_F64) || device < -1)
+        return fail(PBNG_E_INVALID_ARGUMENT, "create_mesh: bad sizes, pointers, dtype or device");
+    if (device >= 0) {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || device >= n)
+            return fail(PBNG_E_CUDA, "create_mesh: CUDA device " + std::to_string(device) + " not available");
+    }
+    for (int64_t k = 0; k < n_vertices * 3; ++k)
+        if (!std::isfinite(rest_xyz[k])) return fail(PBNG_E_INVALID_ARGUMENT, "create_mesh: non-finite rest position");
+    for (int64_t e = 0; e < n_tets; ++e)
+        for (int a = 0; a < 4; ++a)
+            if (tets[4 * e + a] < 0 || tets[4 * e + a] >= n_vertices) {
+                if (bad_index) *bad_index = e;
+                return fail(PBNG_E_INDEX_OUT_OF_RANGE, "create_mesh: tet " + std::to_string(e) + " has a vertex out of range");
+            }
+    pbng_ctx *c = new (std::nothrow) pbng_ctx();
+    if (!c) return fail(PBNG_E_OUT_OF_MEMORY, "create_mesh: host allocation");
+    try {
+        c->nv = n_vertices;
+        c->nt = n_tets;
+        c->nb = n_batch;
+        c->dtype = dtype;
+        c->device = device;
+        c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+        c->X.assign(rest_xyz, rest_xyz + 3 * n_vertices);
+        c->tets.assign(tets, tets + 4 * n_tets);
+        c->Bm.resize((size_t)n_tets * 9);
+        c->V.resize((size_t)n_tets);
+        // rest precompute: Dm = [X1-X0, X2-X0, X3-X0], B = Dm^{-1}, V = |det Dm| / 6
+        for (int64_t e = 0; e < n_tets; ++e) {
+            const int32_t *t = tets + 4 * e;
+            double Dm[9], ell = 0.0;
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b) Dm[3 * a + b] = c->X[3 * t[b + 1] + a] - c->X[3 * t[0] + a];
+            static const int pa[6] = {0, 0, 0, 1, 1, 2}, pb[6] = {1, 2, 3, 2, 3, 3};
+            for (int q = 0; q < 6; ++q) {
+                double d2 = 0;
+                for (int b = 0; b < 3; ++b) {
+                    const double d = c->X[3 * t[pa[q]] + b] - c->X[3 * t[pb[q]] + b];
+                    d2 += d * d;
+                }
+                ell += std::sqrt(d2) / 6.0;
+            }
+            const double det = det3(Dm);
+            if (!(std::fabs(det) > 1e-12 * ell * ell * ell)) {
+                delete c;
+                if (bad_index) *bad_index = e;
+                return fail(PBNG_E_DEGENERATE_ELEMENT, "create_mesh: tet " + std::to_string(e) + " is degenerate");
+            }
+            const double inv = 1.0 / det;
+            double *B = c->Bm.data() + 9 * e;
+            // inverse = adjugate / det (adjugate = transpose of the cofactor matrix)
+            B[0] = (Dm[4] * Dm[8] - Dm[5] * Dm[7]) * inv;
+            B[1] = (Dm[2] * Dm[7] - Dm[1] * Dm[8]) * inv;
+            B[2] = (Dm[1] * Dm[5] - Dm[2] * Dm[4]) * inv;
+            B[3] = (Dm[5] * Dm[6] - Dm[3] * Dm[8]) * inv;
+            B[4] = (Dm[0] * Dm[8] - Dm[2] * Dm[6]) * inv;
+            B[5] = (Dm[2] * Dm[3] - Dm[0] * Dm[5]) * inv;
+            B[6] = (Dm[3] * Dm[7] - Dm[4] * Dm[6]) * inv;
+            B[7] = (Dm[1] * Dm[6] - Dm[0] * Dm[7]) * inv;
+            B[8] = (Dm[0] * Dm[4] - Dm[1] * Dm[3]) * inv;
+            c->V[e] = std::fabs(det) / 6.0;
+        }
+    } catch (const std::bad_alloc &) {
+        delete c;
+        return fail(PBNG_E_OUT_OF_MEMORY, "create_mesh: host allocation");
+    }
+    *out = c;
+    return PBNG_OK;
+}
+
+pbng_status pbng_set_material(pbng_ctx *c, pbng_model model, const double *E, int64_t n_E, double nu, double density,
+                              const double gravity[3]) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    if (model != PBNG_NEOHOOKEAN && model != PBNG_FIXED_COROTATED)
+        return fail(PBNG_E_INVALID_ARGUMENT, "set_material: unknown model");
+    if (!E || (n_E != 1 && n_E != c->nt)) return fail(PBNG_E_INVALID_ARGUMENT, "set_material: E must have 1 or n_tets entries");
+    for (int64_t k = 0; k < n_E; ++k)
+        if (!(E[k] > 0.0) || !std::isfinite(E[k])) return fail(PBNG_E_INVALID_ARGUMENT, "set_material: E must be positive and finite");
+    if (!(nu >= 0.0 && nu < 0.5)) return fail(PBNG_E_INVALID_ARGUMENT, "set_material: nu must be in [0, 0.5)");
+    if (!(density >= 0.0) || !std::isfinite(density)) return fail(PBNG_E_INVALID_ARGUMENT, "set_material: density must be >= 0");
+    double g[3] = {0, 0, 0};
+    if (gravity)
+        for (int k = 0; k < 3; ++k) {
+            if (!std::isfinite(gravity[k])) return fail(PBNG_E_INVALID_ARGUMENT, "set_material: non-finite gravity");
+            g[k] = gravity[k];
+        }
+    try {
+        c->E.assign(E, E + n_E);
+    } catch (const std::bad_alloc &) {
+        return fail(PBNG_E_OUT_OF_MEMORY, "set_material: host allocation");
+    }
+    c->model = model;
+    c->nu = nu;
+    c->density = density;
+    for (int k = 0; k < 3; ++k) c->grav[k] = g[k];
+    c->has_material = true;
+    c->invalidate_colouring();
+    return PBNG_OK;
+}
+
+pbng_status pbng_set_constraints(pbng_ctx *c, const int32_t *pinned, int64_t n_pinned, const double *pinned_xyz,
+                                 const pbng_weak_constraint *wc, int64_t n_wc) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    if (n_pinned < 0 || n_pinned > c->nv || (n_pinned > 0 && (!pinned || !pinned_xyz)) || n_wc < 0 || (n_wc > 0 && !wc))
+        return fail(PBNG_E_INVALID_ARGUMENT, "set_constraints: bad sizes or pointers");
+    std::vector<char> seen((size_t)c->nv, 0);
+    for (int64_t k = 0; k < n_pinned; ++k) {
+        if (pinned[k] < 0 || pinned[k] >= c->nv) return fail(PBNG_E_INDEX_OUT_OF_RANGE, "set_constraints: pinned vertex out of range");
+        if (seen[pinned[k]]) return fail(PBNG_E_INVALID_ARGUMENT, "set_constraints: duplicate pinned vertex");
+        seen[pinned[k]] = 1;
+    }
+    for (int64_t k = 0; k < (int64_t)c->nb * n_pinned * 3; ++k)
+        if (!std::isfinite(pinned_xyz[k])) return fail(PBNG_E_INVALID_ARGUMENT, "set_constraints: non-finite target");
+    for (int64_t q = 0; q < n_wc; ++q) {
+        const pbng_weak_constraint &w = wc[q];
+        if (w.n0 < 1 || w.n0 > 4 || w.n1 < 0 || w.n1 > 4)
+            return fail(PBNG_E_INVALID_ARGUMENT, "set_constraints: weak constraint " + std::to_string(q) + " has bad node counts");
+        for (int a = 0; a < w.n0; ++a)
+            if (w.idx0[a] < 0 || w.idx0[a] >= c->nv || !std::isfinite(w.w0[a]))
+                return fail(PBNG_E_INDEX_OUT_OF_RANGE, "set_constraints: weak constraint " + std::to_string(q) + " side 0");
+        for (int a = 0; a < w.n1; ++a)
+            if (w.idx1[a] < 0 || w.idx1[a] >= c->nv || !std::isfinite(w.w1[a]))
+                return fail(PBNG_E_INDEX_OUT_OF_RANGE, "set_constraints: weak constraint " + std::to_string(q) + " side 1");
+        for (int a = 0; a < 6; ++a)
+            if (!std::isfinite(w.K[a])) return fail(PBNG_E_INVALID_ARGUMENT, "set_constraints: non-finite K");
+        for (int a = 0; a < 3; ++a)
+            if (!std::isfinite(w.anchor[a])) return fail(PBNG_E_INVALID_ARGUMENT, "set_constraints: non-finite anchor");
+    }
+    try {
+        std::vector<int64_t> order((size_t)n_pinned);
+        for (int64_t k = 0; k < n_pinned; ++k) order[k] = k;
+        std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return pinned[a] < pinned[b]; });
+        c->pinned.resize((size_t)n_pinned);
+        c->targets.resize((size_t)c->nb * n_pinned * 3);
+        for (int64_t k = 0; k < n_pinned; ++k) {
+            c->pinned[k] = pinned[order[k]];
+            for (int64_t b = 0; b < c->nb; ++b)
+                for (int a = 0; a < 3; ++a)
+                    c->targets[3 * (b * n_pinned + k) + a] = pinned_xyz[3 * (b * n_pinned + order[k]) + a];
+        }
+        c->wc.assign(wc, wc + n_wc);
+    } catch (const std::bad_alloc &) {
+        return fail(PBNG_E_OUT_OF_MEMORY, "set_constraints: host allocation");
+    }
+    c->has_constraints = true;
+    c->invalidate_colouring();
+    return PBNG_OK;
+}
+
+pbng_status pbng_color(pbng_ctx *c, int32_t *colour_out, int32_t *n_colours_out) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    if (!c->has_material || !c->has_constraints)
+        return fail(PBNG_E_BAD_ORDER, "color: set_material and set_constraints must come first");
+    try {
+        const int64_t nv = c->nv, nt = c->nt, nwc = (int64_t)c->wc.size();
+        // vertex -> incident tets (ascending tet index) and vertex -> stencils (tets, then constraints)
+        std::vector<int64_t> vt_off((size_t)nv + 1, 0), vs_off((size_t)nv + 1, 0);
+        for (int64_t e = 0; e < nt; ++e)
+            for (int a = 0; a < 4; ++a) vt_off[c->tets[4 * e + a] + 1]++;
+        for (int64_t v = 0; v < nv; ++v) vt_off[v + 1] += vt_off[v];
+        std::vector<int32_t> vt((size_t)std::max<int64_t>(vt_off[nv], 1));
+        {
+            std::vector<int64_t> fill(vt_off.begin(), vt_off.end() - 1);
+            for (int64_t e = 0; e < nt; ++e)
+                for (int a = 0; a < 4; ++a) vt[fill[c->tets[4 * e + a]]++] = (int32_t)e;
+        }
+        std::vector<std::vector<int32_t>> cnodes((size_t)nwc);
+        for (int64_t q = 0; q < nwc; ++q) {
+            const pbng_weak_constraint &w = c->wc[q];
+            for (int a = 0; a < w.n0; ++a) cnodes[q].push_back(w.idx0[a]);
+            for (int a = 0; a < w.n1; ++a) cnodes[q].push_back(w.idx1[a]);
+            std::sort(cnodes[q].begin(), cnodes[q].end());
+            cnodes[q].erase(std::unique(cnodes[q].begin(), cnodes[q].end()), cnodes[q].end());
+        }
+        std::vector<int64_t> vc_cnt((size_t)nv, 0);
+        for (int64_t q = 0; q < nwc; ++q)
+            for (int32_t v : cnodes[q]) vc_cnt[v]++;
+        for (int64_t v = 0; v < nv; ++v) vs_off[v + 1] = vs_off[v] + (vt_off[v + 1] - vt_off[v]) + vc_cnt[v];
+        std::vector<int64_t> vs((size_t)std::max<int64_t>(vs_off[nv], 1));
+        {
+            std::vector<int64_t> fill(vs_off.begin(), vs_off.end() - 1);
+            for (int64_t v = 0; v < nv; ++v)
+                for (int64_t k = vt_off[v]; k < vt_off[v + 1]; ++k) vs[fill[v]++] = vt[k];
+            for (int64_t q = 0; q < nwc; ++q)
+                for (int32_t v : cnodes[q]) vs[fill[v]++] = nt + q;
+        }
+        // isolated free vertices make A singular
+        std::vector<char> is_pinned((size_t)nv, 0);
+        for (int32_t p : c->pinned) is_pinned[p] = 1;
+        for (int64_t v = 0; v < nv; ++v)
+            if (!is_pinned[v] && vs_off[v + 1] == vs_off[v])
+                return fail(PBNG_E_ISOLATED_VERTEX, "color: free vertex " + std::to_string(v) + " has no element or constraint");
+        c->colour.assign((size_t)nv, 0);
+        pbng_status st = colour_greedy(c, vs_off, vs);
+        if (st != PBNG_OK) return st;
+        // permutation: free vertices colour-major (ascending original index within a colour), then pinned
+        c->col_vbegin.assign(c->ncol + 1, 0);
+        c->col_nfree.assign(c->ncol, 0);
+        for (int64_t v = 0; v < nv; ++v)
+            if (!is_pinned[v]) c->col_nfree[c->colour[v]]++;
+        for (int32_t k = 0; k < c->ncol; ++k) c->col_vbegin[k + 1] = c->col_vbegin[k] + c->col_nfree[k];
+        c->n_free = c->col_vbegin[c->ncol];
+        c->orig2int.assign((size_t)nv, 0);
+        c->int2orig.assign((size_t)nv, 0);
+        {
+            std::vector<int32_t> fill(c->col_vbegin.begin(), c->col_vbegin.end() - 1);
+            int32_t pin_next = (int32_t)c->n_free;
+            for (int64_t v = 0; v < nv; ++v) {
+                const int32_t i = is_pinned[v] ? pin_next++ : fill[c->colour[v]]++;
+                c->orig2int[v] = i;
+                c->int2orig[i] = (int32_t)v;
+            }
+        }
+        if (c->dtype == DT_F64) build_layout<double>(c, vt_off, vt);
+        else build_layout<float>(c, vt_off, vt);
+        plan_workspace(c);
+    } catch (const std::bad_alloc &) {
+        return fail(PBNG_E_OUT_OF_MEMORY, "color: host allocation");
+    }
+    c->colored = true;
+    c->bound = false;
+    c->positions_set = false;
+    if (colour_out) std::memcpy(colour_out, c->colour.data(), (size_t)c->nv * 4);
+    if (n_colours_out) *n_colours_out = c->ncol;
+    return PBNG_OK;
+}
+
+pbng_status pbng_workspace_bytes(pbng_ctx *c, uint64_t *bytes) {
+    if (!c || !bytes) return fail(PBNG_E_INVALID_ARGUMENT, "null argument");
+    if (!c->colored) return fail(PBNG_E_NOT_COLORED, "workspace_bytes: call pbng_color first");
+    *bytes = c->ws_need;
+    return PBNG_OK;
+}
+
+pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    if (!c->colored) return fail(PBNG_E_NOT_COLORED, "bind_workspace: call pbng_color first");
+    if (!dptr || (reinterpret_cast<uintptr_t>(dptr) & 255u) != 0)
+        return fail(PBNG_E_INVALID_ARGUMENT, "bind_workspace: pointer must be non-null and 256-byte aligned");
+    if (bytes < c->ws_need) return fail(PBNG_E_OUT_OF_MEMORY, "bind_workspace: workspace smaller than pbng_workspace_bytes");
+    DevGuard g(c->device);
+    char *base = static_cast<char *>(dptr);
+    auto at = [&](const Region &r) { return static_cast<void *>(base + r.off); };
+    Layout L;
+    L.rec_id = static_cast<const int4 *>(at(c->r_rec_id));
+    L.rec_a = at(c->r_rec_a);
+    L.rec_b = at(c->r_rec_b);
+    L.rec_c = at(c->r_rec_c);
+    L.chunk_off = static_cast<const int64_t *>(at(c->r_chunk_off));
+    L.chunk_v = static_cast<const int2 *>(at(c->r_chunk_v));
+    L.deg = static_cast<const int32_t *>(at(c->r_deg));
+    L.fext = c->prob.has_fext ? at(c->r_fext) : nullptr;
+    L.wc_off = static_cast<const int32_t *>(at(c->r_wc_off));
+    L.wc_cid = static_cast<const int32_t *>(at(c->r_wc_cid));
+    L.wc_d = at(c->r_wc_d);
+    L.c_n = static_cast<const int32_t *>(at(c->r_c_n));
+    L.c_node = static_cast<const int32_t *>(at(c->r_c_node));
+    L.c_w = at(c->r_c_w);
+    L.c_anchor = at(c->r_c_anchor);
+    L.c_K = at(c->r_c_K);
+    L.tet_id = static_cast<const int4 *>(at(c->r_tet_id));
+    L.tet_a = at(c->r_tet_a);
+    L.tet_b = at(c->r_tet_b);
+    L.tet_c = at(c->r_tet_c);
+    L.int2orig = static_cast<const int32_t *>(at(c->r_int2orig));
+    L.targets = at(c->r_targets);
+    for (int k = 0; k < 3; ++k) L.xbuf[k] = at(c->r_x[k]);
+    L.stage = at(c->r_stage);
+    L.part_e = static_cast<double *>(at(c->r_part_e));
+    L.part_r = static_cast<double *>(at(c->r_part_r));
+    L.results = static_cast<double *>(at(c->r_results));
+    L.flag = static_cast<int32_t *>(at(c->r_flag));
+    auto up = [&](const Region &r, const void *src, size_t n) -> cudaError_t {
+        if (n == 0) return cudaSuccess;
+        return cudaMemcpyAsync(base + r.off, src, n, cudaMemcpyHostToDevice, c->stream);
+    };
+    cudaError_t e = cudaSuccess;
+    auto chk = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
+    chk(up(c->r_rec_id, c->h_rec_id.data(), c->h_rec_id.size() * 16));
+    chk(up(c->r_rec_a, c->h_rec_a.data(), c->h_rec_a.size()));
+    chk(up(c->r_rec_b, c->h_rec_b.data(), c->h_rec_b.size()));
+    chk(up(c->r_rec_c, c->h_rec_c.data(), c->h_rec_c.size()));
+    chk(up(c->r_chunk_off, c->h_chunk_off.data(), c->h_chunk_off.size() * 8));
+    chk(up(c->r_chunk_v, c->h_chunk_v.data(), c->h_chunk_v.size() * 8));
+    chk(up(c->r_deg, c->h_deg.data(), c->h_deg.size() * 4));
+    chk(up(c->r_fext, c->h_fext.data(), c->h_fext.size()));
+    chk(up(c->r_wc_off, c->h_wc_off.data(), c->h_wc_off.size() * 4));
+    chk(up(c->r_wc_cid, c->h_wc_cid.data(), c->h_wc_cid.size() * 4));
+    chk(up(c->r_wc_d, c->h_wc_d.data(), c->h_wc_d.size()));
+    chk(up(c->r_c_n, c->h_c_n.data(), c->h_c_n.size() * 4));
+    chk(up(c->r_c_node, c->h_c_node.data(), c->h_c_node.size() * 4));
+    chk(up(c->r_c_w, c->h_c_w.data(), c->h_c_w.size()));
+    chk(up(c->r_c_anchor, c->h_c_anchor.data(), c->h_c_anchor.size()));
+    chk(up(c->r_c_K, c->h_c_K.data(), c->h_c_K.size()));
+    chk(up(c->r_tet_id, c->h_tet_id.data(), c->h_tet_id.size() * 16));
+    chk(up(c->r_tet_a, c->h_tet_a.data(), c->h_tet_a.size()));
+    chk(up(c->r_tet_b, c->h_tet_b.data(), c->h_tet_b.size()));
+    chk(up(c->r_tet_c, c->h_tet_c.data(), c->h_tet_c.size()));
+    chk(up(c->r_int2orig, c->int2orig.data(), c->int2orig.size() * 4));
+    chk(up(c->r_targets, c->h_targets.data(), c->h_targets.size()));
+    chk(cudaMemsetAsync(base + c->r_flag.off, 0, 4, c->stream));
+    chk(cudaStreamSynchronize(c->stream));
+    if (e != cudaSuccess) return cuda_fail(e, "bind_workspace");
+    c->ws = dptr;
+    c->L = L;
+    c->bound = true;
+    c->positions_set = false;
+    return PBNG_OK;
+}
+
+pbng_status pbng_set_positions(pbng_ctx *c, const void *x) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    if (!c->bound) return fail(PBNG_E_BAD_ORDER, "set_positions: bind a workspace first");
+    if (!x) return fail(PBNG_E_INVALID_ARGUMENT, "set_positions: null pointer");
+    DevGuard g(c->device);
+    const size_t n = (size_t)c->nb * (size_t)c->nv * 3 * c->real_size();
+    PBNG_CUDA(cudaMemcpyAsync(c->L.stage, x, n, cudaMemcpyDefault, c->stream), "set_positions: copy");
+    PBNG_CUDA(cudaMemsetAsync(c->L.flag, 0, 4, c->stream), "set_positions: flag");
+    PBNG_CUDA(launch_set_positions(c->prob, c->L, 3, c->stream), "set_positions: kernel");
+    c->launches += 1;
+    c->work = 0;
+    c->out = 1;
+    c->hist = 2;
+    c->l = 0;
+    c->hist_valid = true;
+    c->positions_set = true;
+    return PBNG_OK;
+}
+
+pbng_status pbng_get_positions(pbng_ctx *c, void *x_out) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    if (!c->positions_set) return fail(PBNG_E_BAD_ORDER, "get_positions: set_positions first");
+    if (!x_out) return fail(PBNG_E_INVALID_ARGUMENT, "get_positions: null pointer");
+    DevGuard g(c->device);
+    PBNG_CUDA(launch_get_positions(c->prob, c->L, c->work, c->stream), "get_positions: kernel");
+    c->launches += 1;
+    const size_t n = (size_t)c->nb * (size_t)c->nv * 3 * c->real_size();
+    PBNG_CUDA(cudaMemcpyAsync(x_out, c->L.stage, n, cudaMemcpyDefault, c->stream), "get_positions: copy");
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, x_out) != cudaSuccess) {
+        cudaGetLastError();
+        attr.type = cudaMemoryTypeUnregistered;
+    }
+    if (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged)
+        PBNG_CUDA(cudaStreamSynchronize(c->stream), "get_positions: synchronize");
+    return PBNG_OK;
+}
+
+pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, double omega, double rho, double gamma) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    if (!c->positions_set) return fail(PBNG_E_BAD_ORDER, "iterate: set_positions first");
+    if (n_iterations < 0) return fail(PBNG_E_INVALID_ARGUMENT, "iterate: negative iteration count");
+    if (accel != PBNG_ACCEL_NONE && accel != PBNG_ACCEL_SOR && accel != PBNG_ACCEL_CHEBYSHEV)
+        return fail(PBNG_E_INVALID_ARGUMENT, "iterate: unknown acceleration");
+    if (accel == PBNG_ACCEL_SOR && !(omega > 0.0 && omega < 2.0))
+        return fail(PBNG_E_INVALID_ARGUMENT, "iterate: SOR omega must be in (0, 2)");
+    if (accel == PBNG_ACCEL_CHEBYSHEV && (!(rho >= 0.0 && rho < 1.0) || !(gamma > 0.0 && gamma <= 2.0)))
+        return fail(PBNG_E_INVALID_ARGUMENT, "iterate: Chebyshev needs rho in [0,1) and gamma in (0,2]");
+    if (accel != PBNG_ACCEL_NONE && !c->hist_valid)
+        return fail(PBNG_E_BAD_ORDER, "iterate: x^{l-1} was not kept by non-accelerated iterations; call set_positions");
+    DevGuard g(c->device);
+    for (int32_t it = 0; it < n_iterations; ++it) {
+        SweepLaunch s;
+        s.accel = accel;
+        s.work = c->work;
+        s.out = c->out;
+        s.hist = c->hist;
+        if (accel == PBNG_ACCEL_SOR) {
+            s.omega = omega;
+        } else if (accel == PBNG_ACCEL_CHEBYSHEV) {
+            s.omega = chebyshev_weight(c->l + 1, rho);
+            s.gamma = gamma;
+        }
+        for (int32_t col = 0; col < c->ncol; ++col) {
+            s.v_begin = c->col_vbegin[col];
+            s.n_v = c->col_nfree[col];
+            s.chunk_begin = c->col_chunk[col];
+            if (s.n_v == 0) continue;
+            PBNG_CUDA(timed_sweep(c, s), "iterate: sweep kernel");
+            c->launches += 1;
+        }
+        if (accel != PBNG_ACCEL_NONE) std::swap(c->work, c->out);
+        else c->hist_valid = false;
+        c->l += 1;
+    }
+    return PBNG_OK;
+}
+
+pbng_status pbng_synchronize(pbng_ctx *c) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    DevGuard g(c->device);
+    PBNG_CUDA(cudaStreamSynchronize(c->stream), "synchronize");
+    if (c->bound) {
+        int32_t flag = 0;
+        PBNG_CUDA(cudaMemcpy(&flag, c->L.flag, 4, cudaMemcpyDeviceToHost), "synchronize: flag");
+        if (flag) return fail(PBNG_E_NONFINITE, "a non-finite position was produced");
+    }
+    return PBNG_OK;
+}
+
+pbng_status pbng_energy_residual(pbng_ctx *c, double *energy_out, double *residual_out) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    if (!c->positions_set) return fail(PBNG_E_BAD_ORDER, "energy_residual: set_positions first");
+    DevGuard g(c->device);
+    PBNG_CUDA(launch_energy_residual(c->prob, c->L, c->work, c->stream), "energy_residual: kernels");
+    c->launches += kernels_per_energy_residual();
+    std::vector<double> res((size_t)c->nb * 2);
+    int32_t flag = 0;
+    PBNG_CUDA(cudaMemcpyAsync(res.data(), c->L.results, res.size() * 8, cudaMemcpyDeviceToHost, c->stream),
+              "energy_residual: copy");
+    PBNG_CUDA(cudaMemcpyAsync(&flag, c->L.flag, 4, cudaMemcpyDeviceToHost, c->stream), "energy_residual: flag");
+    PBNG_CUDA(cudaStreamSynchronize(c->stream), "energy_residual: synchronize");
+    for (int64_t b = 0; b < c->nb; ++b) {
+        if (energy_out) energy_out[b] = res[2 * b];
+        if (residual_out) residual_out[b] = res[2 * b + 1];
+    }
+    if (flag) return fail(PBNG_E_NONFINITE, "a non-finite position was produced");
+    return PBNG_OK;
+}
+
+pbng_status pbng_query(pbng_ctx *c, pbng_info *info) {
+    if (!c || !info) return fail(PBNG_E_INVALID_ARGUMENT, "null argument");
+    std::memset(info, 0, sizeof(*info));
+    info->n_vertices = c->nv;
+    info->n_tets = c->nt;
+    info->n_pinned = (int64_t)c->pinned.size();
+    info->n_weak_constraints = (int64_t)c->wc.size();
+    info->n_batch = c->nb;
+    info->dtype = c->dtype;
+    info->model = c->model;
+    info->iteration = c->l;
+    info->kernel_launches = c->launches;
+    if (c->colored) {
+        info->n_free = c->n_free;
+        info->n_pairs = c->n_pairs;
+        info->n_pair_slots = c->n_slots;
+        info->n_colours = c->ncol;
+        info->sweep_bytes = sweep_bytes_model(c);
+        info->accel_bytes = accel_bytes_model(c);
+        const double per_pair = c->model == MODEL_FCR ? 130.0 + 700.0 : 130.0;
+        info->sweep_flops = (double)c->nb * ((double)c->n_pairs * per_pair + (double)c->n_free * 40.0);
+    }
+    return PBNG_OK;
+}
+
+pbng_status pbng_profile_enable(pbng_ctx *c, int enable) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    c->profiling = enable != 0;
+    return PBNG_OK;
+}
+
+pbng_status pbng_profile_read(pbng_ctx *c, double *sweep_ms, int64_t *sweep_launches) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    DevGuard g(c->device);
+    PBNG_CUDA(cudaStreamSynchronize(c->stream), "profile_read: synchronize");
+    double total = 0.0;
+    for (auto &ev : c->ev_used) {
+        float ms = 0.f;
+        PBNG_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second), "profile_read: elapsed");
+        total += ms;
+        c->ev_free.push_back(ev);
+    }
+    if (sweep_ms) *sweep_ms = total;
+    if (sweep_launches) *sweep_launches = (int64_t)c->ev_used.size();
+    c->ev_used.clear();
+    return PBNG_OK;
+}
+
+pbng_status pbng_destroy(pbng_ctx *c) {
+    if (!c) return PBNG_OK;
+    if (c->on_device()) {
+        DevGuard g(c->device);
+        cudaStreamSynchronize(c->stream);
+        delete c;
+    } else {
+        delete c;
+    }
+    return PBNG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// pbng_internal.h -- host <-> device launch interface of libpbng (not part of the public C ABI).
+//
+// The host library (pbng_host.cpp) owns validation, the fp64 rest precompute, the greedy colouring and
+// the colour-sorted layout; the kernels (pbng_kernels.cu) own every step of the per-iteration path.
+// All pointers below point into the caller-bound workspace.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pbng {
+
+enum { MODEL_NH = 0, MODEL_FCR = 1 };
+enum { ACCEL_NONE = 0, ACCEL_SOR = 1, ACCEL_CHEB = 2 };
+enum { DT_F32 = 0, DT_F64 = 1 };
+
+constexpr int kChunk = 32;        // vertices per SELL chunk == one warp
+constexpr int kSweepBlock = 128;  // threads per sweep CTA (4 chunks)
+constexpr int kWcMaxNodes = 8;    // distinct nodes per weak constraint
+constexpr int kRedBlock = 256;    // threads per reduction CTA
+
+// Pair-record layout (SELL-32, one record per (free vertex i, incident tet e), vertex-major within a
+// 32-vertex chunk: slot = chunk_off[chunk] + k * 32 + lane).  For the tet's three OTHER vertices j
+// (in slot order) the record holds the internal vertex ids and the shape-function gradients g_j
+// (rows of Dm^{-1} or minus their sum); g_i = -(g_1 + g_2 + g_3); VE = V_e E_e.
+//   f32: rec_id int4 {n1, n2, n3, bits(VE)}; rec_a float4 {g1x g1y g1z g2x}; rec_b float4
+//        {g2y g2z g3x g3y}; rec_c float {g3z}                                      -> 52 bytes
+//   f64: rec_id int4 {n1, n2, n3, 0}; rec_a double4; rec_b double4; rec_c double2 {g3z, VE} -> 96 bytes
+struct Layout {
+    const int4 *rec_id = nullptr;
+    const void *rec_a = nullptr, *rec_b = nullptr, *rec_c = nullptr;
+    const int64_t *chunk_off = nullptr;  // [n_chunks + 1]
+    const int2 *chunk_v = nullptr;       // [n_chunks] {first internal vertex, vertices in chunk}
+    const int32_t *deg = nullptr;        // [n_free]
+    const void *fext = nullptr;          // Real4 [n_free] or null (no body force)
+    // weak constraints: per free vertex CSR of (constraint id, w0_i - w1_i) in input order
+    const int32_t *wc_off = nullptr;     // [n_free + 1]
+    const int32_t *wc_cid = nullptr;
+    const void *wc_d = nullptr;          // Real
+    const int32_t *c_n = nullptr;        // [n_cons] distinct nodes
+    const int32_t *c_node = nullptr;     // [n_cons * 8] internal ids
+    const void *c_w = nullptr;           // Real [n_cons * 8] combined signed weights w0_j - w1_j
+    const void *c_anchor = nullptr;      // Real4 [n_cons] (anchor if side 1 is a fixed point, else 0)
+    const void *c_K = nullptr;           // Real [n_cons * 8] xx yy zz xy yz xz (padded)
+    // tets for the energy pass: tet_id int4 internal ids; tet_a/b/c Real4 {B00 B01 B02 B10}
+    // {B11 B12 B20 B21} {B22 VE V 0}
+    const int4 *tet_id = nullptr;
+    const void *tet_a = nullptr, *tet_b = nullptr, *tet_c = nullptr;
+    const int32_t *int2orig = nullptr;   // [n_vertices]
+    const void *targets = nullptr;       // Real4 [n_batch][n_pinned]
+    void *xbuf[3] = {nullptr, nullptr, nullptr};  // Real4 [n_batch][x_stride] each
+    void *stage = nullptr;               // Real [n_batch][n_vertices][3]
+    double *part_e = nullptr;            // [n_batch][ge]
+    double *part_r = nullptr;            // [n_batch][gr]
+    double *results = nullptr;           // [n_batch][2]
+    int32_t *flag = nullptr;             // non-finite flag
+};
+
+struct Problem {
+    int dtype = DT_F32, model = MODEL_NH;
+    int64_t n_vertices = 0, n_free = 0, n_pinned = 0, n_tets = 0, n_cons = 0, n_chunks = 0;
+    int32_t n_batch = 1;
+    int64_t x_stride = 0;  // Real4 elements between samples
+    double cmu = 0, clam = 0;  // mu_e = cmu * E_e, lambda_e = clam * E_e  (eq:lame)
+    double rho_g[3] = {0, 0, 0};  // density * gravity (energy's external-work term)
+    bool has_fext = false, has_wc = false;
+    int ge = 1, gr = 1;  // energy / residual partial blocks per sample
+};
+
+struct SweepLaunch {
+    int32_t v_begin = 0, n_v = 0;  // colour's internal vertex range
+    int64_t chunk_begin = 0;
+    int work = 0, out = 1, hist = 2;  // xbuf indices
+    int accel = ACCEL_NONE;
+    double omega = 1, gamma = 1;  // SOR omega, or Chebyshev omega_{l+1} and gamma
+};
+
+// launchers (pbng_kernels.cu); return cudaGetLastError()
+cudaError_t launch_sweep(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st);
+cudaError_t launch_set_positions(const Problem &p, const Layout &L, int n_buffers, cudaStream_t st);
+cudaError_t launch_get_positions(const Problem &p, const Layout &L, int work, cudaStream_t st);
+cudaError_t launch_energy_residual(const Problem &p, const Layout &L, int work, cudaStream_t st);
+int kernels_per_energy_residual();
+
+}  // namespace pbng

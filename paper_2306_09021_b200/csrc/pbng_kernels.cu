@@ -1,0 +1,631 @@
+// pbng_kernels.cu -- sm_100a kernels of the PBNG hot path (arXiv 2306.09021).
+//
+//  sweep_kernel        one colour of one PBNG iteration: every free vertex of
+//                      the colour accumulates f_i + f^ext_i and the SPD modified Hessian A (eq:mod_hess)
+//                      over its incident tets and weak constraints, solves the 3x3 system in registers
+//                      and takes one Newton step; the SOR / Chebyshev blend is fused
+//                      into the same store.  One thread per vertex, one warp per 32-vertex SELL chunk:
+//                      record k of the 32 lanes is one contiguous 512 B (f32) line per field.
+//  energy_kernel       per-tet energy sum V_e Psi(F_e) - x.f^ext and weak-constraint energy, fp64 math,
+//                      fixed-order block partials (deterministic).
+//  residual_kernel     ||f_i + f^ext_i|| over free vertices from the same pair records, fp64 math.
+//  reduce_kernel       per-sample final reduction of the partials.
+//  set/get_positions   original <-> internal (colour-major) vertex order.
+// No tensor cores: the path is a gather + 3x3 register math, not a dense contraction.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "pbng_internal.h"
+
+namespace pbng {
+namespace {
+
+template <class R> struct RT;
+template <> struct RT<float> { using R4 = float4; using RC = float; };
+template <> struct RT<double> { using R4 = double4; using RC = double2; };
+
+__device__ __forceinline__ float ld(const float *p) { return __ldg(p); }
+__device__ __forceinline__ double ld(const double *p) { return __ldg(p); }
+__device__ __forceinline__ int ld(const int *p) { return __ldg(p); }
+__device__ __forceinline__ int64_t ld(const int64_t *p) {
+    return (int64_t)__ldg(reinterpret_cast<const long long *>(p));
+}
+__device__ __forceinline__ int4 ld(const int4 *p) { return __ldg(p); }
+__device__ __forceinline__ float4 ld(const float4 *p) { return __ldg(p); }
+__device__ __forceinline__ double2 ld(const double2 *p) { return __ldg(p); }
+__device__ __forceinline__ double4 ld(const double4 *p) {
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+    const double2 a = __ldg(q), b = __ldg(q + 1);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+
+__device__ __forceinline__ float rsq(float x) { return rsqrtf(x); }
+__device__ __forceinline__ double rsq(double x) { return rsqrt(x); }
+__device__ __forceinline__ float sq(float x) { return sqrtf(x); }
+__device__ __forceinline__ double sq(double x) { return sqrt(x); }
+
+template <class R> __device__ __forceinline__ typename RT<R>::R4 mk4(R x, R y, R z);
+template <> __device__ __forceinline__ float4 mk4<float>(float x, float y, float z) { return make_float4(x, y, z, 0.f); }
+template <> __device__ __forceinline__ double4 mk4<double>(double x, double y, double z) { return make_double4(x, y, z, 0.0); }
+
+// ------------------------------------------------------------------------------------------------
+// Polar rotation R(F) (eq:cor): closest rotation, det R = +1 also for inverted F.
+// Cyclic Jacobi on S = F^T F (fixed sweep count) -> V; B = F V with columns sorted by decreasing norm
+// (each swap negates one column so det V stays +1); Givens QR of B -> Q (a rotation, the sign of
+// det F lands in the last diagonal entry); R = Q V^T.
+// ------------------------------------------------------------------------------------------------
+template <class R> struct PolarSweeps { static constexpr int n = 4; };
+template <> struct PolarSweeps<double> { static constexpr int n = 7; };
+
+template <int p, int q, class R>
+__device__ __forceinline__ void jacobi_rot(R (&S)[3][3], R (&V)[3][3]) {
+    constexpr int r = 3 - p - q;
+    const R apq = S[p][q];
+    const R d = S[q][q] - S[p][p];
+    const R den = fabs(d) + sq(d * d + R(4) * apq * apq);
+    R t = den > R(0) ? R(2) * apq / den : R(0);
+    t = d < R(0) ? -t : t;
+    const R c = rsq(R(1) + t * t);
+    const R s = t * c;
+    S[p][p] -= t * apq;
+    S[q][q] += t * apq;
+    S[p][q] = S[q][p] = R(0);
+    const R srp = S[r][p], srq = S[r][q];
+    S[r][p] = S[p][r] = c * srp - s * srq;
+    S[r][q] = S[q][r] = s * srp + c * srq;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const R vkp = V[k][p], vkq = V[k][q];
+        V[k][p] = c * vkp - s * vkq;
+        V[k][q] = s * vkp + c * vkq;
+    }
+}
+
+template <int i, int j, class R>
+__device__ __forceinline__ void sort_swap(R (&B)[3][3], R (&V)[3][3], R (&n)[3]) {
+    const bool sw = n[i] < n[j];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const R bi = B[k][i], bj = B[k][j], vi = V[k][i], vj = V[k][j];
+        B[k][i] = sw ? bj : bi;
+        B[k][j] = sw ? -bi : bj;
+        V[k][i] = sw ? vj : vi;
+        V[k][j] = sw ? -vi : vj;
+    }
+    const R ni = n[i], nj = n[j];
+    n[i] = sw ? nj : ni;
+    n[j] = sw ? ni : nj;
+}
+
+template <class R>
+__device__ __forceinline__ void givens(R a, R b, R &c, R &s) {
+    const R n2 = a * a + b * b;
+    const bool ok = n2 > R(0);
+    const R inv = ok ? rsq(n2) : R(0);
+    c = ok ? a * inv : R(1);
+    s = b * inv;
+}
+
+template <int r0, int r1, int c0, class R>
+__device__ __forceinline__ void rot_rows(R (&M)[3][3], R c, R s) {
+#pragma unroll
+    for (int k = c0; k < 3; ++k) {
+        const R a = M[r0][k], b = M[r1][k];
+        M[r0][k] = c * a + s * b;
+        M[r1][k] = -s * a + c * b;
+    }
+}
+
+template <class R>
+__device__ __forceinline__ void polar_rotation(const R (&F)[3][3], R (&Rm)[3][3]) {
+    R S[3][3], V[3][3], B[3][3], Qt[3][3], n[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = a; b < 3; ++b) {
+            S[a][b] = F[0][a] * F[0][b] + F[1][a] * F[1][b] + F[2][a] * F[2][b];
+            S[b][a] = S[a][b];
+        }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) V[a][b] = Qt[a][b] = (a == b) ? R(1) : R(0);
+#pragma unroll
+    for (int it = 0; it < PolarSweeps<R>::n; ++it) {
+        jacobi_rot<0, 1>(S, V);
+        jacobi_rot<0, 2>(S, V);
+        jacobi_rot<1, 2>(S, V);
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) B[i][k] = F[i][0] * V[0][k] + F[i][1] * V[1][k] + F[i][2] * V[2][k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) n[k] = B[0][k] * B[0][k] + B[1][k] * B[1][k] + B[2][k] * B[2][k];
+    sort_swap<0, 1>(B, V, n);
+    sort_swap<0, 2>(B, V, n);
+    sort_swap<1, 2>(B, V, n);
+    R c, s;
+    givens(B[0][0], B[1][0], c, s);
+    rot_rows<0, 1, 0>(B, c, s);
+    rot_rows<0, 1, 0>(Qt, c, s);
+    givens(B[0][0], B[2][0], c, s);
+    rot_rows<0, 2, 0>(B, c, s);
+    rot_rows<0, 2, 0>(Qt, c, s);
+    givens(B[1][1], B[2][1], c, s);
+    rot_rows<1, 2, 0>(Qt, c, s);
+    // R = Q V^T, Q = Qt^T
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) Rm[i][j] = Qt[0][i] * V[j][0] + Qt[1][i] * V[j][1] + Qt[2][i] * V[j][2];
+}
+
+// ------------------------------------------------------------------------------------------------
+// Per (vertex, tet) contribution: F = sum_j (x_j - x_i) g_j^T, C = cof F,
+//   f -= V P(F) g_i,   A += V (2 mu |g_i|^2 I + lambda (C g_i)(C g_i)^T).
+// NH: V P g = Vmu F g + (Vlamhat (J - 1) - Vmu) C g (eq:nh, lamhat = mu + lambda).
+// FCR: V P g = 2 Vmu (F g - R g) + Vlam (J - 1) C g (eq:cor).
+// A is kept as {00, 11, 22, 01, 12, 02}.
+// ------------------------------------------------------------------------------------------------
+template <int MODEL, bool HESS, class T>
+__device__ __forceinline__ void pair_contrib(const T (&d1)[3], const T (&d2)[3], const T (&d3)[3],
+                                             const T (&g1)[3], const T (&g2)[3], const T (&g3)[3], T Vmu, T Vlam,
+                                             T (&f)[3], T (&A)[6]) {
+    T F[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) F[r][c] = d1[r] * g1[c] + d2[r] * g2[c] + d3[r] * g3[c];
+    const T g[3] = {-(g1[0] + g2[0] + g3[0]), -(g1[1] + g2[1] + g3[1]), -(g1[2] + g2[2] + g3[2])};
+    T C[3][3];
+    C[0][0] = F[1][1] * F[2][2] - F[1][2] * F[2][1];
+    C[0][1] = F[1][2] * F[2][0] - F[1][0] * F[2][2];
+    C[0][2] = F[1][0] * F[2][1] - F[1][1] * F[2][0];
+    C[1][0] = F[0][2] * F[2][1] - F[0][1] * F[2][2];
+    C[1][1] = F[0][0] * F[2][2] - F[0][2] * F[2][0];
+    C[1][2] = F[0][1] * F[2][0] - F[0][0] * F[2][1];
+    C[2][0] = F[0][1] * F[1][2] - F[0][2] * F[1][1];
+    C[2][1] = F[0][2] * F[1][0] - F[0][0] * F[1][2];
+    C[2][2] = F[0][0] * F[1][1] - F[0][1] * F[1][0];
+    const T J = F[0][0] * C[0][0] + F[0][1] * C[0][1] + F[0][2] * C[0][2];
+    T Fg[3], w[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        Fg[r] = F[r][0] * g[0] + F[r][1] * g[1] + F[r][2] * g[2];
+        w[r] = C[r][0] * g[0] + C[r][1] * g[1] + C[r][2] * g[2];
+    }
+    if (MODEL == MODEL_NH) {
+        const T s = (Vmu + Vlam) * (J - T(1)) - Vmu;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) f[r] -= Vmu * Fg[r] + s * w[r];
+    } else {
+        T Rm[3][3];
+        polar_rotation(F, Rm);
+        const T s = Vlam * (J - T(1));
+        const T m2 = T(2) * Vmu;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const T Rg = Rm[r][0] * g[0] + Rm[r][1] * g[1] + Rm[r][2] * g[2];
+            f[r] -= m2 * (Fg[r] - Rg) + s * w[r];
+        }
+    }
+    if (HESS) {
+        const T dg = T(2) * Vmu * (g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+        A[0] += dg + Vlam * w[0] * w[0];
+        A[1] += dg + Vlam * w[1] * w[1];
+        A[2] += dg + Vlam * w[2] * w[2];
+        A[3] += Vlam * w[0] * w[1];
+        A[4] += Vlam * w[1] * w[2];
+        A[5] += Vlam * w[0] * w[2];
+    }
+}
+
+// record field decode
+template <class R> struct Rec;
+template <> struct Rec<float> {
+    static __device__ __forceinline__ void load(const Layout &L, int64_t r, int4 &id, float (&g1)[3], float (&g2)[3],
+                                                float (&g3)[3], float &VE) {
+        id = ld(L.rec_id + r);
+        const float4 a = ld(reinterpret_cast<const float4 *>(L.rec_a) + r);
+        const float4 b = ld(reinterpret_cast<const float4 *>(L.rec_b) + r);
+        const float c = ld(reinterpret_cast<const float *>(L.rec_c) + r);
+        g1[0] = a.x; g1[1] = a.y; g1[2] = a.z;
+        g2[0] = a.w; g2[1] = b.x; g2[2] = b.y;
+        g3[0] = b.z; g3[1] = b.w; g3[2] = c;
+        VE = __int_as_float(id.w);
+    }
+};
+template <> struct Rec<double> {
+    static __device__ __forceinline__ void load(const Layout &L, int64_t r, int4 &id, double (&g1)[3], double (&g2)[3],
+                                                double (&g3)[3], double &VE) {
+        id = ld(L.rec_id + r);
+        const double4 a = ld(reinterpret_cast<const double4 *>(L.rec_a) + r);
+        const double4 b = ld(reinterpret_cast<const double4 *>(L.rec_b) + r);
+        const double2 c = ld(reinterpret_cast<const double2 *>(L.rec_c) + r);
+        g1[0] = a.x; g1[1] = a.y; g1[2] = a.z;
+        g2[0] = a.w; g2[1] = b.x; g2[2] = b.y;
+        g3[0] = b.z; g3[1] = b.w; g3[2] = c.x;
+        VE = c.y;
+    }
+};
+
+// weak-constraint terms for vertex v: f -= d K C_c, A += d^2 K
+template <class R, class T, bool HESS>
+__device__ __forceinline__ void wc_contrib(const Layout &L, const typename RT<R>::R4 *x, int v, const T (&xa)[3],
+                                           T (&f)[3], T (&A)[6]) {
+    using R4 = typename RT<R>::R4;
+    const int e0 = ld(L.wc_off + v), e1 = ld(L.wc_off + v + 1);
+    for (int e = e0; e < e1; ++e) {
+        const int cid = ld(L.wc_cid + e);
+        const T d = T(ld(reinterpret_cast<const R *>(L.wc_d) + e));
+        const R4 an = ld(reinterpret_cast<const R4 *>(L.c_anchor) + cid);
+        T C[3] = {-T(an.x), -T(an.y), -T(an.z)};
+        const int nn = ld(L.c_n + cid);
+        for (int q = 0; q < nn; ++q) {
+            const int node = ld(L.c_node + kWcMaxNodes * cid + q);
+            const T w = T(ld(reinterpret_cast<const R *>(L.c_w) + kWcMaxNodes * cid + q));
+            if (node == v) {
+                C[0] += w * xa[0]; C[1] += w * xa[1]; C[2] += w * xa[2];
+            } else {
+                const R4 y = ld(x + node);
+                C[0] += w * T(y.x); C[1] += w * T(y.y); C[2] += w * T(y.z);
+            }
+        }
+        const R *Kp = reinterpret_cast<const R *>(L.c_K) + kWcMaxNodes * cid;
+        const T kxx = T(ld(Kp + 0)), kyy = T(ld(Kp + 1)), kzz = T(ld(Kp + 2));
+        const T kxy = T(ld(Kp + 3)), kyz = T(ld(Kp + 4)), kxz = T(ld(Kp + 5));
+        f[0] -= d * (kxx * C[0] + kxy * C[1] + kxz * C[2]);
+        f[1] -= d * (kxy * C[0] + kyy * C[1] + kyz * C[2]);
+        f[2] -= d * (kxz * C[0] + kyz * C[1] + kzz * C[2]);
+        if (HESS) {
+            const T d2 = d * d;
+            A[0] += d2 * kxx; A[1] += d2 * kyy; A[2] += d2 * kzz;
+            A[3] += d2 * kxy; A[4] += d2 * kyz; A[5] += d2 * kxz;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// colour sweep
+// ------------------------------------------------------------------------------------------------
+template <class R, int MODEL, int ACCEL, bool FEXT, bool WC>
+__global__ void __launch_bounds__(kSweepBlock) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
+                                                            const int64_t chunk_begin, const int64_t x_stride,
+                                                            const int wi, const int oi, const int hi, const R cmu,
+                                                            const R clam, const R omega, const R gamma) {
+    using R4 = typename RT<R>::R4;
+    const int t = blockIdx.x * kSweepBlock + threadIdx.x;
+    if (t >= n_v) return;
+    const int v = v_begin + t;
+    const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
+    const int deg = ld(L.deg + v);
+    const int64_t xs = (int64_t)blockIdx.y * x_stride;
+    R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
+
+    const R4 xa4 = work[v];
+    const R xa[3] = {xa4.x, xa4.y, xa4.z};
+    R f[3] = {R(0), R(0), R(0)};
+    if (FEXT) {
+        const R4 fe = ld(reinterpret_cast<const R4 *>(L.fext) + v);
+        f[0] = fe.x; f[1] = fe.y; f[2] = fe.z;
+    }
+    R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
+
+    for (int k = 0; k < deg; ++k) {
+        int4 id;
+        R g1[3], g2[3], g3[3], VE;
+        Rec<R>::load(L, base + (int64_t)k * kChunk, id, g1, g2, g3, VE);
+        const R4 p1 = ld(work + id.x), p2 = ld(work + id.y), p3 = ld(work + id.z);
+        const R d1[3] = {p1.x - xa[0], p1.y - xa[1], p1.z - xa[2]};
+        const R d2[3] = {p2.x - xa[0], p2.y - xa[1], p2.z - xa[2]};
+        const R d3[3] = {p3.x - xa[0], p3.y - xa[1], p3.z - xa[2]};
+        pair_contrib<MODEL, true>(d1, d2, d3, g1, g2, g3, VE * cmu, VE * clam, f, A);
+    }
+    if (WC) wc_contrib<R, R, true>(L, work, v, xa, f, A);
+
+    // A dx = f by Cholesky in registers (A is SPD)
+    const R i00 = rsq(A[0]);
+    const R l10 = A[3] * i00, l20 = A[5] * i00;
+    const R i11 = rsq(A[1] - l10 * l10);
+    const R l21 = (A[4] - l20 * l10) * i11;
+    const R i22 = rsq(A[2] - l20 * l20 - l21 * l21);
+    const R z0 = f[0] * i00;
+    const R z1 = (f[1] - l10 * z0) * i11;
+    const R z2 = (f[2] - l20 * z0 - l21 * z1) * i22;
+    const R x2 = z2 * i22;
+    const R x1 = (z1 - l21 * x2) * i11;
+    const R x0 = (z0 - l10 * x1 - l20 * x2) * i00;
+    const R p[3] = {xa[0] + x0, xa[1] + x1, xa[2] + x2};
+    if (!(isfinite(p[0]) && isfinite(p[1]) && isfinite(p[2]))) atomicOr(L.flag, 1);
+
+    work[v] = mk4<R>(p[0], p[1], p[2]);
+    if (ACCEL != ACCEL_NONE) {
+        R4 *__restrict__ out = reinterpret_cast<R4 *>(L.xbuf[oi]) + xs;
+        R4 *__restrict__ hist = reinterpret_cast<R4 *>(L.xbuf[hi]) + xs;
+        const R4 h4 = hist[v];
+        const R h[3] = {h4.x, h4.y, h4.z};
+        R o[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (ACCEL == ACCEL_SOR)  // x^{l+1} = omega (x_PBNG - x^{l-1}) + x^{l-1}
+                o[c] = omega * (p[c] - h[c]) + h[c];
+            else  // x^{l+1} = omega_{l+1} (gamma (x_PBNG - x^l) + x^l - x^{l-1}) + x^{l-1}
+                o[c] = omega * (gamma * (p[c] - xa[c]) + xa[c] - h[c]) + h[c];
+        }
+        out[v] = mk4<R>(o[0], o[1], o[2]);
+        hist[v] = xa4;
+    }
+}
+
+template <class R, int MODEL, int ACCEL>
+cudaError_t sweep_dispatch3(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
+    dim3 grid((unsigned)((s.n_v + kSweepBlock - 1) / kSweepBlock), (unsigned)p.n_batch);
+    const R cmu = R(p.cmu), clam = R(p.clam), om = R(s.omega), ga = R(s.gamma);
+#define PBNG_SWEEP(FE, W)                                                                                     \
+    sweep_kernel<R, MODEL, ACCEL, FE, W><<<grid, kSweepBlock, 0, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,   \
+                                                                        p.x_stride, s.work, s.out, s.hist, cmu, \
+                                                                        clam, om, ga)
+    if (p.has_fext) {
+        if (p.has_wc) PBNG_SWEEP(true, true); else PBNG_SWEEP(true, false);
+    } else {
+        if (p.has_wc) PBNG_SWEEP(false, true); else PBNG_SWEEP(false, false);
+    }
+#undef PBNG_SWEEP
+    return cudaGetLastError();
+}
+
+template <class R, int MODEL>
+cudaError_t sweep_dispatch2(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
+    switch (s.accel) {
+        case ACCEL_SOR: return sweep_dispatch3<R, MODEL, ACCEL_SOR>(p, L, s, st);
+        case ACCEL_CHEB: return sweep_dispatch3<R, MODEL, ACCEL_CHEB>(p, L, s, st);
+        default: return sweep_dispatch3<R, MODEL, ACCEL_NONE>(p, L, s, st);
+    }
+}
+
+template <class R>
+cudaError_t sweep_dispatch1(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
+    return p.model == MODEL_FCR ? sweep_dispatch2<R, MODEL_FCR>(p, L, s, st) : sweep_dispatch2<R, MODEL_NH>(p, L, s, st);
+}
+
+// ------------------------------------------------------------------------------------------------
+// positions: original <-> internal order
+// ------------------------------------------------------------------------------------------------
+template <class R>
+__global__ void set_positions_kernel(const Layout L, const int64_t nv, const int64_t n_free, const int64_t n_pin,
+                                     const int64_t x_stride, const int nbuf) {
+    using R4 = typename RT<R>::R4;
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    const int64_t b = blockIdx.y;
+    R4 val;
+    if (v < n_free) {
+        const R *s = reinterpret_cast<const R *>(L.stage) + (b * nv + L.int2orig[v]) * 3;
+        val = mk4<R>(s[0], s[1], s[2]);
+    } else {
+        val = reinterpret_cast<const R4 *>(L.targets)[b * n_pin + (v - n_free)];
+    }
+    for (int k = 0; k < nbuf; ++k) reinterpret_cast<R4 *>(L.xbuf[k])[b * x_stride + v] = val;
+}
+
+template <class R>
+__global__ void get_positions_kernel(const Layout L, const int64_t nv, const int64_t x_stride, const int wi) {
+    using R4 = typename RT<R>::R4;
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    const int64_t b = blockIdx.y;
+    const R4 x = reinterpret_cast<const R4 *>(L.xbuf[wi])[b * x_stride + v];
+    R *d = reinterpret_cast<R *>(L.stage) + (b * nv + L.int2orig[v]) * 3;
+    d[0] = x.x;
+    d[1] = x.y;
+    d[2] = x.z;
+}
+
+// ------------------------------------------------------------------------------------------------
+// energy and residual (fp64 arithmetic for both dtypes; fixed-order reductions)
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+    }
+    return r;  // valid in thread 0
+}
+
+template <class R, int MODEL>
+__global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const int64_t nt, const int64_t n_cons,
+                                                           const int64_t x_stride, const int wi, const double cmu,
+                                                           const double clam, const double rgx, const double rgy,
+                                                           const double rgz, const int ge) {
+    using R4 = typename RT<R>::R4;
+    __shared__ double sh[32];
+    const int64_t b = blockIdx.y;
+    const R4 *x = reinterpret_cast<const R4 *>(L.xbuf[wi]) + b * x_stride;
+    const double r_mu = cmu / (cmu + clam);  // mu / lambdahat, independent of E
+    double acc = 0.0;
+    for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < nt + n_cons;
+         item += (int64_t)gridDim.x * blockDim.x) {
+        if (item < nt) {
+            const int4 id = ld(L.tet_id + item);
+            const R4 ta = ld(reinterpret_cast<const R4 *>(L.tet_a) + item);
+            const R4 tb = ld(reinterpret_cast<const R4 *>(L.tet_b) + item);
+            const R4 tc = ld(reinterpret_cast<const R4 *>(L.tet_c) + item);
+            const R4 q0 = ld(x + id.x), q1 = ld(x + id.y), q2 = ld(x + id.z), q3 = ld(x + id.w);
+            const double Bm[3][3] = {{ta.x, ta.y, ta.z}, {ta.w, tb.x, tb.y}, {tb.z, tb.w, tc.x}};
+            const double VE = tc.y, V = tc.z;
+            const double d[3][3] = {{double(q1.x) - q0.x, double(q1.y) - q0.y, double(q1.z) - q0.z},
+                                    {double(q2.x) - q0.x, double(q2.y) - q0.y, double(q2.z) - q0.z},
+                                    {double(q3.x) - q0.x, double(q3.y) - q0.y, double(q3.z) - q0.z}};
+            double F[3][3];
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) F[r][c] = d[0][r] * Bm[0][c] + d[1][r] * Bm[1][c] + d[2][r] * Bm[2][c];
+            const double J = F[0][0] * (F[1][1] * F[2][2] - F[1][2] * F[2][1]) -
+                             F[0][1] * (F[1][0] * F[2][2] - F[1][2] * F[2][0]) +
+                             F[0][2] * (F[1][0] * F[2][1] - F[1][1] * F[2][0]);
+            const double Vmu = VE * cmu, Vlam = VE * clam;
+            double e;
+            if (MODEL == MODEL_NH) {
+                double fro = 0.0;
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) fro += F[r][c] * F[r][c];
+                const double t = J - 1.0 - r_mu;
+                e = 0.5 * Vmu * (fro - 3.0) + 0.5 * (Vmu + Vlam) * t * t - 0.5 * Vmu * r_mu;
+            } else {
+                double Rm[3][3];
+                polar_rotation(F, Rm);
+                double s = 0.0;
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) s += (F[r][c] - Rm[r][c]) * (F[r][c] - Rm[r][c]);
+                e = Vmu * s + 0.5 * Vlam * (J - 1.0) * (J - 1.0);
+            }
+            // - x . f^ext with f^ext_i = sum_e rho g V_e / 4, distributed per tet
+            const double sx = double(q0.x) + q1.x + q2.x + q3.x, sy = double(q0.y) + q1.y + q2.y + q3.y,
+                         sz = double(q0.z) + q1.z + q2.z + q3.z;
+            e -= 0.25 * V * (rgx * sx + rgy * sy + rgz * sz);
+            acc += e;
+        } else {
+            const int64_t c = item - nt;
+            const R4 an = ld(reinterpret_cast<const R4 *>(L.c_anchor) + c);
+            double C[3] = {-double(an.x), -double(an.y), -double(an.z)};
+            const int nn = ld(L.c_n + c);
+            for (int q = 0; q < nn; ++q) {
+                const R4 y = ld(x + ld(L.c_node + kWcMaxNodes * c + q));
+                const double w = ld(reinterpret_cast<const R *>(L.c_w) + kWcMaxNodes * c + q);
+                C[0] += w * y.x; C[1] += w * y.y; C[2] += w * y.z;
+            }
+            const R *Kp = reinterpret_cast<const R *>(L.c_K) + kWcMaxNodes * c;
+            const double kxx = ld(Kp + 0), kyy = ld(Kp + 1), kzz = ld(Kp + 2), kxy = ld(Kp + 3), kyz = ld(Kp + 4),
+                         kxz = ld(Kp + 5);
+            acc += 0.5 * (C[0] * (kxx * C[0] + kxy * C[1] + kxz * C[2]) + C[1] * (kxy * C[0] + kyy * C[1] + kyz * C[2]) +
+                          C[2] * (kxz * C[0] + kyz * C[1] + kzz * C[2]));
+        }
+    }
+    const double s = block_sum(acc, sh);
+    if (threadIdx.x == 0) L.part_e[b * ge + blockIdx.x] = s;
+}
+
+template <class R, int MODEL, bool FEXT, bool WC>
+__global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, const int64_t n_chunks,
+                                                             const int64_t x_stride, const int wi, const double cmu,
+                                                             const double clam, const int gr) {
+    using R4 = typename RT<R>::R4;
+    __shared__ double sh[32];
+    const int64_t b = blockIdx.y;
+    const R4 *x = reinterpret_cast<const R4 *>(L.xbuf[wi]) + b * x_stride;
+    double acc = 0.0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_chunks * kChunk;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t chunk = t >> 5;
+        const int lane = (int)(t & 31);
+        const int2 cv = L.chunk_v[chunk];
+        if (lane >= cv.y) continue;
+        const int v = cv.x + lane;
+        const int64_t base = L.chunk_off[chunk] + lane;
+        const int deg = L.deg[v];
+        const R4 xa4 = x[v];
+        const double xa[3] = {xa4.x, xa4.y, xa4.z};
+        double f[3] = {0.0, 0.0, 0.0}, A[6];
+        if (FEXT) {
+            const R4 fe = reinterpret_cast<const R4 *>(L.fext)[v];
+            f[0] = fe.x; f[1] = fe.y; f[2] = fe.z;
+        }
+        for (int k = 0; k < deg; ++k) {
+            int4 id;
+            R g1r[3], g2r[3], g3r[3], VE;
+            Rec<R>::load(L, base + (int64_t)k * kChunk, id, g1r, g2r, g3r, VE);
+            const R4 p1 = ld(x + id.x), p2 = ld(x + id.y), p3 = ld(x + id.z);
+            const double d1[3] = {p1.x - xa[0], p1.y - xa[1], p1.z - xa[2]};
+            const double d2[3] = {p2.x - xa[0], p2.y - xa[1], p2.z - xa[2]};
+            const double d3[3] = {p3.x - xa[0], p3.y - xa[1], p3.z - xa[2]};
+            const double g1[3] = {g1r[0], g1r[1], g1r[2]}, g2[3] = {g2r[0], g2r[1], g2r[2]},
+                         g3[3] = {g3r[0], g3r[1], g3r[2]};
+            pair_contrib<MODEL, false>(d1, d2, d3, g1, g2, g3, double(VE) * cmu, double(VE) * clam, f, A);
+        }
+        if (WC) wc_contrib<R, double, false>(L, x, v, xa, f, A);
+        acc += f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+    }
+    const double s = block_sum(acc, sh);
+    if (threadIdx.x == 0) L.part_r[b * gr + blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kRedBlock) reduce_kernel(const Layout L, const int ge, const int gr) {
+    __shared__ double sh[32];
+    const int64_t b = blockIdx.x;
+    double e = 0.0, r = 0.0;
+    for (int k = threadIdx.x; k < ge; k += blockDim.x) e += L.part_e[b * ge + k];
+    for (int k = threadIdx.x; k < gr; k += blockDim.x) r += L.part_r[b * gr + k];
+    e = block_sum(e, sh);
+    __syncthreads();
+    r = block_sum(r, sh);
+    if (threadIdx.x == 0) {
+        L.results[2 * b] = e;
+        L.results[2 * b + 1] = sqrt(r);
+    }
+}
+
+template <class R, int MODEL>
+cudaError_t energy_dispatch(const Problem &p, const Layout &L, int wi, cudaStream_t st) {
+    energy_kernel<R, MODEL><<<dim3(p.ge, p.n_batch), kRedBlock, 0, st>>>(
+        L, p.n_tets, p.n_cons, p.x_stride, wi, p.cmu, p.clam, p.rho_g[0], p.rho_g[1], p.rho_g[2], p.ge);
+    dim3 gr(p.gr, p.n_batch);
+    if (p.has_fext) {
+        if (p.has_wc) residual_kernel<R, MODEL, true, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr);
+        else residual_kernel<R, MODEL, true, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr);
+    } else {
+        if (p.has_wc) residual_kernel<R, MODEL, false, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr);
+        else residual_kernel<R, MODEL, false, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr);
+    }
+    reduce_kernel<<<p.n_batch, kRedBlock, 0, st>>>(L, p.ge, p.gr);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_sweep(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
+    if (s.n_v <= 0) return cudaSuccess;
+    return p.dtype == DT_F64 ? sweep_dispatch1<double>(p, L, s, st) : sweep_dispatch1<float>(p, L, s, st);
+}
+
+cudaError_t launch_set_positions(const Problem &p, const Layout &L, int n_buffers, cudaStream_t st) {
+    dim3 grid((unsigned)((p.n_vertices + 255) / 256), (unsigned)p.n_batch);
+    if (p.dtype == DT_F64)
+        set_positions_kernel<double><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_free, p.n_pinned, p.x_stride, n_buffers);
+    else
+        set_positions_kernel<float><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_free, p.n_pinned, p.x_stride, n_buffers);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_get_positions(const Problem &p, const Layout &L, int work, cudaStream_t st) {
+    dim3 grid((unsigned)((p.n_vertices + 255) / 256), (unsigned)p.n_batch);
+    if (p.dtype == DT_F64)
+        get_positions_kernel<double><<<grid, 256, 0, st>>>(L, p.n_vertices, p.x_stride, work);
+    else
+        get_positions_kernel<float><<<grid, 256, 0, st>>>(L, p.n_vertices, p.x_stride, work);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_energy_residual(const Problem &p, const Layout &L, int work, cudaStream_t st) {
+    if (p.dtype == DT_F64)
+        return p.model == MODEL_FCR ? energy_dispatch<double, MODEL_FCR>(p, L, work, st)
+                                    : energy_dispatch<double, MODEL_NH>(p, L, work, st);
+    return p.model == MODEL_FCR ? energy_dispatch<float, MODEL_FCR>(p, L, work, st)
+                                : energy_dispatch<float, MODEL_NH>(p, L, work, st);
+}
+
+int kernels_per_energy_residual() { return 3; }
+
+}  // namespace pbng

@@ -1,0 +1,261 @@
+"""Thin ctypes binding of libpbng (include/pbng.h) -- argument marshalling only.
+
+Every step of the PBNG path runs in the library's CUDA kernels; PyTorch supplies device memory (the
+workspace tensor), the CUDA stream and the process group.  There is no CPU fallback: if libpbng.so is
+missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpbng.so")
+
+OK = 0
+STATUS = {0: "PBNG_OK", 1: "PBNG_E_INVALID_ARGUMENT", 2: "PBNG_E_INDEX_OUT_OF_RANGE", 3: "PBNG_E_DEGENERATE_ELEMENT",
+          4: "PBNG_E_ISOLATED_VERTEX", 5: "PBNG_E_BAD_ORDER", 6: "PBNG_E_NOT_COLORED", 7: "PBNG_E_NONFINITE",
+          8: "PBNG_E_CUDA", 9: "PBNG_E_NCCL", 10: "PBNG_E_OUT_OF_MEMORY", 11: "PBNG_E_NO_DEVICE"}
+DTYPE = {"f32": 0, "f64": 1}
+MODEL = {"nh": 0, "fcr": 1}
+ACCEL = {"none": 0, "sor": 1, "chebyshev": 2}
+EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbng_color", "pbng_workspace_bytes",
+           "pbng_bind_workspace", "pbng_set_positions", "pbng_get_positions", "pbng_iterate", "pbng_energy_residual",
+           "pbng_synchronize", "pbng_query", "pbng_profile_enable", "pbng_profile_read", "pbng_destroy",
+           "pbng_last_error", "pbng_version")
+
+WC_DTYPE = np.dtype([("n0", "<i4"), ("n1", "<i4"), ("idx0", "<i4", 4), ("idx1", "<i4", 4), ("w0", "<f8", 4),
+                     ("w1", "<f8", 4), ("anchor", "<f8", 3), ("K", "<f8", 6)])
+assert WC_DTYPE.itemsize == 176
+
+
+class PBNGError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Info(C.Structure):
+    _fields_ = [("n_vertices", C.c_int64), ("n_tets", C.c_int64), ("n_free", C.c_int64), ("n_pinned", C.c_int64),
+                ("n_weak_constraints", C.c_int64), ("n_pairs", C.c_int64), ("n_pair_slots", C.c_int64),
+                ("n_batch", C.c_int32), ("n_colours", C.c_int32), ("dtype", C.c_int32), ("model", C.c_int32),
+                ("iteration", C.c_int64), ("kernel_launches", C.c_int64), ("sweep_bytes", C.c_double),
+                ("accel_bytes", C.c_double), ("sweep_flops", C.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libpbng.so (building it in-tree first if it is missing and nvcc is available)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        from . import build as _build
+        _build.build()
+    L = C.CDLL(LIB_PATH)
+    vp, i64, i32, d = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+    L.pbng_create_mesh.argtypes = [vp, i64, vp, i64, i32, C.c_int, C.c_int, C.c_size_t, C.POINTER(vp),
+                                   C.POINTER(i64)]
+    L.pbng_set_material.argtypes = [vp, C.c_int, vp, i64, d, d, vp]
+    L.pbng_set_constraints.argtypes = [vp, vp, i64, vp, vp, i64]
+    L.pbng_color.argtypes = [vp, vp, vp]
+    L.pbng_workspace_bytes.argtypes = [vp, C.POINTER(C.c_uint64)]
+    L.pbng_bind_workspace.argtypes = [vp, vp, C.c_uint64]
+    L.pbng_set_positions.argtypes = [vp, vp]
+    L.pbng_get_positions.argtypes = [vp, vp]
+    L.pbng_iterate.argtypes = [vp, i32, C.c_int, d, d, d]
+    L.pbng_energy_residual.argtypes = [vp, vp, vp]
+    L.pbng_synchronize.argtypes = [vp]
+    L.pbng_query.argtypes = [vp, C.POINTER(Info)]
+    L.pbng_profile_enable.argtypes = [vp, C.c_int]
+    L.pbng_profile_read.argtypes = [vp, C.POINTER(d), C.POINTER(i64)]
+    L.pbng_destroy.argtypes = [vp]
+    L.pbng_last_error.restype = C.c_char_p
+    L.pbng_version.restype = i32
+    for name in EXPORTS:
+        if name not in ("pbng_last_error", "pbng_version"):
+            getattr(L, name).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != OK:
+        raise PBNGError(status, lib().pbng_last_error().decode())
+
+
+def _np(a, dt):
+    return np.ascontiguousarray(np.asarray(a, dtype=dt))
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def weak_constraints_array(wc: Optional[dict]) -> np.ndarray:
+    if wc is None:
+        return np.zeros(0, WC_DTYPE)
+    n = wc["n0"].shape[0]
+    out = np.zeros(n, WC_DTYPE)
+    for k in ("n0", "n1", "idx0", "idx1", "w0", "w1", "anchor", "K"):
+        out[k] = wc[k]
+    return out
+
+
+class Context:
+    """One PBNG problem (or a batch of samples sharing mesh, material and colouring) on one device.
+
+    Mirrors the C ABI: create_mesh (constructor) -> set_material -> set_constraints -> color ->
+    bind_workspace -> set_positions -> iterate / energy_residual / get_positions."""
+
+    def __init__(self, X, tets, n_batch: int = 1, dtype: str = "f32", device=0, stream=None):
+        import torch
+        self._torch = torch
+        L = lib()
+        X = _np(X, np.float64).reshape(-1, 3)
+        tets = _np(tets, np.int32).reshape(-1, 4)
+        self.n_vertices = X.shape[0]
+        self.n_tets = tets.shape[0]
+        self.n_batch = int(n_batch)
+        self.dtype = dtype
+        self.np_dtype = np.float32 if dtype == "f32" else np.float64
+        self.torch_dtype = torch.float32 if dtype == "f32" else torch.float64
+        if isinstance(device, torch.device):
+            device = device.index if device.index is not None else torch.cuda.current_device()
+        self.device = int(device)
+        if self.device >= 0:
+            if stream is None:
+                stream = torch.cuda.current_stream(self.device)
+            self.stream = stream
+            handle = stream.cuda_stream
+        else:
+            self.stream = None
+            handle = 0
+        h = C.c_void_p()
+        bad = C.c_int64(-1)
+        st = L.pbng_create_mesh(_ptr(X), X.shape[0], _ptr(tets) if tets.size else None, tets.shape[0],
+                                self.n_batch, DTYPE[dtype], self.device, handle, C.byref(h), C.byref(bad))
+        if st != OK:
+            err = PBNGError(st, L.pbng_last_error().decode())
+            err.bad_index = bad.value
+            raise err
+        self._h = h
+        self.workspace = None
+
+    # ---------------------------------------------------------------------------------------------
+    def set_material(self, model: str, E, nu: float, density: float = 0.0, gravity=(0.0, 0.0, 0.0)):
+        E = _np(np.atleast_1d(E), np.float64)
+        g = _np(gravity, np.float64)
+        _check(lib().pbng_set_material(self._h, MODEL[model], _ptr(E), E.size, float(nu), float(density), _ptr(g)))
+
+    def set_constraints(self, pinned, targets, wc: Optional[dict] = None):
+        pinned = _np(pinned, np.int32).reshape(-1)
+        targets = _np(targets, np.float64).reshape(-1)
+        w = weak_constraints_array(wc)
+        _check(lib().pbng_set_constraints(self._h, _ptr(pinned) if pinned.size else None, pinned.size,
+                                          _ptr(targets) if targets.size else None, _ptr(w) if w.size else None,
+                                          w.size))
+
+    def color(self):
+        out = np.empty(self.n_vertices, np.int32)
+        n = C.c_int32()
+        _check(lib().pbng_color(self._h, _ptr(out), C.byref(n)))
+        return out, n.value
+
+    def workspace_bytes(self) -> int:
+        b = C.c_uint64()
+        _check(lib().pbng_workspace_bytes(self._h, C.byref(b)))
+        return b.value
+
+    def bind_workspace(self, tensor=None):
+        torch = self._torch
+        nbytes = self.workspace_bytes()
+        if tensor is None:
+            tensor = torch.empty(nbytes + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
+        ptr = tensor.data_ptr()
+        pad = (-ptr) % 256
+        _check(lib().pbng_bind_workspace(self._h, ptr + pad, tensor.numel() - pad))
+        self.workspace = tensor
+        return tensor
+
+    # ---------------------------------------------------------------------------------------------
+    def _shape(self):
+        return (self.n_batch, self.n_vertices, 3)
+
+    def set_positions(self, x):
+        """x: torch tensor (device or pinned/pageable host) or numpy array, [n_batch, n_vertices, 3]."""
+        torch = self._torch
+        if isinstance(x, np.ndarray):
+            x = torch.from_numpy(_np(x, self.np_dtype))
+        if x.dtype != self.torch_dtype or not x.is_contiguous():
+            x = x.to(self.torch_dtype).contiguous()
+        if x.numel() != self.n_batch * self.n_vertices * 3:
+            raise ValueError(f"positions must have {self._shape()} entries")
+        self._x_keep = x
+        _check(lib().pbng_set_positions(self._h, x.data_ptr()))
+
+    def get_positions(self, out=None):
+        torch = self._torch
+        if out is None:
+            out = torch.empty(self._shape(), dtype=self.torch_dtype, device=f"cuda:{self.device}")
+        if out.dtype != self.torch_dtype or not out.is_contiguous() or out.numel() != self.n_batch * self.n_vertices * 3:
+            raise ValueError("out must be a contiguous tensor of the context dtype and shape")
+        _check(lib().pbng_get_positions(self._h, out.data_ptr()))
+        return out
+
+    def iterate(self, n: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0, gamma: float = 1.0):
+        _check(lib().pbng_iterate(self._h, int(n), ACCEL[accel], float(omega), float(rho), float(gamma)))
+
+    def energy_residual(self):
+        e = np.empty(self.n_batch)
+        r = np.empty(self.n_batch)
+        _check(lib().pbng_energy_residual(self._h, _ptr(e), _ptr(r)))
+        return e, r
+
+    def synchronize(self):
+        _check(lib().pbng_synchronize(self._h))
+
+    def query(self) -> dict:
+        info = Info()
+        _check(lib().pbng_query(self._h, C.byref(info)))
+        return {k: getattr(info, k) for k, _ in Info._fields_}
+
+    def profile_enable(self, on: bool = True):
+        _check(lib().pbng_profile_enable(self._h, int(bool(on))))
+
+    def profile_read(self):
+        ms = C.c_double()
+        n = C.c_int64()
+        _check(lib().pbng_profile_read(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.pbng_destroy(h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def context_from_scene(scene, device=0, dtype: Optional[str] = None, stream=None, bind: bool = True,
+                       set_positions: bool = True) -> Context:
+    """Build, colour, bind and initialise a Context for a scenes.Scene (all samples of its batch)."""
+    ctx = Context(scene.X, scene.tets, n_batch=scene.n_batch, dtype=dtype or scene.dtype, device=device, stream=stream)
+    ctx.set_material(scene.model, scene.E, scene.nu, scene.density, scene.gravity)
+    ctx.set_constraints(scene.pinned, scene.targets, scene.wc)
+    ctx.colours, ctx.n_colours = ctx.color()
+    if bind and ctx.device >= 0:
+        ctx.bind_workspace()
+        if set_positions:
+            ctx.set_positions(np.asarray(scene.x0))
+    return ctx

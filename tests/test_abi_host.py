@@ -1,0 +1,121 @@
+"""CPU tests of the C-ABI boundary: the library loads, exports every symbol include/pbng.h declares, and
+its host logic (validation, greedy colouring, layout sizes) behaves -- no compute call needs a GPU here
+(host-only contexts, device = -1)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2306_09021_b200 import pbng as P
+from scenes import generators as G
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "pbng.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pbng_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = P.lib()
+    names = declared_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) == set(P.EXPORTS)
+    assert L.pbng_version() == 100
+    # the library is the in-tree build
+    assert os.path.dirname(P.LIB_PATH) == os.path.join(ROOT, "paper_2306_09021_b200")
+
+
+def test_nm_shows_c_linkage():
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", P.LIB_PATH], capture_output=True, text=True).stdout
+    for n in declared_functions():
+        assert re.search(rf"\bT {n}$", out, flags=re.M), n
+
+
+def host_ctx(scene, dtype="f64"):
+    return P.context_from_scene(scene, device=-1, dtype=dtype)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_library_colouring_equals_oracle(cfg):
+    from oracle import Oracle
+    s = G.make_config(cfg, "small")
+    ctx = host_ctx(s)
+    o = Oracle(s)
+    assert ctx.n_colours == o.n_colours
+    assert np.array_equal(ctx.colours, o.colours())
+
+
+def test_library_colouring_table1_and_spring_network():
+    from oracle import Oracle
+    for n in (16, 32):
+        X, T = G.five_tet_grid(n)
+        ctx = P.Context(X, T, device=-1)
+        ctx.set_material("nh", 1e5, 0.3)
+        ctx.set_constraints(np.zeros(0, np.int32), np.zeros(0))
+        col, nc = ctx.color()
+        assert nc == 5  # PAPER.md Table 1 (tests/golden/table1_colours.json)
+    s = G.spring_network()
+    ctx = host_ctx(s)
+    assert np.array_equal(ctx.colours, Oracle(s).colours())
+
+
+def test_query_counts():
+    s = G.config1_tiny_cube()
+    ctx = host_ctx(s)
+    q = ctx.query()
+    assert q["n_vertices"] == 125 and q["n_tets"] == 384 and q["n_pinned"] == 50 and q["n_free"] == 75
+    deg = np.bincount(s.tets.reshape(-1), minlength=125)
+    free = np.setdiff1d(np.arange(125), s.pinned)
+    assert q["n_pairs"] == deg[free].sum()
+    assert q["n_pair_slots"] >= q["n_pairs"] and q["n_pair_slots"] % 32 == 0
+    assert q["n_colours"] == 8
+
+
+def test_errors():
+    X = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 1, 0]], float)
+    with pytest.raises(P.PBNGError) as ei:
+        P.Context(X, [[0, 1, 2, 3], [0, 1, 4, 2]], device=-1)
+    assert ei.value.status == 3 and ei.value.bad_index == 1
+    with pytest.raises(P.PBNGError) as ei:
+        P.Context(X, [[0, 1, 2, 7]], device=-1)
+    assert ei.value.status == 2 and ei.value.bad_index == 0
+    ctx = P.Context(X, [[0, 1, 2, 3]], device=-1)
+    with pytest.raises(P.PBNGError) as ei:
+        ctx.set_material("nh", 1e5, 0.5)
+    assert ei.value.status == 1
+    with pytest.raises(P.PBNGError) as ei:
+        ctx.color()
+    assert ei.value.status == 5  # bad order: material / constraints missing
+    ctx.set_material("nh", 1e5, 0.3)
+    ctx.set_constraints(np.zeros(0, np.int32), np.zeros(0))
+    with pytest.raises(P.PBNGError) as ei:
+        ctx.color()
+    assert ei.value.status == 4  # vertex 4 is free and isolated
+    ctx.set_constraints(np.array([4], np.int32), np.array([1.0, 1.0, 0.0]))
+    col, nc = ctx.color()
+    assert nc == 4
+    with pytest.raises(P.PBNGError) as ei:
+        ctx.bind_workspace  # attribute exists
+        P._check(P.lib().pbng_set_positions(ctx._h, None))
+    assert ei.value.status == 11  # host-only context
+    with pytest.raises(P.PBNGError) as ei:
+        ctx.set_constraints(np.array([4, 4], np.int32), np.zeros(6))
+    assert ei.value.status == 1
+
+
+def test_weak_constraint_struct_layout():
+    import ctypes as C
+
+    class WC(C.Structure):
+        _fields_ = [("n0", C.c_int32), ("n1", C.c_int32), ("idx0", C.c_int32 * 4), ("idx1", C.c_int32 * 4),
+                    ("w0", C.c_double * 4), ("w1", C.c_double * 4), ("anchor", C.c_double * 3), ("K", C.c_double * 6)]
+    assert C.sizeof(WC) == P.WC_DTYPE.itemsize == 176
+    for name in ("w0", "w1", "anchor", "K"):
+        assert getattr(WC, name).offset == P.WC_DTYPE.fields[name][1]
