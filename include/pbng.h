@@ -151,9 +151,12 @@ pbng_status pbng_synchronize(pbng_ctx *ctx);
 /* Sizes, byte / flop model and counters. */
 pbng_status pbng_query(pbng_ctx *ctx, pbng_info *info);
 
-/* Per-launch timing of the colour-sweep kernel with CUDA events on the context stream (bench.py's
- * roofline).  enable != 0 starts recording; pbng_profile_read synchronises, returns the summed sweep
- * kernel time (ms) and the number of timed launches since the last read, then clears them. */
+/* Timing of the colour-sweep kernel with CUDA events on the context stream (bench.py's roofline).
+ * enable = 1: an event pair around every sweep launch; enable = 2: an event pair around the
+ * back-to-back sweep launches of each pbng_iterate call (no events between launches, so the kernels
+ * are not perturbed; launch gaps are included, a conservative average); 0: off.  pbng_profile_read
+ * synchronises, returns the summed time (ms) and the number of sweep launches it covers since the last
+ * read, then clears them. */
 pbng_status pbng_profile_enable(pbng_ctx *ctx, int enable);
 pbng_status pbng_profile_read(pbng_ctx *ctx, double *sweep_ms, int64_t *sweep_launches);
 

@@ -77,6 +77,8 @@ def lib():
             L.orc_get_fext.argtypes = [vp, vp]
             L.orc_deformation_gradient.argtypes = [vp, vp, i64, vp]
             L.orc_nodal.argtypes = [vp, vp, i64, vp, vp]
+            L.orc_sweep_colour.argtypes = [vp, vp, i32]
+            L.orc_sweep_colour.restype = i64
             L.orc_sweep.argtypes = [vp, vp]
             L.orc_sweep.restype = i64
             L.orc_chebyshev_omega.argtypes = [i64, d]
@@ -274,6 +276,13 @@ class Oracle:
         if fails:
             raise RuntimeError(f"{fails} nodal solves failed")
         return w
+
+    def sweep_colour_inplace(self, w: np.ndarray, c: int) -> None:
+        """One colour pass of a PBNG iteration, in place on a float64 C-contiguous (nv, 3) array."""
+        assert w.dtype == np.float64 and w.flags.c_contiguous and w.shape == (self.nv, 3)
+        fails = lib().orc_sweep_colour(self._h, _p(w), int(c))
+        if fails:
+            raise RuntimeError(f"{fails} nodal solves failed")
 
     def iterate(self, x, xm1, l0: int, n: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0,
                 gamma: float = 1.0):

@@ -637,19 +637,24 @@ static int spd_solve3(const double *A, const double *r, double *x) {
 /* One PBNG iteration in place: colours in ascending order; within a
  * colour, free nodes in ascending index; each node takes ONE modified-Newton step from a zero initial
  * guess, x_i += A^{-1} (f_i + f^ext_i), with no line search.  Returns the number of failed solves. */
+int64_t orc_sweep_colour(const orc_prep *p, double *w, int32_t c) {
+    int64_t i, fails = 0;
+    for (i = 0; i < p->nv; ++i) {
+        double f[3], A[9], dx[3];
+        if (p->colour[i] != c || p->pinned[i]) continue;
+        orc_nodal(p, w, i, f, A);
+        if (spd_solve3(A, f, dx)) { ++fails; continue; }
+        w[3 * i + 0] += dx[0];
+        w[3 * i + 1] += dx[1];
+        w[3 * i + 2] += dx[2];
+    }
+    return fails;
+}
+
 int64_t orc_sweep(const orc_prep *p, double *w) {
     int32_t c;
-    int64_t i, fails = 0;
-    for (c = 0; c < p->ncolours; ++c)
-        for (i = 0; i < p->nv; ++i) {
-            double f[3], A[9], dx[3];
-            if (p->colour[i] != c || p->pinned[i]) continue;
-            orc_nodal(p, w, i, f, A);
-            if (spd_solve3(A, f, dx)) { ++fails; continue; }
-            w[3 * i + 0] += dx[0];
-            w[3 * i + 1] += dx[1];
-            w[3 * i + 2] += dx[2];
-        }
+    int64_t fails = 0;
+    for (c = 0; c < p->ncolours; ++c) fails += orc_sweep_colour(p, w, c);
     return fails;
 }
 

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -66,6 +67,24 @@ struct Region {
     size_t off = 0, bytes = 0;
 };
 
+// 3 x 21-bit Morton (Z-order) interleave
+uint64_t spread21(uint64_t x) {
+    x &= 0x1fffffull;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+uint64_t morton3(uint64_t a, uint64_t b, uint64_t c) { return spread21(a) | spread21(b) << 1 | spread21(c) << 2; }
+
+// intra-colour vertex order: Morton (default) or ascending index (PBNG_ORDER=index, for experiments)
+bool spatial_order() {
+    const char *e = getenv("PBNG_ORDER");
+    return !(e && std::string(e) == "index");
+}
+
 }  // namespace
 
 struct pbng_ctx {
@@ -121,8 +140,9 @@ struct pbng_ctx {
     bool hist_valid = true;
     int64_t launches = 0;
     // profiling
-    bool profiling = false;
+    int profiling = 0;  // 0 off, 1 per sweep launch, 2 per iterate span (back-to-back sweep launches)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
+    std::vector<int64_t> ev_launches;
 
     size_t real_size() const { return dtype == DT_F64 ? 8 : 4; }
     size_t real4_size() const { return dtype == DT_F64 ? 32 : 16; }
@@ -441,22 +461,28 @@ pbng_status require_device(pbng_ctx *c) {
     return PBNG_OK;
 }
 
-cudaError_t timed_sweep(pbng_ctx *c, const SweepLaunch &s) {
-    if (!c->profiling) return launch_sweep(c->prob, c->L, s, c->stream);
-    std::pair<cudaEvent_t, cudaEvent_t> ev;
+cudaError_t get_event_pair(pbng_ctx *c, std::pair<cudaEvent_t, cudaEvent_t> &ev) {
     if (!c->ev_free.empty()) {
         ev = c->ev_free.back();
         c->ev_free.pop_back();
-    } else {
-        cudaError_t e = cudaEventCreate(&ev.first);
-        if (e != cudaSuccess) return e;
-        e = cudaEventCreate(&ev.second);
-        if (e != cudaSuccess) return e;
+        return cudaSuccess;
     }
+    cudaError_t e = cudaEventCreate(&ev.first);
+    if (e != cudaSuccess) return e;
+    return cudaEventCreate(&ev.second);
+}
+
+// profiling mode 1: an event pair around every sweep launch
+cudaError_t timed_sweep(pbng_ctx *c, const SweepLaunch &s) {
+    if (c->profiling != 1) return launch_sweep(c->prob, c->L, s, c->stream);
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    cudaError_t e = get_event_pair(c, ev);
+    if (e != cudaSuccess) return e;
     cudaEventRecord(ev.first, c->stream);
-    cudaError_t e = launch_sweep(c->prob, c->L, s, c->stream);
+    e = launch_sweep(c->prob, c->L, s, c->stream);
     cudaEventRecord(ev.second, c->stream);
     c->ev_used.push_back(ev);
+    c->ev_launches.push_back(1);
     return e;
 }
 
@@ -689,6 +715,32 @@ pbng_status pbng_color(pbng_ctx *c, int32_t *colour_out, int32_t *n_colours_out)
                 c->int2orig[i] = (int32_t)v;
             }
         }
+        // Within a colour the update order is free (same-coloured vertices share no stencil, PAPER.md:
+        // 697-705), so each colour's free vertices are laid out along a Morton curve of their rest
+        // positions: a warp's 32 vertices are spatially compact and their neighbour gathers share cache
+        // lines.  Results are unchanged bit for bit (each vertex's own summation order is fixed).
+        if (spatial_order()) {
+            double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+            for (int64_t v = 0; v < nv; ++v)
+                for (int a = 0; a < 3; ++a) {
+                    lo[a] = std::min(lo[a], c->X[3 * v + a]);
+                    hi[a] = std::max(hi[a], c->X[3 * v + a]);
+                }
+            double ext = 0;
+            for (int a = 0; a < 3; ++a) ext = std::max(ext, hi[a] - lo[a]);
+            const double scale = ext > 0 ? (double)((1u << 21) - 1) / ext : 0.0;
+            std::vector<uint64_t> key((size_t)nv);
+            for (int64_t v = 0; v < nv; ++v) {
+                uint64_t q[3];
+                for (int a = 0; a < 3; ++a) q[a] = (uint64_t)((c->X[3 * v + a] - lo[a]) * scale);
+                key[v] = morton3(q[0], q[1], q[2]);
+            }
+            for (int32_t col = 0; col < c->ncol; ++col) {
+                int32_t *b = c->int2orig.data() + c->col_vbegin[col];
+                std::stable_sort(b, b + c->col_nfree[col], [&](int32_t x, int32_t y) { return key[x] < key[y]; });
+                for (int32_t q = 0; q < c->col_nfree[col]; ++q) c->orig2int[b[q]] = c->col_vbegin[col] + q;
+            }
+        }
         if (c->dtype == DT_F64) build_layout<double>(c, vt_off, vt);
         else build_layout<float>(c, vt_off, vt);
         plan_workspace(c);
@@ -841,6 +893,13 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
     if (accel != PBNG_ACCEL_NONE && !c->hist_valid)
         return fail(PBNG_E_BAD_ORDER, "iterate: x^{l-1} was not kept by non-accelerated iterations; call set_positions");
     DevGuard g(c->device);
+    std::pair<cudaEvent_t, cudaEvent_t> span;
+    const bool span_prof = c->profiling == 2 && n_iterations > 0;
+    int64_t span_launches = 0;
+    if (span_prof) {
+        PBNG_CUDA(get_event_pair(c, span), "iterate: profiling events");
+        PBNG_CUDA(cudaEventRecord(span.first, c->stream), "iterate: event");
+    }
     for (int32_t it = 0; it < n_iterations; ++it) {
         SweepLaunch s;
         s.accel = accel;
@@ -860,10 +919,16 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
             if (s.n_v == 0) continue;
             PBNG_CUDA(timed_sweep(c, s), "iterate: sweep kernel");
             c->launches += 1;
+            span_launches += 1;
         }
         if (accel != PBNG_ACCEL_NONE) std::swap(c->work, c->out);
         else c->hist_valid = false;
         c->l += 1;
+    }
+    if (span_prof) {
+        PBNG_CUDA(cudaEventRecord(span.second, c->stream), "iterate: event");
+        c->ev_used.push_back(span);
+        c->ev_launches.push_back(span_launches);
     }
     return PBNG_OK;
 }
@@ -930,7 +995,8 @@ pbng_status pbng_query(pbng_ctx *c, pbng_info *info) {
 pbng_status pbng_profile_enable(pbng_ctx *c, int enable) {
     pbng_status st = require_device(c);
     if (st != PBNG_OK) return st;
-    c->profiling = enable != 0;
+    if (enable < 0 || enable > 2) return fail(PBNG_E_INVALID_ARGUMENT, "profile_enable: mode must be 0, 1 or 2");
+    c->profiling = enable;
     return PBNG_OK;
 }
 
@@ -940,15 +1006,18 @@ pbng_status pbng_profile_read(pbng_ctx *c, double *sweep_ms, int64_t *sweep_laun
     DevGuard g(c->device);
     PBNG_CUDA(cudaStreamSynchronize(c->stream), "profile_read: synchronize");
     double total = 0.0;
-    for (auto &ev : c->ev_used) {
+    int64_t n = 0;
+    for (size_t k = 0; k < c->ev_used.size(); ++k) {
         float ms = 0.f;
-        PBNG_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second), "profile_read: elapsed");
+        PBNG_CUDA(cudaEventElapsedTime(&ms, c->ev_used[k].first, c->ev_used[k].second), "profile_read: elapsed");
         total += ms;
-        c->ev_free.push_back(ev);
+        n += c->ev_launches[k];
+        c->ev_free.push_back(c->ev_used[k]);
     }
     if (sweep_ms) *sweep_ms = total;
-    if (sweep_launches) *sweep_launches = (int64_t)c->ev_used.size();
+    if (sweep_launches) *sweep_launches = n;
     c->ev_used.clear();
+    c->ev_launches.clear();
     return PBNG_OK;
 }
 

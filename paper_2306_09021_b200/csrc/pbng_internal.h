@@ -15,7 +15,10 @@ enum { ACCEL_NONE = 0, ACCEL_SOR = 1, ACCEL_CHEB = 2 };
 enum { DT_F32 = 0, DT_F64 = 1 };
 
 constexpr int kChunk = 32;        // vertices per SELL chunk == one warp
-constexpr int kSweepBlock = 128;  // threads per sweep CTA (4 chunks)
+#ifndef PBNG_SWEEP_BLOCK
+#define PBNG_SWEEP_BLOCK 128
+#endif
+constexpr int kSweepBlock = PBNG_SWEEP_BLOCK;  // threads per sweep CTA (a multiple of the 32-vertex chunk)
 constexpr int kWcMaxNodes = 8;    // distinct nodes per weak constraint
 constexpr int kRedBlock = 256;    // threads per reduction CTA
 

@@ -221,15 +221,61 @@ __device__ __forceinline__ void pair_contrib(const T (&d1)[3], const T (&d2)[3],
     }
 }
 
+// streamed (read-once) record loads: L1::no_allocate keeps L1 for the neighbour-position gathers
+#ifndef PBNG_REC_HINT
+#define PBNG_REC_HINT 1
+#endif
+__device__ __forceinline__ int4 lds(const int4 *p) {
+#if PBNG_REC_HINT
+    int4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ float4 lds(const float4 *p) {
+#if PBNG_REC_HINT
+    float4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ float lds(const float *p) {
+#if PBNG_REC_HINT
+    float r;
+    asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    return r;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double2 lds(const double2 *p) {
+#if PBNG_REC_HINT
+    double2 r;
+    asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double4 lds(const double4 *p) {
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+    const double2 a = lds(q), b = lds(q + 1);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+
 // record field decode
 template <class R> struct Rec;
 template <> struct Rec<float> {
     static __device__ __forceinline__ void load(const Layout &L, int64_t r, int4 &id, float (&g1)[3], float (&g2)[3],
                                                 float (&g3)[3], float &VE) {
-        id = ld(L.rec_id + r);
-        const float4 a = ld(reinterpret_cast<const float4 *>(L.rec_a) + r);
-        const float4 b = ld(reinterpret_cast<const float4 *>(L.rec_b) + r);
-        const float c = ld(reinterpret_cast<const float *>(L.rec_c) + r);
+        id = lds(L.rec_id + r);
+        const float4 a = lds(reinterpret_cast<const float4 *>(L.rec_a) + r);
+        const float4 b = lds(reinterpret_cast<const float4 *>(L.rec_b) + r);
+        const float c = lds(reinterpret_cast<const float *>(L.rec_c) + r);
         g1[0] = a.x; g1[1] = a.y; g1[2] = a.z;
         g2[0] = a.w; g2[1] = b.x; g2[2] = b.y;
         g3[0] = b.z; g3[1] = b.w; g3[2] = c;
@@ -239,10 +285,10 @@ template <> struct Rec<float> {
 template <> struct Rec<double> {
     static __device__ __forceinline__ void load(const Layout &L, int64_t r, int4 &id, double (&g1)[3], double (&g2)[3],
                                                 double (&g3)[3], double &VE) {
-        id = ld(L.rec_id + r);
-        const double4 a = ld(reinterpret_cast<const double4 *>(L.rec_a) + r);
-        const double4 b = ld(reinterpret_cast<const double4 *>(L.rec_b) + r);
-        const double2 c = ld(reinterpret_cast<const double2 *>(L.rec_c) + r);
+        id = lds(L.rec_id + r);
+        const double4 a = lds(reinterpret_cast<const double4 *>(L.rec_a) + r);
+        const double4 b = lds(reinterpret_cast<const double4 *>(L.rec_b) + r);
+        const double2 c = lds(reinterpret_cast<const double2 *>(L.rec_c) + r);
         g1[0] = a.x; g1[1] = a.y; g1[2] = a.z;
         g2[0] = a.w; g2[1] = b.x; g2[2] = b.y;
         g3[0] = b.z; g3[1] = b.w; g3[2] = c.x;
@@ -289,42 +335,22 @@ __device__ __forceinline__ void wc_contrib(const Layout &L, const typename RT<R>
 // ------------------------------------------------------------------------------------------------
 // colour sweep
 // ------------------------------------------------------------------------------------------------
-template <class R, int MODEL, int ACCEL, bool FEXT, bool WC>
-__global__ void __launch_bounds__(kSweepBlock) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
-                                                            const int64_t chunk_begin, const int64_t x_stride,
-                                                            const int wi, const int oi, const int hi, const R cmu,
-                                                            const R clam, const R omega, const R gamma) {
+template <class R>
+__device__ __forceinline__ void sub3(const typename RT<R>::R4 &p, const R (&xa)[3], R (&d)[3]) {
+    d[0] = p.x - xa[0];
+    d[1] = p.y - xa[1];
+    d[2] = p.z - xa[2];
+}
+
+// one modified-Newton step from a zero initial guess (eq:pbgn_dx): dx = A^{-1} (f_i + f^ext_i) by
+// Cholesky in registers (A is SPD); then the fused acceleration blend and the stores.
+template <class R, int ACCEL>
+__device__ __forceinline__ void finish_vertex(const Layout &L, typename RT<R>::R4 *__restrict__ work, const int64_t xs,
+                                              const int v, const int oi, const int hi,
+                                              const typename RT<R>::R4 &xa4, const R (&f)[3], const R (&A)[6],
+                                              const R omega, const R gamma) {
     using R4 = typename RT<R>::R4;
-    const int t = blockIdx.x * kSweepBlock + threadIdx.x;
-    if (t >= n_v) return;
-    const int v = v_begin + t;
-    const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
-    const int deg = ld(L.deg + v);
-    const int64_t xs = (int64_t)blockIdx.y * x_stride;
-    R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
-
-    const R4 xa4 = work[v];
     const R xa[3] = {xa4.x, xa4.y, xa4.z};
-    R f[3] = {R(0), R(0), R(0)};
-    if (FEXT) {
-        const R4 fe = ld(reinterpret_cast<const R4 *>(L.fext) + v);
-        f[0] = fe.x; f[1] = fe.y; f[2] = fe.z;
-    }
-    R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
-
-    for (int k = 0; k < deg; ++k) {
-        int4 id;
-        R g1[3], g2[3], g3[3], VE;
-        Rec<R>::load(L, base + (int64_t)k * kChunk, id, g1, g2, g3, VE);
-        const R4 p1 = ld(work + id.x), p2 = ld(work + id.y), p3 = ld(work + id.z);
-        const R d1[3] = {p1.x - xa[0], p1.y - xa[1], p1.z - xa[2]};
-        const R d2[3] = {p2.x - xa[0], p2.y - xa[1], p2.z - xa[2]};
-        const R d3[3] = {p3.x - xa[0], p3.y - xa[1], p3.z - xa[2]};
-        pair_contrib<MODEL, true>(d1, d2, d3, g1, g2, g3, VE * cmu, VE * clam, f, A);
-    }
-    if (WC) wc_contrib<R, R, true>(L, work, v, xa, f, A);
-
-    // A dx = f by Cholesky in registers (A is SPD)
     const R i00 = rsq(A[0]);
     const R l10 = A[3] * i00, l20 = A[5] * i00;
     const R i11 = rsq(A[1] - l10 * l10);
@@ -356,6 +382,49 @@ __global__ void __launch_bounds__(kSweepBlock) sweep_kernel(const Layout L, cons
         out[v] = mk4<R>(o[0], o[1], o[2]);
         hist[v] = xa4;
     }
+}
+
+// One thread per free vertex of the colour; a warp owns one 32-vertex SELL chunk, so record k of its
+// 32 lanes is one contiguous 512 B (f32) segment per field.  The record stream is read once with
+// L1::no_allocate; the neighbour positions are gathered through L1 (different colour, read-only in this
+// launch).  The per-vertex summation order is ascending tet index, as in the oracle.
+template <class R, int MODEL, int ACCEL, bool FEXT, bool WC>
+#ifndef PBNG_SWEEP_MINB
+#define PBNG_SWEEP_MINB 1
+#endif
+__global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
+                                                            const int64_t chunk_begin, const int64_t x_stride,
+                                                            const int wi, const int oi, const int hi, const R cmu,
+                                                            const R clam, const R omega, const R gamma) {
+    using R4 = typename RT<R>::R4;
+    const int t = blockIdx.x * kSweepBlock + threadIdx.x;
+    if (t >= n_v) return;
+    const int v = v_begin + t;
+    const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
+    const int deg = ld(L.deg + v);
+    const int64_t xs = (int64_t)blockIdx.y * x_stride;
+    R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
+
+    const R4 xa4 = work[v];
+    const R xa[3] = {xa4.x, xa4.y, xa4.z};
+    R f[3] = {R(0), R(0), R(0)};
+    if (FEXT) {
+        const R4 fe = ld(reinterpret_cast<const R4 *>(L.fext) + v);
+        f[0] = fe.x; f[1] = fe.y; f[2] = fe.z;
+    }
+    R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
+
+    for (int k = 0; k < deg; ++k) {
+        int4 id;
+        R g1[3], g2[3], g3[3], VE, d1[3], d2[3], d3[3];
+        Rec<R>::load(L, base + (int64_t)k * kChunk, id, g1, g2, g3, VE);
+        sub3<R>(ld(work + id.x), xa, d1);
+        sub3<R>(ld(work + id.y), xa, d2);
+        sub3<R>(ld(work + id.z), xa, d3);
+        pair_contrib<MODEL, true>(d1, d2, d3, g1, g2, g3, VE * cmu, VE * clam, f, A);
+    }
+    if (WC) wc_contrib<R, R, true>(L, work, v, xa, f, A);
+    finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
 }
 
 template <class R, int MODEL, int ACCEL>

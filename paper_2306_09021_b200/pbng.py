@@ -13,7 +13,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpbng.so")
+LIB_PATH = os.environ.get("PBNG_LIB", os.path.join(_HERE, "libpbng.so"))  # PBNG_LIB: tuning builds only
 
 OK = 0
 STATUS = {0: "PBNG_OK", 1: "PBNG_E_INVALID_ARGUMENT", 2: "PBNG_E_INDEX_OUT_OF_RANGE", 3: "PBNG_E_DEGENERATE_ELEMENT",
@@ -225,8 +225,9 @@ class Context:
         _check(lib().pbng_query(self._h, C.byref(info)))
         return {k: getattr(info, k) for k, _ in Info._fields_}
 
-    def profile_enable(self, on: bool = True):
-        _check(lib().pbng_profile_enable(self._h, int(bool(on))))
+    def profile_enable(self, mode: int = 2):
+        """mode 1: events around every sweep launch; 2: around each iterate call's sweep launches; 0: off."""
+        _check(lib().pbng_profile_enable(self._h, int(mode)))
 
     def profile_read(self):
         ms = C.c_double()
