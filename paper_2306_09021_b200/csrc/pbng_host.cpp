@@ -455,6 +455,22 @@ double accel_bytes_model(const pbng_ctx *c) {
     return (double)c->nb * (double)c->n_free * 9.0 * (double)c->real_size();
 }
 
+// Warps per 32-vertex chunk for a colour pass: the fixed-corotated pair (a polar decomposition) is
+// compute-heavy, and small colours leave SMs idle with one thread per vertex, so both split the pair
+// loop over several warps.  PBNG_SPLIT=1|2|4 overrides (experiments).
+int choose_split(const pbng_ctx *c, int64_t n_v) {
+    static const int forced = [] {
+        const char *e = getenv("PBNG_SPLIT");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
+    const int64_t threads = n_v * c->nb;
+    if (c->model == MODEL_FCR) return 4;
+    if (threads < 148 * 512) return 4;
+    if (threads < 148 * 1024) return 2;
+    return 1;
+}
+
 pbng_status require_device(pbng_ctx *c) {
     if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
     if (!c->on_device()) return fail(PBNG_E_NO_DEVICE, "host-only context (device = -1)");
@@ -916,6 +932,7 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
             s.v_begin = c->col_vbegin[col];
             s.n_v = c->col_nfree[col];
             s.chunk_begin = c->col_chunk[col];
+            s.split = choose_split(c, s.n_v);
             if (s.n_v == 0) continue;
             PBNG_CUDA(timed_sweep(c, s), "iterate: sweep kernel");
             c->launches += 1;

@@ -76,6 +76,7 @@ struct SweepLaunch {
     int work = 0, out = 1, hist = 2;  // xbuf indices
     int accel = ACCEL_NONE;
     double omega = 1, gamma = 1;  // SOR omega, or Chebyshev omega_{l+1} and gamma
+    int split = 1;  // warps sharing one 32-vertex chunk (1, 2 or 4)
 };
 
 // launchers (pbng_kernels.cu); return cudaGetLastError()

@@ -427,21 +427,102 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_kernel(con
     finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
 }
 
+// Split variant for compute-heavy pairs (fixed-corotated: a polar decomposition per pair) and small
+// colours: SPLIT warps share one 32-vertex chunk, warp s takes records k = s, s + SPLIT, ...; the nine
+// partial sums (f: 3, A: 6) are combined through shared memory in fixed warp order (deterministic),
+// and warp 0 solves and stores.  Block = SPLIT * 32 * CPB threads, CPB chunks per block.
+template <int SPLIT> struct SplitBlock { static constexpr int n = SPLIT * 32 > kSweepBlock ? SPLIT * 32 : kSweepBlock; };
+template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int SPLIT>
+__global__ void __launch_bounds__(SplitBlock<SPLIT>::n) sweep_split_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
+                                                                  const int64_t chunk_begin, const int64_t x_stride,
+                                                                  const int wi, const int oi, const int hi, const R cmu,
+                                                                  const R clam, const R omega, const R gamma) {
+    using R4 = typename RT<R>::R4;
+    constexpr int CPB = SplitBlock<SPLIT>::n / (32 * SPLIT);
+    static_assert(CPB >= 1 && CPB * SPLIT * 32 == SplitBlock<SPLIT>::n, "block must hold whole chunk groups");
+    __shared__ R red[CPB][SPLIT - 1][9][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cl = warp / SPLIT, sub = warp % SPLIT;
+    const int tc = (blockIdx.x * CPB + cl) * 32 + lane;  // vertex index within the colour
+    const bool valid = tc < n_v;
+    const int v = v_begin + tc;
+    const int64_t xs = (int64_t)blockIdx.y * x_stride;
+    R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
+    R f[3] = {R(0), R(0), R(0)};
+    R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
+    R4 xa4 = mk4<R>(R(0), R(0), R(0));
+    if (valid) {
+        const int64_t base = ld(L.chunk_off + chunk_begin + (tc >> 5)) + lane;
+        const int deg = ld(L.deg + v);
+        xa4 = work[v];
+        const R xa[3] = {xa4.x, xa4.y, xa4.z};
+        for (int k = sub; k < deg; k += SPLIT) {
+            int4 id;
+            R g1[3], g2[3], g3[3], VE, d1[3], d2[3], d3[3];
+            Rec<R>::load(L, base + (int64_t)k * kChunk, id, g1, g2, g3, VE);
+            sub3<R>(ld(work + id.x), xa, d1);
+            sub3<R>(ld(work + id.y), xa, d2);
+            sub3<R>(ld(work + id.z), xa, d3);
+            pair_contrib<MODEL, true>(d1, d2, d3, g1, g2, g3, VE * cmu, VE * clam, f, A);
+        }
+    }
+    if (sub > 0) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) red[cl][sub - 1][q][lane] = f[q];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) red[cl][sub - 1][3 + q][lane] = A[q];
+    }
+    __syncthreads();
+    if (sub != 0 || !valid) return;
+#pragma unroll
+    for (int s = 0; s < SPLIT - 1; ++s) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) f[q] += red[cl][s][q][lane];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) A[q] += red[cl][s][3 + q][lane];
+    }
+    if (FEXT) {
+        const R4 fe = ld(reinterpret_cast<const R4 *>(L.fext) + v);
+        f[0] += fe.x; f[1] += fe.y; f[2] += fe.z;
+    }
+    const R xa[3] = {xa4.x, xa4.y, xa4.z};
+    if (WC) wc_contrib<R, R, true>(L, work, v, xa, f, A);
+    finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
+}
+
+template <class R, int MODEL, int ACCEL, bool FE, bool W>
+cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
+    const R cmu = R(p.cmu), clam = R(p.clam), om = R(s.omega), ga = R(s.gamma);
+    if (s.split <= 1) {
+        dim3 grid((unsigned)((s.n_v + kSweepBlock - 1) / kSweepBlock), (unsigned)p.n_batch);
+        sweep_kernel<R, MODEL, ACCEL, FE, W><<<grid, kSweepBlock, 0, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,
+                                                                            p.x_stride, s.work, s.out, s.hist, cmu,
+                                                                            clam, om, ga);
+        return cudaGetLastError();
+    }
+#define PBNG_SPLIT(S)                                                                                             \
+    do {                                                                                                          \
+        constexpr int B = SplitBlock<S>::n, VPB = B / S;                                                          \
+        dim3 grid((unsigned)((s.n_v + VPB - 1) / VPB), (unsigned)p.n_batch);                                     \
+        sweep_split_kernel<R, MODEL, ACCEL, FE, W, S><<<grid, B, 0, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,    \
+                                                                           p.x_stride, s.work, s.out, s.hist, cmu, \
+                                                                           clam, om, ga);                           \
+    } while (0)
+    if (s.split == 2) PBNG_SPLIT(2);
+    else if (s.split == 8) PBNG_SPLIT(8);
+    else PBNG_SPLIT(4);
+#undef PBNG_SPLIT
+    return cudaGetLastError();
+}
+
 template <class R, int MODEL, int ACCEL>
 cudaError_t sweep_dispatch3(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
-    dim3 grid((unsigned)((s.n_v + kSweepBlock - 1) / kSweepBlock), (unsigned)p.n_batch);
-    const R cmu = R(p.cmu), clam = R(p.clam), om = R(s.omega), ga = R(s.gamma);
-#define PBNG_SWEEP(FE, W)                                                                                     \
-    sweep_kernel<R, MODEL, ACCEL, FE, W><<<grid, kSweepBlock, 0, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,   \
-                                                                        p.x_stride, s.work, s.out, s.hist, cmu, \
-                                                                        clam, om, ga)
     if (p.has_fext) {
-        if (p.has_wc) PBNG_SWEEP(true, true); else PBNG_SWEEP(true, false);
-    } else {
-        if (p.has_wc) PBNG_SWEEP(false, true); else PBNG_SWEEP(false, false);
+        if (p.has_wc) return sweep_dispatch4<R, MODEL, ACCEL, true, true>(p, L, s, st);
+        return sweep_dispatch4<R, MODEL, ACCEL, true, false>(p, L, s, st);
     }
-#undef PBNG_SWEEP
-    return cudaGetLastError();
+    if (p.has_wc) return sweep_dispatch4<R, MODEL, ACCEL, false, true>(p, L, s, st);
+    return sweep_dispatch4<R, MODEL, ACCEL, false, false>(p, L, s, st);
 }
 
 template <class R, int MODEL>
