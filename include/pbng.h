@@ -87,6 +87,9 @@ typedef struct {
     double sweep_bytes;       /* algorithmic HBM bytes of one non-accelerated iteration (all colours, samples) */
     double accel_bytes;       /* extra algorithmic bytes of one SOR / Chebyshev iteration (blend traffic) */
     double sweep_flops;       /* nominal flops of one iteration (per-pair counts) */
+    int64_t n_local_vertices; /* vertices held by this context (owned free + ghosts + held pinned) */
+    int64_t n_ghosts;         /* free vertices owned by other ranks and held here */
+    int32_t rank, n_ranks;
 } pbng_info;
 
 /* Create a mesh context: rest positions X (n_vertices*3 doubles), tets (n_tets*4
@@ -144,6 +147,40 @@ pbng_status pbng_iterate(pbng_ctx *ctx, int32_t n_iterations, pbng_accel accel, 
  * (PAPER.md:926), per sample, accumulated in fp64 in a fixed order (deterministic).  Either output may
  * be NULL.  Synchronises; returns PBNG_E_NONFINITE if a non-finite position was produced. */
 pbng_status pbng_energy_residual(pbng_ctx *ctx, double *energy_out, double *residual_out);
+
+/* ---- fine-grained iteration (domain decomposition drives these; pbng_iterate = loops of them) ---------
+ * pbng_sweep_colour: the colour pass `colour` of the current iteration l, with the
+ * blend of `accel` fused (the same weights as pbng_iterate).  pbng_end_iteration closes iteration l
+ * (x^{l+1} becomes current, l += 1).  Every colour of an iteration must use the same acceleration;
+ * mixing returns PBNG_E_BAD_ORDER, as does pbng_iterate while a colour-by-colour iteration is open. */
+pbng_status pbng_sweep_colour(pbng_ctx *ctx, int32_t colour, pbng_accel accel, double omega, double rho, double gamma);
+pbng_status pbng_end_iteration(pbng_ctx *ctx, pbng_accel accel);
+
+/* ---- domain decomposition -------------------------------------------------------------
+ * pbng_set_partition (before pbng_color): owner[v] in [0, n_ranks) for every vertex; this context is rank
+ * `rank` (n_ranks <= 64; n_ranks == 1 and owner == NULL is the undecomposed default).  The context then
+ * sweeps only its owned free vertices and holds ghost copies of the other vertices its stencils touch;
+ * the colouring stays global (identical on every rank), so iterates equal the undecomposed ones bit for
+ * bit when the halos are exchanged after every colour pass.  Energy is evaluated for the tets /
+ * constraints whose first vertex this rank owns and the residual over owned free vertices, so the
+ * global values are the sum over ranks (energy) and the root of the sum of squares (residual).
+ * pbng_get_positions writes the rows of held vertices; other rows keep the last pbng_set_positions values.
+ *
+ * Halo lists: after colour pass k, this rank sends its owned colour-k vertices held by `peer` and receives
+ * the colour-k vertices owned by `peer` that it holds; both lists are in ascending original index, so
+ * the send list of rank a to b equals the receive list of b from a.  pbng_halo_counts gives the list
+ * lengths, pbng_halo_vertices the original vertex ids (host arrays, either may be NULL).
+ * pbng_halo_pack gathers the send list into `device_buffer` = Real4 [n_batch][n_send][n_fields], fields =
+ * (x_work) or (x_work, x_out, x_hist) for accelerated iterations (n_fields = 3); pbng_halo_unpack
+ * scatters a received buffer into the ghost rows.  Both are asynchronous on the context stream; the
+ * caller moves the buffers between ranks (bench.py / dd.py: NCCL through torch.distributed). */
+pbng_status pbng_set_partition(pbng_ctx *ctx, const int32_t *owner, int32_t rank, int32_t n_ranks);
+pbng_status pbng_halo_counts(pbng_ctx *ctx, int32_t colour, int32_t peer, int64_t *n_send, int64_t *n_recv);
+pbng_status pbng_halo_vertices(pbng_ctx *ctx, int32_t colour, int32_t peer, int32_t *send_vertices,
+                               int32_t *recv_vertices);
+pbng_status pbng_halo_pack(pbng_ctx *ctx, int32_t colour, int32_t peer, int32_t n_fields, void *device_buffer);
+pbng_status pbng_halo_unpack(pbng_ctx *ctx, int32_t colour, int32_t peer, int32_t n_fields,
+                             const void *device_buffer);
 
 /* Wait for the context's stream; PBNG_E_NONFINITE if any iteration produced a non-finite position. */
 pbng_status pbng_synchronize(pbng_ctx *ctx);

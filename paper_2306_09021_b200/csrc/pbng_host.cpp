@@ -108,13 +108,28 @@ struct pbng_ctx {
     std::vector<int32_t> pinned;   // ascending
     std::vector<double> targets;   // [nb][npin][3] in ascending pinned order
     std::vector<pbng_weak_constraint> wc;
-    // colouring + layout
+    // domain decomposition (pbng_set_partition); an empty owner list means one rank owns everything
+    std::vector<int32_t> owner;
+    int32_t rank = 0, n_ranks = 1;
+    // colouring + layout.  Local vertex order: owned free (colour-major) | ghost free | held pinned.
     bool colored = false;
     std::vector<int32_t> colour;
     int32_t ncol = 0;
-    std::vector<int32_t> orig2int, int2orig;
-    int64_t n_free = 0, n_pairs = 0, n_slots = 0, n_chunks = 0, n_vc = 0;
+    std::vector<int32_t> orig2int, int2orig;  // orig2int = -1 for vertices this context does not hold
+    int64_t n_free = 0;        // owned free vertices (the swept set)
+    int64_t n_local_free = 0;  // owned + ghost free vertices
+    int64_t n_local = 0;       // all held vertices
+    int64_t n_pairs = 0, n_slots = 0, n_chunks = 0, n_vc = 0;
+    std::vector<int32_t> local_pinned;  // indices into `pinned` of the held pinned vertices
+    std::vector<int32_t> tet_local;     // tets whose energy this context evaluates (owner of vertex 0)
+    std::vector<int32_t> cons_local;    // constraints held: owned ones (energy) first, then the others
+    int64_t n_cons_owned = 0;
+    std::vector<int64_t> halo_send_off, halo_recv_off;  // [ncol * n_ranks + 1]
+    std::vector<int32_t> h_halo_send, h_halo_recv;      // internal ids, ascending original index
+    std::vector<int32_t> halo_send_orig, halo_recv_orig;  // the same lists as original vertex ids
+    int cur_accel = -1;  // acceleration of the colour passes of the iteration in progress (-1: none yet)
     std::vector<int32_t> col_vbegin, col_nfree;
+    std::vector<int64_t> gcol_nfree;  // free vertices per colour over the whole mesh (all ranks)
     std::vector<int64_t> col_chunk;
     // host images of the device arrays (uploaded by bind)
     std::vector<int4> h_rec_id;
@@ -128,7 +143,7 @@ struct pbng_ctx {
     // workspace plan
     Region r_rec_id, r_rec_a, r_rec_b, r_rec_c, r_chunk_off, r_chunk_v, r_deg, r_fext, r_wc_off, r_wc_cid, r_wc_d,
         r_c_n, r_c_node, r_c_w, r_c_anchor, r_c_K, r_tet_id, r_tet_a, r_tet_b, r_tet_c, r_int2orig, r_targets,
-        r_x[3], r_stage, r_part_e, r_part_r, r_results, r_flag;
+        r_x[3], r_stage, r_part_e, r_part_r, r_results, r_flag, r_halo_send, r_halo_recv;
     size_t ws_need = 0;
     // bound device state
     bool bound = false;
@@ -218,7 +233,7 @@ pbng_status colour_greedy(pbng_ctx *c, const std::vector<int64_t> &vs_off, const
 
 template <class R>
 void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::vector<int32_t> &vt) {
-    const int64_t nv = c->nv, nt = c->nt, nb = c->nb;
+    const int64_t nv = c->nv, nb = c->nb;
     const size_t s = sizeof(R), s4 = 4 * sizeof(R);
     const double cmu = 1.0 / (2.0 * (1.0 + c->nu));
     const double clam = c->nu / ((1.0 + c->nu) * (1.0 - 2.0 * c->nu));
@@ -308,16 +323,22 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
             put4<R>(c->h_fext, i, m * c->grav[0], m * c->grav[1], m * c->grav[2], 0.0);
         }
 
-    // weak constraints: distinct nodes with combined weights w0_j - w1_j; per free vertex CSR
-    const int64_t nwc = (int64_t)c->wc.size();
-    c->h_c_n.assign((size_t)std::max<int64_t>(nwc, 1), 0);
-    c->h_c_node.assign((size_t)std::max<int64_t>(nwc, 1) * kWcMaxNodes, 0);
-    c->h_c_w.assign((size_t)std::max<int64_t>(nwc, 1) * kWcMaxNodes * s, 0);
-    c->h_c_anchor.assign((size_t)std::max<int64_t>(nwc, 1) * s4, 0);
-    c->h_c_K.assign((size_t)std::max<int64_t>(nwc, 1) * kWcMaxNodes * s, 0);
+    // weak constraints held by this context (owned first): distinct nodes with combined weights
+    // w0_j - w1_j; per owned free vertex the list of (constraint, w0_i - w1_i) in input order
+    const int64_t ncl = (int64_t)c->cons_local.size();
+    const int64_t ncap = std::max<int64_t>(ncl, 1);
+    c->h_c_n.assign((size_t)ncap, 0);
+    c->h_c_node.assign((size_t)ncap * kWcMaxNodes, 0);
+    c->h_c_w.assign((size_t)ncap * kWcMaxNodes * s, 0);
+    c->h_c_anchor.assign((size_t)ncap * s4, 0);
+    c->h_c_K.assign((size_t)ncap * kWcMaxNodes * s, 0);
+    std::vector<std::pair<int32_t, int32_t>> by_gid;  // (global id, local id), ascending global id
+    for (int64_t li = 0; li < ncl; ++li) by_gid.push_back({c->cons_local[li], (int32_t)li});
+    std::sort(by_gid.begin(), by_gid.end());
     std::vector<std::vector<std::pair<int32_t, double>>> per_v((size_t)c->n_free);
-    for (int64_t ci = 0; ci < nwc; ++ci) {
-        const pbng_weak_constraint &w = c->wc[ci];
+    for (const auto &gl : by_gid) {
+        const int32_t li = gl.second;
+        const pbng_weak_constraint &w = c->wc[gl.first];
         int32_t nodes[kWcMaxNodes];
         double wt[kWcMaxNodes];
         int nn = 0;
@@ -330,15 +351,15 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
         };
         for (int q = 0; q < w.n0; ++q) add(w.idx0[q], w.w0[q]);
         for (int q = 0; q < w.n1; ++q) add(w.idx1[q], -w.w1[q]);
-        c->h_c_n[ci] = nn;
+        c->h_c_n[li] = nn;
         for (int q = 0; q < nn; ++q) {
-            c->h_c_node[kWcMaxNodes * ci + q] = c->orig2int[nodes[q]];
-            put1<R>(c->h_c_w, kWcMaxNodes * ci + q, wt[q]);
             const int32_t vi = c->orig2int[nodes[q]];
-            if (vi < c->n_free) per_v[vi].push_back({(int32_t)ci, wt[q]});
+            c->h_c_node[kWcMaxNodes * li + q] = vi;
+            put1<R>(c->h_c_w, kWcMaxNodes * li + q, wt[q]);
+            if (vi >= 0 && vi < c->n_free) per_v[vi].push_back({li, wt[q]});
         }
-        if (w.n1 == 0) put4<R>(c->h_c_anchor, ci, w.anchor[0], w.anchor[1], w.anchor[2], 0.0);
-        for (int q = 0; q < 6; ++q) put1<R>(c->h_c_K, kWcMaxNodes * ci + q, w.K[q]);
+        if (w.n1 == 0) put4<R>(c->h_c_anchor, li, w.anchor[0], w.anchor[1], w.anchor[2], 0.0);
+        for (int q = 0; q < 6; ++q) put1<R>(c->h_c_K, kWcMaxNodes * li + q, w.K[q]);
     }
     c->h_wc_off.assign((size_t)c->n_free + 1, 0);
     for (int64_t i = 0; i < c->n_free; ++i) c->h_wc_off[i + 1] = c->h_wc_off[i] + (int32_t)per_v[i].size();
@@ -351,48 +372,51 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
             put1<R>(c->h_wc_d, c->h_wc_off[i] + q, per_v[i][q].second);
         }
 
-    // tet records for the energy pass
-    const int64_t ntr = std::max<int64_t>(nt, 1);
+    // tet records for the energy pass (the tets this context owns)
+    const int64_t ntl = (int64_t)c->tet_local.size();
+    const int64_t ntr = std::max<int64_t>(ntl, 1);
     c->h_tet_id.assign((size_t)ntr, make_int4(0, 0, 0, 0));
     c->h_tet_a.assign((size_t)ntr * s4, 0);
     c->h_tet_b.assign((size_t)ntr * s4, 0);
     c->h_tet_c.assign((size_t)ntr * s4, 0);
-    for (int64_t e = 0; e < nt; ++e) {
+    for (int64_t q = 0; q < ntl; ++q) {
+        const int64_t e = c->tet_local[q];
         const int32_t *t = c->tets.data() + 4 * e;
         const double *B = c->Bm.data() + 9 * e;
-        c->h_tet_id[e] = make_int4(c->orig2int[t[0]], c->orig2int[t[1]], c->orig2int[t[2]], c->orig2int[t[3]]);
-        put4<R>(c->h_tet_a, e, B[0], B[1], B[2], B[3]);
-        put4<R>(c->h_tet_b, e, B[4], B[5], B[6], B[7]);
-        put4<R>(c->h_tet_c, e, B[8], c->V[e] * Ee(e), c->V[e], 0.0);
+        c->h_tet_id[q] = make_int4(c->orig2int[t[0]], c->orig2int[t[1]], c->orig2int[t[2]], c->orig2int[t[3]]);
+        put4<R>(c->h_tet_a, q, B[0], B[1], B[2], B[3]);
+        put4<R>(c->h_tet_b, q, B[4], B[5], B[6], B[7]);
+        put4<R>(c->h_tet_c, q, B[8], c->V[e] * Ee(e), c->V[e], 0.0);
     }
 
-    // Dirichlet targets as Real4 [nb][npin]
-    const int64_t np = (int64_t)c->pinned.size();
-    c->h_targets.assign((size_t)std::max<int64_t>(nb * np, 1) * s4, 0);
+    // Dirichlet targets of the held pinned vertices as Real4 [nb][n_pinned_local]
+    const int64_t np = (int64_t)c->pinned.size(), npl = (int64_t)c->local_pinned.size();
+    c->h_targets.assign((size_t)std::max<int64_t>(nb * npl, 1) * s4, 0);
     for (int64_t b = 0; b < nb; ++b)
-        for (int64_t k = 0; k < np; ++k) {
-            const double *t = c->targets.data() + 3 * (b * np + k);
-            put4<R>(c->h_targets, b * np + k, t[0], t[1], t[2], 0.0);
+        for (int64_t k = 0; k < npl; ++k) {
+            const double *t = c->targets.data() + 3 * (b * np + c->local_pinned[k]);
+            put4<R>(c->h_targets, b * npl + k, t[0], t[1], t[2], 0.0);
         }
 
     // problem constants
     Problem &p = c->prob;
     p.dtype = c->dtype;
     p.model = c->model;
-    p.n_vertices = nv;
-    p.n_free = c->n_free;
-    p.n_pinned = np;
-    p.n_tets = nt;
-    p.n_cons = nwc;
+    p.n_vertices = c->n_local;
+    p.n_global = nv;
+    p.n_free = c->n_local_free;
+    p.n_pinned = npl;
+    p.n_tets = ntl;
+    p.n_cons = c->n_cons_owned;
     p.n_chunks = n_chunks;
     p.n_batch = c->nb;
-    p.x_stride = (int64_t)align_up((size_t)nv, 64);
+    p.x_stride = (int64_t)align_up((size_t)std::max<int64_t>(c->n_local, 1), 64);
     p.cmu = cmu;
     p.clam = clam;
     for (int k = 0; k < 3; ++k) p.rho_g[k] = c->density * c->grav[k];
     p.has_fext = has_fext;
     p.has_wc = c->n_vc > 0;
-    const int64_t items = nt + nwc;
+    const int64_t items = ntl + c->n_cons_owned;
     p.ge = (int)std::max<int64_t>(1, std::min<int64_t>((items + kRedBlock - 1) / kRedBlock, 1184));
     p.gr = (int)std::max<int64_t>(1, std::min<int64_t>((n_chunks * kChunk + kRedBlock - 1) / kRedBlock, 1184));
 }
@@ -427,7 +451,7 @@ void plan_workspace(pbng_ctx *c) {
     take(c->r_tet_a, c->h_tet_a.size());
     take(c->r_tet_b, c->h_tet_b.size());
     take(c->r_tet_c, c->h_tet_c.size());
-    take(c->r_int2orig, (size_t)c->nv * 4);
+    take(c->r_int2orig, (size_t)std::max<int64_t>(c->n_local, 1) * 4);
     take(c->r_targets, c->h_targets.size());
     for (int k = 0; k < 3; ++k) take(c->r_x[k], (size_t)c->nb * (size_t)p.x_stride * s4);
     take(c->r_stage, (size_t)c->nb * (size_t)c->nv * 3 * s);
@@ -435,6 +459,8 @@ void plan_workspace(pbng_ctx *c) {
     take(c->r_part_r, (size_t)c->nb * p.gr * 8);
     take(c->r_results, (size_t)c->nb * 2 * 8);
     take(c->r_flag, 4);
+    take(c->r_halo_send, std::max<size_t>(c->h_halo_send.size(), 1) * 4);
+    take(c->r_halo_recv, std::max<size_t>(c->h_halo_recv.size(), 1) * 4);
     c->ws_need = off;
 }
 
@@ -447,7 +473,7 @@ double sweep_bytes_model(const pbng_ctx *c) {
     double b = (double)c->n_pairs * rec + (double)(c->n_chunks + 1) * 8.0 + (double)c->n_free * 4.0;
     double per_v = 3 * s;  // write x_PBNG
     per_v += (c->prob.has_fext ? 3 * s : 0);
-    b += (double)c->nb * ((double)c->n_free * per_v + (double)c->nv * 3 * s);
+    b += (double)c->nb * ((double)c->n_free * per_v + (double)c->n_local * 3 * s);
     return b;
 }
 
@@ -464,7 +490,7 @@ int choose_split(const pbng_ctx *c, int64_t n_v) {
         return e ? atoi(e) : 0;
     }();
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
-    const int64_t threads = n_v * c->nb;
+    const int64_t threads = n_v * c->nb;  // n_v: the colour's GLOBAL free count (same split on every rank)
     if (c->model == MODEL_FCR) return 4;
     if (threads < 148 * 512) return 4;
     if (threads < 148 * 1024) return 2;
@@ -500,6 +526,55 @@ cudaError_t timed_sweep(pbng_ctx *c, const SweepLaunch &s) {
     c->ev_used.push_back(ev);
     c->ev_launches.push_back(1);
     return e;
+}
+
+pbng_status check_iterate(pbng_ctx *c, pbng_accel accel, double omega, double rho, double gamma, const char *who) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    const std::string w(who);
+    if (!c->positions_set) return fail(PBNG_E_BAD_ORDER, w + ": set_positions first");
+    if (accel != PBNG_ACCEL_NONE && accel != PBNG_ACCEL_SOR && accel != PBNG_ACCEL_CHEBYSHEV)
+        return fail(PBNG_E_INVALID_ARGUMENT, w + ": unknown acceleration");
+    if (accel == PBNG_ACCEL_SOR && !(omega > 0.0 && omega < 2.0))
+        return fail(PBNG_E_INVALID_ARGUMENT, w + ": SOR omega must be in (0, 2)");
+    if (accel == PBNG_ACCEL_CHEBYSHEV && (!(rho >= 0.0 && rho < 1.0) || !(gamma > 0.0 && gamma <= 2.0)))
+        return fail(PBNG_E_INVALID_ARGUMENT, w + ": Chebyshev needs rho in [0,1) and gamma in (0,2]");
+    if (accel != PBNG_ACCEL_NONE && !c->hist_valid)
+        return fail(PBNG_E_BAD_ORDER, w + ": x^{l-1} was not kept by non-accelerated iterations; call set_positions");
+    return PBNG_OK;
+}
+
+// one colour pass of iteration l with the blend weights of PAPER.md:605-616
+cudaError_t sweep_colour_impl(pbng_ctx *c, int32_t col, pbng_accel accel, double omega, double rho, double gamma,
+                              int64_t *launched) {
+    SweepLaunch s;
+    s.accel = accel;
+    s.work = c->work;
+    s.out = c->out;
+    s.hist = c->hist;
+    if (accel == PBNG_ACCEL_SOR) {
+        s.omega = omega;
+    } else if (accel == PBNG_ACCEL_CHEBYSHEV) {
+        s.omega = chebyshev_weight(c->l + 1, rho);
+        s.gamma = gamma;
+    }
+    s.v_begin = c->col_vbegin[col];
+    s.n_v = c->col_nfree[col];
+    s.chunk_begin = c->col_chunk[col];
+    s.split = choose_split(c, c->gcol_nfree[col]);
+    if (s.n_v == 0) return cudaSuccess;
+    cudaError_t e = timed_sweep(c, s);
+    c->launches += 1;
+    *launched += 1;
+    return e;
+}
+
+// after the last colour: x^{l+1} becomes the working buffer (accelerated), l += 1
+void end_iteration_impl(pbng_ctx *c, pbng_accel accel) {
+    if (accel != PBNG_ACCEL_NONE) std::swap(c->work, c->out);
+    else c->hist_valid = false;
+    c->l += 1;
+    c->cur_accel = -1;
 }
 
 }  // namespace
@@ -713,22 +788,105 @@ pbng_status pbng_color(pbng_ctx *c, int32_t *colour_out, int32_t *n_colours_out)
         c->colour.assign((size_t)nv, 0);
         pbng_status st = colour_greedy(c, vs_off, vs);
         if (st != PBNG_OK) return st;
-        // permutation: free vertices colour-major (ascending original index within a colour), then pinned
+        // ---- which vertices this context holds (domain decomposition; one rank = everything) ----------
+        // need[v] = ranks that hold v: a rank holds every vertex of a stencil touching one of its free
+        // vertices, and the vertices of the tets / constraints whose energy it evaluates (owner of the
+        // first vertex).  The colouring above is global, identical on every rank.
+        const int32_t me = c->rank, nranks = c->n_ranks;
+        std::vector<int32_t> own = c->owner.empty() ? std::vector<int32_t>((size_t)nv, 0) : c->owner;
+        std::vector<uint64_t> need((size_t)nv, 0ull);
+        auto bit = [](int32_t r) { return 1ull << r; };
+        for (int64_t e = 0; e < nt; ++e) {
+            const int32_t *t = c->tets.data() + 4 * e;
+            uint64_t m = bit(own[t[0]]);
+            for (int a = 0; a < 4; ++a)
+                if (!is_pinned[t[a]]) m |= bit(own[t[a]]);
+            for (int a = 0; a < 4; ++a) need[t[a]] |= m;
+        }
+        for (int64_t q = 0; q < nwc; ++q) {
+            uint64_t m = bit(own[c->wc[q].idx0[0]]);
+            for (int32_t v : cnodes[q])
+                if (!is_pinned[v]) m |= bit(own[v]);
+            for (int32_t v : cnodes[q]) need[v] |= m;
+        }
+        for (int64_t v = 0; v < nv; ++v) {
+            if (!is_pinned[v]) need[v] |= bit(own[v]);
+            else if (nranks == 1) need[v] |= 1ull;
+        }
+        auto held = [&](int64_t v) { return ((need[v] >> me) & 1ull) != 0; };
+        // permutation: owned free vertices colour-major | ghost free vertices | held pinned vertices
         c->col_vbegin.assign(c->ncol + 1, 0);
         c->col_nfree.assign(c->ncol, 0);
+        c->gcol_nfree.assign(c->ncol, 0);
         for (int64_t v = 0; v < nv; ++v)
-            if (!is_pinned[v]) c->col_nfree[c->colour[v]]++;
+            if (!is_pinned[v]) {
+                c->gcol_nfree[c->colour[v]]++;
+                if (own[v] == me) c->col_nfree[c->colour[v]]++;
+            }
         for (int32_t k = 0; k < c->ncol; ++k) c->col_vbegin[k + 1] = c->col_vbegin[k] + c->col_nfree[k];
         c->n_free = c->col_vbegin[c->ncol];
-        c->orig2int.assign((size_t)nv, 0);
-        c->int2orig.assign((size_t)nv, 0);
+        c->orig2int.assign((size_t)nv, -1);
+        c->int2orig.assign((size_t)c->n_free, 0);
         {
             std::vector<int32_t> fill(c->col_vbegin.begin(), c->col_vbegin.end() - 1);
-            int32_t pin_next = (int32_t)c->n_free;
+            for (int64_t v = 0; v < nv; ++v)
+                if (!is_pinned[v] && own[v] == me) {
+                    const int32_t i = fill[c->colour[v]]++;
+                    c->orig2int[v] = i;
+                    c->int2orig[i] = (int32_t)v;
+                }
+            for (int64_t v = 0; v < nv; ++v)
+                if (!is_pinned[v] && own[v] != me && held(v)) {
+                    c->orig2int[v] = (int32_t)c->int2orig.size();
+                    c->int2orig.push_back((int32_t)v);
+                }
+            c->n_local_free = (int64_t)c->int2orig.size();
+            c->local_pinned.clear();
+            for (size_t k = 0; k < c->pinned.size(); ++k)
+                if (held(c->pinned[k])) {
+                    c->orig2int[c->pinned[k]] = (int32_t)c->int2orig.size();
+                    c->int2orig.push_back(c->pinned[k]);
+                    c->local_pinned.push_back((int32_t)k);
+                }
+            c->n_local = (int64_t)c->int2orig.size();
+        }
+        // energy ownership: tets and constraints by the owner of their first vertex
+        c->tet_local.clear();
+        for (int64_t e = 0; e < nt; ++e)
+            if (own[c->tets[4 * e]] == me) c->tet_local.push_back((int32_t)e);
+        c->cons_local.clear();
+        for (int64_t q = 0; q < nwc; ++q)
+            if (own[c->wc[q].idx0[0]] == me) c->cons_local.push_back((int32_t)q);
+        c->n_cons_owned = (int64_t)c->cons_local.size();
+        for (int64_t q = 0; q < nwc; ++q) {
+            if (own[c->wc[q].idx0[0]] == me) continue;
+            bool touches = false;
+            for (int32_t v : cnodes[q]) touches |= (!is_pinned[v] && own[v] == me);
+            if (touches) c->cons_local.push_back((int32_t)q);
+        }
+        // halo plan: after colour k, rank `me` sends its owned colour-k vertices held by peer p and
+        // receives the colour-k vertices of p that it holds; both lists ascending in original index
+        c->halo_send_off.assign((size_t)c->ncol * nranks + 1, 0);
+        c->halo_recv_off.assign((size_t)c->ncol * nranks + 1, 0);
+        c->halo_send_orig.clear();
+        c->halo_recv_orig.clear();
+        if (nranks > 1) {
+            std::vector<std::vector<int32_t>> snd((size_t)c->ncol * nranks), rcv((size_t)c->ncol * nranks);
             for (int64_t v = 0; v < nv; ++v) {
-                const int32_t i = is_pinned[v] ? pin_next++ : fill[c->colour[v]]++;
-                c->orig2int[v] = i;
-                c->int2orig[i] = (int32_t)v;
+                if (is_pinned[v]) continue;
+                const int32_t k = c->colour[v];
+                if (own[v] == me) {
+                    for (int32_t p = 0; p < nranks; ++p)
+                        if (p != me && ((need[v] >> p) & 1ull)) snd[(size_t)k * nranks + p].push_back((int32_t)v);
+                } else if (held(v)) {
+                    rcv[(size_t)k * nranks + own[v]].push_back((int32_t)v);
+                }
+            }
+            for (size_t s = 0; s < snd.size(); ++s) {
+                c->halo_send_off[s + 1] = c->halo_send_off[s] + (int64_t)snd[s].size();
+                c->halo_recv_off[s + 1] = c->halo_recv_off[s] + (int64_t)rcv[s].size();
+                c->halo_send_orig.insert(c->halo_send_orig.end(), snd[s].begin(), snd[s].end());
+                c->halo_recv_orig.insert(c->halo_recv_orig.end(), rcv[s].begin(), rcv[s].end());
             }
         }
         // Within a colour the update order is free (same-coloured vertices share no stencil, PAPER.md:
@@ -757,6 +915,10 @@ pbng_status pbng_color(pbng_ctx *c, int32_t *colour_out, int32_t *n_colours_out)
                 for (int32_t q = 0; q < c->col_nfree[col]; ++q) c->orig2int[b[q]] = c->col_vbegin[col] + q;
             }
         }
+        c->h_halo_send.resize(c->halo_send_orig.size());
+        c->h_halo_recv.resize(c->halo_recv_orig.size());
+        for (size_t q = 0; q < c->halo_send_orig.size(); ++q) c->h_halo_send[q] = c->orig2int[c->halo_send_orig[q]];
+        for (size_t q = 0; q < c->halo_recv_orig.size(); ++q) c->h_halo_recv[q] = c->orig2int[c->halo_recv_orig[q]];
         if (c->dtype == DT_F64) build_layout<double>(c, vt_off, vt);
         else build_layout<float>(c, vt_off, vt);
         plan_workspace(c);
@@ -817,6 +979,8 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     L.part_r = static_cast<double *>(at(c->r_part_r));
     L.results = static_cast<double *>(at(c->r_results));
     L.flag = static_cast<int32_t *>(at(c->r_flag));
+    L.halo_send = static_cast<const int32_t *>(at(c->r_halo_send));
+    L.halo_recv = static_cast<const int32_t *>(at(c->r_halo_recv));
     auto up = [&](const Region &r, const void *src, size_t n) -> cudaError_t {
         if (n == 0) return cudaSuccess;
         return cudaMemcpyAsync(base + r.off, src, n, cudaMemcpyHostToDevice, c->stream);
@@ -844,6 +1008,8 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     chk(up(c->r_tet_b, c->h_tet_b.data(), c->h_tet_b.size()));
     chk(up(c->r_tet_c, c->h_tet_c.data(), c->h_tet_c.size()));
     chk(up(c->r_int2orig, c->int2orig.data(), c->int2orig.size() * 4));
+    chk(up(c->r_halo_send, c->h_halo_send.data(), c->h_halo_send.size() * 4));
+    chk(up(c->r_halo_recv, c->h_halo_recv.data(), c->h_halo_recv.size() * 4));
     chk(up(c->r_targets, c->h_targets.data(), c->h_targets.size()));
     chk(cudaMemsetAsync(base + c->r_flag.off, 0, 4, c->stream));
     chk(cudaStreamSynchronize(c->stream));
@@ -872,6 +1038,7 @@ pbng_status pbng_set_positions(pbng_ctx *c, const void *x) {
     c->l = 0;
     c->hist_valid = true;
     c->positions_set = true;
+    c->cur_accel = -1;
     return PBNG_OK;
 }
 
@@ -896,18 +1063,10 @@ pbng_status pbng_get_positions(pbng_ctx *c, void *x_out) {
 }
 
 pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, double omega, double rho, double gamma) {
-    pbng_status st = require_device(c);
+    pbng_status st = check_iterate(c, accel, omega, rho, gamma, "iterate");
     if (st != PBNG_OK) return st;
-    if (!c->positions_set) return fail(PBNG_E_BAD_ORDER, "iterate: set_positions first");
     if (n_iterations < 0) return fail(PBNG_E_INVALID_ARGUMENT, "iterate: negative iteration count");
-    if (accel != PBNG_ACCEL_NONE && accel != PBNG_ACCEL_SOR && accel != PBNG_ACCEL_CHEBYSHEV)
-        return fail(PBNG_E_INVALID_ARGUMENT, "iterate: unknown acceleration");
-    if (accel == PBNG_ACCEL_SOR && !(omega > 0.0 && omega < 2.0))
-        return fail(PBNG_E_INVALID_ARGUMENT, "iterate: SOR omega must be in (0, 2)");
-    if (accel == PBNG_ACCEL_CHEBYSHEV && (!(rho >= 0.0 && rho < 1.0) || !(gamma > 0.0 && gamma <= 2.0)))
-        return fail(PBNG_E_INVALID_ARGUMENT, "iterate: Chebyshev needs rho in [0,1) and gamma in (0,2]");
-    if (accel != PBNG_ACCEL_NONE && !c->hist_valid)
-        return fail(PBNG_E_BAD_ORDER, "iterate: x^{l-1} was not kept by non-accelerated iterations; call set_positions");
+    if (c->cur_accel >= 0) return fail(PBNG_E_BAD_ORDER, "iterate: an iteration started by pbng_sweep_colour is open");
     DevGuard g(c->device);
     std::pair<cudaEvent_t, cudaEvent_t> span;
     const bool span_prof = c->profiling == 2 && n_iterations > 0;
@@ -917,30 +1076,10 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
         PBNG_CUDA(cudaEventRecord(span.first, c->stream), "iterate: event");
     }
     for (int32_t it = 0; it < n_iterations; ++it) {
-        SweepLaunch s;
-        s.accel = accel;
-        s.work = c->work;
-        s.out = c->out;
-        s.hist = c->hist;
-        if (accel == PBNG_ACCEL_SOR) {
-            s.omega = omega;
-        } else if (accel == PBNG_ACCEL_CHEBYSHEV) {
-            s.omega = chebyshev_weight(c->l + 1, rho);
-            s.gamma = gamma;
-        }
         for (int32_t col = 0; col < c->ncol; ++col) {
-            s.v_begin = c->col_vbegin[col];
-            s.n_v = c->col_nfree[col];
-            s.chunk_begin = c->col_chunk[col];
-            s.split = choose_split(c, s.n_v);
-            if (s.n_v == 0) continue;
-            PBNG_CUDA(timed_sweep(c, s), "iterate: sweep kernel");
-            c->launches += 1;
-            span_launches += 1;
+            PBNG_CUDA(sweep_colour_impl(c, col, accel, omega, rho, gamma, &span_launches), "iterate: sweep kernel");
         }
-        if (accel != PBNG_ACCEL_NONE) std::swap(c->work, c->out);
-        else c->hist_valid = false;
-        c->l += 1;
+        end_iteration_impl(c, accel);
     }
     if (span_prof) {
         PBNG_CUDA(cudaEventRecord(span.second, c->stream), "iterate: event");
@@ -948,6 +1087,115 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
         c->ev_launches.push_back(span_launches);
     }
     return PBNG_OK;
+}
+
+pbng_status pbng_sweep_colour(pbng_ctx *c, int32_t colour, pbng_accel accel, double omega, double rho, double gamma) {
+    pbng_status st = check_iterate(c, accel, omega, rho, gamma, "sweep_colour");
+    if (st != PBNG_OK) return st;
+    if (colour < 0 || colour >= c->ncol) return fail(PBNG_E_INVALID_ARGUMENT, "sweep_colour: colour out of range");
+    if (c->cur_accel >= 0 && c->cur_accel != (int)accel)
+        return fail(PBNG_E_BAD_ORDER, "sweep_colour: acceleration changed within an iteration");
+    DevGuard g(c->device);
+    int64_t n = 0;
+    PBNG_CUDA(sweep_colour_impl(c, colour, accel, omega, rho, gamma, &n), "sweep_colour: sweep kernel");
+    c->cur_accel = (int)accel;
+    return PBNG_OK;
+}
+
+pbng_status pbng_end_iteration(pbng_ctx *c, pbng_accel accel) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    if (c->cur_accel < 0 || c->cur_accel != (int)accel)
+        return fail(PBNG_E_BAD_ORDER, "end_iteration: no colour pass of this acceleration is open");
+    end_iteration_impl(c, accel);
+    return PBNG_OK;
+}
+
+pbng_status pbng_set_partition(pbng_ctx *c, const int32_t *owner, int32_t rank, int32_t n_ranks) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    if (n_ranks < 1 || n_ranks > 64 || rank < 0 || rank >= n_ranks)
+        return fail(PBNG_E_INVALID_ARGUMENT, "set_partition: need 1 <= n_ranks <= 64 and 0 <= rank < n_ranks");
+    if (n_ranks > 1 && !owner) return fail(PBNG_E_INVALID_ARGUMENT, "set_partition: owner is null");
+    try {
+        std::vector<int32_t> o;
+        if (n_ranks > 1) {
+            o.assign(owner, owner + c->nv);
+            for (int64_t v = 0; v < c->nv; ++v)
+                if (o[v] < 0 || o[v] >= n_ranks)
+                    return fail(PBNG_E_INDEX_OUT_OF_RANGE, "set_partition: owner rank out of range at vertex " + std::to_string(v));
+        }
+        c->owner.swap(o);
+    } catch (const std::bad_alloc &) {
+        return fail(PBNG_E_OUT_OF_MEMORY, "set_partition: host allocation");
+    }
+    c->rank = rank;
+    c->n_ranks = n_ranks;
+    c->invalidate_colouring();
+    return PBNG_OK;
+}
+
+static pbng_status halo_segment(pbng_ctx *c, int32_t colour, int32_t peer, size_t *seg, const char *who) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    if (!c->colored) return fail(PBNG_E_NOT_COLORED, std::string(who) + ": call pbng_color first");
+    if (colour < 0 || colour >= c->ncol || peer < 0 || peer >= c->n_ranks)
+        return fail(PBNG_E_INVALID_ARGUMENT, std::string(who) + ": colour or peer out of range");
+    *seg = (size_t)colour * (size_t)c->n_ranks + (size_t)peer;
+    return PBNG_OK;
+}
+
+pbng_status pbng_halo_counts(pbng_ctx *c, int32_t colour, int32_t peer, int64_t *n_send, int64_t *n_recv) {
+    size_t seg = 0;
+    pbng_status st = halo_segment(c, colour, peer, &seg, "halo_counts");
+    if (st != PBNG_OK) return st;
+    const bool dd = c->n_ranks > 1;
+    if (n_send) *n_send = dd ? c->halo_send_off[seg + 1] - c->halo_send_off[seg] : 0;
+    if (n_recv) *n_recv = dd ? c->halo_recv_off[seg + 1] - c->halo_recv_off[seg] : 0;
+    return PBNG_OK;
+}
+
+pbng_status pbng_halo_vertices(pbng_ctx *c, int32_t colour, int32_t peer, int32_t *send_vertices, int32_t *recv_vertices) {
+    size_t seg = 0;
+    pbng_status st = halo_segment(c, colour, peer, &seg, "halo_vertices");
+    if (st != PBNG_OK) return st;
+    if (c->n_ranks == 1) return PBNG_OK;
+    if (send_vertices)
+        std::copy(c->halo_send_orig.begin() + c->halo_send_off[seg], c->halo_send_orig.begin() + c->halo_send_off[seg + 1],
+                  send_vertices);
+    if (recv_vertices)
+        std::copy(c->halo_recv_orig.begin() + c->halo_recv_off[seg], c->halo_recv_orig.begin() + c->halo_recv_off[seg + 1],
+                  recv_vertices);
+    return PBNG_OK;
+}
+
+static pbng_status halo_io(pbng_ctx *c, int32_t colour, int32_t peer, int32_t n_fields, const void *buf, bool pack) {
+    const char *who = pack ? "halo_pack" : "halo_unpack";
+    size_t seg = 0;
+    pbng_status st = halo_segment(c, colour, peer, &seg, who);
+    if (st != PBNG_OK) return st;
+    st = require_device(c);
+    if (st != PBNG_OK) return st;
+    if (!c->positions_set) return fail(PBNG_E_BAD_ORDER, std::string(who) + ": set_positions first");
+    if (n_fields != 1 && n_fields != 3) return fail(PBNG_E_INVALID_ARGUMENT, std::string(who) + ": n_fields must be 1 or 3");
+    if (c->n_ranks == 1) return PBNG_OK;
+    const int64_t off = pack ? c->halo_send_off[seg] : c->halo_recv_off[seg];
+    const int64_t n = (pack ? c->halo_send_off[seg + 1] : c->halo_recv_off[seg + 1]) - off;
+    if (n == 0) return PBNG_OK;
+    if (!buf) return fail(PBNG_E_INVALID_ARGUMENT, std::string(who) + ": null buffer");
+    DevGuard g(c->device);
+    const int bufs[3] = {c->work, c->out, c->hist};
+    cudaError_t e = pack ? launch_halo_pack(c->prob, c->L, c->L.halo_send + off, n, n_fields, bufs, const_cast<void *>(buf), c->stream)
+                         : launch_halo_unpack(c->prob, c->L, c->L.halo_recv + off, n, n_fields, bufs, buf, c->stream);
+    if (e != cudaSuccess) return cuda_fail(e, who);
+    c->launches += 1;
+    return PBNG_OK;
+}
+
+pbng_status pbng_halo_pack(pbng_ctx *c, int32_t colour, int32_t peer, int32_t n_fields, void *device_buffer) {
+    return halo_io(c, colour, peer, n_fields, device_buffer, true);
+}
+
+pbng_status pbng_halo_unpack(pbng_ctx *c, int32_t colour, int32_t peer, int32_t n_fields, const void *device_buffer) {
+    return halo_io(c, colour, peer, n_fields, device_buffer, false);
 }
 
 pbng_status pbng_synchronize(pbng_ctx *c) {
@@ -996,6 +1244,8 @@ pbng_status pbng_query(pbng_ctx *c, pbng_info *info) {
     info->model = c->model;
     info->iteration = c->l;
     info->kernel_launches = c->launches;
+    info->rank = c->rank;
+    info->n_ranks = c->n_ranks;
     if (c->colored) {
         info->n_free = c->n_free;
         info->n_pairs = c->n_pairs;
@@ -1005,6 +1255,8 @@ pbng_status pbng_query(pbng_ctx *c, pbng_info *info) {
         info->accel_bytes = accel_bytes_model(c);
         const double per_pair = c->model == MODEL_FCR ? 130.0 + 700.0 : 130.0;
         info->sweep_flops = (double)c->nb * ((double)c->n_pairs * per_pair + (double)c->n_free * 40.0);
+        info->n_local_vertices = c->n_local;
+        info->n_ghosts = c->n_local_free - c->n_free;
     }
     return PBNG_OK;
 }

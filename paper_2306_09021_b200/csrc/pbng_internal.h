@@ -57,11 +57,15 @@ struct Layout {
     double *part_r = nullptr;            // [n_batch][gr]
     double *results = nullptr;           // [n_batch][2]
     int32_t *flag = nullptr;             // non-finite flag
+    const int32_t *halo_send = nullptr;  // internal ids of the per-(colour, peer) send lists
+    const int32_t *halo_recv = nullptr;  // internal ids of the per-(colour, peer) receive lists
 };
 
 struct Problem {
     int dtype = DT_F32, model = MODEL_NH;
-    int64_t n_vertices = 0, n_free = 0, n_pinned = 0, n_tets = 0, n_cons = 0, n_chunks = 0;
+    // n_vertices: vertices held by this context (owned free | ghost free | held pinned); n_global: all
+    // vertices of the mesh (the caller's position arrays); n_free: owned + ghost free vertices
+    int64_t n_vertices = 0, n_global = 0, n_free = 0, n_pinned = 0, n_tets = 0, n_cons = 0, n_chunks = 0;
     int32_t n_batch = 1;
     int64_t x_stride = 0;  // Real4 elements between samples
     double cmu = 0, clam = 0;  // mu_e = cmu * E_e, lambda_e = clam * E_e  (eq:lame)
@@ -84,6 +88,11 @@ cudaError_t launch_sweep(const Problem &p, const Layout &L, const SweepLaunch &s
 cudaError_t launch_set_positions(const Problem &p, const Layout &L, int n_buffers, cudaStream_t st);
 cudaError_t launch_get_positions(const Problem &p, const Layout &L, int work, cudaStream_t st);
 cudaError_t launch_energy_residual(const Problem &p, const Layout &L, int work, cudaStream_t st);
+// halo exchange of one (colour, peer) list: buf is Real4 [n_batch][n][n_fields], fields = work (, out, hist)
+cudaError_t launch_halo_pack(const Problem &p, const Layout &L, const int32_t *idx, int64_t n, int n_fields,
+                             const int (&bufs)[3], void *buf, cudaStream_t st);
+cudaError_t launch_halo_unpack(const Problem &p, const Layout &L, const int32_t *idx, int64_t n, int n_fields,
+                               const int (&bufs)[3], const void *buf, cudaStream_t st);
 int kernels_per_energy_residual();
 
 }  // namespace pbng

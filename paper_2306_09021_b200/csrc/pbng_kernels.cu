@@ -543,15 +543,15 @@ cudaError_t sweep_dispatch1(const Problem &p, const Layout &L, const SweepLaunch
 // positions: original <-> internal order
 // ------------------------------------------------------------------------------------------------
 template <class R>
-__global__ void set_positions_kernel(const Layout L, const int64_t nv, const int64_t n_free, const int64_t n_pin,
-                                     const int64_t x_stride, const int nbuf) {
+__global__ void set_positions_kernel(const Layout L, const int64_t nv, const int64_t n_global, const int64_t n_free,
+                                     const int64_t n_pin, const int64_t x_stride, const int nbuf) {
     using R4 = typename RT<R>::R4;
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= nv) return;
     const int64_t b = blockIdx.y;
     R4 val;
     if (v < n_free) {
-        const R *s = reinterpret_cast<const R *>(L.stage) + (b * nv + L.int2orig[v]) * 3;
+        const R *s = reinterpret_cast<const R *>(L.stage) + (b * n_global + L.int2orig[v]) * 3;
         val = mk4<R>(s[0], s[1], s[2]);
     } else {
         val = reinterpret_cast<const R4 *>(L.targets)[b * n_pin + (v - n_free)];
@@ -560,16 +560,45 @@ __global__ void set_positions_kernel(const Layout L, const int64_t nv, const int
 }
 
 template <class R>
-__global__ void get_positions_kernel(const Layout L, const int64_t nv, const int64_t x_stride, const int wi) {
+__global__ void get_positions_kernel(const Layout L, const int64_t nv, const int64_t n_global, const int64_t x_stride,
+                                     const int wi) {
     using R4 = typename RT<R>::R4;
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= nv) return;
     const int64_t b = blockIdx.y;
     const R4 x = reinterpret_cast<const R4 *>(L.xbuf[wi])[b * x_stride + v];
-    R *d = reinterpret_cast<R *>(L.stage) + (b * nv + L.int2orig[v]) * 3;
+    R *d = reinterpret_cast<R *>(L.stage) + (b * n_global + L.int2orig[v]) * 3;
     d[0] = x.x;
     d[1] = x.y;
     d[2] = x.z;
+}
+
+// halo exchange (domain decomposition): pack the listed vertices' work (, out, hist) values into a
+// contiguous [n_batch][n][n_fields] Real4 buffer, or scatter such a buffer into the ghost rows
+template <class R>
+__global__ void halo_pack_kernel(const Layout L, const int32_t *__restrict__ idx, const int64_t n, const int nf,
+                                 const int64_t x_stride, const int b0, const int b1, const int b2, void *buf) {
+    using R4 = typename RT<R>::R4;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t b = blockIdx.y;
+    const int64_t v = b * x_stride + idx[i];
+    R4 *o = reinterpret_cast<R4 *>(buf) + (b * n + i) * nf;
+    const int bb[3] = {b0, b1, b2};
+    for (int k = 0; k < nf; ++k) o[k] = reinterpret_cast<const R4 *>(L.xbuf[bb[k]])[v];
+}
+
+template <class R>
+__global__ void halo_unpack_kernel(const Layout L, const int32_t *__restrict__ idx, const int64_t n, const int nf,
+                                   const int64_t x_stride, const int b0, const int b1, const int b2, const void *buf) {
+    using R4 = typename RT<R>::R4;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t b = blockIdx.y;
+    const int64_t v = b * x_stride + idx[i];
+    const R4 *o = reinterpret_cast<const R4 *>(buf) + (b * n + i) * nf;
+    const int bb[3] = {b0, b1, b2};
+    for (int k = 0; k < nf; ++k) reinterpret_cast<R4 *>(L.xbuf[bb[k]])[v] = o[k];
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -751,20 +780,44 @@ cudaError_t launch_sweep(const Problem &p, const Layout &L, const SweepLaunch &s
 }
 
 cudaError_t launch_set_positions(const Problem &p, const Layout &L, int n_buffers, cudaStream_t st) {
+    if (p.n_vertices <= 0) return cudaSuccess;
     dim3 grid((unsigned)((p.n_vertices + 255) / 256), (unsigned)p.n_batch);
     if (p.dtype == DT_F64)
-        set_positions_kernel<double><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_free, p.n_pinned, p.x_stride, n_buffers);
+        set_positions_kernel<double><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_global, p.n_free, p.n_pinned, p.x_stride, n_buffers);
     else
-        set_positions_kernel<float><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_free, p.n_pinned, p.x_stride, n_buffers);
+        set_positions_kernel<float><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_global, p.n_free, p.n_pinned, p.x_stride, n_buffers);
     return cudaGetLastError();
 }
 
 cudaError_t launch_get_positions(const Problem &p, const Layout &L, int work, cudaStream_t st) {
+    if (p.n_vertices <= 0) return cudaSuccess;
     dim3 grid((unsigned)((p.n_vertices + 255) / 256), (unsigned)p.n_batch);
     if (p.dtype == DT_F64)
-        get_positions_kernel<double><<<grid, 256, 0, st>>>(L, p.n_vertices, p.x_stride, work);
+        get_positions_kernel<double><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_global, p.x_stride, work);
     else
-        get_positions_kernel<float><<<grid, 256, 0, st>>>(L, p.n_vertices, p.x_stride, work);
+        get_positions_kernel<float><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_global, p.x_stride, work);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_pack(const Problem &p, const Layout &L, const int32_t *idx, int64_t n, int n_fields,
+                             const int (&bufs)[3], void *buf, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((n + 255) / 256), (unsigned)p.n_batch);
+    if (p.dtype == DT_F64)
+        halo_pack_kernel<double><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf);
+    else
+        halo_pack_kernel<float><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_unpack(const Problem &p, const Layout &L, const int32_t *idx, int64_t n, int n_fields,
+                               const int (&bufs)[3], const void *buf, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((n + 255) / 256), (unsigned)p.n_batch);
+    if (p.dtype == DT_F64)
+        halo_unpack_kernel<double><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf);
+    else
+        halo_unpack_kernel<float><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf);
     return cudaGetLastError();
 }
 

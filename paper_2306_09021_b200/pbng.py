@@ -25,7 +25,8 @@ ACCEL = {"none": 0, "sor": 1, "chebyshev": 2}
 EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbng_color", "pbng_workspace_bytes",
            "pbng_bind_workspace", "pbng_set_positions", "pbng_get_positions", "pbng_iterate", "pbng_energy_residual",
            "pbng_synchronize", "pbng_query", "pbng_profile_enable", "pbng_profile_read", "pbng_destroy",
-           "pbng_last_error", "pbng_version")
+           "pbng_last_error", "pbng_version", "pbng_sweep_colour", "pbng_end_iteration", "pbng_set_partition",
+           "pbng_halo_counts", "pbng_halo_vertices", "pbng_halo_pack", "pbng_halo_unpack")
 
 WC_DTYPE = np.dtype([("n0", "<i4"), ("n1", "<i4"), ("idx0", "<i4", 4), ("idx1", "<i4", 4), ("w0", "<f8", 4),
                      ("w1", "<f8", 4), ("anchor", "<f8", 3), ("K", "<f8", 6)])
@@ -43,7 +44,8 @@ class Info(C.Structure):
                 ("n_weak_constraints", C.c_int64), ("n_pairs", C.c_int64), ("n_pair_slots", C.c_int64),
                 ("n_batch", C.c_int32), ("n_colours", C.c_int32), ("dtype", C.c_int32), ("model", C.c_int32),
                 ("iteration", C.c_int64), ("kernel_launches", C.c_int64), ("sweep_bytes", C.c_double),
-                ("accel_bytes", C.c_double), ("sweep_flops", C.c_double)]
+                ("accel_bytes", C.c_double), ("sweep_flops", C.c_double), ("n_local_vertices", C.c_int64),
+                ("n_ghosts", C.c_int64), ("rank", C.c_int32), ("n_ranks", C.c_int32)]
 
 
 _lib = None
@@ -75,6 +77,13 @@ def lib():
     L.pbng_profile_enable.argtypes = [vp, C.c_int]
     L.pbng_profile_read.argtypes = [vp, C.POINTER(d), C.POINTER(i64)]
     L.pbng_destroy.argtypes = [vp]
+    L.pbng_sweep_colour.argtypes = [vp, i32, C.c_int, d, d, d]
+    L.pbng_end_iteration.argtypes = [vp, C.c_int]
+    L.pbng_set_partition.argtypes = [vp, vp, i32, i32]
+    L.pbng_halo_counts.argtypes = [vp, i32, i32, C.POINTER(i64), C.POINTER(i64)]
+    L.pbng_halo_vertices.argtypes = [vp, i32, i32, vp, vp]
+    L.pbng_halo_pack.argtypes = [vp, i32, i32, i32, vp]
+    L.pbng_halo_unpack.argtypes = [vp, i32, i32, i32, vp]
     L.pbng_last_error.restype = C.c_char_p
     L.pbng_version.restype = i32
     for name in EXPORTS:
@@ -165,6 +174,7 @@ class Context:
         out = np.empty(self.n_vertices, np.int32)
         n = C.c_int32()
         _check(lib().pbng_color(self._h, _ptr(out), C.byref(n)))
+        self.colours, self.n_colours = out, n.value
         return out, n.value
 
     def workspace_bytes(self) -> int:
@@ -235,6 +245,36 @@ class Context:
         _check(lib().pbng_profile_read(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    # ---- colour-by-colour iteration and domain decomposition -------------------------------------
+    def sweep_colour(self, colour: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0, gamma: float = 1.0):
+        _check(lib().pbng_sweep_colour(self._h, int(colour), ACCEL[accel], float(omega), float(rho), float(gamma)))
+
+    def end_iteration(self, accel: str = "none"):
+        _check(lib().pbng_end_iteration(self._h, ACCEL[accel]))
+
+    def set_partition(self, owner, rank: int, n_ranks: int):
+        owner = _np(owner, np.int32).reshape(-1) if owner is not None else None
+        self._owner = owner
+        _check(lib().pbng_set_partition(self._h, _ptr(owner) if owner is not None else None, int(rank), int(n_ranks)))
+
+    def halo_counts(self, colour: int, peer: int):
+        ns, nr = C.c_int64(), C.c_int64()
+        _check(lib().pbng_halo_counts(self._h, int(colour), int(peer), C.byref(ns), C.byref(nr)))
+        return ns.value, nr.value
+
+    def halo_vertices(self, colour: int, peer: int):
+        ns, nr = self.halo_counts(colour, peer)
+        snd = np.empty(max(ns, 1), np.int32)
+        rcv = np.empty(max(nr, 1), np.int32)
+        _check(lib().pbng_halo_vertices(self._h, int(colour), int(peer), _ptr(snd), _ptr(rcv)))
+        return snd[:ns], rcv[:nr]
+
+    def halo_pack(self, colour: int, peer: int, n_fields: int, buf):
+        _check(lib().pbng_halo_pack(self._h, int(colour), int(peer), int(n_fields), buf.data_ptr()))
+
+    def halo_unpack(self, colour: int, peer: int, n_fields: int, buf):
+        _check(lib().pbng_halo_unpack(self._h, int(colour), int(peer), int(n_fields), buf.data_ptr()))
+
     def close(self):
         h = getattr(self, "_h", None)
         if h is not None and _lib is not None:
@@ -249,11 +289,14 @@ class Context:
 
 
 def context_from_scene(scene, device=0, dtype: Optional[str] = None, stream=None, bind: bool = True,
-                       set_positions: bool = True) -> Context:
-    """Build, colour, bind and initialise a Context for a scenes.Scene (all samples of its batch)."""
+                       set_positions: bool = True, partition=None) -> Context:
+    """Build, colour, bind and initialise a Context for a scenes.Scene (all samples of its batch).
+    partition = (owner, rank, n_ranks) builds the rank-local context of a domain decomposition."""
     ctx = Context(scene.X, scene.tets, n_batch=scene.n_batch, dtype=dtype or scene.dtype, device=device, stream=stream)
     ctx.set_material(scene.model, scene.E, scene.nu, scene.density, scene.gravity)
     ctx.set_constraints(scene.pinned, scene.targets, scene.wc)
+    if partition is not None:
+        ctx.set_partition(*partition)
     ctx.colours, ctx.n_colours = ctx.color()
     if bind and ctx.device >= 0:
         ctx.bind_workspace()
