@@ -346,7 +346,7 @@ def run_ours(args):
                 "free_vertices_per_gpu": q["n_free"] * q["n_batch"], "iterations_per_step": iters,
                 "pairs_per_iteration": q["n_pairs"], "colours": q["n_colours"],
                 "step": "set_positions(x0, device) + iterate + energy_residual",
-                "l2": "inputs larger than L2: %.2f GB of pair records per iteration vs 126 MB L2" % (q["n_pairs"] * (52 if q["dtype"] == 0 else 96) / 1e9),
+                "l2": "inputs larger than L2: %.2f GB of pair records per iteration vs 126 MB L2" % (q["sweep_bytes"] / 1e9),
                 "parallelism": (f"domain decomposition over {world} GPUs (slabs), NCCL halo exchange after every colour"
                                 if decomposed else f"samples sharded over {world} GPUs (no collective)" if args.config == 4
                                 else f"replicas x{world} (independent problems, no collective)"),

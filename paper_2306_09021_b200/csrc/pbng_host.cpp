@@ -55,6 +55,19 @@ double det3(const double *M) {
            M[2] * (M[3] * M[7] - M[4] * M[6]);
 }
 
+// cofactor matrix, cof(M)_ab = d det M / d M_ab (row-major)
+void cof3(const double *M, double *C) {
+    C[0] = M[4] * M[8] - M[5] * M[7];
+    C[1] = M[5] * M[6] - M[3] * M[8];
+    C[2] = M[3] * M[7] - M[4] * M[6];
+    C[3] = M[2] * M[7] - M[1] * M[8];
+    C[4] = M[0] * M[8] - M[2] * M[6];
+    C[5] = M[1] * M[6] - M[0] * M[7];
+    C[6] = M[1] * M[5] - M[2] * M[4];
+    C[7] = M[2] * M[3] - M[0] * M[5];
+    C[8] = M[0] * M[4] - M[1] * M[3];
+}
+
 // Chebyshev weights: omega_m = 1 (m <= 2), 2/(2-rho^2) (m = 3), 4/(4 - rho^2 omega_{m-1})
 double chebyshev_weight(int64_t m, double rho) {
     if (m <= 2) return 1.0;
@@ -78,6 +91,9 @@ uint64_t spread21(uint64_t x) {
     return x;
 }
 uint64_t morton3(uint64_t a, uint64_t b, uint64_t c) { return spread21(a) | spread21(b) << 1 | spread21(c) << 2; }
+
+// sample-minor position layout for large batches (the batched sweep kernel); PBNG_BATCHED=0 disables
+bool batched_layout(const pbng_ctx *c);
 
 // intra-colour vertex order: Morton (default) or ascending index (PBNG_ORDER=index, for experiments)
 bool spatial_order() {
@@ -273,7 +289,10 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     c->h_rec_id.assign((size_t)ns, make_int4(0, 0, 0, 0));
     c->h_rec_a.assign((size_t)ns * s4, 0);
     c->h_rec_b.assign((size_t)ns * s4, 0);
-    c->h_rec_c.assign((size_t)ns * (c->dtype == DT_F64 ? 2 * s : s), 0);
+    const bool nh = c->model == MODEL_NH;
+    // rec_c: FCR g3z (+ VE in fp64); NH: VE in fp64, unused in fp32 (VE rides in rec_id.w)
+    const size_t rec_c_bytes = nh ? (c->dtype == DT_F64 ? s : 0) : (c->dtype == DT_F64 ? 2 * s : s);
+    c->h_rec_c.assign(std::max<size_t>((size_t)ns * rec_c_bytes, s), 0);
     for (int64_t ch = 0; ch < n_chunks; ++ch) {
         const int2 cv = c->h_chunk_v[ch];
         for (int32_t lane = 0; lane < cv.y; ++lane) {
@@ -300,13 +319,30 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
                     std::memcpy(&id.w, &vf, 4);
                 }
                 c->h_rec_id[r] = id;
-                put4<R>(c->h_rec_a, r, g[0][0], g[0][1], g[0][2], g[1][0]);
-                put4<R>(c->h_rec_b, r, g[1][1], g[1][2], g[2][0], g[2][1]);
-                if (c->dtype == DT_F64) {
-                    put1<R>(c->h_rec_c, 2 * r, g[2][2]);
-                    put1<R>(c->h_rec_c, 2 * r + 1, VE);
+                if (nh) {
+                    // compact Neo-Hookean record: u = cof(B) g_i, s_j = g_j . g_i, |g_i|^2, det B, with
+                    // B = rows g_j of the three other vertices (pbng_kernels.cu, Pair<R, MODEL_NH>)
+                    double gi[3], cof[9], u[3], sj[3];
+                    shape_grad(c, e, a, gi);
+                    const double Bp[9] = {g[0][0], g[0][1], g[0][2], g[1][0], g[1][1], g[1][2], g[2][0], g[2][1], g[2][2]};
+                    cof3(Bp, cof);
+                    for (int q2 = 0; q2 < 3; ++q2) {
+                        u[q2] = cof[3 * q2] * gi[0] + cof[3 * q2 + 1] * gi[1] + cof[3 * q2 + 2] * gi[2];
+                        sj[q2] = g[q2][0] * gi[0] + g[q2][1] * gi[1] + g[q2][2] * gi[2];
+                    }
+                    const double gg = gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2];
+                    put4<R>(c->h_rec_a, r, u[0], u[1], u[2], sj[0]);
+                    put4<R>(c->h_rec_b, r, sj[1], sj[2], gg, det3(Bp));
+                    if (c->dtype == DT_F64) put1<R>(c->h_rec_c, r, VE);
                 } else {
-                    put1<R>(c->h_rec_c, r, g[2][2]);
+                    put4<R>(c->h_rec_a, r, g[0][0], g[0][1], g[0][2], g[1][0]);
+                    put4<R>(c->h_rec_b, r, g[1][1], g[1][2], g[2][0], g[2][1]);
+                    if (c->dtype == DT_F64) {
+                        put1<R>(c->h_rec_c, 2 * r, g[2][2]);
+                        put1<R>(c->h_rec_c, 2 * r + 1, VE);
+                    } else {
+                        put1<R>(c->h_rec_c, r, g[2][2]);
+                    }
                 }
             }
         }
@@ -411,6 +447,7 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     p.n_chunks = n_chunks;
     p.n_batch = c->nb;
     p.x_stride = (int64_t)align_up((size_t)std::max<int64_t>(c->n_local, 1), 64);
+    p.lane_shift = batched_layout(c) ? 5 : 0;
     p.cmu = cmu;
     p.clam = clam;
     for (int k = 0; k < 3; ++k) p.rho_g[k] = c->density * c->grav[k];
@@ -453,7 +490,8 @@ void plan_workspace(pbng_ctx *c) {
     take(c->r_tet_c, c->h_tet_c.size());
     take(c->r_int2orig, (size_t)std::max<int64_t>(c->n_local, 1) * 4);
     take(c->r_targets, c->h_targets.size());
-    for (int k = 0; k < 3; ++k) take(c->r_x[k], (size_t)c->nb * (size_t)p.x_stride * s4);
+    const size_t groups = (size_t)((c->nb + (1 << p.lane_shift) - 1) >> p.lane_shift);
+    for (int k = 0; k < 3; ++k) take(c->r_x[k], (groups << p.lane_shift) * (size_t)p.x_stride * s4);
     take(c->r_stage, (size_t)c->nb * (size_t)c->nv * 3 * s);
     take(c->r_part_e, (size_t)c->nb * p.ge * 8);
     take(c->r_part_r, (size_t)c->nb * p.gr * 8);
@@ -469,7 +507,7 @@ double sweep_bytes_model(const pbng_ctx *c) {
     // samples of a batch), chunk offsets, per free vertex and sample: degree, position write, blend
     // traffic (x^{l-1} read, x^{l-1} and x^{l+1} writes) and body force; all positions read once.
     const double s = (double)c->real_size();
-    const double rec = c->dtype == DT_F64 ? 96.0 : 52.0;
+    const double rec = c->model == MODEL_NH ? (c->dtype == DT_F64 ? 88.0 : 48.0) : (c->dtype == DT_F64 ? 96.0 : 52.0);
     double b = (double)c->n_pairs * rec + (double)(c->n_chunks + 1) * 8.0 + (double)c->n_free * 4.0;
     double per_v = 3 * s;  // write x_PBNG
     per_v += (c->prob.has_fext ? 3 * s : 0);
@@ -484,6 +522,14 @@ double accel_bytes_model(const pbng_ctx *c) {
 // Warps per 32-vertex chunk for a colour pass: the fixed-corotated pair (a polar decomposition) is
 // compute-heavy, and small colours leave SMs idle with one thread per vertex, so both split the pair
 // loop over several warps.  PBNG_SPLIT=1|2|4 overrides (experiments).
+bool batched_layout(const pbng_ctx *c) {
+    static const int mode = [] {
+        const char *e = getenv("PBNG_BATCHED");
+        return e ? atoi(e) : 1;
+    }();
+    return mode != 0 && c->nb >= 32;
+}
+
 int choose_split(const pbng_ctx *c, int64_t n_v) {
     static const int forced = [] {
         const char *e = getenv("PBNG_SPLIT");

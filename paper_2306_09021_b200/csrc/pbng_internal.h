@@ -67,7 +67,8 @@ struct Problem {
     // vertices of the mesh (the caller's position arrays); n_free: owned + ghost free vertices
     int64_t n_vertices = 0, n_global = 0, n_free = 0, n_pinned = 0, n_tets = 0, n_cons = 0, n_chunks = 0;
     int32_t n_batch = 1;
-    int64_t x_stride = 0;  // Real4 elements between samples
+    int64_t x_stride = 0;  // vertex slots per sample group (positions: pos_index in pbng_kernels.cu)
+    int lane_shift = 0;    // 0: [n_batch][x_stride]; 5: [n_batch/32][x_stride][32] (batched, n_batch >= 32)
     double cmu = 0, clam = 0;  // mu_e = cmu * E_e, lambda_e = clam * E_e  (eq:lame)
     double rho_g[3] = {0, 0, 0};  // density * gravity (energy's external-work term)
     bool has_fext = false, has_wc = false;

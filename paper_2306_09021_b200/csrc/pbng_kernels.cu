@@ -270,6 +270,18 @@ __device__ __forceinline__ double4 lds(const double4 *p) {
 // record field decode
 template <class R> struct Rec;
 template <> struct Rec<float> {
+    // shared by the 32 lanes of a warp (batched kernel): cached broadcast loads
+    static __device__ __forceinline__ void load_shared(const Layout &L, int64_t r, int4 &id, float (&g1)[3],
+                                                       float (&g2)[3], float (&g3)[3], float &VE) {
+        id = ld(L.rec_id + r);
+        const float4 a = ld(reinterpret_cast<const float4 *>(L.rec_a) + r);
+        const float4 b = ld(reinterpret_cast<const float4 *>(L.rec_b) + r);
+        const float c = ld(reinterpret_cast<const float *>(L.rec_c) + r);
+        g1[0] = a.x; g1[1] = a.y; g1[2] = a.z;
+        g2[0] = a.w; g2[1] = b.x; g2[2] = b.y;
+        g3[0] = b.z; g3[1] = b.w; g3[2] = c;
+        VE = __int_as_float(id.w);
+    }
     static __device__ __forceinline__ void load(const Layout &L, int64_t r, int4 &id, float (&g1)[3], float (&g2)[3],
                                                 float (&g3)[3], float &VE) {
         id = lds(L.rec_id + r);
@@ -283,6 +295,17 @@ template <> struct Rec<float> {
     }
 };
 template <> struct Rec<double> {
+    static __device__ __forceinline__ void load_shared(const Layout &L, int64_t r, int4 &id, double (&g1)[3],
+                                                       double (&g2)[3], double (&g3)[3], double &VE) {
+        id = ld(L.rec_id + r);
+        const double4 a = ld(reinterpret_cast<const double4 *>(L.rec_a) + r);
+        const double4 b = ld(reinterpret_cast<const double4 *>(L.rec_b) + r);
+        const double2 c = ld(reinterpret_cast<const double2 *>(L.rec_c) + r);
+        g1[0] = a.x; g1[1] = a.y; g1[2] = a.z;
+        g2[0] = a.w; g2[1] = b.x; g2[2] = b.y;
+        g3[0] = b.z; g3[1] = b.w; g3[2] = c.x;
+        VE = c.y;
+    }
     static __device__ __forceinline__ void load(const Layout &L, int64_t r, int4 &id, double (&g1)[3], double (&g2)[3],
                                                 double (&g3)[3], double &VE) {
         id = lds(L.rec_id + r);
@@ -296,10 +319,97 @@ template <> struct Rec<double> {
     }
 };
 
+// ------------------------------------------------------------------------------------------------
+// Pair records decoded in registers.  Fixed-corotated needs F itself (for R(F)), so its record carries
+// the three shape-function gradients g_j.  Neo-Hookean only needs F g_i, cof(F) g_i and det F, and with
+// F = Ds B (Ds = [d_1 d_2 d_3], B = rows g_j):
+//   F g_i = sum_j d_j (g_j . g_i),   cof(F) g_i = cof(Ds) (cof(B) g_i) = sum_k u_k c_k,   det F = det Ds det B
+// with c_1 = d_2 x d_3, c_2 = d_3 x d_1, c_3 = d_1 x d_2 (the columns of cof Ds, cof being multiplicative),
+// so its record carries u = cof(B) g_i, s_j = g_j . g_i, |g_i|^2 and det B (precomputed in fp64): 48 B
+// instead of 52 B and about 70 instead of 110 flops per pair.
+// ------------------------------------------------------------------------------------------------
+template <class R, int MODEL> struct Pair;
+template <class R> struct Pair<R, MODEL_FCR> {
+    int4 id;
+    R g1[3], g2[3], g3[3], VE;
+};
+template <class R> struct Pair<R, MODEL_NH> {
+    int4 id;
+    R u[3], s[3], gg, detB, VE;
+};
+
+// STREAM: read-once record (L1::no_allocate); otherwise cached (the batched kernel's broadcast loads)
+template <bool STREAM, class R>
+__device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<R, MODEL_FCR> &p) {
+    if (STREAM) Rec<R>::load(L, r, p.id, p.g1, p.g2, p.g3, p.VE);
+    else Rec<R>::load_shared(L, r, p.id, p.g1, p.g2, p.g3, p.VE);
+}
+template <bool STREAM>
+__device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<float, MODEL_NH> &p) {
+    const float4 *a = reinterpret_cast<const float4 *>(L.rec_a) + r;
+    const float4 *b = reinterpret_cast<const float4 *>(L.rec_b) + r;
+    const int4 id = STREAM ? lds(L.rec_id + r) : ld(L.rec_id + r);
+    const float4 x = STREAM ? lds(a) : ld(a);
+    const float4 y = STREAM ? lds(b) : ld(b);
+    p.id = id;
+    p.u[0] = x.x; p.u[1] = x.y; p.u[2] = x.z; p.s[0] = x.w;
+    p.s[1] = y.x; p.s[2] = y.y; p.gg = y.z; p.detB = y.w;
+    p.VE = __int_as_float(id.w);
+}
+template <bool STREAM>
+__device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<double, MODEL_NH> &p) {
+    const double4 *a = reinterpret_cast<const double4 *>(L.rec_a) + r;
+    const double4 *b = reinterpret_cast<const double4 *>(L.rec_b) + r;
+    const double *c = reinterpret_cast<const double *>(L.rec_c) + r;
+    p.id = STREAM ? lds(L.rec_id + r) : ld(L.rec_id + r);
+    const double4 x = STREAM ? lds(a) : ld(a);
+    const double4 y = STREAM ? lds(b) : ld(b);
+    p.u[0] = x.x; p.u[1] = x.y; p.u[2] = x.z; p.s[0] = x.w;
+    p.s[1] = y.x; p.s[2] = y.y; p.gg = y.z; p.detB = y.w;
+    p.VE = ld(c);
+}
+
+template <bool HESS, class T, class R>
+__device__ __forceinline__ void contrib(const T (&d1)[3], const T (&d2)[3], const T (&d3)[3],
+                                        const Pair<R, MODEL_FCR> &p, T cmu, T clam, T (&f)[3], T (&A)[6]) {
+    const T g1[3] = {T(p.g1[0]), T(p.g1[1]), T(p.g1[2])}, g2[3] = {T(p.g2[0]), T(p.g2[1]), T(p.g2[2])},
+            g3[3] = {T(p.g3[0]), T(p.g3[1]), T(p.g3[2])};
+    pair_contrib<MODEL_FCR, HESS>(d1, d2, d3, g1, g2, g3, T(p.VE) * cmu, T(p.VE) * clam, f, A);
+}
+
+template <bool HESS, class T, class R>
+__device__ __forceinline__ void contrib(const T (&d1)[3], const T (&d2)[3], const T (&d3)[3],
+                                        const Pair<R, MODEL_NH> &p, T cmu, T clam, T (&f)[3], T (&A)[6]) {
+    // columns of cof(Ds)
+    const T c1[3] = {d2[1] * d3[2] - d2[2] * d3[1], d2[2] * d3[0] - d2[0] * d3[2], d2[0] * d3[1] - d2[1] * d3[0]};
+    const T c2[3] = {d3[1] * d1[2] - d3[2] * d1[1], d3[2] * d1[0] - d3[0] * d1[2], d3[0] * d1[1] - d3[1] * d1[0]};
+    const T c3[3] = {d1[1] * d2[2] - d1[2] * d2[1], d1[2] * d2[0] - d1[0] * d2[2], d1[0] * d2[1] - d1[1] * d2[0]};
+    const T J = (d1[0] * c1[0] + d1[1] * c1[1] + d1[2] * c1[2]) * T(p.detB);
+    const T u0 = T(p.u[0]), u1 = T(p.u[1]), u2 = T(p.u[2]), s0 = T(p.s[0]), s1 = T(p.s[1]), s2 = T(p.s[2]);
+    const T Vmu = T(p.VE) * cmu, Vlam = T(p.VE) * clam;
+    const T sc = (Vmu + Vlam) * (J - T(1)) - Vmu;  // lamhat (J - 1) - mu, times V (eq:nh)
+    T w[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        w[r] = u0 * c1[r] + u1 * c2[r] + u2 * c3[r];                   // cof(F) g_i
+        const T Fg = s0 * d1[r] + s1 * d2[r] + s2 * d3[r];             // F g_i
+        f[r] -= Vmu * Fg + sc * w[r];
+    }
+    if (HESS) {
+        const T dg = T(2) * Vmu * T(p.gg);
+        A[0] += dg + Vlam * w[0] * w[0];
+        A[1] += dg + Vlam * w[1] * w[1];
+        A[2] += dg + Vlam * w[2] * w[2];
+        A[3] += Vlam * w[0] * w[1];
+        A[4] += Vlam * w[1] * w[2];
+        A[5] += Vlam * w[0] * w[2];
+    }
+}
+
 // weak-constraint terms for vertex v: f -= d K C_c, A += d^2 K
 template <class R, class T, bool HESS>
-__device__ __forceinline__ void wc_contrib(const Layout &L, const typename RT<R>::R4 *x, int v, const T (&xa)[3],
-                                           T (&f)[3], T (&A)[6]) {
+__device__ __forceinline__ void wc_contrib(const Layout &L, const typename RT<R>::R4 *x, const int sh, int v,
+                                           const T (&xa)[3], T (&f)[3], T (&A)[6]) {
     using R4 = typename RT<R>::R4;
     const int e0 = ld(L.wc_off + v), e1 = ld(L.wc_off + v + 1);
     for (int e = e0; e < e1; ++e) {
@@ -314,7 +424,7 @@ __device__ __forceinline__ void wc_contrib(const Layout &L, const typename RT<R>
             if (node == v) {
                 C[0] += w * xa[0]; C[1] += w * xa[1]; C[2] += w * xa[2];
             } else {
-                const R4 y = ld(x + node);
+                const R4 y = ld(x + ((int64_t)node << sh));
                 C[0] += w * T(y.x); C[1] += w * T(y.y); C[2] += w * T(y.z);
             }
         }
@@ -346,7 +456,7 @@ __device__ __forceinline__ void sub3(const typename RT<R>::R4 &p, const R (&xa)[
 // Cholesky in registers (A is SPD); then the fused acceleration blend and the stores.
 template <class R, int ACCEL>
 __device__ __forceinline__ void finish_vertex(const Layout &L, typename RT<R>::R4 *__restrict__ work, const int64_t xs,
-                                              const int v, const int oi, const int hi,
+                                              const int64_t v, const int oi, const int hi,
                                               const typename RT<R>::R4 &xa4, const R (&f)[3], const R (&A)[6],
                                               const R omega, const R gamma) {
     using R4 = typename RT<R>::R4;
@@ -415,15 +525,15 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_kernel(con
     R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
 
     for (int k = 0; k < deg; ++k) {
-        int4 id;
-        R g1[3], g2[3], g3[3], VE, d1[3], d2[3], d3[3];
-        Rec<R>::load(L, base + (int64_t)k * kChunk, id, g1, g2, g3, VE);
-        sub3<R>(ld(work + id.x), xa, d1);
-        sub3<R>(ld(work + id.y), xa, d2);
-        sub3<R>(ld(work + id.z), xa, d3);
-        pair_contrib<MODEL, true>(d1, d2, d3, g1, g2, g3, VE * cmu, VE * clam, f, A);
+        Pair<R, MODEL> pr;
+        load_pair<true>(L, base + (int64_t)k * kChunk, pr);
+        R d1[3], d2[3], d3[3];
+        sub3<R>(ld(work + pr.id.x), xa, d1);
+        sub3<R>(ld(work + pr.id.y), xa, d2);
+        sub3<R>(ld(work + pr.id.z), xa, d3);
+        contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
     }
-    if (WC) wc_contrib<R, R, true>(L, work, v, xa, f, A);
+    if (WC) wc_contrib<R, R, true>(L, work, 0, v, xa, f, A);
     finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
 }
 
@@ -457,13 +567,13 @@ __global__ void __launch_bounds__(SplitBlock<SPLIT>::n) sweep_split_kernel(const
         xa4 = work[v];
         const R xa[3] = {xa4.x, xa4.y, xa4.z};
         for (int k = sub; k < deg; k += SPLIT) {
-            int4 id;
-            R g1[3], g2[3], g3[3], VE, d1[3], d2[3], d3[3];
-            Rec<R>::load(L, base + (int64_t)k * kChunk, id, g1, g2, g3, VE);
-            sub3<R>(ld(work + id.x), xa, d1);
-            sub3<R>(ld(work + id.y), xa, d2);
-            sub3<R>(ld(work + id.z), xa, d3);
-            pair_contrib<MODEL, true>(d1, d2, d3, g1, g2, g3, VE * cmu, VE * clam, f, A);
+            Pair<R, MODEL> pr;
+            load_pair<true>(L, base + (int64_t)k * kChunk, pr);
+            R d1[3], d2[3], d3[3];
+            sub3<R>(ld(work + pr.id.x), xa, d1);
+            sub3<R>(ld(work + pr.id.y), xa, d2);
+            sub3<R>(ld(work + pr.id.z), xa, d3);
+            contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
         }
     }
     if (sub > 0) {
@@ -486,13 +596,63 @@ __global__ void __launch_bounds__(SplitBlock<SPLIT>::n) sweep_split_kernel(const
         f[0] += fe.x; f[1] += fe.y; f[2] += fe.z;
     }
     const R xa[3] = {xa4.x, xa4.y, xa4.z};
-    if (WC) wc_contrib<R, R, true>(L, work, v, xa, f, A);
+    if (WC) wc_contrib<R, R, true>(L, work, 0, v, xa, f, A);
     finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
+}
+
+// Batched samples (n_batch >= 32): positions are stored sample-minor,
+// x[(group * x_stride + v) * 32 + lane] with sample = 32 * group + lane.  A warp updates ONE vertex for
+// 32 samples: the pair record (shared rest mesh) is a warp-broadcast load and every neighbour gather is
+// one coalesced 512 B (f32) line.  Same arithmetic and per-vertex order as sweep_kernel.
+template <class R, int MODEL, int ACCEL, bool FEXT, bool WC>
+__global__ void __launch_bounds__(kSweepBlock) sweep_batched_kernel(const Layout L, const int32_t v_begin,
+                                                                    const int32_t n_v, const int64_t chunk_begin,
+                                                                    const int64_t x_stride, const int32_t n_batch,
+                                                                    const int wi, const int oi, const int hi,
+                                                                    const R cmu, const R clam, const R omega,
+                                                                    const R gamma) {
+    using R4 = typename RT<R>::R4;
+    constexpr int WPB = kSweepBlock / 32;
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * WPB + (threadIdx.x >> 5);  // vertex index within the colour
+    const int b = blockIdx.y * 32 + lane;                  // sample
+    if (t >= n_v || b >= n_batch) return;
+    const int v = v_begin + t;
+    const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
+    const int deg = ld(L.deg + v);
+    const int64_t xs = ((int64_t)blockIdx.y * x_stride << 5) + lane;  // this lane's sample offset
+    R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
+    const R4 xa4 = work[(int64_t)v << 5];
+    const R xa[3] = {xa4.x, xa4.y, xa4.z};
+    R f[3] = {R(0), R(0), R(0)};
+    if (FEXT) {
+        const R4 fe = ld(reinterpret_cast<const R4 *>(L.fext) + v);
+        f[0] = fe.x; f[1] = fe.y; f[2] = fe.z;
+    }
+    R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
+    for (int k = 0; k < deg; ++k) {
+        Pair<R, MODEL> pr;
+        load_pair<false>(L, base + (int64_t)k * kChunk, pr);
+        R d1[3], d2[3], d3[3];
+        sub3<R>(ld(work + ((int64_t)pr.id.x << 5)), xa, d1);
+        sub3<R>(ld(work + ((int64_t)pr.id.y << 5)), xa, d2);
+        sub3<R>(ld(work + ((int64_t)pr.id.z << 5)), xa, d3);
+        contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
+    }
+    if (WC) wc_contrib<R, R, true>(L, work, 5, v, xa, f, A);
+    finish_vertex<R, ACCEL>(L, work, xs, (int64_t)v << 5, oi, hi, xa4, f, A, omega, gamma);
 }
 
 template <class R, int MODEL, int ACCEL, bool FE, bool W>
 cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
     const R cmu = R(p.cmu), clam = R(p.clam), om = R(s.omega), ga = R(s.gamma);
+    if (p.lane_shift == 5) {
+        constexpr int WPB = kSweepBlock / 32;
+        dim3 grid((unsigned)((s.n_v + WPB - 1) / WPB), (unsigned)((p.n_batch + 31) / 32));
+        sweep_batched_kernel<R, MODEL, ACCEL, FE, W><<<grid, kSweepBlock, 0, st>>>(
+            L, s.v_begin, s.n_v, s.chunk_begin, p.x_stride, p.n_batch, s.work, s.out, s.hist, cmu, clam, om, ga);
+        return cudaGetLastError();
+    }
     if (s.split <= 1) {
         dim3 grid((unsigned)((s.n_v + kSweepBlock - 1) / kSweepBlock), (unsigned)p.n_batch);
         sweep_kernel<R, MODEL, ACCEL, FE, W><<<grid, kSweepBlock, 0, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,
@@ -542,9 +702,16 @@ cudaError_t sweep_dispatch1(const Problem &p, const Layout &L, const SweepLaunch
 // ------------------------------------------------------------------------------------------------
 // positions: original <-> internal order
 // ------------------------------------------------------------------------------------------------
+// element index of (sample b, vertex v): samples grouped by 2^sh lanes, sample-minor inside a group
+// (sh = 0: [n_batch][x_stride]; sh = 5: [n_batch/32][x_stride][32])
+__device__ __forceinline__ int64_t pos_index(int64_t b, int64_t v, int64_t xs, int sh) {
+    return (((b >> sh) * xs + v) << sh) + (b & ((1 << sh) - 1));
+}
+
 template <class R>
 __global__ void set_positions_kernel(const Layout L, const int64_t nv, const int64_t n_global, const int64_t n_free,
-                                     const int64_t n_pin, const int64_t x_stride, const int nbuf) {
+                                     const int64_t n_pin, const int64_t x_stride, const int nbuf,
+                                     const int sh) {
     using R4 = typename RT<R>::R4;
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= nv) return;
@@ -556,17 +723,18 @@ __global__ void set_positions_kernel(const Layout L, const int64_t nv, const int
     } else {
         val = reinterpret_cast<const R4 *>(L.targets)[b * n_pin + (v - n_free)];
     }
-    for (int k = 0; k < nbuf; ++k) reinterpret_cast<R4 *>(L.xbuf[k])[b * x_stride + v] = val;
+    const int64_t e = pos_index(b, v, x_stride, sh);
+    for (int k = 0; k < nbuf; ++k) reinterpret_cast<R4 *>(L.xbuf[k])[e] = val;
 }
 
 template <class R>
 __global__ void get_positions_kernel(const Layout L, const int64_t nv, const int64_t n_global, const int64_t x_stride,
-                                     const int wi) {
+                                     const int wi, const int sh) {
     using R4 = typename RT<R>::R4;
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= nv) return;
     const int64_t b = blockIdx.y;
-    const R4 x = reinterpret_cast<const R4 *>(L.xbuf[wi])[b * x_stride + v];
+    const R4 x = reinterpret_cast<const R4 *>(L.xbuf[wi])[pos_index(b, v, x_stride, sh)];
     R *d = reinterpret_cast<R *>(L.stage) + (b * n_global + L.int2orig[v]) * 3;
     d[0] = x.x;
     d[1] = x.y;
@@ -577,12 +745,13 @@ __global__ void get_positions_kernel(const Layout L, const int64_t nv, const int
 // contiguous [n_batch][n][n_fields] Real4 buffer, or scatter such a buffer into the ghost rows
 template <class R>
 __global__ void halo_pack_kernel(const Layout L, const int32_t *__restrict__ idx, const int64_t n, const int nf,
-                                 const int64_t x_stride, const int b0, const int b1, const int b2, void *buf) {
+                                 const int64_t x_stride, const int b0, const int b1, const int b2, void *buf,
+                                 const int sh) {
     using R4 = typename RT<R>::R4;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int64_t b = blockIdx.y;
-    const int64_t v = b * x_stride + idx[i];
+    const int64_t v = pos_index(b, idx[i], x_stride, sh);
     R4 *o = reinterpret_cast<R4 *>(buf) + (b * n + i) * nf;
     const int bb[3] = {b0, b1, b2};
     for (int k = 0; k < nf; ++k) o[k] = reinterpret_cast<const R4 *>(L.xbuf[bb[k]])[v];
@@ -590,12 +759,13 @@ __global__ void halo_pack_kernel(const Layout L, const int32_t *__restrict__ idx
 
 template <class R>
 __global__ void halo_unpack_kernel(const Layout L, const int32_t *__restrict__ idx, const int64_t n, const int nf,
-                                   const int64_t x_stride, const int b0, const int b1, const int b2, const void *buf) {
+                                   const int64_t x_stride, const int b0, const int b1, const int b2, const void *buf,
+                                   const int sh) {
     using R4 = typename RT<R>::R4;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int64_t b = blockIdx.y;
-    const int64_t v = b * x_stride + idx[i];
+    const int64_t v = pos_index(b, idx[i], x_stride, sh);
     const R4 *o = reinterpret_cast<const R4 *>(buf) + (b * n + i) * nf;
     const int bb[3] = {b0, b1, b2};
     for (int k = 0; k < nf; ++k) reinterpret_cast<R4 *>(L.xbuf[bb[k]])[v] = o[k];
@@ -623,11 +793,11 @@ template <class R, int MODEL>
 __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const int64_t nt, const int64_t n_cons,
                                                            const int64_t x_stride, const int wi, const double cmu,
                                                            const double clam, const double rgx, const double rgy,
-                                                           const double rgz, const int ge) {
+                                                           const double rgz, const int ge, const int sh) {
     using R4 = typename RT<R>::R4;
-    __shared__ double sh[32];
+    __shared__ double red_sh[32];
     const int64_t b = blockIdx.y;
-    const R4 *x = reinterpret_cast<const R4 *>(L.xbuf[wi]) + b * x_stride;
+    const R4 *x = reinterpret_cast<const R4 *>(L.xbuf[wi]) + pos_index(b, 0, x_stride, sh);
     const double r_mu = cmu / (cmu + clam);  // mu / lambdahat, independent of E
     double acc = 0.0;
     for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < nt + n_cons;
@@ -637,7 +807,8 @@ __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const
             const R4 ta = ld(reinterpret_cast<const R4 *>(L.tet_a) + item);
             const R4 tb = ld(reinterpret_cast<const R4 *>(L.tet_b) + item);
             const R4 tc = ld(reinterpret_cast<const R4 *>(L.tet_c) + item);
-            const R4 q0 = ld(x + id.x), q1 = ld(x + id.y), q2 = ld(x + id.z), q3 = ld(x + id.w);
+            const R4 q0 = ld(x + ((int64_t)id.x << sh)), q1 = ld(x + ((int64_t)id.y << sh)),
+                     q2 = ld(x + ((int64_t)id.z << sh)), q3 = ld(x + ((int64_t)id.w << sh));
             const double Bm[3][3] = {{ta.x, ta.y, ta.z}, {ta.w, tb.x, tb.y}, {tb.z, tb.w, tc.x}};
             const double VE = tc.y, V = tc.z;
             const double d[3][3] = {{double(q1.x) - q0.x, double(q1.y) - q0.y, double(q1.z) - q0.z},
@@ -682,7 +853,7 @@ __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const
             double C[3] = {-double(an.x), -double(an.y), -double(an.z)};
             const int nn = ld(L.c_n + c);
             for (int q = 0; q < nn; ++q) {
-                const R4 y = ld(x + ld(L.c_node + kWcMaxNodes * c + q));
+                const R4 y = ld(x + ((int64_t)ld(L.c_node + kWcMaxNodes * c + q) << sh));
                 const double w = ld(reinterpret_cast<const R *>(L.c_w) + kWcMaxNodes * c + q);
                 C[0] += w * y.x; C[1] += w * y.y; C[2] += w * y.z;
             }
@@ -693,18 +864,18 @@ __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const
                           C[2] * (kxz * C[0] + kyz * C[1] + kzz * C[2]));
         }
     }
-    const double s = block_sum(acc, sh);
+    const double s = block_sum(acc, red_sh);
     if (threadIdx.x == 0) L.part_e[b * ge + blockIdx.x] = s;
 }
 
 template <class R, int MODEL, bool FEXT, bool WC>
 __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, const int64_t n_chunks,
                                                              const int64_t x_stride, const int wi, const double cmu,
-                                                             const double clam, const int gr) {
+                                                             const double clam, const int gr, const int sh) {
     using R4 = typename RT<R>::R4;
-    __shared__ double sh[32];
+    __shared__ double red_sh[32];
     const int64_t b = blockIdx.y;
-    const R4 *x = reinterpret_cast<const R4 *>(L.xbuf[wi]) + b * x_stride;
+    const R4 *x = reinterpret_cast<const R4 *>(L.xbuf[wi]) + pos_index(b, 0, x_stride, sh);
     double acc = 0.0;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_chunks * kChunk;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -715,7 +886,7 @@ __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, con
         const int v = cv.x + lane;
         const int64_t base = L.chunk_off[chunk] + lane;
         const int deg = L.deg[v];
-        const R4 xa4 = x[v];
+        const R4 xa4 = x[(int64_t)v << sh];
         const double xa[3] = {xa4.x, xa4.y, xa4.z};
         double f[3] = {0.0, 0.0, 0.0}, A[6];
         if (FEXT) {
@@ -723,33 +894,31 @@ __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, con
             f[0] = fe.x; f[1] = fe.y; f[2] = fe.z;
         }
         for (int k = 0; k < deg; ++k) {
-            int4 id;
-            R g1r[3], g2r[3], g3r[3], VE;
-            Rec<R>::load(L, base + (int64_t)k * kChunk, id, g1r, g2r, g3r, VE);
-            const R4 p1 = ld(x + id.x), p2 = ld(x + id.y), p3 = ld(x + id.z);
+            Pair<R, MODEL> pr;
+            load_pair<true>(L, base + (int64_t)k * kChunk, pr);
+            const R4 p1 = ld(x + ((int64_t)pr.id.x << sh)), p2 = ld(x + ((int64_t)pr.id.y << sh)),
+                     p3 = ld(x + ((int64_t)pr.id.z << sh));
             const double d1[3] = {p1.x - xa[0], p1.y - xa[1], p1.z - xa[2]};
             const double d2[3] = {p2.x - xa[0], p2.y - xa[1], p2.z - xa[2]};
             const double d3[3] = {p3.x - xa[0], p3.y - xa[1], p3.z - xa[2]};
-            const double g1[3] = {g1r[0], g1r[1], g1r[2]}, g2[3] = {g2r[0], g2r[1], g2r[2]},
-                         g3[3] = {g3r[0], g3r[1], g3r[2]};
-            pair_contrib<MODEL, false>(d1, d2, d3, g1, g2, g3, double(VE) * cmu, double(VE) * clam, f, A);
+            contrib<false>(d1, d2, d3, pr, cmu, clam, f, A);
         }
-        if (WC) wc_contrib<R, double, false>(L, x, v, xa, f, A);
+        if (WC) wc_contrib<R, double, false>(L, x, sh, v, xa, f, A);
         acc += f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
     }
-    const double s = block_sum(acc, sh);
+    const double s = block_sum(acc, red_sh);
     if (threadIdx.x == 0) L.part_r[b * gr + blockIdx.x] = s;
 }
 
 __global__ void __launch_bounds__(kRedBlock) reduce_kernel(const Layout L, const int ge, const int gr) {
-    __shared__ double sh[32];
+    __shared__ double red_sh[32];
     const int64_t b = blockIdx.x;
     double e = 0.0, r = 0.0;
     for (int k = threadIdx.x; k < ge; k += blockDim.x) e += L.part_e[b * ge + k];
     for (int k = threadIdx.x; k < gr; k += blockDim.x) r += L.part_r[b * gr + k];
-    e = block_sum(e, sh);
+    e = block_sum(e, red_sh);
     __syncthreads();
-    r = block_sum(r, sh);
+    r = block_sum(r, red_sh);
     if (threadIdx.x == 0) {
         L.results[2 * b] = e;
         L.results[2 * b + 1] = sqrt(r);
@@ -759,14 +928,14 @@ __global__ void __launch_bounds__(kRedBlock) reduce_kernel(const Layout L, const
 template <class R, int MODEL>
 cudaError_t energy_dispatch(const Problem &p, const Layout &L, int wi, cudaStream_t st) {
     energy_kernel<R, MODEL><<<dim3(p.ge, p.n_batch), kRedBlock, 0, st>>>(
-        L, p.n_tets, p.n_cons, p.x_stride, wi, p.cmu, p.clam, p.rho_g[0], p.rho_g[1], p.rho_g[2], p.ge);
+        L, p.n_tets, p.n_cons, p.x_stride, wi, p.cmu, p.clam, p.rho_g[0], p.rho_g[1], p.rho_g[2], p.ge, p.lane_shift);
     dim3 gr(p.gr, p.n_batch);
     if (p.has_fext) {
-        if (p.has_wc) residual_kernel<R, MODEL, true, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr);
-        else residual_kernel<R, MODEL, true, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr);
+        if (p.has_wc) residual_kernel<R, MODEL, true, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift);
+        else residual_kernel<R, MODEL, true, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift);
     } else {
-        if (p.has_wc) residual_kernel<R, MODEL, false, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr);
-        else residual_kernel<R, MODEL, false, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr);
+        if (p.has_wc) residual_kernel<R, MODEL, false, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift);
+        else residual_kernel<R, MODEL, false, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift);
     }
     reduce_kernel<<<p.n_batch, kRedBlock, 0, st>>>(L, p.ge, p.gr);
     return cudaGetLastError();
@@ -783,9 +952,9 @@ cudaError_t launch_set_positions(const Problem &p, const Layout &L, int n_buffer
     if (p.n_vertices <= 0) return cudaSuccess;
     dim3 grid((unsigned)((p.n_vertices + 255) / 256), (unsigned)p.n_batch);
     if (p.dtype == DT_F64)
-        set_positions_kernel<double><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_global, p.n_free, p.n_pinned, p.x_stride, n_buffers);
+        set_positions_kernel<double><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_global, p.n_free, p.n_pinned, p.x_stride, n_buffers, p.lane_shift);
     else
-        set_positions_kernel<float><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_global, p.n_free, p.n_pinned, p.x_stride, n_buffers);
+        set_positions_kernel<float><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_global, p.n_free, p.n_pinned, p.x_stride, n_buffers, p.lane_shift);
     return cudaGetLastError();
 }
 
@@ -793,9 +962,9 @@ cudaError_t launch_get_positions(const Problem &p, const Layout &L, int work, cu
     if (p.n_vertices <= 0) return cudaSuccess;
     dim3 grid((unsigned)((p.n_vertices + 255) / 256), (unsigned)p.n_batch);
     if (p.dtype == DT_F64)
-        get_positions_kernel<double><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_global, p.x_stride, work);
+        get_positions_kernel<double><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_global, p.x_stride, work, p.lane_shift);
     else
-        get_positions_kernel<float><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_global, p.x_stride, work);
+        get_positions_kernel<float><<<grid, 256, 0, st>>>(L, p.n_vertices, p.n_global, p.x_stride, work, p.lane_shift);
     return cudaGetLastError();
 }
 
@@ -804,9 +973,9 @@ cudaError_t launch_halo_pack(const Problem &p, const Layout &L, const int32_t *i
     if (n <= 0) return cudaSuccess;
     dim3 grid((unsigned)((n + 255) / 256), (unsigned)p.n_batch);
     if (p.dtype == DT_F64)
-        halo_pack_kernel<double><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf);
+        halo_pack_kernel<double><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf, p.lane_shift);
     else
-        halo_pack_kernel<float><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf);
+        halo_pack_kernel<float><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf, p.lane_shift);
     return cudaGetLastError();
 }
 
@@ -815,9 +984,9 @@ cudaError_t launch_halo_unpack(const Problem &p, const Layout &L, const int32_t 
     if (n <= 0) return cudaSuccess;
     dim3 grid((unsigned)((n + 255) / 256), (unsigned)p.n_batch);
     if (p.dtype == DT_F64)
-        halo_unpack_kernel<double><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf);
+        halo_unpack_kernel<double><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf, p.lane_shift);
     else
-        halo_unpack_kernel<float><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf);
+        halo_unpack_kernel<float><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf, p.lane_shift);
     return cudaGetLastError();
 }
 

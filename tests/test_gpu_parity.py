@@ -103,6 +103,23 @@ def test_batched_parity_and_independence(dtype):
     assert np.array_equal(alone[0], xg[3]) and Ea[0] == Eg[3]
 
 
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_batched_sample_minor_layout_ragged(dtype):
+    # n_batch >= 32 switches to the sample-minor layout and the warp-per-vertex batched kernel; 40 samples
+    # = one full group of 32 lanes + a ragged group of 8
+    s = G.config4_batched(n_samples=40, n=5, iterations=30)
+    xg, Eg, rg, q = run_gpu(s, dtype)
+    for b in (0, 31, 32, 39):
+        xo, Eo, _, _ = run_oracle(s, sample=b)
+        assert_parity(s, dtype, xg[b], Eg[b], xo, Eo, extra=f"sample {b}")
+    # the same sample alone (thread-per-vertex kernel, sample-major layout) gives the same iterate up to
+    # the rounding of a different kernel instantiation
+    alone, Ea, ra, _ = run_gpu(s.sample(33), dtype)
+    tol = 1e-14 if dtype == "f64" else 1e-6
+    assert np.abs(alone[0] - xg[33]).max() <= tol * s.bbox_diag()
+    assert abs(Ea[0] - Eg[33]) <= max(tol, 1e-12) * abs(Eg[33])
+
+
 def test_energy_residual_at_x0_fp64():
     from oracle import Oracle
     for cfg in (1, 2, 3, 5):
