@@ -197,6 +197,12 @@ pbng_status pbng_query(pbng_ctx *ctx, pbng_info *info);
 pbng_status pbng_profile_enable(pbng_ctx *ctx, int enable);
 pbng_status pbng_profile_read(pbng_ctx *ctx, double *sweep_ms, int64_t *sweep_launches);
 
+/* TEST HOOK (not on the solve path): the device polar rotation R(F) of eq:cor (closest rotation, det R =
+ * +1) for n row-major 3x3 matrices F (host, doubles), computed in `dtype` by the same
+ * device routine the fixed-corotated sweep uses; R (host, n*9 doubles).  Allocates its own scratch with
+ * cudaMalloc and synchronises (tests only).  Lets the tests pin the routine against numpy's SVD. */
+pbng_status pbng_test_polar(pbng_dtype dtype, const double *F, double *R, int64_t n, int device);
+
 /* Release the context (not the workspace, which the caller owns). NULL is a no-op. */
 pbng_status pbng_destroy(pbng_ctx *ctx);
 

@@ -1336,6 +1336,24 @@ pbng_status pbng_profile_read(pbng_ctx *c, double *sweep_ms, int64_t *sweep_laun
     return PBNG_OK;
 }
 
+pbng_status pbng_test_polar(pbng_dtype dtype, const double *F, double *R, int64_t n, int device) {
+    if (!F || !R || n < 0 || (dtype != PBNG_F32 && dtype != PBNG_F64) || device < 0)
+        return fail(PBNG_E_INVALID_ARGUMENT, "test_polar: bad arguments");
+    if (n == 0) return PBNG_OK;
+    DevGuard g(device);
+    double *dF = nullptr, *dR = nullptr;
+    const size_t bytes = (size_t)n * 9 * sizeof(double);
+    PBNG_CUDA(cudaMalloc(&dF, bytes), "test_polar: cudaMalloc");
+    cudaError_t e = cudaMalloc(&dR, bytes);
+    if (e == cudaSuccess) e = cudaMemcpy(dF, F, bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch_polar_test(dtype, dF, dR, n, nullptr);
+    if (e == cudaSuccess) e = cudaMemcpy(R, dR, bytes, cudaMemcpyDeviceToHost);
+    cudaFree(dF);
+    if (dR) cudaFree(dR);
+    if (e != cudaSuccess) return cuda_fail(e, "test_polar");
+    return PBNG_OK;
+}
+
 pbng_status pbng_destroy(pbng_ctx *c) {
     if (!c) return PBNG_OK;
     if (c->on_device()) {

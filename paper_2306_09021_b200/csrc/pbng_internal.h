@@ -95,5 +95,6 @@ cudaError_t launch_halo_pack(const Problem &p, const Layout &L, const int32_t *i
 cudaError_t launch_halo_unpack(const Problem &p, const Layout &L, const int32_t *idx, int64_t n, int n_fields,
                                const int (&bufs)[3], const void *buf, cudaStream_t st);
 int kernels_per_energy_residual();
+cudaError_t launch_polar_test(int dtype, const double *F, double *R, int64_t n, cudaStream_t st);
 
 }  // namespace pbng

@@ -40,9 +40,13 @@ __device__ __forceinline__ double4 ld(const double4 *p) {
 }
 
 __device__ __forceinline__ float rsq(float x) { return rsqrtf(x); }
+// the fp32 Jacobi rotation does not need IEEE-rounded sqrt / division (the angle only has to zero the
+// off-diagonal to working accuracy): MUFU-based approximations; fp64 keeps the exact operations
+__device__ __forceinline__ float sqrt_fast(float x) { return x > 0.f ? x * rsqrtf(x) : 0.f; }
+__device__ __forceinline__ double sqrt_fast(double x) { return sqrt(x); }
+__device__ __forceinline__ float div_fast(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double div_fast(double a, double b) { return a / b; }
 __device__ __forceinline__ double rsq(double x) { return rsqrt(x); }
-__device__ __forceinline__ float sq(float x) { return sqrtf(x); }
-__device__ __forceinline__ double sq(double x) { return sqrt(x); }
 
 template <class R> __device__ __forceinline__ typename RT<R>::R4 mk4(R x, R y, R z);
 template <> __device__ __forceinline__ float4 mk4<float>(float x, float y, float z) { return make_float4(x, y, z, 0.f); }
@@ -54,7 +58,10 @@ template <> __device__ __forceinline__ double4 mk4<double>(double x, double y, d
 // (each swap negates one column so det V stays +1); Givens QR of B -> Q (a rotation, the sign of
 // det F lands in the last diagonal entry); R = Q V^T.
 // ------------------------------------------------------------------------------------------------
-template <class R> struct PolarSweeps { static constexpr int n = 4; };
+#ifndef PBNG_POLAR_SWEEPS_F32
+#define PBNG_POLAR_SWEEPS_F32 4
+#endif
+template <class R> struct PolarSweeps { static constexpr int n = PBNG_POLAR_SWEEPS_F32; };
 template <> struct PolarSweeps<double> { static constexpr int n = 7; };
 
 template <int p, int q, class R>
@@ -62,8 +69,9 @@ __device__ __forceinline__ void jacobi_rot(R (&S)[3][3], R (&V)[3][3]) {
     constexpr int r = 3 - p - q;
     const R apq = S[p][q];
     const R d = S[q][q] - S[p][p];
-    const R den = fabs(d) + sq(d * d + R(4) * apq * apq);
-    R t = den > R(0) ? R(2) * apq / den : R(0);
+    // t = tan(phi) = sign(d) 2 apq / (|d| + sqrt(d^2 + 4 apq^2)), the smaller root (stable)
+    const R den = fabs(d) + sqrt_fast(d * d + R(4) * apq * apq);
+    R t = den > R(0) ? div_fast(R(2) * apq, den) : R(0);
     t = d < R(0) ? -t : t;
     const R c = rsq(R(1) + t * t);
     const R s = t * c;
@@ -941,6 +949,19 @@ cudaError_t energy_dispatch(const Problem &p, const Layout &L, int wi, cudaStrea
     return cudaGetLastError();
 }
 
+// test hook: R(F) of the device polar decomposition for n matrices (pbng_test_polar)
+template <class R>
+__global__ void polar_test_kernel(const double *F, double *Rout, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    R Fm[3][3], Rm[3][3];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) Fm[a][b] = R(F[9 * i + 3 * a + b]);
+    polar_rotation(Fm, Rm);
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) Rout[9 * i + 3 * a + b] = double(Rm[a][b]);
+}
+
 }  // namespace
 
 cudaError_t launch_sweep(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
@@ -999,5 +1020,13 @@ cudaError_t launch_energy_residual(const Problem &p, const Layout &L, int work, 
 }
 
 int kernels_per_energy_residual() { return 3; }
+
+cudaError_t launch_polar_test(int dtype, const double *F, double *R, int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned g = (unsigned)((n + 127) / 128);
+    if (dtype == DT_F64) polar_test_kernel<double><<<g, 128, 0, st>>>(F, R, n);
+    else polar_test_kernel<float><<<g, 128, 0, st>>>(F, R, n);
+    return cudaGetLastError();
+}
 
 }  // namespace pbng

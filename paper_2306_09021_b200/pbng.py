@@ -26,7 +26,7 @@ EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbn
            "pbng_bind_workspace", "pbng_set_positions", "pbng_get_positions", "pbng_iterate", "pbng_energy_residual",
            "pbng_synchronize", "pbng_query", "pbng_profile_enable", "pbng_profile_read", "pbng_destroy",
            "pbng_last_error", "pbng_version", "pbng_sweep_colour", "pbng_end_iteration", "pbng_set_partition",
-           "pbng_halo_counts", "pbng_halo_vertices", "pbng_halo_pack", "pbng_halo_unpack")
+           "pbng_halo_counts", "pbng_halo_vertices", "pbng_halo_pack", "pbng_halo_unpack", "pbng_test_polar")
 
 WC_DTYPE = np.dtype([("n0", "<i4"), ("n1", "<i4"), ("idx0", "<i4", 4), ("idx1", "<i4", 4), ("w0", "<f8", 4),
                      ("w1", "<f8", 4), ("anchor", "<f8", 3), ("K", "<f8", 6)])
@@ -84,6 +84,7 @@ def lib():
     L.pbng_halo_vertices.argtypes = [vp, i32, i32, vp, vp]
     L.pbng_halo_pack.argtypes = [vp, i32, i32, i32, vp]
     L.pbng_halo_unpack.argtypes = [vp, i32, i32, i32, vp]
+    L.pbng_test_polar.argtypes = [C.c_int, vp, vp, i64, C.c_int]
     L.pbng_last_error.restype = C.c_char_p
     L.pbng_version.restype = i32
     for name in EXPORTS:
@@ -286,6 +287,14 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def test_polar(F, dtype: str = "f32", device: int = 0) -> np.ndarray:
+    """Test hook: the device polar rotation R(F) (fixed-corotated model) of a batch of 3x3 matrices."""
+    F = _np(F, np.float64).reshape(-1, 3, 3)
+    R = np.empty_like(F)
+    _check(lib().pbng_test_polar(DTYPE[dtype], _ptr(F), _ptr(R), F.shape[0], int(device)))
+    return R
 
 
 def context_from_scene(scene, device=0, dtype: Optional[str] = None, stream=None, bind: bool = True,

@@ -1,0 +1,68 @@
+"""The device polar rotation of the fixed-corotated sweep (eq:cor; reading Z4: closest
+rotation, det R = +1 also for inverted F) pinned against numpy.linalg.svd with the sign correction, through
+the pbng_test_polar test hook."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _rot(rng):
+    q, r = np.linalg.qr(rng.standard_normal((3, 3)))
+    q = q * np.sign(np.diag(r))
+    if np.linalg.det(q) < 0:
+        q[:, 0] = -q[:, 0]
+    return q
+
+
+def _cases(n=60000, seed=5):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    Fs = []
+    for t in range(n):
+        kind = t % 5
+        if kind == 0:
+            F = rng.standard_normal((3, 3))
+        elif kind == 1:  # inverted
+            F = _rot(rng) @ np.diag(rng.uniform(0.3, 1.8, 3) * [1, 1, -1]) @ _rot(rng).T
+        elif kind == 2:  # near-singular
+            F = _rot(rng) @ np.diag([rng.uniform(0.5, 2), rng.uniform(0.5, 2), rng.uniform(-1e-4, 1e-4)]) @ _rot(rng).T
+        elif kind == 3:  # elastic-range deformation
+            F = np.eye(3) + 0.2 * rng.standard_normal((3, 3))
+        else:  # large stretch / compression
+            F = _rot(rng) @ np.diag(rng.uniform(0.05, 5.0, 3)) @ _rot(rng).T
+        Fs.append(F)
+    return np.array(Fs)
+
+
+def _reference(F):
+    U, s, Vt = np.linalg.svd(F)
+    flip = np.linalg.det(U) * np.linalg.det(Vt) < 0
+    U[flip, :, 2] *= -1
+    s[flip, 2] *= -1
+    return U @ Vt, s
+
+
+# error bound scales with the conditioning 1 / gap of R(F) (sigma_2 + sign-corrected sigma_3); the base
+# tolerances are ~10x the worst err * gap seen on B200 (f64 1.0e-14, f32 7.3e-7 with 4 Jacobi sweeps)
+@pytest.mark.parametrize("dtype,tol", [("f64", 1e-13), ("f32", 5e-6)])
+def test_device_polar_matches_numpy_svd(dtype, tol):
+    from paper_2306_09021_b200.pbng import test_polar
+    F = _cases()
+    R = test_polar(F, dtype)
+    Rn, s = _reference(F)
+    gap = np.abs(s[:, 1] + s[:, 2]) / np.maximum(1.0, np.abs(s[:, 0]))
+    ok = gap > 1e-3  # R is well conditioned only when the two smallest signed singular values do not cancel
+    assert ok.mean() > 0.95
+    err = np.abs(R - Rn).max(axis=(1, 2))
+    assert (err * gap)[ok].max() <= tol, (dtype, (err * gap)[ok].max())
+    det = np.linalg.det(R)
+    assert np.abs(det - 1).max() <= (1e-12 if dtype == "f64" else 1e-5)
+    orth = np.abs(np.einsum("nki,nkj->nij", R, R) - np.eye(3)).max()
+    assert orth <= (1e-12 if dtype == "f64" else 1e-5)
