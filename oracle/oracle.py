@@ -90,6 +90,9 @@ def lib():
             L.orc_residual.restype = d
             L.orc_energy.argtypes = [vp, vp, vp]
             L.orc_energy.restype = d
+            L.orc_set_inertia.argtypes = [vp, d, vp]
+            L.orc_set_inertia.restype = C.c_int
+            L.orc_get_mass.argtypes = [vp, vp]
             _lib = L
     return _lib
 
@@ -229,6 +232,18 @@ class Oracle:
         V = np.empty(max(self.nt, 1))
         lib().orc_get_rest(self._h, _p(B), _p(V))
         return B[:self.nt], V[:self.nt]
+
+    def mass(self) -> np.ndarray:
+        out = np.empty(self.nv)
+        lib().orc_get_mass(self._h, _p(out))
+        return out
+
+    def set_inertia(self, dt: float, xtilde=None):
+        """Backward Euler (eq:fem_be): dt > 0 with xtilde = 2 x^n - x^{n-1}; dt = 0 -> quasistatic."""
+        xt = None if xtilde is None else self._x(xtilde)
+        st = lib().orc_set_inertia(self._h, float(dt), _p(xt) if xt is not None else None)
+        if st:
+            raise OracleError(st)
 
     def fext(self) -> np.ndarray:
         out = np.empty((self.nv, 3))

@@ -20,6 +20,8 @@
  *   Z8  x^{-1} := x^0.    Z9  Dirichlet rows keep their targets under blending.
  *   Z13 the external-work term sums over all vertices.  Z14 residual = 2-norm over free vertices.
  *   Weak constraint with an empty side 1 uses a fixed anchor point instead (rigid-plane contact).
+ *   Backward Euler (eq:fem_be) keeps f^ext in the residual and uses xtilde = 2 x^n - x^{n-1}; the
+ *   energy then is the incremental potential with the inertia of the free nodes.
  *
  * Matrices are row-major double[9]: M[3*a+b] = M_{ab}.  Fourth-order tensors are double[81] with
  * T[(3*alpha+gamma)*9 + 3*beta+delta] = T_{alpha gamma beta delta}.
@@ -285,6 +287,11 @@ typedef struct {
     int32_t *vc;
     int32_t *colour;
     int32_t ncolours;
+    /* backward Euler (eq:fem_be): lumped masses m_i = sum_e R^0 V_e / 4, 1/dt^2 (0 =
+     * quasistatic) and the inertial target xtilde_i = 2 x^n_i - x^{n-1}_i */
+    double *mass;
+    double inv_dt2;
+    double *xtilde;
 } orc_prep;
 
 void orc_free(orc_prep *p) {
@@ -292,7 +299,7 @@ void orc_free(orc_prep *p) {
     free(p->X); free(p->tets); free(p->B); free(p->V); free(p->mu); free(p->lambda); free(p->fext);
     free(p->pinned); free(p->wc_n0); free(p->wc_n1); free(p->wc_idx0); free(p->wc_idx1);
     free(p->wc_w0); free(p->wc_w1); free(p->wc_anchor); free(p->wc_K); free(p->vt_off); free(p->vt);
-    free(p->vc_off); free(p->vc); free(p->colour);
+    free(p->vc_off); free(p->vc); free(p->colour); free(p->mass); free(p->xtilde);
     free(p);
 }
 
@@ -456,7 +463,11 @@ int orc_prepare(const orc_scene *s, orc_prep **out, int64_t *bad) {
     p->fext = calloc((size_t)s->nv * 3, sizeof(double));
     p->pinned = calloc((size_t)s->nv, 1);
     p->colour = malloc((size_t)s->nv * sizeof(int32_t));
-    if (!p->X || !p->tets || !p->B || !p->V || !p->mu || !p->lambda || !p->fext || !p->pinned || !p->colour) {
+    p->mass = calloc((size_t)s->nv, sizeof(double));
+    p->xtilde = calloc((size_t)s->nv * 3, sizeof(double));
+    p->inv_dt2 = 0.0;
+    if (!p->X || !p->tets || !p->B || !p->V || !p->mu || !p->lambda || !p->fext || !p->pinned || !p->colour ||
+        !p->mass || !p->xtilde) {
         orc_free(p);
         return ORC_E_NOMEM;
     }
@@ -490,8 +501,10 @@ int orc_prepare(const orc_scene *s, orc_prep **out, int64_t *bad) {
             orc_free(p);
             return ORC_E_ARG;
         }
-        for (a = 0; a < 4; ++a)
+        for (a = 0; a < 4; ++a) {
             for (b = 0; b < 3; ++b) p->fext[3 * t[a] + b] += p->density * p->gravity[b] * p->V[e] / 4.0;
+            p->mass[t[a]] += p->density * p->V[e] / 4.0; /* m_ii = int R^0 N_i dX */
+        }
     }
     st = build_incidence(p);
     if (st != ORC_OK) { orc_free(p); return st; }
@@ -604,7 +617,31 @@ void orc_nodal(const orc_prep *p, const double *y, int64_t i, double *f, double 
                 A[3 * a + b] += d * d * K[3 * a + b];
             }
     }
+    /* backward Euler: the node's share of the incremental potential m_i / (2 dt^2) |y_i - xtilde_i|^2 adds
+     * -m_i (y_i - xtilde_i) / dt^2 to the right-hand side and m_i / dt^2 I to A (eq:fem_be) */
+    if (p->inv_dt2 > 0.0) {
+        const double m = p->mass[i] * p->inv_dt2;
+        for (a = 0; a < 3; ++a) {
+            f[a] -= m * (y[3 * i + a] - p->xtilde[3 * i + a]);
+            A[4 * a] += m;
+        }
+    }
 }
+
+/* backward-Euler mode: dt > 0 with xtilde (nv*3) = 2 x^n - x^{n-1}; dt == 0 returns to quasistatics */
+int orc_set_inertia(orc_prep *p, double dt, const double *xtilde) {
+    if (!(dt >= 0.0)) return ORC_E_ARG;
+    if (dt == 0.0) {
+        p->inv_dt2 = 0.0;
+        return ORC_OK;
+    }
+    if (!xtilde) return ORC_E_ARG;
+    p->inv_dt2 = 1.0 / (dt * dt);
+    memcpy(p->xtilde, xtilde, (size_t)p->nv * 3 * sizeof(double));
+    return ORC_OK;
+}
+
+void orc_get_mass(const orc_prep *p, double *out) { memcpy(out, p->mass, (size_t)p->nv * sizeof(double)); }
 
 /* solve the 3x3 SPD system A dx = r by Cholesky (plain, fp64) */
 static int spd_solve3(const double *A, const double *r, double *x) {
@@ -741,6 +778,15 @@ double orc_energy(const orc_prep *p, const double *y, double *parts) {
             for (b = 0; b < 3; ++b) wc += 0.5 * C[a] * K[3 * a + b] * C[b];
     }
     for (i = 0; i < p->nv * 3; ++i) ext -= y[i] * p->fext[i];
+    if (p->inv_dt2 > 0.0) /* incremental potential: inertia of the free nodes (pinned nodes are constant) */
+        for (i = 0; i < p->nv; ++i) {
+            int a;
+            if (p->pinned[i]) continue;
+            for (a = 0; a < 3; ++a) {
+                const double dx = y[3 * i + a] - p->xtilde[3 * i + a];
+                ext += 0.5 * p->inv_dt2 * p->mass[i] * dx * dx;
+            }
+        }
     if (parts) { parts[0] = el; parts[1] = wc; parts[2] = ext; }
     return el + wc + ext;
 }
