@@ -130,6 +130,15 @@ pbng_status pbng_bind_workspace(pbng_ctx *ctx, void *device_ptr, uint64_t bytes)
  * overwritten by their targets.  Resets the acceleration state: l = 0, x^{-1} = x^0. */
 pbng_status pbng_set_positions(pbng_ctx *ctx, const void *x);
 
+/* Backward Euler (eq:fem_be): with dt > 0 every colour pass
+ * minimises the incremental potential sum_i m_i/(2 dt^2)|y_i - xtilde_i|^2 + PE(y) - y . f^ext, i.e. adds
+ * -m_i (y_i - xtilde_i)/dt^2 to f_i + f^ext_i and m_i/dt^2 I to A, with lumped masses m_ii = int R^0 N_i
+ * (needs density > 0) and xtilde = 2 x^n - x^{n-1} ([n_batch][n_vertices][3], context dtype, host or
+ * device, original order) supplied by the caller for the step.  The energy / residual of
+ * pbng_energy_residual then include the inertia of the (owned) free vertices.  dt = 0 returns to
+ * quasistatics.  Asynchronous; requires a bound workspace. */
+pbng_status pbng_set_inertia(pbng_ctx *ctx, double dt, const void *xtilde);
+
 /* Current positions x^l into `x_out` (host or device, [n_batch][n_vertices][3], context dtype).
  * Synchronises when x_out is host memory. */
 pbng_status pbng_get_positions(pbng_ctx *ctx, void *x_out);

@@ -154,12 +154,13 @@ struct pbng_ctx {
     std::vector<int64_t> h_chunk_off;
     std::vector<int2> h_chunk_v;
     std::vector<int32_t> h_deg, h_wc_off, h_wc_cid, h_c_n, h_c_node;
+    std::vector<unsigned char> h_mass;  // Real [n_own] lumped masses (backward Euler)
     std::vector<int4> h_tet_id;
     Problem prob;
     // workspace plan
     Region r_rec_id, r_rec_a, r_rec_b, r_rec_c, r_chunk_off, r_chunk_v, r_deg, r_fext, r_wc_off, r_wc_cid, r_wc_d,
         r_c_n, r_c_node, r_c_w, r_c_anchor, r_c_K, r_tet_id, r_tet_a, r_tet_b, r_tet_c, r_int2orig, r_targets,
-        r_x[3], r_stage, r_part_e, r_part_r, r_results, r_flag, r_halo_send, r_halo_recv;
+        r_x[3], r_stage, r_part_e, r_part_r, r_results, r_flag, r_halo_send, r_halo_recv, r_mass, r_xt;
     size_t ws_need = 0;
     // bound device state
     bool bound = false;
@@ -359,6 +360,15 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
             put4<R>(c->h_fext, i, m * c->grav[0], m * c->grav[1], m * c->grav[2], 0.0);
         }
 
+    // lumped masses m_ii = int R^0 N_i dX = sum_e R^0 V_e / 4, owned free vertices
+    c->h_mass.assign((size_t)std::max<int64_t>(c->n_free, 1) * s, 0);
+    for (int64_t i = 0; i < c->n_free; ++i) {
+        const int32_t o = c->int2orig[i];
+        double m = 0;
+        for (int64_t q = vt_off[o]; q < vt_off[o + 1]; ++q) m += c->density * c->V[vt[q]] / 4.0;
+        put1<R>(c->h_mass, i, m);
+    }
+
     // weak constraints held by this context (owned first): distinct nodes with combined weights
     // w0_j - w1_j; per owned free vertex the list of (constraint, w0_i - w1_i) in input order
     const int64_t ncl = (int64_t)c->cons_local.size();
@@ -453,7 +463,9 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     for (int k = 0; k < 3; ++k) p.rho_g[k] = c->density * c->grav[k];
     p.has_fext = has_fext;
     p.has_wc = c->n_vc > 0;
-    const int64_t items = ntl + c->n_cons_owned;
+    p.n_own = c->n_free;
+    p.inv_dt2 = 0.0;
+    const int64_t items = ntl + c->n_cons_owned + c->n_free;
     p.ge = (int)std::max<int64_t>(1, std::min<int64_t>((items + kRedBlock - 1) / kRedBlock, 1184));
     p.gr = (int)std::max<int64_t>(1, std::min<int64_t>((n_chunks * kChunk + kRedBlock - 1) / kRedBlock, 1184));
 }
@@ -497,6 +509,8 @@ void plan_workspace(pbng_ctx *c) {
     take(c->r_part_r, (size_t)c->nb * p.gr * 8);
     take(c->r_results, (size_t)c->nb * 2 * 8);
     take(c->r_flag, 4);
+    take(c->r_mass, c->h_mass.size());
+    take(c->r_xt, (groups << p.lane_shift) * (size_t)p.x_stride * s4);
     take(c->r_halo_send, std::max<size_t>(c->h_halo_send.size(), 1) * 4);
     take(c->r_halo_recv, std::max<size_t>(c->h_halo_recv.size(), 1) * 4);
     c->ws_need = off;
@@ -1025,6 +1039,8 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     L.part_r = static_cast<double *>(at(c->r_part_r));
     L.results = static_cast<double *>(at(c->r_results));
     L.flag = static_cast<int32_t *>(at(c->r_flag));
+    L.mass = at(c->r_mass);
+    L.xtilde = at(c->r_xt);
     L.halo_send = static_cast<const int32_t *>(at(c->r_halo_send));
     L.halo_recv = static_cast<const int32_t *>(at(c->r_halo_recv));
     auto up = [&](const Region &r, const void *src, size_t n) -> cudaError_t {
@@ -1054,6 +1070,7 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     chk(up(c->r_tet_b, c->h_tet_b.data(), c->h_tet_b.size()));
     chk(up(c->r_tet_c, c->h_tet_c.data(), c->h_tet_c.size()));
     chk(up(c->r_int2orig, c->int2orig.data(), c->int2orig.size() * 4));
+    chk(up(c->r_mass, c->h_mass.data(), c->h_mass.size()));
     chk(up(c->r_halo_send, c->h_halo_send.data(), c->h_halo_send.size() * 4));
     chk(up(c->r_halo_recv, c->h_halo_recv.data(), c->h_halo_recv.size() * 4));
     chk(up(c->r_targets, c->h_targets.data(), c->h_targets.size()));
@@ -1085,6 +1102,26 @@ pbng_status pbng_set_positions(pbng_ctx *c, const void *x) {
     c->hist_valid = true;
     c->positions_set = true;
     c->cur_accel = -1;
+    return PBNG_OK;
+}
+
+pbng_status pbng_set_inertia(pbng_ctx *c, double dt, const void *xtilde) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    if (!c->bound) return fail(PBNG_E_BAD_ORDER, "set_inertia: bind a workspace first");
+    if (!(dt >= 0.0) || !std::isfinite(dt)) return fail(PBNG_E_INVALID_ARGUMENT, "set_inertia: dt must be >= 0");
+    if (dt == 0.0) {
+        c->prob.inv_dt2 = 0.0;
+        return PBNG_OK;
+    }
+    if (!(c->density > 0.0)) return fail(PBNG_E_INVALID_ARGUMENT, "set_inertia: backward Euler needs density > 0");
+    if (!xtilde) return fail(PBNG_E_INVALID_ARGUMENT, "set_inertia: null xtilde");
+    DevGuard g(c->device);
+    const size_t n = (size_t)c->nb * (size_t)c->nv * 3 * c->real_size();
+    PBNG_CUDA(cudaMemcpyAsync(c->L.stage, xtilde, n, cudaMemcpyDefault, c->stream), "set_inertia: copy");
+    PBNG_CUDA(launch_set_positions(c->prob, c->L, -1, c->stream), "set_inertia: kernel");
+    c->launches += 1;
+    c->prob.inv_dt2 = 1.0 / (dt * dt);
     return PBNG_OK;
 }
 

@@ -59,6 +59,8 @@ struct Layout {
     int32_t *flag = nullptr;             // non-finite flag
     const int32_t *halo_send = nullptr;  // internal ids of the per-(colour, peer) send lists
     const int32_t *halo_recv = nullptr;  // internal ids of the per-(colour, peer) receive lists
+    const void *mass = nullptr;          // Real [n_own] lumped masses m_i = sum_e R^0 V_e / 4 (backward Euler)
+    void *xtilde = nullptr;              // Real4, position layout: inertial target 2 x^n - x^{n-1}
 };
 
 struct Problem {
@@ -73,6 +75,8 @@ struct Problem {
     double rho_g[3] = {0, 0, 0};  // density * gravity (energy's external-work term)
     bool has_fext = false, has_wc = false;
     int ge = 1, gr = 1;  // energy / residual partial blocks per sample
+    int64_t n_own = 0;     // owned free vertices (swept)
+    double inv_dt2 = 0;    // backward Euler 1/dt^2 (0: quasistatic)
 };
 
 struct SweepLaunch {

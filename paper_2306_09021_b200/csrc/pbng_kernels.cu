@@ -414,6 +414,20 @@ __device__ __forceinline__ void contrib(const T (&d1)[3], const T (&d2)[3], cons
     }
 }
 
+// backward Euler (eq:fem_be): the node's inertia m_i/(2 dt^2)|y_i - xtilde_i|^2 adds
+// -m_i/dt^2 (y_i - xtilde_i) to f and m_i/dt^2 I to A.  `xt` = xtilde at this vertex's element index.
+template <class R, class T>
+__device__ __forceinline__ void inertia_contrib(const Layout &L, int v, const typename RT<R>::R4 &xt, T idt2,
+                                                const T (&xa)[3], T (&f)[3], T (&A)[6]) {
+    const T m = T(ld(reinterpret_cast<const R *>(L.mass) + v)) * idt2;
+    f[0] -= m * (xa[0] - T(xt.x));
+    f[1] -= m * (xa[1] - T(xt.y));
+    f[2] -= m * (xa[2] - T(xt.z));
+    A[0] += m;
+    A[1] += m;
+    A[2] += m;
+}
+
 // weak-constraint terms for vertex v: f -= d K C_c, A += d^2 K
 template <class R, class T, bool HESS>
 __device__ __forceinline__ void wc_contrib(const Layout &L, const typename RT<R>::R4 *x, const int sh, int v,
@@ -513,7 +527,7 @@ template <class R, int MODEL, int ACCEL, bool FEXT, bool WC>
 __global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
                                                             const int64_t chunk_begin, const int64_t x_stride,
                                                             const int wi, const int oi, const int hi, const R cmu,
-                                                            const R clam, const R omega, const R gamma) {
+                                                            const R clam, const R omega, const R gamma, const R idt2) {
     using R4 = typename RT<R>::R4;
     const int t = blockIdx.x * kSweepBlock + threadIdx.x;
     if (t >= n_v) return;
@@ -542,6 +556,7 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_kernel(con
         contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
     }
     if (WC) wc_contrib<R, R, true>(L, work, 0, v, xa, f, A);
+    if (idt2 > R(0)) inertia_contrib<R, R>(L, v, ld(reinterpret_cast<const R4 *>(L.xtilde) + xs + v), idt2, xa, f, A);
     finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
 }
 
@@ -554,7 +569,8 @@ template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int SPLIT>
 __global__ void __launch_bounds__(SplitBlock<SPLIT>::n) sweep_split_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
                                                                   const int64_t chunk_begin, const int64_t x_stride,
                                                                   const int wi, const int oi, const int hi, const R cmu,
-                                                                  const R clam, const R omega, const R gamma) {
+                                                                  const R clam, const R omega, const R gamma,
+                                                                  const R idt2) {
     using R4 = typename RT<R>::R4;
     constexpr int CPB = SplitBlock<SPLIT>::n / (32 * SPLIT);
     static_assert(CPB >= 1 && CPB * SPLIT * 32 == SplitBlock<SPLIT>::n, "block must hold whole chunk groups");
@@ -605,6 +621,7 @@ __global__ void __launch_bounds__(SplitBlock<SPLIT>::n) sweep_split_kernel(const
     }
     const R xa[3] = {xa4.x, xa4.y, xa4.z};
     if (WC) wc_contrib<R, R, true>(L, work, 0, v, xa, f, A);
+    if (idt2 > R(0)) inertia_contrib<R, R>(L, v, ld(reinterpret_cast<const R4 *>(L.xtilde) + xs + v), idt2, xa, f, A);
     finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
 }
 
@@ -618,7 +635,7 @@ __global__ void __launch_bounds__(kSweepBlock) sweep_batched_kernel(const Layout
                                                                     const int64_t x_stride, const int32_t n_batch,
                                                                     const int wi, const int oi, const int hi,
                                                                     const R cmu, const R clam, const R omega,
-                                                                    const R gamma) {
+                                                                    const R gamma, const R idt2) {
     using R4 = typename RT<R>::R4;
     constexpr int WPB = kSweepBlock / 32;
     const int lane = threadIdx.x & 31;
@@ -648,24 +665,26 @@ __global__ void __launch_bounds__(kSweepBlock) sweep_batched_kernel(const Layout
         contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
     }
     if (WC) wc_contrib<R, R, true>(L, work, 5, v, xa, f, A);
+    if (idt2 > R(0))
+        inertia_contrib<R, R>(L, v, ld(reinterpret_cast<const R4 *>(L.xtilde) + xs + ((int64_t)v << 5)), idt2, xa, f, A);
     finish_vertex<R, ACCEL>(L, work, xs, (int64_t)v << 5, oi, hi, xa4, f, A, omega, gamma);
 }
 
 template <class R, int MODEL, int ACCEL, bool FE, bool W>
 cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
-    const R cmu = R(p.cmu), clam = R(p.clam), om = R(s.omega), ga = R(s.gamma);
+    const R cmu = R(p.cmu), clam = R(p.clam), om = R(s.omega), ga = R(s.gamma), idt2 = R(p.inv_dt2);
     if (p.lane_shift == 5) {
         constexpr int WPB = kSweepBlock / 32;
         dim3 grid((unsigned)((s.n_v + WPB - 1) / WPB), (unsigned)((p.n_batch + 31) / 32));
         sweep_batched_kernel<R, MODEL, ACCEL, FE, W><<<grid, kSweepBlock, 0, st>>>(
-            L, s.v_begin, s.n_v, s.chunk_begin, p.x_stride, p.n_batch, s.work, s.out, s.hist, cmu, clam, om, ga);
+            L, s.v_begin, s.n_v, s.chunk_begin, p.x_stride, p.n_batch, s.work, s.out, s.hist, cmu, clam, om, ga, idt2);
         return cudaGetLastError();
     }
     if (s.split <= 1) {
         dim3 grid((unsigned)((s.n_v + kSweepBlock - 1) / kSweepBlock), (unsigned)p.n_batch);
         sweep_kernel<R, MODEL, ACCEL, FE, W><<<grid, kSweepBlock, 0, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,
                                                                             p.x_stride, s.work, s.out, s.hist, cmu,
-                                                                            clam, om, ga);
+                                                                            clam, om, ga, idt2);
         return cudaGetLastError();
     }
 #define PBNG_SPLIT(S)                                                                                             \
@@ -674,7 +693,7 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
         dim3 grid((unsigned)((s.n_v + VPB - 1) / VPB), (unsigned)p.n_batch);                                     \
         sweep_split_kernel<R, MODEL, ACCEL, FE, W, S><<<grid, B, 0, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,    \
                                                                            p.x_stride, s.work, s.out, s.hist, cmu, \
-                                                                           clam, om, ga);                           \
+                                                                           clam, om, ga, idt2);                     \
     } while (0)
     if (s.split == 2) PBNG_SPLIT(2);
     else if (s.split == 8) PBNG_SPLIT(8);
@@ -725,13 +744,17 @@ __global__ void set_positions_kernel(const Layout L, const int64_t nv, const int
     if (v >= nv) return;
     const int64_t b = blockIdx.y;
     R4 val;
-    if (v < n_free) {
+    if (v < n_free || nbuf < 0) {
         const R *s = reinterpret_cast<const R *>(L.stage) + (b * n_global + L.int2orig[v]) * 3;
         val = mk4<R>(s[0], s[1], s[2]);
     } else {
         val = reinterpret_cast<const R4 *>(L.targets)[b * n_pin + (v - n_free)];
     }
     const int64_t e = pos_index(b, v, x_stride, sh);
+    if (nbuf < 0) {  // backward-Euler inertial target xtilde (pbng_set_inertia)
+        reinterpret_cast<R4 *>(L.xtilde)[e] = val;
+        return;
+    }
     for (int k = 0; k < nbuf; ++k) reinterpret_cast<R4 *>(L.xbuf[k])[e] = val;
 }
 
@@ -801,16 +824,24 @@ template <class R, int MODEL>
 __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const int64_t nt, const int64_t n_cons,
                                                            const int64_t x_stride, const int wi, const double cmu,
                                                            const double clam, const double rgx, const double rgy,
-                                                           const double rgz, const int ge, const int sh) {
+                                                           const double rgz, const int ge, const int sh,
+                                                           const int64_t n_own, const double idt2) {
     using R4 = typename RT<R>::R4;
     __shared__ double red_sh[32];
     const int64_t b = blockIdx.y;
     const R4 *x = reinterpret_cast<const R4 *>(L.xbuf[wi]) + pos_index(b, 0, x_stride, sh);
     const double r_mu = cmu / (cmu + clam);  // mu / lambdahat, independent of E
     double acc = 0.0;
-    for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < nt + n_cons;
+    const int64_t n_items = nt + n_cons + (idt2 > 0.0 ? n_own : 0);
+    for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < n_items;
          item += (int64_t)gridDim.x * blockDim.x) {
-        if (item < nt) {
+        if (item >= nt + n_cons) {  // backward Euler: inertia m_i/(2 dt^2) |x_i - xtilde_i|^2 of owned free nodes
+            const int64_t v = item - nt - n_cons;
+            const R4 xv = ld(x + (v << sh));
+            const R4 xt = ld(reinterpret_cast<const R4 *>(L.xtilde) + pos_index(b, v, x_stride, sh));
+            const double dx = double(xv.x) - xt.x, dy = double(xv.y) - xt.y, dz = double(xv.z) - xt.z;
+            acc += 0.5 * idt2 * double(ld(reinterpret_cast<const R *>(L.mass) + v)) * (dx * dx + dy * dy + dz * dz);
+        } else if (item < nt) {
             const int4 id = ld(L.tet_id + item);
             const R4 ta = ld(reinterpret_cast<const R4 *>(L.tet_a) + item);
             const R4 tb = ld(reinterpret_cast<const R4 *>(L.tet_b) + item);
@@ -879,7 +910,8 @@ __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const
 template <class R, int MODEL, bool FEXT, bool WC>
 __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, const int64_t n_chunks,
                                                              const int64_t x_stride, const int wi, const double cmu,
-                                                             const double clam, const int gr, const int sh) {
+                                                             const double clam, const int gr, const int sh,
+                                                             const double idt2) {
     using R4 = typename RT<R>::R4;
     __shared__ double red_sh[32];
     const int64_t b = blockIdx.y;
@@ -912,6 +944,9 @@ __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, con
             contrib<false>(d1, d2, d3, pr, cmu, clam, f, A);
         }
         if (WC) wc_contrib<R, double, false>(L, x, sh, v, xa, f, A);
+        if (idt2 > 0.0)
+            inertia_contrib<R, double>(L, v, ld(reinterpret_cast<const R4 *>(L.xtilde) + pos_index(b, v, x_stride, sh)),
+                                       idt2, xa, f, A);
         acc += f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
     }
     const double s = block_sum(acc, red_sh);
@@ -936,14 +971,14 @@ __global__ void __launch_bounds__(kRedBlock) reduce_kernel(const Layout L, const
 template <class R, int MODEL>
 cudaError_t energy_dispatch(const Problem &p, const Layout &L, int wi, cudaStream_t st) {
     energy_kernel<R, MODEL><<<dim3(p.ge, p.n_batch), kRedBlock, 0, st>>>(
-        L, p.n_tets, p.n_cons, p.x_stride, wi, p.cmu, p.clam, p.rho_g[0], p.rho_g[1], p.rho_g[2], p.ge, p.lane_shift);
+        L, p.n_tets, p.n_cons, p.x_stride, wi, p.cmu, p.clam, p.rho_g[0], p.rho_g[1], p.rho_g[2], p.ge, p.lane_shift, p.n_own, p.inv_dt2);
     dim3 gr(p.gr, p.n_batch);
     if (p.has_fext) {
-        if (p.has_wc) residual_kernel<R, MODEL, true, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift);
-        else residual_kernel<R, MODEL, true, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift);
+        if (p.has_wc) residual_kernel<R, MODEL, true, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2);
+        else residual_kernel<R, MODEL, true, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2);
     } else {
-        if (p.has_wc) residual_kernel<R, MODEL, false, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift);
-        else residual_kernel<R, MODEL, false, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift);
+        if (p.has_wc) residual_kernel<R, MODEL, false, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2);
+        else residual_kernel<R, MODEL, false, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2);
     }
     reduce_kernel<<<p.n_batch, kRedBlock, 0, st>>>(L, p.ge, p.gr);
     return cudaGetLastError();
@@ -969,6 +1004,7 @@ cudaError_t launch_sweep(const Problem &p, const Layout &L, const SweepLaunch &s
     return p.dtype == DT_F64 ? sweep_dispatch1<double>(p, L, s, st) : sweep_dispatch1<float>(p, L, s, st);
 }
 
+// n_buffers = -1: write the staged array into the backward-Euler target xtilde instead
 cudaError_t launch_set_positions(const Problem &p, const Layout &L, int n_buffers, cudaStream_t st) {
     if (p.n_vertices <= 0) return cudaSuccess;
     dim3 grid((unsigned)((p.n_vertices + 255) / 256), (unsigned)p.n_batch);

@@ -26,7 +26,8 @@ EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbn
            "pbng_bind_workspace", "pbng_set_positions", "pbng_get_positions", "pbng_iterate", "pbng_energy_residual",
            "pbng_synchronize", "pbng_query", "pbng_profile_enable", "pbng_profile_read", "pbng_destroy",
            "pbng_last_error", "pbng_version", "pbng_sweep_colour", "pbng_end_iteration", "pbng_set_partition",
-           "pbng_halo_counts", "pbng_halo_vertices", "pbng_halo_pack", "pbng_halo_unpack", "pbng_test_polar")
+           "pbng_halo_counts", "pbng_halo_vertices", "pbng_halo_pack", "pbng_halo_unpack", "pbng_test_polar",
+           "pbng_set_inertia")
 
 WC_DTYPE = np.dtype([("n0", "<i4"), ("n1", "<i4"), ("idx0", "<i4", 4), ("idx1", "<i4", 4), ("w0", "<f8", 4),
                      ("w1", "<f8", 4), ("anchor", "<f8", 3), ("K", "<f8", 6)])
@@ -85,6 +86,7 @@ def lib():
     L.pbng_halo_pack.argtypes = [vp, i32, i32, i32, vp]
     L.pbng_halo_unpack.argtypes = [vp, i32, i32, i32, vp]
     L.pbng_test_polar.argtypes = [C.c_int, vp, vp, i64, C.c_int]
+    L.pbng_set_inertia.argtypes = [vp, d, vp]
     L.pbng_last_error.restype = C.c_char_p
     L.pbng_version.restype = i32
     for name in EXPORTS:
@@ -209,6 +211,19 @@ class Context:
             raise ValueError(f"positions must have {self._shape()} entries")
         self._x_keep = x
         _check(lib().pbng_set_positions(self._h, x.data_ptr()))
+
+    def set_inertia(self, dt: float, xtilde=None):
+        """Backward Euler: dt > 0 with xtilde = 2 x^n - x^{n-1} ([n_batch, n_vertices, 3]); dt = 0 -> quasistatic."""
+        torch = self._torch
+        if dt == 0 or xtilde is None:
+            _check(lib().pbng_set_inertia(self._h, float(dt), None))
+            return
+        if isinstance(xtilde, np.ndarray):
+            xtilde = torch.from_numpy(_np(xtilde, self.np_dtype))
+        if xtilde.dtype != self.torch_dtype or not xtilde.is_contiguous():
+            xtilde = xtilde.to(self.torch_dtype).contiguous()
+        self._xt_keep = xtilde
+        _check(lib().pbng_set_inertia(self._h, float(dt), xtilde.data_ptr()))
 
     def get_positions(self, out=None):
         torch = self._torch
