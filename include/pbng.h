@@ -56,8 +56,12 @@ typedef enum {
 typedef enum { PBNG_F32 = 0, PBNG_F64 = 1 } pbng_dtype;
 
 /* PBNG_NEOHOOKEAN: eq:nh with lambdahat = mu + lambda.
- * PBNG_FIXED_COROTATED: eq:cor, R(F) the closest rotation (polar decomposition). */
-typedef enum { PBNG_NEOHOOKEAN = 0, PBNG_FIXED_COROTATED = 1 } pbng_model;
+ * PBNG_FIXED_COROTATED: eq:cor, R(F) the closest rotation (polar decomposition).
+ * PBNG_STABLE_NEOHOOKEAN: eq:snh read with the cited model's Lame re-parameterisation
+ *   mu_s = 4 mu/3, lambda_s = lambda + 5 mu/6 and volume coefficient lambda_s/2 (reading Z18),
+ *   which makes it Lame-consistent at F = I as PAPER.md:645 requires.  All models share the modified
+ *   Hessian density of eq:mod_hess_dens with the Lame mu, lambda. */
+typedef enum { PBNG_NEOHOOKEAN = 0, PBNG_FIXED_COROTATED = 1, PBNG_STABLE_NEOHOOKEAN = 2 } pbng_model;
 
 /* PAPER.md:603-618.  SOR: x^{l+1} = omega (x_PBNG - x^{l-1}) + x^{l-1}.
  * Chebyshev: x^{l+1} = omega_{l+1} (gamma (x_PBNG - x^l) + x^l - x^{l-1}) + x^{l-1},

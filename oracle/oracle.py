@@ -19,7 +19,7 @@ _lock = threading.Lock()
 _lib = None
 
 ACCEL = {"none": 0, "sor": 1, "chebyshev": 2}
-MODEL = {"nh": 0, "fcr": 1}
+MODEL = {"nh": 0, "fcr": 1, "snh": 2}
 ERR = {0: "ok", 1: "invalid argument", 2: "degenerate element", 3: "isolated vertex", 4: "out of memory"}
 
 

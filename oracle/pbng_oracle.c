@@ -33,7 +33,7 @@
 #include <string.h>
 
 enum { ORC_OK = 0, ORC_E_ARG = 1, ORC_E_DEGENERATE = 2, ORC_E_ISOLATED = 3, ORC_E_NOMEM = 4 };
-enum { ORC_NH = 0, ORC_FCR = 1 };
+enum { ORC_NH = 0, ORC_FCR = 1, ORC_SNH = 2 };
 enum { ORC_ACCEL_NONE = 0, ORC_ACCEL_SOR = 1, ORC_ACCEL_CHEBYSHEV = 2 };
 
 /* ------------------------------------------------------------------------------------------------ */
@@ -195,6 +195,17 @@ void orc_polar(const double *F, double *R) {
 /* Constitutive models                                                           */
 /* ------------------------------------------------------------------------------------------------ */
 
+/* Stable Neo-Hookean (eq:snh), reading Z18: the printed volume coefficient 1/2 is taken
+ * as lambda_s/2 and the Lame parameters are re-parameterised as in the cited model, mu_s = 4 mu / 3,
+ * lambda_s = lambda + 5 mu / 6, alpha = 1 + 3 mu_s / (4 lambda_s), which makes the Hessian at F = I equal
+ * linear elasticity's (the requirement of PAPER.md:645; pinned by the tests):
+ *   Psi = mu_s/2 (|F|^2 - 3) + lambda_s/2 (J - alpha)^2 - mu_s/2 log(1 + |F|^2)  [- Psi(I) unless raw] */
+static void snh_params(double mu, double lambda, double *ms, double *ls, double *alpha) {
+    *ms = 4.0 * mu / 3.0;
+    *ls = lambda + 5.0 * mu / 6.0;
+    *alpha = 1.0 + 3.0 * (*ms) / (4.0 * (*ls));
+}
+
 /* Psi(F).  FCR eq:cor: mu |F - R(F)|_F^2 + lambda/2 (det F - 1)^2.
  * NH eq:nh: 1/2 mu |F|_F^2 + lambdahat/2 (det F - 1 - mu/lambdahat)^2, lambdahat = mu +
  * lambda; with raw == 0 the constant 3/2 mu + mu^2/(2 lambdahat) is subtracted (reading Z1). */
@@ -206,6 +217,13 @@ double orc_psi(int model, double mu, double lambda, const double *F, int raw) {
         orc_polar(F, R);
         for (k = 0; k < 9; ++k) s += (F[k] - R[k]) * (F[k] - R[k]);
         return mu * s + 0.5 * lambda * (J - 1.0) * (J - 1.0);
+    } else if (model == ORC_SNH) {
+        double ms, ls, al, ic = 0.0, psi;
+        snh_params(mu, lambda, &ms, &ls, &al);
+        for (k = 0; k < 9; ++k) ic += F[k] * F[k];
+        psi = 0.5 * ms * (ic - 3.0) + 0.5 * ls * (J - al) * (J - al) - 0.5 * ms * log(1.0 + ic);
+        if (!raw) psi -= 0.5 * ls * (1.0 - al) * (1.0 - al) - 0.5 * ms * log(4.0);
+        return psi;
     } else {
         double lh = mu + lambda, fro = 0.0, t, psi;
         for (k = 0; k < 9; ++k) fro += F[k] * F[k];
@@ -226,6 +244,12 @@ void orc_piola(int model, double mu, double lambda, const double *F, double *P) 
         double R[9];
         orc_polar(F, R);
         for (k = 0; k < 9; ++k) P[k] = 2.0 * mu * (F[k] - R[k]) + lambda * (J - 1.0) * C[k];
+    } else if (model == ORC_SNH) {
+        /* P = mu_s F + lambda_s (J - alpha) cof F - mu_s F / (1 + |F|^2) */
+        double ms, ls, al, ic = 0.0;
+        snh_params(mu, lambda, &ms, &ls, &al);
+        for (k = 0; k < 9; ++k) ic += F[k] * F[k];
+        for (k = 0; k < 9; ++k) P[k] = ms * F[k] + ls * (J - al) * C[k] - ms * F[k] / (1.0 + ic);
     } else {
         double lh = mu + lambda;
         for (k = 0; k < 9; ++k) P[k] = mu * F[k] + lh * (J - 1.0 - mu / lh) * C[k];
@@ -426,7 +450,7 @@ int orc_prepare(const orc_scene *s, orc_prep **out, int64_t *bad) {
     int st;
     *out = NULL;
     if (bad) *bad = -1;
-    if (s->nv <= 0 || s->nt < 0 || (s->model != ORC_NH && s->model != ORC_FCR)) return ORC_E_ARG;
+    if (s->nv <= 0 || s->nt < 0 || (s->model != ORC_NH && s->model != ORC_FCR && s->model != ORC_SNH)) return ORC_E_ARG;
     if (s->nE != 1 && s->nE != s->nt) return ORC_E_ARG;
     if (!(s->nu >= 0.0 && s->nu < 0.5)) return ORC_E_ARG;
     for (e = 0; e < s->nt * 4; ++e)

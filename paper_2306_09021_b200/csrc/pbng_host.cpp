@@ -726,7 +726,7 @@ pbng_status pbng_create_mesh(const double *rest_xyz, int64_t n_vertices, const i
 pbng_status pbng_set_material(pbng_ctx *c, pbng_model model, const double *E, int64_t n_E, double nu, double density,
                               const double gravity[3]) {
     if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
-    if (model != PBNG_NEOHOOKEAN && model != PBNG_FIXED_COROTATED)
+    if (model != PBNG_NEOHOOKEAN && model != PBNG_FIXED_COROTATED && model != PBNG_STABLE_NEOHOOKEAN)
         return fail(PBNG_E_INVALID_ARGUMENT, "set_material: unknown model");
     if (!E || (n_E != 1 && n_E != c->nt)) return fail(PBNG_E_INVALID_ARGUMENT, "set_material: E must have 1 or n_tets entries");
     for (int64_t k = 0; k < n_E; ++k)

@@ -10,7 +10,7 @@
 
 namespace pbng {
 
-enum { MODEL_NH = 0, MODEL_FCR = 1 };
+enum { MODEL_NH = 0, MODEL_FCR = 1, MODEL_SNH = 2 };
 enum { ACCEL_NONE = 0, ACCEL_SOR = 1, ACCEL_CHEB = 2 };
 enum { DT_F32 = 0, DT_F64 = 1 };
 

@@ -207,6 +207,17 @@ __device__ __forceinline__ void pair_contrib(const T (&d1)[3], const T (&d2)[3],
         const T s = (Vmu + Vlam) * (J - T(1)) - Vmu;
 #pragma unroll
         for (int r = 0; r < 3; ++r) f[r] -= Vmu * Fg[r] + s * w[r];
+    } else if (MODEL == MODEL_SNH) {
+        // eq:snh with mu_s = 4 mu/3, lambda_s = lambda + 5 mu/6, alpha = 1 + 3 mu_s/(4 lambda_s) (reading
+        // Z18): V P g = V mu_s (1 - 1/(1 + |F|^2)) F g + V lambda_s (J - alpha) cof(F) g
+        T ic = T(0);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) ic += F[r][0] * F[r][0] + F[r][1] * F[r][1] + F[r][2] * F[r][2];
+        const T Vms = T(4) / T(3) * Vmu, Vls = Vlam + T(5) / T(6) * Vmu;
+        const T alpha = T(1) + T(3) * Vms / (T(4) * Vls);
+        const T a = Vms * (T(1) - T(1) / (T(1) + ic)), b = Vls * (J - alpha);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) f[r] -= a * Fg[r] + b * w[r];
     } else {
         T Rm[3][3];
         polar_rotation(F, Rm);
@@ -337,10 +348,12 @@ template <> struct Rec<double> {
 // instead of 52 B and about 70 instead of 110 flops per pair.
 // ------------------------------------------------------------------------------------------------
 template <class R, int MODEL> struct Pair;
-template <class R> struct Pair<R, MODEL_FCR> {
+template <class R> struct PairG {  // gradient record (FCR, SNH)
     int4 id;
     R g1[3], g2[3], g3[3], VE;
 };
+template <class R> struct Pair<R, MODEL_FCR> : PairG<R> {};
+template <class R> struct Pair<R, MODEL_SNH> : PairG<R> {};
 template <class R> struct Pair<R, MODEL_NH> {
     int4 id;
     R u[3], s[3], gg, detB, VE;
@@ -348,7 +361,7 @@ template <class R> struct Pair<R, MODEL_NH> {
 
 // STREAM: read-once record (L1::no_allocate); otherwise cached (the batched kernel's broadcast loads)
 template <bool STREAM, class R>
-__device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<R, MODEL_FCR> &p) {
+__device__ __forceinline__ void load_pair(const Layout &L, int64_t r, PairG<R> &p) {
     if (STREAM) Rec<R>::load(L, r, p.id, p.g1, p.g2, p.g3, p.VE);
     else Rec<R>::load_shared(L, r, p.id, p.g1, p.g2, p.g3, p.VE);
 }
@@ -383,6 +396,14 @@ __device__ __forceinline__ void contrib(const T (&d1)[3], const T (&d2)[3], cons
     const T g1[3] = {T(p.g1[0]), T(p.g1[1]), T(p.g1[2])}, g2[3] = {T(p.g2[0]), T(p.g2[1]), T(p.g2[2])},
             g3[3] = {T(p.g3[0]), T(p.g3[1]), T(p.g3[2])};
     pair_contrib<MODEL_FCR, HESS>(d1, d2, d3, g1, g2, g3, T(p.VE) * cmu, T(p.VE) * clam, f, A);
+}
+
+template <bool HESS, class T, class R>
+__device__ __forceinline__ void contrib(const T (&d1)[3], const T (&d2)[3], const T (&d3)[3],
+                                        const Pair<R, MODEL_SNH> &p, T cmu, T clam, T (&f)[3], T (&A)[6]) {
+    const T g1[3] = {T(p.g1[0]), T(p.g1[1]), T(p.g1[2])}, g2[3] = {T(p.g2[0]), T(p.g2[1]), T(p.g2[2])},
+            g3[3] = {T(p.g3[0]), T(p.g3[1]), T(p.g3[2])};
+    pair_contrib<MODEL_SNH, HESS>(d1, d2, d3, g1, g2, g3, T(p.VE) * cmu, T(p.VE) * clam, f, A);
 }
 
 template <bool HESS, class T, class R>
@@ -723,7 +744,9 @@ cudaError_t sweep_dispatch2(const Problem &p, const Layout &L, const SweepLaunch
 
 template <class R>
 cudaError_t sweep_dispatch1(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
-    return p.model == MODEL_FCR ? sweep_dispatch2<R, MODEL_FCR>(p, L, s, st) : sweep_dispatch2<R, MODEL_NH>(p, L, s, st);
+    if (p.model == MODEL_FCR) return sweep_dispatch2<R, MODEL_FCR>(p, L, s, st);
+    if (p.model == MODEL_SNH) return sweep_dispatch2<R, MODEL_SNH>(p, L, s, st);
+    return sweep_dispatch2<R, MODEL_NH>(p, L, s, st);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -871,6 +894,17 @@ __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const
                     for (int c = 0; c < 3; ++c) fro += F[r][c] * F[r][c];
                 const double t = J - 1.0 - r_mu;
                 e = 0.5 * Vmu * (fro - 3.0) + 0.5 * (Vmu + Vlam) * t * t - 0.5 * Vmu * r_mu;
+            } else if (MODEL == MODEL_SNH) {
+                double ic = 0.0;
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) ic += F[r][c] * F[r][c];
+                const double Vms = 4.0 / 3.0 * Vmu, Vls = Vlam + 5.0 / 6.0 * Vmu;
+                const double al = 1.0 + 3.0 * Vms / (4.0 * Vls);
+                // shifted so that Psi(I) = 0 (as Z1 for eq:nh)
+                e = 0.5 * Vms * (ic - 3.0) + 0.5 * Vls * (J - al) * (J - al) - 0.5 * Vms * log(1.0 + ic) -
+                    (0.5 * Vls * (1.0 - al) * (1.0 - al) - 0.5 * Vms * log(4.0));
             } else {
                 double Rm[3][3];
                 polar_rotation(F, Rm);
@@ -1048,11 +1082,14 @@ cudaError_t launch_halo_unpack(const Problem &p, const Layout &L, const int32_t 
 }
 
 cudaError_t launch_energy_residual(const Problem &p, const Layout &L, int work, cudaStream_t st) {
-    if (p.dtype == DT_F64)
-        return p.model == MODEL_FCR ? energy_dispatch<double, MODEL_FCR>(p, L, work, st)
-                                    : energy_dispatch<double, MODEL_NH>(p, L, work, st);
-    return p.model == MODEL_FCR ? energy_dispatch<float, MODEL_FCR>(p, L, work, st)
-                                : energy_dispatch<float, MODEL_NH>(p, L, work, st);
+    if (p.dtype == DT_F64) {
+        if (p.model == MODEL_FCR) return energy_dispatch<double, MODEL_FCR>(p, L, work, st);
+        if (p.model == MODEL_SNH) return energy_dispatch<double, MODEL_SNH>(p, L, work, st);
+        return energy_dispatch<double, MODEL_NH>(p, L, work, st);
+    }
+    if (p.model == MODEL_FCR) return energy_dispatch<float, MODEL_FCR>(p, L, work, st);
+    if (p.model == MODEL_SNH) return energy_dispatch<float, MODEL_SNH>(p, L, work, st);
+    return energy_dispatch<float, MODEL_NH>(p, L, work, st);
 }
 
 int kernels_per_energy_residual() { return 3; }

@@ -20,7 +20,7 @@ STATUS = {0: "PBNG_OK", 1: "PBNG_E_INVALID_ARGUMENT", 2: "PBNG_E_INDEX_OUT_OF_RA
           4: "PBNG_E_ISOLATED_VERTEX", 5: "PBNG_E_BAD_ORDER", 6: "PBNG_E_NOT_COLORED", 7: "PBNG_E_NONFINITE",
           8: "PBNG_E_CUDA", 9: "PBNG_E_NCCL", 10: "PBNG_E_OUT_OF_MEMORY", 11: "PBNG_E_NO_DEVICE"}
 DTYPE = {"f32": 0, "f64": 1}
-MODEL = {"nh": 0, "fcr": 1}
+MODEL = {"nh": 0, "fcr": 1, "snh": 2}
 ACCEL = {"none": 0, "sor": 1, "chebyshev": 2}
 EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbng_color", "pbng_workspace_bytes",
            "pbng_bind_workspace", "pbng_set_positions", "pbng_get_positions", "pbng_iterate", "pbng_energy_residual",

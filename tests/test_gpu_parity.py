@@ -80,7 +80,7 @@ def test_parity_iterations(cfg, scale, dtype, accel):
     assert abs(rg[0] - r_at) <= (1e-9 if dtype == "f64" else 2e-3) * max(r_at, o.residual(s.x0[0]) * 1e-3)
 
 
-@pytest.mark.parametrize("model", ["nh", "fcr"])
+@pytest.mark.parametrize("model", ["nh", "fcr", "snh"])
 def test_fcr_and_nh_tiny_cube_fp64(model):
     s = G.config1_tiny_cube()
     s.model = model
@@ -118,6 +118,16 @@ def test_batched_sample_minor_layout_ragged(dtype):
     tol = 1e-14 if dtype == "f64" else 1e-6
     assert np.abs(alone[0] - xg[33]).max() <= tol * s.bbox_diag()
     assert abs(Ea[0] - Eg[33]) <= max(tol, 1e-12) * abs(Eg[33])
+
+
+@pytest.mark.parametrize("cfg,dtype", [(3, "f32"), (2, "f32"), (3, "f64")])
+def test_stable_neohookean_parity(cfg, dtype):
+    # eq:snh (reading Z18) on the NH and FCR scenes
+    s = G.make_config(cfg, "small")
+    s.model = "snh"
+    xg, Eg, _, _ = run_gpu(s, dtype)
+    xo, Eo, _, _ = run_oracle(s)
+    assert_parity(s, dtype, xg[0], Eg[0], xo, Eo)
 
 
 def test_energy_residual_at_x0_fp64():

@@ -43,6 +43,17 @@ def test_lame_rejects(E, nu):
         lame(E, nu)
 
 
+def test_snh_printed_form_with_reparameterised_lame():
+    # eq:snh evaluated literally with mu_s = 4 mu/3, lambda_s = lambda + 5 mu/6 and the
+    # volume coefficient lambda_s / 2 (reading Z18), raw (unshifted) at a generic F
+    mu, lam = 1.3, 2.2
+    ms, ls = 4 * mu / 3, lam + 5 * mu / 6
+    F = np.array([[1.1, 0.2, -0.1], [0.05, 0.9, 0.3], [0.0, -0.2, 1.2]])
+    ic, J = np.sum(F * F), np.linalg.det(F)
+    printed = 0.5 * ms * (ic - 3) + 0.5 * ls * (J - 1 - 3 * ms / (4 * ls)) ** 2 - 0.5 * ms * np.log(1 + ic)
+    assert abs(psi("snh", mu, lam, F, raw=True) - printed) < 1e-13
+
+
 def test_psi_golden():
     g = json.load(open(os.path.join(GOLD, "closed_forms.json")))
     for row in g["psi"]:
@@ -64,7 +75,7 @@ def test_cofactor_identities():
     assert np.allclose(cofactor(F) @ F.T, 0.0, atol=1e-12)
 
 
-@pytest.mark.parametrize("model", ["nh", "fcr"])
+@pytest.mark.parametrize("model", ["nh", "fcr", "snh"])
 def test_zero_energy_and_stress_at_rest(model):
     mu, lam = lame(1e5, 0.3)
     assert abs(psi(model, mu, lam, np.eye(3))) < 1e-9
@@ -76,7 +87,7 @@ def test_zero_energy_and_stress_at_rest(model):
             assert np.abs(piola(model, mu, lam, Q)).max() < 1e-6
 
 
-@pytest.mark.parametrize("model", ["nh", "fcr"])
+@pytest.mark.parametrize("model", ["nh", "fcr", "snh"])
 def test_piola_matches_finite_differences(model):
     mu, lam = 1.3, 2.1
     for t in range(60):
@@ -92,7 +103,7 @@ def test_piola_matches_finite_differences(model):
         assert np.abs(P - Pfd).max() <= 1e-6 * (1 + np.abs(P).max())
 
 
-@pytest.mark.parametrize("model", ["nh", "fcr"])
+@pytest.mark.parametrize("model", ["nh", "fcr", "snh"])
 def test_rotation_invariance(model):
     mu, lam = 1.7, 0.9
     for t in range(60):
@@ -141,10 +152,11 @@ def _fd_density_hessian(model, mu, lam, F, h=1e-5):
     return 0.5 * (H + H.T)
 
 
-@pytest.mark.parametrize("model", ["nh", "fcr"])
+@pytest.mark.parametrize("model", ["nh", "fcr", "snh"])
 def test_lame_consistency_at_identity(model):
     # the Hessian at F = I must equal linear elasticity's 2 mu P_sym + lambda I(x)I, which is
-    # why eq:nh uses lambdahat = mu + lambda.  Also Ctilde(I) - C(I) = 2 mu P_skew (PSD).
+    # why eq:nh uses lambdahat = mu + lambda (and why eq:snh is read with the cited model's re-parameterised
+    # Lame pair, reading Z18).  Also Ctilde(I) - C(I) = 2 mu P_skew (PSD).
     mu, lam = lame(1e5, 0.3)
     H = _fd_density_hessian(model, mu, lam, np.eye(3), h=1e-4)
     I9 = np.eye(9)

@@ -13,12 +13,11 @@ from test_oracle_mesh import make_scene
 
 def scene_with_model(model):
     s = G.config1_tiny_cube()
-    if model == "fcr":
-        s.model = "fcr"
+    s.model = model
     return s
 
 
-@pytest.mark.parametrize("model", ["nh", "fcr"])
+@pytest.mark.parametrize("model", ["nh", "fcr", "snh"])
 def test_nodal_force_is_minus_energy_gradient(model):
     # P4: f_i + f^ext_i = -dE/dx_i by central differences of the total energy
     s = scene_with_model(model)
@@ -279,7 +278,7 @@ def _newton(o, s, x0, tol=1e-12, max_it=60):
     return x.reshape(-1, 3), r0
 
 
-@pytest.mark.parametrize("model", ["nh", "fcr"])
+@pytest.mark.parametrize("model", ["nh", "fcr", "snh"])
 def test_pbng_fixed_point_equals_global_newton(model):
     # P11 / north_star item 4: every stationary point of the sweep has f_i + f^ext_i = 0
     s = scene_with_model(model)
