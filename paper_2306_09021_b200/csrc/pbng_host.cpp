@@ -55,19 +55,6 @@ double det3(const double *M) {
            M[2] * (M[3] * M[7] - M[4] * M[6]);
 }
 
-// cofactor matrix, cof(M)_ab = d det M / d M_ab (row-major)
-void cof3(const double *M, double *C) {
-    C[0] = M[4] * M[8] - M[5] * M[7];
-    C[1] = M[5] * M[6] - M[3] * M[8];
-    C[2] = M[3] * M[7] - M[4] * M[6];
-    C[3] = M[2] * M[7] - M[1] * M[8];
-    C[4] = M[0] * M[8] - M[2] * M[6];
-    C[5] = M[1] * M[6] - M[0] * M[7];
-    C[6] = M[1] * M[5] - M[2] * M[4];
-    C[7] = M[2] * M[3] - M[0] * M[5];
-    C[8] = M[0] * M[4] - M[1] * M[3];
-}
-
 // Chebyshev weights: omega_m = 1 (m <= 2), 2/(2-rho^2) (m = 3), 4/(4 - rho^2 omega_{m-1})
 double chebyshev_weight(int64_t m, double rho) {
     if (m <= 2) return 1.0;
@@ -289,8 +276,8 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     const int64_t ns = std::max<int64_t>(c->n_slots, 1);
     c->h_rec_id.assign((size_t)ns, make_int4(0, 0, 0, 0));
     c->h_rec_a.assign((size_t)ns * s4, 0);
-    c->h_rec_b.assign((size_t)ns * s4, 0);
     const bool nh = c->model == MODEL_NH;
+    c->h_rec_b.assign(nh ? s4 : (size_t)ns * s4, 0);  // NH: unused
     // rec_c: FCR g3z (+ VE in fp64); NH: VE in fp64, unused in fp32 (VE rides in rec_id.w)
     const size_t rec_c_bytes = nh ? (c->dtype == DT_F64 ? s : 0) : (c->dtype == DT_F64 ? 2 * s : s);
     c->h_rec_c.assign(std::max<size_t>((size_t)ns * rec_c_bytes, s), 0);
@@ -321,19 +308,13 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
                 }
                 c->h_rec_id[r] = id;
                 if (nh) {
-                    // compact Neo-Hookean record: u = cof(B) g_i, s_j = g_j . g_i, |g_i|^2, det B, with
-                    // B = rows g_j of the three other vertices (pbng_kernels.cu, Pair<R, MODEL_NH>)
-                    double gi[3], cof[9], u[3], sj[3];
+                    // compact Neo-Hookean record: s_j = g_j . g_i and det B, with B = rows g_j of the three
+                    // other vertices (pbng_kernels.cu, Pair<R, MODEL_NH>); |g_i|^2 = -(s_1 + s_2 + s_3)
+                    double gi[3], sj[3];
                     shape_grad(c, e, a, gi);
                     const double Bp[9] = {g[0][0], g[0][1], g[0][2], g[1][0], g[1][1], g[1][2], g[2][0], g[2][1], g[2][2]};
-                    cof3(Bp, cof);
-                    for (int q2 = 0; q2 < 3; ++q2) {
-                        u[q2] = cof[3 * q2] * gi[0] + cof[3 * q2 + 1] * gi[1] + cof[3 * q2 + 2] * gi[2];
-                        sj[q2] = g[q2][0] * gi[0] + g[q2][1] * gi[1] + g[q2][2] * gi[2];
-                    }
-                    const double gg = gi[0] * gi[0] + gi[1] * gi[1] + gi[2] * gi[2];
-                    put4<R>(c->h_rec_a, r, u[0], u[1], u[2], sj[0]);
-                    put4<R>(c->h_rec_b, r, sj[1], sj[2], gg, det3(Bp));
+                    for (int q2 = 0; q2 < 3; ++q2) sj[q2] = g[q2][0] * gi[0] + g[q2][1] * gi[1] + g[q2][2] * gi[2];
+                    put4<R>(c->h_rec_a, r, sj[0], sj[1], sj[2], det3(Bp));
                     if (c->dtype == DT_F64) put1<R>(c->h_rec_c, r, VE);
                 } else {
                     put4<R>(c->h_rec_a, r, g[0][0], g[0][1], g[0][2], g[1][0]);
@@ -482,7 +463,7 @@ void plan_workspace(pbng_ctx *c) {
     const int64_t ns = std::max<int64_t>(c->n_slots, 1);
     take(c->r_rec_id, (size_t)ns * 16);
     take(c->r_rec_a, (size_t)ns * s4);
-    take(c->r_rec_b, (size_t)ns * s4);
+    take(c->r_rec_b, c->h_rec_b.size());
     take(c->r_rec_c, c->h_rec_c.size());
     take(c->r_chunk_off, c->h_chunk_off.size() * 8);
     take(c->r_chunk_v, std::max<size_t>(c->h_chunk_v.size(), 1) * 8);
@@ -521,7 +502,7 @@ double sweep_bytes_model(const pbng_ctx *c) {
     // samples of a batch), chunk offsets, per free vertex and sample: degree, position write, blend
     // traffic (x^{l-1} read, x^{l-1} and x^{l+1} writes) and body force; all positions read once.
     const double s = (double)c->real_size();
-    const double rec = c->model == MODEL_NH ? (c->dtype == DT_F64 ? 88.0 : 48.0) : (c->dtype == DT_F64 ? 96.0 : 52.0);
+    const double rec = c->model == MODEL_NH ? (c->dtype == DT_F64 ? 56.0 : 32.0) : (c->dtype == DT_F64 ? 96.0 : 52.0);
     double b = (double)c->n_pairs * rec + (double)(c->n_chunks + 1) * 8.0 + (double)c->n_free * 4.0;
     double per_v = 3 * s;  // write x_PBNG
     per_v += (c->prob.has_fext ? 3 * s : 0);

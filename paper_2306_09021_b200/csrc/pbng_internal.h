@@ -24,11 +24,15 @@ constexpr int kRedBlock = 256;    // threads per reduction CTA
 
 // Pair-record layout (SELL-32, one record per (free vertex i, incident tet e), vertex-major within a
 // 32-vertex chunk: slot = chunk_off[chunk] + k * 32 + lane).  For the tet's three OTHER vertices j
-// (in slot order) the record holds the internal vertex ids and the shape-function gradients g_j
-// (rows of Dm^{-1} or minus their sum); g_i = -(g_1 + g_2 + g_3); VE = V_e E_e.
-//   f32: rec_id int4 {n1, n2, n3, bits(VE)}; rec_a float4 {g1x g1y g1z g2x}; rec_b float4
-//        {g2y g2z g3x g3y}; rec_c float {g3z}                                      -> 52 bytes
-//   f64: rec_id int4 {n1, n2, n3, 0}; rec_a double4; rec_b double4; rec_c double2 {g3z, VE} -> 96 bytes
+// (in slot order) the record holds the internal vertex ids and rest-shape data derived from the
+// shape-function gradients g_j (rows of Dm^{-1}); g_i = -(g_1 + g_2 + g_3); VE = V_e E_e.
+//   fixed-corotated / stable NH (needs F):
+//     f32: rec_id int4 {n1, n2, n3, bits(VE)}; rec_a float4 {g1x g1y g1z g2x}; rec_b float4
+//          {g2y g2z g3x g3y}; rec_c float {g3z}                                    -> 52 bytes
+//     f64: rec_id int4 {n1, n2, n3, 0}; rec_a double4; rec_b double4; rec_c double2 {g3z, VE} -> 96 bytes
+//   Neo-Hookean (needs F g_i, cof(F) g_i, det F only; pbng_kernels.cu Pair<R, MODEL_NH>):
+//     f32: rec_id int4 {n1, n2, n3, bits(VE)}; rec_a float4 {s1 s2 s3 detB}, s_j = g_j . g_i -> 32 bytes
+//     f64: rec_id int4 {n1, n2, n3, 0}; rec_a double4 {s1 s2 s3 detB}; rec_c double {VE}     -> 56 bytes
 struct Layout {
     const int4 *rec_id = nullptr;
     const void *rec_a = nullptr, *rec_b = nullptr, *rec_c = nullptr;

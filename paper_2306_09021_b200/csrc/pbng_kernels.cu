@@ -340,12 +340,15 @@ template <> struct Rec<double> {
 
 // ------------------------------------------------------------------------------------------------
 // Pair records decoded in registers.  Fixed-corotated needs F itself (for R(F)), so its record carries
-// the three shape-function gradients g_j.  Neo-Hookean only needs F g_i, cof(F) g_i and det F, and with
-// F = Ds B (Ds = [d_1 d_2 d_3], B = rows g_j):
-//   F g_i = sum_j d_j (g_j . g_i),   cof(F) g_i = cof(Ds) (cof(B) g_i) = sum_k u_k c_k,   det F = det Ds det B
-// with c_1 = d_2 x d_3, c_2 = d_3 x d_1, c_3 = d_1 x d_2 (the columns of cof Ds, cof being multiplicative),
-// so its record carries u = cof(B) g_i, s_j = g_j . g_i, |g_i|^2 and det B (precomputed in fp64): 48 B
-// instead of 52 B and about 70 instead of 110 flops per pair.
+// the three shape-function gradients g_j.  Neo-Hookean only needs F g_i, cof(F) g_i and det F.  With
+// F = Ds B (Ds = [d_1 d_2 d_3], d_j = x_j - x_i, B = Dm^{-1} with rows g_j, g_i = -(g_1 + g_2 + g_3)):
+//   F g_i = sum_j s_j d_j  with s_j = g_j . g_i,
+//   cof(F) g_i = cof(Ds) cof(B) g_i = cof(Ds) Dm^T g_i / det Dm = -det B (c_1 + c_2 + c_3)
+//     (g_i . D_k = -1 because B Dm = I), where c_1 + c_2 + c_3 = d_2 x d_3 + d_3 x d_1 + d_1 x d_2
+//     = (d_2 - d_1) x (d_3 - d_1) =: n, the deformed face normal opposite vertex i,
+//   det F = det Ds det B = (d_1 . n) det B,   |g_i|^2 = -(s_1 + s_2 + s_3),
+// so its record carries s_1, s_2, s_3 and det B (precomputed in fp64): 32 B per pair in fp32 instead of
+// 52 B, and about 60 instead of 110 flops per pair.
 // ------------------------------------------------------------------------------------------------
 template <class R, int MODEL> struct Pair;
 template <class R> struct PairG {  // gradient record (FCR, SNH)
@@ -356,7 +359,7 @@ template <class R> struct Pair<R, MODEL_FCR> : PairG<R> {};
 template <class R> struct Pair<R, MODEL_SNH> : PairG<R> {};
 template <class R> struct Pair<R, MODEL_NH> {
     int4 id;
-    R u[3], s[3], gg, detB, VE;
+    R s[3], detB, VE;
 };
 
 // STREAM: read-once record (L1::no_allocate); otherwise cached (the batched kernel's broadcast loads)
@@ -368,25 +371,19 @@ __device__ __forceinline__ void load_pair(const Layout &L, int64_t r, PairG<R> &
 template <bool STREAM>
 __device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<float, MODEL_NH> &p) {
     const float4 *a = reinterpret_cast<const float4 *>(L.rec_a) + r;
-    const float4 *b = reinterpret_cast<const float4 *>(L.rec_b) + r;
     const int4 id = STREAM ? lds(L.rec_id + r) : ld(L.rec_id + r);
     const float4 x = STREAM ? lds(a) : ld(a);
-    const float4 y = STREAM ? lds(b) : ld(b);
     p.id = id;
-    p.u[0] = x.x; p.u[1] = x.y; p.u[2] = x.z; p.s[0] = x.w;
-    p.s[1] = y.x; p.s[2] = y.y; p.gg = y.z; p.detB = y.w;
+    p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
     p.VE = __int_as_float(id.w);
 }
 template <bool STREAM>
 __device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<double, MODEL_NH> &p) {
     const double4 *a = reinterpret_cast<const double4 *>(L.rec_a) + r;
-    const double4 *b = reinterpret_cast<const double4 *>(L.rec_b) + r;
     const double *c = reinterpret_cast<const double *>(L.rec_c) + r;
     p.id = STREAM ? lds(L.rec_id + r) : ld(L.rec_id + r);
     const double4 x = STREAM ? lds(a) : ld(a);
-    const double4 y = STREAM ? lds(b) : ld(b);
-    p.u[0] = x.x; p.u[1] = x.y; p.u[2] = x.z; p.s[0] = x.w;
-    p.s[1] = y.x; p.s[2] = y.y; p.gg = y.z; p.detB = y.w;
+    p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
     p.VE = ld(c);
 }
 
@@ -409,23 +406,24 @@ __device__ __forceinline__ void contrib(const T (&d1)[3], const T (&d2)[3], cons
 template <bool HESS, class T, class R>
 __device__ __forceinline__ void contrib(const T (&d1)[3], const T (&d2)[3], const T (&d3)[3],
                                         const Pair<R, MODEL_NH> &p, T cmu, T clam, T (&f)[3], T (&A)[6]) {
-    // columns of cof(Ds)
-    const T c1[3] = {d2[1] * d3[2] - d2[2] * d3[1], d2[2] * d3[0] - d2[0] * d3[2], d2[0] * d3[1] - d2[1] * d3[0]};
-    const T c2[3] = {d3[1] * d1[2] - d3[2] * d1[1], d3[2] * d1[0] - d3[0] * d1[2], d3[0] * d1[1] - d3[1] * d1[0]};
-    const T c3[3] = {d1[1] * d2[2] - d1[2] * d2[1], d1[2] * d2[0] - d1[0] * d2[2], d1[0] * d2[1] - d1[1] * d2[0]};
-    const T J = (d1[0] * c1[0] + d1[1] * c1[1] + d1[2] * c1[2]) * T(p.detB);
-    const T u0 = T(p.u[0]), u1 = T(p.u[1]), u2 = T(p.u[2]), s0 = T(p.s[0]), s1 = T(p.s[1]), s2 = T(p.s[2]);
+    // n = (d_2 - d_1) x (d_3 - d_1) = sum of the columns of cof(Ds)
+    const T e1[3] = {d2[0] - d1[0], d2[1] - d1[1], d2[2] - d1[2]};
+    const T e2[3] = {d3[0] - d1[0], d3[1] - d1[1], d3[2] - d1[2]};
+    const T n[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+    const T detB = T(p.detB);
+    const T J = (d1[0] * n[0] + d1[1] * n[1] + d1[2] * n[2]) * detB;
+    const T s0 = T(p.s[0]), s1 = T(p.s[1]), s2 = T(p.s[2]);
     const T Vmu = T(p.VE) * cmu, Vlam = T(p.VE) * clam;
     const T sc = (Vmu + Vlam) * (J - T(1)) - Vmu;  // lamhat (J - 1) - mu, times V (eq:nh)
     T w[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-        w[r] = u0 * c1[r] + u1 * c2[r] + u2 * c3[r];                   // cof(F) g_i
+        w[r] = -detB * n[r];                                           // cof(F) g_i
         const T Fg = s0 * d1[r] + s1 * d2[r] + s2 * d3[r];             // F g_i
         f[r] -= Vmu * Fg + sc * w[r];
     }
     if (HESS) {
-        const T dg = T(2) * Vmu * T(p.gg);
+        const T dg = T(-2) * Vmu * (s0 + s1 + s2);                     // 2 mu V |g_i|^2
         A[0] += dg + Vlam * w[0] * w[0];
         A[1] += dg + Vlam * w[1] * w[1];
         A[2] += dg + Vlam * w[2] * w[2];
@@ -541,6 +539,10 @@ __device__ __forceinline__ void finish_vertex(const Layout &L, typename RT<R>::R
 // 32 lanes is one contiguous 512 B (f32) segment per field.  The record stream is read once with
 // L1::no_allocate; the neighbour positions are gathered through L1 (different colour, read-only in this
 // launch).  The per-vertex summation order is ascending tet index, as in the oracle.
+#ifndef PBNG_SWEEP_UNROLL
+#define PBNG_SWEEP_UNROLL 2
+#endif
+constexpr int kSweepUnroll = PBNG_SWEEP_UNROLL;  // pair-loop unroll (loads of record k+1 issued early)
 template <class R, int MODEL, int ACCEL, bool FEXT, bool WC>
 #ifndef PBNG_SWEEP_MINB
 #define PBNG_SWEEP_MINB 1
@@ -567,6 +569,7 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_kernel(con
     }
     R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
 
+#pragma unroll kSweepUnroll
     for (int k = 0; k < deg; ++k) {
         Pair<R, MODEL> pr;
         load_pair<true>(L, base + (int64_t)k * kChunk, pr);
@@ -740,13 +743,6 @@ cudaError_t sweep_dispatch2(const Problem &p, const Layout &L, const SweepLaunch
         case ACCEL_CHEB: return sweep_dispatch3<R, MODEL, ACCEL_CHEB>(p, L, s, st);
         default: return sweep_dispatch3<R, MODEL, ACCEL_NONE>(p, L, s, st);
     }
-}
-
-template <class R>
-cudaError_t sweep_dispatch1(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
-    if (p.model == MODEL_FCR) return sweep_dispatch2<R, MODEL_FCR>(p, L, s, st);
-    if (p.model == MODEL_SNH) return sweep_dispatch2<R, MODEL_SNH>(p, L, s, st);
-    return sweep_dispatch2<R, MODEL_NH>(p, L, s, st);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1033,9 +1029,38 @@ __global__ void polar_test_kernel(const double *F, double *Rout, int64_t n) {
 
 }  // namespace
 
+// Per-(dtype, model) entry points.  build.py compiles this file once per (dtype, model) with
+// PBNG_TU_R / PBNG_TU_MODEL set (the sweep and energy/residual instantiations of that pair, compiled in
+// parallel) and once without them (the dispatchers and the model-independent kernels).
+template <class R, int MODEL>
+cudaError_t sweep_entry(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st);
+template <class R, int MODEL>
+cudaError_t energy_entry(const Problem &p, const Layout &L, int work, cudaStream_t st);
+
+#if defined(PBNG_TU_R)
+template <class R, int MODEL>
+cudaError_t sweep_entry(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
+    return sweep_dispatch2<R, MODEL>(p, L, s, st);
+}
+template <class R, int MODEL>
+cudaError_t energy_entry(const Problem &p, const Layout &L, int work, cudaStream_t st) {
+    return energy_dispatch<R, MODEL>(p, L, work, st);
+}
+template cudaError_t sweep_entry<PBNG_TU_R, PBNG_TU_MODEL>(const Problem &, const Layout &, const SweepLaunch &,
+                                                           cudaStream_t);
+template cudaError_t energy_entry<PBNG_TU_R, PBNG_TU_MODEL>(const Problem &, const Layout &, int, cudaStream_t);
+#else
+
 cudaError_t launch_sweep(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
     if (s.n_v <= 0) return cudaSuccess;
-    return p.dtype == DT_F64 ? sweep_dispatch1<double>(p, L, s, st) : sweep_dispatch1<float>(p, L, s, st);
+    if (p.dtype == DT_F64) {
+        if (p.model == MODEL_FCR) return sweep_entry<double, MODEL_FCR>(p, L, s, st);
+        if (p.model == MODEL_SNH) return sweep_entry<double, MODEL_SNH>(p, L, s, st);
+        return sweep_entry<double, MODEL_NH>(p, L, s, st);
+    }
+    if (p.model == MODEL_FCR) return sweep_entry<float, MODEL_FCR>(p, L, s, st);
+    if (p.model == MODEL_SNH) return sweep_entry<float, MODEL_SNH>(p, L, s, st);
+    return sweep_entry<float, MODEL_NH>(p, L, s, st);
 }
 
 // n_buffers = -1: write the staged array into the backward-Euler target xtilde instead
@@ -1083,13 +1108,13 @@ cudaError_t launch_halo_unpack(const Problem &p, const Layout &L, const int32_t 
 
 cudaError_t launch_energy_residual(const Problem &p, const Layout &L, int work, cudaStream_t st) {
     if (p.dtype == DT_F64) {
-        if (p.model == MODEL_FCR) return energy_dispatch<double, MODEL_FCR>(p, L, work, st);
-        if (p.model == MODEL_SNH) return energy_dispatch<double, MODEL_SNH>(p, L, work, st);
-        return energy_dispatch<double, MODEL_NH>(p, L, work, st);
+        if (p.model == MODEL_FCR) return energy_entry<double, MODEL_FCR>(p, L, work, st);
+        if (p.model == MODEL_SNH) return energy_entry<double, MODEL_SNH>(p, L, work, st);
+        return energy_entry<double, MODEL_NH>(p, L, work, st);
     }
-    if (p.model == MODEL_FCR) return energy_dispatch<float, MODEL_FCR>(p, L, work, st);
-    if (p.model == MODEL_SNH) return energy_dispatch<float, MODEL_SNH>(p, L, work, st);
-    return energy_dispatch<float, MODEL_NH>(p, L, work, st);
+    if (p.model == MODEL_FCR) return energy_entry<float, MODEL_FCR>(p, L, work, st);
+    if (p.model == MODEL_SNH) return energy_entry<float, MODEL_SNH>(p, L, work, st);
+    return energy_entry<float, MODEL_NH>(p, L, work, st);
 }
 
 int kernels_per_energy_residual() { return 3; }
@@ -1101,5 +1126,7 @@ cudaError_t launch_polar_test(int dtype, const double *F, double *R, int64_t n, 
     else polar_test_kernel<float><<<g, 128, 0, st>>>(F, R, n);
     return cudaGetLastError();
 }
+
+#endif  // PBNG_TU_R
 
 }  // namespace pbng
