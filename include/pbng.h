@@ -94,7 +94,21 @@ typedef struct {
     int64_t n_local_vertices; /* vertices held by this context (owned free + ghosts + held pinned) */
     int64_t n_ghosts;         /* free vertices owned by other ranks and held here */
     int32_t rank, n_ranks;
+    int32_t schedule;         /* pbng_schedule pbng_iterate uses now (1 colour launches, 2 pipelined) */
+    int32_t reserved;
 } pbng_info;
+
+/* How pbng_iterate orders the colour passes (PAPER.md:693-705 fixes only the ORDER: colour after colour,
+ * each pass reading the latest values of the other colours).
+ * PBNG_SCHEDULE_COLOUR_LAUNCHES: one kernel launch per colour pass (a grid-wide barrier between colours).
+ * PBNG_SCHEDULE_PIPELINED: one persistent launch runs up to 64 whole iterations; a 32-vertex chunk starts
+ *   as soon as the chunks holding its stencil neighbours have finished the passes it must read after
+ *   (earlier colours: this iteration; later colours and itself: the previous one).  Every vertex reads
+ *   exactly the values the barrier schedule gives it, so the iterates are bitwise identical; only the
+ *   barrier stalls disappear.  Needs an undecomposed context with n_batch < 32.
+ * PBNG_SCHEDULE_AUTO (default): pipelined for small problems (few 32-vertex chunks per colour, where the
+ *   colour passes are launch / barrier latency bound), colour launches otherwise. */
+typedef enum { PBNG_SCHEDULE_AUTO = 0, PBNG_SCHEDULE_COLOUR_LAUNCHES = 1, PBNG_SCHEDULE_PIPELINED = 2 } pbng_schedule;
 
 /* Create a mesh context: rest positions X (n_vertices*3 doubles), tets (n_tets*4
  * int32, any orientation), n_batch >= 1 independent samples sharing mesh, material and colouring
@@ -200,6 +214,11 @@ pbng_status pbng_synchronize(pbng_ctx *ctx);
 
 /* Sizes, byte / flop model and counters. */
 pbng_status pbng_query(pbng_ctx *ctx, pbng_info *info);
+
+/* Choose the schedule of pbng_iterate (pbng_schedule above).  PBNG_SCHEDULE_PIPELINED requires a coloured
+ * context that supports it (PBNG_E_NOT_COLORED / PBNG_E_INVALID_ARGUMENT otherwise).  Results do not
+ * depend on the schedule.  Host-only; may be called between iterations. */
+pbng_status pbng_set_schedule(pbng_ctx *ctx, pbng_schedule schedule);
 
 /* Timing of the colour-sweep kernel with CUDA events on the context stream (bench.py's roofline).
  * enable = 1: an event pair around every sweep launch; enable = 2: an event pair around the

@@ -142,12 +142,15 @@ struct pbng_ctx {
     std::vector<int2> h_chunk_v;
     std::vector<int32_t> h_deg, h_wc_off, h_wc_cid, h_c_n, h_c_node;
     std::vector<unsigned char> h_mass;  // Real [n_own] lumped masses (backward Euler)
+    std::vector<int32_t> h_dep_off, h_deps;  // pipelined schedule: per chunk its neighbour chunks (Layout)
+    int schedule = 0;                        // pbng_schedule requested (0 auto, 1 colour launches, 2 pipelined)
     std::vector<int4> h_tet_id;
     Problem prob;
     // workspace plan
     Region r_rec_id, r_rec_a, r_rec_b, r_rec_c, r_chunk_off, r_chunk_v, r_deg, r_fext, r_wc_off, r_wc_cid, r_wc_d,
         r_c_n, r_c_node, r_c_w, r_c_anchor, r_c_K, r_tet_id, r_tet_a, r_tet_b, r_tet_c, r_int2orig, r_targets,
-        r_x[3], r_stage, r_part_e, r_part_r, r_results, r_flag, r_halo_send, r_halo_recv, r_mass, r_xt;
+        r_x[3], r_stage, r_part_e, r_part_r, r_results, r_flag, r_halo_send, r_halo_recv, r_mass, r_xt, r_dep_off,
+        r_deps, r_pipe;
     size_t ws_need = 0;
     // bound device state
     bool bound = false;
@@ -451,6 +454,67 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     p.gr = (int)std::max<int64_t>(1, std::min<int64_t>((n_chunks * kChunk + kRedBlock - 1) / kRedBlock, 1184));
 }
 
+// Pipelined schedule (pbng_kernels.cu sweep_pipe_kernel): for every chunk, the chunks holding the other
+// nodes of its vertices' stencils (tets and weak constraints) and the chunk itself, each tagged with
+// whether it belongs to an earlier colour (must have finished the current iteration) or not (the
+// previous one).  Only for an undecomposed context (ghost values arrive by halo exchange between
+// colour passes, which needs the per-colour launches).
+void build_pipeline(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::vector<int32_t> &vt) {
+    c->h_dep_off.assign((size_t)c->n_chunks + 1, 0);
+    c->h_deps.clear();
+    if (c->n_ranks > 1) return;
+    std::vector<int32_t> chunk_of((size_t)std::max<int64_t>(c->n_free, 1), -1), chunk_col((size_t)std::max<int64_t>(c->n_chunks, 1), 0);
+    for (int32_t col = 0; col < c->ncol; ++col)
+        for (int64_t ch = c->col_chunk[col]; ch < c->col_chunk[col + 1]; ++ch) {
+            chunk_col[ch] = col;
+            const int2 cv = c->h_chunk_v[ch];
+            for (int32_t q = 0; q < cv.y; ++q) chunk_of[cv.x + q] = (int32_t)ch;
+        }
+    std::vector<int32_t> tmp;
+    for (int64_t ch = 0; ch < c->n_chunks; ++ch) {
+        tmp.clear();
+        tmp.push_back((int32_t)ch);
+        const int2 cv = c->h_chunk_v[ch];
+        auto add = [&](int32_t j) {
+            if (j >= 0 && j < c->n_free) tmp.push_back(chunk_of[j]);
+        };
+        for (int32_t q = 0; q < cv.y; ++q) {
+            const int32_t i = cv.x + q, o = c->int2orig[i];
+            for (int64_t k = vt_off[o]; k < vt_off[o + 1]; ++k) {
+                const int32_t *t = c->tets.data() + 4 * vt[k];
+                for (int a = 0; a < 4; ++a) add(c->orig2int[t[a]]);
+            }
+            for (int32_t k = c->h_wc_off[i]; k < c->h_wc_off[i + 1]; ++k) {
+                const int32_t cid = c->h_wc_cid[k];
+                for (int32_t m = 0; m < c->h_c_n[cid]; ++m) add(c->h_c_node[kWcMaxNodes * cid + m]);
+            }
+        }
+        std::sort(tmp.begin(), tmp.end());
+        tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+        for (int32_t y : tmp) c->h_deps.push_back((y << 1) | (chunk_col[y] < chunk_col[ch] ? 1 : 0));
+        c->h_dep_off[ch + 1] = (int32_t)c->h_deps.size();
+    }
+}
+
+bool pipeline_available(const pbng_ctx *c) { return c->n_ranks == 1 && c->prob.lane_shift == 0 && c->n_chunks > 0; }
+
+int problem_split(const pbng_ctx *c);
+
+// schedule pbng_iterate uses: 1 = one launch per colour pass, 2 = pipelined (PBNG_SCHEDULE env overrides
+// auto).  Auto pipelines small problems, whose colour passes are too short to fill the machine (launch
+// and barrier latency dominate; measured 1.3x on config 1); large ones keep the colour launches, whose
+// neighbour gathers may use the read-only L1 path (the pipelined kernel needs coherent loads, measured
+// 7% slower on config 3).
+int effective_schedule(const pbng_ctx *c) {
+    static const int env = [] {
+        const char *e = getenv("PBNG_SCHEDULE");
+        return e ? atoi(e) : 0;
+    }();
+    int want = c->schedule != 0 ? c->schedule : env;
+    if (want == 0) want = problem_split(c) == 4 ? 2 : 1;
+    return (want == 2 && pipeline_available(c)) ? 2 : 1;
+}
+
 void plan_workspace(pbng_ctx *c) {
     size_t off = 0;
     auto take = [&](Region &r, size_t bytes) {
@@ -494,6 +558,9 @@ void plan_workspace(pbng_ctx *c) {
     take(c->r_xt, (groups << p.lane_shift) * (size_t)p.x_stride * s4);
     take(c->r_halo_send, std::max<size_t>(c->h_halo_send.size(), 1) * 4);
     take(c->r_halo_recv, std::max<size_t>(c->h_halo_recv.size(), 1) * 4);
+    take(c->r_dep_off, c->h_dep_off.size() * 4);
+    take(c->r_deps, std::max<size_t>(c->h_deps.size(), 1) * 4);
+    take(c->r_pipe, 8 + (size_t)c->nb * (size_t)std::max<int64_t>(c->n_chunks, 1) * 4);  // counter, flags
     c->ws_need = off;
 }
 
@@ -514,9 +581,11 @@ double accel_bytes_model(const pbng_ctx *c) {
     return (double)c->nb * (double)c->n_free * 9.0 * (double)c->real_size();
 }
 
-// Warps per 32-vertex chunk for a colour pass: the fixed-corotated pair (a polar decomposition) is
-// compute-heavy, and small colours leave SMs idle with one thread per vertex, so both split the pair
-// loop over several warps.  PBNG_SPLIT=1|2|4 overrides (experiments).
+// Warps per 32-vertex chunk (sweep_split_kernel / the pipelined kernel's groups), ONE value per problem so
+// that both schedules and every rank of a decomposition sum each vertex's terms in the same order: the
+// fixed-corotated pair (a polar decomposition) is compute-heavy, and with few chunks per colour one warp
+// per chunk leaves the machine idle (the colour's dependency chain is then latency bound), so both split
+// the pair loop over several warps.  PBNG_SPLIT=1|2|4 overrides (experiments).
 bool batched_layout(const pbng_ctx *c) {
     static const int mode = [] {
         const char *e = getenv("PBNG_BATCHED");
@@ -525,16 +594,18 @@ bool batched_layout(const pbng_ctx *c) {
     return mode != 0 && c->nb >= 32;
 }
 
-int choose_split(const pbng_ctx *c, int64_t n_v) {
+int problem_split(const pbng_ctx *c) {
     static const int forced = [] {
         const char *e = getenv("PBNG_SPLIT");
         return e ? atoi(e) : 0;
     }();
-    if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
-    const int64_t threads = n_v * c->nb;  // n_v: the colour's GLOBAL free count (same split on every rank)
+    if (forced == 1 || forced == 2 || forced == 4) return forced;
     if (c->model == MODEL_FCR) return 4;
-    if (threads < 148 * 512) return 4;
-    if (threads < 148 * 1024) return 2;
+    int64_t gfree = 0;  // free vertices of the whole mesh (all ranks)
+    for (int64_t k : c->gcol_nfree) gfree += k;
+    const int64_t chunks_per_colour = gfree * c->nb / kChunk / std::max(c->ncol, 1);
+    if (chunks_per_colour < 148 * 16) return 4;
+    if (chunks_per_colour < 148 * 32) return 2;
     return 1;
 }
 
@@ -556,17 +627,21 @@ cudaError_t get_event_pair(pbng_ctx *c, std::pair<cudaEvent_t, cudaEvent_t> &ev)
 }
 
 // profiling mode 1: an event pair around every sweep launch
-cudaError_t timed_sweep(pbng_ctx *c, const SweepLaunch &s) {
-    if (c->profiling != 1) return launch_sweep(c->prob, c->L, s, c->stream);
+template <class F>
+cudaError_t timed_launch(pbng_ctx *c, F &&launch) {
+    if (c->profiling != 1) return launch();
     std::pair<cudaEvent_t, cudaEvent_t> ev;
     cudaError_t e = get_event_pair(c, ev);
     if (e != cudaSuccess) return e;
     cudaEventRecord(ev.first, c->stream);
-    e = launch_sweep(c->prob, c->L, s, c->stream);
+    e = launch();
     cudaEventRecord(ev.second, c->stream);
     c->ev_used.push_back(ev);
     c->ev_launches.push_back(1);
     return e;
+}
+cudaError_t timed_sweep(pbng_ctx *c, const SweepLaunch &s) {
+    return timed_launch(c, [&] { return launch_sweep(c->prob, c->L, s, c->stream); });
 }
 
 pbng_status check_iterate(pbng_ctx *c, pbng_accel accel, double omega, double rho, double gamma, const char *who) {
@@ -602,7 +677,7 @@ cudaError_t sweep_colour_impl(pbng_ctx *c, int32_t col, pbng_accel accel, double
     s.v_begin = c->col_vbegin[col];
     s.n_v = c->col_nfree[col];
     s.chunk_begin = c->col_chunk[col];
-    s.split = choose_split(c, c->gcol_nfree[col]);
+    s.split = problem_split(c);
     if (s.n_v == 0) return cudaSuccess;
     cudaError_t e = timed_sweep(c, s);
     c->launches += 1;
@@ -962,6 +1037,7 @@ pbng_status pbng_color(pbng_ctx *c, int32_t *colour_out, int32_t *n_colours_out)
         for (size_t q = 0; q < c->halo_recv_orig.size(); ++q) c->h_halo_recv[q] = c->orig2int[c->halo_recv_orig[q]];
         if (c->dtype == DT_F64) build_layout<double>(c, vt_off, vt);
         else build_layout<float>(c, vt_off, vt);
+        build_pipeline(c, vt_off, vt);
         plan_workspace(c);
     } catch (const std::bad_alloc &) {
         return fail(PBNG_E_OUT_OF_MEMORY, "color: host allocation");
@@ -1024,6 +1100,10 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     L.xtilde = at(c->r_xt);
     L.halo_send = static_cast<const int32_t *>(at(c->r_halo_send));
     L.halo_recv = static_cast<const int32_t *>(at(c->r_halo_recv));
+    L.dep_off = static_cast<const int32_t *>(at(c->r_dep_off));
+    L.deps = static_cast<const int32_t *>(at(c->r_deps));
+    L.pipe_counter = static_cast<uint64_t *>(at(c->r_pipe));
+    L.pipe_flags = reinterpret_cast<int32_t *>(static_cast<char *>(at(c->r_pipe)) + 8);
     auto up = [&](const Region &r, const void *src, size_t n) -> cudaError_t {
         if (n == 0) return cudaSuccess;
         return cudaMemcpyAsync(base + r.off, src, n, cudaMemcpyHostToDevice, c->stream);
@@ -1055,6 +1135,8 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     chk(up(c->r_halo_send, c->h_halo_send.data(), c->h_halo_send.size() * 4));
     chk(up(c->r_halo_recv, c->h_halo_recv.data(), c->h_halo_recv.size() * 4));
     chk(up(c->r_targets, c->h_targets.data(), c->h_targets.size()));
+    chk(up(c->r_dep_off, c->h_dep_off.data(), c->h_dep_off.size() * 4));
+    chk(up(c->r_deps, c->h_deps.data(), c->h_deps.size() * 4));
     chk(cudaMemsetAsync(base + c->r_flag.off, 0, 4, c->stream));
     chk(cudaStreamSynchronize(c->stream));
     if (e != cudaSuccess) return cuda_fail(e, "bind_workspace");
@@ -1139,11 +1221,33 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
         PBNG_CUDA(get_event_pair(c, span), "iterate: profiling events");
         PBNG_CUDA(cudaEventRecord(span.first, c->stream), "iterate: event");
     }
-    for (int32_t it = 0; it < n_iterations; ++it) {
-        for (int32_t col = 0; col < c->ncol; ++col) {
-            PBNG_CUDA(sweep_colour_impl(c, col, accel, omega, rho, gamma, &span_launches), "iterate: sweep kernel");
+    if (effective_schedule(c) == 2) {
+        // pipelined: one persistent launch per kPipeMaxIter iterations, no barrier between colours
+        for (int32_t it = 0; it < n_iterations; it += kPipeMaxIter) {
+            PipeLaunch P;
+            P.n_iter = std::min<int32_t>(kPipeMaxIter, n_iterations - it);
+            P.accel = accel;
+            P.work = c->work;
+            P.out = c->out;
+            P.hist = c->hist;
+            P.split = problem_split(c);
+            P.gamma = accel == PBNG_ACCEL_CHEBYSHEV ? gamma : 1.0;
+            for (int j = 0; j < P.n_iter; ++j)
+                P.omega[j] = accel == PBNG_ACCEL_SOR ? omega
+                             : accel == PBNG_ACCEL_CHEBYSHEV ? chebyshev_weight(c->l + j + 1, rho) : 1.0;
+            PBNG_CUDA(cudaMemsetAsync(c->L.pipe_counter, 0, c->r_pipe.bytes, c->stream), "iterate: pipeline reset");
+            PBNG_CUDA(timed_launch(c, [&] { return launch_sweep_pipe(c->prob, c->L, P, c->stream); }), "iterate: pipelined sweep");
+            c->launches += 1;
+            span_launches += 1;
+            for (int j = 0; j < P.n_iter; ++j) end_iteration_impl(c, accel);
         }
-        end_iteration_impl(c, accel);
+    } else {
+        for (int32_t it = 0; it < n_iterations; ++it) {
+            for (int32_t col = 0; col < c->ncol; ++col) {
+                PBNG_CUDA(sweep_colour_impl(c, col, accel, omega, rho, gamma, &span_launches), "iterate: sweep kernel");
+            }
+            end_iteration_impl(c, accel);
+        }
     }
     if (span_prof) {
         PBNG_CUDA(cudaEventRecord(span.second, c->stream), "iterate: event");
@@ -1321,7 +1425,22 @@ pbng_status pbng_query(pbng_ctx *c, pbng_info *info) {
         info->sweep_flops = (double)c->nb * ((double)c->n_pairs * per_pair + (double)c->n_free * 40.0);
         info->n_local_vertices = c->n_local;
         info->n_ghosts = c->n_local_free - c->n_free;
+        info->schedule = effective_schedule(c);
     }
+    return PBNG_OK;
+}
+
+pbng_status pbng_set_schedule(pbng_ctx *c, pbng_schedule schedule) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    if (schedule != PBNG_SCHEDULE_AUTO && schedule != PBNG_SCHEDULE_COLOUR_LAUNCHES && schedule != PBNG_SCHEDULE_PIPELINED)
+        return fail(PBNG_E_INVALID_ARGUMENT, "set_schedule: unknown schedule");
+    if (schedule == PBNG_SCHEDULE_PIPELINED) {
+        if (!c->colored) return fail(PBNG_E_NOT_COLORED, "set_schedule: call pbng_color first");
+        if (!pipeline_available(c))
+            return fail(PBNG_E_INVALID_ARGUMENT, "set_schedule: the pipelined schedule needs an undecomposed context with n_batch < 32");
+    }
+    if (c->cur_accel >= 0) return fail(PBNG_E_BAD_ORDER, "set_schedule: a colour-by-colour iteration is open");
+    c->schedule = (int)schedule;
     return PBNG_OK;
 }
 

@@ -65,6 +65,13 @@ struct Layout {
     const int32_t *halo_recv = nullptr;  // internal ids of the per-(colour, peer) receive lists
     const void *mass = nullptr;          // Real [n_own] lumped masses m_i = sum_e R^0 V_e / 4 (backward Euler)
     void *xtilde = nullptr;              // Real4, position layout: inertial target 2 x^n - x^{n-1}
+    // pipelined schedule (sweep_pipe_kernel): per chunk the chunks holding its stencil neighbours, CSR,
+    // entry = (chunk << 1) | 1 for an earlier colour (must have finished iteration l), (chunk << 1) for a
+    // later colour or the chunk itself (iteration l - 1); done counters [n_batch][n_chunks]; work counter
+    const int32_t *dep_off = nullptr;    // [n_chunks + 1]
+    const int32_t *deps = nullptr;
+    int32_t *pipe_flags = nullptr;
+    uint64_t *pipe_counter = nullptr;
 };
 
 struct Problem {
@@ -92,7 +99,22 @@ struct SweepLaunch {
     int split = 1;  // warps sharing one 32-vertex chunk (1, 2 or 4)
 };
 
+// one launch of the pipelined schedule: n_iter <= kPipeMaxIter whole iterations; iteration l (0-based
+// within the launch) reads xbuf[work] (l even) / xbuf[out] (l odd) when accelerated (the buffers swap
+// after every accelerated iteration), with blend weight omega[l]
+constexpr int kPipeMaxIter = 64;
+struct PipeLaunch {
+    int n_iter = 0;
+    int accel = ACCEL_NONE;
+    int work = 0, out = 1, hist = 2;
+    int split = 1;  // warps per chunk item (1, 2 or 4), the same as the colour launches use
+    double gamma = 1;
+    double omega[kPipeMaxIter] = {};
+};
+
 // launchers (pbng_kernels.cu); return cudaGetLastError()
+// pipelined sweep: the caller zeroes pipe_flags and pipe_counter before each launch
+cudaError_t launch_sweep_pipe(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st);
 cudaError_t launch_sweep(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st);
 cudaError_t launch_set_positions(const Problem &p, const Layout &L, int n_buffers, cudaStream_t st);
 cudaError_t launch_get_positions(const Problem &p, const Layout &L, int work, cudaStream_t st);

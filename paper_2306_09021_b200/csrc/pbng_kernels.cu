@@ -12,6 +12,7 @@
 //  reduce_kernel       per-sample final reduction of the partials.
 //  set/get_positions   original <-> internal (colour-major) vertex order.
 // No tensor cores: the path is a gather + 3x3 register math, not a dense contraction.
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -31,12 +32,21 @@ __device__ __forceinline__ int64_t ld(const int64_t *p) {
     return (int64_t)__ldg(reinterpret_cast<const long long *>(p));
 }
 __device__ __forceinline__ int4 ld(const int4 *p) { return __ldg(p); }
+__device__ __forceinline__ int2 ld(const int2 *p) { return __ldg(p); }
 __device__ __forceinline__ float4 ld(const float4 *p) { return __ldg(p); }
 __device__ __forceinline__ double2 ld(const double2 *p) { return __ldg(p); }
 __device__ __forceinline__ double4 ld(const double4 *p) {
     const double2 *q = reinterpret_cast<const double2 *>(p);
     const double2 a = __ldg(q), b = __ldg(q + 1);
     return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// neighbour-position gathers: read-only path inside one colour launch (the neighbours belong to other
+// colours), coherent loads in the pipelined kernel (positions written by other CTAs of the same launch)
+enum { GATHER_NC = 0, GATHER_COHERENT = 1 };
+template <int G, class R4> __device__ __forceinline__ R4 gather(const R4 *p) {
+    if (G == GATHER_NC) return ld(p);
+    return *p;
 }
 
 __device__ __forceinline__ float rsq(float x) { return rsqrtf(x); }
@@ -387,6 +397,15 @@ __device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<doubl
     p.VE = ld(c);
 }
 
+// L2 prefetch of a later record of the stream (no registers held while it is in flight)
+__device__ __forceinline__ void pf_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+template <class R, int MODEL>
+__device__ __forceinline__ void prefetch_pair(const Layout &L, int64_t r) {
+    pf_l2(L.rec_id + r);
+    pf_l2(reinterpret_cast<const typename RT<R>::R4 *>(L.rec_a) + r);
+    if (MODEL != MODEL_NH) pf_l2(reinterpret_cast<const typename RT<R>::R4 *>(L.rec_b) + r);
+}
+
 template <bool HESS, class T, class R>
 __device__ __forceinline__ void contrib(const T (&d1)[3], const T (&d2)[3], const T (&d3)[3],
                                         const Pair<R, MODEL_FCR> &p, T cmu, T clam, T (&f)[3], T (&A)[6]) {
@@ -448,7 +467,7 @@ __device__ __forceinline__ void inertia_contrib(const Layout &L, int v, const ty
 }
 
 // weak-constraint terms for vertex v: f -= d K C_c, A += d^2 K
-template <class R, class T, bool HESS>
+template <class R, class T, bool HESS, int G = GATHER_NC>
 __device__ __forceinline__ void wc_contrib(const Layout &L, const typename RT<R>::R4 *x, const int sh, int v,
                                            const T (&xa)[3], T (&f)[3], T (&A)[6]) {
     using R4 = typename RT<R>::R4;
@@ -465,7 +484,7 @@ __device__ __forceinline__ void wc_contrib(const Layout &L, const typename RT<R>
             if (node == v) {
                 C[0] += w * xa[0]; C[1] += w * xa[1]; C[2] += w * xa[2];
             } else {
-                const R4 y = ld(x + ((int64_t)node << sh));
+                const R4 y = gather<G>(x + ((int64_t)node << sh));
                 C[0] += w * T(y.x); C[1] += w * T(y.y); C[2] += w * T(y.z);
             }
         }
@@ -535,18 +554,73 @@ __device__ __forceinline__ void finish_vertex(const Layout &L, typename RT<R>::R
     }
 }
 
-// One thread per free vertex of the colour; a warp owns one 32-vertex SELL chunk, so record k of its
-// 32 lanes is one contiguous 512 B (f32) segment per field.  The record stream is read once with
-// L1::no_allocate; the neighbour positions are gathered through L1 (different colour, read-only in this
-// launch).  The per-vertex summation order is ascending tet index, as in the oracle.
 #ifndef PBNG_SWEEP_UNROLL
 #define PBNG_SWEEP_UNROLL 2
 #endif
 constexpr int kSweepUnroll = PBNG_SWEEP_UNROLL;  // pair-loop unroll (loads of record k+1 issued early)
-template <class R, int MODEL, int ACCEL, bool FEXT, bool WC>
+#ifndef PBNG_SWEEP_PREFETCH
+#define PBNG_SWEEP_PREFETCH 4
+#endif
+constexpr int kSweepPrefetch = PBNG_SWEEP_PREFETCH;  // L2 prefetch distance of the record stream (0: off)
 #ifndef PBNG_SWEEP_MINB
 #define PBNG_SWEEP_MINB 1
 #endif
+
+// partial sums of warp `sub` of a SPLIT-warp group over records k = sub, sub + SPLIT, ... (ascending)
+template <class R, int MODEL, int G, int SPLIT>
+__device__ __forceinline__ void split_partial(const Layout &L, const typename RT<R>::R4 *work, const R (&xa)[3],
+                                              const int64_t base, const int deg, const int sub, const R cmu,
+                                              const R clam, R (&f)[3], R (&A)[6]) {
+    for (int k = sub; k < deg; k += SPLIT) {
+        Pair<R, MODEL> pr;
+        load_pair<true>(L, base + (int64_t)k * kChunk, pr);
+        R d1[3], d2[3], d3[3];
+        sub3<R>(gather<G>(work + pr.id.x), xa, d1);
+        sub3<R>(gather<G>(work + pr.id.y), xa, d2);
+        sub3<R>(gather<G>(work + pr.id.z), xa, d3);
+        contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
+    }
+}
+
+// One free vertex's PBNG update: accumulate over its records in ascending tet order,
+// weak constraints, inertia, then solve + blend + store (finish_vertex).
+template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int G>
+__device__ __forceinline__ void update_vertex(const Layout &L, typename RT<R>::R4 *__restrict__ work, const int64_t xs,
+                                              const int v, const int64_t base, const int deg, const int oi,
+                                              const int hi, const R cmu, const R clam, const R omega, const R gamma,
+                                              const R idt2) {
+    using R4 = typename RT<R>::R4;
+    const R4 xa4 = work[v];
+    const R xa[3] = {xa4.x, xa4.y, xa4.z};
+    R f[3] = {R(0), R(0), R(0)};
+    if (FEXT) {
+        const R4 fe = ld(reinterpret_cast<const R4 *>(L.fext) + v);
+        f[0] = fe.x; f[1] = fe.y; f[2] = fe.z;
+    }
+    R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
+
+#pragma unroll kSweepUnroll
+    for (int k = 0; k < deg; ++k) {
+        if (kSweepPrefetch > 0 && k + kSweepPrefetch < deg)
+            prefetch_pair<R, MODEL>(L, base + (int64_t)(k + kSweepPrefetch) * kChunk);
+        Pair<R, MODEL> pr;
+        load_pair<true>(L, base + (int64_t)k * kChunk, pr);
+        R d1[3], d2[3], d3[3];
+        sub3<R>(gather<G>(work + pr.id.x), xa, d1);
+        sub3<R>(gather<G>(work + pr.id.y), xa, d2);
+        sub3<R>(gather<G>(work + pr.id.z), xa, d3);
+        contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
+    }
+    if (WC) wc_contrib<R, R, true, G>(L, work, 0, v, xa, f, A);
+    if (idt2 > R(0)) inertia_contrib<R, R>(L, v, ld(reinterpret_cast<const R4 *>(L.xtilde) + xs + v), idt2, xa, f, A);
+    finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
+}
+
+// One thread per free vertex of the colour; a warp owns one 32-vertex SELL chunk, so record k of its
+// 32 lanes is one contiguous 512 B (f32) segment per field.  The record stream is read once with
+// L1::no_allocate; the neighbour positions are gathered through L1 (different colour, read-only in this
+// launch).  The per-vertex summation order is ascending tet index, as in the oracle.
+template <class R, int MODEL, int ACCEL, bool FEXT, bool WC>
 __global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
                                                             const int64_t chunk_begin, const int64_t x_stride,
                                                             const int wi, const int oi, const int hi, const R cmu,
@@ -559,29 +633,133 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_kernel(con
     const int deg = ld(L.deg + v);
     const int64_t xs = (int64_t)blockIdx.y * x_stride;
     R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
+    update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_NC>(L, work, xs, v, base, deg, oi, hi, cmu, clam, omega, gamma,
+                                                        idt2);
+}
 
-    const R4 xa4 = work[v];
-    const R xa[3] = {xa4.x, xa4.y, xa4.z};
-    R f[3] = {R(0), R(0), R(0)};
-    if (FEXT) {
-        const R4 fe = ld(reinterpret_cast<const R4 *>(L.fext) + v);
-        f[0] = fe.x; f[1] = fe.y; f[2] = fe.z;
-    }
-    R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
+// ------------------------------------------------------------------------------------------------
+// Pipelined (dataflow) sweep: ONE persistent launch runs up to kPipeMaxIter whole iterations.  Work
+// items are (iteration l, chunk X, sample b) in lexicographic order -- iteration-major, then colour-
+// major chunk order -- taken by warps from a global counter.  Instead of a grid-wide barrier between
+// colours, a chunk waits only for the chunks holding its stencil neighbours (host-built list,
+// pbng_host.cpp build_pipeline): a neighbour chunk of an EARLIER colour must have finished iteration
+// l (done >= l + 1), one of a LATER colour (and the chunk itself) iteration l - 1 (done >= l).  This
+// is exactly the order the per-colour launches impose on every (reader, writer) pair of positions
+// -- including the work/out buffer swap of the accelerated blends -- so every vertex reads the same
+// values and the results are bitwise those of the barrier schedule.  No deadlock: an item only waits
+// for items earlier in the counter order, which running warps already hold.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int32_t *p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
-#pragma unroll kSweepUnroll
-    for (int k = 0; k < deg; ++k) {
-        Pair<R, MODEL> pr;
-        load_pair<true>(L, base + (int64_t)k * kChunk, pr);
-        R d1[3], d2[3], d3[3];
-        sub3<R>(ld(work + pr.id.x), xa, d1);
-        sub3<R>(ld(work + pr.id.y), xa, d2);
-        sub3<R>(ld(work + pr.id.z), xa, d3);
-        contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
+__device__ __forceinline__ void group_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// SPLIT warps form a group that owns one item at a time (SPLIT = 1: update_vertex, the arithmetic of
+// sweep_kernel; SPLIT > 1: the partial sums and fixed-order combination of sweep_split_kernel), so the
+// per-vertex summation order -- and the result -- is that of the colour-launch schedule with the same
+// split (pbng_host.cpp problem_split).
+template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int SPLIT>
+__global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_pipe_kernel(const Layout L, const PipeLaunch P,
+                                                                 const int64_t x_stride, const int32_t n_batch,
+                                                                 const int64_t n_chunks, const R cmu, const R clam,
+                                                                 const R idt2) {
+    using R4 = typename RT<R>::R4;
+    constexpr int GROUPS = kSweepBlock / (32 * SPLIT);
+    static_assert(GROUPS >= 1 && GROUPS * SPLIT * 32 == kSweepBlock, "block must hold whole groups");
+    __shared__ R red[GROUPS][SPLIT > 1 ? SPLIT - 1 : 1][9][32];
+    __shared__ int64_t item_sh[GROUPS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = warp / SPLIT, sub = warp % SPLIT;
+    const int64_t per_iter = n_chunks * n_batch;
+    const int64_t n_items = per_iter * P.n_iter;
+    auto gsync = [&] {
+        if (SPLIT == 1) __syncwarp();
+        else group_sync(1 + grp, SPLIT * 32);
+    };
+    for (;;) {
+        if (sub == 0 && lane == 0)
+            item_sh[grp] = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(L.pipe_counter), 1ull);
+        gsync();
+        const int64_t q = item_sh[grp];
+        if (q >= n_items) return;
+        const int l = (int)(q / per_iter);
+        const int64_t rem = q - (int64_t)l * per_iter;
+        const int64_t X = rem / n_batch;
+        const int b = (int)(rem - X * n_batch);
+        int32_t *flags = L.pipe_flags + (int64_t)b * n_chunks;
+        if (sub == 0) {  // wait for the neighbour chunks (one dependency per lane)
+            const int d0 = ld(L.dep_off + X), d1 = ld(L.dep_off + X + 1);
+            for (int d = d0 + lane; d < d1; d += 32) {
+                const int dep = ld(L.deps + d);
+                const int target = l + (dep & 1);
+                const int32_t *fl = flags + (dep >> 1);
+                while (ld_acquire(fl) < target) __nanosleep(32);
+            }
+        }
+        gsync();
+        __threadfence();
+        const int wi = (ACCEL != ACCEL_NONE && (l & 1)) ? P.out : P.work;
+        const int oi = (ACCEL != ACCEL_NONE && (l & 1)) ? P.work : P.out;
+        const R omega = R(P.omega[l]), gamma = R(P.gamma);
+        const int2 cv = ld(L.chunk_v + X);
+        const bool valid = lane < cv.y;
+        const int v = cv.x + lane;
+        const int64_t xs = (int64_t)b * x_stride;
+        R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
+        const int64_t base = ld(L.chunk_off + X) + lane;
+        if (SPLIT == 1) {
+            if (valid)
+                update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_COHERENT>(L, work, xs, v, base, ld(L.deg + v), oi,
+                                                                          P.hist, cmu, clam, omega, gamma, idt2);
+        } else {
+            R f[3] = {R(0), R(0), R(0)};
+            R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
+            R4 xa4 = mk4<R>(R(0), R(0), R(0));
+            if (valid) {
+                xa4 = work[v];
+                const R xa[3] = {xa4.x, xa4.y, xa4.z};
+                split_partial<R, MODEL, GATHER_COHERENT, SPLIT>(L, work, xa, base, ld(L.deg + v), sub, cmu, clam, f, A);
+            }
+            if (sub > 0) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) red[grp][sub - 1][c][lane] = f[c];
+#pragma unroll
+                for (int c = 0; c < 6; ++c) red[grp][sub - 1][3 + c][lane] = A[c];
+            }
+            gsync();
+            if (sub == 0 && valid) {
+#pragma unroll
+                for (int t = 0; t < SPLIT - 1; ++t) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) f[c] += red[grp][t][c][lane];
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) A[c] += red[grp][t][3 + c][lane];
+                }
+                if (FEXT) {
+                    const R4 fe = ld(reinterpret_cast<const R4 *>(L.fext) + v);
+                    f[0] += fe.x; f[1] += fe.y; f[2] += fe.z;
+                }
+                const R xa[3] = {xa4.x, xa4.y, xa4.z};
+                if (WC) wc_contrib<R, R, true, GATHER_COHERENT>(L, work, 0, v, xa, f, A);
+                if (idt2 > R(0))
+                    inertia_contrib<R, R>(L, v, ld(reinterpret_cast<const R4 *>(L.xtilde) + xs + v), idt2, xa, f, A);
+                finish_vertex<R, ACCEL>(L, work, xs, v, oi, P.hist, xa4, f, A, omega, gamma);
+            }
+        }
+        if (sub == 0) {
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) st_release(flags + X, l + 1);
+        }
     }
-    if (WC) wc_contrib<R, R, true>(L, work, 0, v, xa, f, A);
-    if (idt2 > R(0)) inertia_contrib<R, R>(L, v, ld(reinterpret_cast<const R4 *>(L.xtilde) + xs + v), idt2, xa, f, A);
-    finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
 }
 
 // Split variant for compute-heavy pairs (fixed-corotated: a polar decomposition per pair) and small
@@ -614,15 +792,7 @@ __global__ void __launch_bounds__(SplitBlock<SPLIT>::n) sweep_split_kernel(const
         const int deg = ld(L.deg + v);
         xa4 = work[v];
         const R xa[3] = {xa4.x, xa4.y, xa4.z};
-        for (int k = sub; k < deg; k += SPLIT) {
-            Pair<R, MODEL> pr;
-            load_pair<true>(L, base + (int64_t)k * kChunk, pr);
-            R d1[3], d2[3], d3[3];
-            sub3<R>(ld(work + pr.id.x), xa, d1);
-            sub3<R>(ld(work + pr.id.y), xa, d2);
-            sub3<R>(ld(work + pr.id.z), xa, d3);
-            contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
-        }
+        split_partial<R, MODEL, GATHER_NC, SPLIT>(L, work, xa, base, deg, sub, cmu, clam, f, A);
     }
     if (sub > 0) {
 #pragma unroll
@@ -724,6 +894,53 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
     else PBNG_SPLIT(4);
 #undef PBNG_SPLIT
     return cudaGetLastError();
+}
+
+// persistent grid: every SM filled to the kernel's occupancy (queried once per instantiation)
+template <class R, int MODEL, int ACCEL, bool FE, bool W, int SPLIT>
+cudaError_t pipe_launch(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st) {
+    static int blocks = 0;
+    if (blocks == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_pipe_kernel<R, MODEL, ACCEL, FE, W, SPLIT>,
+                                                      kSweepBlock, 0);
+        blocks = std::max(1, sms * std::max(1, per_sm));
+    }
+    constexpr int GROUPS = kSweepBlock / (32 * SPLIT);
+    const int64_t items = p.n_chunks * p.n_batch * s.n_iter;
+    const int64_t g = std::min<int64_t>(blocks, (items + GROUPS - 1) / GROUPS);
+    if (g <= 0) return cudaSuccess;
+    sweep_pipe_kernel<R, MODEL, ACCEL, FE, W, SPLIT><<<(unsigned)g, kSweepBlock, 0, st>>>(
+        L, s, p.x_stride, p.n_batch, p.n_chunks, R(p.cmu), R(p.clam), R(p.inv_dt2));
+    return cudaGetLastError();
+}
+
+template <class R, int MODEL, int ACCEL, bool FE, bool W>
+cudaError_t pipe_dispatch4(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st) {
+    if (s.split == 2) return pipe_launch<R, MODEL, ACCEL, FE, W, 2>(p, L, s, st);
+    if (s.split == 4) return pipe_launch<R, MODEL, ACCEL, FE, W, 4>(p, L, s, st);
+    return pipe_launch<R, MODEL, ACCEL, FE, W, 1>(p, L, s, st);
+}
+
+template <class R, int MODEL, int ACCEL>
+cudaError_t pipe_dispatch3(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st) {
+    if (p.has_fext) {
+        if (p.has_wc) return pipe_dispatch4<R, MODEL, ACCEL, true, true>(p, L, s, st);
+        return pipe_dispatch4<R, MODEL, ACCEL, true, false>(p, L, s, st);
+    }
+    if (p.has_wc) return pipe_dispatch4<R, MODEL, ACCEL, false, true>(p, L, s, st);
+    return pipe_dispatch4<R, MODEL, ACCEL, false, false>(p, L, s, st);
+}
+
+template <class R, int MODEL>
+cudaError_t pipe_dispatch2(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st) {
+    switch (s.accel) {
+        case ACCEL_SOR: return pipe_dispatch3<R, MODEL, ACCEL_SOR>(p, L, s, st);
+        case ACCEL_CHEB: return pipe_dispatch3<R, MODEL, ACCEL_CHEB>(p, L, s, st);
+        default: return pipe_dispatch3<R, MODEL, ACCEL_NONE>(p, L, s, st);
+    }
 }
 
 template <class R, int MODEL, int ACCEL>
@@ -1036,8 +1253,16 @@ template <class R, int MODEL>
 cudaError_t sweep_entry(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st);
 template <class R, int MODEL>
 cudaError_t energy_entry(const Problem &p, const Layout &L, int work, cudaStream_t st);
+template <class R, int MODEL>
+cudaError_t pipe_entry(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st);
 
 #if defined(PBNG_TU_R)
+template <class R, int MODEL>
+cudaError_t pipe_entry(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st) {
+    return pipe_dispatch2<R, MODEL>(p, L, s, st);
+}
+template cudaError_t pipe_entry<PBNG_TU_R, PBNG_TU_MODEL>(const Problem &, const Layout &, const PipeLaunch &,
+                                                          cudaStream_t);
 template <class R, int MODEL>
 cudaError_t sweep_entry(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
     return sweep_dispatch2<R, MODEL>(p, L, s, st);
@@ -1050,6 +1275,18 @@ template cudaError_t sweep_entry<PBNG_TU_R, PBNG_TU_MODEL>(const Problem &, cons
                                                            cudaStream_t);
 template cudaError_t energy_entry<PBNG_TU_R, PBNG_TU_MODEL>(const Problem &, const Layout &, int, cudaStream_t);
 #else
+
+cudaError_t launch_sweep_pipe(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st) {
+    if (s.n_iter <= 0 || p.n_chunks <= 0) return cudaSuccess;
+    if (p.dtype == DT_F64) {
+        if (p.model == MODEL_FCR) return pipe_entry<double, MODEL_FCR>(p, L, s, st);
+        if (p.model == MODEL_SNH) return pipe_entry<double, MODEL_SNH>(p, L, s, st);
+        return pipe_entry<double, MODEL_NH>(p, L, s, st);
+    }
+    if (p.model == MODEL_FCR) return pipe_entry<float, MODEL_FCR>(p, L, s, st);
+    if (p.model == MODEL_SNH) return pipe_entry<float, MODEL_SNH>(p, L, s, st);
+    return pipe_entry<float, MODEL_NH>(p, L, s, st);
+}
 
 cudaError_t launch_sweep(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
     if (s.n_v <= 0) return cudaSuccess;

@@ -22,12 +22,13 @@ STATUS = {0: "PBNG_OK", 1: "PBNG_E_INVALID_ARGUMENT", 2: "PBNG_E_INDEX_OUT_OF_RA
 DTYPE = {"f32": 0, "f64": 1}
 MODEL = {"nh": 0, "fcr": 1, "snh": 2}
 ACCEL = {"none": 0, "sor": 1, "chebyshev": 2}
+SCHEDULE = {"auto": 0, "colour_launches": 1, "pipelined": 2}
 EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbng_color", "pbng_workspace_bytes",
            "pbng_bind_workspace", "pbng_set_positions", "pbng_get_positions", "pbng_iterate", "pbng_energy_residual",
            "pbng_synchronize", "pbng_query", "pbng_profile_enable", "pbng_profile_read", "pbng_destroy",
            "pbng_last_error", "pbng_version", "pbng_sweep_colour", "pbng_end_iteration", "pbng_set_partition",
            "pbng_halo_counts", "pbng_halo_vertices", "pbng_halo_pack", "pbng_halo_unpack", "pbng_test_polar",
-           "pbng_set_inertia")
+           "pbng_set_inertia", "pbng_set_schedule")
 
 WC_DTYPE = np.dtype([("n0", "<i4"), ("n1", "<i4"), ("idx0", "<i4", 4), ("idx1", "<i4", 4), ("w0", "<f8", 4),
                      ("w1", "<f8", 4), ("anchor", "<f8", 3), ("K", "<f8", 6)])
@@ -46,7 +47,8 @@ class Info(C.Structure):
                 ("n_batch", C.c_int32), ("n_colours", C.c_int32), ("dtype", C.c_int32), ("model", C.c_int32),
                 ("iteration", C.c_int64), ("kernel_launches", C.c_int64), ("sweep_bytes", C.c_double),
                 ("accel_bytes", C.c_double), ("sweep_flops", C.c_double), ("n_local_vertices", C.c_int64),
-                ("n_ghosts", C.c_int64), ("rank", C.c_int32), ("n_ranks", C.c_int32)]
+                ("n_ghosts", C.c_int64), ("rank", C.c_int32), ("n_ranks", C.c_int32), ("schedule", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 _lib = None
@@ -87,6 +89,7 @@ def lib():
     L.pbng_halo_unpack.argtypes = [vp, i32, i32, i32, vp]
     L.pbng_test_polar.argtypes = [C.c_int, vp, vp, i64, C.c_int]
     L.pbng_set_inertia.argtypes = [vp, d, vp]
+    L.pbng_set_schedule.argtypes = [vp, C.c_int]
     L.pbng_last_error.restype = C.c_char_p
     L.pbng_version.restype = i32
     for name in EXPORTS:
@@ -236,6 +239,10 @@ class Context:
 
     def iterate(self, n: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0, gamma: float = 1.0):
         _check(lib().pbng_iterate(self._h, int(n), ACCEL[accel], float(omega), float(rho), float(gamma)))
+
+    def set_schedule(self, schedule: str = "auto"):
+        """'colour_launches' (one launch per colour pass), 'pipelined' (persistent dataflow launch) or 'auto'."""
+        _check(lib().pbng_set_schedule(self._h, SCHEDULE[schedule]))
 
     def energy_residual(self):
         e = np.empty(self.n_batch)

@@ -119,3 +119,29 @@ def test_weak_constraint_struct_layout():
     assert C.sizeof(WC) == P.WC_DTYPE.itemsize == 176
     for name in ("w0", "w1", "anchor", "K"):
         assert getattr(WC, name).offset == P.WC_DTYPE.fields[name][1]
+
+
+def test_schedule_selection():
+    s = G.config1_tiny_cube()
+    ctx = P.Context(s.X, s.tets, n_batch=1, dtype="f64", device=-1)
+    ctx.set_material(s.model, s.E, s.nu, s.density, s.gravity)
+    ctx.set_constraints(s.pinned, s.targets, s.wc)
+    with pytest.raises(P.PBNGError) as e:
+        ctx.set_schedule("pipelined")
+    assert e.value.status == 6  # not coloured yet
+    ctx.color()
+    assert ctx.query()["schedule"] == 2  # auto -> pipelined on a small undecomposed context
+    ctx.set_schedule("colour_launches")
+    assert ctx.query()["schedule"] == 1
+    ctx.set_schedule("pipelined")
+    assert ctx.query()["schedule"] == 2
+    # a domain-decomposed context needs the halo exchange between colour passes
+    d = P.Context(s.X, s.tets, n_batch=1, dtype="f64", device=-1)
+    d.set_material(s.model, s.E, s.nu, s.density, s.gravity)
+    d.set_constraints(s.pinned, s.targets, s.wc)
+    d.set_partition((np.arange(125) >= 60).astype(np.int32), 0, 2)
+    d.color()
+    assert d.query()["schedule"] == 1
+    with pytest.raises(P.PBNGError) as e:
+        d.set_schedule("pipelined")
+    assert e.value.status == 1

@@ -1,0 +1,79 @@
+"""The pipelined (dataflow) schedule of pbng_iterate against the per-colour-launch schedule.
+
+Both schedules make every vertex read exactly the same neighbour values (include/pbng.h pbng_schedule;
+PAPER.md:693-705 fixes only the colour order), so the iterates, energies and residuals must be BITWISE
+equal -- not merely within tolerance.  Iteration counts above 64 span several persistent launches.
+"""
+import numpy as np
+import pytest
+
+from scenes import generators as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def run(scene, dtype, schedule, parts, accel=None):
+    from paper_2306_09021_b200 import context_from_scene
+    ctx = context_from_scene(scene, device=0, dtype=dtype)
+    ctx.set_schedule(schedule)
+    acc = scene.accel if accel is None else accel
+    for k in parts:
+        ctx.iterate(k, acc, scene.omega, scene.rho, scene.gamma)
+    E, r = ctx.energy_residual()
+    x = ctx.get_positions().cpu().numpy()
+    q = ctx.query()
+    ctx.close()
+    return x, E, r, q
+
+
+CASES = [
+    (1, "full", "f64", None, [70]), (1, "full", "f64", "sor", [3, 66]), (1, "full", "f64", "chebyshev", [65, 2]),
+    (2, "small", "f32", None, [20]), (3, "small", "f32", None, [30]), (3, "small", "f64", "sor", [7]),
+    (5, "small", "f32", None, [12]), (5, "small", "f64", None, [5]), (4, "small", "f32", None, [9]),
+]
+
+
+@pytest.mark.parametrize("cfg,scale,dtype,accel,parts", CASES)
+def test_pipelined_equals_colour_launches_bitwise(cfg, scale, dtype, accel, parts):
+    s = G.make_config(cfg, scale)
+    if accel == "sor":
+        s.accel, s.omega = "sor", 1.5
+    elif accel == "chebyshev":
+        s.accel, s.rho, s.gamma = "chebyshev", 0.95, 1.7
+    xa, Ea, ra, qa = run(s, dtype, "colour_launches", parts)
+    xb, Eb, rb, qb = run(s, dtype, "pipelined", parts)
+    assert qa["schedule"] == 1 and qb["schedule"] == 2
+    assert np.array_equal(xa, xb), f"max diff {np.abs(xa - xb).max()}"
+    assert np.array_equal(Ea, Eb) and np.array_equal(ra, rb)
+    assert qb["iteration"] == qa["iteration"] == sum(parts)
+
+
+@pytest.mark.parametrize("model", ["nh", "fcr", "snh"])
+def test_pipelined_models_and_backward_euler(model):
+    s = G.make_config(5, "small")
+    s.model = model
+    from paper_2306_09021_b200 import context_from_scene
+    out = []
+    for sched in ("colour_launches", "pipelined"):
+        ctx = context_from_scene(s, device=0, dtype="f32")
+        ctx.set_schedule(sched)
+        ctx.set_inertia(1e-2, np.asarray(s.x0))
+        ctx.iterate(10, "chebyshev", 1.0, 0.9, 1.0)
+        out.append((ctx.get_positions().cpu().numpy(), ctx.energy_residual()))
+        ctx.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1][0], out[1][1][0])
+
+
+def test_full_config3_pipelined_bitwise():
+    s = G.make_config(3, "full")
+    xa, Ea, _, _ = run(s, "f32", "colour_launches", [3])
+    xb, Eb, _, _ = run(s, "f32", "pipelined", [3])
+    assert np.array_equal(xa, xb) and np.array_equal(Ea, Eb)
