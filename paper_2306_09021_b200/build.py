@@ -34,23 +34,39 @@ def stale(out: str = LIB) -> bool:
     return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB, jobs: int = 0) -> str:
-    """Compile the library; `defines` (e.g. ["PBNG_SWEEP_MINB=12"]) build tuning variants into `out`."""
+CACHE = os.path.join(ROOT, "build", "obj")  # objects of the last default build (tuning variants reuse them)
+
+
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB, jobs: int = 0,
+          only=None) -> str:
+    """Compile the library; `defines` (e.g. ["PBNG_SWEEP_MINB=12"]) build tuning variants into `out`.
+    only = [(R, MODEL), ...]: apply `defines` to those kernel objects only and reuse the cached default
+    objects for the rest (a variant for one workload in a fraction of the time)."""
     if not force and not defines and out == LIB and not stale():
         return LIB
     tag = f"{os.path.basename(out)}.{os.getpid()}"
     objdir = os.path.join(os.path.dirname(out), f".obj_{tag}")
     os.makedirs(objdir, exist_ok=True)
+    os.makedirs(CACHE, exist_ok=True)
     extra = [*(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines]]
+    default = not defines
 
     def compile_unit(unit):
+        name = "kernels_common.o" if unit is None else f"kernels_{unit[0]}_{unit[1]}.o"
+        cached = os.path.join(CACHE, name)
+        if only is not None and unit not in only and not stale(cached):
+            return cached
         if unit is None:
-            src, o, udef = KERNELS, os.path.join(objdir, "kernels_common.o"), []
+            src, o, udef = KERNELS, os.path.join(objdir, name), []
         else:
             r, m = unit
-            src, o = KERNELS, os.path.join(objdir, f"kernels_{r}_{m}.o")
+            src, o = KERNELS, os.path.join(objdir, name)
             udef = [f"-DPBNG_TU_R={r}", f"-DPBNG_TU_MODEL={m}"]
-        subprocess.check_call([NVCC, *ARCH, *FLAGS, *extra, *udef, "-c", "-o", o, src])
+        use = extra if (only is None or unit in only) else []
+        subprocess.check_call([NVCC, *ARCH, *FLAGS, *use, *udef, "-c", "-o", o, src])
+        if default or (only is not None and unit not in only):
+            import shutil
+            shutil.copyfile(o, cached)
         return o
 
     def compile_host():

@@ -406,6 +406,96 @@ __device__ __forceinline__ void prefetch_pair(const Layout &L, int64_t r) {
     if (MODEL != MODEL_NH) pf_l2(reinterpret_cast<const typename RT<R>::R4 *>(L.rec_b) + r);
 }
 
+// byte sizes of the record fields per slot (field 0 = rec_id, 1 = rec_a, 2 = rec_b, 3 = rec_c) and their
+// offsets inside a shared-memory stage holding one record step of 32 lanes
+template <class R, int MODEL> struct RecFmt {
+    static constexpr bool nh = MODEL == MODEL_NH;
+    static constexpr int s0 = 16, s1 = 4 * (int)sizeof(R), s2 = nh ? 0 : 4 * (int)sizeof(R),
+                         s3 = nh ? (sizeof(R) == 8 ? 8 : 0) : (sizeof(R) == 8 ? 16 : 4);
+    static __host__ __device__ constexpr int size(int k) { return k == 0 ? s0 : k == 1 ? s1 : k == 2 ? s2 : s3; }
+    static __host__ __device__ constexpr int off(int k) {
+        return k == 0 ? 0 : k == 1 ? 32 * s0 : k == 2 ? 32 * (s0 + s1) : 32 * (s0 + s1 + s2);
+    }
+    static constexpr int stage_bytes = 32 * (s0 + s1 + s2 + s3);
+};
+template <class R, int MODEL> __device__ __forceinline__ const void *rec_field(const Layout &L, int k) {
+    return k == 0 ? static_cast<const void *>(L.rec_id) : k == 1 ? L.rec_a : k == 2 ? L.rec_b : L.rec_c;
+}
+// a record from a shared-memory group of kg record steps: step j, lane `lane` (plain loads)
+__device__ __forceinline__ void decode_stage(const unsigned char *g, int kg, int j, int lane, Pair<float, MODEL_NH> &p) {
+    using F = RecFmt<float, MODEL_NH>;
+    const int e = j * 32 + lane;
+    p.id = reinterpret_cast<const int4 *>(g)[e];
+    const float4 x = reinterpret_cast<const float4 *>(g + kg * F::off(1))[e];
+    p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
+    p.VE = __int_as_float(p.id.w);
+}
+__device__ __forceinline__ void decode_stage(const unsigned char *g, int kg, int j, int lane, Pair<double, MODEL_NH> &p) {
+    using F = RecFmt<double, MODEL_NH>;
+    const int e = j * 32 + lane;
+    p.id = reinterpret_cast<const int4 *>(g)[e];
+    const double4 x = reinterpret_cast<const double4 *>(g + kg * F::off(1))[e];
+    p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
+    p.VE = reinterpret_cast<const double *>(g + kg * F::off(3))[e];
+}
+__device__ __forceinline__ void decode_stage(const unsigned char *g, int kg, int j, int lane, PairG<float> &p) {
+    using F = RecFmt<float, MODEL_FCR>;
+    const int e = j * 32 + lane;
+    p.id = reinterpret_cast<const int4 *>(g)[e];
+    const float4 a = reinterpret_cast<const float4 *>(g + kg * F::off(1))[e];
+    const float4 b = reinterpret_cast<const float4 *>(g + kg * F::off(2))[e];
+    const float c = reinterpret_cast<const float *>(g + kg * F::off(3))[e];
+    p.g1[0] = a.x; p.g1[1] = a.y; p.g1[2] = a.z;
+    p.g2[0] = a.w; p.g2[1] = b.x; p.g2[2] = b.y;
+    p.g3[0] = b.z; p.g3[1] = b.w; p.g3[2] = c;
+    p.VE = __int_as_float(p.id.w);
+}
+__device__ __forceinline__ void decode_stage(const unsigned char *g, int kg, int j, int lane, PairG<double> &p) {
+    using F = RecFmt<double, MODEL_FCR>;
+    const int e = j * 32 + lane;
+    p.id = reinterpret_cast<const int4 *>(g)[e];
+    const double4 a = reinterpret_cast<const double4 *>(g + kg * F::off(1))[e];
+    const double4 b = reinterpret_cast<const double4 *>(g + kg * F::off(2))[e];
+    const double2 c = reinterpret_cast<const double2 *>(g + kg * F::off(3))[e];
+    p.g1[0] = a.x; p.g1[1] = a.y; p.g1[2] = a.z;
+    p.g2[0] = a.w; p.g2[1] = b.x; p.g2[2] = b.y;
+    p.g3[0] = b.z; p.g3[1] = b.w; p.g3[2] = c.x;
+    p.VE = c.y;
+}
+
+// TMA (bulk copy) + mbarrier primitives for the record ring of sweep_kernel
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(bar), "r"(phase)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// global -> shared bulk copy completing on `bar`; the record stream is read once: evict-first in L2
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+
 template <bool HESS, class T, class R>
 __device__ __forceinline__ void contrib(const T (&d1)[3], const T (&d2)[3], const T (&d3)[3],
                                         const Pair<R, MODEL_FCR> &p, T cmu, T clam, T (&f)[3], T (&A)[6]) {
@@ -616,9 +706,31 @@ __device__ __forceinline__ void update_vertex(const Layout &L, typename RT<R>::R
     finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
 }
 
-// One thread per free vertex of the colour; a warp owns one 32-vertex SELL chunk, so record k of its
-// 32 lanes is one contiguous 512 B (f32) segment per field.  The record stream is read once with
-// L1::no_allocate; the neighbour positions are gathered through L1 (different colour, read-only in this
+#ifndef PBNG_SWEEP_TMA
+#define PBNG_SWEEP_TMA 0
+#endif
+#ifndef PBNG_TMA_GROUP
+#define PBNG_TMA_GROUP 2
+#endif
+#ifndef PBNG_TMA_GROUPS
+#define PBNG_TMA_GROUPS 3
+#endif
+// record stream of sweep_kernel through a TMA ring (1) or register loads + L2 prefetch (0, default).
+// Measured on config 3: the ring's shared memory is carved out of the L1 that
+// serves the neighbour gathers, and every ring depth tried was slower (0.42-0.60 vs 0.39 ms/iteration).
+constexpr bool kSweepTma = PBNG_SWEEP_TMA;
+constexpr int kGroup = PBNG_TMA_GROUP;      // record steps per bulk copy
+constexpr int kGroups = PBNG_TMA_GROUPS;    // ring depth in groups
+template <class R, int MODEL> struct StageSmem {  // per warp: [ring][kGroups mbarriers, padded]
+    static constexpr int group_bytes = kGroup * RecFmt<R, MODEL>::stage_bytes;
+    static constexpr int per_warp = kSweepTma ? kGroups * group_bytes + 128 : 0;
+};
+
+// One thread per free vertex of the colour; a warp owns one 32-vertex SELL chunk.  The chunk's record
+// stream is contiguous (record step k of the 32 lanes is one run of 32 slots per field, consecutive
+// steps adjacent), so lane 0 streams it into a ring of kGroups groups of kGroup steps with bulk copies
+// (TMA), one mbarrier per group: HBM latency is hidden without holding registers, and the lanes only
+// gather their neighbour positions (through L1; they belong to other colours, read-only in this
 // launch).  The per-vertex summation order is ascending tet index, as in the oracle.
 template <class R, int MODEL, int ACCEL, bool FEXT, bool WC>
 __global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
@@ -626,15 +738,91 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_kernel(con
                                                             const int wi, const int oi, const int hi, const R cmu,
                                                             const R clam, const R omega, const R gamma, const R idt2) {
     using R4 = typename RT<R>::R4;
-    const int t = blockIdx.x * kSweepBlock + threadIdx.x;
-    if (t >= n_v) return;
+    if (!kSweepTma) {
+        const int t = blockIdx.x * kSweepBlock + threadIdx.x;
+        if (t >= n_v) return;
+        const int v = v_begin + t;
+        const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
+        const int deg = ld(L.deg + v);
+        const int64_t xs = (int64_t)blockIdx.y * x_stride;
+        R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
+        update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_NC>(L, work, xs, v, base, deg, oi, hi, cmu, clam, omega,
+                                                            gamma, idt2);
+        return;
+    }
+    using F = RecFmt<R, MODEL>;
+    using SS = StageSmem<R, MODEL>;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cw = blockIdx.x * (kSweepBlock / 32) + warp;  // chunk within the colour
+    if (cw * kChunk >= n_v) return;                         // warp-uniform
+    unsigned char *ring = dsm + (size_t)warp * SS::per_warp;
+    const uint32_t bar0 = smem_u32(ring + kGroups * SS::group_bytes);
+    const int64_t ch = chunk_begin + cw;
+    const int64_t r0 = ld(L.chunk_off + ch);
+    const int W = (int)((ld(L.chunk_off + ch + 1) - r0) >> 5);  // records per lane incl. padding
+    const int NGRP = (W + kGroup - 1) / kGroup;
+    uint64_t pol = 0;
+    auto issue = [&](int g) {  // lane 0: record steps [g kGroup, (g + 1) kGroup) into ring slot g % kGroups
+        const int k0 = g * kGroup, n = min(kGroup, W - k0);
+        const uint32_t bar = bar0 + 8 * (g % kGroups);
+        const uint32_t dst = smem_u32(ring + (g % kGroups) * SS::group_bytes);
+        mbar_expect_tx(bar, n * F::stage_bytes);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (F::size(q) > 0)
+                bulk_g2s(dst + kGroup * F::off(q),
+                         static_cast<const char *>(rec_field<R, MODEL>(L, q)) + (r0 + (int64_t)k0 * kChunk) * F::size(q),
+                         n * kChunk * F::size(q), bar, pol);
+    };
+    if (lane == 0) {
+        for (int g = 0; g < kGroups; ++g) mbar_init(bar0 + 8 * g, 1);
+        mbar_fence_init();
+        pol = l2_evict_first();
+        for (int g = 0; g < min(kGroups, NGRP); ++g) issue(g);
+    }
+    __syncwarp();
+    const int t = cw * kChunk + lane;
+    const bool valid = t < n_v;
     const int v = v_begin + t;
-    const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
-    const int deg = ld(L.deg + v);
     const int64_t xs = (int64_t)blockIdx.y * x_stride;
     R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
-    update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_NC>(L, work, xs, v, base, deg, oi, hi, cmu, clam, omega, gamma,
-                                                        idt2);
+    const R4 xa4 = valid ? work[v] : mk4<R>(R(0), R(0), R(0));
+    const R xa[3] = {xa4.x, xa4.y, xa4.z};
+    const int deg = valid ? ld(L.deg + v) : 0;
+    R f[3] = {R(0), R(0), R(0)};
+    if (FEXT && valid) {
+        const R4 fe = ld(reinterpret_cast<const R4 *>(L.fext) + v);
+        f[0] = fe.x; f[1] = fe.y; f[2] = fe.z;
+    }
+    R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
+    for (int g = 0; g < NGRP; ++g) {
+        const unsigned char *grp = ring + (g % kGroups) * SS::group_bytes;
+        mbar_wait(bar0 + 8 * (g % kGroups), (g / kGroups) & 1);
+        const int kd = deg - g * kGroup;
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) {
+            if (j < kd) {
+                Pair<R, MODEL> pr;
+                decode_stage(grp, kGroup, j, lane, pr);
+                R d1[3], d2[3], d3[3];
+                sub3<R>(ld(work + pr.id.x), xa, d1);
+                sub3<R>(ld(work + pr.id.y), xa, d2);
+                sub3<R>(ld(work + pr.id.z), xa, d3);
+                contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
+            }
+        }
+        // group g is consumed by every lane: refill its ring slot with group g + kGroups
+        __syncwarp();
+        if (lane == 0 && g + kGroups < NGRP) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(g + kGroups);
+        }
+    }
+    if (!valid) return;
+    if (WC) wc_contrib<R, R, true>(L, work, 0, v, xa, f, A);
+    if (idt2 > R(0)) inertia_contrib<R, R>(L, v, ld(reinterpret_cast<const R4 *>(L.xtilde) + xs + v), idt2, xa, f, A);
+    finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -875,10 +1063,18 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
         return cudaGetLastError();
     }
     if (s.split <= 1) {
+        constexpr int smem = (kSweepBlock / 32) * StageSmem<R, MODEL>::per_warp;
+        static bool attr = false;
+        if (smem > 48 * 1024 && !attr) {
+            cudaError_t e = cudaFuncSetAttribute(sweep_kernel<R, MODEL, ACCEL, FE, W>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
         dim3 grid((unsigned)((s.n_v + kSweepBlock - 1) / kSweepBlock), (unsigned)p.n_batch);
-        sweep_kernel<R, MODEL, ACCEL, FE, W><<<grid, kSweepBlock, 0, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,
-                                                                            p.x_stride, s.work, s.out, s.hist, cmu,
-                                                                            clam, om, ga, idt2);
+        sweep_kernel<R, MODEL, ACCEL, FE, W><<<grid, kSweepBlock, smem, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,
+                                                                               p.x_stride, s.work, s.out, s.hist, cmu,
+                                                                               clam, om, ga, idt2);
         return cudaGetLastError();
     }
 #define PBNG_SPLIT(S)                                                                                             \
