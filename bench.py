@@ -223,7 +223,9 @@ def run_ours(args):
     from paper_2306_09021_b200 import context_from_scene, dd
 
     scene, full = scene_for(args.config, rank, world)
-    decomposed = args.config == 5 and world > 1  # one mesh, domain-decomposed, halo exchange per colour
+    # one mesh, domain-decomposed, halo exchange per colour: config 5 always at N > 1; any other
+    # single-mesh config with --dd (e.g. config 3 in z slabs)
+    decomposed = world > 1 and (args.config == 5 or (args.dd and args.config != 4))
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
         part = None
@@ -338,7 +340,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if args.config in (4, 5) else "weak",
+            "scaling": "strong" if (args.config == 4 or decomposed) else "weak",
             "vs_baseline": None,
             "dtype": "f32" if q["dtype"] == 0 else "f64", "data": "synthetic",
             "config": {
@@ -379,6 +381,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling runs)")
+    ap.add_argument("--dd", action="store_true", help="N > 1: domain-decompose one mesh (z slabs) instead of replicas")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("bench.py: warmup raised to 3 (timing rule)", file=sys.stderr)
