@@ -209,6 +209,40 @@ pbng_status pbng_halo_pack(pbng_ctx *ctx, int32_t colour, int32_t peer, int32_t 
 pbng_status pbng_halo_unpack(pbng_ctx *ctx, int32_t colour, int32_t peer, int32_t n_fields,
                              const void *device_buffer);
 
+/* ---- dynamic weak constraints --------------------------
+ * pbng_detect_contacts: proximity detection on the device at the current positions of sample `sample`.
+ * Boundary triangles = the tet faces that belong to exactly one tet, in order of (tet index, local face
+ * k), face k = the three vertices other than local vertex k in ascending local order, the last two swapped
+ * when the rest-state normal (v1 - v0) x (v2 - v0) points towards vertex k; bodies = connected components
+ * of tets sharing a vertex.  For every free vertex on a boundary triangle, the boundary triangle of
+ * ANOTHER body whose closest point q satisfies |x - q| <= thickness, minimising |x - q| (ties: lower
+ * triangle index), gives one weak constraint: side 0 = the vertex (weight 1), side 1 = the triangle's
+ * vertices with q's barycentric weights, K = k_n n n^T + k_t (I - n n^T), n the triangle's unit normal at
+ * the current positions (the paper's collision constraints use k_t = 0).  The paper builds
+ * such constraints every time step but gives no detection scheme (reading Z21).  Constraints
+ * are written to `out` in ascending vertex index; *n_out = their number (PBNG_E_OUT_OF_MEMORY, with
+ * *n_out set, if it exceeds max_out).  fp64 arithmetic; synchronises.  Undecomposed contexts only.
+ *
+ * pbng_update_constraints: replace the weak constraints (and, if pinned_xyz is not NULL, the Dirichlet
+ * targets, [n_batch][n_pinned][3] in the caller's original pinned order) WITHOUT a full recolouring:
+ * only the nodes incident to newly added constraints (node sets absent from the previous constraints)
+ * are recoloured, in ascending index; each keeps its previous colour unless a node sharing a tet or
+ * constraint holds it, else takes the least free colour (reading Z20).
+ * The device layout is rebuilt and re-uploaded into the bound workspace and the current iterate is
+ * kept (acceleration state reset, as pbng_set_positions; the backward-Euler target is cleared: call
+ * pbng_set_inertia again).  If the new layout needs more than the bound workspace, returns
+ * PBNG_E_OUT_OF_MEMORY with the context coloured but unbound (bind a workspace of pbng_workspace_bytes
+ * and set positions).  *n_recoloured (optional) = nodes whose colour changed.  Synchronises.
+ * Works on host-only contexts (recolouring + layout only).  Undecomposed contexts only. */
+pbng_status pbng_detect_contacts(pbng_ctx *ctx, int32_t sample, double thickness, double k_n, double k_t,
+                                 pbng_weak_constraint *out, int64_t max_out, int64_t *n_out);
+pbng_status pbng_update_constraints(pbng_ctx *ctx, const double *pinned_xyz, const pbng_weak_constraint *wc,
+                                    int64_t n_wc, int64_t *n_recoloured);
+/* The colouring in use (n_vertices int32, optional) and the number of colours (optional): pbng_color's
+ * result, or the incremental one after pbng_update_constraints.  Host-only; PBNG_E_NOT_COLORED before
+ * pbng_color. */
+pbng_status pbng_get_colours(pbng_ctx *ctx, int32_t *colour_out, int32_t *n_colours_out);
+
 /* Wait for the context's stream; PBNG_E_NONFINITE if any iteration produced a non-finite position. */
 pbng_status pbng_synchronize(pbng_ctx *ctx);
 

@@ -93,6 +93,17 @@ def lib():
             L.orc_set_inertia.argtypes = [vp, d, vp]
             L.orc_set_inertia.restype = C.c_int
             L.orc_get_mass.argtypes = [vp, vp]
+            L.orc_recolor_incremental.argtypes = [i64, i64, vp, i64, vp, vp, vp, vp, vp, C.POINTER(i64)]
+            L.orc_recolor_incremental.restype = C.c_int
+            L.orc_closest_point_triangle.argtypes = [vp, vp, vp, vp, vp]
+            L.orc_surface.argtypes = [i64, vp, vp, vp, vp]
+            L.orc_surface.restype = i64
+            L.orc_bodies.argtypes = [i64, i64, vp, vp]
+            L.orc_detect_contacts.argtypes = [i64, vp, vp, i64, vp, vp, d, vp, vp, vp]
+            L.orc_detect_contacts.restype = i64
+            L.orc_contact_stiffness.argtypes = [vp, d, d, vp]
+            L.orc_set_colours.argtypes = [vp, vp]
+            L.orc_set_colours.restype = C.c_int
             _lib = L
     return _lib
 
@@ -149,6 +160,107 @@ def mod_hess_density(mu: float, lam: float, F):
 
 def chebyshev_omega(m: int, rho: float) -> float:
     return lib().orc_chebyshev_omega(m, rho)
+
+
+# ---- dynamic weak constraints ----------------------------------------------------
+def _i32(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def _f64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def constraint_nodes(wc) -> list:
+    """Node list of every weak constraint of a scenes-style dict (side 0 then side 1, as given)."""
+    if wc is None:
+        return []
+    out = []
+    for c in range(len(wc["n0"])):
+        out.append([int(v) for v in wc["idx0"][c][:wc["n0"][c]]] + [int(v) for v in wc["idx1"][c][:wc["n1"][c]]])
+    return out
+
+
+def recolor_incremental(nv: int, tets, nodes: list, is_new, colour_prev):
+    """PAPER.md:748-754 incremental recolouring (pbng_oracle.c orc_recolor_incremental): returns
+    (colours, number of nodes whose colour changed)."""
+    tets = _i32(tets).reshape(-1, 4)
+    off = np.zeros(len(nodes) + 1, np.int64)
+    for c, n in enumerate(nodes):
+        off[c + 1] = off[c] + len(n)
+    flat = _i32(np.concatenate([np.asarray(n, np.int32) for n in nodes]) if nodes else np.zeros(1, np.int32))
+    new = np.ascontiguousarray(np.asarray(is_new, dtype=np.uint8).reshape(-1)) if nodes else np.zeros(1, np.uint8)
+    prev = _i32(colour_prev)
+    out = np.empty(nv, np.int32)
+    ch = C.c_int64()
+    st = lib().orc_recolor_incremental(nv, tets.shape[0], _p(tets), len(nodes), _p(off), _p(flat), _p(new), _p(prev),
+                                       _p(out), C.byref(ch))
+    if st:
+        raise OracleError(st)
+    return out, ch.value
+
+
+def closest_point_triangle(p, a, b, c):
+    args = [_f64(v).reshape(3) for v in (p, a, b, c)]
+    out = np.empty(3)
+    lib().orc_closest_point_triangle(*[_p(v) for v in args], _p(out))
+    return out
+
+
+def surface(tets, X):
+    tets = _i32(tets).reshape(-1, 4)
+    X = _f64(X).reshape(-1, 3)
+    tri = np.empty((4 * tets.shape[0] + 1, 3), np.int32)
+    tt = np.empty(4 * tets.shape[0] + 1, np.int32)
+    n = lib().orc_surface(tets.shape[0], _p(tets), _p(X), _p(tri), _p(tt))
+    if n < 0:
+        raise OracleError(4)
+    return tri[:n].copy(), tt[:n].copy()
+
+
+def bodies(nv: int, tets):
+    tets = _i32(tets).reshape(-1, 4)
+    out = np.empty(nv, np.int32)
+    lib().orc_bodies(nv, tets.shape[0], _p(tets), _p(out))
+    return out
+
+
+def detect_contacts(X, y, tets, free_mask, thickness: float):
+    """Per-vertex closest other-body boundary triangle within `thickness` (pbng_oracle.c
+    orc_detect_contacts): dict of tri (nv, 3; -1 = none), bary (nv, 3), normal (nv, 3), count."""
+    X = _f64(X).reshape(-1, 3)
+    y = _f64(y).reshape(-1, 3)
+    tets = _i32(tets).reshape(-1, 4)
+    fm = np.ascontiguousarray(np.asarray(free_mask, dtype=np.uint8))
+    nv = X.shape[0]
+    tri = np.empty((nv, 3), np.int32)
+    bary = np.empty((nv, 3))
+    nrm = np.empty((nv, 3))
+    n = lib().orc_detect_contacts(nv, _p(X), _p(y), tets.shape[0], _p(tets), _p(fm), float(thickness), _p(tri),
+                                  _p(bary), _p(nrm))
+    if n < 0:
+        raise OracleError(4)
+    return {"tri": tri, "bary": bary, "normal": nrm, "count": int(n)}
+
+
+def contact_constraints(contacts, kn: float, kt: float = 0.0) -> dict:
+    """The weak constraints of detected contacts, in ascending vertex order (scenes-style dict): side 0 =
+    the vertex, side 1 = the triangle with barycentric weights, K = k_n n n^T + k_t (I - n n^T)."""
+    vs = np.nonzero(contacts["tri"][:, 0] >= 0)[0]
+    n = len(vs)
+    wc = {"n0": np.ones(n, np.int32), "n1": np.full(n, 3, np.int32), "idx0": np.zeros((n, 4), np.int32),
+          "idx1": np.zeros((n, 4), np.int32), "w0": np.zeros((n, 4)), "w1": np.zeros((n, 4)),
+          "anchor": np.zeros((n, 3)), "K": np.zeros((n, 6))}
+    for k, v in enumerate(vs):
+        wc["idx0"][k, 0] = v
+        wc["w0"][k, 0] = 1.0
+        wc["idx1"][k, :3] = contacts["tri"][v]
+        wc["w1"][k, :3] = contacts["bary"][v]
+        nv_ = _f64(contacts["normal"][v])
+        K6 = np.empty(6)
+        lib().orc_contact_stiffness(_p(nv_), float(kn), float(kt), _p(K6))
+        wc["K"][k] = K6
+    return wc
 
 
 class Oracle:
@@ -219,6 +331,13 @@ class Oracle:
 
     # ---- precompute getters ------------------------------------------------------------------------
     @property
+    def set_colours(self, colours) -> None:
+        """Use a given colouring (e.g. recolor_incremental's) for the sweeps."""
+        c = np.ascontiguousarray(np.asarray(colours, dtype=np.int32))
+        st = lib().orc_set_colours(self._h, _p(c))
+        if st:
+            raise OracleError(st)
+
     def n_colours(self) -> int:
         return int(lib().orc_num_colours(self._h))
 

@@ -814,3 +814,310 @@ double orc_energy(const orc_prep *p, const double *y, double *parts) {
     if (parts) { parts[0] = el; parts[1] = wc; parts[2] = ext; }
     return el + wc + ext;
 }
+
+/* ------------------------------------------------------------------------------------------------ */
+/* Dynamic weak constraints                                                      */
+/* ------------------------------------------------------------------------------------------------ */
+
+/* Incremental node recolouring, PAPER.md:748-754 ("Collision Coloring"): only the nodes incident to the
+ * newly added weak constraints are recoloured; for each such node x the used colour set is the union
+ * of the colours of the stencils containing x; x keeps its previous colour as the initial guess unless
+ * that colour is used, in which case it takes the minimal unused colour.  Reading Z20 (the paper is
+ * silent on the order): the nodes are visited in ascending index and a node's used set sees the NEW
+ * colours of the nodes visited before it; a stencil's colours exclude x itself.
+ * Stencils: the nt tets (4 nodes each) and the nc constraints of the NEW constraint set (node lists in
+ * CSR c_off / c_nodes, duplicates allowed); is_new[c] != 0 marks the newly added ones.
+ * Returns the number of nodes whose colour changed in *n_changed (optional). */
+int orc_recolor_incremental(int64_t nv, int64_t nt, const int32_t *tets, int64_t nc, const int64_t *c_off,
+                            const int32_t *c_nodes, const uint8_t *is_new, const int32_t *colour_prev,
+                            int32_t *colour_out, int64_t *n_changed) {
+    int64_t v, e, c, k, changed = 0;
+    int64_t *vs_off = calloc((size_t)nv + 1, sizeof(int64_t));
+    int64_t *vs, *fill;
+    uint8_t *extra = calloc((size_t)nv + 1, 1);
+    int32_t maxc = 0;
+    char *used;
+    if (!vs_off || !extra) { free(vs_off); free(extra); return ORC_E_NOMEM; }
+    for (v = 0; v < nv; ++v) {
+        colour_out[v] = colour_prev[v];
+        if (colour_prev[v] + 1 > maxc) maxc = colour_prev[v] + 1;
+    }
+    /* vertex -> stencil incidence (stencil id: tets 0..nt-1, constraint c -> nt + c) */
+    for (e = 0; e < nt; ++e)
+        for (k = 0; k < 4; ++k) vs_off[tets[4 * e + k] + 1]++;
+    for (c = 0; c < nc; ++c)
+        for (k = c_off[c]; k < c_off[c + 1]; ++k) vs_off[c_nodes[k] + 1]++;
+    for (v = 0; v < nv; ++v) vs_off[v + 1] += vs_off[v];
+    vs = malloc(((size_t)vs_off[nv] + 1) * sizeof(int64_t));
+    fill = malloc(((size_t)nv + 1) * sizeof(int64_t));
+    used = malloc((size_t)maxc + 8 * (size_t)(nc + 1) + 64);
+    if (!vs || !fill || !used) { free(vs_off); free(extra); free(vs); free(fill); free(used); return ORC_E_NOMEM; }
+    memcpy(fill, vs_off, (size_t)nv * sizeof(int64_t));
+    for (e = 0; e < nt; ++e)
+        for (k = 0; k < 4; ++k) vs[fill[tets[4 * e + k]]++] = e;
+    for (c = 0; c < nc; ++c)
+        for (k = c_off[c]; k < c_off[c + 1]; ++k) vs[fill[c_nodes[k]]++] = nt + c;
+    /* the nodes incident to newly added constraints */
+    for (c = 0; c < nc; ++c)
+        if (is_new[c])
+            for (k = c_off[c]; k < c_off[c + 1]; ++k) extra[c_nodes[k]] = 1;
+    for (v = 0; v < nv; ++v) {
+        int64_t q;
+        int32_t col, cap;
+        if (!extra[v]) continue;
+        cap = maxc + 1;
+        memset(used, 0, (size_t)cap + 1);
+        for (q = vs_off[v]; q < vs_off[v + 1]; ++q) {
+            const int64_t s = vs[q];
+            if (s < nt) {
+                for (k = 0; k < 4; ++k)
+                    if (tets[4 * s + k] != v) used[colour_out[tets[4 * s + k]]] = 1;
+            } else {
+                for (k = c_off[s - nt]; k < c_off[s - nt + 1]; ++k)
+                    if (c_nodes[k] != v) used[colour_out[c_nodes[k]]] = 1;
+            }
+        }
+        if (used[colour_prev[v]]) {
+            col = 0;
+            while (used[col]) ++col;
+            colour_out[v] = col;
+            if (col + 1 > maxc) maxc = col + 1;
+            ++changed;
+        }
+    }
+    if (n_changed) *n_changed = changed;
+    free(vs_off); free(extra); free(vs); free(fill); free(used);
+    return ORC_OK;
+}
+
+/* Closest point of triangle (a, b, c) to p, as barycentric weights (u, v, w): q = u a + v b + w c.
+ * Textbook Voronoi-region classification: vertex regions, then edge regions, then the interior. */
+void orc_closest_point_triangle(const double *p, const double *a, const double *b, const double *c, double *bary) {
+    double ab[3], ac[3], ap[3], bp[3], cp[3];
+    double d1, d2, d3, d4, d5, d6, va, vb, vc, t, den;
+    int k;
+    for (k = 0; k < 3; ++k) {
+        ab[k] = b[k] - a[k];
+        ac[k] = c[k] - a[k];
+        ap[k] = p[k] - a[k];
+        bp[k] = p[k] - b[k];
+        cp[k] = p[k] - c[k];
+    }
+    d1 = ab[0] * ap[0] + ab[1] * ap[1] + ab[2] * ap[2];
+    d2 = ac[0] * ap[0] + ac[1] * ap[1] + ac[2] * ap[2];
+    if (d1 <= 0.0 && d2 <= 0.0) { bary[0] = 1.0; bary[1] = 0.0; bary[2] = 0.0; return; }
+    d3 = ab[0] * bp[0] + ab[1] * bp[1] + ab[2] * bp[2];
+    d4 = ac[0] * bp[0] + ac[1] * bp[1] + ac[2] * bp[2];
+    if (d3 >= 0.0 && d4 <= d3) { bary[0] = 0.0; bary[1] = 1.0; bary[2] = 0.0; return; }
+    vc = d1 * d4 - d3 * d2;
+    if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+        t = d1 / (d1 - d3);
+        bary[0] = 1.0 - t; bary[1] = t; bary[2] = 0.0;
+        return;
+    }
+    d5 = ab[0] * cp[0] + ab[1] * cp[1] + ab[2] * cp[2];
+    d6 = ac[0] * cp[0] + ac[1] * cp[1] + ac[2] * cp[2];
+    if (d6 >= 0.0 && d5 <= d6) { bary[0] = 0.0; bary[1] = 0.0; bary[2] = 1.0; return; }
+    vb = d5 * d2 - d1 * d6;
+    if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+        t = d2 / (d2 - d6);
+        bary[0] = 1.0 - t; bary[1] = 0.0; bary[2] = t;
+        return;
+    }
+    va = d3 * d6 - d5 * d4;
+    if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
+        t = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+        bary[0] = 0.0; bary[1] = 1.0 - t; bary[2] = t;
+        return;
+    }
+    den = 1.0 / (va + vb + vc);
+    bary[1] = vb * den;
+    bary[2] = vc * den;
+    bary[0] = 1.0 - bary[1] - bary[2];
+}
+
+/* Boundary triangles of a tet mesh: the faces that belong to exactly one tet, in order of (tet index,
+ * local face k), face k = the three vertices other than local vertex k, oriented so that the normal
+ * (v1 - v0) x (v2 - v0) points away from the tet's vertex k at the REST positions X.  tri (capacity
+ * 3 * 4 nt) receives the vertex triples, tri_tet the owning tet; returns the count. */
+int64_t orc_surface(int64_t nt, const int32_t *tets, const double *X, int32_t *tri, int32_t *tri_tet) {
+    int64_t e, f, n = 0;
+    /* a face is interior iff another tet has the same vertex set: brute-force key compare over all faces
+     * (sorted triples, quadratic in the face count is too slow, so sort the keys) */
+    int64_t nf = 4 * nt, i, j;
+    int64_t *key = malloc((size_t)(nf + 1) * 3 * sizeof(int64_t));
+    int64_t *idx = malloc((size_t)(nf + 1) * sizeof(int64_t));
+    uint8_t *interior = calloc((size_t)nf + 1, 1);
+    if (!key || !idx || !interior) { free(key); free(idx); free(interior); return -1; }
+    for (e = 0; e < nt; ++e)
+        for (f = 0; f < 4; ++f) {
+            int32_t v[3], m = 0, k, t;
+            for (k = 0; k < 4; ++k)
+                if (k != f) v[m++] = tets[4 * e + k];
+            /* sort the triple */
+            if (v[0] > v[1]) { t = v[0]; v[0] = v[1]; v[1] = t; }
+            if (v[1] > v[2]) { t = v[1]; v[1] = v[2]; v[2] = t; }
+            if (v[0] > v[1]) { t = v[0]; v[0] = v[1]; v[1] = t; }
+            key[3 * (4 * e + f)] = v[0]; key[3 * (4 * e + f) + 1] = v[1]; key[3 * (4 * e + f) + 2] = v[2];
+            idx[4 * e + f] = 4 * e + f;
+        }
+    /* insertion-free sort: simple bottom-up merge sort of idx by key */
+    {
+        int64_t *tmp = malloc((size_t)(nf + 1) * sizeof(int64_t)), w;
+        if (!tmp) { free(key); free(idx); free(interior); return -1; }
+        for (w = 1; w < nf; w *= 2) {
+            for (i = 0; i < nf; i += 2 * w) {
+                int64_t lo = i, mid = i + w < nf ? i + w : nf, hi = i + 2 * w < nf ? i + 2 * w : nf;
+                int64_t a = lo, b = mid, o = lo;
+                while (a < mid && b < hi) {
+                    const int64_t *ka = key + 3 * idx[a], *kb = key + 3 * idx[b];
+                    int less = ka[0] < kb[0] || (ka[0] == kb[0] && (ka[1] < kb[1] || (ka[1] == kb[1] && ka[2] <= kb[2])));
+                    tmp[o++] = less ? idx[a++] : idx[b++];
+                }
+                while (a < mid) tmp[o++] = idx[a++];
+                while (b < hi) tmp[o++] = idx[b++];
+            }
+            memcpy(idx, tmp, (size_t)nf * sizeof(int64_t));
+        }
+        free(tmp);
+    }
+    for (i = 0; i + 1 < nf; ++i) {
+        const int64_t *ka = key + 3 * idx[i];
+        for (j = i + 1; j < nf; ++j) {
+            const int64_t *kb = key + 3 * idx[j];
+            if (ka[0] != kb[0] || ka[1] != kb[1] || ka[2] != kb[2]) break;
+            interior[idx[i]] = 1;
+            interior[idx[j]] = 1;
+        }
+    }
+    for (e = 0; e < nt; ++e)
+        for (f = 0; f < 4; ++f) {
+            int32_t v[3], m = 0, k;
+            double u[3], w[3], nrm[3], d[3], s;
+            if (interior[4 * e + f]) continue;
+            for (k = 0; k < 4; ++k)
+                if (k != f) v[m++] = tets[4 * e + k];
+            for (k = 0; k < 3; ++k) {
+                u[k] = X[3 * v[1] + k] - X[3 * v[0] + k];
+                w[k] = X[3 * v[2] + k] - X[3 * v[0] + k];
+                d[k] = X[3 * tets[4 * e + f] + k] - X[3 * v[0] + k];
+            }
+            cross3(u, w, nrm);
+            s = nrm[0] * d[0] + nrm[1] * d[1] + nrm[2] * d[2];
+            if (s > 0.0) { int32_t t = v[1]; v[1] = v[2]; v[2] = t; } /* vertex k must lie behind */
+            tri[3 * n] = v[0]; tri[3 * n + 1] = v[1]; tri[3 * n + 2] = v[2];
+            tri_tet[n] = (int32_t)e;
+            ++n;
+        }
+    free(key); free(idx); free(interior);
+    return n;
+}
+
+/* Bodies: connected components of the tets (two tets are connected when they share a vertex); body[v]
+ * = smallest vertex index of v's component (vertices in no tet are their own body). */
+void orc_bodies(int64_t nv, int64_t nt, const int32_t *tets, int32_t *body) {
+    int64_t v, e, k;
+    int changed = 1;
+    for (v = 0; v < nv; ++v) body[v] = (int32_t)v;
+    while (changed) { /* label propagation to the component minimum (plain fixed-point iteration) */
+        changed = 0;
+        for (e = 0; e < nt; ++e) {
+            int32_t m = body[tets[4 * e]];
+            for (k = 1; k < 4; ++k)
+                if (body[tets[4 * e + k]] < m) m = body[tets[4 * e + k]];
+            for (k = 0; k < 4; ++k)
+                if (body[tets[4 * e + k]] != m) { body[tets[4 * e + k]] = m; changed = 1; }
+        }
+        for (v = 0; v < nv; ++v) /* path compression: follow labels to their fixed point */
+            while (body[body[v]] != body[v]) body[v] = body[body[v]];
+    }
+}
+
+/* Contact weak constraints at positions y (the paper builds collision weak constraints
+ * dynamically but specifies no detection scheme, PAPER.md:843-846 -- reading Z21): for every free vertex
+ * of a boundary triangle, the closest boundary triangle of ANOTHER body (orc_bodies) whose closest point
+ * is within `thickness` (|p - q|^2 <= thickness^2; ties -> lower triangle index).  The constraint has side
+ * 0 = the vertex (weight 1), side 1 = the triangle's vertices with the closest point's barycentric
+ * weights, and K = k_n n n^T with n the triangle's unit normal at y (k_tau = 0).
+ * Outputs per vertex (dense, nv entries): tri_out (3 ids, -1 if none), bary (3), normal (3).
+ * Brute force over all triangle pairs (test sizes only).  Returns the number of contacts. */
+int64_t orc_detect_contacts(int64_t nv, const double *X, const double *y, int64_t nt, const int32_t *tets,
+                            const uint8_t *is_free, double thickness, int32_t *tri_out, double *bary_out,
+                            double *normal_out) {
+    int32_t *tri = malloc((size_t)(12 * nt + 3) * sizeof(int32_t));
+    int32_t *tri_tet = malloc((size_t)(4 * nt + 1) * sizeof(int32_t));
+    int32_t *body = malloc((size_t)(nv + 1) * sizeof(int32_t));
+    uint8_t *on_surf = calloc((size_t)nv + 1, 1);
+    int64_t ntri, v, t, found = 0;
+    if (!tri || !tri_tet || !body || !on_surf) { free(tri); free(tri_tet); free(body); free(on_surf); return -1; }
+    ntri = orc_surface(nt, tets, X, tri, tri_tet);
+    orc_bodies(nv, nt, tets, body);
+    for (t = 0; t < 3 * ntri; ++t) on_surf[tri[t]] = 1;
+    for (v = 0; v < nv; ++v) {
+        double best = 0.0, bb[3] = {0, 0, 0};
+        int64_t bt = -1;
+        tri_out[3 * v] = tri_out[3 * v + 1] = tri_out[3 * v + 2] = -1;
+        bary_out[3 * v] = bary_out[3 * v + 1] = bary_out[3 * v + 2] = 0.0;
+        normal_out[3 * v] = normal_out[3 * v + 1] = normal_out[3 * v + 2] = 0.0;
+        if (!on_surf[v] || !is_free[v]) continue;
+        for (t = 0; t < ntri; ++t) {
+            const int32_t *tv = tri + 3 * t;
+            double br[3], q[3], d2 = 0.0;
+            int k;
+            if (body[tv[0]] == body[v]) continue;
+            orc_closest_point_triangle(y + 3 * v, y + 3 * tv[0], y + 3 * tv[1], y + 3 * tv[2], br);
+            for (k = 0; k < 3; ++k) {
+                q[k] = br[0] * y[3 * tv[0] + k] + br[1] * y[3 * tv[1] + k] + br[2] * y[3 * tv[2] + k];
+                d2 += (y[3 * v + k] - q[k]) * (y[3 * v + k] - q[k]);
+            }
+            if (d2 <= thickness * thickness && (bt < 0 || d2 < best)) {
+                best = d2; bt = t;
+                bb[0] = br[0]; bb[1] = br[1]; bb[2] = br[2];
+            }
+        }
+        if (bt >= 0) {
+            const int32_t *tv = tri + 3 * bt;
+            double u[3], w[3], nrm[3], s;
+            int k;
+            for (k = 0; k < 3; ++k) {
+                u[k] = y[3 * tv[1] + k] - y[3 * tv[0] + k];
+                w[k] = y[3 * tv[2] + k] - y[3 * tv[0] + k];
+            }
+            cross3(u, w, nrm);
+            s = norm3(nrm);
+            for (k = 0; k < 3; ++k) {
+                tri_out[3 * v + k] = tv[k];
+                bary_out[3 * v + k] = bb[k];
+                normal_out[3 * v + k] = s > 0.0 ? nrm[k] / s : 0.0;
+            }
+            ++found;
+        }
+    }
+    free(tri); free(tri_tet); free(body); free(on_surf);
+    return found;
+}
+
+/* K = k_n n n^T + k_tau (I - n n^T) of a contact weak constraint (k_tau = 0 for collisions),
+ * as the six entries xx, yy, zz, xy, yz, xz */
+void orc_contact_stiffness(const double *n, double kn, double kt, double *K6) {
+    K6[0] = kn * n[0] * n[0] + kt * (1.0 - n[0] * n[0]);
+    K6[1] = kn * n[1] * n[1] + kt * (1.0 - n[1] * n[1]);
+    K6[2] = kn * n[2] * n[2] + kt * (1.0 - n[2] * n[2]);
+    K6[3] = (kn - kt) * n[0] * n[1];
+    K6[4] = (kn - kt) * n[1] * n[2];
+    K6[5] = (kn - kt) * n[0] * n[2];
+}
+
+/* Replace the colouring (e.g. by orc_recolor_incremental's); sweeps then visit these colours in ascending
+ * order.  Returns ORC_E_ARG for a negative colour. */
+int orc_set_colours(orc_prep *p, const int32_t *colour) {
+    int64_t v;
+    int32_t m = 0;
+    for (v = 0; v < p->nv; ++v) {
+        if (colour[v] < 0) return ORC_E_ARG;
+        if (colour[v] + 1 > m) m = colour[v] + 1;
+    }
+    memcpy(p->colour, colour, (size_t)p->nv * sizeof(int32_t));
+    p->ncolours = m;
+    return ORC_OK;
+}

@@ -7,6 +7,7 @@
 #include "pbng.h"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -143,6 +144,13 @@ struct pbng_ctx {
     std::vector<int32_t> h_deg, h_wc_off, h_wc_cid, h_c_n, h_c_node;
     std::vector<unsigned char> h_mass;  // Real [n_own] lumped masses (backward Euler)
     std::vector<int32_t> h_dep_off, h_deps;  // pipelined schedule: per chunk its neighbour chunks (Layout)
+    // contact detection (pbng_detect_contacts): boundary triangles {v0, v1, v2, body} and the free boundary
+    // vertices {vertex, body}, internal ids; tri_orig = the triangles' original vertex ids
+    std::vector<int4> h_surf;
+    std::vector<int2> h_sv;
+    std::vector<int32_t> surf_orig;
+    std::vector<int64_t> pin_order;  // caller order of the pinned set -> ascending order (set_constraints)
+    uint64_t ws_bytes = 0;           // bytes of the bound workspace
     int schedule = 0;                        // pbng_schedule requested (0 auto, 1 colour launches, 2 pipelined)
     std::vector<int4> h_tet_id;
     Problem prob;
@@ -150,7 +158,7 @@ struct pbng_ctx {
     Region r_rec_id, r_rec_a, r_rec_b, r_rec_c, r_chunk_off, r_chunk_v, r_deg, r_fext, r_wc_off, r_wc_cid, r_wc_d,
         r_c_n, r_c_node, r_c_w, r_c_anchor, r_c_K, r_tet_id, r_tet_a, r_tet_b, r_tet_c, r_int2orig, r_targets,
         r_x[3], r_stage, r_part_e, r_part_r, r_results, r_flag, r_halo_send, r_halo_recv, r_mass, r_xt, r_dep_off,
-        r_deps, r_pipe;
+        r_deps, r_pipe, r_surf, r_sv, r_chead, r_cnext, r_cres, r_cscal;
     size_t ws_need = 0;
     // bound device state
     bool bound = false;
@@ -496,6 +504,154 @@ void build_pipeline(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::
     }
 }
 
+// Boundary triangles of the mesh (faces of exactly one tet) in order of (tet, local face k), face k = the
+// other three vertices in ascending local order, the last two swapped when the rest-state normal
+// (v1 - v0) x (v2 - v0) points towards local vertex k (include/pbng.h pbng_detect_contacts), and bodies
+// = connected components of tets sharing a vertex, labelled by their smallest vertex index.  Only for
+// an undecomposed context.
+void build_surface(pbng_ctx *c) {
+    c->h_surf.clear();
+    c->h_sv.clear();
+    c->surf_orig.clear();
+    c->prob.n_surf = c->prob.n_sv = 0;
+    c->prob.n_cbuckets = 1;
+    if (c->n_ranks > 1 || c->nt == 0) return;
+    const int64_t nt = c->nt, nv = c->nv;
+    // union-find over vertices
+    std::vector<int32_t> par((size_t)nv);
+    for (int64_t v = 0; v < nv; ++v) par[v] = (int32_t)v;
+    auto root = [&](int32_t v) {
+        while (par[v] != v) { par[v] = par[par[v]]; v = par[v]; }
+        return v;
+    };
+    for (int64_t e = 0; e < nt; ++e)
+        for (int a = 1; a < 4; ++a) {
+            const int32_t r0 = root(c->tets[4 * e]), r1 = root(c->tets[4 * e + a]);
+            if (r0 != r1) par[std::max(r0, r1)] = std::min(r0, r1);
+        }
+    std::vector<int32_t> body((size_t)nv);
+    for (int64_t v = 0; v < nv; ++v) body[v] = root((int32_t)v);  // the component's minimum vertex
+    // faces keyed by their sorted triple; a face is on the boundary iff its key occurs once
+    std::vector<std::pair<std::array<int32_t, 3>, int64_t>> key((size_t)(4 * nt));
+    for (int64_t e = 0; e < nt; ++e)
+        for (int f = 0; f < 4; ++f) {
+            std::array<int32_t, 3> k;
+            int m = 0;
+            for (int a = 0; a < 4; ++a)
+                if (a != f) k[m++] = c->tets[4 * e + a];
+            std::sort(k.begin(), k.end());
+            key[4 * e + f] = {k, 4 * e + f};
+        }
+    std::sort(key.begin(), key.end());
+    std::vector<char> boundary((size_t)(4 * nt), 0);
+    for (size_t i = 0; i < key.size();) {
+        size_t j = i + 1;
+        while (j < key.size() && key[j].first == key[i].first) ++j;
+        if (j == i + 1) boundary[key[i].second] = 1;
+        i = j;
+    }
+    std::vector<char> on_surf((size_t)nv, 0);
+    for (int64_t e = 0; e < nt; ++e)
+        for (int f = 0; f < 4; ++f) {
+            if (!boundary[4 * e + f]) continue;
+            int32_t v[3];
+            int m = 0;
+            for (int a = 0; a < 4; ++a)
+                if (a != f) v[m++] = c->tets[4 * e + a];
+            const double *x0 = &c->X[3 * v[0]], *x1 = &c->X[3 * v[1]], *x2 = &c->X[3 * v[2]],
+                         *xk = &c->X[3 * c->tets[4 * e + f]];
+            const double u[3] = {x1[0] - x0[0], x1[1] - x0[1], x1[2] - x0[2]};
+            const double w[3] = {x2[0] - x0[0], x2[1] - x0[1], x2[2] - x0[2]};
+            const double n[3] = {u[1] * w[2] - u[2] * w[1], u[2] * w[0] - u[0] * w[2], u[0] * w[1] - u[1] * w[0]};
+            if (n[0] * (xk[0] - x0[0]) + n[1] * (xk[1] - x0[1]) + n[2] * (xk[2] - x0[2]) > 0.0) std::swap(v[1], v[2]);
+            for (int a = 0; a < 3; ++a) {
+                c->surf_orig.push_back(v[a]);
+                on_surf[v[a]] = 1;
+            }
+            c->h_surf.push_back(make_int4(c->orig2int[v[0]], c->orig2int[v[1]], c->orig2int[v[2]], body[v[0]]));
+        }
+    std::vector<char> is_pinned((size_t)nv, 0);
+    for (int32_t p : c->pinned) is_pinned[p] = 1;
+    for (int64_t v = 0; v < nv; ++v)
+        if (on_surf[v] && !is_pinned[v]) c->h_sv.push_back(make_int2(c->orig2int[v], body[v]));
+    c->prob.n_surf = (int64_t)c->h_surf.size();
+    c->prob.n_sv = (int64_t)c->h_sv.size();
+    int64_t nb = 1;
+    while (nb < 16 * std::max<int64_t>(c->prob.n_surf, 1)) nb <<= 1;
+    c->prob.n_cbuckets = nb;
+}
+
+// Incremental recolouring of pbng_update_constraints: the nodes incident to the new
+// constraints (nodes_new) are visited in ascending index; each keeps its colour unless a node sharing a
+// stencil (tet or constraint of the new set) holds it, in which case it takes the least colour no such
+// node holds (reading Z20).  `nodes` = distinct node lists of the new constraint set.
+std::vector<int32_t> recolour_incremental(const pbng_ctx *c, const std::vector<std::vector<int32_t>> &nodes,
+                                          const std::vector<char> &is_new, int64_t *changed) {
+    const int64_t nv = c->nv, nt = c->nt;
+    std::vector<int32_t> col = c->colour;
+    std::vector<std::vector<int32_t>> vcons((size_t)nv);  // vertex -> constraints
+    std::vector<char> extra((size_t)nv, 0);
+    for (size_t q = 0; q < nodes.size(); ++q)
+        for (int32_t v : nodes[q]) {
+            vcons[v].push_back((int32_t)q);
+            if (is_new[q]) extra[v] = 1;
+        }
+    std::vector<std::vector<int32_t>> vtets((size_t)nv);
+    for (int64_t e = 0; e < nt; ++e)
+        for (int a = 0; a < 4; ++a)
+            if (extra[c->tets[4 * e + a]]) vtets[c->tets[4 * e + a]].push_back((int32_t)e);
+    int32_t ncol = 0;
+    for (int32_t k : col) ncol = std::max(ncol, k + 1);
+    *changed = 0;
+    std::vector<char> used;
+    for (int64_t v = 0; v < nv; ++v) {
+        if (!extra[v]) continue;
+        used.assign((size_t)ncol + 1, 0);
+        for (int32_t e : vtets[v])
+            for (int a = 0; a < 4; ++a)
+                if (c->tets[4 * e + a] != v) used[col[c->tets[4 * e + a]]] = 1;
+        for (int32_t q : vcons[v])
+            for (int32_t u : nodes[q])
+                if (u != v) used[col[u]] = 1;
+        if (!used[col[v]]) continue;
+        int32_t k = 0;
+        while (used[k]) ++k;
+        col[v] = k;
+        ncol = std::max(ncol, k + 1);
+        ++*changed;
+    }
+    return col;
+}
+
+pbng_status validate_wc(const pbng_ctx *c, const pbng_weak_constraint *wc, int64_t n_wc, const char *who) {
+    const std::string w0(who);
+    for (int64_t q = 0; q < n_wc; ++q) {
+        const pbng_weak_constraint &w = wc[q];
+        if (w.n0 < 1 || w.n0 > 4 || w.n1 < 0 || w.n1 > 4)
+            return fail(PBNG_E_INVALID_ARGUMENT, w0 + ": weak constraint " + std::to_string(q) + " has bad node counts");
+        for (int a = 0; a < w.n0; ++a)
+            if (w.idx0[a] < 0 || w.idx0[a] >= c->nv || !std::isfinite(w.w0[a]))
+                return fail(PBNG_E_INDEX_OUT_OF_RANGE, w0 + ": weak constraint " + std::to_string(q) + " side 0");
+        for (int a = 0; a < w.n1; ++a)
+            if (w.idx1[a] < 0 || w.idx1[a] >= c->nv || !std::isfinite(w.w1[a]))
+                return fail(PBNG_E_INDEX_OUT_OF_RANGE, w0 + ": weak constraint " + std::to_string(q) + " side 1");
+        for (int a = 0; a < 6; ++a)
+            if (!std::isfinite(w.K[a])) return fail(PBNG_E_INVALID_ARGUMENT, w0 + ": non-finite K");
+        for (int a = 0; a < 3; ++a)
+            if (!std::isfinite(w.anchor[a])) return fail(PBNG_E_INVALID_ARGUMENT, w0 + ": non-finite anchor");
+    }
+    return PBNG_OK;
+}
+
+std::vector<int32_t> distinct_nodes(const pbng_weak_constraint &w) {
+    std::vector<int32_t> n;
+    for (int a = 0; a < w.n0; ++a) n.push_back(w.idx0[a]);
+    for (int a = 0; a < w.n1; ++a) n.push_back(w.idx1[a]);
+    std::sort(n.begin(), n.end());
+    n.erase(std::unique(n.begin(), n.end()), n.end());
+    return n;
+}
+
 bool pipeline_available(const pbng_ctx *c) { return c->n_ranks == 1 && c->prob.lane_shift == 0 && c->n_chunks > 0; }
 
 int problem_split(const pbng_ctx *c);
@@ -561,6 +717,12 @@ void plan_workspace(pbng_ctx *c) {
     take(c->r_dep_off, c->h_dep_off.size() * 4);
     take(c->r_deps, std::max<size_t>(c->h_deps.size(), 1) * 4);
     take(c->r_pipe, 8 + (size_t)c->nb * (size_t)std::max<int64_t>(c->n_chunks, 1) * 4);  // counter, flags
+    take(c->r_surf, std::max<size_t>(c->h_surf.size(), 1) * 16);
+    take(c->r_sv, std::max<size_t>(c->h_sv.size(), 1) * 8);
+    take(c->r_chead, (size_t)std::max<int64_t>(c->prob.n_cbuckets, 1) * 4);
+    take(c->r_cnext, std::max<size_t>(c->h_surf.size(), 1) * 8 * 8);  // <= 8 cells per triangle, {tri, next}
+    take(c->r_cres, std::max<size_t>(c->h_sv.size(), 1) * sizeof(ContactHit));
+    take(c->r_cscal, 64);
     c->ws_need = off;
 }
 
@@ -822,25 +984,15 @@ pbng_status pbng_set_constraints(pbng_ctx *c, const int32_t *pinned, int64_t n_p
     }
     for (int64_t k = 0; k < (int64_t)c->nb * n_pinned * 3; ++k)
         if (!std::isfinite(pinned_xyz[k])) return fail(PBNG_E_INVALID_ARGUMENT, "set_constraints: non-finite target");
-    for (int64_t q = 0; q < n_wc; ++q) {
-        const pbng_weak_constraint &w = wc[q];
-        if (w.n0 < 1 || w.n0 > 4 || w.n1 < 0 || w.n1 > 4)
-            return fail(PBNG_E_INVALID_ARGUMENT, "set_constraints: weak constraint " + std::to_string(q) + " has bad node counts");
-        for (int a = 0; a < w.n0; ++a)
-            if (w.idx0[a] < 0 || w.idx0[a] >= c->nv || !std::isfinite(w.w0[a]))
-                return fail(PBNG_E_INDEX_OUT_OF_RANGE, "set_constraints: weak constraint " + std::to_string(q) + " side 0");
-        for (int a = 0; a < w.n1; ++a)
-            if (w.idx1[a] < 0 || w.idx1[a] >= c->nv || !std::isfinite(w.w1[a]))
-                return fail(PBNG_E_INDEX_OUT_OF_RANGE, "set_constraints: weak constraint " + std::to_string(q) + " side 1");
-        for (int a = 0; a < 6; ++a)
-            if (!std::isfinite(w.K[a])) return fail(PBNG_E_INVALID_ARGUMENT, "set_constraints: non-finite K");
-        for (int a = 0; a < 3; ++a)
-            if (!std::isfinite(w.anchor[a])) return fail(PBNG_E_INVALID_ARGUMENT, "set_constraints: non-finite anchor");
+    {
+        pbng_status st = validate_wc(c, wc, n_wc, "set_constraints");
+        if (st != PBNG_OK) return st;
     }
     try {
         std::vector<int64_t> order((size_t)n_pinned);
         for (int64_t k = 0; k < n_pinned; ++k) order[k] = k;
         std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return pinned[a] < pinned[b]; });
+        c->pin_order = order;
         c->pinned.resize((size_t)n_pinned);
         c->targets.resize((size_t)c->nb * n_pinned * 3);
         for (int64_t k = 0; k < n_pinned; ++k) {
@@ -858,10 +1010,9 @@ pbng_status pbng_set_constraints(pbng_ctx *c, const int32_t *pinned, int64_t n_p
     return PBNG_OK;
 }
 
-pbng_status pbng_color(pbng_ctx *c, int32_t *colour_out, int32_t *n_colours_out) {
-    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
-    if (!c->has_material || !c->has_constraints)
-        return fail(PBNG_E_BAD_ORDER, "color: set_material and set_constraints must come first");
+// colouring (greedy, or `given` -- the incremental recolouring of pbng_update_constraints) and the
+// colour-sorted device layout it implies
+static pbng_status colour_and_layout(pbng_ctx *c, const std::vector<int32_t> *given) {
     try {
         const int64_t nv = c->nv, nt = c->nt, nwc = (int64_t)c->wc.size();
         // vertex -> incident tets (ascending tet index) and vertex -> stencils (tets, then constraints)
@@ -901,9 +1052,15 @@ pbng_status pbng_color(pbng_ctx *c, int32_t *colour_out, int32_t *n_colours_out)
         for (int64_t v = 0; v < nv; ++v)
             if (!is_pinned[v] && vs_off[v + 1] == vs_off[v])
                 return fail(PBNG_E_ISOLATED_VERTEX, "color: free vertex " + std::to_string(v) + " has no element or constraint");
-        c->colour.assign((size_t)nv, 0);
-        pbng_status st = colour_greedy(c, vs_off, vs);
-        if (st != PBNG_OK) return st;
+        if (given) {
+            c->colour = *given;
+            c->ncol = 0;
+            for (int32_t k : c->colour) c->ncol = std::max(c->ncol, k + 1);
+        } else {
+            c->colour.assign((size_t)nv, 0);
+            pbng_status st = colour_greedy(c, vs_off, vs);
+            if (st != PBNG_OK) return st;
+        }
         // ---- which vertices this context holds (domain decomposition; one rank = everything) ----------
         // need[v] = ranks that hold v: a rank holds every vertex of a stencil touching one of its free
         // vertices, and the vertices of the tets / constraints whose energy it evaluates (owner of the
@@ -1038,6 +1195,7 @@ pbng_status pbng_color(pbng_ctx *c, int32_t *colour_out, int32_t *n_colours_out)
         if (c->dtype == DT_F64) build_layout<double>(c, vt_off, vt);
         else build_layout<float>(c, vt_off, vt);
         build_pipeline(c, vt_off, vt);
+        build_surface(c);
         plan_workspace(c);
     } catch (const std::bad_alloc &) {
         return fail(PBNG_E_OUT_OF_MEMORY, "color: host allocation");
@@ -1045,6 +1203,15 @@ pbng_status pbng_color(pbng_ctx *c, int32_t *colour_out, int32_t *n_colours_out)
     c->colored = true;
     c->bound = false;
     c->positions_set = false;
+    return PBNG_OK;
+}
+
+pbng_status pbng_color(pbng_ctx *c, int32_t *colour_out, int32_t *n_colours_out) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    if (!c->has_material || !c->has_constraints)
+        return fail(PBNG_E_BAD_ORDER, "color: set_material and set_constraints must come first");
+    pbng_status st = colour_and_layout(c, nullptr);
+    if (st != PBNG_OK) return st;
     if (colour_out) std::memcpy(colour_out, c->colour.data(), (size_t)c->nv * 4);
     if (n_colours_out) *n_colours_out = c->ncol;
     return PBNG_OK;
@@ -1100,6 +1267,12 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     L.xtilde = at(c->r_xt);
     L.halo_send = static_cast<const int32_t *>(at(c->r_halo_send));
     L.halo_recv = static_cast<const int32_t *>(at(c->r_halo_recv));
+    L.surf = static_cast<const int4 *>(at(c->r_surf));
+    L.sv = static_cast<const int2 *>(at(c->r_sv));
+    L.c_head = static_cast<int32_t *>(at(c->r_chead));
+    L.c_next = static_cast<int2 *>(at(c->r_cnext));
+    L.c_res = static_cast<ContactHit *>(at(c->r_cres));
+    L.c_scal = static_cast<uint32_t *>(at(c->r_cscal));
     L.dep_off = static_cast<const int32_t *>(at(c->r_dep_off));
     L.deps = static_cast<const int32_t *>(at(c->r_deps));
     L.pipe_counter = static_cast<uint64_t *>(at(c->r_pipe));
@@ -1135,12 +1308,15 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     chk(up(c->r_halo_send, c->h_halo_send.data(), c->h_halo_send.size() * 4));
     chk(up(c->r_halo_recv, c->h_halo_recv.data(), c->h_halo_recv.size() * 4));
     chk(up(c->r_targets, c->h_targets.data(), c->h_targets.size()));
+    chk(up(c->r_surf, c->h_surf.data(), c->h_surf.size() * 16));
+    chk(up(c->r_sv, c->h_sv.data(), c->h_sv.size() * 8));
     chk(up(c->r_dep_off, c->h_dep_off.data(), c->h_dep_off.size() * 4));
     chk(up(c->r_deps, c->h_deps.data(), c->h_deps.size() * 4));
     chk(cudaMemsetAsync(base + c->r_flag.off, 0, 4, c->stream));
     chk(cudaStreamSynchronize(c->stream));
     if (e != cudaSuccess) return cuda_fail(e, "bind_workspace");
     c->ws = dptr;
+    c->ws_bytes = bytes;
     c->L = L;
     c->bound = true;
     c->positions_set = false;
@@ -1488,6 +1664,131 @@ pbng_status pbng_test_polar(pbng_dtype dtype, const double *F, double *R, int64_
     cudaFree(dF);
     if (dR) cudaFree(dR);
     if (e != cudaSuccess) return cuda_fail(e, "test_polar");
+    return PBNG_OK;
+}
+
+pbng_status pbng_update_constraints(pbng_ctx *c, const double *pinned_xyz, const pbng_weak_constraint *wc, int64_t n_wc,
+                                    int64_t *n_recoloured) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    if (!c->colored) return fail(PBNG_E_NOT_COLORED, "update_constraints: call pbng_color first");
+    if (c->n_ranks > 1) return fail(PBNG_E_INVALID_ARGUMENT, "update_constraints: not supported on a decomposed context");
+    if (c->cur_accel >= 0) return fail(PBNG_E_BAD_ORDER, "update_constraints: a colour-by-colour iteration is open");
+    if (n_wc < 0 || (n_wc > 0 && !wc)) return fail(PBNG_E_INVALID_ARGUMENT, "update_constraints: bad sizes or pointers");
+    const int64_t np = (int64_t)c->pinned.size();
+    if (pinned_xyz)
+        for (int64_t k = 0; k < (int64_t)c->nb * np * 3; ++k)
+            if (!std::isfinite(pinned_xyz[k])) return fail(PBNG_E_INVALID_ARGUMENT, "update_constraints: non-finite target");
+    pbng_status st = validate_wc(c, wc, n_wc, "update_constraints");
+    if (st != PBNG_OK) return st;
+    const bool keep = c->bound && c->positions_set;
+    std::vector<unsigned char> saved;
+    int64_t changed = 0;
+    try {
+        // "newly added" = node set not present among the previous constraints (removed ones only relax)
+        std::vector<std::vector<int32_t>> old_nodes, nodes((size_t)n_wc);
+        for (const auto &w : c->wc) old_nodes.push_back(distinct_nodes(w));
+        std::sort(old_nodes.begin(), old_nodes.end());
+        std::vector<char> is_new((size_t)n_wc, 0);
+        for (int64_t q = 0; q < n_wc; ++q) {
+            nodes[q] = distinct_nodes(wc[q]);
+            is_new[q] = !std::binary_search(old_nodes.begin(), old_nodes.end(), nodes[q]);
+        }
+        std::vector<int32_t> col = recolour_incremental(c, nodes, is_new, &changed);
+        if (keep) {  // the current iterate, original order (restored after the re-layout)
+            saved.resize((size_t)c->nb * c->nv * 3 * c->real_size());
+            st = pbng_get_positions(c, saved.data());
+            if (st != PBNG_OK) return st;
+        }
+        c->wc.assign(wc, wc + n_wc);
+        if (pinned_xyz)
+            for (int64_t k = 0; k < np; ++k)
+                for (int64_t b = 0; b < c->nb; ++b)
+                    for (int a = 0; a < 3; ++a)
+                        c->targets[3 * (b * np + k) + a] = pinned_xyz[3 * (b * np + c->pin_order[k]) + a];
+        const bool was_bound = c->bound;
+        void *ws = c->ws;
+        const uint64_t ws_bytes = c->ws_bytes;
+        st = colour_and_layout(c, &col);
+        if (st != PBNG_OK) return st;
+        c->prob.inv_dt2 = 0.0;  // the backward-Euler target is not carried over (pbng_set_inertia again)
+        if (was_bound) {
+            if (c->ws_need > ws_bytes)
+                return fail(PBNG_E_OUT_OF_MEMORY, "update_constraints: the new layout needs " + std::to_string(c->ws_need) +
+                                                      " workspace bytes; bind a larger workspace and set positions");
+            st = pbng_bind_workspace(c, ws, ws_bytes);
+            if (st != PBNG_OK) return st;
+            if (keep) {
+                st = pbng_set_positions(c, saved.data());
+                if (st != PBNG_OK) return st;
+                DevGuard g(c->device);
+                PBNG_CUDA(cudaStreamSynchronize(c->stream), "update_constraints: synchronize");
+            }
+        }
+    } catch (const std::bad_alloc &) {
+        return fail(PBNG_E_OUT_OF_MEMORY, "update_constraints: host allocation");
+    }
+    if (n_recoloured) *n_recoloured = changed;
+    return PBNG_OK;
+}
+
+pbng_status pbng_get_colours(pbng_ctx *c, int32_t *colour_out, int32_t *n_colours_out) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    if (!c->colored) return fail(PBNG_E_NOT_COLORED, "get_colours: call pbng_color first");
+    if (colour_out) std::memcpy(colour_out, c->colour.data(), (size_t)c->nv * 4);
+    if (n_colours_out) *n_colours_out = c->ncol;
+    return PBNG_OK;
+}
+
+pbng_status pbng_detect_contacts(pbng_ctx *c, int32_t sample, double thickness, double k_n, double k_t,
+                                 pbng_weak_constraint *out, int64_t max_out, int64_t *n_out) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    if (!c->positions_set) return fail(PBNG_E_BAD_ORDER, "detect_contacts: set_positions first");
+    if (sample < 0 || sample >= c->nb || !(thickness > 0.0) || !std::isfinite(thickness) || !std::isfinite(k_n) ||
+        !std::isfinite(k_t) || k_n < 0.0 || k_t < 0.0 || max_out < 0 || (max_out > 0 && !out) || !n_out)
+        return fail(PBNG_E_INVALID_ARGUMENT, "detect_contacts: bad arguments");
+    if (c->n_ranks > 1) return fail(PBNG_E_INVALID_ARGUMENT, "detect_contacts: not supported on a decomposed context");
+    *n_out = 0;
+    if (c->h_sv.empty()) return PBNG_OK;
+    DevGuard g(c->device);
+    PBNG_CUDA(launch_contacts(c->prob, c->L, c->work, sample, thickness, c->stream), "detect_contacts: kernels");
+    c->launches += kernels_per_contacts();
+    std::vector<ContactHit> hit(c->h_sv.size());
+    PBNG_CUDA(cudaMemcpyAsync(hit.data(), c->L.c_res, hit.size() * sizeof(ContactHit), cudaMemcpyDeviceToHost, c->stream),
+              "detect_contacts: copy");
+    PBNG_CUDA(cudaStreamSynchronize(c->stream), "detect_contacts: synchronize");
+    // one constraint per contacting vertex, in ascending original vertex index
+    std::vector<std::pair<int32_t, size_t>> order;
+    for (size_t q = 0; q < hit.size(); ++q)
+        if (hit[q].tri >= 0) order.push_back({c->int2orig[c->h_sv[q].x], q});
+    std::sort(order.begin(), order.end());
+    int64_t n = 0;
+    for (const auto &o : order) {
+        if (n < max_out) {
+            const ContactHit &h = hit[o.second];
+            pbng_weak_constraint w;
+            std::memset(&w, 0, sizeof(w));
+            w.n0 = 1;
+            w.idx0[0] = o.first;
+            w.w0[0] = 1.0;
+            w.n1 = 3;
+            for (int a = 0; a < 3; ++a) {
+                w.idx1[a] = c->surf_orig[3 * (size_t)h.tri + a];
+                w.w1[a] = h.bary[a];
+            }
+            const double *nn = h.normal;  // K = k_n n n^T + k_t (I - n n^T)
+            w.K[0] = k_n * nn[0] * nn[0] + k_t * (1.0 - nn[0] * nn[0]);
+            w.K[1] = k_n * nn[1] * nn[1] + k_t * (1.0 - nn[1] * nn[1]);
+            w.K[2] = k_n * nn[2] * nn[2] + k_t * (1.0 - nn[2] * nn[2]);
+            w.K[3] = (k_n - k_t) * nn[0] * nn[1];
+            w.K[4] = (k_n - k_t) * nn[1] * nn[2];
+            w.K[5] = (k_n - k_t) * nn[0] * nn[2];
+            out[n] = w;
+        }
+        ++n;
+    }
+    *n_out = n;
+    if (n > max_out) return fail(PBNG_E_OUT_OF_MEMORY, "detect_contacts: " + std::to_string(n) + " contacts exceed max_out");
     return PBNG_OK;
 }
 

@@ -33,6 +33,13 @@ constexpr int kRedBlock = 256;    // threads per reduction CTA
 //   Neo-Hookean (needs F g_i, cof(F) g_i, det F only; pbng_kernels.cu Pair<R, MODEL_NH>):
 //     f32: rec_id int4 {n1, n2, n3, bits(VE)}; rec_a float4 {s1 s2 s3 detB}, s_j = g_j . g_i -> 32 bytes
 //     f64: rec_id int4 {n1, n2, n3, 0}; rec_a double4 {s1 s2 s3 detB}; rec_c double {VE}     -> 56 bytes
+// closest boundary triangle of another body found for one free boundary vertex (pbng_detect_contacts)
+struct ContactHit {
+    int32_t tri = -1, pad = 0;  // boundary-triangle index, -1 = none within the thickness
+    double bary[3] = {0, 0, 0};  // closest point = sum bary[a] x_{v_a}
+    double normal[3] = {0, 0, 0};  // unit normal of the triangle at the current positions
+};
+
 struct Layout {
     const int4 *rec_id = nullptr;
     const void *rec_a = nullptr, *rec_b = nullptr, *rec_c = nullptr;
@@ -68,6 +75,14 @@ struct Layout {
     // pipelined schedule (sweep_pipe_kernel): per chunk the chunks holding its stencil neighbours, CSR,
     // entry = (chunk << 1) | 1 for an earlier colour (must have finished iteration l), (chunk << 1) for a
     // later colour or the chunk itself (iteration l - 1); done counters [n_batch][n_chunks]; work counter
+    // contact detection: boundary triangles {v0, v1, v2, body}, free boundary vertices {vertex, body},
+    // hash grid (bucket heads, entries {triangle, next}), per-vertex results, scratch scalars
+    const int4 *surf = nullptr;
+    const int2 *sv = nullptr;
+    int32_t *c_head = nullptr;
+    int2 *c_next = nullptr;
+    struct ContactHit *c_res = nullptr;
+    uint32_t *c_scal = nullptr;
     const int32_t *dep_off = nullptr;    // [n_chunks + 1]
     const int32_t *deps = nullptr;
     int32_t *pipe_flags = nullptr;
@@ -88,6 +103,7 @@ struct Problem {
     int ge = 1, gr = 1;  // energy / residual partial blocks per sample
     int64_t n_own = 0;     // owned free vertices (swept)
     double inv_dt2 = 0;    // backward Euler 1/dt^2 (0: quasistatic)
+    int64_t n_surf = 0, n_sv = 0, n_cbuckets = 1;  // contact detection sizes
 };
 
 struct SweepLaunch {
@@ -125,6 +141,10 @@ cudaError_t launch_halo_pack(const Problem &p, const Layout &L, const int32_t *i
 cudaError_t launch_halo_unpack(const Problem &p, const Layout &L, const int32_t *idx, int64_t n, int n_fields,
                                const int (&bufs)[3], const void *buf, cudaStream_t st);
 int kernels_per_energy_residual();
+// contact detection at the positions of buffer `work`, sample `sample`: per free boundary vertex the closest
+// boundary triangle of another body within `thickness` (L.c_res); fp64 arithmetic
+cudaError_t launch_contacts(const Problem &p, const Layout &L, int work, int sample, double thickness, cudaStream_t st);
+int kernels_per_contacts();
 cudaError_t launch_polar_test(int dtype, const double *F, double *R, int64_t n, cudaStream_t st);
 
 }  // namespace pbng

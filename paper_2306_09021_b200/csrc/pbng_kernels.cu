@@ -1235,6 +1235,142 @@ __global__ void halo_unpack_kernel(const Layout L, const int32_t *__restrict__ i
 }
 
 // ------------------------------------------------------------------------------------------------
+// contact detection (pbng_detect_contacts): a uniform hash grid of the boundary
+// triangles (cell size = largest triangle extent + 2 thickness, so a triangle's thickness-inflated box
+// covers at most 2 cells per axis), then one thread per free boundary vertex walks its cell's bucket and
+// keeps the closest triangle of another body, lexicographically (|p - q|^2, triangle index) -- the
+// result does not depend on the bucket order.  fp64 arithmetic for both dtypes.
+// ------------------------------------------------------------------------------------------------
+template <class R>
+__device__ __forceinline__ double3 pos_d(const Layout &L, int work, int64_t b, int64_t v, int64_t xs, int sh) {
+    const typename RT<R>::R4 x = reinterpret_cast<const typename RT<R>::R4 *>(L.xbuf[work])[pos_index(b, v, xs, sh)];
+    return make_double3(double(x.x), double(x.y), double(x.z));
+}
+__device__ __forceinline__ double3 sub(double3 a, double3 b) { return make_double3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ double dot(double3 a, double3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ double3 cross(double3 a, double3 b) {
+    return make_double3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ int64_t cell_of(double x, double cs) { return (int64_t)floor(x / cs); }
+__device__ __forceinline__ int64_t bucket_of(int64_t i, int64_t j, int64_t k, int64_t nb) {
+    const uint64_t h = (uint64_t)i * 73856093ull ^ (uint64_t)j * 19349663ull ^ (uint64_t)k * 83492791ull;
+    return (int64_t)(h & (uint64_t)(nb - 1));
+}
+
+// closest point of triangle (a, b, c) to p as barycentric weights: the plane projection when it falls
+// inside the triangle, else the closest of the three edge-segment projections
+__device__ __forceinline__ void closest_on_triangle(double3 p, double3 a, double3 b, double3 c, double (&w)[3]) {
+    const double3 e0 = sub(b, a), e1 = sub(c, a), d = sub(p, a);
+    const double d00 = dot(e0, e0), d01 = dot(e0, e1), d11 = dot(e1, e1);
+    const double den = d00 * d11 - d01 * d01;
+    if (den > 0.0) {
+        const double d20 = dot(d, e0), d21 = dot(d, e1);
+        const double v = (d11 * d20 - d01 * d21) / den, t = (d00 * d21 - d01 * d20) / den;
+        if (v >= 0.0 && t >= 0.0 && v + t <= 1.0) {
+            w[0] = 1.0 - v - t; w[1] = v; w[2] = t;
+            return;
+        }
+    }
+    const double3 P[3] = {a, b, c};
+    double best = -1.0;
+    for (int k = 0; k < 3; ++k) {  // edge P[k] -> P[k+1]
+        const double3 s0 = P[k], s1 = P[(k + 1) % 3], e = sub(s1, s0);
+        const double ee = dot(e, e);
+        double t = ee > 0.0 ? dot(sub(p, s0), e) / ee : 0.0;
+        t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+        const double3 q = make_double3(s0.x + t * e.x, s0.y + t * e.y, s0.z + t * e.z);
+        const double dd = dot(sub(p, q), sub(p, q));
+        if (best < 0.0 || dd < best) {
+            best = dd;
+            w[0] = w[1] = w[2] = 0.0;
+            w[k] = 1.0 - t;
+            w[(k + 1) % 3] = t;
+        }
+    }
+}
+
+template <class R>
+__global__ void contact_extent_kernel(const Layout L, const int64_t n_surf, const int work, const int64_t b,
+                                      const int64_t xs, const int sh) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_surf) return;
+    const int4 tr = L.surf[t];
+    const double3 a = pos_d<R>(L, work, b, tr.x, xs, sh), p = pos_d<R>(L, work, b, tr.y, xs, sh),
+                  c = pos_d<R>(L, work, b, tr.z, xs, sh);
+    const double ex = fmax(fmax(a.x, p.x), c.x) - fmin(fmin(a.x, p.x), c.x);
+    const double ey = fmax(fmax(a.y, p.y), c.y) - fmin(fmin(a.y, p.y), c.y);
+    const double ez = fmax(fmax(a.z, p.z), c.z) - fmin(fmin(a.z, p.z), c.z);
+    atomicMax(L.c_scal, __float_as_uint(__double2float_ru(fmax(fmax(ex, ey), ez))));
+}
+
+template <class R>
+__global__ void contact_insert_kernel(const Layout L, const int64_t n_surf, const int work, const int64_t b,
+                                      const int64_t xs, const int sh, const double thick, const int64_t nb) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_surf) return;
+    const double cs = double(__uint_as_float(L.c_scal[0])) + 2.0 * thick;
+    const int4 tr = L.surf[t];
+    const double3 a = pos_d<R>(L, work, b, tr.x, xs, sh), p = pos_d<R>(L, work, b, tr.y, xs, sh),
+                  c = pos_d<R>(L, work, b, tr.z, xs, sh);
+    const int64_t i0 = cell_of(fmin(fmin(a.x, p.x), c.x) - thick, cs), i1 = cell_of(fmax(fmax(a.x, p.x), c.x) + thick, cs);
+    const int64_t j0 = cell_of(fmin(fmin(a.y, p.y), c.y) - thick, cs), j1 = cell_of(fmax(fmax(a.y, p.y), c.y) + thick, cs);
+    const int64_t k0 = cell_of(fmin(fmin(a.z, p.z), c.z) - thick, cs), k1 = cell_of(fmax(fmax(a.z, p.z), c.z) + thick, cs);
+    int e = 0;
+    for (int64_t i = i0; i <= i1 && i <= i0 + 1; ++i)
+        for (int64_t j = j0; j <= j1 && j <= j0 + 1; ++j)
+            for (int64_t k = k0; k <= k1 && k <= k0 + 1; ++k, ++e) {
+                const int32_t slot = (int32_t)(t * 8 + e);
+                const int32_t old = atomicExch(L.c_head + bucket_of(i, j, k, nb), slot);
+                L.c_next[slot] = make_int2((int32_t)t, old);
+            }
+}
+
+template <class R>
+__global__ void contact_query_kernel(const Layout L, const int64_t n_sv, const int work, const int64_t b,
+                                     const int64_t xs, const int sh, const double thick, const int64_t nb) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_sv) return;
+    const double cs = double(__uint_as_float(L.c_scal[0])) + 2.0 * thick;
+    const int2 sv = L.sv[q];
+    const double3 p = pos_d<R>(L, work, b, sv.x, xs, sh);
+    const double t2 = thick * thick;
+    double best = 0.0, bw[3] = {0.0, 0.0, 0.0};
+    int32_t bt = -1;
+    for (int32_t e = L.c_head[bucket_of(cell_of(p.x, cs), cell_of(p.y, cs), cell_of(p.z, cs), nb)]; e >= 0;) {
+        const int2 en = L.c_next[e];
+        e = en.y;
+        const int4 tr = L.surf[en.x];
+        if (tr.w == sv.y) continue;  // same body
+        const double3 a = pos_d<R>(L, work, b, tr.x, xs, sh), bb = pos_d<R>(L, work, b, tr.y, xs, sh),
+                      c = pos_d<R>(L, work, b, tr.z, xs, sh);
+        double w[3];
+        closest_on_triangle(p, a, bb, c, w);
+        const double3 d = make_double3(p.x - (w[0] * a.x + w[1] * bb.x + w[2] * c.x), p.y - (w[0] * a.y + w[1] * bb.y + w[2] * c.y),
+                                       p.z - (w[0] * a.z + w[1] * bb.z + w[2] * c.z));
+        const double d2 = dot(d, d);
+        if (d2 <= t2 && (bt < 0 || d2 < best || (d2 == best && en.x < bt))) {
+            best = d2;
+            bt = en.x;
+            bw[0] = w[0]; bw[1] = w[1]; bw[2] = w[2];
+        }
+    }
+    ContactHit h;
+    h.tri = bt;
+    if (bt >= 0) {
+        const int4 tr = L.surf[bt];
+        const double3 a = pos_d<R>(L, work, b, tr.x, xs, sh), bb = pos_d<R>(L, work, b, tr.y, xs, sh),
+                      c = pos_d<R>(L, work, b, tr.z, xs, sh);
+        const double3 n = cross(sub(bb, a), sub(c, a));
+        const double nn = sqrt(dot(n, n));
+        for (int k = 0; k < 3; ++k) h.bary[k] = bw[k];
+        h.normal[0] = nn > 0.0 ? n.x / nn : 0.0;
+        h.normal[1] = nn > 0.0 ? n.y / nn : 0.0;
+        h.normal[2] = nn > 0.0 ? n.z / nn : 0.0;
+    }
+    L.c_res[q] = h;
+}
+
+// ------------------------------------------------------------------------------------------------
 // energy and residual (fp64 arithmetic for both dtypes; fixed-order reductions)
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ double block_sum(double v, double *sh) {
@@ -1551,6 +1687,27 @@ cudaError_t launch_energy_residual(const Problem &p, const Layout &L, int work, 
 }
 
 int kernels_per_energy_residual() { return 3; }
+
+template <class R>
+cudaError_t contacts_dispatch(const Problem &p, const Layout &L, int work, int sample, double thick, cudaStream_t st) {
+    const unsigned g1 = (unsigned)((p.n_surf + 255) / 256), g2 = (unsigned)((p.n_sv + 255) / 256);
+    cudaError_t e = cudaMemsetAsync(L.c_scal, 0, 4, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(L.c_head, 0xff, (size_t)p.n_cbuckets * 4, st);
+    if (e != cudaSuccess) return e;
+    contact_extent_kernel<R><<<g1, 256, 0, st>>>(L, p.n_surf, work, sample, p.x_stride, p.lane_shift);
+    contact_insert_kernel<R><<<g1, 256, 0, st>>>(L, p.n_surf, work, sample, p.x_stride, p.lane_shift, thick, p.n_cbuckets);
+    contact_query_kernel<R><<<g2, 256, 0, st>>>(L, p.n_sv, work, sample, p.x_stride, p.lane_shift, thick, p.n_cbuckets);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_contacts(const Problem &p, const Layout &L, int work, int sample, double thickness, cudaStream_t st) {
+    if (p.n_surf <= 0 || p.n_sv <= 0) return cudaSuccess;
+    return p.dtype == DT_F64 ? contacts_dispatch<double>(p, L, work, sample, thickness, st)
+                             : contacts_dispatch<float>(p, L, work, sample, thickness, st);
+}
+
+int kernels_per_contacts() { return 3; }
 
 cudaError_t launch_polar_test(int dtype, const double *F, double *R, int64_t n, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;

@@ -28,7 +28,8 @@ EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbn
            "pbng_synchronize", "pbng_query", "pbng_profile_enable", "pbng_profile_read", "pbng_destroy",
            "pbng_last_error", "pbng_version", "pbng_sweep_colour", "pbng_end_iteration", "pbng_set_partition",
            "pbng_halo_counts", "pbng_halo_vertices", "pbng_halo_pack", "pbng_halo_unpack", "pbng_test_polar",
-           "pbng_set_inertia", "pbng_set_schedule")
+           "pbng_set_inertia", "pbng_set_schedule", "pbng_detect_contacts", "pbng_update_constraints",
+           "pbng_get_colours")
 
 WC_DTYPE = np.dtype([("n0", "<i4"), ("n1", "<i4"), ("idx0", "<i4", 4), ("idx1", "<i4", 4), ("w0", "<f8", 4),
                      ("w1", "<f8", 4), ("anchor", "<f8", 3), ("K", "<f8", 6)])
@@ -90,6 +91,9 @@ def lib():
     L.pbng_test_polar.argtypes = [C.c_int, vp, vp, i64, C.c_int]
     L.pbng_set_inertia.argtypes = [vp, d, vp]
     L.pbng_set_schedule.argtypes = [vp, C.c_int]
+    L.pbng_detect_contacts.argtypes = [vp, i32, d, d, d, vp, i64, C.POINTER(i64)]
+    L.pbng_update_constraints.argtypes = [vp, vp, vp, i64, C.POINTER(i64)]
+    L.pbng_get_colours.argtypes = [vp, vp, C.POINTER(i32)]
     L.pbng_last_error.restype = C.c_char_p
     L.pbng_version.restype = i32
     for name in EXPORTS:
@@ -243,6 +247,50 @@ class Context:
     def set_schedule(self, schedule: str = "auto"):
         """'colour_launches' (one launch per colour pass), 'pipelined' (persistent dataflow launch) or 'auto'."""
         _check(lib().pbng_set_schedule(self._h, SCHEDULE[schedule]))
+
+    # ---- dynamic weak constraints ----------------------------------------------------------------
+    def detect_contacts(self, thickness: float, k_n: float, k_t: float = 0.0, sample: int = 0) -> np.ndarray:
+        """Contact weak constraints at the current positions (pbng_detect_contacts) as a WC_DTYPE array."""
+        cap = max(64, self.n_vertices)
+        while True:
+            out = np.zeros(cap, WC_DTYPE)
+            n = C.c_int64()
+            st = lib().pbng_detect_contacts(self._h, int(sample), float(thickness), float(k_n), float(k_t), _ptr(out),
+                                            cap, C.byref(n))
+            if st == 10 and n.value > cap:
+                cap = n.value
+                continue
+            _check(st)
+            return out[:n.value].copy()
+
+    def update_constraints(self, wc, targets=None) -> int:
+        """Replace the weak constraints (dict or WC_DTYPE array) with incremental recolouring
+        (pbng_update_constraints); grows the workspace if the new layout needs it.  Returns the number of
+        recoloured nodes."""
+        w = wc if isinstance(wc, np.ndarray) and wc.dtype == WC_DTYPE else weak_constraints_array(wc)
+        w = np.ascontiguousarray(w)
+        t = None if targets is None else _np(targets, np.float64).reshape(-1)
+        saved = self.get_positions().clone() if (self.device >= 0 and self.workspace is not None) else None
+        n = C.c_int64()
+        st = lib().pbng_update_constraints(self._h, _ptr(t) if t is not None else None, _ptr(w) if w.size else None,
+                                           w.size, C.byref(n))
+        if st == 10 and saved is not None and self.workspace_bytes() > 0:
+            nbytes = self.workspace_bytes()
+            self.bind_workspace(self._torch.empty(int(nbytes * 1.25) + 256, dtype=self._torch.uint8,
+                                                  device=f"cuda:{self.device}"))
+            self.set_positions(saved)
+            self.colours, self.n_colours = self.get_colours()
+            return n.value
+        _check(st)
+        self.colours, self.n_colours = self.get_colours()
+        return n.value
+
+    def get_colours(self):
+        """The colouring in use (after incremental updates): (colour per vertex, number of colours)."""
+        out = np.empty(self.n_vertices, np.int32)
+        n = C.c_int32()
+        _check(lib().pbng_get_colours(self._h, _ptr(out), C.byref(n)))
+        return out, n.value
 
     def energy_residual(self):
         e = np.empty(self.n_batch)

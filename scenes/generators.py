@@ -353,6 +353,41 @@ def config5_muscle_stack(n_blocks: int = 8, n: int = 48, dtype: str = "f32", ite
                          "n_contacts": int(face.shape[0]), "blocks": n_blocks})
 
 
+def two_blocks_colliding(n: int = 4, gap: float = 0.1, speed: float = 2.5, dt: float = 0.002,
+                         dtype: str = "f64") -> Scene:
+    """The paper's dynamic-constraint example ('Two Blocks Colliding'): two unit blocks
+    of n^3 Kuhn cells along x with a gap, block-major numbering; the outer x faces are pinned and driven
+    toward each other at `speed` (targets_at(step)).  Backward Euler with dt = 0.002,
+    R0 = 10, E = 1000, contact stiffness k_n = 1e8, k_t = 0.  Not stated by the paper and
+    read here: Neo-Hookean, nu = 0.3, contact thickness 0.02 (reading Z21)."""
+    h = 1.0 / n
+    XA, TA = kuhn_grid(n, n, n, h)
+    nvb = XA.shape[0]
+    XB, TB = kuhn_grid(n, n, n, h, origin=(1.0 + gap, 0.0, 0.0), vertex_offset=nvb)
+    X = np.concatenate([XA, XB])
+    tets = np.concatenate([TA, TB])
+    left = np.nonzero(np.isclose(X[:, 0], 0.0))[0]
+    right = np.nonzero(np.isclose(X[:, 0], 2.0 + gap))[0]
+    pinned = np.concatenate([left, right]).astype(np.int32)
+    targets = X[pinned][None]
+    x0 = X[None].copy()
+    sc = _finish("two_blocks_colliding", X, tets, "nh", 1000.0, 0.3, 10.0, (0.0, 0.0, 0.0), pinned, targets, x0,
+                 wc=None, iterations=20, accel="none", omega=1.0, dtype=dtype, h=h,
+                 meta={"dt": dt, "speed": speed, "thickness": 0.02, "k_n": 1e8, "k_t": 0.0, "gap": gap})
+    return sc
+
+
+def targets_at(scene: Scene, step: int) -> np.ndarray:
+    """Dirichlet targets of two_blocks_colliding after `step` time steps: the left face moves by
+    +speed dt per step along x, the right face by -speed dt (prescribed motion, no method arithmetic)."""
+    t = scene.targets.copy()
+    left = scene.X[scene.pinned, 0] < 1.0
+    d = scene.meta["speed"] * scene.meta["dt"] * step
+    t[:, left, 0] += d
+    t[:, ~left, 0] -= d
+    return t
+
+
 def make_config(index: int, scale: str = "full", dtype: Optional[str] = None) -> Scene:
     """Config by BASELINE.json index (1-based).  scale="full" is BASELINE.json's size; "small" is a
     reduced copy that still spans several colours, several 32-vertex chunks and a ragged tail."""

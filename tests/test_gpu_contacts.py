@@ -1,0 +1,114 @@
+"""Dynamic weak constraints on the GPU: the library's device proximity detection
+against the oracle's brute force at the same positions, and the paper's 'two blocks colliding' backward-
+Euler example stepped with per-step detection + incremental recolouring
+ against the oracle doing the same with its own detection and recolouring."""
+import numpy as np
+import pytest
+
+from scenes import generators as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _free(s):
+    f = np.ones(s.n_vertices, bool)
+    f[s.pinned] = False
+    return f
+
+
+def _as_sets(vs, tris, w1):
+    return {(int(v), tuple(int(t) for t in tri)): tuple(w) for v, tri, w in zip(vs, tris, w1)}
+
+
+def compare(gpu_wc, orc_wc, tol=1e-9):
+    g = _as_sets(gpu_wc["idx0"][:, 0], gpu_wc["idx1"][:, :3], gpu_wc["w1"][:, :3])
+    o = _as_sets(orc_wc["idx0"][:, 0], orc_wc["idx1"][:, :3], orc_wc["w1"][:, :3])
+    assert set(g) == set(o)
+    for k in g:
+        np.testing.assert_allclose(g[k], o[k], atol=tol)
+    np.testing.assert_allclose(gpu_wc["K"], orc_wc["K"], rtol=1e-9, atol=1e-6)
+    assert np.all(gpu_wc["n0"] == 1) and np.all(gpu_wc["n1"] == 3)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_device_detection_equals_oracle(dtype):
+    import oracle.oracle as O
+    from paper_2306_09021_b200 import context_from_scene
+    s = G.two_blocks_colliding(n=4, gap=0.01)
+    rng = np.random.default_rng(5)
+    x = s.X + rng.uniform(-0.004, 0.004, s.X.shape)
+    x[s.pinned] = s.X[s.pinned]
+    ctx = context_from_scene(s, device=0, dtype=dtype)
+    ctx.set_positions(x[None])
+    xg = ctx.get_positions().cpu().numpy()[0].astype(np.float64)  # the device's copy (f32-rounded)
+    wc = ctx.detect_contacts(0.02, 1e8)
+    c = O.detect_contacts(s.X, xg, s.tets, _free(s), 0.02)
+    assert c["count"] > 20 and len(wc) == c["count"]
+    compare(wc, O.contact_constraints(c, 1e8))
+    # separated: nothing
+    ctx.set_positions(s.X[None] - np.where(np.arange(s.n_vertices) < 125, 0.05, -0.05)[None, :, None] * [1, 0, 0])
+    assert len(ctx.detect_contacts(0.02, 1e8)) == 0
+    ctx.close()
+
+
+def test_two_blocks_colliding_backward_euler_matches_oracle():
+    import torch
+
+    import oracle.oracle as O
+    from paper_2306_09021_b200 import context_from_scene
+    s = G.two_blocks_colliding(n=4, gap=0.1)
+    dt, th, kn, K = s.meta["dt"], s.meta["thickness"], s.meta["k_n"], 20
+    free = _free(s)
+    # --- GPU: detect -> update (incremental recolour) -> inertia -> iterate, every step
+    ctx = context_from_scene(s, device=0, dtype="f64")
+    xg_prev = torch.tensor(s.x0, dtype=torch.float64, device="cuda:0")
+    xg = xg_prev.clone()
+    gpu_hist, gpu_wcs = [], []
+    # --- oracle: the same with its own detection and recolouring
+    col = O.Oracle(s).colours()
+    nodes_prev = []
+    xo_prev = s.x0[0].copy()
+    xo = s.x0[0].copy()
+    n_contact_steps = 0
+    for step in range(1, 15):
+        tgt = G.targets_at(s, step)
+        wc = ctx.detect_contacts(th, kn)
+        ctx.update_constraints(wc, targets=tgt)
+        ctx.set_inertia(dt, 2 * xg - xg_prev)
+        ctx.iterate(K)
+        xg_prev, xg = xg, ctx.get_positions()
+        gpu_hist.append(xg.cpu().numpy()[0])
+        gpu_wcs.append(wc)
+
+        c = O.detect_contacts(s.X, xo, s.tets, free, th)
+        owc = O.contact_constraints(c, kn)
+        compare(wc, owc)
+        n_contact_steps += c["count"] > 0
+        nodes = O.constraint_nodes(owc) if c["count"] else []
+        prev = {tuple(sorted(set(n))) for n in nodes_prev}
+        is_new = [tuple(sorted(set(n))) not in prev for n in nodes]
+        col, _ = O.recolor_incremental(s.n_vertices, s.tets, nodes, is_new, col)
+        nodes_prev = nodes
+        sc = G.two_blocks_colliding(n=4, gap=0.1)
+        sc.wc = owc if c["count"] else None
+        sc.targets = tgt
+        o = O.Oracle(sc)
+        o.set_colours(col)
+        o.set_inertia(dt, 2 * xo - xo_prev)
+        x_in = xo.copy()
+        x_in[sc.pinned] = tgt[0]
+        x_new, _ = o.iterate(x_in, x_in, 0, K, "none")
+        xo_prev, xo = xo, x_new
+        gcol, _ = ctx.get_colours()
+        assert np.array_equal(gcol, col), f"step {step}: colourings differ"
+        err = np.abs(gpu_hist[-1] - xo).max() / s.bbox_diag()
+        assert err <= 1e-10, f"step {step}: position error {err:.3e}"
+    assert n_contact_steps >= 3  # the blocks met and stayed in contact for several steps
+    ctx.close()
