@@ -330,7 +330,6 @@ class Oracle:
             self._h = None
 
     # ---- precompute getters ------------------------------------------------------------------------
-    @property
     def set_colours(self, colours) -> None:
         """Use a given colouring (e.g. recolor_incremental's) for the sweeps."""
         c = np.ascontiguousarray(np.asarray(colours, dtype=np.int32))
@@ -338,6 +337,7 @@ class Oracle:
         if st:
             raise OracleError(st)
 
+    @property
     def n_colours(self) -> int:
         return int(lib().orc_num_colours(self._h))
 
