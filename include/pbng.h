@@ -215,8 +215,9 @@ pbng_status pbng_halo_unpack(pbng_ctx *ctx, int32_t colour, int32_t peer, int32_
  * k), face k = the three vertices other than local vertex k in ascending local order, the last two swapped
  * when the rest-state normal (v1 - v0) x (v2 - v0) points towards vertex k; bodies = connected components
  * of tets sharing a vertex.  For every free vertex on a boundary triangle, the boundary triangle of
- * ANOTHER body whose closest point q satisfies |x - q| <= thickness, minimising |x - q| (ties: lower
- * triangle index), gives one weak constraint: side 0 = the vertex (weight 1), side 1 = the triangle's
+ * ANOTHER body whose closest point q satisfies |x - q| <= thickness and |x - q|^2 is within
+ * 1e-10 thickness^2 of the least such value (closest points on shared edges / vertices tie), the lowest
+ * triangle index among those, gives one weak constraint: side 0 = the vertex (weight 1), side 1 = the triangle's
  * vertices with q's barycentric weights, K = k_n n n^T + k_t (I - n n^T), n the triangle's unit normal at
  * the current positions (the paper's collision constraints use k_t = 0).  The paper builds
  * such constraints every time step but gives no detection scheme (reading Z21).  Constraints

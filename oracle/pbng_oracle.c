@@ -1036,7 +1036,8 @@ void orc_bodies(int64_t nv, int64_t nt, const int32_t *tets, int32_t *body) {
 /* Contact weak constraints at positions y (the paper builds collision weak constraints
  * dynamically but specifies no detection scheme, PAPER.md:843-846 -- reading Z21): for every free vertex
  * of a boundary triangle, the closest boundary triangle of ANOTHER body (orc_bodies) whose closest point
- * is within `thickness` (|p - q|^2 <= thickness^2; ties -> lower triangle index).  The constraint has side
+ * is within `thickness` (|p - q|^2 <= thickness^2); among the triangles whose squared distance is within
+ * 1e-10 thickness^2 of the least one (shared edges / vertices), the lowest triangle index.  The constraint has side
  * 0 = the vertex (weight 1), side 1 = the triangle's vertices with the closest point's barycentric
  * weights, and K = k_n n n^T with n the triangle's unit normal at y (k_tau = 0).
  * Outputs per vertex (dense, nv entries): tri_out (3 ids, -1 if none), bary (3), normal (3).
@@ -1049,6 +1050,7 @@ int64_t orc_detect_contacts(int64_t nv, const double *X, const double *y, int64_
     int32_t *body = malloc((size_t)(nv + 1) * sizeof(int32_t));
     uint8_t *on_surf = calloc((size_t)nv + 1, 1);
     int64_t ntri, v, t, found = 0;
+    int pass;
     if (!tri || !tri_tet || !body || !on_surf) { free(tri); free(tri_tet); free(body); free(on_surf); return -1; }
     ntri = orc_surface(nt, tets, X, tri, tri_tet);
     orc_bodies(nv, nt, tets, body);
@@ -1060,21 +1062,28 @@ int64_t orc_detect_contacts(int64_t nv, const double *X, const double *y, int64_
         bary_out[3 * v] = bary_out[3 * v + 1] = bary_out[3 * v + 2] = 0.0;
         normal_out[3 * v] = normal_out[3 * v + 1] = normal_out[3 * v + 2] = 0.0;
         if (!on_surf[v] || !is_free[v]) continue;
-        for (t = 0; t < ntri; ++t) {
-            const int32_t *tv = tri + 3 * t;
-            double br[3], q[3], d2 = 0.0;
-            int k;
-            if (body[tv[0]] == body[v]) continue;
-            orc_closest_point_triangle(y + 3 * v, y + 3 * tv[0], y + 3 * tv[1], y + 3 * tv[2], br);
-            for (k = 0; k < 3; ++k) {
-                q[k] = br[0] * y[3 * tv[0] + k] + br[1] * y[3 * tv[1] + k] + br[2] * y[3 * tv[2] + k];
-                d2 += (y[3 * v + k] - q[k]) * (y[3 * v + k] - q[k]);
+        /* pass 1: the least squared distance; pass 2: the lowest-index triangle within 1e-10 thickness^2 of
+         * it (a closest point on an edge or vertex shared by several triangles is a tie, reading Z21) */
+        for (pass = 0; pass < 2; ++pass)
+            for (t = 0; t < ntri; ++t) {
+                const int32_t *tv = tri + 3 * t;
+                double br[3], q[3], d2 = 0.0;
+                int k;
+                if (body[tv[0]] == body[v]) continue;
+                orc_closest_point_triangle(y + 3 * v, y + 3 * tv[0], y + 3 * tv[1], y + 3 * tv[2], br);
+                for (k = 0; k < 3; ++k) {
+                    q[k] = br[0] * y[3 * tv[0] + k] + br[1] * y[3 * tv[1] + k] + br[2] * y[3 * tv[2] + k];
+                    d2 += (y[3 * v + k] - q[k]) * (y[3 * v + k] - q[k]);
+                }
+                if (d2 > thickness * thickness) continue;
+                if (pass == 0) {
+                    if (bt < 0 || d2 < best) { best = d2; bt = t; }
+                } else if (d2 <= best + 1e-10 * thickness * thickness) {
+                    bt = t;
+                    bb[0] = br[0]; bb[1] = br[1]; bb[2] = br[2];
+                    break;
+                }
             }
-            if (d2 <= thickness * thickness && (bt < 0 || d2 < best)) {
-                best = d2; bt = t;
-                bb[0] = br[0]; bb[1] = br[1]; bb[2] = br[2];
-            }
-        }
         if (bt >= 0) {
             const int32_t *tv = tri + 3 * bt;
             double u[3], w[3], nrm[3], s;

@@ -1334,26 +1334,35 @@ __global__ void contact_query_kernel(const Layout L, const int64_t n_sv, const i
     const int2 sv = L.sv[q];
     const double3 p = pos_d<R>(L, work, b, sv.x, xs, sh);
     const double t2 = thick * thick;
+    const int32_t head = L.c_head[bucket_of(cell_of(p.x, cs), cell_of(p.y, cs), cell_of(p.z, cs), nb)];
+    // pass 0: the least squared distance; pass 1: the lowest triangle index within 1e-10 thickness^2 of
+    // it (closest points on shared edges / vertices are ties; include/pbng.h)
     double best = 0.0, bw[3] = {0.0, 0.0, 0.0};
+    bool any = false;
     int32_t bt = -1;
-    for (int32_t e = L.c_head[bucket_of(cell_of(p.x, cs), cell_of(p.y, cs), cell_of(p.z, cs), nb)]; e >= 0;) {
-        const int2 en = L.c_next[e];
-        e = en.y;
-        const int4 tr = L.surf[en.x];
-        if (tr.w == sv.y) continue;  // same body
-        const double3 a = pos_d<R>(L, work, b, tr.x, xs, sh), bb = pos_d<R>(L, work, b, tr.y, xs, sh),
-                      c = pos_d<R>(L, work, b, tr.z, xs, sh);
-        double w[3];
-        closest_on_triangle(p, a, bb, c, w);
-        const double3 d = make_double3(p.x - (w[0] * a.x + w[1] * bb.x + w[2] * c.x), p.y - (w[0] * a.y + w[1] * bb.y + w[2] * c.y),
-                                       p.z - (w[0] * a.z + w[1] * bb.z + w[2] * c.z));
-        const double d2 = dot(d, d);
-        if (d2 <= t2 && (bt < 0 || d2 < best || (d2 == best && en.x < bt))) {
-            best = d2;
-            bt = en.x;
-            bw[0] = w[0]; bw[1] = w[1]; bw[2] = w[2];
+    for (int pass = 0; pass < 2 && (pass == 0 || any); ++pass)
+        for (int32_t e = head; e >= 0;) {
+            const int2 en = L.c_next[e];
+            e = en.y;
+            const int4 tr = L.surf[en.x];
+            if (tr.w == sv.y) continue;  // same body
+            const double3 a = pos_d<R>(L, work, b, tr.x, xs, sh), bb = pos_d<R>(L, work, b, tr.y, xs, sh),
+                          c = pos_d<R>(L, work, b, tr.z, xs, sh);
+            double w[3];
+            closest_on_triangle(p, a, bb, c, w);
+            const double3 d = make_double3(p.x - (w[0] * a.x + w[1] * bb.x + w[2] * c.x),
+                                           p.y - (w[0] * a.y + w[1] * bb.y + w[2] * c.y),
+                                           p.z - (w[0] * a.z + w[1] * bb.z + w[2] * c.z));
+            const double d2 = dot(d, d);
+            if (d2 > t2) continue;
+            if (pass == 0) {
+                if (!any || d2 < best) best = d2;
+                any = true;
+            } else if (d2 <= best + 1e-10 * t2 && (bt < 0 || en.x < bt)) {
+                bt = en.x;
+                bw[0] = w[0]; bw[1] = w[1]; bw[2] = w[2];
+            }
         }
-    }
     ContactHit h;
     h.tri = bt;
     if (bt >= 0) {

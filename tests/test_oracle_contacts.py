@@ -119,21 +119,25 @@ def test_detection_equals_brute_force_rule():
     body = O.bodies(s.n_vertices, s.tets)
     on = np.zeros(s.n_vertices, bool)
     on[tri.reshape(-1)] = True
+    ties = 0
     for v in range(s.n_vertices):
-        best = None
+        cand = []
         if on[v] and free[v]:
             for k, t in enumerate(tri):
                 if body[t[0]] == body[v]:
                     continue
                 w = O.closest_point_triangle(y[v], *y[t])
-                d = np.linalg.norm(y[v] - w @ y[t])
-                if d <= th and (best is None or d < best[0]):
-                    best = (d, k)
-        if best is None:
+                d2 = np.sum((y[v] - w @ y[t]) ** 2)
+                if d2 <= th * th:
+                    cand.append((d2, k))
+        if not cand:
             assert c["tri"][v, 0] == -1
-        else:
-            assert list(c["tri"][v]) == list(tri[best[1]])
-    assert c["count"] > 0
+        else:  # the lowest index among the (near-)least distances (shared edges / vertices tie)
+            dmin = min(d for d, _ in cand)
+            k = min(k for d, k in cand if d <= dmin + 1e-10 * th * th)
+            ties += sum(1 for d, _ in cand if d <= dmin + 1e-10 * th * th) > 1
+            assert list(c["tri"][v]) == list(tri[k])
+    assert c["count"] > 0 and ties > 0
 
 
 # ---- incremental recolouring ----------------------------------------------------------------------------
