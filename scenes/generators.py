@@ -353,13 +353,14 @@ def config5_muscle_stack(n_blocks: int = 8, n: int = 48, dtype: str = "f32", ite
                          "n_contacts": int(face.shape[0]), "blocks": n_blocks})
 
 
-def two_blocks_colliding(n: int = 4, gap: float = 0.1, speed: float = 2.5, dt: float = 0.002,
+def two_blocks_colliding(n: int = 4, gap: float = 0.05, speed: float = 5.0, dt: float = 0.002,
                          dtype: str = "f64") -> Scene:
     """The paper's dynamic-constraint example ('Two Blocks Colliding'): two unit blocks
     of n^3 Kuhn cells along x with a gap, block-major numbering; the outer x faces are pinned and driven
-    toward each other at `speed` (targets_at(step)).  Backward Euler with dt = 0.002,
-    R0 = 10, E = 1000, contact stiffness k_n = 1e8, k_t = 0.  Not stated by the paper and
-    read here: Neo-Hookean, nu = 0.3, contact thickness 0.02 (reading Z21)."""
+    toward each other at `speed` (targets_at(step)), and the blocks start moving at that speed
+    (meta["x_prev"] = x^{-1}).  Backward Euler with dt = 0.002, R0 = 10, E = 1000, contact
+    stiffness k_n = 1e8, k_t = 0.  Not stated by the paper and read here: Neo-Hookean,
+    nu = 0.3, contact thickness 0.02, the initial velocity (reading Z21)."""
     h = 1.0 / n
     XA, TA = kuhn_grid(n, n, n, h)
     nvb = XA.shape[0]
@@ -374,6 +375,10 @@ def two_blocks_colliding(n: int = 4, gap: float = 0.1, speed: float = 2.5, dt: f
     sc = _finish("two_blocks_colliding", X, tets, "nh", 1000.0, 0.3, 10.0, (0.0, 0.0, 0.0), pinned, targets, x0,
                  wc=None, iterations=20, accel="none", omega=1.0, dtype=dtype, h=h,
                  meta={"dt": dt, "speed": speed, "thickness": 0.02, "k_n": 1e8, "k_t": 0.0, "gap": gap})
+    x_prev = X.copy()
+    x_prev[:nvb, 0] -= speed * dt
+    x_prev[nvb:, 0] += speed * dt
+    sc.meta["x_prev"] = x_prev
     return sc
 
 
