@@ -27,13 +27,13 @@ def _as_sets(vs, tris, w1):
     return {(int(v), tuple(int(t) for t in tri)): tuple(w) for v, tri, w in zip(vs, tris, w1)}
 
 
-def compare(gpu_wc, orc_wc, tol=1e-9):
+def compare(gpu_wc, orc_wc, tol=1e-9, k_atol=1e-6):
     g = _as_sets(gpu_wc["idx0"][:, 0], gpu_wc["idx1"][:, :3], gpu_wc["w1"][:, :3])
     o = _as_sets(orc_wc["idx0"][:, 0], orc_wc["idx1"][:, :3], orc_wc["w1"][:, :3])
     assert set(g) == set(o)
     for k in g:
         np.testing.assert_allclose(g[k], o[k], atol=tol)
-    np.testing.assert_allclose(gpu_wc["K"], orc_wc["K"], rtol=1e-9, atol=1e-6)
+    np.testing.assert_allclose(gpu_wc["K"], orc_wc["K"], rtol=1e-9, atol=k_atol)
     assert np.all(gpu_wc["n0"] == 1) and np.all(gpu_wc["n1"] == 3)
 
 
@@ -89,7 +89,9 @@ def test_two_blocks_colliding_backward_euler_matches_oracle():
 
         c = O.detect_contacts(s.X, xo, s.tets, free, th)
         owc = O.contact_constraints(c, kn)
-        compare(wc, owc)
+        # separately integrated trajectories differ by rounding (~1e-14): K = k_n n n^T then differs by
+        # ~k_n 1e-14
+        compare(wc, owc, tol=1e-9, k_atol=1e-12 * kn)
         n_contact_steps += c["count"] > 0
         nodes = O.constraint_nodes(owc) if c["count"] else []
         prev = {tuple(sorted(set(n))) for n in nodes_prev}
