@@ -658,16 +658,21 @@ int problem_split(const pbng_ctx *c);
 
 // schedule pbng_iterate uses: 1 = one launch per colour pass, 2 = pipelined (PBNG_SCHEDULE env overrides
 // auto).  Auto pipelines small problems, whose colour passes are too short to fill the machine (launch
-// and barrier latency dominate; measured 1.3x on config 1); large ones keep the colour launches, whose
-// neighbour gathers may use the read-only L1 path (the pipelined kernel needs coherent loads, measured
-// 7% slower on config 3).
+// and barrier latency dominate; measured 1.3x on config 1, 1.03x on config 2); large ones keep the colour
+// launches, whose neighbour gathers may use the read-only L1 path (the pipelined kernel needs coherent
+// loads, measured 7% slower on config 3 and 15% on config 5).
 int effective_schedule(const pbng_ctx *c) {
     static const int env = [] {
         const char *e = getenv("PBNG_SCHEDULE");
         return e ? atoi(e) : 0;
     }();
     int want = c->schedule != 0 ? c->schedule : env;
-    if (want == 0) want = problem_split(c) == 4 ? 2 : 1;
+    if (want == 0) {  // fewer 32-vertex chunks per colour than 8 per SM: the colour passes cannot fill the GPU
+        int64_t gfree = 0;
+        for (int64_t k : c->gcol_nfree) gfree += k;
+        const int64_t chunks_per_colour = gfree * c->nb / kChunk / std::max(c->ncol, 1);
+        want = chunks_per_colour < 148 * 8 ? 2 : 1;
+    }
     return (want == 2 && pipeline_available(c)) ? 2 : 1;
 }
 

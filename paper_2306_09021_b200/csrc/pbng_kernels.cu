@@ -179,6 +179,67 @@ __device__ __forceinline__ void polar_rotation(const R (&F)[3][3], R (&Rm)[3][3]
         for (int j = 0; j < 3; ++j) Rm[i][j] = Qt[0][i] * V[j][0] + Qt[1][i] * V[j][1] + Qt[2][i] * V[j][2];
 }
 
+// Scaled Newton iteration for the polar factor (fp32 fast path of the fixed-corotated sweep):
+// X_{k+1} = (g X_k + X_k^{-T} / g) / 2 with g = |det X_k|^{-1/3} and X^{-T} = cof(X) / det X, from
+// X_0 = F (cofactor C and J = det F already computed by the caller).  For det F > 0 it converges to the
+// orthogonal polar factor, which then is the closest rotation (det +1) of reading Z4; 6 iterations reach
+// fp32 accuracy for condition numbers up to ~1e3.  The caller routes inverted and nearly
+// singular F (det F <= 1e-4 |F|^3) to the Jacobi routine.
+#ifndef PBNG_NEWTON_ITERS
+#define PBNG_NEWTON_ITERS 6
+#endif
+template <class R>
+__device__ __forceinline__ void polar_newton(const R (&F)[3][3], const R (&C0)[3][3], R J0, R (&X)[3][3]) {
+    R C[3][3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            X[a][b] = F[a][b];
+            C[a][b] = C0[a][b];
+        }
+    R d = J0;
+#pragma unroll
+    for (int it = 0; it < PBNG_NEWTON_ITERS; ++it) {
+        const R g = exp2f(-0.33333334f * __log2f(d));  // |det X|^{-1/3}, det X > 0 along the iteration
+        const R hx = R(0.5) * g, hc = R(0.5) / (g * d);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) X[a][b] = hx * X[a][b] + hc * C[a][b];
+        if (it + 1 < PBNG_NEWTON_ITERS) {
+            C[0][0] = X[1][1] * X[2][2] - X[1][2] * X[2][1];
+            C[0][1] = X[1][2] * X[2][0] - X[1][0] * X[2][2];
+            C[0][2] = X[1][0] * X[2][1] - X[1][1] * X[2][0];
+            C[1][0] = X[0][2] * X[2][1] - X[0][1] * X[2][2];
+            C[1][1] = X[0][0] * X[2][2] - X[0][2] * X[2][0];
+            C[1][2] = X[0][1] * X[2][0] - X[0][0] * X[2][1];
+            C[2][0] = X[0][1] * X[1][2] - X[0][2] * X[1][1];
+            C[2][1] = X[0][2] * X[1][0] - X[0][0] * X[1][2];
+            C[2][2] = X[0][0] * X[1][1] - X[0][1] * X[1][0];
+            d = X[0][0] * C[0][0] + X[0][1] * C[0][1] + X[0][2] * C[0][2];
+        }
+    }
+}
+
+// R(F) as the fixed-corotated sweep computes it: fp32 -> scaled Newton when det F > 1e-4 |F|_F^3, else the
+// Jacobi routine; fp64 -> Jacobi (7 sweeps).  C = cof F and J = det F are passed in.
+template <class R>
+__device__ __forceinline__ void polar_fcr(const R (&F)[3][3], const R (&C)[3][3], R J, R (&Rm)[3][3]) {
+    if (sizeof(R) == 4) {
+        R fro = R(0);
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) fro += F[a][b] * F[a][b];
+        if (J > R(1e-4) * fro * sqrt_fast(fro)) {
+            polar_newton(F, C, J, Rm);
+            return;
+        }
+    }
+    polar_rotation(F, Rm);
+}
+
 // ------------------------------------------------------------------------------------------------
 // Per (vertex, tet) contribution: F = sum_j (x_j - x_i) g_j^T, C = cof F,
 //   f -= V P(F) g_i,   A += V (2 mu |g_i|^2 I + lambda (C g_i)(C g_i)^T).
@@ -230,7 +291,7 @@ __device__ __forceinline__ void pair_contrib(const T (&d1)[3], const T (&d2)[3],
         for (int r = 0; r < 3; ++r) f[r] -= a * Fg[r] + b * w[r];
     } else {
         T Rm[3][3];
-        polar_rotation(F, Rm);
+        polar_fcr(F, C, J, Rm);
         const T s = Vlam * (J - T(1));
         const T m2 = T(2) * Vmu;
 #pragma unroll
@@ -1580,7 +1641,18 @@ __global__ void polar_test_kernel(const double *F, double *Rout, int64_t n) {
     R Fm[3][3], Rm[3][3];
     for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b) Fm[a][b] = R(F[9 * i + 3 * a + b]);
-    polar_rotation(Fm, Rm);
+    R C[3][3];
+    C[0][0] = Fm[1][1] * Fm[2][2] - Fm[1][2] * Fm[2][1];
+    C[0][1] = Fm[1][2] * Fm[2][0] - Fm[1][0] * Fm[2][2];
+    C[0][2] = Fm[1][0] * Fm[2][1] - Fm[1][1] * Fm[2][0];
+    C[1][0] = Fm[0][2] * Fm[2][1] - Fm[0][1] * Fm[2][2];
+    C[1][1] = Fm[0][0] * Fm[2][2] - Fm[0][2] * Fm[2][0];
+    C[1][2] = Fm[0][1] * Fm[2][0] - Fm[0][0] * Fm[2][1];
+    C[2][0] = Fm[0][1] * Fm[1][2] - Fm[0][2] * Fm[1][1];
+    C[2][1] = Fm[0][2] * Fm[1][0] - Fm[0][0] * Fm[1][2];
+    C[2][2] = Fm[0][0] * Fm[1][1] - Fm[0][1] * Fm[1][0];
+    const R J = Fm[0][0] * C[0][0] + Fm[0][1] * C[0][1] + Fm[0][2] * C[0][2];
+    polar_fcr(Fm, C, J, Rm);  // the routine the fixed-corotated sweep uses for this dtype
     for (int a = 0; a < 3; ++a)
         for (int b = 0; b < 3; ++b) Rout[9 * i + 3 * a + b] = double(Rm[a][b]);
 }

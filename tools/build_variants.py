@@ -1,6 +1,6 @@
 """Build tuning variants of libpbng.so into build_variants/ (git-ignored; they travel to the GPU box).
 
-    python tools/build_variants.py [--only float:MODEL_NH] NAME=DEF1,DEF2 [NAME=...]
+    python tools/build_variants.py [--only float:MODEL_NH,common] NAME=DEF1,DEF2 [NAME=...]
 e.g.  python tools/build_variants.py u2=PBNG_SWEEP_UNROLL=2 b256=PBNG_SWEEP_BLOCK=256
 Time one with:  PBNG_LIB=build_variants/libpbng_u2.so python tools/tune_sweep.py --config 3
 """
@@ -17,7 +17,7 @@ if __name__ == "__main__":
     args = sys.argv[1:]
     only = None
     if args and args[0] == "--only":
-        only = [tuple(u.split(":")) for u in args[1].split(",")]
+        only = [None if u == "common" else tuple(u.split(":")) for u in args[1].split(",")]
         args = args[2:]
     for arg in args:
         name, defs = arg.split("=", 1)
