@@ -1068,10 +1068,23 @@ __global__ void __launch_bounds__(SplitBlock<SPLIT>::n) sweep_split_kernel(const
     finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
 }
 
+// a pair record held by lane `src`, broadcast to the warp (32-bit words)
+template <class P> __device__ __forceinline__ P shfl_pair(const P &p, int src) {
+    static_assert(sizeof(P) % 4 == 0, "pair records are whole words");
+    P out;
+    const uint32_t *a = reinterpret_cast<const uint32_t *>(&p);
+    uint32_t *o = reinterpret_cast<uint32_t *>(&out);
+#pragma unroll
+    for (int k = 0; k < (int)(sizeof(P) / 4); ++k) o[k] = __shfl_sync(0xffffffffu, a[k], src);
+    return out;
+}
+
 // Batched samples (n_batch >= 32): positions are stored sample-minor,
 // x[(group * x_stride + v) * 32 + lane] with sample = 32 * group + lane.  A warp updates ONE vertex for
-// 32 samples: the pair record (shared rest mesh) is a warp-broadcast load and every neighbour gather is
-// one coalesced 512 B (f32) line.  Same arithmetic and per-vertex order as sweep_kernel.
+// 32 samples: lane k loads the vertex's record k once (shared rest mesh), each pair's record is then a
+// warp shuffle, so the neighbour gathers -- each one coalesced 512 B (f32) line -- of consecutive pairs
+// are independent of any load and overlap (unrolled x4).  Same arithmetic and per-vertex order as
+// sweep_kernel.
 template <class R, int MODEL, int ACCEL, bool FEXT, bool WC>
 __global__ void __launch_bounds__(kSweepBlock) sweep_batched_kernel(const Layout L, const int32_t v_begin,
                                                                     const int32_t n_v, const int64_t chunk_begin,
@@ -1083,8 +1096,8 @@ __global__ void __launch_bounds__(kSweepBlock) sweep_batched_kernel(const Layout
     constexpr int WPB = kSweepBlock / 32;
     const int lane = threadIdx.x & 31;
     const int t = blockIdx.x * WPB + (threadIdx.x >> 5);  // vertex index within the colour
-    const int b = blockIdx.y * 32 + lane;                  // sample
-    if (t >= n_v || b >= n_batch) return;
+    const int b = blockIdx.y * 32 + lane;                  // sample (lanes past n_batch compute, never store)
+    if (t >= n_v) return;                                  // warp-uniform
     const int v = v_begin + t;
     const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
     const int deg = ld(L.deg + v);
@@ -1098,15 +1111,21 @@ __global__ void __launch_bounds__(kSweepBlock) sweep_batched_kernel(const Layout
         f[0] = fe.x; f[1] = fe.y; f[2] = fe.z;
     }
     R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
-    for (int k = 0; k < deg; ++k) {
-        Pair<R, MODEL> pr;
-        load_pair<false>(L, base + (int64_t)k * kChunk, pr);
-        R d1[3], d2[3], d3[3];
-        sub3<R>(ld(work + ((int64_t)pr.id.x << 5)), xa, d1);
-        sub3<R>(ld(work + ((int64_t)pr.id.y << 5)), xa, d2);
-        sub3<R>(ld(work + ((int64_t)pr.id.z << 5)), xa, d3);
-        contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
+    for (int k0 = 0; k0 < deg; k0 += 32) {
+        Pair<R, MODEL> mine = {};
+        if (k0 + lane < deg) load_pair<false>(L, base + (int64_t)(k0 + lane) * kChunk, mine);
+        const int n = min(32, deg - k0);
+#pragma unroll 4
+        for (int j = 0; j < n; ++j) {
+            const Pair<R, MODEL> pr = shfl_pair(mine, j);
+            R d1[3], d2[3], d3[3];
+            sub3<R>(ld(work + ((int64_t)pr.id.x << 5)), xa, d1);
+            sub3<R>(ld(work + ((int64_t)pr.id.y << 5)), xa, d2);
+            sub3<R>(ld(work + ((int64_t)pr.id.z << 5)), xa, d3);
+            contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
+        }
     }
+    if (b >= n_batch) return;
     if (WC) wc_contrib<R, R, true>(L, work, 5, v, xa, f, A);
     if (idt2 > R(0))
         inertia_contrib<R, R>(L, v, ld(reinterpret_cast<const R4 *>(L.xtilde) + xs + ((int64_t)v << 5)), idt2, xa, f, A);
