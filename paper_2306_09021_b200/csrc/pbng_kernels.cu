@@ -780,6 +780,10 @@ __device__ __forceinline__ void update_vertex(const Layout &L, typename RT<R>::R
 // Measured on config 3: the ring's shared memory is carved out of the L1 that
 // serves the neighbour gathers, and every ring depth tried was slower (0.42-0.60 vs 0.39 ms/iteration).
 constexpr bool kSweepTma = PBNG_SWEEP_TMA;
+#ifndef PBNG_PDL
+#define PBNG_PDL 1
+#endif
+constexpr bool kPdl = PBNG_PDL;  // colour launches as programmatic dependent launches (register path)
 constexpr int kGroup = PBNG_TMA_GROUP;      // record steps per bulk copy
 constexpr int kGroups = PBNG_TMA_GROUPS;    // ring depth in groups
 template <class R, int MODEL> struct StageSmem {  // per warp: [ring][kGroups mbarriers, padded]
@@ -800,11 +804,19 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_kernel(con
                                                             const R clam, const R omega, const R gamma, const R idt2) {
     using R4 = typename RT<R>::R4;
     if (!kSweepTma) {
+        // programmatic dependent launch: let the next colour's CTAs start in this launch's tail; before
+        // waiting for the previous colour they touch only static data (offsets, degree) and prefetch their
+        // first records into L2 (the record stream does not depend on any position)
+        if (kPdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         const int t = blockIdx.x * kSweepBlock + threadIdx.x;
         if (t >= n_v) return;
         const int v = v_begin + t;
         const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
         const int deg = ld(L.deg + v);
+        if (kPdl) {
+            for (int k = 0; k < kSweepPrefetch && k < deg; ++k) prefetch_pair<R, MODEL>(L, base + (int64_t)k * kChunk);
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+        }
         const int64_t xs = (int64_t)blockIdx.y * x_stride;
         R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
         update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_NC>(L, work, xs, v, base, deg, oi, hi, cmu, clam, omega,
@@ -1152,10 +1164,18 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
             attr = true;
         }
         dim3 grid((unsigned)((s.n_v + kSweepBlock - 1) / kSweepBlock), (unsigned)p.n_batch);
-        sweep_kernel<R, MODEL, ACCEL, FE, W><<<grid, kSweepBlock, smem, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,
-                                                                               p.x_stride, s.work, s.out, s.hist, cmu,
-                                                                               clam, om, ga, idt2);
-        return cudaGetLastError();
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(kSweepBlock);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = (kPdl && !kSweepTma) ? 1 : 0;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W>, L, s.v_begin, s.n_v, s.chunk_begin,
+                                  p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga, idt2);
     }
 #define PBNG_SPLIT(S)                                                                                             \
     do {                                                                                                          \
