@@ -1048,6 +1048,11 @@ __global__ void __launch_bounds__(SplitBlock<SPLIT>::n) sweep_split_kernel(const
     R f[3] = {R(0), R(0), R(0)};
     R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
     R4 xa4 = mk4<R>(R(0), R(0), R(0));
+    if (kPdl) {  // as sweep_kernel: static data and a record prefetch before waiting for the previous colour
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        if (valid) prefetch_pair<R, MODEL>(L, ld(L.chunk_off + chunk_begin + (tc >> 5)) + lane + (int64_t)sub * kChunk);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     if (valid) {
         const int64_t base = ld(L.chunk_off + chunk_begin + (tc >> 5)) + lane;
         const int deg = ld(L.deg + v);
@@ -1144,6 +1149,23 @@ __global__ void __launch_bounds__(kSweepBlock) sweep_batched_kernel(const Layout
     finish_vertex<R, ACCEL>(L, work, xs, (int64_t)v << 5, oi, hi, xa4, f, A, omega, gamma);
 }
 
+template <class R, int MODEL, int ACCEL, bool FE, bool W, int S>
+cudaError_t split_launch(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
+    constexpr int B = SplitBlock<S>::n, VPB = B / S;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((s.n_v + VPB - 1) / VPB), (unsigned)p.n_batch);
+    cfg.blockDim = dim3(B);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = kPdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, sweep_split_kernel<R, MODEL, ACCEL, FE, W, S>, L, s.v_begin, s.n_v,
+                              s.chunk_begin, p.x_stride, s.work, s.out, s.hist, R(p.cmu), R(p.clam), R(s.omega),
+                              R(s.gamma), R(p.inv_dt2));
+}
+
 template <class R, int MODEL, int ACCEL, bool FE, bool W>
 cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
     const R cmu = R(p.cmu), clam = R(p.clam), om = R(s.omega), ga = R(s.gamma), idt2 = R(p.inv_dt2);
@@ -1177,19 +1199,9 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
         return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W>, L, s.v_begin, s.n_v, s.chunk_begin,
                                   p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga, idt2);
     }
-#define PBNG_SPLIT(S)                                                                                             \
-    do {                                                                                                          \
-        constexpr int B = SplitBlock<S>::n, VPB = B / S;                                                          \
-        dim3 grid((unsigned)((s.n_v + VPB - 1) / VPB), (unsigned)p.n_batch);                                     \
-        sweep_split_kernel<R, MODEL, ACCEL, FE, W, S><<<grid, B, 0, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,    \
-                                                                           p.x_stride, s.work, s.out, s.hist, cmu, \
-                                                                           clam, om, ga, idt2);                     \
-    } while (0)
-    if (s.split == 2) PBNG_SPLIT(2);
-    else if (s.split == 8) PBNG_SPLIT(8);
-    else PBNG_SPLIT(4);
-#undef PBNG_SPLIT
-    return cudaGetLastError();
+    if (s.split == 2) return split_launch<R, MODEL, ACCEL, FE, W, 2>(p, L, s, st);
+    if (s.split == 8) return split_launch<R, MODEL, ACCEL, FE, W, 8>(p, L, s, st);
+    return split_launch<R, MODEL, ACCEL, FE, W, 4>(p, L, s, st);
 }
 
 // persistent grid: every SM filled to the kernel's occupancy (queried once per instantiation)
