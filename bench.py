@@ -232,7 +232,8 @@ def run_ours(args):
         if decomposed:
             owner = dd.slab_partition(scene.X, world)
             part = (owner, rank, world)
-        ctx = context_from_scene(scene, device=local, stream=stream, set_positions=False, partition=part)
+        ctx = context_from_scene(scene, device=local, stream=stream, set_positions=False, partition=part,
+                                 dtype=args.dtype)
         x0_dev = torch.from_numpy(np.ascontiguousarray(scene.x0, dtype=ctx.np_dtype)).to(dev)
         x0_host = torch.from_numpy(np.ascontiguousarray(scene.x0, dtype=ctx.np_dtype)).pin_memory()
         x_out_host = torch.empty_like(x0_host).pin_memory()
@@ -336,7 +337,7 @@ def run_ours(args):
         launches_per_iter = sweep_launches / max(n_sweeps, 1)
         bytes_per_launch = bytes_per_iter / max(launches_per_iter, 1e-9)
         achieved = bytes_per_launch / (sweep_ms / max(sweep_launches, 1) / 1e3) / 1e9
-        traffic = ncu_traffic(args.config)
+        traffic = ncu_traffic(args.config if args.dtype is None else f"{args.config}_{args.dtype}")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
@@ -344,7 +345,9 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f32" if q["dtype"] == 0 else "f64", "data": "synthetic",
             "config": {
-                "workload": workload_name(scene, args.config),
+                "workload": (workload_name(scene, args.config) if args.dtype is None else
+                             workload_name(scene, args.config).replace("fp32", args.dtype.replace("f", "fp"))
+                             .replace("fp64 fp64", "fp64")),
                 "free_vertices_per_gpu": q["n_free"] * q["n_batch"], "iterations_per_step": iters,
                 "pairs_per_iteration": q["n_pairs"], "colours": q["n_colours"],
                 "step": "set_positions(x0, device) + iterate + energy_residual",
@@ -381,6 +384,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling runs)")
+    ap.add_argument("--dtype", default=None, choices=["f32", "f64"],
+                    help="override the config's compute dtype (e.g. config 3 in fp64: the FP64 measurement variant)")
     ap.add_argument("--dd", action="store_true", help="N > 1: domain-decompose one mesh (z slabs) instead of replicas")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

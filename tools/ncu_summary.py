@@ -26,6 +26,12 @@ METRICS = [
     "derived__smsp__sass_thread_inst_executed_op_ffma_pred_on_x2", "derived__smsp__sass_thread_inst_executed_op_dfma_pred_on_x2",
     "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
     "sm__cycles_elapsed.avg.per_second",
+    "smsp__sass_thread_inst_executed_op_fadd_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_fmul_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed",
 ]
 
 
@@ -80,7 +86,8 @@ def launch_shares(path):
 
 def main():
     tag, cfg = sys.argv[1], int(sys.argv[2])
-    d = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "gpurun_out")
+    d = sys.argv[3] if len(sys.argv) > 3 and sys.argv[3] != "-" else os.path.join(ROOT, "gpurun_out")
+    key = sys.argv[4] if len(sys.argv) > 4 else f"config{cfg}"  # sweep_traffic.json key (e.g. config3_f64)
     rep = os.path.join(d, f"{tag}_sweep.ncu-rep")
     kern = ncu_raw(rep)
     bench = json.load(open(os.path.join(d, f"{tag}_plain.json")))
@@ -96,6 +103,7 @@ def main():
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     tot_b = tot_t = 0.0
     flops = 0.0
+    fl = {"f": 0.0, "d": 0.0}
     for i, k in enumerate(kern):
         g = lambda m: k.get(m, ("", ""))
         t = to_us(*g("gpu__time_duration.sum"))
@@ -106,6 +114,15 @@ def main():
         for op in ("ffma", "dfma"):
             v = num(g(f"derived__smsp__sass_thread_inst_executed_op_{op}_pred_on_x2")[0] or "0")
             flops += v or 0
+        hz = num(g("sm__cycles_elapsed.avg.per_second")[0] or "0") or 0.0
+        unit = g("sm__cycles_elapsed.avg.per_second")[1]
+        hz *= {"cycle/second": 1.0, "cycle/usecond": 1e6, "cycle/nsecond": 1e9, "Mcycle/second": 1e6,
+               "Gcycle/second": 1e9, "Kcycle/second": 1e3, "hz": 1.0, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9}.get(unit, 1.0)
+        for p_ in ("f", "d"):  # FLOP = add + mul + 2 fma (thread-level SASS ops per elapsed cycle, whole GPU)
+            a = num(g(f"smsp__sass_thread_inst_executed_op_{p_}add_pred_on.sum.per_cycle_elapsed")[0] or "0") or 0.0
+            m = num(g(f"smsp__sass_thread_inst_executed_op_{p_}mul_pred_on.sum.per_cycle_elapsed")[0] or "0") or 0.0
+            f_ = num(g(f"smsp__sass_thread_inst_executed_op_{p_}fma_pred_on.sum.per_cycle_elapsed")[0] or "0") or 0.0
+            fl[p_] += (a + m + 2 * f_) * hz * t * 1e-6  # flops of this launch
         lines.append(f"| {i} | {g('launch__grid_size')[0]} | {g('launch__registers_per_thread')[0]} | {t:.1f} | {rb/1e6:.1f} | {wb/1e6:.1f} | "
                      f"{(rb+wb)/t/1e3:.0f} | {g('lts__t_sector_hit_rate.pct')[0]} | {g('l1tex__t_sector_hit_rate.pct')[0]} | "
                      f"{g('sm__warps_active.avg.pct_of_peak_sustained_active')[0]} | {g('smsp__issue_active.avg.pct_of_peak_sustained_active')[0]} | "
@@ -115,7 +132,9 @@ def main():
     alg = bench["roofline"]["algorithmic_bytes_per_launch"]
     lines += ["", f"Mean DRAM traffic per sweep launch (ncu): **{tot_b/n/1e6:.1f} MB**; algorithmic bytes per launch "
               f"(bench.py model, DESIGN.md): **{alg/1e6:.1f} MB** (ratio {tot_b/n/alg:.3f}).",
-              f"ncu DRAM bandwidth over the iteration: {tot_b/tot_t/1e3:.0f} GB/s (cold cache, serialised launches).", "",
+              f"ncu DRAM bandwidth over the iteration: {tot_b/tot_t/1e3:.0f} GB/s (cold cache, serialised launches).",
+              f"FLOP rate over the iteration (SASS add + mul + 2 fma): FP32 {fl['f']/tot_t/1e6:.2f} TFLOP/s, "
+              f"FP64 {fl['d']/tot_t/1e6:.2f} TFLOP/s (derived peaks: FP32 74.4, FP64 37.2 TFLOP/s at 1965 MHz).", "",
               "## Launch list (share of GPU time, all launches of the command)", "",
               "| kernel | launches | total us | share |", "|---|---|---|---|"]
     for name, c, t, sh in shares:
@@ -126,7 +145,7 @@ def main():
     open(os.path.join(ROOT, "profiles", f"{tag}_summary.md"), "w").write("\n".join(lines))
     tp = os.path.join(ROOT, "profiles", "sweep_traffic.json")
     tj = json.load(open(tp)) if os.path.exists(tp) else {}
-    tj[f"config{cfg}"] = {"dram_bytes_per_launch": tot_b / n, "algorithmic_bytes_per_launch": alg, "capture": f"profiles/{tag}_summary.md",
+    tj[key] = {"dram_bytes_per_launch": tot_b / n, "algorithmic_bytes_per_launch": alg, "capture": f"profiles/{tag}_summary.md",
                           "launches": n}
     json.dump(tj, open(tp, "w"), indent=1)
     print("\n".join(lines[:40]))

@@ -3,7 +3,7 @@
 # one whole iteration (8 colour launches, skipping the first iteration).
 # usage: bash tools/ncu_sweep.sh <tag> <config> [extra bench args]
 TAG=${1:-r1}; CFG=${2:-3}; shift 2
-CMD="python bench.py --config $CFG --steps 1 --warmup 3 --no-cpu-baseline --no-e2e $@"
+CMD="python bench.py --config $CFG --steps 1 --warmup 3 --no-cpu-baseline --no-e2e $*"
 mkdir -p gpurun_out
 $CMD > gpurun_out/${TAG}_plain.json 2> gpurun_out/${TAG}_plain.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 1300 --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu1.log 2>&1 && \
