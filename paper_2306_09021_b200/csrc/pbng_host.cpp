@@ -766,11 +766,11 @@ int problem_split(const pbng_ctx *c) {
         const char *e = getenv("PBNG_SPLIT");
         return e ? atoi(e) : 0;
     }();
-    if (forced == 1 || forced == 2 || forced == 4) return forced;
-    if (c->model == MODEL_FCR) return 4;
+    if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
     int64_t gfree = 0;  // free vertices of the whole mesh (all ranks)
     for (int64_t k : c->gcol_nfree) gfree += k;
     const int64_t chunks_per_colour = gfree * c->nb / kChunk / std::max(c->ncol, 1);
+    if (c->model == MODEL_FCR) return chunks_per_colour < 148 * 8 ? 8 : 4;  // config 2: 8 warps 1.17x faster
     if (chunks_per_colour < 148 * 16) return 4;
     if (chunks_per_colour < 148 * 32) return 2;
     return 1;

@@ -112,7 +112,7 @@ struct SweepLaunch {
     int work = 0, out = 1, hist = 2;  // xbuf indices
     int accel = ACCEL_NONE;
     double omega = 1, gamma = 1;  // SOR omega, or Chebyshev omega_{l+1} and gamma
-    int split = 1;  // warps sharing one 32-vertex chunk (1, 2 or 4)
+    int split = 1;  // warps sharing one 32-vertex chunk (1, 2, 4 or 8)
 };
 
 // one launch of the pipelined schedule: n_iter <= kPipeMaxIter whole iterations; iteration l (0-based
@@ -123,7 +123,7 @@ struct PipeLaunch {
     int n_iter = 0;
     int accel = ACCEL_NONE;
     int work = 0, out = 1, hist = 2;
-    int split = 1;  // warps per chunk item (1, 2 or 4), the same as the colour launches use
+    int split = 1;  // warps per chunk item (1, 2, 4 or 8), the same as the colour launches use
     double gamma = 1;
     double omega[kPipeMaxIter] = {};
 };

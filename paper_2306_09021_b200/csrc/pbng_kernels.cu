@@ -923,18 +923,21 @@ __device__ __forceinline__ void group_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// threads per CTA of the split and pipelined kernels: whole SPLIT-warp groups, at least kSweepBlock
+template <int SPLIT> struct SplitBlock { static constexpr int n = SPLIT * 32 > kSweepBlock ? SPLIT * 32 : kSweepBlock; };
+
 // SPLIT warps form a group that owns one item at a time (SPLIT = 1: update_vertex, the arithmetic of
 // sweep_kernel; SPLIT > 1: the partial sums and fixed-order combination of sweep_split_kernel), so the
 // per-vertex summation order -- and the result -- is that of the colour-launch schedule with the same
 // split (pbng_host.cpp problem_split).
 template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int SPLIT>
-__global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_pipe_kernel(const Layout L, const PipeLaunch P,
+__global__ void __launch_bounds__(SplitBlock<SPLIT>::n, PBNG_SWEEP_MINB) sweep_pipe_kernel(const Layout L, const PipeLaunch P,
                                                                  const int64_t x_stride, const int32_t n_batch,
                                                                  const int64_t n_chunks, const R cmu, const R clam,
                                                                  const R idt2) {
     using R4 = typename RT<R>::R4;
-    constexpr int GROUPS = kSweepBlock / (32 * SPLIT);
-    static_assert(GROUPS >= 1 && GROUPS * SPLIT * 32 == kSweepBlock, "block must hold whole groups");
+    constexpr int GROUPS = SplitBlock<SPLIT>::n / (32 * SPLIT);
+    static_assert(GROUPS >= 1 && GROUPS * SPLIT * 32 == SplitBlock<SPLIT>::n, "block must hold whole groups");
     __shared__ R red[GROUPS][SPLIT > 1 ? SPLIT - 1 : 1][9][32];
     __shared__ int64_t item_sh[GROUPS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1027,7 +1030,6 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_pipe_kerne
 // colours: SPLIT warps share one 32-vertex chunk, warp s takes records k = s, s + SPLIT, ...; the nine
 // partial sums (f: 3, A: 6) are combined through shared memory in fixed warp order (deterministic),
 // and warp 0 solves and stores.  Block = SPLIT * 32 * CPB threads, CPB chunks per block.
-template <int SPLIT> struct SplitBlock { static constexpr int n = SPLIT * 32 > kSweepBlock ? SPLIT * 32 : kSweepBlock; };
 template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int SPLIT>
 __global__ void __launch_bounds__(SplitBlock<SPLIT>::n) sweep_split_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
                                                                   const int64_t chunk_begin, const int64_t x_stride,
@@ -1213,14 +1215,14 @@ cudaError_t pipe_launch(const Problem &p, const Layout &L, const PipeLaunch &s, 
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_pipe_kernel<R, MODEL, ACCEL, FE, W, SPLIT>,
-                                                      kSweepBlock, 0);
+                                                      SplitBlock<SPLIT>::n, 0);
         blocks = std::max(1, sms * std::max(1, per_sm));
     }
-    constexpr int GROUPS = kSweepBlock / (32 * SPLIT);
+    constexpr int GROUPS = SplitBlock<SPLIT>::n / (32 * SPLIT);
     const int64_t items = p.n_chunks * p.n_batch * s.n_iter;
     const int64_t g = std::min<int64_t>(blocks, (items + GROUPS - 1) / GROUPS);
     if (g <= 0) return cudaSuccess;
-    sweep_pipe_kernel<R, MODEL, ACCEL, FE, W, SPLIT><<<(unsigned)g, kSweepBlock, 0, st>>>(
+    sweep_pipe_kernel<R, MODEL, ACCEL, FE, W, SPLIT><<<(unsigned)g, SplitBlock<SPLIT>::n, 0, st>>>(
         L, s, p.x_stride, p.n_batch, p.n_chunks, R(p.cmu), R(p.clam), R(p.inv_dt2));
     return cudaGetLastError();
 }
@@ -1229,6 +1231,7 @@ template <class R, int MODEL, int ACCEL, bool FE, bool W>
 cudaError_t pipe_dispatch4(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st) {
     if (s.split == 2) return pipe_launch<R, MODEL, ACCEL, FE, W, 2>(p, L, s, st);
     if (s.split == 4) return pipe_launch<R, MODEL, ACCEL, FE, W, 4>(p, L, s, st);
+    if (s.split == 8) return pipe_launch<R, MODEL, ACCEL, FE, W, 8>(p, L, s, st);
     return pipe_launch<R, MODEL, ACCEL, FE, W, 1>(p, L, s, st);
 }
 
