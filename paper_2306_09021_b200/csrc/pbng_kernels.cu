@@ -201,8 +201,11 @@ __device__ __forceinline__ void polar_newton(const R (&F)[3][3], const R (&C0)[3
     R d = J0;
 #pragma unroll
     for (int it = 0; it < PBNG_NEWTON_ITERS; ++it) {
-        const R g = exp2f(-0.33333334f * __log2f(d));  // |det X|^{-1/3}, det X > 0 along the iteration
-        const R hx = R(0.5) * g, hc = R(0.5) / (g * d);
+        // g = |det X|^{-1/3} (det X > 0 along the iteration); MUFU approximations suffice for a scaling
+        float lg, g;
+        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(float(d)));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(-0.33333334f * lg));
+        const R hx = R(0.5) * R(g), hc = div_fast(R(0.5), R(g) * d);
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
