@@ -288,8 +288,8 @@ __device__ __forceinline__ void pair_contrib(const T (&d1)[3], const T (&d2)[3],
 #pragma unroll
         for (int r = 0; r < 3; ++r) ic += F[r][0] * F[r][0] + F[r][1] * F[r][1] + F[r][2] * F[r][2];
         const T Vms = T(4) / T(3) * Vmu, Vls = Vlam + T(5) / T(6) * Vmu;
-        const T alpha = T(1) + T(3) * Vms / (T(4) * Vls);
-        const T a = Vms * (T(1) - T(1) / (T(1) + ic)), b = Vls * (J - alpha);
+        const T alpha = T(1) + div_fast(T(3) * Vms, T(4) * Vls);
+        const T a = Vms * (T(1) - div_fast(T(1), T(1) + ic)), b = Vls * (J - alpha);
 #pragma unroll
         for (int r = 0; r < 3; ++r) f[r] -= a * Fg[r] + b * w[r];
     } else {
@@ -957,10 +957,20 @@ __global__ void __launch_bounds__(SplitBlock<SPLIT>::n, PBNG_SWEEP_MINB) sweep_p
         gsync();
         const int64_t q = item_sh[grp];
         if (q >= n_items) return;
-        const int l = (int)(q / per_iter);
-        const int64_t rem = q - (int64_t)l * per_iter;
-        const int64_t X = rem / n_batch;
-        const int b = (int)(rem - X * n_batch);
+        int l, b;
+        int64_t X;
+        if (n_items < (int64_t(1) << 31)) {  // 32-bit division (64-bit integer division is a slow subroutine)
+            const uint32_t qq = (uint32_t)q, pi = (uint32_t)per_iter, nb = (uint32_t)n_batch;
+            l = (int)(qq / pi);
+            const uint32_t rem = qq - (uint32_t)l * pi;
+            X = rem / nb;
+            b = (int)(rem - (uint32_t)X * nb);
+        } else {
+            l = (int)(q / per_iter);
+            const int64_t rem = q - (int64_t)l * per_iter;
+            X = rem / n_batch;
+            b = (int)(rem - X * n_batch);
+        }
         int32_t *flags = L.pipe_flags + (int64_t)b * n_chunks;
         if (sub == 0) {  // wait for the neighbour chunks (one dependency per lane)
             const int d0 = ld(L.dep_off + X), d1 = ld(L.dep_off + X + 1);
