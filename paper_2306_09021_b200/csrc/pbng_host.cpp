@@ -151,6 +151,7 @@ struct pbng_ctx {
     std::vector<int32_t> surf_orig;
     std::vector<int64_t> pin_order;  // caller order of the pinned set -> ascending order (set_constraints)
     uint64_t ws_bytes = 0;           // bytes of the bound workspace
+    bool l2_persist = false;         // pbng_set_l2_persistence (re-applied by every bind)
     int schedule = 0;                        // pbng_schedule requested (0 auto, 1 colour launches, 2 pipelined)
     std::vector<int4> h_tet_id;
     Problem prob;
@@ -1325,6 +1326,7 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     c->L = L;
     c->bound = true;
     c->positions_set = false;
+    if (c->l2_persist) return apply_l2_persistence(c, 1);  // the position buffers may have moved
     return PBNG_OK;
 }
 
@@ -1622,6 +1624,43 @@ pbng_status pbng_set_schedule(pbng_ctx *c, pbng_schedule schedule) {
     }
     if (c->cur_accel >= 0) return fail(PBNG_E_BAD_ORDER, "set_schedule: a colour-by-colour iteration is open");
     c->schedule = (int)schedule;
+    return PBNG_OK;
+}
+
+pbng_status apply_l2_persistence(pbng_ctx *c, int enable);
+
+pbng_status pbng_set_l2_persistence(pbng_ctx *c, int enable) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    if (!c->bound) return fail(PBNG_E_BAD_ORDER, "set_l2_persistence: bind a workspace first");
+    st = apply_l2_persistence(c, enable);
+    if (st == PBNG_OK) c->l2_persist = enable != 0;
+    return st;
+}
+
+pbng_status apply_l2_persistence(pbng_ctx *c, int enable) {
+    DevGuard g(c->device);
+    cudaStreamAttrValue v;
+    std::memset(&v, 0, sizeof(v));
+    if (enable) {
+        // the two buffers the colour passes gather from (work, and out = the next iteration's work) are
+        // contiguous regions of the workspace; the record stream passing through L2 is left to stream
+        int max_window = 0, max_persist = 0;
+        PBNG_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device), "l2: attribute");
+        PBNG_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device), "l2: attribute");
+        const char *base = static_cast<const char *>(c->ws) + c->r_x[0].off;
+        const size_t bytes = std::min<size_t>((c->r_x[1].off + c->r_x[1].bytes) - c->r_x[0].off, (size_t)max_window);
+        PBNG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(bytes, (size_t)max_persist)),
+                  "l2: persisting limit");
+        v.accessPolicyWindow.base_ptr = const_cast<char *>(base);
+        v.accessPolicyWindow.num_bytes = bytes;
+        v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)std::max<size_t>(bytes, 1));
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    } else {
+        v.accessPolicyWindow.num_bytes = 0;
+    }
+    PBNG_CUDA(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v), "l2: stream attribute");
     return PBNG_OK;
 }
 

@@ -29,7 +29,7 @@ EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbn
            "pbng_last_error", "pbng_version", "pbng_sweep_colour", "pbng_end_iteration", "pbng_set_partition",
            "pbng_halo_counts", "pbng_halo_vertices", "pbng_halo_pack", "pbng_halo_unpack", "pbng_test_polar",
            "pbng_set_inertia", "pbng_set_schedule", "pbng_detect_contacts", "pbng_update_constraints",
-           "pbng_get_colours")
+           "pbng_get_colours", "pbng_set_l2_persistence")
 
 WC_DTYPE = np.dtype([("n0", "<i4"), ("n1", "<i4"), ("idx0", "<i4", 4), ("idx1", "<i4", 4), ("w0", "<f8", 4),
                      ("w1", "<f8", 4), ("anchor", "<f8", 3), ("K", "<f8", 6)])
@@ -94,6 +94,7 @@ def lib():
     L.pbng_detect_contacts.argtypes = [vp, i32, d, d, d, vp, i64, C.POINTER(i64)]
     L.pbng_update_constraints.argtypes = [vp, vp, vp, i64, C.POINTER(i64)]
     L.pbng_get_colours.argtypes = [vp, vp, C.POINTER(i32)]
+    L.pbng_set_l2_persistence.argtypes = [vp, C.c_int]
     L.pbng_last_error.restype = C.c_char_p
     L.pbng_version.restype = i32
     for name in EXPORTS:
@@ -244,6 +245,10 @@ class Context:
     def iterate(self, n: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0, gamma: float = 1.0):
         _check(lib().pbng_iterate(self._h, int(n), ACCEL[accel], float(omega), float(rho), float(gamma)))
 
+    def set_l2_persistence(self, enable: bool = True):
+        """Keep the gathered position buffers resident in L2 (pbng_set_l2_persistence)."""
+        _check(lib().pbng_set_l2_persistence(self._h, int(bool(enable))))
+
     def set_schedule(self, schedule: str = "auto"):
         """'colour_launches' (one launch per colour pass), 'pipelined' (persistent dataflow launch) or 'auto'."""
         _check(lib().pbng_set_schedule(self._h, SCHEDULE[schedule]))
@@ -368,9 +373,10 @@ def test_polar(F, dtype: str = "f32", device: int = 0) -> np.ndarray:
 
 
 def context_from_scene(scene, device=0, dtype: Optional[str] = None, stream=None, bind: bool = True,
-                       set_positions: bool = True, partition=None) -> Context:
+                       set_positions: bool = True, partition=None, l2_persist: bool = True) -> Context:
     """Build, colour, bind and initialise a Context for a scenes.Scene (all samples of its batch).
-    partition = (owner, rank, n_ranks) builds the rank-local context of a domain decomposition."""
+    partition = (owner, rank, n_ranks) builds the rank-local context of a domain decomposition;
+    l2_persist keeps the gathered position buffers L2-resident (pbng_set_l2_persistence)."""
     ctx = Context(scene.X, scene.tets, n_batch=scene.n_batch, dtype=dtype or scene.dtype, device=device, stream=stream)
     ctx.set_material(scene.model, scene.E, scene.nu, scene.density, scene.gravity)
     ctx.set_constraints(scene.pinned, scene.targets, scene.wc)
@@ -379,6 +385,8 @@ def context_from_scene(scene, device=0, dtype: Optional[str] = None, stream=None
     ctx.colours, ctx.n_colours = ctx.color()
     if bind and ctx.device >= 0:
         ctx.bind_workspace()
+        if l2_persist:
+            ctx.set_l2_persistence(True)
         if set_positions:
             ctx.set_positions(np.asarray(scene.x0))
     return ctx

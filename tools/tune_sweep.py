@@ -27,6 +27,8 @@ def main():
     args = ap.parse_args()
     s = G.make_config(args.config, "full")
     ctx = context_from_scene(s, device=0, dtype=args.dtype)
+    if os.environ.get("PBNG_L2PERSIST", "1") == "0":
+        ctx.set_l2_persistence(False)
     q = ctx.query()
     acc = (s.accel, s.omega, s.rho, s.gamma)
     ctx.iterate(3, *acc)
