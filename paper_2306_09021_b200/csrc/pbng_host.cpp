@@ -861,6 +861,33 @@ void end_iteration_impl(pbng_ctx *c, pbng_accel accel) {
     c->cur_accel = -1;
 }
 
+// L2 access-policy window over the gathered position buffers (pbng_set_l2_persistence)
+pbng_status apply_l2_persistence(pbng_ctx *c, int enable) {
+    DevGuard g(c->device);
+    cudaStreamAttrValue v;
+    std::memset(&v, 0, sizeof(v));
+    if (enable) {
+        // the two buffers the colour passes gather from (work, and out = the next iteration's work) are
+        // contiguous regions of the workspace; the record stream passing through L2 is left to stream
+        int max_window = 0, max_persist = 0;
+        PBNG_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device), "l2: attribute");
+        PBNG_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device), "l2: attribute");
+        const char *base = static_cast<const char *>(c->ws) + c->r_x[0].off;
+        const size_t bytes = std::min<size_t>((c->r_x[1].off + c->r_x[1].bytes) - c->r_x[0].off, (size_t)max_window);
+        PBNG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(bytes, (size_t)max_persist)),
+                  "l2: persisting limit");
+        v.accessPolicyWindow.base_ptr = const_cast<char *>(base);
+        v.accessPolicyWindow.num_bytes = bytes;
+        v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)std::max<size_t>(bytes, 1));
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    } else {
+        v.accessPolicyWindow.num_bytes = 0;
+    }
+    PBNG_CUDA(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v), "l2: stream attribute");
+    return PBNG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1627,8 +1654,6 @@ pbng_status pbng_set_schedule(pbng_ctx *c, pbng_schedule schedule) {
     return PBNG_OK;
 }
 
-pbng_status apply_l2_persistence(pbng_ctx *c, int enable);
-
 pbng_status pbng_set_l2_persistence(pbng_ctx *c, int enable) {
     pbng_status st = require_device(c);
     if (st != PBNG_OK) return st;
@@ -1636,32 +1661,6 @@ pbng_status pbng_set_l2_persistence(pbng_ctx *c, int enable) {
     st = apply_l2_persistence(c, enable);
     if (st == PBNG_OK) c->l2_persist = enable != 0;
     return st;
-}
-
-pbng_status apply_l2_persistence(pbng_ctx *c, int enable) {
-    DevGuard g(c->device);
-    cudaStreamAttrValue v;
-    std::memset(&v, 0, sizeof(v));
-    if (enable) {
-        // the two buffers the colour passes gather from (work, and out = the next iteration's work) are
-        // contiguous regions of the workspace; the record stream passing through L2 is left to stream
-        int max_window = 0, max_persist = 0;
-        PBNG_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device), "l2: attribute");
-        PBNG_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device), "l2: attribute");
-        const char *base = static_cast<const char *>(c->ws) + c->r_x[0].off;
-        const size_t bytes = std::min<size_t>((c->r_x[1].off + c->r_x[1].bytes) - c->r_x[0].off, (size_t)max_window);
-        PBNG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(bytes, (size_t)max_persist)),
-                  "l2: persisting limit");
-        v.accessPolicyWindow.base_ptr = const_cast<char *>(base);
-        v.accessPolicyWindow.num_bytes = bytes;
-        v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)std::max<size_t>(bytes, 1));
-        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    } else {
-        v.accessPolicyWindow.num_bytes = 0;
-    }
-    PBNG_CUDA(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v), "l2: stream attribute");
-    return PBNG_OK;
 }
 
 pbng_status pbng_profile_enable(pbng_ctx *c, int enable) {
