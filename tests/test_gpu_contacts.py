@@ -114,3 +114,24 @@ def test_two_blocks_colliding_backward_euler_matches_oracle():
         assert err <= 1e-10, f"step {step}: position error {err:.3e}"
     assert n_contact_steps >= 4  # the blocks met (step 3) and stayed in contact
     ctx.close()
+
+
+def test_detection_on_a_batched_context_uses_the_requested_sample():
+    import oracle.oracle as O
+    from paper_2306_09021_b200 import context_from_scene
+    base = G.two_blocks_colliding(n=3, gap=0.01)
+    nb = 40  # sample-minor layout (n_batch >= 32)
+    rng = np.random.default_rng(9)
+    xs = base.X[None] + rng.uniform(-0.004, 0.004, (nb,) + base.X.shape)
+    xs[:, base.pinned] = base.X[base.pinned]
+    s = G.two_blocks_colliding(n=3, gap=0.01)
+    s.x0 = xs
+    s.targets = np.repeat(base.targets, nb, axis=0)
+    ctx = context_from_scene(s, device=0, dtype="f64")
+    assert ctx.n_batch == nb
+    for b in (0, 33, 39):
+        wc = ctx.detect_contacts(0.02, 1e8, sample=b)
+        c = O.detect_contacts(s.X, xs[b], s.tets, _free(s), 0.02)
+        assert len(wc) == c["count"] > 0
+        compare(wc, O.contact_constraints(c, 1e8))
+    ctx.close()

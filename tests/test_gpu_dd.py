@@ -66,3 +66,13 @@ def test_full_config5_two_rank_loopback_one_iteration():
     xd, Ed, _, infos = decomposed(s, "f32", 2)
     assert np.array_equal(x1, xd)
     assert all(i["n_ghosts"] > 0 for i in infos)
+
+
+def test_batched_sample_minor_decomposition_is_bitwise():
+    """n_batch >= 32 (sample-minor position layout): halo pack/unpack address samples by group and lane."""
+    s = G.config4_batched(n_samples=40, n=4, iterations=12)
+    x1, E1, R1 = single(s, "f32")
+    xd, Ed, Rd, infos = decomposed(s, "f32", 2)
+    assert infos[0]["n_batch"] == 40 and sum(i["n_ghosts"] for i in infos) > 0
+    assert np.array_equal(x1, xd), np.abs(x1 - xd).max()
+    np.testing.assert_allclose(Ed, E1, rtol=1e-12, atol=0)
