@@ -182,6 +182,16 @@ pbng_status pbng_energy_residual(pbng_ctx *ctx, double *energy_out, double *resi
  * mixing returns PBNG_E_BAD_ORDER, as does pbng_iterate while a colour-by-colour iteration is open. */
 pbng_status pbng_sweep_colour(pbng_ctx *ctx, int32_t colour, pbng_accel accel, double omega, double rho, double gamma);
 pbng_status pbng_end_iteration(pbng_ctx *ctx, pbng_accel accel);
+/* pbng_sweep_colour_part: part 1 = the colour's owned vertices that another rank holds as ghosts (laid out
+ * first within the colour), part 2 = the others, 0 = both (= pbng_sweep_colour).  Doing part 1, then
+ * packing/sending the colour's halo on another stream while part 2 runs, overlaps the exchange with
+ * computation (dd.py); the intra-colour order does not change any result.  On an
+ * undecomposed context part 1 is empty.
+ * pbng_set_stream: the stream later calls of this context use (cudaStream_t as an integer); lets a driver
+ * issue the halo pack/unpack on a side stream. */
+pbng_status pbng_sweep_colour_part(pbng_ctx *ctx, int32_t colour, int32_t part, pbng_accel accel, double omega,
+                                   double rho, double gamma);
+pbng_status pbng_set_stream(pbng_ctx *ctx, uintptr_t cuda_stream);
 
 /* ---- domain decomposition -------------------------------------------------------------
  * pbng_set_partition (before pbng_color): owner[v] in [0, n_ranks) for every vertex; this context is rank

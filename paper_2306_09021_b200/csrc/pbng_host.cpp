@@ -133,6 +133,8 @@ struct pbng_ctx {
     std::vector<int32_t> halo_send_orig, halo_recv_orig;  // the same lists as original vertex ids
     int cur_accel = -1;  // acceleration of the colour passes of the iteration in progress (-1: none yet)
     std::vector<int32_t> col_vbegin, col_nfree;
+    std::vector<int32_t> col_nsend;   // per colour: owned free vertices some other rank holds (laid out first)
+    std::vector<int64_t> col_chunk_mid;  // per colour: first chunk of the vertices after the halo-send ones
     std::vector<int64_t> gcol_nfree;  // free vertices per colour over the whole mesh (all ranks)
     std::vector<int64_t> col_chunk;
     // host images of the device arrays (uploaded by bind)
@@ -266,16 +268,23 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     c->h_chunk_v.clear();
     c->h_chunk_off.push_back(0);
     int64_t n_chunks = 0;
+    c->col_chunk_mid.assign(c->ncol, 0);
+    if (c->col_nsend.size() != (size_t)c->ncol) c->col_nsend.assign(c->ncol, 0);
     for (int32_t col = 0; col < c->ncol; ++col) {
         c->col_chunk[col] = n_chunks;
-        const int32_t v0 = c->col_vbegin[col], nc = c->col_nfree[col];
-        for (int32_t k = 0; k < nc; k += kChunk) {
-            const int32_t cnt = std::min<int32_t>(kChunk, nc - k);
-            int32_t width = 0;
-            for (int32_t q = 0; q < cnt; ++q) width = std::max(width, c->h_deg[v0 + k + q]);
-            c->h_chunk_v.push_back(make_int2(v0 + k, cnt));
-            c->h_chunk_off.push_back(c->h_chunk_off.back() + (int64_t)width * kChunk);
-            ++n_chunks;
+        // two parts, each chunked from its own start: the halo-send vertices, then the rest
+        for (int part = 0; part < 2; ++part) {
+            if (part == 1) c->col_chunk_mid[col] = n_chunks;
+            const int32_t ns = c->col_nsend[col];
+            const int32_t v0 = c->col_vbegin[col] + (part ? ns : 0), nc = part ? c->col_nfree[col] - ns : ns;
+            for (int32_t k = 0; k < nc; k += kChunk) {
+                const int32_t cnt = std::min<int32_t>(kChunk, nc - k);
+                int32_t width = 0;
+                for (int32_t q = 0; q < cnt; ++q) width = std::max(width, c->h_deg[v0 + k + q]);
+                c->h_chunk_v.push_back(make_int2(v0 + k, cnt));
+                c->h_chunk_off.push_back(c->h_chunk_off.back() + (int64_t)width * kChunk);
+                ++n_chunks;
+            }
         }
     }
     c->col_chunk[c->ncol] = n_chunks;
@@ -828,9 +837,10 @@ pbng_status check_iterate(pbng_ctx *c, pbng_accel accel, double omega, double rh
     return PBNG_OK;
 }
 
-// one colour pass of iteration l with the blend weights of PAPER.md:605-616
+// one colour pass of iteration l with the blend weights of PAPER.md:605-616; part 1 =
+// the colour's halo-send vertices, 2 = the others, 0 = both (one launch per non-empty part)
 cudaError_t sweep_colour_impl(pbng_ctx *c, int32_t col, pbng_accel accel, double omega, double rho, double gamma,
-                              int64_t *launched) {
+                              int64_t *launched, int part = 0) {
     SweepLaunch s;
     s.accel = accel;
     s.work = c->work;
@@ -842,15 +852,20 @@ cudaError_t sweep_colour_impl(pbng_ctx *c, int32_t col, pbng_accel accel, double
         s.omega = chebyshev_weight(c->l + 1, rho);
         s.gamma = gamma;
     }
-    s.v_begin = c->col_vbegin[col];
-    s.n_v = c->col_nfree[col];
-    s.chunk_begin = c->col_chunk[col];
     s.split = problem_split(c);
-    if (s.n_v == 0) return cudaSuccess;
-    cudaError_t e = timed_sweep(c, s);
-    c->launches += 1;
-    *launched += 1;
-    return e;
+    const int32_t ns = c->col_nsend[col];
+    for (int p = 1; p <= 2; ++p) {
+        if (part != 0 && part != p) continue;
+        s.v_begin = c->col_vbegin[col] + (p == 1 ? 0 : ns);
+        s.n_v = p == 1 ? ns : c->col_nfree[col] - ns;
+        s.chunk_begin = p == 1 ? c->col_chunk[col] : c->col_chunk_mid[col];
+        if (s.n_v == 0) continue;
+        cudaError_t e = timed_sweep(c, s);
+        if (e != cudaSuccess) return e;
+        c->launches += 1;
+        *launched += 1;
+    }
+    return cudaSuccess;
 }
 
 // after the last colour: x^{l+1} becomes the working buffer (accelerated), l += 1
@@ -1120,6 +1135,9 @@ static pbng_status colour_and_layout(pbng_ctx *c, const std::vector<int32_t> *gi
             else if (nranks == 1) need[v] |= 1ull;
         }
         auto held = [&](int64_t v) { return ((need[v] >> me) & 1ull) != 0; };
+        // an owned free vertex another rank holds is sent after its colour pass: laid out first in its
+        // colour so that its part of the pass can run before the rest (dd.py overlaps the exchange)
+        auto is_send = [&](int64_t v) { return !is_pinned[v] && own[v] == me && (need[v] & ~bit(me)) != 0ull; };
         // permutation: owned free vertices colour-major | ghost free vertices | held pinned vertices
         c->col_vbegin.assign(c->ncol + 1, 0);
         c->col_nfree.assign(c->ncol, 0);
@@ -1131,16 +1149,20 @@ static pbng_status colour_and_layout(pbng_ctx *c, const std::vector<int32_t> *gi
             }
         for (int32_t k = 0; k < c->ncol; ++k) c->col_vbegin[k + 1] = c->col_vbegin[k] + c->col_nfree[k];
         c->n_free = c->col_vbegin[c->ncol];
+        c->col_nsend.assign(c->ncol, 0);
+        for (int64_t v = 0; v < nv; ++v)
+            if (is_send(v)) c->col_nsend[c->colour[v]]++;
         c->orig2int.assign((size_t)nv, -1);
         c->int2orig.assign((size_t)c->n_free, 0);
         {
             std::vector<int32_t> fill(c->col_vbegin.begin(), c->col_vbegin.end() - 1);
-            for (int64_t v = 0; v < nv; ++v)
-                if (!is_pinned[v] && own[v] == me) {
-                    const int32_t i = fill[c->colour[v]]++;
-                    c->orig2int[v] = i;
-                    c->int2orig[i] = (int32_t)v;
-                }
+            for (int pass = 0; pass < 2; ++pass)  // halo-send vertices first within each colour
+                for (int64_t v = 0; v < nv; ++v)
+                    if (!is_pinned[v] && own[v] == me && is_send(v) == (pass == 0)) {
+                        const int32_t i = fill[c->colour[v]]++;
+                        c->orig2int[v] = i;
+                        c->int2orig[i] = (int32_t)v;
+                    }
             for (int64_t v = 0; v < nv; ++v)
                 if (!is_pinned[v] && own[v] != me && held(v)) {
                     c->orig2int[v] = (int32_t)c->int2orig.size();
@@ -1215,9 +1237,11 @@ static pbng_status colour_and_layout(pbng_ctx *c, const std::vector<int32_t> *gi
                 for (int a = 0; a < 3; ++a) q[a] = (uint64_t)((c->X[3 * v + a] - lo[a]) * scale);
                 key[v] = morton3(q[0], q[1], q[2]);
             }
-            for (int32_t col = 0; col < c->ncol; ++col) {
+            for (int32_t col = 0; col < c->ncol; ++col) {  // each part (halo-send | rest) sorted on its own
                 int32_t *b = c->int2orig.data() + c->col_vbegin[col];
-                std::stable_sort(b, b + c->col_nfree[col], [&](int32_t x, int32_t y) { return key[x] < key[y]; });
+                const int32_t ns = c->col_nsend[col];
+                std::stable_sort(b, b + ns, [&](int32_t x, int32_t y) { return key[x] < key[y]; });
+                std::stable_sort(b + ns, b + c->col_nfree[col], [&](int32_t x, int32_t y) { return key[x] < key[y]; });
                 for (int32_t q = 0; q < c->col_nfree[col]; ++q) c->orig2int[b[q]] = c->col_vbegin[col] + q;
             }
         }
@@ -1477,6 +1501,27 @@ pbng_status pbng_sweep_colour(pbng_ctx *c, int32_t colour, pbng_accel accel, dou
     int64_t n = 0;
     PBNG_CUDA(sweep_colour_impl(c, colour, accel, omega, rho, gamma, &n), "sweep_colour: sweep kernel");
     c->cur_accel = (int)accel;
+    return PBNG_OK;
+}
+
+pbng_status pbng_sweep_colour_part(pbng_ctx *c, int32_t colour, int32_t part, pbng_accel accel, double omega,
+                                   double rho, double gamma) {
+    pbng_status st = check_iterate(c, accel, omega, rho, gamma, "sweep_colour_part");
+    if (st != PBNG_OK) return st;
+    if (colour < 0 || colour >= c->ncol) return fail(PBNG_E_INVALID_ARGUMENT, "sweep_colour_part: colour out of range");
+    if (part < 0 || part > 2) return fail(PBNG_E_INVALID_ARGUMENT, "sweep_colour_part: part must be 0, 1 or 2");
+    if (c->cur_accel >= 0 && c->cur_accel != (int)accel)
+        return fail(PBNG_E_BAD_ORDER, "sweep_colour_part: acceleration changed within an iteration");
+    DevGuard g(c->device);
+    int64_t n = 0;
+    PBNG_CUDA(sweep_colour_impl(c, colour, accel, omega, rho, gamma, &n, part), "sweep_colour_part: sweep kernel");
+    c->cur_accel = (int)accel;
+    return PBNG_OK;
+}
+
+pbng_status pbng_set_stream(pbng_ctx *c, uintptr_t cuda_stream) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
     return PBNG_OK;
 }
 

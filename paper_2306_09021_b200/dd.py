@@ -110,17 +110,53 @@ class LoopbackExchange:
 
 
 def iterate(ctxs: List[Context], exchanger, n: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0,
-            gamma: float = 1.0):
+            gamma: float = 1.0, overlap: bool = True):
     """n PBNG iterations of a decomposed mesh: every colour pass on every local rank context, then the
-    halo exchange of that colour (PAPER.md:693-705 order), then the fused blend closes the iteration."""
+    halo exchange of that colour (PAPER.md:693-705 order), then the fused blend closes the iteration.
+
+    overlap: each colour pass is split (pbng_sweep_colour_part): the halo-send vertices first, then the
+    halo of the colour is packed, exchanged and unpacked on a side stream while the colour's remaining
+    vertices are updated on the main stream; the next colour waits for both.  Packing reads only the
+    halo-send rows and unpacking writes only ghost rows of this colour, which no vertex of this colour
+    reads, so the results are those of the serial order bit for bit."""
     n_col = ctxs[0].n_colours
-    for _ in range(n):
-        for c in range(n_col):
+    if not overlap:
+        for _ in range(n):
+            for c in range(n_col):
+                for ctx in ctxs:
+                    ctx.sweep_colour(c, accel, omega, rho, gamma)
+                exchanger.exchange(c)
             for ctx in ctxs:
-                ctx.sweep_colour(c, accel, omega, rho, gamma)
-            exchanger.exchange(c)
-        for ctx in ctxs:
-            ctx.end_iteration(accel)
+                ctx.end_iteration(accel)
+        return
+    import torch
+    main = torch.cuda.current_stream(ctxs[0].device)
+    side = torch.cuda.Stream(ctxs[0].device)
+    boundary_done, exchange_done = torch.cuda.Event(), torch.cuda.Event()
+    saved = [ctx.stream for ctx in ctxs]
+    try:
+        for _ in range(n):
+            for c in range(n_col):
+                for ctx in ctxs:
+                    ctx.set_stream(main)
+                    ctx.sweep_colour_part(c, 1, accel, omega, rho, gamma)
+                boundary_done.record(main)
+                side.wait_event(boundary_done)
+                for ctx in ctxs:
+                    ctx.set_stream(side)
+                with torch.cuda.stream(side):
+                    exchanger.exchange(c)
+                exchange_done.record(side)
+                for ctx in ctxs:
+                    ctx.set_stream(main)
+                    ctx.sweep_colour_part(c, 2, accel, omega, rho, gamma)
+                main.wait_event(exchange_done)
+            for ctx in ctxs:
+                ctx.end_iteration(accel)
+    finally:
+        for ctx, st in zip(ctxs, saved):
+            if st is not None:
+                ctx.set_stream(st)
 
 
 def combine_energy_residual(parts):

@@ -29,7 +29,7 @@ EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbn
            "pbng_last_error", "pbng_version", "pbng_sweep_colour", "pbng_end_iteration", "pbng_set_partition",
            "pbng_halo_counts", "pbng_halo_vertices", "pbng_halo_pack", "pbng_halo_unpack", "pbng_test_polar",
            "pbng_set_inertia", "pbng_set_schedule", "pbng_detect_contacts", "pbng_update_constraints",
-           "pbng_get_colours", "pbng_set_l2_persistence")
+           "pbng_get_colours", "pbng_set_l2_persistence", "pbng_sweep_colour_part", "pbng_set_stream")
 
 WC_DTYPE = np.dtype([("n0", "<i4"), ("n1", "<i4"), ("idx0", "<i4", 4), ("idx1", "<i4", 4), ("w0", "<f8", 4),
                      ("w1", "<f8", 4), ("anchor", "<f8", 3), ("K", "<f8", 6)])
@@ -95,6 +95,8 @@ def lib():
     L.pbng_update_constraints.argtypes = [vp, vp, vp, i64, C.POINTER(i64)]
     L.pbng_get_colours.argtypes = [vp, vp, C.POINTER(i32)]
     L.pbng_set_l2_persistence.argtypes = [vp, C.c_int]
+    L.pbng_sweep_colour_part.argtypes = [vp, i32, i32, C.c_int, d, d, d]
+    L.pbng_set_stream.argtypes = [vp, C.c_size_t]
     L.pbng_last_error.restype = C.c_char_p
     L.pbng_version.restype = i32
     for name in EXPORTS:
@@ -324,6 +326,17 @@ class Context:
     # ---- colour-by-colour iteration and domain decomposition -------------------------------------
     def sweep_colour(self, colour: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0, gamma: float = 1.0):
         _check(lib().pbng_sweep_colour(self._h, int(colour), ACCEL[accel], float(omega), float(rho), float(gamma)))
+
+    def sweep_colour_part(self, colour: int, part: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0,
+                          gamma: float = 1.0):
+        """part 1: the colour's halo-send vertices; 2: the rest; 0: both (pbng_sweep_colour_part)."""
+        _check(lib().pbng_sweep_colour_part(self._h, int(colour), int(part), ACCEL[accel], float(omega), float(rho),
+                                            float(gamma)))
+
+    def set_stream(self, stream):
+        """Issue this context's later calls on `stream` (a torch.cuda.Stream)."""
+        self.stream = stream
+        _check(lib().pbng_set_stream(self._h, stream.cuda_stream))
 
     def end_iteration(self, accel: str = "none"):
         _check(lib().pbng_end_iteration(self._h, ACCEL[accel]))

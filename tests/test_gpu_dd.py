@@ -26,11 +26,11 @@ def single(scene, dtype):
     return x, E, R
 
 
-def decomposed(scene, dtype, world):
+def decomposed(scene, dtype, world, overlap=True):
     from paper_2306_09021_b200 import dd
     ctxs, owner = dd.loopback_contexts(scene, world, dtype=dtype)
     ex = dd.LoopbackExchange(ctxs, scene.accel)
-    dd.iterate(ctxs, ex, scene.iterations, scene.accel, scene.omega, scene.rho, scene.gamma)
+    dd.iterate(ctxs, ex, scene.iterations, scene.accel, scene.omega, scene.rho, scene.gamma, overlap=overlap)
     E, R = dd.combine_energy_residual([c.energy_residual() for c in ctxs])
     xs = [c.get_positions().cpu().numpy() for c in ctxs]
     infos = [c.query() for c in ctxs]
@@ -76,3 +76,12 @@ def test_batched_sample_minor_decomposition_is_bitwise():
     assert infos[0]["n_batch"] == 40 and sum(i["n_ghosts"] for i in infos) > 0
     assert np.array_equal(x1, xd), np.abs(x1 - xd).max()
     np.testing.assert_allclose(Ed, E1, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("cfg,world", [(5, 2), (3, 3)])
+def test_decomposition_without_overlap_is_bitwise(cfg, world):
+    """The serial exchange order (colour pass, then its exchange) gives the same bits as the overlapped one."""
+    s = G.make_config(cfg, "small")
+    x1, E1, _ = single(s, "f32")
+    xd, Ed, _, _ = decomposed(s, "f32", world, overlap=False)
+    assert np.array_equal(x1, xd)
