@@ -718,7 +718,8 @@ void plan_workspace(pbng_ctx *c) {
     take(c->r_tet_c, c->h_tet_c.size());
     take(c->r_int2orig, (size_t)std::max<int64_t>(c->n_local, 1) * 4);
     take(c->r_targets, c->h_targets.size());
-    const size_t groups = (size_t)((c->nb + (1 << p.lane_shift) - 1) >> p.lane_shift);
+    size_t groups = (size_t)((c->nb + (1 << p.lane_shift) - 1) >> p.lane_shift);
+    if (p.lane_shift == 5) groups += groups & 1;  // an even number of sample groups (sweep_batched2_kernel)
     for (int k = 0; k < 3; ++k) take(c->r_x[k], (groups << p.lane_shift) * (size_t)p.x_stride * s4);
     take(c->r_stage, (size_t)c->nb * (size_t)c->nv * 3 * s);
     take(c->r_part_e, (size_t)c->nb * p.ge * 8);
@@ -1370,6 +1371,9 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     chk(up(c->r_dep_off, c->h_dep_off.data(), c->h_dep_off.size() * 4));
     chk(up(c->r_deps, c->h_deps.data(), c->h_deps.size() * 4));
     chk(cudaMemsetAsync(base + c->r_flag.off, 0, 4, c->stream));
+    // position buffers start at zero: padding rows / lanes (x_stride, sample groups) are then finite
+    for (int k = 0; k < 3; ++k) chk(cudaMemsetAsync(base + c->r_x[k].off, 0, c->r_x[k].bytes, c->stream));
+    chk(cudaMemsetAsync(base + c->r_xt.off, 0, c->r_xt.bytes, c->stream));
     chk(cudaStreamSynchronize(c->stream));
     if (e != cudaSuccess) return cuda_fail(e, "bind_workspace");
     c->ws = dptr;

@@ -1164,6 +1164,125 @@ __global__ void __launch_bounds__(kSweepBlock) sweep_batched_kernel(const Layout
     finish_vertex<R, ACCEL>(L, work, xs, (int64_t)v << 5, oi, hi, xa4, f, A, omega, gamma);
 }
 
+// ------------------------------------------------------------------------------------------------
+// Batched samples, two groups per warp (fp32 Neo-Hookean, n_batch >= 64): lane holds samples
+// 64 g + lane and 64 g + 32 + lane, and every pair's arithmetic runs in packed FP32x2 instructions
+// (FFMA2 / FADD2 / FMUL2: two fused multiply-adds per lane per instruction on sm_100), which halves the
+// issued instructions of this issue-bound kernel.  The record is shared by both samples (one shuffle).
+// Same per-vertex order as sweep_kernel; the rounding of the packed expressions differs from the
+// compiler's scalar contraction by an ulp per operation.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 ng(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, ng(b)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+// eq:nh pair term for two samples at once (see contrib<..., Pair<R, MODEL_NH>>)
+__device__ __forceinline__ void contrib_nh2(const float2 (&d1)[3], const float2 (&d2)[3], const float2 (&d3)[3],
+                                            const Pair<float, MODEL_NH> &p, float cmu, float clam, float2 (&f)[3],
+                                            float2 (&A)[6]) {
+    const float2 e1[3] = {sub2(d2[0], d1[0]), sub2(d2[1], d1[1]), sub2(d2[2], d1[2])};
+    const float2 e2[3] = {sub2(d3[0], d1[0]), sub2(d3[1], d1[1]), sub2(d3[2], d1[2])};
+    const float2 n[3] = {fma2(e1[1], e2[2], ng(mul2(e1[2], e2[1]))), fma2(e1[2], e2[0], ng(mul2(e1[0], e2[2]))),
+                         fma2(e1[0], e2[1], ng(mul2(e1[1], e2[0])))};
+    const float2 J = mul2(fma2(d1[0], n[0], fma2(d1[1], n[1], mul2(d1[2], n[2]))), bc(p.detB));
+    const float Vmu = p.VE * cmu, Vlam = p.VE * clam, lh = Vmu + Vlam;
+    const float2 sc = fma2(bc(lh), J, bc(-lh - Vmu));  // lamhat (J - 1) - mu, times V
+    const float dg = -2.f * Vmu * (p.s[0] + p.s[1] + p.s[2]);
+    float2 w[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        w[r] = mul2(bc(-p.detB), n[r]);
+        const float2 Fg = fma2(bc(p.s[2]), d3[r], fma2(bc(p.s[1]), d2[r], mul2(bc(p.s[0]), d1[r])));
+        f[r] = fma2(ng(sc), w[r], fma2(bc(-Vmu), Fg, f[r]));
+    }
+    const float2 t0 = mul2(bc(Vlam), w[0]), t1 = mul2(bc(Vlam), w[1]), t2 = mul2(bc(Vlam), w[2]);
+    A[0] = fma2(t0, w[0], add2(A[0], bc(dg)));
+    A[1] = fma2(t1, w[1], add2(A[1], bc(dg)));
+    A[2] = fma2(t2, w[2], add2(A[2], bc(dg)));
+    A[3] = fma2(t0, w[1], A[3]);
+    A[4] = fma2(t1, w[2], A[4]);
+    A[5] = fma2(t0, w[2], A[5]);
+}
+
+#ifndef PBNG_B2_MINB
+#define PBNG_B2_MINB 1
+#endif
+template <int ACCEL, bool FEXT, bool WC>
+__global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_kernel(const Layout L, const int32_t v_begin,
+                                                                     const int32_t n_v, const int64_t chunk_begin,
+                                                                     const int64_t x_stride, const int32_t n_batch,
+                                                                     const int wi, const int oi, const int hi,
+                                                                     const float cmu, const float clam,
+                                                                     const float omega, const float gamma,
+                                                                     const float idt2) {
+    constexpr int WPB = kSweepBlock / 32;
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * WPB + (threadIdx.x >> 5);  // vertex index within the colour
+    if (t >= n_v) return;                                  // warp-uniform
+    const int v = v_begin + t;
+    const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
+    const int deg = ld(L.deg + v);
+    const int64_t g0 = 2 * (int64_t)blockIdx.y;             // the warp's two sample groups g0, g0 + 1
+    const int64_t xs[2] = {((g0 * x_stride) << 5) + lane, (((g0 + 1) * x_stride) << 5) + lane};
+    float4 *__restrict__ work0 = reinterpret_cast<float4 *>(L.xbuf[wi]) + xs[0];
+    float4 *__restrict__ work1 = reinterpret_cast<float4 *>(L.xbuf[wi]) + xs[1];
+    const int64_t vv = (int64_t)v << 5;
+    const float4 xa0 = work0[vv], xa1 = work1[vv];
+    const float2 xa[3] = {make_float2(xa0.x, xa1.x), make_float2(xa0.y, xa1.y), make_float2(xa0.z, xa1.z)};
+    float2 f[3] = {bc(0.f), bc(0.f), bc(0.f)};
+    if (FEXT) {
+        const float4 fe = ld(reinterpret_cast<const float4 *>(L.fext) + v);
+        f[0] = bc(fe.x); f[1] = bc(fe.y); f[2] = bc(fe.z);
+    }
+    float2 A[6] = {bc(0.f), bc(0.f), bc(0.f), bc(0.f), bc(0.f), bc(0.f)};
+    for (int k0 = 0; k0 < deg; k0 += 32) {
+        Pair<float, MODEL_NH> mine = {};
+        if (k0 + lane < deg) load_pair<false>(L, base + (int64_t)(k0 + lane) * kChunk, mine);
+        const int n = min(32, deg - k0);
+#pragma unroll 2
+        for (int j = 0; j < n; ++j) {
+            const Pair<float, MODEL_NH> pr = shfl_pair(mine, j);
+            const int64_t i1 = (int64_t)pr.id.x << 5, i2 = (int64_t)pr.id.y << 5, i3 = (int64_t)pr.id.z << 5;
+            const float4 a0 = ld(work0 + i1), a1 = ld(work1 + i1), b0 = ld(work0 + i2), b1 = ld(work1 + i2),
+                         c0 = ld(work0 + i3), c1 = ld(work1 + i3);
+            const float2 d1[3] = {sub2(make_float2(a0.x, a1.x), xa[0]), sub2(make_float2(a0.y, a1.y), xa[1]),
+                                  sub2(make_float2(a0.z, a1.z), xa[2])};
+            const float2 d2[3] = {sub2(make_float2(b0.x, b1.x), xa[0]), sub2(make_float2(b0.y, b1.y), xa[1]),
+                                  sub2(make_float2(b0.z, b1.z), xa[2])};
+            const float2 d3[3] = {sub2(make_float2(c0.x, c1.x), xa[0]), sub2(make_float2(c0.y, c1.y), xa[1]),
+                                  sub2(make_float2(c0.z, c1.z), xa[2])};
+            contrib_nh2(d1, d2, d3, pr, cmu, clam, f, A);
+        }
+    }
+    // per sample: weak constraints, inertia, solve, blend, store (scalar)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int b = (int)((g0 + q) * 32 + lane);
+        if (b >= n_batch) continue;
+        float4 *__restrict__ work = q ? work1 : work0;
+        const float4 xa4 = q ? xa1 : xa0;
+        const float xs3[3] = {xa4.x, xa4.y, xa4.z};
+        float fs[3], As[6];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) fs[r] = q ? f[r].y : f[r].x;
+#pragma unroll
+        for (int r = 0; r < 6; ++r) As[r] = q ? A[r].y : A[r].x;
+        if (WC) wc_contrib<float, float, true>(L, work, 5, v, xs3, fs, As);
+        if (idt2 > 0.f)
+            inertia_contrib<float, float>(L, v, ld(reinterpret_cast<const float4 *>(L.xtilde) + xs[q] + vv), idt2, xs3, fs,
+                                          As);
+        finish_vertex<float, ACCEL>(L, work, xs[q], vv, oi, hi, xa4, fs, As, omega, gamma);
+    }
+}
+
+#ifndef PBNG_BATCHED2
+#define PBNG_BATCHED2 1
+#endif
+constexpr bool kBatched2 = PBNG_BATCHED2;  // packed FP32x2 batched kernel for fp32 Neo-Hookean
+
 template <class R, int MODEL, int ACCEL, bool FE, bool W, int S>
 cudaError_t split_launch(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
     constexpr int B = SplitBlock<S>::n, VPB = B / S;
@@ -1184,6 +1303,16 @@ cudaError_t split_launch(const Problem &p, const Layout &L, const SweepLaunch &s
 template <class R, int MODEL, int ACCEL, bool FE, bool W>
 cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
     const R cmu = R(p.cmu), clam = R(p.clam), om = R(s.omega), ga = R(s.gamma), idt2 = R(p.inv_dt2);
+    if (p.lane_shift == 5 && kBatched2 && sizeof(R) == 4 && MODEL == MODEL_NH) {
+        constexpr int WPB = kSweepBlock / 32;
+        const int64_t groups = (p.n_batch + 31) / 32;  // pairs of groups; the workspace holds an even count
+        dim3 grid((unsigned)((s.n_v + WPB - 1) / WPB), (unsigned)((groups + 1) / 2));
+        sweep_batched2_kernel<ACCEL, FE, W><<<grid, kSweepBlock, 0, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,
+                                                                          p.x_stride, p.n_batch, s.work, s.out,
+                                                                          s.hist, float(cmu), float(clam), float(om),
+                                                                          float(ga), float(idt2));
+        return cudaGetLastError();
+    }
     if (p.lane_shift == 5) {
         constexpr int WPB = kSweepBlock / 32;
         dim3 grid((unsigned)((s.n_v + WPB - 1) / WPB), (unsigned)((p.n_batch + 31) / 32));
