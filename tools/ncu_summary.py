@@ -63,7 +63,8 @@ def to_bytes(v, u):
 
 def to_us(v, u):
     x = num(v)
-    return x * {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3, "second": 1e6}.get(u, 1)
+    return x * {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3, "second": 1e6, "ns": 1e-3, "us": 1, "ms": 1e3,
+                "s": 1e6}.get(u, 1)
 
 
 def launch_shares(path):
