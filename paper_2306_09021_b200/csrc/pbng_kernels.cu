@@ -62,6 +62,15 @@ template <class R> __device__ __forceinline__ typename RT<R>::R4 mk4(R x, R y, R
 template <> __device__ __forceinline__ float4 mk4<float>(float x, float y, float z) { return make_float4(x, y, z, 0.f); }
 template <> __device__ __forceinline__ double4 mk4<double>(double x, double y, double z) { return make_double4(x, y, z, 0.0); }
 
+// packed FP32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2: two fp32 operations per lane per instruction,
+// each rounded as the scalar operation)
+__device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 ng(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, ng(b)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
 // ------------------------------------------------------------------------------------------------
 // Polar rotation R(F) (eq:cor): closest rotation, det R = +1 also for inverted F.
 // Cyclic Jacobi on S = F^T F (fixed sweep count) -> V; B = F V with columns sorted by decreasing norm
@@ -225,6 +234,53 @@ __device__ __forceinline__ void polar_newton(const R (&F)[3][3], const R (&C0)[3
     }
 }
 
+#ifndef PBNG_FCR_PACKED
+#define PBNG_FCR_PACKED 1
+#endif
+// fp32 overload: the X update runs in packed FP32x2 on X and cof(X) held as register pairs (element
+// 3a + b in pair (3a + b) / 2); the cofactor itself stays scalar.  Same iteration as the template.
+__device__ __forceinline__ void polar_newton(const float (&F)[3][3], const float (&C0)[3][3], float J0,
+                                             float (&Xo)[3][3]) {
+    if (!PBNG_FCR_PACKED) {
+        polar_newton<float>(F, C0, J0, Xo);
+        return;
+    }
+    float2 X[5], C[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int e0 = 2 * k, e1 = 2 * k + 1;
+        X[k] = make_float2(F[e0 / 3][e0 % 3], e1 < 9 ? F[e1 / 3][e1 % 3] : 0.f);
+        C[k] = make_float2(C0[e0 / 3][e0 % 3], e1 < 9 ? C0[e1 / 3][e1 % 3] : 0.f);
+    }
+#define PX(e) (((e) & 1) ? X[(e) >> 1].y : X[(e) >> 1].x)
+    float d = J0;
+#pragma unroll
+    for (int it = 0; it < PBNG_NEWTON_ITERS; ++it) {
+        float lg, g;
+        asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(d));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(-0.33333334f * lg));
+        const float2 hx = bc(0.5f * g), hc = bc(__fdividef(0.5f, g * d));
+#pragma unroll
+        for (int k = 0; k < 5; ++k) X[k] = fma2(hc, C[k], mul2(hx, X[k]));
+        if (it + 1 < PBNG_NEWTON_ITERS) {
+            const float c00 = PX(4) * PX(8) - PX(5) * PX(7), c01 = PX(5) * PX(6) - PX(3) * PX(8),
+                        c02 = PX(3) * PX(7) - PX(4) * PX(6), c10 = PX(2) * PX(7) - PX(1) * PX(8),
+                        c11 = PX(0) * PX(8) - PX(2) * PX(6), c12 = PX(1) * PX(6) - PX(0) * PX(7),
+                        c20 = PX(1) * PX(5) - PX(2) * PX(4), c21 = PX(2) * PX(3) - PX(0) * PX(5),
+                        c22 = PX(0) * PX(4) - PX(1) * PX(3);
+            C[0] = make_float2(c00, c01);
+            C[1] = make_float2(c02, c10);
+            C[2] = make_float2(c11, c12);
+            C[3] = make_float2(c20, c21);
+            C[4] = make_float2(c22, 0.f);
+            d = PX(0) * c00 + PX(1) * c01 + PX(2) * c02;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 9; ++e) Xo[e / 3][e % 3] = PX(e);
+#undef PX
+}
+
 // R(F) as the fixed-corotated sweep computes it: fp32 -> scaled Newton when det F > 1e-4 |F|_F^3, else the
 // Jacobi routine; fp64 -> Jacobi (7 sweeps).  C = cof F and J = det F are passed in.
 template <class R>
@@ -255,10 +311,21 @@ __device__ __forceinline__ void pair_contrib(const T (&d1)[3], const T (&d2)[3],
                                              const T (&g1)[3], const T (&g2)[3], const T (&g3)[3], T Vmu, T Vlam,
                                              T (&f)[3], T (&A)[6]) {
     T F[3][3];
+    if constexpr (sizeof(T) == 4 && PBNG_FCR_PACKED) {  // columns 0, 1 of F in packed FP32x2
+        const float2 g1p = make_float2(g1[0], g1[1]), g2p = make_float2(g2[0], g2[1]), g3p = make_float2(g3[0], g3[1]);
 #pragma unroll
-    for (int r = 0; r < 3; ++r)
+        for (int r = 0; r < 3; ++r) {
+            const float2 fr = fma2(bc(d3[r]), g3p, fma2(bc(d2[r]), g2p, mul2(bc(d1[r]), g1p)));
+            F[r][0] = fr.x;
+            F[r][1] = fr.y;
+            F[r][2] = d1[r] * g1[2] + d2[r] * g2[2] + d3[r] * g3[2];
+        }
+    } else {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) F[r][c] = d1[r] * g1[c] + d2[r] * g2[c] + d3[r] * g3[c];
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) F[r][c] = d1[r] * g1[c] + d2[r] * g2[c] + d3[r] * g3[c];
+    }
     const T g[3] = {-(g1[0] + g2[0] + g3[0]), -(g1[1] + g2[1] + g3[1]), -(g1[2] + g2[2] + g3[2])};
     T C[3][3];
     C[0][0] = F[1][1] * F[2][2] - F[1][2] * F[2][1];
@@ -1172,12 +1239,6 @@ __global__ void __launch_bounds__(kSweepBlock) sweep_batched_kernel(const Layout
 // Same per-vertex order as sweep_kernel; the rounding of the packed expressions differs from the
 // compiler's scalar contraction by an ulp per operation.
 // ------------------------------------------------------------------------------------------------
-__device__ __forceinline__ float2 bc(float a) { return make_float2(a, a); }
-__device__ __forceinline__ float2 ng(float2 a) { return make_float2(-a.x, -a.y); }
-__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, ng(b)); }
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 
 // eq:nh pair term for two samples at once (see contrib<..., Pair<R, MODEL_NH>>)
 __device__ __forceinline__ void contrib_nh2(const float2 (&d1)[3], const float2 (&d2)[3], const float2 (&d3)[3],
