@@ -262,8 +262,9 @@ pbng_status pbng_query(pbng_ctx *ctx, pbng_info *info);
 
 /* L2 residency of the gathered positions: enable != 0 sets an access-policy window on the context's stream
  * that marks the two position buffers the colour passes gather from (current and next iterate) as
- * persisting in L2 (and sets the device's persisting-L2 limit to their size, capped by the device
- * maximum), so the record stream streaming through L2 does not evict them between colour passes;
+ * persisting in L2 (and sets the device's persisting-L2 limit to their size) when they fit in the device's
+ * persisting carve-out (otherwise no window is set: larger buffers would thrash it), so the record
+ * stream streaming through L2 does not evict them between colour passes;
  * enable = 0 clears the window.  Affects every kernel later launched on that stream.  Requires a bound
  * workspace; every later pbng_bind_workspace re-applies it. */
 pbng_status pbng_set_l2_persistence(pbng_ctx *ctx, int enable);

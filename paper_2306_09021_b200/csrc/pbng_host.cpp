@@ -889,12 +889,19 @@ pbng_status apply_l2_persistence(pbng_ctx *c, int enable) {
         PBNG_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device), "l2: attribute");
         PBNG_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device), "l2: attribute");
         const char *base = static_cast<const char *>(c->ws) + c->r_x[0].off;
-        const size_t bytes = std::min<size_t>((c->r_x[1].off + c->r_x[1].bytes) - c->r_x[0].off, (size_t)max_window);
+        const size_t bytes = (c->r_x[1].off + c->r_x[1].bytes) - c->r_x[0].off;
+        if (bytes > (size_t)max_window || bytes > (size_t)max_persist) {
+            // buffers larger than the persisting carve-out would thrash it (measured slower on config 4
+            // and the fp64 variant of config 3): no window
+            v.accessPolicyWindow.num_bytes = 0;
+            PBNG_CUDA(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v), "l2: stream attribute");
+            return PBNG_OK;
+        }
         PBNG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(bytes, (size_t)max_persist)),
                   "l2: persisting limit");
         v.accessPolicyWindow.base_ptr = const_cast<char *>(base);
         v.accessPolicyWindow.num_bytes = bytes;
-        v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)std::max<size_t>(bytes, 1));
+        v.accessPolicyWindow.hitRatio = 1.0f;
         v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     } else {
