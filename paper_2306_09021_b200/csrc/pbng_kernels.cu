@@ -995,13 +995,22 @@ __device__ __forceinline__ void group_sync(int id, int nthreads) {
 
 // threads per CTA of the split and pipelined kernels: whole SPLIT-warp groups, at least kSweepBlock
 template <int SPLIT> struct SplitBlock { static constexpr int n = SPLIT * 32 > kSweepBlock ? SPLIT * 32 : kSweepBlock; };
+// resident CTAs the split kernel is compiled for: fp32 at 64 registers (32 warps per SM; without the hint
+// ptxas picks 91 registers for the fixed-corotated kernel and config 5 runs 25% slower), fp64 unconstrained
+#ifndef PBNG_SPLIT_WARPS_F32
+#define PBNG_SPLIT_WARPS_F32 32
+#endif
+template <class R, int SPLIT> struct SplitMinBlocks {
+    static constexpr int n = sizeof(R) == 4 ? PBNG_SPLIT_WARPS_F32 * 32 / SplitBlock<SPLIT>::n : 1;
+};
 
 // SPLIT warps form a group that owns one item at a time (SPLIT = 1: update_vertex, the arithmetic of
 // sweep_kernel; SPLIT > 1: the partial sums and fixed-order combination of sweep_split_kernel), so the
 // per-vertex summation order -- and the result -- is that of the colour-launch schedule with the same
 // split (pbng_host.cpp problem_split).
 template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int SPLIT>
-__global__ void __launch_bounds__(SplitBlock<SPLIT>::n, PBNG_SWEEP_MINB) sweep_pipe_kernel(const Layout L, const PipeLaunch P,
+__global__ void __launch_bounds__(SplitBlock<SPLIT>::n, (MODEL == MODEL_FCR && SPLIT == 8) ? 3 : PBNG_SWEEP_MINB)
+    sweep_pipe_kernel(const Layout L, const PipeLaunch P,
                                                                  const int64_t x_stride, const int32_t n_batch,
                                                                  const int64_t n_chunks, const R cmu, const R clam,
                                                                  const R idt2) {
@@ -1111,7 +1120,7 @@ __global__ void __launch_bounds__(SplitBlock<SPLIT>::n, PBNG_SWEEP_MINB) sweep_p
 // partial sums (f: 3, A: 6) are combined through shared memory in fixed warp order (deterministic),
 // and warp 0 solves and stores.  Block = SPLIT * 32 * CPB threads, CPB chunks per block.
 template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int SPLIT>
-__global__ void __launch_bounds__(SplitBlock<SPLIT>::n) sweep_split_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
+__global__ void __launch_bounds__(SplitBlock<SPLIT>::n, (SplitMinBlocks<R, SPLIT>::n)) sweep_split_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
                                                                   const int64_t chunk_begin, const int64_t x_stride,
                                                                   const int wi, const int oi, const int hi, const R cmu,
                                                                   const R clam, const R omega, const R gamma,
