@@ -803,6 +803,12 @@ __device__ __forceinline__ void split_partial(const Layout &L, const typename RT
     }
 }
 
+// resident CTAs sweep_kernel is compiled for (PBNG_SWEEP_MINB: fp32; PBNG_SWEEP_MINB_F64: fp64)
+#ifndef PBNG_SWEEP_MINB_F64
+#define PBNG_SWEEP_MINB_F64 1
+#endif
+template <class R> struct SweepMinBlocks { static constexpr int n = sizeof(R) == 4 ? PBNG_SWEEP_MINB : PBNG_SWEEP_MINB_F64; };
+
 // One free vertex's PBNG update: accumulate over its records in ascending tet order,
 // weak constraints, inertia, then solve + blend + store (finish_vertex).
 template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int G>
@@ -868,7 +874,7 @@ template <class R, int MODEL> struct StageSmem {  // per warp: [ring][kGroups mb
 // gather their neighbour positions (through L1; they belong to other colours, read-only in this
 // launch).  The per-vertex summation order is ascending tet index, as in the oracle.
 template <class R, int MODEL, int ACCEL, bool FEXT, bool WC>
-__global__ void __launch_bounds__(kSweepBlock, PBNG_SWEEP_MINB) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
+__global__ void __launch_bounds__(kSweepBlock, (SweepMinBlocks<R>::n)) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
                                                             const int64_t chunk_begin, const int64_t x_stride,
                                                             const int wi, const int oi, const int hi, const R cmu,
                                                             const R clam, const R omega, const R gamma, const R idt2) {
