@@ -11,6 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def main():
+    full = "--full-fcr" in sys.argv  # configs 2 and 5 over all their iterations (oracle: ~3 and ~30 min)
     from oracle import Oracle
     from paper_2306_09021_b200 import context_from_scene
     from scenes import generators as G
@@ -20,6 +21,9 @@ def main():
              ("config3_f64", G.config3_hetero_cube(), "f64", 1, [0]),
              ("config4", G.config4_batched(), "f32", None, [0, 1777, 4095]),
              ("config5", G.config5_muscle_stack(), "f32", 1, [0])]
+    if full:
+        cases = [("config2_all_iterations", G.config2_twisted_bar(), "f32", None, [0]),
+                 ("config5_all_iterations", G.config5_muscle_stack(), "f32", None, [0])]
     for name, s, dtype, iters, samples in cases:
         n = s.iterations if iters is None else iters
         ctx = context_from_scene(s, device=0, dtype=dtype)
