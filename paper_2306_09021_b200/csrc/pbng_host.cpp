@@ -1809,6 +1809,7 @@ pbng_status pbng_update_constraints(pbng_ctx *c, const double *pinned_xyz, const
         const uint64_t ws_bytes = c->ws_bytes;
         st = colour_and_layout(c, &col);
         if (st != PBNG_OK) return st;
+        if (n_recoloured) *n_recoloured = changed;
         c->prob.inv_dt2 = 0.0;  // the backward-Euler target is not carried over (pbng_set_inertia again)
         if (was_bound) {
             if (c->ws_need > ws_bytes)

@@ -277,7 +277,12 @@ class Context:
         w = wc if isinstance(wc, np.ndarray) and wc.dtype == WC_DTYPE else weak_constraints_array(wc)
         w = np.ascontiguousarray(w)
         t = None if targets is None else _np(targets, np.float64).reshape(-1)
-        saved = self.get_positions().clone() if (self.device >= 0 and self.workspace is not None) else None
+        saved = None  # the iterate, kept for the re-bind when the new layout outgrows the workspace
+        if self.device >= 0 and self.workspace is not None:
+            try:
+                saved = self.get_positions()
+            except PBNGError:  # positions never set: nothing to keep
+                saved = None
         n = C.c_int64()
         st = lib().pbng_update_constraints(self._h, _ptr(t) if t is not None else None, _ptr(w) if w.size else None,
                                            w.size, C.byref(n))
