@@ -233,3 +233,15 @@ def test_full_config5_one_iteration():
     assert q["n_pairs"] == 21206016 and q["n_colours"] == 8
     xo, Eo, _, _ = run_oracle(s, iterations=1)
     assert_parity(s, "f32", xg[0], Eg[0], xo, Eo)
+
+
+@pytest.mark.parametrize("n_samples", [72, 97])
+def test_batched_odd_group_count(n_samples):
+    # 3 / 4 sample groups of 32 (the last ragged): the packed two-group fp32 kernel pairs groups (0, 1),
+    # (2, 3) -- with 3 groups the last pair is padded by a zeroed group that is never stored
+    s = G.config4_batched(n_samples=n_samples, n=4, iterations=20)
+    xg, Eg, rg, q = run_gpu(s, "f32")
+    assert q["n_batch"] == n_samples
+    for b in (0, 63, 64, n_samples - 1):
+        xo, Eo, _, _ = run_oracle(s, sample=b)
+        assert_parity(s, "f32", xg[b], Eg[b], xo, Eo, extra=f"sample {b}")
