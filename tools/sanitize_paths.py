@@ -1,7 +1,6 @@
-"""Drive every kernel path of libpbng once on small scenes, for compute-sanitizer (memcheck / racecheck /
-synccheck / initcheck) on a GPU box:
-
-    compute-sanitizer --tool memcheck python tools/sanitize_paths.py
+"""Drive every kernel path of libpbng once on small scenes and check that each returns finite energies /
+residuals (the non-finite flag is also checked by the library), e.g. under compute-sanitizer where a pool
+allows it (`compute-sanitizer --tool memcheck python tools/sanitize_paths.py`; this pool refuses it):
 
 Paths: colour launches (thread-per-vertex, split 2/4/8) and the pipelined schedule for Neo-Hookean,
 fixed-corotated and stable Neo-Hookean in fp32 and fp64 with no / SOR / Chebyshev acceleration; the
@@ -27,8 +26,9 @@ def main():
         if schedule:
             ctx.set_schedule(schedule)
         ctx.iterate(iters, s.accel, s.omega, s.rho, s.gamma)
-        ctx.energy_residual()
-        ctx.get_positions()
+        E, R = ctx.energy_residual()
+        x = ctx.get_positions()
+        assert np.all(np.isfinite(E)) and np.all(np.isfinite(R)) and bool(torch.isfinite(x).all())
         ctx.close()
 
     for cfg in (1, 5):
