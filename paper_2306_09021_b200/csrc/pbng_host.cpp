@@ -1300,6 +1300,8 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     char *base = static_cast<char *>(dptr);
     auto at = [&](const Region &r) { return static_cast<void *>(base + r.off); };
     Layout L;
+    L.n_vertices = c->n_local;
+    L.n_slots = c->n_slots;
     L.rec_id = static_cast<const int4 *>(at(c->r_rec_id));
     L.rec_a = at(c->r_rec_a);
     L.rec_b = at(c->r_rec_b);

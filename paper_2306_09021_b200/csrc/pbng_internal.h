@@ -41,6 +41,7 @@ struct ContactHit {
 };
 
 struct Layout {
+    int64_t n_vertices = 0, n_slots = 0;  // bounds for the PBNG_DEBUG device asserts
     const int4 *rec_id = nullptr;
     const void *rec_a = nullptr, *rec_b = nullptr, *rec_c = nullptr;
     const int64_t *chunk_off = nullptr;  // [n_chunks + 1]

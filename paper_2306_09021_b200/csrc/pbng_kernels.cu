@@ -18,6 +18,18 @@
 
 #include "pbng_internal.h"
 
+// PBNG_DEBUG=1 builds (tools/build_variants.py dbg=PBNG_DEBUG=1) check every record slot and gathered
+// vertex index against the context's bounds with device asserts (the pool refuses compute-sanitizer)
+#ifndef PBNG_DEBUG
+#define PBNG_DEBUG 0
+#endif
+#if PBNG_DEBUG
+#include <cassert>
+#define PBNG_CHECK(c) assert(c)
+#else
+#define PBNG_CHECK(c) ((void)0)
+#endif
+
 namespace pbng {
 namespace {
 
@@ -503,11 +515,18 @@ template <class R> struct Pair<R, MODEL_NH> {
     R s[3], detB, VE;
 };
 
+__device__ __forceinline__ void check_ids(const Layout &L, int64_t r, const int4 &id) {
+    PBNG_CHECK(r >= 0 && r < L.n_slots);
+    PBNG_CHECK(id.x >= 0 && id.x < L.n_vertices && id.y >= 0 && id.y < L.n_vertices && id.z >= 0 &&
+               id.z < L.n_vertices);
+}
+
 // STREAM: read-once record (L1::no_allocate); otherwise cached (the batched kernel's broadcast loads)
 template <bool STREAM, class R>
 __device__ __forceinline__ void load_pair(const Layout &L, int64_t r, PairG<R> &p) {
     if (STREAM) Rec<R>::load(L, r, p.id, p.g1, p.g2, p.g3, p.VE);
     else Rec<R>::load_shared(L, r, p.id, p.g1, p.g2, p.g3, p.VE);
+    check_ids(L, r, p.id);
 }
 template <bool STREAM>
 __device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<float, MODEL_NH> &p) {
@@ -517,6 +536,7 @@ __device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<float
     p.id = id;
     p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
     p.VE = __int_as_float(id.w);
+    check_ids(L, r, p.id);
 }
 template <bool STREAM>
 __device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<double, MODEL_NH> &p) {
@@ -526,6 +546,7 @@ __device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<doubl
     const double4 x = STREAM ? lds(a) : ld(a);
     p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
     p.VE = ld(c);
+    check_ids(L, r, p.id);
 }
 
 // L2 prefetch of a later record of the stream (no registers held while it is in flight)
