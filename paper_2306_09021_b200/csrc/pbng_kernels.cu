@@ -880,7 +880,11 @@ constexpr bool kSweepTma = PBNG_SWEEP_TMA;
 #ifndef PBNG_PDL
 #define PBNG_PDL 1
 #endif
-constexpr bool kPdl = PBNG_PDL;  // colour launches as programmatic dependent launches (register path)
+constexpr bool kPdl = PBNG_PDL;
+#ifndef PBNG_ONE_WAVE
+#define PBNG_ONE_WAVE 1
+#endif
+constexpr bool kOneWave = PBNG_ONE_WAVE;  // register-capped sweep instance for colours of ~1 wave  // colour launches as programmatic dependent launches (register path)
 constexpr int kGroup = PBNG_TMA_GROUP;      // record steps per bulk copy
 constexpr int kGroups = PBNG_TMA_GROUPS;    // ring depth in groups
 template <class R, int MODEL> struct StageSmem {  // per warp: [ring][kGroups mbarriers, padded]
@@ -894,8 +898,8 @@ template <class R, int MODEL> struct StageSmem {  // per warp: [ring][kGroups mb
 // (TMA), one mbarrier per group: HBM latency is hidden without holding registers, and the lanes only
 // gather their neighbour positions (through L1; they belong to other colours, read-only in this
 // launch).  The per-vertex summation order is ascending tet index, as in the oracle.
-template <class R, int MODEL, int ACCEL, bool FEXT, bool WC>
-__global__ void __launch_bounds__(kSweepBlock, (SweepMinBlocks<R>::n)) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
+template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, bool ONE_WAVE = false>
+__global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : SweepMinBlocks<R>::n)) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
                                                             const int64_t chunk_begin, const int64_t x_stride,
                                                             const int wi, const int oi, const int hi, const R cmu,
                                                             const R clam, const R omega, const R gamma, const R idt2) {
@@ -1437,6 +1441,18 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
         at[0].val.programmaticStreamSerializationAllowed = (kPdl && !kSweepTma) ? 1 : 0;
         cfg.attrs = at;
         cfg.numAttrs = 1;
+        // a colour that fits in one wave only at full occupancy (the two small colours of config 3) runs a
+        // register-capped instance so that it does not leave a second, almost empty wave
+        static int sms = 0;
+        if (sms == 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const int64_t blocks = (int64_t)grid.x * grid.y;
+        if (kOneWave && sizeof(R) == 4 && !kSweepTma && blocks > (int64_t)sms * 6 && blocks <= (int64_t)sms * (1024 / kSweepBlock))
+            return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, true>, L, s.v_begin, s.n_v,
+                                      s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga, idt2);
         return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W>, L, s.v_begin, s.n_v, s.chunk_begin,
                                   p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga, idt2);
     }
