@@ -24,6 +24,8 @@ def main():
     if full:
         cases = [("config2_all_iterations", G.config2_twisted_bar(), "f32", None, [0]),
                  ("config5_all_iterations", G.config5_muscle_stack(), "f32", None, [0])]
+    if "--full-nh" in sys.argv:  # config 3 over its 50 iterations (oracle ~9 min)
+        cases = [("config3_all_iterations", G.config3_hetero_cube(), "f32", None, [0])]
     for name, s, dtype, iters, samples in cases:
         n = s.iterations if iters is None else iters
         ctx = context_from_scene(s, device=0, dtype=dtype)
