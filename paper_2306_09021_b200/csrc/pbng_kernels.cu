@@ -1450,6 +1450,18 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         }
         const int64_t blocks = (int64_t)grid.x * grid.y;
+        // L1 / shared-memory split of the register path (PBNG_CARVEOUT = percent of the unified array
+        // given to shared memory; unset: the driver's choice)
+        static const int carve = [] {
+            const char *e = getenv("PBNG_CARVEOUT");
+            return e ? atoi(e) : -1;
+        }();
+        static bool carved = false;
+        if (!kSweepTma && carve >= 0 && !carved) {
+            cudaFuncSetAttribute(sweep_kernel<R, MODEL, ACCEL, FE, W>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+            cudaFuncSetAttribute(sweep_kernel<R, MODEL, ACCEL, FE, W, true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+            carved = true;
+        }
         if (kOneWave && sizeof(R) == 4 && !kSweepTma && blocks > (int64_t)sms * 6 && blocks <= (int64_t)sms * (1024 / kSweepBlock))
             return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, true>, L, s.v_begin, s.n_v,
                                       s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga, idt2);
