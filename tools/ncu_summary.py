@@ -135,7 +135,9 @@ def main():
               f"(bench.py model, DESIGN.md): **{alg/1e6:.1f} MB** (ratio {tot_b/n/alg:.3f}).",
               f"ncu DRAM bandwidth over the iteration: {tot_b/tot_t/1e3:.0f} GB/s (cold cache, serialised launches).",
               f"FLOP rate over the iteration (SASS add + mul + 2 fma): FP32 {fl['f']/tot_t/1e6:.2f} TFLOP/s, "
-              f"FP64 {fl['d']/tot_t/1e6:.2f} TFLOP/s (derived peaks: FP32 74.4, FP64 37.2 TFLOP/s at 1965 MHz).", "",
+              f"FP64 {fl['d']/tot_t/1e6:.2f} TFLOP/s (derived peaks: FP32 74.4, FP64 37.2 TFLOP/s at 1965 MHz; scalar "
+              "FADD/FMUL/FFMA thread-op counters: the packed FP32x2 FFMA2/FADD2/FMUL2 of the FCR and batched NH kernels have "
+              "no counter in this ncu set, so those kernels are under-counted).", "",
               "## Launch list (share of GPU time, all launches of the command)", "",
               "| kernel | launches | total us | share |", "|---|---|---|---|"]
     for name, c, t, sh in shares:
