@@ -26,6 +26,8 @@ def main():
                  ("config5_all_iterations", G.config5_muscle_stack(), "f32", None, [0])]
     if "--full-nh" in sys.argv:  # config 3 over its 50 iterations (oracle ~9 min)
         cases = [("config3_all_iterations", G.config3_hetero_cube(), "f32", None, [0])]
+    if "--full-nh-f64" in sys.argv:  # the fp64 measurement variant of config 3 over its 50 iterations
+        cases = [("config3_f64_all_iterations", G.config3_hetero_cube(), "f64", None, [0])]
     if "--many-c4" in sys.argv:  # config 4: 64 seeded random samples over all 100 iterations (~2 s each)
         picks = sorted(np.random.default_rng(2306).choice(4096, size=64, replace=False).tolist())
         cases = [("config4_64_samples", G.config4_batched(), "f32", None, picks)]
