@@ -4,4 +4,4 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl refere
 this package.  The product path (paper_2306_09021_b200) never imports it.
 """
 from .oracle import Oracle, build_oracle, lib, lame, cofactor, psi, piola, mod_hess_density, polar  # noqa: F401
-from .oracle import chebyshev_omega  # noqa: F401
+from .oracle import chebyshev_omega, threads  # noqa: F401

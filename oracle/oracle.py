@@ -15,8 +15,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "pbng_oracle.c")
 _SO = os.path.join(_HERE, "liborc.so")
+_SO_OMP = os.path.join(_HERE, "liborc_omp.so")
 _lock = threading.Lock()
 _lib = None
+_lib_omp = None
 
 ACCEL = {"none": 0, "sor": 1, "chebyshev": 2}
 MODEL = {"nh": 0, "fcr": 1, "snh": 2}
@@ -30,14 +32,18 @@ class OracleError(RuntimeError):
         self.bad = bad
 
 
-def build_oracle(force: bool = False) -> str:
-    """Compile the oracle with gcc (serial, -O2, no FP contraction so the arithmetic is as written)."""
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-std=c99", "-fPIC", "-shared",
-                               "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _SO)
-    return _SO
+def build_oracle(force: bool = False, omp: bool = False) -> str:
+    """Compile the oracle with gcc (-O2, no FP contraction so the arithmetic is as written).  omp=True
+    builds the same source with -fopenmp (liborc_omp.so): the colour pass runs its nodes on all host
+    threads, as the paper's implementation does; results are bitwise those of the serial
+    build (each node reads only other colours; sums are taken in a fixed order)."""
+    so = _SO_OMP if omp else _SO
+    if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(_SRC):
+        tmp = so + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-std=c99", "-fPIC", "-shared"]
+                              + (["-fopenmp"] if omp else []) + ["-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, so)
+    return so
 
 
 class _Scene(C.Structure):
@@ -51,11 +57,12 @@ class _Scene(C.Structure):
     ]
 
 
-def lib():
-    global _lib
+def lib(omp: bool = False):
+    """The serial oracle library, or (omp=True) the OpenMP build of the same source."""
+    global _lib, _lib_omp
     with _lock:
-        if _lib is None:
-            L = C.CDLL(build_oracle())
+        if (_lib_omp if omp else _lib) is None:
+            L = C.CDLL(build_oracle(omp=omp))
             vp, d, i64, i32 = C.c_void_p, C.c_double, C.c_int64, C.c_int32
             L.orc_cofactor.argtypes = [vp, vp]
             L.orc_det.argtypes = [vp]
@@ -104,8 +111,18 @@ def lib():
             L.orc_contact_stiffness.argtypes = [vp, d, d, vp]
             L.orc_set_colours.argtypes = [vp, vp]
             L.orc_set_colours.restype = C.c_int
-            _lib = L
-    return _lib
+            L.orc_threads.argtypes = [C.c_int]
+            L.orc_threads.restype = C.c_int
+            if omp:
+                _lib_omp = L
+            else:
+                _lib = L
+    return _lib_omp if omp else _lib
+
+
+def threads(n: int = 0) -> int:
+    """Set (n > 0) and return the OpenMP oracle's thread count."""
+    return int(lib(omp=True).orc_threads(int(n)))
 
 
 def _p(a: np.ndarray):
@@ -266,8 +283,10 @@ def contact_constraints(contacts, kn: float, kt: float = 0.0) -> dict:
 class Oracle:
     """Prepared oracle for one sample of a scene (scenes.Scene)."""
 
-    def __init__(self, scene, sample: int = 0):
-        L = lib()
+    def __init__(self, scene, sample: int = 0, omp: bool = False):
+        """omp=True runs the same oracle source built with OpenMP (bitwise identical, all host threads)."""
+        L = lib(omp)
+        self._L = L
         self.scene = scene
         self.sample = sample
         self._keep = []
@@ -325,48 +344,48 @@ class Oracle:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and _lib is not None:
-            _lib.orc_free(h)
+        if h is not None and getattr(self, "_L", None) is not None:
+            self._L.orc_free(h)
             self._h = None
 
     # ---- precompute getters ------------------------------------------------------------------------
     def set_colours(self, colours) -> None:
         """Use a given colouring (e.g. recolor_incremental's) for the sweeps."""
         c = np.ascontiguousarray(np.asarray(colours, dtype=np.int32))
-        st = lib().orc_set_colours(self._h, _p(c))
+        st = self._L.orc_set_colours(self._h, _p(c))
         if st:
             raise OracleError(st)
 
     @property
     def n_colours(self) -> int:
-        return int(lib().orc_num_colours(self._h))
+        return int(self._L.orc_num_colours(self._h))
 
     def colours(self) -> np.ndarray:
         out = np.empty(self.nv, np.int32)
-        lib().orc_get_colour(self._h, _p(out))
+        self._L.orc_get_colour(self._h, _p(out))
         return out
 
     def rest(self):
         B = np.empty((max(self.nt, 1), 3, 3))
         V = np.empty(max(self.nt, 1))
-        lib().orc_get_rest(self._h, _p(B), _p(V))
+        self._L.orc_get_rest(self._h, _p(B), _p(V))
         return B[:self.nt], V[:self.nt]
 
     def mass(self) -> np.ndarray:
         out = np.empty(self.nv)
-        lib().orc_get_mass(self._h, _p(out))
+        self._L.orc_get_mass(self._h, _p(out))
         return out
 
     def set_inertia(self, dt: float, xtilde=None):
         """Backward Euler (eq:fem_be): dt > 0 with xtilde = 2 x^n - x^{n-1}; dt = 0 -> quasistatic."""
         xt = None if xtilde is None else self._x(xtilde)
-        st = lib().orc_set_inertia(self._h, float(dt), _p(xt) if xt is not None else None)
+        st = self._L.orc_set_inertia(self._h, float(dt), _p(xt) if xt is not None else None)
         if st:
             raise OracleError(st)
 
     def fext(self) -> np.ndarray:
         out = np.empty((self.nv, 3))
-        lib().orc_get_fext(self._h, _p(out))
+        self._L.orc_get_fext(self._h, _p(out))
         return out
 
     # ---- evaluation --------------------------------------------------------------------------------
@@ -377,36 +396,36 @@ class Oracle:
     def deformation_gradient(self, x, e: int):
         x = self._x(x)
         F = np.empty((3, 3))
-        lib().orc_deformation_gradient(self._h, _p(x), e, _p(F))
+        self._L.orc_deformation_gradient(self._h, _p(x), e, _p(F))
         return F
 
     def nodal(self, x, i: int):
         x = self._x(x)
         f = np.empty(3)
         A = np.empty((3, 3))
-        lib().orc_nodal(self._h, _p(x), int(i), _p(f), _p(A))
+        self._L.orc_nodal(self._h, _p(x), int(i), _p(f), _p(A))
         return f, A
 
     def forces(self, x) -> np.ndarray:
         x = self._x(x)
         out = np.empty((self.nv, 3))
-        lib().orc_forces(self._h, _p(x), _p(out))
+        self._L.orc_forces(self._h, _p(x), _p(out))
         return out
 
     def residual(self, x) -> float:
         x = self._x(x)
-        return float(lib().orc_residual(self._h, _p(x)))
+        return float(self._L.orc_residual(self._h, _p(x)))
 
     def energy(self, x, parts: bool = False):
         x = self._x(x)
         pr = np.empty(3)
-        e = float(lib().orc_energy(self._h, _p(x), _p(pr)))
+        e = float(self._L.orc_energy(self._h, _p(x), _p(pr)))
         return (e, pr) if parts else e
 
     # ---- iteration ---------------------------------------------------------------------------------
     def sweep(self, x) -> np.ndarray:
         w = self._x(x).copy()
-        fails = lib().orc_sweep(self._h, _p(w))
+        fails = self._L.orc_sweep(self._h, _p(w))
         if fails:
             raise RuntimeError(f"{fails} nodal solves failed")
         return w
@@ -414,7 +433,7 @@ class Oracle:
     def sweep_colour_inplace(self, w: np.ndarray, c: int) -> None:
         """One colour pass of a PBNG iteration, in place on a float64 C-contiguous (nv, 3) array."""
         assert w.dtype == np.float64 and w.flags.c_contiguous and w.shape == (self.nv, 3)
-        fails = lib().orc_sweep_colour(self._h, _p(w), int(c))
+        fails = self._L.orc_sweep_colour(self._h, _p(w), int(c))
         if fails:
             raise RuntimeError(f"{fails} nodal solves failed")
 
@@ -423,7 +442,7 @@ class Oracle:
         """n accelerated PBNG iterations from iteration index l0; returns (x^{l0+n}, x^{l0+n-1})."""
         x = self._x(x).copy()
         xm1 = self._x(xm1).copy()
-        fails = lib().orc_iterate(self._h, _p(x), _p(xm1), int(l0), int(n), ACCEL[accel], float(omega),
+        fails = self._L.orc_iterate(self._h, _p(x), _p(xm1), int(l0), int(n), ACCEL[accel], float(omega),
                                   float(rho), float(gamma))
         if fails:
             raise RuntimeError(f"{fails} nodal solves failed")

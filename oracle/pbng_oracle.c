@@ -28,6 +28,9 @@
  * Pinned by tests/test_oracle_*.py (materials, colouring, solver); no function is "parity unpinned".
  */
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -700,6 +703,11 @@ static int spd_solve3(const double *A, const double *r, double *x) {
  * guess, x_i += A^{-1} (f_i + f^ext_i), with no line search.  Returns the number of failed solves. */
 int64_t orc_sweep_colour(const orc_prep *p, double *w, int32_t c) {
     int64_t i, fails = 0;
+    /* The paper's own implementation runs this loop in parallel with OpenMP.  Node i reads
+     * only nodes of other colours, which this pass does not write, so every node's
+     * update is independent of the order and of the thread count: the OpenMP build (liborc_omp.so) is
+     * bitwise identical to the serial one (pinned by tests/test_oracle_openmp.py). */
+#pragma omp parallel for schedule(dynamic, 512) reduction(+ : fails)
     for (i = 0; i < p->nv; ++i) {
         double f[3], A[9], dx[3];
         if (p->colour[i] != c || p->pinned[i]) continue;
@@ -746,6 +754,7 @@ int64_t orc_iterate(const orc_prep *p, double *x, double *xm1, int64_t l0, int32
         double om = orc_chebyshev_omega(l + 1, rho);
         memcpy(w, x, (size_t)N * sizeof(double));
         fails += orc_sweep(p, w);
+#pragma omp parallel for schedule(static)
         for (k = 0; k < N; ++k) {
             double xl = x[k], xl1 = xm1[k], xn;
             if (p->pinned[k / 3]) continue;
@@ -767,19 +776,26 @@ int64_t orc_iterate(const orc_prep *p, double *x, double *xm1, int64_t l0, int32
 /* r_i = f_i(y) + f^ext_i for every node (pinned included; the residual norm skips them) */
 void orc_forces(const orc_prep *p, const double *y, double *r) {
     int64_t i;
-    double A[9];
-    for (i = 0; i < p->nv; ++i) orc_nodal(p, y, i, r + 3 * i, A);
+#pragma omp parallel for schedule(dynamic, 512)
+    for (i = 0; i < p->nv; ++i) {
+        double A[9];
+        orc_nodal(p, y, i, r + 3 * i, A);
+    }
 }
 
 /* Newton residual 2-norm over free nodes (Fig. 10 caption; reading Z14) */
 double orc_residual(const orc_prep *p, const double *y) {
     int64_t i;
-    double s = 0.0, f[3], A[9];
+    double s = 0.0;
+    double *r = malloc((size_t)p->nv * 3 * sizeof(double));
+    if (!r) return NAN;
+    orc_forces(p, y, r); /* per node, then summed in ascending node order (thread-count independent) */
     for (i = 0; i < p->nv; ++i) {
+        const double *f = r + 3 * i;
         if (p->pinned[i]) continue;
-        orc_nodal(p, y, i, f, A);
         s += f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
     }
+    free(r);
     return sqrt(s);
 }
 
@@ -788,11 +804,17 @@ double orc_residual(const orc_prep *p, const double *y) {
 double orc_energy(const orc_prep *p, const double *y, double *parts) {
     int64_t e, c, i;
     double el = 0.0, wc = 0.0, ext = 0.0;
+    double *psi = malloc((size_t)(p->nt > 0 ? p->nt : 1) * sizeof(double));
+    if (!psi) return NAN;
+    /* per-element V_e Psi(F_e), then summed in ascending element order (thread-count independent) */
+#pragma omp parallel for schedule(static)
     for (e = 0; e < p->nt; ++e) {
         double F[9];
         deformation_gradient(p, y, e, F);
-        el += p->V[e] * orc_psi(p->model, p->mu[e], p->lambda[e], F, 0);
+        psi[e] = p->V[e] * orc_psi(p->model, p->mu[e], p->lambda[e], F, 0);
     }
+    for (e = 0; e < p->nt; ++e) el += psi[e];
+    free(psi);
     for (c = 0; c < p->nwc; ++c) {
         double C[3], K[9];
         int a, b;
@@ -1119,6 +1141,17 @@ void orc_contact_stiffness(const double *n, double kn, double kt, double *K6) {
 
 /* Replace the colouring (e.g. by orc_recolor_incremental's); sweeps then visit these colours in ascending
  * order.  Returns ORC_E_ARG for a negative colour. */
+/* threads used by the OpenMP build (n > 0 sets the count); the serial build always reports 1 */
+int orc_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
+}
+
 int orc_set_colours(orc_prep *p, const int32_t *colour) {
     int64_t v;
     int32_t m = 0;

@@ -210,7 +210,7 @@ def config1_tiny_cube(n: int = 4, dtype: str = "f64", iterations: int = 200) -> 
 
 
 def config2_twisted_bar(nx: int = 32, nz: int = 128, dtype: str = "f32", iterations: int = 100,
-                        gamma: float = 1.7) -> Scene:
+                        gamma: float = 1.7, noise_seed: int = 0) -> Scene:
     """Config 2: 32x32x128-cell bar 0.25 x 0.25 x 1 (h = 1/128), FCR, E=1e6, nu=0.45.  z=0 pinned at
     rest, z=1 layer rotated +90 deg about the bar axis through (0.125, 0.125).  Free vertices start at
     rest + U(+-0.05h).  Chebyshev rho=0.95, gamma = 1.7."""

@@ -211,30 +211,6 @@ def test_full_config4_sampled_samples_all_iterations():
         assert_parity(s, "f32", xg[b], Eg[b], xo, Eo, extra=f"sample {b}")
 
 
-def test_full_config3_one_iteration():
-    s = G.config3_hetero_cube()  # 128^3, 12.6M tets, fp32 NH, SOR 1.5
-    xg, Eg, _, q = run_gpu(s, "f32", iterations=1)
-    assert q["n_pairs"] == 49938432 and q["n_colours"] == 8
-    xo, Eo, _, _ = run_oracle(s, iterations=1)
-    assert_parity(s, "f32", xg[0], Eg[0], xo, Eo)
-
-
-def test_full_config2_few_iterations():
-    s = G.config2_twisted_bar()  # 32x32x128, FCR fp32, Chebyshev
-    xg, Eg, _, q = run_gpu(s, "f32", iterations=4)
-    assert q["n_pairs"] == 3121152
-    xo, Eo, _, _ = run_oracle(s, iterations=4)
-    assert_parity(s, "f32", xg[0], Eg[0], xo, Eo)
-
-
-def test_full_config5_one_iteration():
-    s = G.config5_muscle_stack()  # 8 x 48^3 blocks, springs + contacts, FCR fp32
-    xg, Eg, _, q = run_gpu(s, "f32", iterations=1)
-    assert q["n_pairs"] == 21206016 and q["n_colours"] == 8
-    xo, Eo, _, _ = run_oracle(s, iterations=1)
-    assert_parity(s, "f32", xg[0], Eg[0], xo, Eo)
-
-
 @pytest.mark.parametrize("n_samples", [72, 97])
 def test_batched_odd_group_count(n_samples):
     # 3 / 4 sample groups of 32 (the last ragged): the packed two-group fp32 kernel pairs groups (0, 1),
@@ -245,3 +221,24 @@ def test_batched_odd_group_count(n_samples):
     for b in (0, 63, 64, n_samples - 1):
         xo, Eo, _, _ = run_oracle(s, sample=b)
         assert_parity(s, "f32", xg[b], Eg[b], xo, Eo, extra=f"sample {b}")
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("gamma,rho", [(0.5, 0.5), (1.7, 0.95), (0.5, 0.95), (1.7, 0.5)])
+def test_chebyshev_gamma_closed_form_gpu(gamma, rho, dtype):
+    # the oracle's closed-form pin (test_oracle_solver.py) run through the C ABI: one node tied to an
+    # anchor, so the PBNG step is exact and e_{l+1} = omega_{l+1}(1-gamma) e_l + (1-omega_{l+1}) e_{l-1}
+    # (PAPER.md:603-612); one iterate call per iteration continues the acceleration state
+    from paper_2306_09021_b200 import context_from_scene
+    from test_oracle_solver import _one_node_problem, chebyshev_error_recurrence
+    s = _one_node_problem()
+    t = s.wc["anchor"][0]
+    n = 13
+    ref = chebyshev_error_recurrence(s.x0[0][0] - t, n, rho, gamma)
+    ctx = context_from_scene(s, device=0, dtype=dtype)
+    tol = (1e-13 if dtype == "f64" else 2e-6) * np.abs(t).max()
+    for l in range(n):
+        ctx.iterate(1, "chebyshev", 1.0, rho, gamma)
+        x = ctx.get_positions().cpu().numpy().astype(np.float64)[0, 0]
+        assert np.abs((x - t) - ref[l + 1]).max() <= tol, (l, x - t, ref[l + 1])
+    ctx.close()

@@ -223,6 +223,55 @@ def test_chebyshev_index_convention_and_limit():
         assert all(b <= a for a, b in zip(seq[2:], seq[3:]))
 
 
+def chebyshev_weights_from_paper(m_max, rho):
+    """omega_1..omega_{m_max} written out from PAPER.md:603-608 (reading Z5): 1 for the first two
+    iterates, 2/(2 - rho^2) for the third, then 4/(4 - rho^2 omega_prev).  Independent of the oracle."""
+    w = [None, 1.0, 1.0]
+    while len(w) <= m_max:
+        w.append(2.0 / (2.0 - rho * rho) if len(w) == 3 else 4.0 / (4.0 - rho * rho * w[-1]))
+    return w
+
+
+def chebyshev_error_recurrence(e0, n, rho, gamma, variant="paper"):
+    """Error e_l = x^l - t on a problem whose PBNG step is exact (p = t every iteration).  From
+    x^{l+1} = omega_{l+1}(gamma (p - x^l) + x^l - x^{l-1}) + x^{l-1} (PAPER.md:603-612):
+        e_{l+1} = omega_{l+1} (1 - gamma) e_l + (1 - omega_{l+1}) e_{l-1},   e_{-1} = e_0 (Z8).
+    The two misreadings this pin must reject:
+      'gamma_on_prev' : gamma multiplies (p - x^{l-1}) instead of (p - x^l)
+      'omega_l'       : omega_l used in place of omega_{l+1}"""
+    w = chebyshev_weights_from_paper(n + 2, rho)
+    em1, e = e0.copy(), e0.copy()
+    out = [e.copy()]
+    for l in range(n):
+        om = w[l] if (variant == "omega_l" and l >= 1) else w[l + 1]
+        if variant == "gamma_on_prev":
+            en = om * (-gamma * em1 + e - em1) + em1
+        else:
+            en = om * (1.0 - gamma) * e + (1.0 - om) * em1
+        em1, e = e, en
+        out.append(e.copy())
+    return out
+
+
+@pytest.mark.parametrize("gamma", [0.5, 1.7])
+@pytest.mark.parametrize("rho", [0.5, 0.95])
+def test_chebyshev_gamma_closed_form_on_exactly_solvable_problem(gamma, rho):
+    # VERDICT r1 "What's weak" 1: pins gamma's placement and the omega_{l+1} index for gamma != 1.
+    s = _one_node_problem()
+    o = Oracle(s)
+    t = s.wc["anchor"][0]
+    n = 13
+    ref = chebyshev_error_recurrence(s.x0[0][0] - t, n, rho, gamma)
+    x, xm1 = s.x0[0], s.x0[0]
+    for l in range(n):
+        x, xm1 = o.iterate(x, xm1, l, 1, "chebyshev", rho=rho, gamma=gamma)
+        assert np.abs((x[0] - t) - ref[l + 1]).max() <= 1e-13 * np.abs(t).max(), l
+    # the pin discriminates: both misreadings leave the paper's trajectory by far more than the tolerance
+    for bad in ("gamma_on_prev", "omega_l"):
+        alt = chebyshev_error_recurrence(s.x0[0][0] - t, n, rho, gamma, bad)
+        assert max(np.abs(a - b).max() for a, b in zip(alt, ref)) > 1e-3 * np.abs(t).max(), bad
+
+
 @pytest.mark.parametrize("accel", ["sor", "chebyshev"])
 def test_acceleration_degenerate_cases(accel):
     # P13: SOR omega = 1 == plain; Chebyshev gamma = 1, rho = 0 == plain (SPEC.md:409-411)
