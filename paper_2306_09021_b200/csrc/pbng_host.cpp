@@ -154,6 +154,12 @@ struct pbng_ctx {
     std::vector<int64_t> pin_order;  // caller order of the pinned set -> ascending order (set_constraints)
     uint64_t ws_bytes = 0;           // bytes of the bound workspace
     bool l2_persist = false;         // pbng_set_l2_persistence (re-applied by every bind)
+    // state the library changed outside its own memory while the L2 window is on, restored by
+    // clear_l2_persistence (pbng_destroy, set_stream, disabling): the stream that carries the window and
+    // the device's persisting-L2 limit before the library set it
+    bool l2_applied = false;
+    cudaStream_t l2_stream = nullptr;
+    size_t l2_prev_limit = 0;
     int schedule = 0;                        // pbng_schedule requested (0 auto, 1 colour launches, 2 pipelined)
     std::vector<int4> h_tet_id;
     Problem prob;
@@ -877,37 +883,54 @@ void end_iteration_impl(pbng_ctx *c, pbng_accel accel) {
     c->cur_accel = -1;
 }
 
-// L2 access-policy window over the gathered position buffers (pbng_set_l2_persistence)
-pbng_status apply_l2_persistence(pbng_ctx *c, int enable) {
+// Undo what apply_l2_persistence changed outside the workspace: the access-policy window on the stream it
+// was set on, the persisting lines it left in L2 and the device's persisting-L2 limit.
+void clear_l2_persistence(pbng_ctx *c) {
+    if (!c->l2_applied) return;
     DevGuard g(c->device);
     cudaStreamAttrValue v;
     std::memset(&v, 0, sizeof(v));
-    if (enable) {
-        // the two buffers the colour passes gather from (work, and out = the next iteration's work) are
-        // contiguous regions of the workspace; the record stream passing through L2 is left to stream
-        int max_window = 0, max_persist = 0;
-        PBNG_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device), "l2: attribute");
-        PBNG_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device), "l2: attribute");
-        const char *base = static_cast<const char *>(c->ws) + c->r_x[0].off;
-        const size_t bytes = (c->r_x[1].off + c->r_x[1].bytes) - c->r_x[0].off;
-        if (bytes > (size_t)max_window || bytes > (size_t)max_persist) {
-            // buffers larger than the persisting carve-out would thrash it (measured slower on config 4
-            // and the fp64 variant of config 3): no window
-            v.accessPolicyWindow.num_bytes = 0;
-            PBNG_CUDA(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v), "l2: stream attribute");
-            return PBNG_OK;
-        }
-        PBNG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(bytes, (size_t)max_persist)),
-                  "l2: persisting limit");
-        v.accessPolicyWindow.base_ptr = const_cast<char *>(base);
-        v.accessPolicyWindow.num_bytes = bytes;
-        v.accessPolicyWindow.hitRatio = 1.0f;
-        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    } else {
-        v.accessPolicyWindow.num_bytes = 0;
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(c->l2_stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c->l2_prev_limit);
+    c->l2_applied = false;
+}
+
+// L2 access-policy window over the gathered position buffers (pbng_set_l2_persistence)
+pbng_status apply_l2_persistence(pbng_ctx *c, int enable) {
+    clear_l2_persistence(c);
+    if (!enable) return PBNG_OK;
+    DevGuard g(c->device);
+    // the two buffers the colour passes gather from (work, and out = the next iteration's work) are
+    // contiguous regions of the workspace; the record stream passing through L2 is left to stream
+    int max_window = 0, max_persist = 0;
+    PBNG_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c->device), "l2: attribute");
+    PBNG_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device), "l2: attribute");
+    const char *base = static_cast<const char *>(c->ws) + c->r_x[0].off;
+    const size_t bytes = (c->r_x[1].off + c->r_x[1].bytes) - c->r_x[0].off;
+    // buffers larger than the persisting carve-out would thrash it (measured slower on config 4 and the
+    // fp64 variant of config 3): no window
+    if (bytes > (size_t)max_window || bytes > (size_t)max_persist) return PBNG_OK;
+    size_t prev = 0;
+    PBNG_CUDA(cudaDeviceGetLimit(&prev, cudaLimitPersistingL2CacheSize), "l2: persisting limit");
+    PBNG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(bytes, (size_t)max_persist)),
+              "l2: persisting limit");
+    cudaStreamAttrValue v;
+    std::memset(&v, 0, sizeof(v));
+    v.accessPolicyWindow.base_ptr = const_cast<char *>(base);
+    v.accessPolicyWindow.num_bytes = bytes;
+    v.accessPolicyWindow.hitRatio = 1.0f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaError_t e = cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    if (e != cudaSuccess) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prev);
+        return cuda_fail(e, "l2: stream attribute");
     }
-    PBNG_CUDA(cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v), "l2: stream attribute");
+    c->l2_applied = true;
+    c->l2_stream = c->stream;
+    c->l2_prev_limit = prev;
     return PBNG_OK;
 }
 
@@ -950,6 +973,8 @@ pbng_status pbng_create_mesh(const double *rest_xyz, int64_t n_vertices, const i
         c->dtype = dtype;
         c->device = device;
         c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+        c->prob.device = device >= 0 ? device : 0;
+        if (device >= 0) cudaDeviceGetAttribute(&c->prob.sm_count, cudaDevAttrMultiProcessorCount, device);
         c->X.assign(rest_xyz, rest_xyz + 3 * n_vertices);
         c->tets.assign(tets, tets + 4 * n_tets);
         c->Bm.resize((size_t)n_tets * 9);
@@ -1534,7 +1559,11 @@ pbng_status pbng_sweep_colour_part(pbng_ctx *c, int32_t colour, int32_t part, pb
 
 pbng_status pbng_set_stream(pbng_ctx *c, uintptr_t cuda_stream) {
     if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
-    c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+    const cudaStream_t s = reinterpret_cast<cudaStream_t>(cuda_stream);
+    if (s == c->stream) return PBNG_OK;
+    c->stream = s;
+    // the L2 window belongs to the stream the context issues on: move it (and never leave it behind)
+    if (c->l2_applied) return apply_l2_persistence(c, 1);
     return PBNG_OK;
 }
 
@@ -1899,6 +1928,7 @@ pbng_status pbng_destroy(pbng_ctx *c) {
     if (c->on_device()) {
         DevGuard g(c->device);
         cudaStreamSynchronize(c->stream);
+        clear_l2_persistence(c);  // restore the caller's stream window and the device's persisting limit
         delete c;
     } else {
         delete c;

@@ -105,7 +105,10 @@ struct Problem {
     int64_t n_own = 0;     // owned free vertices (swept)
     double inv_dt2 = 0;    // backward Euler 1/dt^2 (0: quasistatic)
     int64_t n_surf = 0, n_sv = 0, n_cbuckets = 1;  // contact detection sizes
+    int device = 0, sm_count = 0;  // the context's CUDA device and its SM count (queried at bind)
 };
+
+constexpr int kMaxDevices = 64;  // per-device launch caches (pbng_kernels.cu) are indexed by ordinal
 
 struct SweepLaunch {
     int32_t v_begin = 0, n_v = 0;  // colour's internal vertex range

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <atomic>
 
 #include "pbng_internal.h"
 
@@ -1423,12 +1424,13 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
     }
     if (s.split <= 1) {
         constexpr int smem = (kSweepBlock / 32) * StageSmem<R, MODEL>::per_warp;
-        static bool attr = false;
-        if (smem > 48 * 1024 && !attr) {
+        // function attributes are per device: one flag per ordinal (setting one twice is harmless)
+        static std::atomic<bool> attr[kMaxDevices];
+        if (smem > 48 * 1024 && !attr[p.device % kMaxDevices].load(std::memory_order_acquire)) {
             cudaError_t e = cudaFuncSetAttribute(sweep_kernel<R, MODEL, ACCEL, FE, W>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             if (e != cudaSuccess) return e;
-            attr = true;
+            attr[p.device % kMaxDevices].store(true, std::memory_order_release);
         }
         dim3 grid((unsigned)((s.n_v + kSweepBlock - 1) / kSweepBlock), (unsigned)p.n_batch);
         cudaLaunchConfig_t cfg = {};
@@ -1443,12 +1445,7 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
         cfg.numAttrs = 1;
         // a colour that fits in one wave only at full occupancy (the two small colours of config 3) runs a
         // register-capped instance so that it does not leave a second, almost empty wave
-        static int sms = 0;
-        if (sms == 0) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        }
+        const int sms = p.sm_count > 0 ? p.sm_count : 148;
         const int64_t blocks = (int64_t)grid.x * grid.y;
         // L1 / shared-memory split of the register path (PBNG_CARVEOUT = percent of the unified array
         // given to shared memory; unset: the driver's choice)
@@ -1456,11 +1453,11 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
             const char *e = getenv("PBNG_CARVEOUT");
             return e ? atoi(e) : -1;
         }();
-        static bool carved = false;
-        if (!kSweepTma && carve >= 0 && !carved) {
+        static std::atomic<bool> carved[kMaxDevices];
+        if (!kSweepTma && carve >= 0 && !carved[p.device % kMaxDevices].load(std::memory_order_acquire)) {
             cudaFuncSetAttribute(sweep_kernel<R, MODEL, ACCEL, FE, W>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
             cudaFuncSetAttribute(sweep_kernel<R, MODEL, ACCEL, FE, W, true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-            carved = true;
+            carved[p.device % kMaxDevices].store(true, std::memory_order_release);
         }
         if (kOneWave && sizeof(R) == 4 && !kSweepTma && blocks > (int64_t)sms * 6 && blocks <= (int64_t)sms * (1024 / kSweepBlock))
             return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, true>, L, s.v_begin, s.n_v,
@@ -1473,17 +1470,18 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
     return split_launch<R, MODEL, ACCEL, FE, W, 4>(p, L, s, st);
 }
 
-// persistent grid: every SM filled to the kernel's occupancy (queried once per instantiation)
+// persistent grid: every SM filled to the kernel's occupancy (queried once per instantiation and device;
+// racing threads compute and store the same value)
 template <class R, int MODEL, int ACCEL, bool FE, bool W, int SPLIT>
 cudaError_t pipe_launch(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st) {
-    static int blocks = 0;
+    static std::atomic<int> cache[kMaxDevices];
+    int blocks = cache[p.device % kMaxDevices].load(std::memory_order_acquire);
     if (blocks == 0) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_pipe_kernel<R, MODEL, ACCEL, FE, W, SPLIT>,
                                                       SplitBlock<SPLIT>::n, 0);
-        blocks = std::max(1, sms * std::max(1, per_sm));
+        blocks = std::max(1, (p.sm_count > 0 ? p.sm_count : 148) * std::max(1, per_sm));
+        cache[p.device % kMaxDevices].store(blocks, std::memory_order_release);
     }
     constexpr int GROUPS = SplitBlock<SPLIT>::n / (32 * SPLIT);
     const int64_t items = p.n_chunks * p.n_batch * s.n_iter;

@@ -217,7 +217,8 @@ def config2_twisted_bar(nx: int = 32, nz: int = 128, dtype: str = "f32", iterati
     h = 1.0 / nz
     X, tets = kuhn_grid(nx, nx, nz, h)
     length = nz * h
-    rng = _rng(2)
+    # noise_seed > 0 draws the noise from another stream, PCG64(SEED_BASE + 2 + 1000 noise_seed) (margin checks)
+    rng = _rng(2 + 1000 * noise_seed)
     noise = rng.uniform(-0.05 * h, 0.05 * h, size=X.shape)
     bottom = _layer(X, 2, 0.0)
     top = _layer(X, 2, length)
