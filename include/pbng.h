@@ -48,7 +48,7 @@ typedef enum {
     PBNG_E_NOT_COLORED = 6,        /* device call before pbng_color */
     PBNG_E_NONFINITE = 7,          /* a non-finite position was produced (positions left as computed) */
     PBNG_E_CUDA = 8,               /* CUDA runtime error (message in pbng_last_error) */
-    PBNG_E_NCCL = 9,               /* reserved for the domain-decomposed path */
+    PBNG_E_NCCL = 9,               /* NCCL could not be loaded or an NCCL call failed (pbng_partition path) */
     PBNG_E_OUT_OF_MEMORY = 10,     /* host allocation failed or the bound workspace is too small */
     PBNG_E_NO_DEVICE = 11          /* device call on a host-only context */
 } pbng_status;
@@ -95,7 +95,7 @@ typedef struct {
     int64_t n_ghosts;         /* free vertices owned by other ranks and held here */
     int32_t rank, n_ranks;
     int32_t schedule;         /* pbng_schedule pbng_iterate uses now (1 colour launches, 2 pipelined) */
-    int32_t reserved;
+    int32_t graph_replays;    /* CUDA-graph replays of decomposed iterate blocks owned by this context */
 } pbng_info;
 
 /* How pbng_iterate orders the colour passes (PAPER.md:693-705 fixes only the ORDER: colour after colour,
@@ -218,6 +218,41 @@ pbng_status pbng_halo_vertices(pbng_ctx *ctx, int32_t colour, int32_t peer, int3
 pbng_status pbng_halo_pack(pbng_ctx *ctx, int32_t colour, int32_t peer, int32_t n_fields, void *device_buffer);
 pbng_status pbng_halo_unpack(pbng_ctx *ctx, int32_t colour, int32_t peer, int32_t n_fields,
                              const void *device_buffer);
+
+/* ---- domain decomposition with the library's own halo transport ----------------
+ * The colour loop of PAPER.md:693-705 across ranks: after colour pass k every rank needs the new colour-k
+ * values of the ghosts it holds, and nothing else (the colouring is global; PAPER.md:697-698 makes the
+ * intra-colour order irrelevant).  With a transport attached, pbng_iterate runs, per colour, entirely
+ * inside the library: the colour's halo-send vertices (sweep part 1) on the context stream; then, on a
+ * library-owned side stream, pack -> exchange -> unpack while the colour's other vertices (part 2) run on
+ * the context stream; the next colour waits for both.  The whole block of n iterations is captured once
+ * as a CUDA graph and replayed when pbng_iterate is called again from the same state (same n, blend
+ * parameters, iteration index and buffer roles -- e.g. every solve after pbng_set_positions), so the host
+ * submits one graph launch per call.  Iterates are bitwise those of the undecomposed context.
+ *
+ * pbng_nccl_unique_id: writes an NCCL unique id (128 bytes) to id_out (host memory).  Call it on ONE rank
+ *   and give the same bytes to every rank (e.g. a torch.distributed broadcast).  PBNG_E_NCCL if NCCL
+ *   (libnccl.so.2, loaded at run time; the copy PyTorch already loaded is reused) is not available.
+ * pbng_partition (before pbng_color; collective: every rank calls it with the same id): pbng_set_partition
+ *   (owner[v] in [0, n_ranks), this context is `rank`) plus an NCCL communicator over the n_ranks ranks on
+ *   the context's device, created by the library (ncclCommInitRank).  n_ranks == 1 needs no id (may be
+ *   NULL) and creates no communicator.  pbng_energy_residual then returns the GLOBAL energy (sum over
+ *   ranks) and residual (root of the summed squares), all-reduced with NCCL in fp64.
+ * pbng_group_create / pbng_group_iterate / pbng_group_destroy: the in-process loopback transport (tests
+ *   and single-GPU emulation).  ctxs[r] must be rank r of the same n_ranks-rank partition (pbng_set_partition,
+ *   no communicator), all on one device, coloured and bound; pbng_group_iterate runs the same per-colour
+ *   schedule as the NCCL path for all ranks in turn on ctxs[0]'s stream, the exchange being device-to-device
+ *   copies between the ranks' halo buffers.  No kernel ever waits for another rank's kernel.  The group
+ *   borrows the contexts (destroy the group first).
+ * Halo buffers live in the bound workspace (pbng_workspace_bytes counts them). */
+typedef struct pbng_group pbng_group;
+pbng_status pbng_nccl_unique_id(void *id_out);
+pbng_status pbng_partition(pbng_ctx *ctx, const int32_t *owner_rank, int32_t rank, int32_t n_ranks,
+                           const void *nccl_unique_id);
+pbng_status pbng_group_create(pbng_ctx *const *ctxs, int32_t n_ranks, pbng_group **out);
+pbng_status pbng_group_iterate(pbng_group *group, int32_t n_iterations, pbng_accel accel, double omega, double rho,
+                               double gamma);
+pbng_status pbng_group_destroy(pbng_group *group);
 
 /* ---- dynamic weak constraints --------------------------
  * pbng_detect_contacts: proximity detection on the device at the current positions of sample `sample`.

@@ -7,12 +7,14 @@ from .pbng import (  # noqa: F401
     ACCEL,
     Context,
     DTYPE,
+    Group,
     EXPORTS,
     LIB_PATH,
     MODEL,
     PBNGError,
     context_from_scene,
     lib,
+    nccl_unique_id,
     weak_constraints_array,
 )
 

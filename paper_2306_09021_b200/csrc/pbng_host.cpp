@@ -6,11 +6,15 @@
 // runs in the kernels of pbng_kernels.cu; there is no CPU fallback.
 #include "pbng.h"
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <utility>
@@ -167,7 +171,7 @@ struct pbng_ctx {
     Region r_rec_id, r_rec_a, r_rec_b, r_rec_c, r_chunk_off, r_chunk_v, r_deg, r_fext, r_wc_off, r_wc_cid, r_wc_d,
         r_c_n, r_c_node, r_c_w, r_c_anchor, r_c_K, r_tet_id, r_tet_a, r_tet_b, r_tet_c, r_int2orig, r_targets,
         r_x[3], r_stage, r_part_e, r_part_r, r_results, r_flag, r_halo_send, r_halo_recv, r_mass, r_xt, r_dep_off,
-        r_deps, r_pipe, r_surf, r_sv, r_chead, r_cnext, r_cres, r_cscal;
+        r_deps, r_pipe, r_surf, r_sv, r_chead, r_cnext, r_cres, r_cscal, r_hsend, r_hrecv, r_allred;
     size_t ws_need = 0;
     // bound device state
     bool bound = false;
@@ -178,6 +182,33 @@ struct pbng_ctx {
     int64_t l = 0;
     bool hist_valid = true;
     int64_t launches = 0;
+    // in-library halo transport (pbng_partition / pbng_group_*): NCCL communicator, the side stream that
+    // carries pack -> exchange -> unpack, fork/join events, and the CUDA graph of the last iterate block
+    ncclComm_t comm = nullptr;
+    cudaStream_t dd_side = nullptr;
+    cudaEvent_t dd_ev_a = nullptr, dd_ev_b = nullptr;
+    struct GraphKey {
+        int32_t n = -1;
+        int accel = -1;
+        double omega = 0, rho = 0, gamma = 0;
+        int64_t l = -1;
+        int work = -1, out = -1, hist = -1;
+        bool hist_valid = false;
+        const void *ws = nullptr;
+        cudaStream_t stream = nullptr;
+        double inv_dt2 = -1;
+        std::vector<uint64_t> gens;  // layout generation of every rank context the block drives
+        bool operator==(const GraphKey &o) const {
+            return n == o.n && accel == o.accel && omega == o.omega && rho == o.rho && gamma == o.gamma && l == o.l &&
+                   work == o.work && out == o.out && hist == o.hist && hist_valid == o.hist_valid && ws == o.ws &&
+                   stream == o.stream && inv_dt2 == o.inv_dt2 && gens == o.gens;
+        }
+    } dd_key;
+    uint64_t layout_gen = 0;  // bumped by every re-layout / bind: captured launches bake the layout in
+    cudaGraphExec_t dd_graph = nullptr;
+    int64_t dd_graph_launches = 0;   // kernels one replay of dd_graph runs
+    int64_t dd_graph_sweeps = 0;     // sweep launches one replay of dd_graph runs
+    int64_t dd_graph_replays = 0;    // replays since creation (tests: the cache is used)
     // profiling
     int profiling = 0;  // 0 off, 1 per sweep launch, 2 per iterate span (back-to-back sweep launches)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_used, ev_free;
@@ -745,6 +776,12 @@ void plan_workspace(pbng_ctx *c) {
     take(c->r_cnext, std::max<size_t>(c->h_surf.size(), 1) * 8 * 8);  // <= 8 cells per triangle, {tri, next}
     take(c->r_cres, std::max<size_t>(c->h_sv.size(), 1) * sizeof(ContactHit));
     take(c->r_cscal, 64);
+    // halo buffers of the in-library transport: Real4 [n_batch][n][3] per (colour, peer) segment
+    const size_t n_send = c->halo_send_off.empty() ? 0 : (size_t)c->halo_send_off.back();
+    const size_t n_recv = c->halo_recv_off.empty() ? 0 : (size_t)c->halo_recv_off.back();
+    take(c->r_hsend, (size_t)c->nb * n_send * 3 * s4);
+    take(c->r_hrecv, (size_t)c->nb * n_recv * 3 * s4);
+    take(c->r_allred, (size_t)c->nb * 2 * 8);
     c->ws_need = off;
 }
 
@@ -934,6 +971,305 @@ pbng_status apply_l2_persistence(pbng_ctx *c, int enable) {
     return PBNG_OK;
 }
 
+// ------------------------------------------------------------------------------------------------
+// In-library halo transport (SURVEY.md §8(b) pbng_partition, §8(e)): NCCL loaded at run time
+// ------------------------------------------------------------------------------------------------
+
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    bool ok = false;
+    std::string why;
+};
+
+// libnccl.so.2 is dlopen'ed on first use: the copy PyTorch already loaded (same SONAME) is reused, so one
+// process never holds two NCCLs; host-only contexts and single-GPU runs never need it.
+const NcclApi &nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            const char *e = dlerror();
+            api.why = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+            return;
+        }
+        bool all = true;
+        auto sym = [&](auto &fn, const char *name) {
+            fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+            if (!fn) {
+                all = false;
+                api.why += std::string(" missing ") + name;
+            }
+        };
+        sym(api.GetUniqueId, "ncclGetUniqueId");
+        sym(api.CommInitRank, "ncclCommInitRank");
+        sym(api.CommDestroy, "ncclCommDestroy");
+        sym(api.Send, "ncclSend");
+        sym(api.Recv, "ncclRecv");
+        sym(api.GroupStart, "ncclGroupStart");
+        sym(api.GroupEnd, "ncclGroupEnd");
+        sym(api.AllReduce, "ncclAllReduce");
+        sym(api.GetErrorString, "ncclGetErrorString");
+        api.ok = all;
+    });
+    return api;
+}
+
+pbng_status nccl_fail(ncclResult_t r, const char *where) {
+    const NcclApi &A = nccl();
+    return fail(PBNG_E_NCCL, std::string(where) + ": " + (A.GetErrorString ? A.GetErrorString(r) : "nccl error"));
+}
+
+// byte offsets of the (colour, peer) segment in the context's halo send / receive buffers
+size_t halo_seg_bytes(const pbng_ctx *c, int64_t count) { return (size_t)c->nb * (size_t)count * 3 * c->real4_size(); }
+char *halo_send_buf(pbng_ctx *c, size_t seg) {
+    return static_cast<char *>(c->ws) + c->r_hsend.off + halo_seg_bytes(c, c->halo_send_off[seg]);
+}
+char *halo_recv_buf(pbng_ctx *c, size_t seg) {
+    return static_cast<char *>(c->ws) + c->r_hrecv.off + halo_seg_bytes(c, c->halo_recv_off[seg]);
+}
+int64_t halo_n_send(const pbng_ctx *c, size_t seg) { return c->halo_send_off[seg + 1] - c->halo_send_off[seg]; }
+int64_t halo_n_recv(const pbng_ctx *c, size_t seg) { return c->halo_recv_off[seg + 1] - c->halo_recv_off[seg]; }
+
+cudaError_t ensure_dd_streams(pbng_ctx *c) {
+    if (c->dd_side) return cudaSuccess;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->dd_side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->dd_ev_a, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->dd_ev_b, cudaEventDisableTiming);
+    return e;
+}
+
+void drop_dd_graph(pbng_ctx *c) {
+    if (c->dd_graph) cudaGraphExecDestroy(c->dd_graph);
+    c->dd_graph = nullptr;
+    c->dd_key = pbng_ctx::GraphKey();
+}
+
+// The exchange step of one colour, on stream `side`, after every rank's part-1 vertices of the colour
+// are final: pack each (rank, peer) send list, move the buffers, unpack each receive list.  `ranks` are
+// the rank contexts this process drives (one with NCCL, all of them in the loopback group).
+struct Exchange {
+    std::vector<pbng_ctx *> ranks;
+    bool loopback = false;
+    int64_t launches = 0;
+    pbng_status status = PBNG_OK;
+
+    cudaError_t run(int32_t col, int nf, cudaStream_t side) {
+        const int n_ranks = ranks[0]->n_ranks;
+        for (pbng_ctx *c : ranks) {
+            const int bufs[3] = {c->work, c->out, c->hist};
+            for (int p = 0; p < n_ranks; ++p) {
+                const size_t seg = (size_t)col * n_ranks + p;
+                const int64_t n = p == c->rank ? 0 : halo_n_send(c, seg);
+                if (n == 0) continue;
+                cudaError_t e = launch_halo_pack(c->prob, c->L, c->L.halo_send + c->halo_send_off[seg], n, nf, bufs,
+                                                 halo_send_buf(c, seg), side);
+                if (e != cudaSuccess) return e;
+                ++launches;
+            }
+        }
+        if (loopback) {
+            for (pbng_ctx *q : ranks)  // q sends to p: p's receive segment (col, q) <- q's send segment (col, p)
+                for (pbng_ctx *p : ranks) {
+                    if (p == q) continue;
+                    const size_t sseg = (size_t)col * n_ranks + p->rank, rseg = (size_t)col * n_ranks + q->rank;
+                    const int64_t n = halo_n_send(q, sseg);
+                    if (n == 0) continue;
+                    cudaError_t e = cudaMemcpyAsync(halo_recv_buf(p, rseg), halo_send_buf(q, sseg),
+                                                    (size_t)q->nb * n * nf * q->real4_size(), cudaMemcpyDeviceToDevice,
+                                                    side);
+                    if (e != cudaSuccess) return e;
+                }
+        } else {
+            pbng_ctx *c = ranks[0];
+            const NcclApi &A = nccl();
+            bool any = false;
+            for (int p = 0; p < n_ranks && !any; ++p)
+                if (p != c->rank) {
+                    const size_t seg = (size_t)col * n_ranks + p;
+                    any = halo_n_send(c, seg) > 0 || halo_n_recv(c, seg) > 0;
+                }
+            if (any) {
+                ncclResult_t r = A.GroupStart();
+                for (int p = 0; p < n_ranks && r == ncclSuccess; ++p) {
+                    if (p == c->rank) continue;
+                    const size_t seg = (size_t)col * n_ranks + p;
+                    const int64_t ns = halo_n_send(c, seg), nr = halo_n_recv(c, seg);
+                    if (ns > 0)
+                        r = A.Send(halo_send_buf(c, seg), (size_t)c->nb * ns * nf * c->real4_size(), ncclUint8, p,
+                                   c->comm, side);
+                    if (r == ncclSuccess && nr > 0)
+                        r = A.Recv(halo_recv_buf(c, seg), (size_t)c->nb * nr * nf * c->real4_size(), ncclUint8, p,
+                                   c->comm, side);
+                }
+                ncclResult_t r2 = A.GroupEnd();
+                if (r == ncclSuccess) r = r2;
+                if (r != ncclSuccess) {
+                    status = nccl_fail(r, "iterate: halo exchange");
+                    return cudaErrorUnknown;
+                }
+            }
+        }
+        for (pbng_ctx *c : ranks) {
+            const int bufs[3] = {c->work, c->out, c->hist};
+            for (int p = 0; p < n_ranks; ++p) {
+                const size_t seg = (size_t)col * n_ranks + p;
+                const int64_t n = p == c->rank ? 0 : halo_n_recv(c, seg);
+                if (n == 0) continue;
+                cudaError_t e = launch_halo_unpack(c->prob, c->L, c->L.halo_recv + c->halo_recv_off[seg], n, nf, bufs,
+                                                   halo_recv_buf(c, seg), side);
+                if (e != cudaSuccess) return e;
+                ++launches;
+            }
+        }
+        return cudaSuccess;
+    }
+};
+
+// n decomposed PBNG iterations of the rank contexts `X.ranks` (PAPER.md:693-705 colour order), every
+// launch on `main` except the exchange on `side`: per colour, part 1 (halo-send vertices) of every rank
+// -> fork -> [side: pack, exchange, unpack] || [main: part 2 of every rank] -> join.  Packing reads only
+// part-1 rows and unpacking writes only ghost rows of the colour, which no vertex of the colour reads,
+// so the result is that of the serial order bit for bit (tests/test_gpu_dd.py).
+cudaError_t dd_iterations(Exchange &X, cudaStream_t main, cudaStream_t side, cudaEvent_t ev_a, cudaEvent_t ev_b,
+                          int32_t n, pbng_accel accel, double omega, double rho, double gamma, int64_t *sweeps) {
+    const int nf = accel == PBNG_ACCEL_NONE ? 1 : 3;
+    const int32_t ncol = X.ranks[0]->ncol;
+    for (int32_t it = 0; it < n; ++it) {
+        for (int32_t col = 0; col < ncol; ++col) {
+            for (pbng_ctx *c : X.ranks) {
+                cudaError_t e = sweep_colour_impl(c, col, accel, omega, rho, gamma, sweeps, 1);
+                if (e != cudaSuccess) return e;
+            }
+            cudaError_t e = cudaEventRecord(ev_a, main);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_a, 0);
+            if (e == cudaSuccess) e = X.run(col, nf, side);
+            if (e == cudaSuccess) e = cudaEventRecord(ev_b, side);
+            if (e != cudaSuccess) return e;
+            for (pbng_ctx *c : X.ranks) {
+                e = sweep_colour_impl(c, col, accel, omega, rho, gamma, sweeps, 2);
+                if (e != cudaSuccess) return e;
+            }
+            e = cudaStreamWaitEvent(main, ev_b, 0);
+            if (e != cudaSuccess) return e;
+        }
+        for (pbng_ctx *c : X.ranks) end_iteration_impl(c, accel);
+    }
+    return cudaSuccess;
+}
+
+// PBNG_DD_GRAPH=0 runs the decomposed iterations as direct launches (read per call: tests compare both)
+bool dd_graphs_enabled() {
+    const char *e = getenv("PBNG_DD_GRAPH");
+    return !(e && atoi(e) == 0);
+}
+
+// Run dd_iterations through a CUDA graph cached on `owner` (captured on the first call from a given state,
+// replayed afterwards); state = the host-side iteration state the captured launches bake in.  Falls back
+// to direct launches if the capture is refused.
+pbng_status dd_run(pbng_ctx *owner, Exchange &X, cudaStream_t main, cudaStream_t side, cudaEvent_t ev_a, cudaEvent_t ev_b,
+                   int32_t n, pbng_accel accel, double omega, double rho, double gamma, int64_t *sweeps,
+                   const char *who) {
+    pbng_ctx::GraphKey key;
+    key.n = n;
+    key.accel = (int)accel;
+    key.omega = accel == PBNG_ACCEL_SOR ? omega : 0.0;
+    key.rho = accel == PBNG_ACCEL_CHEBYSHEV ? rho : 0.0;
+    key.gamma = accel == PBNG_ACCEL_CHEBYSHEV ? gamma : 0.0;
+    key.l = owner->l;
+    key.work = owner->work;
+    key.out = owner->out;
+    key.hist = owner->hist;
+    key.hist_valid = owner->hist_valid;
+    key.ws = owner->ws;
+    key.stream = main;
+    key.inv_dt2 = owner->prob.inv_dt2;
+    for (pbng_ctx *c : X.ranks) {
+        key.gens.push_back(c->layout_gen);
+        key.gens.push_back(reinterpret_cast<uintptr_t>(c->ws));
+        key.gens.push_back((uint64_t)c->work | (uint64_t)c->l << 8);
+    }
+    const bool use_graph = dd_graphs_enabled() && owner->profiling != 1 && n > 0;
+    if (use_graph && owner->dd_graph && owner->dd_key == key) {
+        PBNG_CUDA(cudaGraphLaunch(owner->dd_graph, main), who);
+        for (int32_t it = 0; it < n; ++it)
+            for (pbng_ctx *c : X.ranks) end_iteration_impl(c, accel);
+        for (pbng_ctx *c : X.ranks) c->launches += owner->dd_graph_launches / (int64_t)X.ranks.size();
+        *sweeps += owner->dd_graph_sweeps;
+        owner->dd_graph_replays += 1;
+        return PBNG_OK;
+    }
+    if (use_graph) {
+        drop_dd_graph(owner);
+        // capture from a copy of the host state; the live state advances only when the graph is launched
+        struct Saved {
+            int work, out, hist;
+            int64_t l, launches;
+            bool hist_valid;
+            int cur_accel;
+        };
+        std::vector<Saved> saved;
+        for (pbng_ctx *c : X.ranks) saved.push_back({c->work, c->out, c->hist, c->l, c->launches, c->hist_valid, c->cur_accel});
+        const int64_t x0 = X.launches;
+        int64_t sw = 0;
+        cudaError_t e = cudaStreamBeginCapture(main, cudaStreamCaptureModeRelaxed);
+        if (e == cudaSuccess) {
+            cudaError_t ei = dd_iterations(X, main, side, ev_a, ev_b, n, accel, omega, rho, gamma, &sw);
+            cudaGraph_t graph = nullptr;
+            cudaError_t ee = cudaStreamEndCapture(main, &graph);
+            cudaGraphExec_t exec = nullptr;
+            if (ei == cudaSuccess && ee == cudaSuccess && graph)
+                e = cudaGraphInstantiate(&exec, graph, 0);
+            else
+                e = ei != cudaSuccess ? ei : (ee != cudaSuccess ? ee : cudaErrorStreamCaptureInvalidated);
+            if (graph) cudaGraphDestroy(graph);
+            int64_t launched = X.launches - x0;
+            for (size_t k = 0; k < X.ranks.size(); ++k) {
+                pbng_ctx *c = X.ranks[k];
+                launched += c->launches - saved[k].launches;
+                c->work = saved[k].work;
+                c->out = saved[k].out;
+                c->hist = saved[k].hist;
+                c->l = saved[k].l;
+                c->launches = saved[k].launches;
+                c->hist_valid = saved[k].hist_valid;
+                c->cur_accel = saved[k].cur_accel;
+            }
+            if (X.status != PBNG_OK) return X.status;
+            if (e == cudaSuccess) {
+                owner->dd_graph = exec;
+                owner->dd_key = key;
+                owner->dd_graph_launches = launched;
+                owner->dd_graph_sweeps = sw;
+                PBNG_CUDA(cudaGraphLaunch(exec, main), who);
+                for (int32_t it = 0; it < n; ++it)
+                    for (pbng_ctx *c : X.ranks) end_iteration_impl(c, accel);
+                for (pbng_ctx *c : X.ranks) c->launches += launched / (int64_t)X.ranks.size();
+                *sweeps += sw;
+                return PBNG_OK;
+            }
+            cudaGetLastError();  // capture refused: run the same launches directly
+        } else {
+            cudaGetLastError();
+        }
+    }
+    cudaError_t e = dd_iterations(X, main, side, ev_a, ev_b, n, accel, omega, rho, gamma, sweeps);
+    if (X.status != PBNG_OK) return X.status;
+    PBNG_CUDA(e, who);
+    for (pbng_ctx *c : X.ranks) c->launches += X.launches / (int64_t)X.ranks.size();
+    return PBNG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1094,6 +1430,8 @@ pbng_status pbng_set_constraints(pbng_ctx *c, const int32_t *pinned, int64_t n_p
 // colouring (greedy, or `given` -- the incremental recolouring of pbng_update_constraints) and the
 // colour-sorted device layout it implies
 static pbng_status colour_and_layout(pbng_ctx *c, const std::vector<int32_t> *given) {
+    drop_dd_graph(c);
+    c->layout_gen += 1;
     try {
         const int64_t nv = c->nv, nt = c->nt, nwc = (int64_t)c->wc.size();
         // vertex -> incident tets (ascending tet index) and vertex -> stencils (tets, then constraints)
@@ -1410,6 +1748,8 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     chk(cudaMemsetAsync(base + c->r_xt.off, 0, c->r_xt.bytes, c->stream));
     chk(cudaStreamSynchronize(c->stream));
     if (e != cudaSuccess) return cuda_fail(e, "bind_workspace");
+    drop_dd_graph(c);  // a captured iterate block holds the old layout and buffers
+    c->layout_gen += 1;
     c->ws = dptr;
     c->ws_bytes = bytes;
     c->L = L;
@@ -1493,7 +1833,21 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
         PBNG_CUDA(get_event_pair(c, span), "iterate: profiling events");
         PBNG_CUDA(cudaEventRecord(span.first, c->stream), "iterate: event");
     }
-    if (effective_schedule(c) == 2) {
+    if (c->n_ranks > 1) {
+        // decomposed: the per-colour halo exchange runs inside the library (pbng_partition's NCCL
+        // communicator); without one the caller drives the colours (pbng_sweep_colour_part + halo calls)
+        if (!c->comm)
+            return fail(PBNG_E_BAD_ORDER, "iterate: decomposed context without a transport (pbng_partition with an "
+                                          "NCCL id, pbng_group_iterate, or the colour-by-colour calls)");
+        PBNG_CUDA(ensure_dd_streams(c), "iterate: side stream");
+        Exchange X;
+        X.ranks = {c};
+        int64_t sweeps = 0;
+        st = dd_run(c, X, c->stream, c->dd_side, c->dd_ev_a, c->dd_ev_b, n_iterations, accel, omega, rho, gamma, &sweeps,
+                    "iterate: decomposed iterations");
+        if (st != PBNG_OK) return st;
+        span_launches += sweeps;
+    } else if (effective_schedule(c) == 2) {
         // pipelined: one persistent launch per kPipeMaxIter iterations, no barrier between colours
         for (int32_t it = 0; it < n_iterations; it += kPipeMaxIter) {
             PipeLaunch P;
@@ -1689,6 +2043,18 @@ pbng_status pbng_energy_residual(pbng_ctx *c, double *energy_out, double *residu
               "energy_residual: copy");
     PBNG_CUDA(cudaMemcpyAsync(&flag, c->L.flag, 4, cudaMemcpyDeviceToHost, c->stream), "energy_residual: flag");
     PBNG_CUDA(cudaStreamSynchronize(c->stream), "energy_residual: synchronize");
+    if (c->comm) {
+        // decomposed with the library's transport: global energy = sum over ranks, residual = root of the
+        // summed squares (each rank holds its owned tets / constraints / free vertices), fp64 all-reduce
+        for (int64_t b = 0; b < c->nb; ++b) res[2 * b + 1] *= res[2 * b + 1];
+        double *d = reinterpret_cast<double *>(static_cast<char *>(c->ws) + c->r_allred.off);
+        PBNG_CUDA(cudaMemcpyAsync(d, res.data(), res.size() * 8, cudaMemcpyHostToDevice, c->stream), "energy_residual: copy");
+        ncclResult_t r = nccl().AllReduce(d, d, res.size(), ncclFloat64, ncclSum, c->comm, c->stream);
+        if (r != ncclSuccess) return nccl_fail(r, "energy_residual: all-reduce");
+        PBNG_CUDA(cudaMemcpyAsync(res.data(), d, res.size() * 8, cudaMemcpyDeviceToHost, c->stream), "energy_residual: copy");
+        PBNG_CUDA(cudaStreamSynchronize(c->stream), "energy_residual: synchronize");
+        for (int64_t b = 0; b < c->nb; ++b) res[2 * b + 1] = std::sqrt(res[2 * b + 1]);
+    }
     for (int64_t b = 0; b < c->nb; ++b) {
         if (energy_out) energy_out[b] = res[2 * b];
         if (residual_out) residual_out[b] = res[2 * b + 1];
@@ -1724,6 +2090,7 @@ pbng_status pbng_query(pbng_ctx *c, pbng_info *info) {
         info->n_ghosts = c->n_local_free - c->n_free;
         info->schedule = effective_schedule(c);
     }
+    info->graph_replays = (int32_t)c->dd_graph_replays;
     return PBNG_OK;
 }
 
@@ -1923,12 +2290,146 @@ pbng_status pbng_detect_contacts(pbng_ctx *c, int32_t sample, double thickness, 
     return PBNG_OK;
 }
 
+pbng_status pbng_nccl_unique_id(void *id_out) {
+    if (!id_out) return fail(PBNG_E_INVALID_ARGUMENT, "nccl_unique_id: null output");
+    const NcclApi &A = nccl();
+    if (!A.ok) return fail(PBNG_E_NCCL, "nccl_unique_id: " + A.why);
+    ncclUniqueId id;
+    ncclResult_t r = A.GetUniqueId(&id);
+    if (r != ncclSuccess) return nccl_fail(r, "nccl_unique_id");
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+    std::memcpy(id_out, &id, sizeof(id));
+    return PBNG_OK;
+}
+
+pbng_status pbng_partition(pbng_ctx *c, const int32_t *owner, int32_t rank, int32_t n_ranks, const void *nccl_unique_id) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    if (n_ranks > 1) {
+        if (!c->on_device()) return fail(PBNG_E_NO_DEVICE, "partition: the NCCL transport needs a device context");
+        if (!nccl_unique_id) return fail(PBNG_E_INVALID_ARGUMENT, "partition: null NCCL unique id");
+        if (!nccl().ok) return fail(PBNG_E_NCCL, "partition: " + nccl().why);
+    }
+    pbng_status st = pbng_set_partition(c, owner, rank, n_ranks);
+    if (st != PBNG_OK) return st;
+    DevGuard g(c->device);
+    drop_dd_graph(c);
+    if (c->comm) {
+        nccl().CommDestroy(c->comm);
+        c->comm = nullptr;
+    }
+    if (n_ranks == 1) return PBNG_OK;
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    ncclResult_t r = nccl().CommInitRank(&comm, n_ranks, id, rank);
+    if (r != ncclSuccess) return nccl_fail(r, "partition: ncclCommInitRank");
+    c->comm = comm;
+    return PBNG_OK;
+}
+
+}  // extern "C"
+
+struct pbng_group {
+    std::vector<pbng_ctx *> ranks;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+};
+
+extern "C" {
+
+pbng_status pbng_group_create(pbng_ctx *const *ctxs, int32_t n_ranks, pbng_group **out) {
+    if (!out) return fail(PBNG_E_INVALID_ARGUMENT, "group_create: null output");
+    *out = nullptr;
+    if (!ctxs || n_ranks < 1 || n_ranks > 64) return fail(PBNG_E_INVALID_ARGUMENT, "group_create: need 1..64 contexts");
+    for (int32_t r = 0; r < n_ranks; ++r) {
+        pbng_ctx *c = ctxs[r];
+        pbng_status st = require_device(c);
+        if (st != PBNG_OK) return st;
+        if (c->n_ranks != n_ranks || c->rank != r)
+            return fail(PBNG_E_INVALID_ARGUMENT, "group_create: ctxs[r] must be rank r of an n_ranks partition");
+        if (c->comm) return fail(PBNG_E_INVALID_ARGUMENT, "group_create: context already has an NCCL transport");
+        if (!c->colored || !c->bound) return fail(PBNG_E_BAD_ORDER, "group_create: colour and bind every context first");
+        const pbng_ctx *c0 = ctxs[0];
+        if (c->device != c0->device || c->nb != c0->nb || c->dtype != c0->dtype || c->ncol != c0->ncol)
+            return fail(PBNG_E_INVALID_ARGUMENT, "group_create: contexts differ in device, batch, dtype or colouring");
+    }
+    pbng_group *g = new (std::nothrow) pbng_group();
+    if (!g) return fail(PBNG_E_OUT_OF_MEMORY, "group_create: host allocation");
+    g->ranks.assign(ctxs, ctxs + n_ranks);
+    DevGuard dg(ctxs[0]->device);
+    cudaError_t e = cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_a, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_b, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        pbng_group_destroy(g);
+        return cuda_fail(e, "group_create");
+    }
+    *out = g;
+    return PBNG_OK;
+}
+
+pbng_status pbng_group_iterate(pbng_group *g, int32_t n_iterations, pbng_accel accel, double omega, double rho,
+                               double gamma) {
+    if (!g) return fail(PBNG_E_INVALID_ARGUMENT, "group_iterate: null group");
+    if (n_iterations < 0) return fail(PBNG_E_INVALID_ARGUMENT, "group_iterate: negative iteration count");
+    pbng_ctx *c0 = g->ranks[0];
+    for (pbng_ctx *c : g->ranks) {
+        pbng_status st = check_iterate(c, accel, omega, rho, gamma, "group_iterate");
+        if (st != PBNG_OK) return st;
+        if (c->cur_accel >= 0) return fail(PBNG_E_BAD_ORDER, "group_iterate: a colour-by-colour iteration is open");
+        if (c->l != c0->l || c->work != c0->work || c->hist_valid != c0->hist_valid)
+            return fail(PBNG_E_BAD_ORDER, "group_iterate: the rank contexts are at different iterations");
+    }
+    DevGuard dg(c0->device);
+    // every rank's launches go to ctxs[0]'s stream for the duration of the call (no kernel waits for another)
+    const cudaStream_t main = c0->stream;
+    std::vector<cudaStream_t> saved;
+    for (pbng_ctx *c : g->ranks) {
+        saved.push_back(c->stream);
+        PBNG_CUDA(cudaStreamSynchronize(c->stream), "group_iterate: synchronize");
+        c->stream = main;
+    }
+    Exchange X;
+    X.ranks = g->ranks;
+    X.loopback = true;
+    int64_t sweeps = 0;
+    pbng_status st = dd_run(c0, X, main, g->side, g->ev_a, g->ev_b, n_iterations, accel, omega, rho, gamma, &sweeps,
+                            "group_iterate");
+    for (size_t k = 0; k < g->ranks.size(); ++k) g->ranks[k]->stream = saved[k];
+    if (st == PBNG_OK) {
+        cudaEvent_t done = g->ev_a;
+        PBNG_CUDA(cudaEventRecord(done, main), "group_iterate: event");
+        for (size_t k = 1; k < g->ranks.size(); ++k)
+            PBNG_CUDA(cudaStreamWaitEvent(g->ranks[k]->stream, done, 0), "group_iterate: event");
+    }
+    return st;
+}
+
+pbng_status pbng_group_destroy(pbng_group *g) {
+    if (!g) return PBNG_OK;
+    if (!g->ranks.empty()) {
+        DevGuard dg(g->ranks[0]->device);
+        if (g->side) cudaStreamSynchronize(g->side);
+        drop_dd_graph(g->ranks[0]);
+        if (g->side) cudaStreamDestroy(g->side);
+        if (g->ev_a) cudaEventDestroy(g->ev_a);
+        if (g->ev_b) cudaEventDestroy(g->ev_b);
+    }
+    delete g;
+    return PBNG_OK;
+}
+
 pbng_status pbng_destroy(pbng_ctx *c) {
     if (!c) return PBNG_OK;
     if (c->on_device()) {
         DevGuard g(c->device);
         cudaStreamSynchronize(c->stream);
         clear_l2_persistence(c);  // restore the caller's stream window and the device's persisting limit
+        drop_dd_graph(c);
+        if (c->comm) nccl().CommDestroy(c->comm);
+        if (c->dd_side) cudaStreamDestroy(c->dd_side);
+        if (c->dd_ev_a) cudaEventDestroy(c->dd_ev_a);
+        if (c->dd_ev_b) cudaEventDestroy(c->dd_ev_b);
         delete c;
     } else {
         delete c;

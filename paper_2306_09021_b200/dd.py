@@ -1,17 +1,17 @@
-"""Domain decomposition of one mesh across ranks with a halo exchange after every colour pass
-(the paper itself runs one shared-memory CPU).
+"""Domain decomposition of one mesh across ranks (the paper itself runs one
+shared-memory CPU).
 
-Each rank holds a rank-local context (`pbng_set_partition`): it sweeps its owned free vertices and keeps
-ghost copies of the vertices its stencils touch.  The colouring is global, so after colour pass k the
-only state another rank needs is the new value of the colour-k vertices it holds as ghosts: the library
-packs them (`pbng_halo_pack`), this module moves the buffers between ranks, and the library scatters them
-(`pbng_halo_unpack`).  Iterates are then bit-identical to the undecomposed run.
-
-Exchangers:
-  * TorchDistExchange -- one rank per GPU, buffers moved with torch.distributed P2P (NCCL over NVLink)
-    on the context stream; no host synchronisation inside an iteration.
-  * LoopbackExchange  -- all ranks' contexts in one process on one device (test / emulation only: plain
-    sequential device copies, no kernel ever waits for another).
+Each rank holds a rank-local context: it sweeps its owned free vertices and keeps ghost copies of the
+vertices its stencils touch.  The colouring is global, so after colour pass k the only state another rank
+needs is the new value of the colour-k vertices it holds as ghosts.  The exchange runs
+INSIDE libpbng:
+  * one rank per GPU: `pbng_partition` gives the context an NCCL communicator, and `pbng_iterate` does
+    part 1 -> (pack -> ncclSend/ncclRecv -> unpack on a side stream || part 2) per colour, captured once as
+    a CUDA graph; this module only bootstraps the NCCL unique id over torch.distributed;
+  * all ranks in one process on one GPU (tests, emulation): `Group` (pbng_group_*), the library's loopback
+    transport with device-to-device copies; no kernel ever waits for another rank's kernel.
+`serial_iterate` is the plain colour-by-colour order (sweep, pack, copy, unpack) through the public per-colour
+calls -- the reference schedule the tests compare the library's overlapped one against.
 This module is argument marshalling and data movement only; all arithmetic is in libpbng.
 """
 from __future__ import annotations
@@ -20,7 +20,7 @@ from typing import List, Optional
 
 import numpy as np
 
-from .pbng import Context, context_from_scene
+from .pbng import Context, Group, context_from_scene, nccl_unique_id as _nccl_unique_id
 
 
 def slab_partition(X: np.ndarray, n_ranks: int, axis: int = 2) -> np.ndarray:
@@ -34,129 +34,49 @@ def slab_partition(X: np.ndarray, n_ranks: int, axis: int = 2) -> np.ndarray:
     return owner
 
 
+def nccl_unique_id(pg=None, rank: int = 0, group=None) -> bytes:
+    """The 128-byte NCCL unique id for pbng_partition: created by the library on rank 0 and broadcast to
+    every rank over the torch.distributed process group `pg` (the module torch.distributed, or None for a
+    single process)."""
+    uid = _nccl_unique_id() if rank == 0 else None
+    if pg is None:
+        return uid
+    obj = [uid]
+    pg.broadcast_object_list(obj, src=0, group=group)
+    return obj[0]
+
+
 def n_fields(accel: str) -> int:
     return 1 if accel == "none" else 3
 
 
-class _Buffers:
-    def __init__(self, ctx: Context, peers: List[int], fields: int):
-        import torch
-        self.send, self.recv = {}, {}
-        dev = f"cuda:{ctx.device}"
-        for c in range(ctx.n_colours):
-            for p in peers:
-                ns, nr = ctx.halo_counts(c, p)
-                if ns:
-                    self.send[(c, p)] = torch.empty((ctx.n_batch, ns, fields, 4), dtype=ctx.torch_dtype, device=dev)
-                if nr:
-                    self.recv[(c, p)] = torch.empty((ctx.n_batch, nr, fields, 4), dtype=ctx.torch_dtype, device=dev)
-
-
-class TorchDistExchange:
-    """Per-colour halo exchange of one rank's context over a torch.distributed process group."""
-
-    def __init__(self, ctx: Context, rank: int, n_ranks: int, accel: str, group=None):
-        import torch.distributed as dist
-        self.dist = dist
-        self.ctx = ctx
-        self.rank = rank
-        self.group = group
-        self.fields = n_fields(accel)
-        self.peers = [p for p in range(n_ranks) if p != rank]
-        self.buf = _Buffers(ctx, self.peers, self.fields)
-
-    def exchange(self, colour: int):
-        dist = self.dist
-        ops = []
-        for p in self.peers:
-            sb = self.buf.send.get((colour, p))
-            if sb is not None:
-                self.ctx.halo_pack(colour, p, self.fields, sb)
-                ops.append(dist.P2POp(dist.isend, sb, p, group=self.group))
-            rb = self.buf.recv.get((colour, p))
-            if rb is not None:
-                ops.append(dist.P2POp(dist.irecv, rb, p, group=self.group))
-        if not ops:
-            return
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
-        for p in self.peers:
-            rb = self.buf.recv.get((colour, p))
-            if rb is not None:
-                self.ctx.halo_unpack(colour, p, self.fields, rb)
-
-
-class LoopbackExchange:
-    """All ranks in one process (emulation / tests): rank q's pack buffer is rank p's unpack buffer."""
-
-    def __init__(self, ctxs: List[Context], accel: str):
-        self.ctxs = ctxs
-        self.fields = n_fields(accel)
-        n = len(ctxs)
-        self.buf = [_Buffers(c, [p for p in range(n) if p != r], self.fields) for r, c in enumerate(ctxs)]
-
-    def exchange(self, colour: int):
-        n = len(self.ctxs)
-        for q in range(n):
-            for p in range(n):
-                if p != q and (colour, p) in self.buf[q].send:
-                    self.ctxs[q].halo_pack(colour, p, self.fields, self.buf[q].send[(colour, p)])
-        for p in range(n):
-            for q in range(n):
-                if p != q and (colour, q) in self.buf[p].recv:
-                    rb = self.buf[p].recv[(colour, q)]
-                    rb.copy_(self.buf[q].send[(colour, p)])
-                    self.ctxs[p].halo_unpack(colour, q, self.fields, rb)
-
-
-def iterate(ctxs: List[Context], exchanger, n: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0,
-            gamma: float = 1.0, overlap: bool = True):
-    """n PBNG iterations of a decomposed mesh: every colour pass on every local rank context, then the
-    halo exchange of that colour (PAPER.md:693-705 order), then the fused blend closes the iteration.
-
-    overlap: each colour pass is split (pbng_sweep_colour_part): the halo-send vertices first, then the
-    halo of the colour is packed, exchanged and unpacked on a side stream while the colour's remaining
-    vertices are updated on the main stream; the next colour waits for both.  Packing reads only the
-    halo-send rows and unpacking writes only ghost rows of this colour, which no vertex of this colour
-    reads, so the results are those of the serial order bit for bit."""
-    n_col = ctxs[0].n_colours
-    if not overlap:
-        for _ in range(n):
-            for c in range(n_col):
-                for ctx in ctxs:
-                    ctx.sweep_colour(c, accel, omega, rho, gamma)
-                exchanger.exchange(c)
-            for ctx in ctxs:
-                ctx.end_iteration(accel)
-        return
+def serial_iterate(ctxs: List[Context], n: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0,
+                   gamma: float = 1.0):
+    """n decomposed iterations in the plain order: every colour pass on every rank context, then the
+    colour's halo (pack, copy, unpack), then the fused blend closes the iteration.
+    Uses only the public per-colour calls; one device, all ranks in this process."""
     import torch
-    main = torch.cuda.current_stream(ctxs[0].device)
-    side = torch.cuda.Stream(ctxs[0].device)
-    boundary_done, exchange_done = torch.cuda.Event(), torch.cuda.Event()
-    saved = [ctx.stream for ctx in ctxs]
-    try:
-        for _ in range(n):
-            for c in range(n_col):
-                for ctx in ctxs:
-                    ctx.set_stream(main)
-                    ctx.sweep_colour_part(c, 1, accel, omega, rho, gamma)
-                boundary_done.record(main)
-                side.wait_event(boundary_done)
-                for ctx in ctxs:
-                    ctx.set_stream(side)
-                with torch.cuda.stream(side):
-                    exchanger.exchange(c)
-                exchange_done.record(side)
-                for ctx in ctxs:
-                    ctx.set_stream(main)
-                    ctx.sweep_colour_part(c, 2, accel, omega, rho, gamma)
-                main.wait_event(exchange_done)
+    nf = n_fields(accel)
+    world = len(ctxs)
+    dev = f"cuda:{ctxs[0].device}"
+    for _ in range(n):
+        for c in range(ctxs[0].n_colours):
             for ctx in ctxs:
-                ctx.end_iteration(accel)
-    finally:
-        for ctx, st in zip(ctxs, saved):
-            if st is not None:
-                ctx.set_stream(st)
+                ctx.sweep_colour(c, accel, omega, rho, gamma)
+            bufs = {}
+            for q, ctx in enumerate(ctxs):
+                for p in range(world):
+                    if p == q:
+                        continue
+                    ns, _ = ctx.halo_counts(c, p)
+                    if ns:
+                        b = torch.empty((ctx.n_batch, ns, nf, 4), dtype=ctx.torch_dtype, device=dev)
+                        ctx.halo_pack(c, p, nf, b)
+                        bufs[(q, p)] = b
+            for (q, p), b in bufs.items():
+                ctxs[p].halo_unpack(c, q, nf, b)
+        for ctx in ctxs:
+            ctx.end_iteration(accel)
 
 
 def combine_energy_residual(parts):
@@ -171,3 +91,7 @@ def loopback_contexts(scene, n_ranks: int, device: int = 0, dtype: Optional[str]
     owner = slab_partition(scene.X, n_ranks) if owner is None else owner
     return [context_from_scene(scene, device=device, dtype=dtype, partition=(owner, r, n_ranks))
             for r in range(n_ranks)], owner
+
+
+__all__ = ["slab_partition", "nccl_unique_id", "n_fields", "serial_iterate", "combine_energy_residual",
+           "loopback_contexts", "Group"]

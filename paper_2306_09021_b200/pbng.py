@@ -29,7 +29,8 @@ EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbn
            "pbng_last_error", "pbng_version", "pbng_sweep_colour", "pbng_end_iteration", "pbng_set_partition",
            "pbng_halo_counts", "pbng_halo_vertices", "pbng_halo_pack", "pbng_halo_unpack", "pbng_test_polar",
            "pbng_set_inertia", "pbng_set_schedule", "pbng_detect_contacts", "pbng_update_constraints",
-           "pbng_get_colours", "pbng_set_l2_persistence", "pbng_sweep_colour_part", "pbng_set_stream")
+           "pbng_get_colours", "pbng_set_l2_persistence", "pbng_sweep_colour_part", "pbng_set_stream",
+           "pbng_nccl_unique_id", "pbng_partition", "pbng_group_create", "pbng_group_iterate", "pbng_group_destroy")
 
 WC_DTYPE = np.dtype([("n0", "<i4"), ("n1", "<i4"), ("idx0", "<i4", 4), ("idx1", "<i4", 4), ("w0", "<f8", 4),
                      ("w1", "<f8", 4), ("anchor", "<f8", 3), ("K", "<f8", 6)])
@@ -49,7 +50,7 @@ class Info(C.Structure):
                 ("iteration", C.c_int64), ("kernel_launches", C.c_int64), ("sweep_bytes", C.c_double),
                 ("accel_bytes", C.c_double), ("sweep_flops", C.c_double), ("n_local_vertices", C.c_int64),
                 ("n_ghosts", C.c_int64), ("rank", C.c_int32), ("n_ranks", C.c_int32), ("schedule", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("graph_replays", C.c_int32)]
 
 
 _lib = None
@@ -97,6 +98,11 @@ def lib():
     L.pbng_set_l2_persistence.argtypes = [vp, C.c_int]
     L.pbng_sweep_colour_part.argtypes = [vp, i32, i32, C.c_int, d, d, d]
     L.pbng_set_stream.argtypes = [vp, C.c_size_t]
+    L.pbng_nccl_unique_id.argtypes = [vp]
+    L.pbng_partition.argtypes = [vp, vp, i32, i32, vp]
+    L.pbng_group_create.argtypes = [C.POINTER(vp), i32, C.POINTER(vp)]
+    L.pbng_group_iterate.argtypes = [vp, i32, C.c_int, d, d, d]
+    L.pbng_group_destroy.argtypes = [vp]
     L.pbng_last_error.restype = C.c_char_p
     L.pbng_version.restype = i32
     for name in EXPORTS:
@@ -351,6 +357,15 @@ class Context:
         self._owner = owner
         _check(lib().pbng_set_partition(self._h, _ptr(owner) if owner is not None else None, int(rank), int(n_ranks)))
 
+    def partition(self, owner, rank: int, n_ranks: int, nccl_id: Optional[bytes] = None):
+        """pbng_partition: set_partition + the library's NCCL communicator (nccl_id: the 128-byte id from
+        nccl_unique_id(), identical on every rank; collective).  pbng_iterate then exchanges the halos itself
+        and pbng_energy_residual returns global values."""
+        owner = _np(owner, np.int32).reshape(-1) if owner is not None else None
+        self._owner = owner
+        idb = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
+        _check(lib().pbng_partition(self._h, _ptr(owner) if owner is not None else None, int(rank), int(n_ranks), idb))
+
     def halo_counts(self, colour: int, peer: int):
         ns, nr = C.c_int64(), C.c_int64()
         _check(lib().pbng_halo_counts(self._h, int(colour), int(peer), C.byref(ns), C.byref(nr)))
@@ -382,6 +397,39 @@ class Context:
             pass
 
 
+def nccl_unique_id() -> bytes:
+    """pbng_nccl_unique_id: a fresh 128-byte NCCL unique id (call on one rank, share the bytes)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().pbng_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Group:
+    """pbng_group_*: the in-process loopback transport over rank contexts ctxs[r] = rank r (one device)."""
+
+    def __init__(self, ctxs):
+        self.ctxs = list(ctxs)
+        arr = (C.c_void_p * len(self.ctxs))(*[c._h for c in self.ctxs])
+        h = C.c_void_p()
+        _check(lib().pbng_group_create(arr, len(self.ctxs), C.byref(h)))
+        self._h = h
+
+    def iterate(self, n: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0, gamma: float = 1.0):
+        _check(lib().pbng_group_iterate(self._h, int(n), ACCEL[accel], float(omega), float(rho), float(gamma)))
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.pbng_group_destroy(h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def test_polar(F, dtype: str = "f32", device: int = 0) -> np.ndarray:
     """Test hook: the device polar rotation R(F) (fixed-corotated model) of a batch of 3x3 matrices."""
     F = _np(F, np.float64).reshape(-1, 3, 3)
@@ -393,13 +441,18 @@ def test_polar(F, dtype: str = "f32", device: int = 0) -> np.ndarray:
 def context_from_scene(scene, device=0, dtype: Optional[str] = None, stream=None, bind: bool = True,
                        set_positions: bool = True, partition=None, l2_persist: bool = True) -> Context:
     """Build, colour, bind and initialise a Context for a scenes.Scene (all samples of its batch).
-    partition = (owner, rank, n_ranks) builds the rank-local context of a domain decomposition;
+    partition = (owner, rank, n_ranks) builds the rank-local context of a domain decomposition (driven by
+    a Group or the colour-by-colour calls); (owner, rank, n_ranks, nccl_id) attaches the library's NCCL
+    halo transport (pbng_partition);
     l2_persist keeps the gathered position buffers L2-resident (pbng_set_l2_persistence)."""
     ctx = Context(scene.X, scene.tets, n_batch=scene.n_batch, dtype=dtype or scene.dtype, device=device, stream=stream)
     ctx.set_material(scene.model, scene.E, scene.nu, scene.density, scene.gravity)
     ctx.set_constraints(scene.pinned, scene.targets, scene.wc)
     if partition is not None:
-        ctx.set_partition(*partition)
+        if len(partition) == 4:
+            ctx.partition(*partition)
+        else:
+            ctx.set_partition(*partition)
     ctx.colours, ctx.n_colours = ctx.color()
     if bind and ctx.device >= 0:
         ctx.bind_workspace()

@@ -124,3 +124,52 @@ def test_slab_partition_aligns_with_blocks():
         owner = slab_partition(s.X, world)
         block = np.arange(s.n_vertices) // nvb
         assert np.array_equal(owner, (block // (8 // world)).astype(np.int32))
+
+
+def _uid_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2306_09021_b200 import PBNGError, context_from_scene, dd
+        uid = dd.nccl_unique_id(dist, rank)
+        # pbng_partition on a host-only context: the NCCL transport needs a device (no communicator made)
+        s = _scene("stack")
+        owner = dd.slab_partition(s.X, world)
+        ctx = context_from_scene(s, device=-1, dtype="f64")
+        try:
+            ctx.partition(owner, rank, world, uid)
+            status = 0
+        except PBNGError as e:
+            status = e.status
+        ctx.partition(None, 0, 1, None)  # n_ranks = 1 needs no id and no device
+        got = [None] * world
+        dist.all_gather_object(got, (uid, status))
+        q.put((rank, got if rank == 0 else None, None))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, None, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_nccl_unique_id_bootstrap_over_process_group(world):
+    """dd.nccl_unique_id: the library makes the id on rank 0 and torch.distributed broadcasts it, so every
+    rank passes the same 128 bytes to pbng_partition."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_uid_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, g, err = q.get(timeout=300)
+        assert err is None, err
+        res[r] = g
+    for p in procs:
+        p.join(timeout=60)
+    got = res[0]
+    uids = [g[0] for g in got]
+    assert all(len(u) == 128 for u in uids) and all(u == uids[0] for u in uids)
+    assert all(g[1] == 11 for g in got)  # PBNG_E_NO_DEVICE

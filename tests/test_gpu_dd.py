@@ -1,6 +1,12 @@
-"""Domain decomposition on one GPU (loopback emulation of G ranks in one process): the
-decomposed iterates must equal the undecomposed ones bit for bit (global colouring, same per-vertex
-arithmetic), and the rank sums of energy / residual must match the undecomposed evaluation."""
+"""Domain decomposition on one GPU: the library's loopback transport
+(pbng_group_iterate: per colour, part 1 -> side-stream pack / copy / unpack || part 2, captured once as a
+CUDA graph and replayed) runs G rank contexts in one process.  The decomposed iterates must equal the
+undecomposed ones bit for bit (global colouring, same per-vertex arithmetic), equal the plain
+colour-by-colour order of the public per-colour calls, and the rank sums of energy / residual must match
+the undecomposed evaluation.  No kernel ever waits for another rank's kernel."""
+import os
+import time
+
 import numpy as np
 import pytest
 
@@ -26,20 +32,32 @@ def single(scene, dtype):
     return x, E, R
 
 
-def decomposed(scene, dtype, world, overlap=True):
-    from paper_2306_09021_b200 import dd
-    ctxs, owner = dd.loopback_contexts(scene, world, dtype=dtype)
-    ex = dd.LoopbackExchange(ctxs, scene.accel)
-    dd.iterate(ctxs, ex, scene.iterations, scene.accel, scene.omega, scene.rho, scene.gamma, overlap=overlap)
-    E, R = dd.combine_energy_residual([c.energy_residual() for c in ctxs])
+def gather(scene, ctxs, owner):
     xs = [c.get_positions().cpu().numpy() for c in ctxs]
-    infos = [c.query() for c in ctxs]
     pinned = np.zeros(scene.n_vertices, bool)
     pinned[scene.pinned] = True
     x = xs[0].copy()
-    for r in range(world):
+    for r in range(len(ctxs)):
         rows = (owner == r) & ~pinned
         x[:, rows] = xs[r][:, rows]
+    return x
+
+
+def decomposed(scene, dtype, world, mode="group", split=None):
+    from paper_2306_09021_b200 import dd
+    ctxs, owner = dd.loopback_contexts(scene, world, dtype=dtype)
+    parts = [scene.iterations] if split is None else split
+    grp = dd.Group(ctxs) if mode == "group" else None
+    for k in parts:
+        if mode == "group":
+            grp.iterate(k, scene.accel, scene.omega, scene.rho, scene.gamma)
+        else:
+            dd.serial_iterate(ctxs, k, scene.accel, scene.omega, scene.rho, scene.gamma)
+    E, R = dd.combine_energy_residual([c.energy_residual() for c in ctxs])
+    x = gather(scene, ctxs, owner)
+    infos = [c.query() for c in ctxs]
+    if grp is not None:
+        grp.close()
     for c in ctxs:
         c.close()
     return x, E, R, infos
@@ -59,7 +77,23 @@ def test_loopback_decomposition_is_bitwise(cfg, world, dtype):
     np.testing.assert_allclose(Rd, R1, rtol=1e-9, atol=0)
 
 
-def test_full_config5_two_rank_loopback_one_iteration():
+@pytest.mark.parametrize("cfg,world", [(5, 2), (3, 3), (2, 2)])
+def test_library_schedule_equals_plain_colour_order(cfg, world):
+    """The library's overlapped, graph-captured schedule gives the bits of the plain colour-by-colour order
+    (public per-colour calls), with and without CUDA graphs, over calls that continue the state."""
+    s = G.make_config(cfg, "small")
+    xs, Es, _, _ = decomposed(s, "f32", world, mode="serial", split=[3, 2, 4])
+    xg, Eg, _, _ = decomposed(s, "f32", world, split=[3, 2, 4])
+    os.environ["PBNG_DD_GRAPH"] = "0"
+    try:
+        xe, Ee, _, _ = decomposed(s, "f32", world, split=[3, 2, 4])
+    finally:
+        del os.environ["PBNG_DD_GRAPH"]
+    assert np.array_equal(xs, xg) and np.array_equal(xs, xe)
+    assert np.array_equal(Es, Eg) and np.array_equal(Es, Ee)
+
+
+def test_full_config5_two_rank_loopback_two_iterations():
     s = G.config5_muscle_stack()
     s.iterations = 2
     x1, E1, _ = single(s, "f32")
@@ -78,10 +112,37 @@ def test_batched_sample_minor_decomposition_is_bitwise():
     np.testing.assert_allclose(Ed, E1, rtol=1e-12, atol=0)
 
 
-@pytest.mark.parametrize("cfg,world", [(5, 2), (3, 3)])
-def test_decomposition_without_overlap_is_bitwise(cfg, world):
-    """The serial exchange order (colour pass, then its exchange) gives the same bits as the overlapped one."""
-    s = G.make_config(cfg, "small")
+def test_full_config5_eight_ranks_graph_replay_bitwise_and_host_submission():
+    """Config 5 at full size over 8 loopback ranks: bitwise equal to one context; the second solve from
+    x^0 replays the captured graph (one host call per solve), and the host submission time of that call
+    is far below the GPU time of the iterations it submits."""
+    import torch
+    from paper_2306_09021_b200 import dd
+    s = G.config5_muscle_stack()
+    s.iterations = 6
     x1, E1, _ = single(s, "f32")
-    xd, Ed, _, _ = decomposed(s, "f32", world, overlap=False)
+    ctxs, owner = dd.loopback_contexts(s, 8, dtype="f32")
+    grp = dd.Group(ctxs)
+    x0 = np.asarray(s.x0)
+    for rep in range(2):
+        for c in ctxs:
+            c.set_positions(x0)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(ctxs[0].stream)
+        t = time.perf_counter()
+        grp.iterate(s.iterations, s.accel)
+        host_s = time.perf_counter() - t
+        ev1.record(ctxs[0].stream)
+        torch.cuda.synchronize()
+        gpu_s = ev0.elapsed_time(ev1) / 1e3
+    xd = gather(s, ctxs, owner)
+    replays = ctxs[0].query()["graph_replays"]
+    print(f"config5 8 loopback ranks: host submission {1e6 * host_s / s.iterations:.1f} us/iteration, "
+          f"GPU {1e6 * gpu_s / s.iterations:.1f} us/iteration, graph replays {replays}")
+    grp.close()
+    for c in ctxs:
+        c.close()
     assert np.array_equal(x1, xd)
+    assert replays >= 1
+    assert host_s < 0.5 * gpu_s

@@ -97,14 +97,14 @@ def test_backward_euler_decomposed_is_bitwise():
     s = hanging()
     xs, E, _ = gpu_steps(s, "f64", 0.01, 2, 20)
     ctxs, owner = dd.loopback_contexts(s, 2, dtype="f64")
-    ex = dd.LoopbackExchange(ctxs, "none")
+    grp = dd.Group(ctxs)
     xn = s.x0.astype(np.float64)
     xnm1 = xn.copy()
     for _ in range(2):
         for c in ctxs:
             c.set_inertia(0.01, 2 * xn - xnm1)
             c.set_positions(xn)
-        dd.iterate(ctxs, ex, 20)
+        grp.iterate(20)
         parts = [c.get_positions().cpu().numpy() for c in ctxs]
         x = parts[0].copy()
         pinned = np.zeros(s.n_vertices, bool)

@@ -64,8 +64,9 @@ def main():
     for cfg in (3, 5):
         s = G.make_config(cfg, "small")
         ctxs, _ = dd.loopback_contexts(s, 2, dtype="f32")
-        ex = dd.LoopbackExchange(ctxs, s.accel)
-        dd.iterate(ctxs, ex, 2, s.accel, s.omega, s.rho, s.gamma)
+        grp = dd.Group(ctxs)
+        grp.iterate(2, s.accel, s.omega, s.rho, s.gamma)
+        grp.close()
         torch.cuda.synchronize()
         for c in ctxs:
             c.close()
