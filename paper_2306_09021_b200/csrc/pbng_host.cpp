@@ -185,7 +185,7 @@ struct pbng_ctx {
     // in-library halo transport (pbng_partition / pbng_group_*): NCCL communicator, the side stream that
     // carries pack -> exchange -> unpack, fork/join events, and the CUDA graph of the last iterate block
     ncclComm_t comm = nullptr;
-    cudaStream_t dd_side = nullptr;
+    cudaStream_t dd_side = nullptr, dd_cap = nullptr;
     cudaEvent_t dd_ev_a = nullptr, dd_ev_b = nullptr;
     struct GraphKey {
         int32_t n = -1;
@@ -1044,6 +1044,7 @@ int64_t halo_n_recv(const pbng_ctx *c, size_t seg) { return c->halo_recv_off[seg
 cudaError_t ensure_dd_streams(pbng_ctx *c) {
     if (c->dd_side) return cudaSuccess;
     cudaError_t e = cudaStreamCreateWithFlags(&c->dd_side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->dd_cap, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->dd_ev_a, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->dd_ev_b, cudaEventDisableTiming);
     return e;
@@ -1177,9 +1178,9 @@ bool dd_graphs_enabled() {
 // Run dd_iterations through a CUDA graph cached on `owner` (captured on the first call from a given state,
 // replayed afterwards); state = the host-side iteration state the captured launches bake in.  Falls back
 // to direct launches if the capture is refused.
-pbng_status dd_run(pbng_ctx *owner, Exchange &X, cudaStream_t main, cudaStream_t side, cudaEvent_t ev_a, cudaEvent_t ev_b,
-                   int32_t n, pbng_accel accel, double omega, double rho, double gamma, int64_t *sweeps,
-                   const char *who) {
+pbng_status dd_run(pbng_ctx *owner, Exchange &X, cudaStream_t main, cudaStream_t side, cudaStream_t cap,
+                   cudaEvent_t ev_a, cudaEvent_t ev_b, int32_t n, pbng_accel accel, double omega, double rho,
+                   double gamma, int64_t *sweeps, const char *who) {
     pbng_ctx::GraphKey key;
     key.n = n;
     key.accel = (int)accel;
@@ -1222,11 +1223,25 @@ pbng_status dd_run(pbng_ctx *owner, Exchange &X, cudaStream_t main, cudaStream_t
         for (pbng_ctx *c : X.ranks) saved.push_back({c->work, c->out, c->hist, c->l, c->launches, c->hist_valid, c->cur_accel});
         const int64_t x0 = X.launches;
         int64_t sw = 0;
-        cudaError_t e = cudaStreamBeginCapture(main, cudaStreamCaptureModeRelaxed);
+        // capture on the library's own stream `cap` (the caller's may be the legacy default stream, which
+        // cannot be captured), with the caller stream's L2 access-policy window copied onto it, then launch
+        // the graph in the caller's stream order
+        cudaStreamAttrValue win;
+        std::memset(&win, 0, sizeof(win));
+        if (cudaStreamGetAttribute(main, cudaStreamAttributeAccessPolicyWindow, &win) == cudaSuccess)
+            cudaStreamSetAttribute(cap, cudaStreamAttributeAccessPolicyWindow, &win);
+        cudaGetLastError();
+        std::vector<cudaStream_t> own_streams;
+        for (pbng_ctx *c : X.ranks) {
+            own_streams.push_back(c->stream);
+            c->stream = cap;
+        }
+        cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed);
         if (e == cudaSuccess) {
-            cudaError_t ei = dd_iterations(X, main, side, ev_a, ev_b, n, accel, omega, rho, gamma, &sw);
+            cudaError_t ei = dd_iterations(X, cap, side, ev_a, ev_b, n, accel, omega, rho, gamma, &sw);
             cudaGraph_t graph = nullptr;
-            cudaError_t ee = cudaStreamEndCapture(main, &graph);
+            cudaError_t ee = cudaStreamEndCapture(cap, &graph);
+            for (size_t k = 0; k < X.ranks.size(); ++k) X.ranks[k]->stream = own_streams[k];
             cudaGraphExec_t exec = nullptr;
             if (ei == cudaSuccess && ee == cudaSuccess && graph)
                 e = cudaGraphInstantiate(&exec, graph, 0);
@@ -1260,6 +1275,7 @@ pbng_status dd_run(pbng_ctx *owner, Exchange &X, cudaStream_t main, cudaStream_t
             }
             cudaGetLastError();  // capture refused: run the same launches directly
         } else {
+            for (size_t k = 0; k < X.ranks.size(); ++k) X.ranks[k]->stream = own_streams[k];
             cudaGetLastError();
         }
     }
@@ -1843,8 +1859,8 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
         Exchange X;
         X.ranks = {c};
         int64_t sweeps = 0;
-        st = dd_run(c, X, c->stream, c->dd_side, c->dd_ev_a, c->dd_ev_b, n_iterations, accel, omega, rho, gamma, &sweeps,
-                    "iterate: decomposed iterations");
+        st = dd_run(c, X, c->stream, c->dd_side, c->dd_cap, c->dd_ev_a, c->dd_ev_b, n_iterations, accel, omega, rho,
+                    gamma, &sweeps, "iterate: decomposed iterations");
         if (st != PBNG_OK) return st;
         span_launches += sweeps;
     } else if (effective_schedule(c) == 2) {
@@ -2331,7 +2347,7 @@ pbng_status pbng_partition(pbng_ctx *c, const int32_t *owner, int32_t rank, int3
 
 struct pbng_group {
     std::vector<pbng_ctx *> ranks;
-    cudaStream_t side = nullptr;
+    cudaStream_t side = nullptr, cap = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
 };
 
@@ -2358,6 +2374,7 @@ pbng_status pbng_group_create(pbng_ctx *const *ctxs, int32_t n_ranks, pbng_group
     g->ranks.assign(ctxs, ctxs + n_ranks);
     DevGuard dg(ctxs[0]->device);
     cudaError_t e = cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->cap, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_a, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_b, cudaEventDisableTiming);
     if (e != cudaSuccess) {
@@ -2384,17 +2401,20 @@ pbng_status pbng_group_iterate(pbng_group *g, int32_t n_iterations, pbng_accel a
     // every rank's launches go to ctxs[0]'s stream for the duration of the call (no kernel waits for another)
     const cudaStream_t main = c0->stream;
     std::vector<cudaStream_t> saved;
-    for (pbng_ctx *c : g->ranks) {
+    for (pbng_ctx *c : g->ranks) {  // main first waits for the work already queued on every rank's stream
         saved.push_back(c->stream);
-        PBNG_CUDA(cudaStreamSynchronize(c->stream), "group_iterate: synchronize");
+        if (c->stream != main) {
+            PBNG_CUDA(cudaEventRecord(g->ev_b, c->stream), "group_iterate: event");
+            PBNG_CUDA(cudaStreamWaitEvent(main, g->ev_b, 0), "group_iterate: event");
+        }
         c->stream = main;
     }
     Exchange X;
     X.ranks = g->ranks;
     X.loopback = true;
     int64_t sweeps = 0;
-    pbng_status st = dd_run(c0, X, main, g->side, g->ev_a, g->ev_b, n_iterations, accel, omega, rho, gamma, &sweeps,
-                            "group_iterate");
+    pbng_status st = dd_run(c0, X, main, g->side, g->cap, g->ev_a, g->ev_b, n_iterations, accel, omega, rho, gamma,
+                            &sweeps, "group_iterate");
     for (size_t k = 0; k < g->ranks.size(); ++k) g->ranks[k]->stream = saved[k];
     if (st == PBNG_OK) {
         cudaEvent_t done = g->ev_a;
@@ -2412,6 +2432,7 @@ pbng_status pbng_group_destroy(pbng_group *g) {
         if (g->side) cudaStreamSynchronize(g->side);
         drop_dd_graph(g->ranks[0]);
         if (g->side) cudaStreamDestroy(g->side);
+        if (g->cap) cudaStreamDestroy(g->cap);
         if (g->ev_a) cudaEventDestroy(g->ev_a);
         if (g->ev_b) cudaEventDestroy(g->ev_b);
     }
@@ -2428,6 +2449,7 @@ pbng_status pbng_destroy(pbng_ctx *c) {
         drop_dd_graph(c);
         if (c->comm) nccl().CommDestroy(c->comm);
         if (c->dd_side) cudaStreamDestroy(c->dd_side);
+        if (c->dd_cap) cudaStreamDestroy(c->dd_cap);
         if (c->dd_ev_a) cudaEventDestroy(c->dd_ev_a);
         if (c->dd_ev_b) cudaEventDestroy(c->dd_ev_b);
         delete c;
