@@ -143,6 +143,10 @@ struct pbng_ctx {
     std::vector<int64_t> col_chunk;
     // host images of the device arrays (uploaded by bind)
     std::vector<int4> h_rec_id;
+    std::vector<int2> h_rec_id2;   // path-ordered NH records: {id | drop << 30, VE bits} (Problem::path)
+    std::vector<int2> h_path0;     // path-ordered NH records: per free vertex the slots S1, S2 before record 0
+    bool path_rec = false;
+    int64_t n_records = 0;         // pair records stored per sweep (path mode: incl. load-only ones)
     std::vector<unsigned char> h_rec_a, h_rec_b, h_rec_c, h_fext, h_wc_d, h_c_w, h_c_anchor, h_c_K, h_tet_a,
         h_tet_b, h_tet_c, h_targets;
     std::vector<int64_t> h_chunk_off;
@@ -171,7 +175,7 @@ struct pbng_ctx {
     Region r_rec_id, r_rec_a, r_rec_b, r_rec_c, r_chunk_off, r_chunk_v, r_deg, r_fext, r_wc_off, r_wc_cid, r_wc_d,
         r_c_n, r_c_node, r_c_w, r_c_anchor, r_c_K, r_tet_id, r_tet_a, r_tet_b, r_tet_c, r_int2orig, r_targets,
         r_x[3], r_stage, r_part_e, r_part_r, r_results, r_flag, r_halo_send, r_halo_recv, r_mass, r_xt, r_dep_off,
-        r_deps, r_pipe, r_surf, r_sv, r_chead, r_cnext, r_cres, r_cscal, r_hsend, r_hrecv, r_allred;
+        r_deps, r_pipe, r_surf, r_sv, r_chead, r_cnext, r_cres, r_cscal, r_hsend, r_hrecv, r_allred, r_path0;
     size_t ws_need = 0;
     // bound device state
     bool bound = false;
@@ -286,6 +290,144 @@ pbng_status colour_greedy(pbng_ctx *c, const std::vector<int64_t> &vs_off, const
     }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Path-ordered Neo-Hookean records.  PAPER.md:697-705 leaves each vertex free to sum its incident tets in
+// any order; the library orders them along paths in the dual graph of the vertex's link (the triangles
+// opposite the vertex, adjacent when two tets share a face through it, i.e. two of their three other
+// vertices).  Consecutive records then share two neighbours, so the kernel keeps three position slots in
+// registers and gathers ONE new neighbour per record instead of three (pbng_kernels.cu "path records").
+// Greedy Warnsdorff cover (next = the unused adjacent triangle with the fewest unused neighbours), retried
+// with seeded tie-breaking while it needs more than one path; Kuhn-grid links take one path per vertex.
+// ------------------------------------------------------------------------------------------------
+void link_paths(const std::vector<std::array<int32_t, 3>> &tri, uint32_t seed, std::vector<std::vector<int>> &best) {
+    const int n = (int)tri.size();
+    std::vector<std::vector<int>> adj(n);
+    for (int a = 0; a < n; ++a)
+        for (int b = a + 1; b < n; ++b) {
+            int sh = 0;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) sh += tri[a][i] == tri[b][j];
+            if (sh == 2) {
+                adj[a].push_back(b);
+                adj[b].push_back(a);
+            }
+        }
+    best.clear();
+    uint32_t rng = seed * 2654435761u + 12345u;
+    std::vector<char> used(n);
+    std::vector<int> free_deg(n);
+    std::vector<std::vector<int>> paths;
+    for (int trial = 0; trial < 24; ++trial) {
+        std::fill(used.begin(), used.end(), 0);
+        for (int k = 0; k < n; ++k) free_deg[k] = (int)adj[k].size();
+        paths.clear();
+        auto take = [&](int k) {
+            used[k] = 1;
+            for (int q : adj[k]) --free_deg[q];
+        };
+        auto pick = [&](const std::vector<int> &cand) {  // fewest unused neighbours; ties: first / seeded
+            int bestk = -1, bd = 1 << 30, ties = 0;
+            for (int k : cand) {
+                if (used[k]) continue;
+                if (free_deg[k] < bd) { bd = free_deg[k]; bestk = k; ties = 1; }
+                else if (free_deg[k] == bd && trial > 0) {
+                    ++ties;
+                    rng = rng * 1664525u + 1013904223u;
+                    if ((rng >> 8) % (uint32_t)ties == 0) bestk = k;
+                }
+            }
+            return bestk;
+        };
+        std::vector<int> all(n);
+        for (int k = 0; k < n; ++k) all[k] = k;
+        for (int remaining = n; remaining > 0;) {
+            int k = pick(all);
+            std::vector<int> path;
+            while (k >= 0) {
+                take(k);
+                path.push_back(k);
+                --remaining;
+                k = pick(adj[k]);
+            }
+            paths.push_back(path);
+        }
+        if (best.empty() || paths.size() < best.size()) best = paths;
+        if (best.size() <= 1) break;
+    }
+}
+
+// records of NH pair k of a vertex in path order: `tet` = index into the vertex's incident-tet list (-1:
+// load-only), `vnew` the neighbour pushed, `drop` the slot code, `slot` the slot contents after the push
+struct PathRec {
+    int tet;
+    int32_t vnew;
+    int drop;
+    int32_t slot[3];
+};
+void vertex_path_records(const std::vector<std::array<int32_t, 3>> &tri, uint32_t seed, std::vector<PathRec> &out,
+                         int32_t path0[2]) {
+    out.clear();
+    std::vector<std::vector<int>> paths;
+    link_paths(tri, seed, paths);
+    int32_t S[3] = {-1, -1, -1};
+    auto push = [&](int tet, int32_t vnew, int drop) {
+        if (drop == 2) S[2] = S[1];
+        if (drop >= 1) S[1] = S[0];
+        S[0] = vnew;
+        out.push_back({tet, vnew, drop, {S[0], S[1], S[2]}});
+    };
+    for (size_t pi = 0; pi < paths.size(); ++pi) {
+        const std::vector<int> &P = paths[pi];
+        const std::array<int32_t, 3> &t0 = tri[P[0]];
+        if (pi == 0) {  // the first triangle's other two vertices come from path0 (S1, S2 before record 0)
+            path0[0] = S[1] = t0[1];
+            path0[1] = S[2] = t0[2];
+            push(P[0], t0[0], 0);
+        } else {  // a further path: two load-only pushes, then the triangle itself
+            push(-1, t0[0], 2);
+            push(-1, t0[1], 2);
+            push(P[0], t0[2], 2);
+        }
+        for (size_t q = 1; q < P.size(); ++q) {
+            const std::array<int32_t, 3> &t = tri[P[q]];
+            int drop = -1;
+            int32_t vnew = -1;
+            for (int sl = 0; sl < 3; ++sl)
+                if (t[0] != S[sl] && t[1] != S[sl] && t[2] != S[sl]) drop = sl;
+            for (int a = 0; a < 3; ++a)
+                if (t[a] != S[0] && t[a] != S[1] && t[a] != S[2]) vnew = t[a];
+            push(P[q], vnew, drop);
+        }
+    }
+    if (paths.empty()) path0[0] = path0[1] = -1;
+}
+
+int problem_split(const pbng_ctx *c);
+bool batched_layout(const pbng_ctx *c);
+
+// PBNG_PATH=0 keeps the plain three-id NH records everywhere (experiments; fp32 NH batches then use the
+// sample-minor sh-5 layout, since sweep_batched2_kernel reads path records only)
+bool path_env() {
+    static const int env = [] {
+        const char *e = getenv("PBNG_PATH");
+        return e ? atoi(e) : 1;
+    }();
+    return env != 0;
+}
+
+int layout_lane_shift(const pbng_ctx *c) {
+    if (!batched_layout(c)) return 0;
+    return (c->dtype == DT_F32 && c->model == MODEL_NH && path_env() && c->n_local < (1 << 30)) ? 6 : 5;
+}
+
+// path-ordered NH records for the kernels that walk a vertex's records in order on one lane or one warp:
+// sweep_kernel with one warp per chunk (problem_split 1) and sweep_batched2_kernel (sh 6)
+bool use_path_records(const pbng_ctx *c) {
+    if (!path_env() || c->model != MODEL_NH || c->n_local >= (1 << 30)) return false;
+    const int sh = layout_lane_shift(c);
+    return sh == 6 || (sh == 0 && problem_split(c) == 1);
+}
+
 template <class R>
 void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::vector<int32_t> &vt) {
     const int64_t nv = c->nv, nb = c->nb;
@@ -294,12 +436,35 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     const double clam = c->nu / ((1.0 + c->nu) * (1.0 - 2.0 * c->nu));
     auto Ee = [&](int64_t e) { return c->E.size() == 1 ? c->E[0] : c->E[(size_t)e]; };
 
-    // chunks and degrees
+    // chunks and degrees (path-ordered NH records: records per vertex incl. load-only ones)
+    c->path_rec = use_path_records(c);
     c->col_chunk.assign(c->ncol + 1, 0);
     c->h_deg.assign(c->n_free, 0);
+    std::vector<std::array<int32_t, 3>> link;
+    std::vector<PathRec> prec;
+    auto vertex_link = [&](int32_t o) {  // the three other vertices of each incident tet, in vt order
+        link.clear();
+        for (int64_t q = vt_off[o]; q < vt_off[o + 1]; ++q) {
+            const int32_t *t = c->tets.data() + 4 * vt[q];
+            std::array<int32_t, 3> tr;
+            int m = 0;
+            for (int sl = 0; sl < 4; ++sl)
+                if (t[sl] != o) tr[m++] = t[sl];
+            link.push_back(tr);
+        }
+    };
+    if (c->path_rec) c->h_path0.assign((size_t)std::max<int64_t>(c->n_free, 1), make_int2(0, 0));
     for (int64_t i = 0; i < c->n_free; ++i) {
         const int32_t o = c->int2orig[i];
-        c->h_deg[i] = (int32_t)(vt_off[o + 1] - vt_off[o]);
+        if (c->path_rec) {
+            vertex_link(o);
+            int32_t p0[2];
+            vertex_path_records(link, (uint32_t)o, prec, p0);
+            c->h_deg[i] = (int32_t)prec.size();
+            c->h_path0[i] = prec.empty() ? make_int2((int32_t)i, (int32_t)i) : make_int2(c->orig2int[p0[0]], c->orig2int[p0[1]]);
+        } else {
+            c->h_deg[i] = (int32_t)(vt_off[o + 1] - vt_off[o]);
+        }
     }
     c->h_chunk_off.clear();
     c->h_chunk_v.clear();
@@ -328,11 +493,17 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     c->n_chunks = n_chunks;
     c->n_slots = c->h_chunk_off.back();
     c->n_pairs = 0;
-    for (int64_t i = 0; i < c->n_free; ++i) c->n_pairs += c->h_deg[i];
+    c->n_records = 0;
+    for (int64_t i = 0; i < c->n_free; ++i) {
+        const int32_t o = c->int2orig[i];
+        c->n_pairs += vt_off[o + 1] - vt_off[o];
+        c->n_records += c->h_deg[i];
+    }
 
     // pair records
     const int64_t ns = std::max<int64_t>(c->n_slots, 1);
-    c->h_rec_id.assign((size_t)ns, make_int4(0, 0, 0, 0));
+    c->h_rec_id.assign(c->path_rec ? 1 : (size_t)ns, make_int4(0, 0, 0, 0));
+    c->h_rec_id2.assign(c->path_rec ? (size_t)ns : 1, make_int2(0, 0));
     c->h_rec_a.assign((size_t)ns * s4, 0);
     const bool nh = c->model == MODEL_NH;
     c->h_rec_b.assign(nh ? s4 : (size_t)ns * s4, 0);  // NH: unused
@@ -343,6 +514,57 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
         const int2 cv = c->h_chunk_v[ch];
         for (int32_t lane = 0; lane < cv.y; ++lane) {
             const int32_t vi = cv.x + lane, o = c->int2orig[vi];
+            if (c->path_rec) {
+                // path-ordered records: slot order (S0, S1, S2) after the push; s'_k and det B' follow the
+                // slots (det B' = sgn(pi) det B keeps J and cof(F) g_i, pbng_kernels.cu "path records")
+                vertex_link(o);
+                int32_t p0[2];
+                vertex_path_records(link, (uint32_t)o, prec, p0);
+                for (size_t k = 0; k < prec.size(); ++k) {
+                    const PathRec &pr = prec[k];
+                    const int64_t r = c->h_chunk_off[ch] + (int64_t)k * kChunk + lane;
+                    const int32_t code = c->orig2int[pr.vnew] | (pr.drop << 30);
+                    if (pr.tet < 0) {  // load-only: VE = 0 and zero rest data contribute exactly 0
+                        c->h_rec_id2[r] = make_int2(code, 0);
+                        put4<R>(c->h_rec_a, r, 0.0, 0.0, 0.0, 0.0);
+                        if (c->dtype == DT_F64) put1<R>(c->h_rec_c, r, 0.0);
+                        continue;
+                    }
+                    const int64_t e = vt[vt_off[o] + pr.tet];
+                    const int32_t *t = c->tets.data() + 4 * e;
+                    int a = 0;
+                    while (t[a] != o) ++a;
+                    int32_t oid[3];
+                    double g[3][3], gi[3], sj[3];
+                    int m = 0;
+                    for (int sl = 0; sl < 4; ++sl) {
+                        if (sl == a) continue;
+                        oid[m] = t[sl];
+                        shape_grad(c, e, sl, g[m]);
+                        ++m;
+                    }
+                    shape_grad(c, e, a, gi);
+                    for (int q2 = 0; q2 < 3; ++q2) sj[q2] = g[q2][0] * gi[0] + g[q2][1] * gi[1] + g[q2][2] * gi[2];
+                    const double Bp[9] = {g[0][0], g[0][1], g[0][2], g[1][0], g[1][1], g[1][2], g[2][0], g[2][1], g[2][2]};
+                    int pi[3];
+                    for (int k2 = 0; k2 < 3; ++k2) {
+                        pi[k2] = 0;
+                        while (oid[pi[k2]] != pr.slot[k2]) ++pi[k2];
+                    }
+                    const int inv = (pi[0] > pi[1]) + (pi[0] > pi[2]) + (pi[1] > pi[2]);
+                    const double sgn = (inv & 1) ? -1.0 : 1.0;
+                    const double VE = c->V[e] * Ee(e);
+                    int2 id = make_int2(code, 0);
+                    if (c->dtype == DT_F32) {
+                        const float vf = (float)VE;
+                        std::memcpy(&id.y, &vf, 4);
+                    }
+                    c->h_rec_id2[r] = id;
+                    put4<R>(c->h_rec_a, r, sj[pi[0]], sj[pi[1]], sj[pi[2]], sgn * det3(Bp));
+                    if (c->dtype == DT_F64) put1<R>(c->h_rec_c, r, VE);
+                }
+                continue;
+            }
             int k = 0;
             for (int64_t q = vt_off[o]; q < vt_off[o + 1]; ++q, ++k) {
                 const int64_t e = vt[q];
@@ -496,7 +718,10 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     p.n_chunks = n_chunks;
     p.n_batch = c->nb;
     p.x_stride = (int64_t)align_up((size_t)std::max<int64_t>(c->n_local, 1), 64);
-    p.lane_shift = batched_layout(c) ? 5 : 0;
+    // batched layouts: fp32 Neo-Hookean -> the component-interleaved two-sample layout of
+    // sweep_batched2_kernel (sh 6), otherwise sample-minor groups of 32 (sh 5)
+    p.lane_shift = layout_lane_shift(c);
+    p.path = c->path_rec;
     p.cmu = cmu;
     p.clam = clam;
     for (int k = 0; k < 3; ++k) p.rho_g[k] = c->density * c->grav[k];
@@ -699,7 +924,9 @@ std::vector<int32_t> distinct_nodes(const pbng_weak_constraint &w) {
     return n;
 }
 
-bool pipeline_available(const pbng_ctx *c) { return c->n_ranks == 1 && c->prob.lane_shift == 0 && c->n_chunks > 0; }
+bool pipeline_available(const pbng_ctx *c) {
+    return c->n_ranks == 1 && c->prob.lane_shift == 0 && c->n_chunks > 0 && !c->path_rec;
+}
 
 int problem_split(const pbng_ctx *c);
 
@@ -733,7 +960,8 @@ void plan_workspace(pbng_ctx *c) {
     const Problem &p = c->prob;
     const size_t s = c->real_size(), s4 = c->real4_size();
     const int64_t ns = std::max<int64_t>(c->n_slots, 1);
-    take(c->r_rec_id, (size_t)ns * 16);
+    take(c->r_rec_id, (size_t)ns * (c->path_rec ? 8 : 16));
+    take(c->r_path0, c->h_path0.size() * 8);
     take(c->r_rec_a, (size_t)ns * s4);
     take(c->r_rec_b, c->h_rec_b.size());
     take(c->r_rec_c, c->h_rec_c.size());
@@ -790,8 +1018,12 @@ double sweep_bytes_model(const pbng_ctx *c) {
     // samples of a batch), chunk offsets, per free vertex and sample: degree, position write, blend
     // traffic (x^{l-1} read, x^{l-1} and x^{l+1} writes) and body force; all positions read once.
     const double s = (double)c->real_size();
-    const double rec = c->model == MODEL_NH ? (c->dtype == DT_F64 ? 56.0 : 32.0) : (c->dtype == DT_F64 ? 96.0 : 52.0);
-    double b = (double)c->n_pairs * rec + (double)(c->n_chunks + 1) * 8.0 + (double)c->n_free * 4.0;
+    // path-ordered NH records: {id | drop, VE} + {s'_0..2, det B'} = 24 B (fp32) / 48 B (fp64) per record
+    // (load-only ones included) + the per-vertex first slots (8 B)
+    const double rec = c->path_rec ? (c->dtype == DT_F64 ? 48.0 : 24.0)
+                       : c->model == MODEL_NH ? (c->dtype == DT_F64 ? 56.0 : 32.0) : (c->dtype == DT_F64 ? 96.0 : 52.0);
+    double b = (double)(c->path_rec ? c->n_records : c->n_pairs) * rec + (double)(c->n_chunks + 1) * 8.0 +
+               (double)c->n_free * (c->path_rec ? 12.0 : 4.0);
     double per_v = 3 * s;  // write x_PBNG
     per_v += (c->prob.has_fext ? 3 * s : 0);
     b += (double)c->nb * ((double)c->n_free * per_v + (double)c->n_local * 3 * s);
@@ -897,6 +1129,9 @@ cudaError_t sweep_colour_impl(pbng_ctx *c, int32_t col, pbng_accel accel, double
         s.gamma = gamma;
     }
     s.split = problem_split(c);
+    // consecutive colour launches of a batched context walk the sample-group pairs in opposite orders, so
+    // a launch starts on the groups whose positions the previous one left in L2
+    s.reverse = col & 1;
     const int32_t ns = c->col_nsend[col];
     for (int p = 1; p <= 2; ++p) {
         if (part != 0 && part != p) continue;
@@ -1682,6 +1917,7 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     L.n_vertices = c->n_local;
     L.n_slots = c->n_slots;
     L.rec_id = static_cast<const int4 *>(at(c->r_rec_id));
+    L.path0 = static_cast<const int2 *>(at(c->r_path0));
     L.rec_a = at(c->r_rec_a);
     L.rec_b = at(c->r_rec_b);
     L.rec_c = at(c->r_rec_c);
@@ -1729,7 +1965,9 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     };
     cudaError_t e = cudaSuccess;
     auto chk = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
-    chk(up(c->r_rec_id, c->h_rec_id.data(), c->h_rec_id.size() * 16));
+    if (c->path_rec) chk(up(c->r_rec_id, c->h_rec_id2.data(), c->h_rec_id2.size() * 8));
+    else chk(up(c->r_rec_id, c->h_rec_id.data(), c->h_rec_id.size() * 16));
+    chk(up(c->r_path0, c->h_path0.data(), c->h_path0.size() * 8));
     chk(up(c->r_rec_a, c->h_rec_a.data(), c->h_rec_a.size()));
     chk(up(c->r_rec_b, c->h_rec_b.data(), c->h_rec_b.size()));
     chk(up(c->r_rec_c, c->h_rec_c.data(), c->h_rec_c.size()));

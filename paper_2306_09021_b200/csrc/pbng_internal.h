@@ -46,7 +46,8 @@ struct Layout {
     const void *rec_a = nullptr, *rec_b = nullptr, *rec_c = nullptr;
     const int64_t *chunk_off = nullptr;  // [n_chunks + 1]
     const int2 *chunk_v = nullptr;       // [n_chunks] {first internal vertex, vertices in chunk}
-    const int32_t *deg = nullptr;        // [n_free]
+    const int32_t *deg = nullptr;        // [n_free] records per vertex
+    const int2 *path0 = nullptr;         // [n_free] path mode: slots S1, S2 before the vertex's first record
     const void *fext = nullptr;          // Real4 [n_free] or null (no body force)
     // weak constraints: per free vertex CSR of (constraint id, w0_i - w1_i) in input order
     const int32_t *wc_off = nullptr;     // [n_free + 1]
@@ -106,6 +107,7 @@ struct Problem {
     double inv_dt2 = 0;    // backward Euler 1/dt^2 (0: quasistatic)
     int64_t n_surf = 0, n_sv = 0, n_cbuckets = 1;  // contact detection sizes
     int device = 0, sm_count = 0;  // the context's CUDA device and its SM count (queried at bind)
+    bool path = false;  // Neo-Hookean pair records in path order (pbng_kernels.cu "path records")
 };
 
 constexpr int kMaxDevices = 64;  // per-device launch caches (pbng_kernels.cu) are indexed by ordinal
@@ -117,6 +119,7 @@ struct SweepLaunch {
     int accel = ACCEL_NONE;
     double omega = 1, gamma = 1;  // SOR omega, or Chebyshev omega_{l+1} and gamma
     int split = 1;  // warps sharing one 32-vertex chunk (1, 2, 4 or 8)
+    int reverse = 0;  // batched sh-6 launches: walk the sample-group pairs last to first (odd colours)
 };
 
 // one launch of the pipelined schedule: n_iter <= kPipeMaxIter whole iterations; iteration l (0-based

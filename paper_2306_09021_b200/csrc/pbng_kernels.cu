@@ -47,6 +47,7 @@ __device__ __forceinline__ int64_t ld(const int64_t *p) {
 __device__ __forceinline__ int4 ld(const int4 *p) { return __ldg(p); }
 __device__ __forceinline__ int2 ld(const int2 *p) { return __ldg(p); }
 __device__ __forceinline__ float4 ld(const float4 *p) { return __ldg(p); }
+__device__ __forceinline__ float2 ld(const float2 *p) { return __ldg(p); }
 __device__ __forceinline__ double2 ld(const double2 *p) { return __ldg(p); }
 __device__ __forceinline__ double4 ld(const double4 *p) {
     const double2 *q = reinterpret_cast<const double2 *>(p);
@@ -74,6 +75,39 @@ __device__ __forceinline__ double rsq(double x) { return rsqrt(x); }
 template <class R> __device__ __forceinline__ typename RT<R>::R4 mk4(R x, R y, R z);
 template <> __device__ __forceinline__ float4 mk4<float>(float x, float y, float z) { return make_float4(x, y, z, 0.f); }
 template <> __device__ __forceinline__ double4 mk4<double>(double x, double y, double z) { return make_double4(x, y, z, 0.0); }
+
+// element index of (sample b, vertex v): samples grouped by 2^sh lanes, sample-minor inside a group
+// (sh = 0: [n_batch][x_stride]; sh = 5: [n_batch/32][x_stride][32])
+__device__ __forceinline__ int64_t pos_index(int64_t b, int64_t v, int64_t xs, int sh) {
+    return (((b >> sh) * xs + v) << sh) + (b & ((1 << sh) - 1));
+}
+// sh = 6 (fp32 Neo-Hookean batches, sweep_batched2_kernel): [n_batch/64][x_stride][32 lanes][8 floats];
+// lane l of group pair gp holds samples 64 gp + l (q = 0) and 64 gp + 32 + l (q = 1) component-
+// interleaved as {x0 x1 y0 y1 z0 z1 0 0}, so that one 16 B + one 8 B load give the packed FP32x2
+// operands of both samples.  Float index of sample b's x at vertex v (y at +2, z at +4):
+__device__ __forceinline__ int64_t pos6_elem(int64_t b, int64_t v, int64_t xs) {
+    return (((((b >> 6) * xs + v) << 5) + (b & 31)) << 3) + ((b >> 5) & 1);
+}
+// position of (sample b, vertex v) in a position-layout buffer, any layout (the w slot reads as 0)
+template <class R>
+__device__ __forceinline__ typename RT<R>::R4 pos_load(const void *buf, int64_t b, int64_t v, int64_t xs, int sh) {
+    if (sh == 6) {
+        const R *q = reinterpret_cast<const R *>(buf) + pos6_elem(b, v, xs);
+        return mk4<R>(q[0], q[2], q[4]);
+    }
+    return reinterpret_cast<const typename RT<R>::R4 *>(buf)[pos_index(b, v, xs, sh)];
+}
+template <class R>
+__device__ __forceinline__ void pos_store(void *buf, int64_t b, int64_t v, int64_t xs, int sh,
+                                          const typename RT<R>::R4 &x) {
+    if (sh == 6) {
+        R *q = reinterpret_cast<R *>(buf) + pos6_elem(b, v, xs);
+        q[0] = x.x; q[2] = x.y; q[4] = x.z;
+        return;
+    }
+    reinterpret_cast<typename RT<R>::R4 *>(buf)[pos_index(b, v, xs, sh)] = x;
+}
+
 
 // packed FP32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2: two fp32 operations per lane per instruction,
 // each rounded as the scalar operation)
@@ -434,6 +468,15 @@ __device__ __forceinline__ double2 lds(const double2 *p) {
     return __ldg(p);
 #endif
 }
+__device__ __forceinline__ int2 lds(const int2 *p) {
+#if PBNG_REC_HINT
+    int2 r;
+    asm("ld.global.nc.L1::no_allocate.v2.s32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+#else
+    return __ldg(p);
+#endif
+}
 __device__ __forceinline__ double4 lds(const double4 *p) {
     const double2 *q = reinterpret_cast<const double2 *>(p);
     const double2 a = lds(q), b = lds(q + 1);
@@ -552,6 +595,53 @@ __device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<doubl
 
 // L2 prefetch of a later record of the stream (no registers held while it is in flight)
 __device__ __forceinline__ void pf_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// ------------------------------------------------------------------------------------------------
+// Path records (Problem::path, Neo-Hookean; host: vertex_path_records).  A vertex's records follow paths
+// in the dual graph of its link, so consecutive records share two of their three neighbours.  The kernels
+// keep three position slots and each record pushes ONE new neighbour:
+//     drop 2: S2 <- S1;   drop >= 1: S1 <- S0;   S0 <- x_new      (drop = the slot whose content leaves)
+// and (d_1, d_2, d_3) = (S0, S1, S2) - x_i with the record's s'_0..2 and det B' in that slot order.  A
+// relabelling pi of the three neighbours flips n = (d_2 - d_1) x (d_3 - d_1) by sgn(pi) and leaves
+// d_j . n unchanged, so det B' = sgn(pi) det B keeps J and cof(F) g_i exact.  Before record 0 the slots
+// S1, S2 hold path0[v].  Load-only records (VE = 0, zero s' and det B') start further paths and add
+// exactly 0.  fp32: rec_id = int2 {id | drop << 30, VE bits}, rec_a float4 {s'_0 s'_1 s'_2 det B'} = 24 B;
+// fp64: int2 {id | drop << 30, 0}, double4, rec_c VE = 48 B.
+// ------------------------------------------------------------------------------------------------
+template <bool STREAM>
+__device__ __forceinline__ int load_path_rec(const Layout &L, int64_t r, Pair<float, MODEL_NH> &p) {
+    const int2 *ip = reinterpret_cast<const int2 *>(L.rec_id) + r;
+    const float4 *a = reinterpret_cast<const float4 *>(L.rec_a) + r;
+    const int2 id = STREAM ? lds(ip) : ld(ip);
+    const float4 x = STREAM ? lds(a) : ld(a);
+    p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
+    p.VE = __int_as_float(id.y);
+    PBNG_CHECK(r >= 0 && r < L.n_slots && (id.x & 0x3fffffff) < L.n_vertices);
+    return id.x;
+}
+template <bool STREAM>
+__device__ __forceinline__ int load_path_rec(const Layout &L, int64_t r, Pair<double, MODEL_NH> &p) {
+    const int2 *ip = reinterpret_cast<const int2 *>(L.rec_id) + r;
+    const double4 *a = reinterpret_cast<const double4 *>(L.rec_a) + r;
+    const int2 id = STREAM ? lds(ip) : ld(ip);
+    const double4 x = STREAM ? lds(a) : ld(a);
+    p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
+    p.VE = ld(reinterpret_cast<const double *>(L.rec_c) + r);
+    PBNG_CHECK(r >= 0 && r < L.n_slots && (id.x & 0x3fffffff) < L.n_vertices);
+    return id.x;
+}
+template <class T>
+__device__ __forceinline__ void path_push(T &S0, T &S1, T &S2, const T &nw, const int code) {
+    const int drop = (int)((unsigned)code >> 30);
+    S2 = drop == 2 ? S1 : S2;
+    S1 = drop >= 1 ? S0 : S1;
+    S0 = nw;
+}
+template <class R>
+__device__ __forceinline__ void prefetch_path(const Layout &L, int64_t r) {
+    pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + r);
+    pf_l2(reinterpret_cast<const typename RT<R>::R4 *>(L.rec_a) + r);
+}
+
 template <class R, int MODEL>
 __device__ __forceinline__ void prefetch_pair(const Layout &L, int64_t r) {
     pf_l2(L.rec_id + r);
@@ -710,9 +800,10 @@ __device__ __forceinline__ void inertia_contrib(const Layout &L, int v, const ty
 }
 
 // weak-constraint terms for vertex v: f -= d K C_c, A += d^2 K
-template <class R, class T, bool HESS, int G = GATHER_NC>
-__device__ __forceinline__ void wc_contrib(const Layout &L, const typename RT<R>::R4 *x, const int sh, int v,
-                                           const T (&xa)[3], T (&f)[3], T (&A)[6]) {
+// (gat(node) returns another node's position)
+template <class R, class T, bool HESS, class Gat>
+__device__ __forceinline__ void wc_terms(const Layout &L, const Gat &gat, int v, const T (&xa)[3], T (&f)[3],
+                                         T (&A)[6]) {
     using R4 = typename RT<R>::R4;
     const int e0 = ld(L.wc_off + v), e1 = ld(L.wc_off + v + 1);
     for (int e = e0; e < e1; ++e) {
@@ -727,7 +818,7 @@ __device__ __forceinline__ void wc_contrib(const Layout &L, const typename RT<R>
             if (node == v) {
                 C[0] += w * xa[0]; C[1] += w * xa[1]; C[2] += w * xa[2];
             } else {
-                const R4 y = gather<G>(x + ((int64_t)node << sh));
+                const R4 y = gat(node);
                 C[0] += w * T(y.x); C[1] += w * T(y.y); C[2] += w * T(y.z);
             }
         }
@@ -743,6 +834,17 @@ __device__ __forceinline__ void wc_contrib(const Layout &L, const typename RT<R>
             A[3] += d2 * kxy; A[4] += d2 * kyz; A[5] += d2 * kxz;
         }
     }
+}
+template <class R, class T, bool HESS, int G = GATHER_NC>
+__device__ __forceinline__ void wc_contrib(const Layout &L, const typename RT<R>::R4 *x, const int sh, int v,
+                                           const T (&xa)[3], T (&f)[3], T (&A)[6]) {
+    wc_terms<R, T, HESS>(L, [&](int node) { return gather<G>(x + ((int64_t)node << sh)); }, v, xa, f, A);
+}
+// the same terms with positions read through the layout accessor (sample b of any position layout)
+template <class R, class T, bool HESS>
+__device__ __forceinline__ void wc_contrib_at(const Layout &L, const void *buf, int64_t b, int64_t xs, int sh, int v,
+                                              const T (&xa)[3], T (&f)[3], T (&A)[6]) {
+    wc_terms<R, T, HESS>(L, [&](int node) { return pos_load<R>(buf, b, node, xs, sh); }, v, xa, f, A);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -865,6 +967,41 @@ __device__ __forceinline__ void update_vertex(const Layout &L, typename RT<R>::R
     finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
 }
 
+// update_vertex for path records (Neo-Hookean, Problem::path): one neighbour gather per record
+template <class R, int ACCEL, bool FEXT, bool WC, int G>
+__device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<R>::R4 *__restrict__ work,
+                                                   const int64_t xs, const int v, const int64_t base, const int deg,
+                                                   const int oi, const int hi, const R cmu, const R clam,
+                                                   const R omega, const R gamma, const R idt2) {
+    using R4 = typename RT<R>::R4;
+    const R4 xa4 = work[v];
+    const R xa[3] = {xa4.x, xa4.y, xa4.z};
+    R f[3] = {R(0), R(0), R(0)};
+    if (FEXT) {
+        const R4 fe = ld(reinterpret_cast<const R4 *>(L.fext) + v);
+        f[0] = fe.x; f[1] = fe.y; f[2] = fe.z;
+    }
+    R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
+    const int2 p0 = ld(L.path0 + v);
+    R4 S0 = xa4, S1 = gather<G>(work + p0.x), S2 = gather<G>(work + p0.y);
+#pragma unroll kSweepUnroll
+    for (int k = 0; k < deg; ++k) {
+        if (kSweepPrefetch > 0 && k + kSweepPrefetch < deg) prefetch_path<R>(L, base + (int64_t)(k + kSweepPrefetch) * kChunk);
+        Pair<R, MODEL_NH> pr;
+        const int code = load_path_rec<true>(L, base + (int64_t)k * kChunk, pr);
+        const R4 nw = gather<G>(work + (code & 0x3fffffff));
+        path_push(S0, S1, S2, nw, code);
+        R d1[3], d2[3], d3[3];
+        sub3<R>(S0, xa, d1);
+        sub3<R>(S1, xa, d2);
+        sub3<R>(S2, xa, d3);
+        contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
+    }
+    if (WC) wc_contrib<R, R, true, G>(L, work, 0, v, xa, f, A);
+    if (idt2 > R(0)) inertia_contrib<R, R>(L, v, ld(reinterpret_cast<const R4 *>(L.xtilde) + xs + v), idt2, xa, f, A);
+    finish_vertex<R, ACCEL>(L, work, xs, v, oi, hi, xa4, f, A, omega, gamma);
+}
+
 #ifndef PBNG_SWEEP_TMA
 #define PBNG_SWEEP_TMA 0
 #endif
@@ -899,7 +1036,7 @@ template <class R, int MODEL> struct StageSmem {  // per warp: [ring][kGroups mb
 // (TMA), one mbarrier per group: HBM latency is hidden without holding registers, and the lanes only
 // gather their neighbour positions (through L1; they belong to other colours, read-only in this
 // launch).  The per-vertex summation order is ascending tet index, as in the oracle.
-template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, bool ONE_WAVE = false>
+template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, bool ONE_WAVE = false, bool PATH = false>
 __global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : SweepMinBlocks<R>::n)) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
                                                             const int64_t chunk_begin, const int64_t x_stride,
                                                             const int wi, const int oi, const int hi, const R cmu,
@@ -916,13 +1053,20 @@ __global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : 
         const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
         const int deg = ld(L.deg + v);
         if (kPdl) {
-            for (int k = 0; k < kSweepPrefetch && k < deg; ++k) prefetch_pair<R, MODEL>(L, base + (int64_t)k * kChunk);
+            for (int k = 0; k < kSweepPrefetch && k < deg; ++k) {
+                if constexpr (PATH) prefetch_path<R>(L, base + (int64_t)k * kChunk);
+                else prefetch_pair<R, MODEL>(L, base + (int64_t)k * kChunk);
+            }
             asm volatile("griddepcontrol.wait;" ::: "memory");
         }
         const int64_t xs = (int64_t)blockIdx.y * x_stride;
         R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
-        update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_NC>(L, work, xs, v, base, deg, oi, hi, cmu, clam, omega,
-                                                            gamma, idt2);
+        if constexpr (PATH && MODEL == MODEL_NH)
+            update_vertex_path<R, ACCEL, FEXT, WC, GATHER_NC>(L, work, xs, v, base, deg, oi, hi, cmu, clam, omega,
+                                                              gamma, idt2);
+        else
+            update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_NC>(L, work, xs, v, base, deg, oi, hi, cmu, clam, omega,
+                                                                gamma, idt2);
         return;
     }
     using F = RecFmt<R, MODEL>;
@@ -1310,8 +1454,46 @@ __device__ __forceinline__ void contrib_nh2(const float2 (&d1)[3], const float2 
 }
 
 #ifndef PBNG_B2_MINB
-#define PBNG_B2_MINB 1
+#define PBNG_B2_MINB 5  // path records + difference slots: 96 registers / 20 warps per SM measured best (1.153 ms per config-4 iteration; 1: 1.179, 4: 1.208)
 #endif
+#ifndef PBNG_B2_UNROLL
+#define PBNG_B2_UNROLL 2
+#endif
+constexpr int kB2Unroll = PBNG_B2_UNROLL;
+#ifndef PBNG_B2_PF
+#define PBNG_B2_PF 4
+#endif
+constexpr int kB2Prefetch = PBNG_B2_PF;  // records ahead whose neighbour slot is prefetched into L1 (0: off)
+__device__ __forceinline__ void pf_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+// the packed positions of a lane's two samples at one vertex (sh 6 slot {x0 x1 y0 y1 | z0 z1 . .})
+struct P6 {
+    float2 x, y, z;
+};
+__device__ __forceinline__ P6 ld_p6(const float *p) {
+    const float4 a = ld(reinterpret_cast<const float4 *>(p));
+    const float2 b = ld(reinterpret_cast<const float2 *>(p + 4));
+    return {make_float2(a.x, a.y), make_float2(a.z, a.w), b};
+}
+
+// dx = A^{-1} f by the same register Cholesky as finish_vertex
+__device__ __forceinline__ void chol_solve3(const float (&A)[6], const float (&f)[3], float (&x)[3]) {
+    const float i00 = rsq(A[0]);
+    const float l10 = A[3] * i00, l20 = A[5] * i00;
+    const float i11 = rsq(A[1] - l10 * l10);
+    const float l21 = (A[4] - l20 * l10) * i11;
+    const float i22 = rsq(A[2] - l20 * l20 - l21 * l21);
+    const float z0 = f[0] * i00;
+    const float z1 = (f[1] - l10 * z0) * i11;
+    const float z2 = (f[2] - l20 * z0 - l21 * z1) * i22;
+    x[2] = z2 * i22;
+    x[1] = (z1 - l21 * x[2]) * i11;
+    x[0] = (z0 - l10 * x[1] - l20 * x[2]) * i00;
+}
+
+// Position layout sh = 6 (pos6_elem): the lane's 32 B slot of vertex u in group pair gp starts at float
+// ((gp * x_stride + u) << 8) + 8 lane and holds {x0 x1 y0 y1 | z0 z1 . .} -- the packed operands of its
+// two samples, loaded with one LDG.128 + one LDG.64 (no repacking moves).  The warp's records are staged
+// in shared memory (lane k stores record k) and read back as warp-broadcast LDS.128 pairs.
 template <int ACCEL, bool FEXT, bool WC>
 __global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_kernel(const Layout L, const int32_t v_begin,
                                                                      const int32_t n_v, const int64_t chunk_begin,
@@ -1319,71 +1501,122 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_kern
                                                                      const int wi, const int oi, const int hi,
                                                                      const float cmu, const float clam,
                                                                      const float omega, const float gamma,
-                                                                     const float idt2) {
+                                                                     const float idt2, const int reverse) {
     constexpr int WPB = kSweepBlock / 32;
-    const int lane = threadIdx.x & 31;
-    const int t = blockIdx.x * WPB + (threadIdx.x >> 5);  // vertex index within the colour
-    if (t >= n_v) return;                                  // warp-uniform
+    __shared__ int2 s_id[WPB][32];
+    __shared__ float4 s_sd[WPB][32];
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    const int t = blockIdx.x * WPB + wq;  // vertex index within the colour
+    if (t >= n_v) return;                  // warp-uniform (only warp-level synchronisation below)
     const int v = v_begin + t;
     const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
     const int deg = ld(L.deg + v);
-    const int64_t g0 = 2 * (int64_t)blockIdx.y;             // the warp's two sample groups g0, g0 + 1
-    const int64_t xs[2] = {((g0 * x_stride) << 5) + lane, (((g0 + 1) * x_stride) << 5) + lane};
-    float4 *__restrict__ work0 = reinterpret_cast<float4 *>(L.xbuf[wi]) + xs[0];
-    float4 *__restrict__ work1 = reinterpret_cast<float4 *>(L.xbuf[wi]) + xs[1];
-    const int64_t vv = (int64_t)v << 5;
-    const float4 xa0 = work0[vv], xa1 = work1[vv];
-    const float2 xa[3] = {make_float2(xa0.x, xa1.x), make_float2(xa0.y, xa1.y), make_float2(xa0.z, xa1.z)};
+    const int64_t gp = reverse ? gridDim.y - 1 - blockIdx.y : blockIdx.y;
+    const int64_t slot = ((gp * x_stride) << 8) + 8 * lane;  // this lane's float offset at vertex 0
+    const float *__restrict__ wk = reinterpret_cast<const float *>(L.xbuf[wi]) + slot;
+    const int64_t vo = (int64_t)v << 8;
+    const float4 a01 = *reinterpret_cast<const float4 *>(wk + vo);
+    const float2 a2 = *reinterpret_cast<const float2 *>(wk + vo + 4);
+    const float2 xa[3] = {make_float2(a01.x, a01.y), make_float2(a01.z, a01.w), a2};
     float2 f[3] = {bc(0.f), bc(0.f), bc(0.f)};
     if (FEXT) {
         const float4 fe = ld(reinterpret_cast<const float4 *>(L.fext) + v);
         f[0] = bc(fe.x); f[1] = bc(fe.y); f[2] = bc(fe.z);
     }
     float2 A[6] = {bc(0.f), bc(0.f), bc(0.f), bc(0.f), bc(0.f), bc(0.f)};
+    // path records (the host always orders sh-6 records along link paths): three slots of packed
+    // positions {x, y, z} x 2 samples; each record gathers one new neighbour (one LDG.128 + one LDG.64)
+    // the slots hold the differences d = x_j - x_i (computed once when a neighbour is pushed)
+    P6 S0, S1, S2;
+    auto diff = [&](const P6 &q) { return P6{sub2(q.x, xa[0]), sub2(q.y, xa[1]), sub2(q.z, xa[2])}; };
+    {
+        const int2 p0 = ld(L.path0 + v);
+        S0 = {bc(0.f), bc(0.f), bc(0.f)};
+        S1 = diff(ld_p6(wk + ((int64_t)p0.x << 8)));
+        S2 = diff(ld_p6(wk + ((int64_t)p0.y << 8)));
+    }
     for (int k0 = 0; k0 < deg; k0 += 32) {
-        Pair<float, MODEL_NH> mine = {};
-        if (k0 + lane < deg) load_pair<false>(L, base + (int64_t)(k0 + lane) * kChunk, mine);
+        if (k0 + lane < deg) {
+            const int64_t r = base + (int64_t)(k0 + lane) * kChunk;
+            s_id[wq][lane] = ld(reinterpret_cast<const int2 *>(L.rec_id) + r);
+            s_sd[wq][lane] = ld(reinterpret_cast<const float4 *>(L.rec_a) + r);
+            PBNG_CHECK(r < L.n_slots && (s_id[wq][lane].x & 0x3fffffff) < L.n_vertices);
+        }
+        __syncwarp();
         const int n = min(32, deg - k0);
-#pragma unroll 2
+#pragma unroll kB2Unroll
         for (int j = 0; j < n; ++j) {
-            const Pair<float, MODEL_NH> pr = shfl_pair(mine, j);
-            const int64_t i1 = (int64_t)pr.id.x << 5, i2 = (int64_t)pr.id.y << 5, i3 = (int64_t)pr.id.z << 5;
-            const float4 a0 = ld(work0 + i1), a1 = ld(work1 + i1), b0 = ld(work0 + i2), b1 = ld(work1 + i2),
-                         c0 = ld(work0 + i3), c1 = ld(work1 + i3);
-            const float2 d1[3] = {sub2(make_float2(a0.x, a1.x), xa[0]), sub2(make_float2(a0.y, a1.y), xa[1]),
-                                  sub2(make_float2(a0.z, a1.z), xa[2])};
-            const float2 d2[3] = {sub2(make_float2(b0.x, b1.x), xa[0]), sub2(make_float2(b0.y, b1.y), xa[1]),
-                                  sub2(make_float2(b0.z, b1.z), xa[2])};
-            const float2 d3[3] = {sub2(make_float2(c0.x, c1.x), xa[0]), sub2(make_float2(c0.y, c1.y), xa[1]),
-                                  sub2(make_float2(c0.z, c1.z), xa[2])};
+            if (kB2Prefetch > 0 && j + kB2Prefetch < n)  // the gather of record j + PF: L2 -> L1 now
+                pf_l1(wk + ((int64_t)(s_id[wq][j + kB2Prefetch].x & 0x3fffffff) << 8));
+            const int2 id = s_id[wq][j];
+            const float4 sd = s_sd[wq][j];
+            Pair<float, MODEL_NH> pr;
+            pr.s[0] = sd.x; pr.s[1] = sd.y; pr.s[2] = sd.z; pr.detB = sd.w;
+            pr.VE = __int_as_float(id.y);
+            const P6 nw = diff(ld_p6(wk + ((int64_t)(id.x & 0x3fffffff) << 8)));
+            path_push(S0, S1, S2, nw, id.x);
+            const float2 d1[3] = {S0.x, S0.y, S0.z};
+            const float2 d2[3] = {S1.x, S1.y, S1.z};
+            const float2 d3[3] = {S2.x, S2.y, S2.z};
             contrib_nh2(d1, d2, d3, pr, cmu, clam, f, A);
         }
+        __syncwarp();
     }
-    // per sample: weak constraints, inertia, solve, blend, store (scalar)
+    // per sample: weak constraints, inertia, solve, blend (scalar); then one interleaved store per buffer
+    float p[2][3], o[2][3];
+    const float *hs = reinterpret_cast<const float *>(L.xbuf[hi]) + slot + vo;
+    float4 h01 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float2 h2 = make_float2(0.f, 0.f);
+    if (ACCEL != ACCEL_NONE) {
+        h01 = *reinterpret_cast<const float4 *>(hs);
+        h2 = *reinterpret_cast<const float2 *>(hs + 4);
+    }
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-        const int b = (int)((g0 + q) * 32 + lane);
-        if (b >= n_batch) continue;
-        float4 *__restrict__ work = q ? work1 : work0;
-        const float4 xa4 = q ? xa1 : xa0;
-        const float xs3[3] = {xa4.x, xa4.y, xa4.z};
+        const int64_t b = gp * 64 + q * 32 + lane;
+        const float xs3[3] = {q ? xa[0].y : xa[0].x, q ? xa[1].y : xa[1].x, q ? xa[2].y : xa[2].x};
+        const float h[3] = {q ? h01.y : h01.x, q ? h01.w : h01.z, q ? h2.y : h2.x};
         float fs[3], As[6];
 #pragma unroll
         for (int r = 0; r < 3; ++r) fs[r] = q ? f[r].y : f[r].x;
 #pragma unroll
         for (int r = 0; r < 6; ++r) As[r] = q ? A[r].y : A[r].x;
-        if (WC) wc_contrib<float, float, true>(L, work, 5, v, xs3, fs, As);
-        if (idt2 > 0.f)
-            inertia_contrib<float, float>(L, v, ld(reinterpret_cast<const float4 *>(L.xtilde) + xs[q] + vv), idt2, xs3, fs,
-                                          As);
-        finish_vertex<float, ACCEL>(L, work, xs[q], vv, oi, hi, xa4, fs, As, omega, gamma);
+        if (b < n_batch) {
+            if (WC) wc_contrib_at<float, float, true>(L, L.xbuf[wi], b, x_stride, 6, v, xs3, fs, As);
+            if (idt2 > 0.f) inertia_contrib<float, float>(L, v, pos_load<float>(L.xtilde, b, v, x_stride, 6), idt2, xs3, fs, As);
+            float dx[3];
+            chol_solve3(As, fs, dx);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) p[q][c] = xs3[c] + dx[c];
+            if (!(isfinite(p[q][0]) && isfinite(p[q][1]) && isfinite(p[q][2]))) atomicOr(L.flag, 1);
+        } else {  // padding sample: keep its (finite) values
+#pragma unroll
+            for (int c = 0; c < 3; ++c) p[q][c] = xs3[c];
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (ACCEL == ACCEL_SOR)  // x^{l+1} = omega (x_PBNG - x^{l-1}) + x^{l-1}
+                o[q][c] = omega * (p[q][c] - h[c]) + h[c];
+            else if (ACCEL == ACCEL_CHEB)  // x^{l+1} = omega_{l+1} (gamma (x_PBNG - x^l) + x^l - x^{l-1}) + x^{l-1}
+                o[q][c] = omega * (gamma * (p[q][c] - xs3[c]) + xs3[c] - h[c]) + h[c];
+        }
+    }
+    float *ws = reinterpret_cast<float *>(L.xbuf[wi]) + slot + vo;
+    *reinterpret_cast<float4 *>(ws) = make_float4(p[0][0], p[1][0], p[0][1], p[1][1]);
+    *reinterpret_cast<float2 *>(ws + 4) = make_float2(p[0][2], p[1][2]);
+    if (ACCEL != ACCEL_NONE) {
+        float *os = reinterpret_cast<float *>(L.xbuf[oi]) + slot + vo;
+        *reinterpret_cast<float4 *>(os) = make_float4(o[0][0], o[1][0], o[0][1], o[1][1]);
+        *reinterpret_cast<float2 *>(os + 4) = make_float2(o[0][2], o[1][2]);
+        float *hw = reinterpret_cast<float *>(L.xbuf[hi]) + slot + vo;
+        *reinterpret_cast<float4 *>(hw) = a01;
+        *reinterpret_cast<float2 *>(hw + 4) = a2;
     }
 }
 
 #ifndef PBNG_BATCHED2
 #define PBNG_BATCHED2 1
 #endif
-constexpr bool kBatched2 = PBNG_BATCHED2;  // packed FP32x2 batched kernel for fp32 Neo-Hookean
 
 template <class R, int MODEL, int ACCEL, bool FE, bool W, int S>
 cudaError_t split_launch(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
@@ -1405,15 +1638,16 @@ cudaError_t split_launch(const Problem &p, const Layout &L, const SweepLaunch &s
 template <class R, int MODEL, int ACCEL, bool FE, bool W>
 cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st) {
     const R cmu = R(p.cmu), clam = R(p.clam), om = R(s.omega), ga = R(s.gamma), idt2 = R(p.inv_dt2);
-    if (p.lane_shift == 5 && kBatched2 && sizeof(R) == 4 && MODEL == MODEL_NH) {
+    if constexpr (sizeof(R) == 4 && MODEL == MODEL_NH) {
+      if (p.lane_shift == 6) {  // fp32 Neo-Hookean batches (the host picks sh 6)
         constexpr int WPB = kSweepBlock / 32;
-        const int64_t groups = (p.n_batch + 31) / 32;  // pairs of groups; the workspace holds an even count
-        dim3 grid((unsigned)((s.n_v + WPB - 1) / WPB), (unsigned)((groups + 1) / 2));
+        dim3 grid((unsigned)((s.n_v + WPB - 1) / WPB), (unsigned)((p.n_batch + 63) / 64));
         sweep_batched2_kernel<ACCEL, FE, W><<<grid, kSweepBlock, 0, st>>>(L, s.v_begin, s.n_v, s.chunk_begin,
                                                                           p.x_stride, p.n_batch, s.work, s.out,
                                                                           s.hist, float(cmu), float(clam), float(om),
-                                                                          float(ga), float(idt2));
+                                                                          float(ga), float(idt2), s.reverse);
         return cudaGetLastError();
+    }
     }
     if (p.lane_shift == 5) {
         constexpr int WPB = kSweepBlock / 32;
@@ -1459,7 +1693,19 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
             cudaFuncSetAttribute(sweep_kernel<R, MODEL, ACCEL, FE, W, true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
             carved[p.device % kMaxDevices].store(true, std::memory_order_release);
         }
-        if (kOneWave && sizeof(R) == 4 && !kSweepTma && blocks > (int64_t)sms * 6 && blocks <= (int64_t)sms * (1024 / kSweepBlock))
+        const bool one_wave = kOneWave && sizeof(R) == 4 && !kSweepTma && blocks > (int64_t)sms * 6 &&
+                              blocks <= (int64_t)sms * (1024 / kSweepBlock);
+        if constexpr (MODEL == MODEL_NH) {
+            if (p.path) {
+                if (one_wave)
+                    return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, true, true>, L, s.v_begin,
+                                              s.n_v, s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga,
+                                              idt2);
+                return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, false, true>, L, s.v_begin, s.n_v,
+                                          s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga, idt2);
+            }
+        }
+        if (one_wave)
             return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, true>, L, s.v_begin, s.n_v,
                                       s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga, idt2);
         return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W>, L, s.v_begin, s.n_v, s.chunk_begin,
@@ -1541,12 +1787,6 @@ cudaError_t sweep_dispatch2(const Problem &p, const Layout &L, const SweepLaunch
 // ------------------------------------------------------------------------------------------------
 // positions: original <-> internal order
 // ------------------------------------------------------------------------------------------------
-// element index of (sample b, vertex v): samples grouped by 2^sh lanes, sample-minor inside a group
-// (sh = 0: [n_batch][x_stride]; sh = 5: [n_batch/32][x_stride][32])
-__device__ __forceinline__ int64_t pos_index(int64_t b, int64_t v, int64_t xs, int sh) {
-    return (((b >> sh) * xs + v) << sh) + (b & ((1 << sh) - 1));
-}
-
 template <class R>
 __global__ void set_positions_kernel(const Layout L, const int64_t nv, const int64_t n_global, const int64_t n_free,
                                      const int64_t n_pin, const int64_t x_stride, const int nbuf,
@@ -1562,12 +1802,11 @@ __global__ void set_positions_kernel(const Layout L, const int64_t nv, const int
     } else {
         val = reinterpret_cast<const R4 *>(L.targets)[b * n_pin + (v - n_free)];
     }
-    const int64_t e = pos_index(b, v, x_stride, sh);
     if (nbuf < 0) {  // backward-Euler inertial target xtilde (pbng_set_inertia)
-        reinterpret_cast<R4 *>(L.xtilde)[e] = val;
+        pos_store<R>(L.xtilde, b, v, x_stride, sh, val);
         return;
     }
-    for (int k = 0; k < nbuf; ++k) reinterpret_cast<R4 *>(L.xbuf[k])[e] = val;
+    for (int k = 0; k < nbuf; ++k) pos_store<R>(L.xbuf[k], b, v, x_stride, sh, val);
 }
 
 template <class R>
@@ -1577,7 +1816,7 @@ __global__ void get_positions_kernel(const Layout L, const int64_t nv, const int
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= nv) return;
     const int64_t b = blockIdx.y;
-    const R4 x = reinterpret_cast<const R4 *>(L.xbuf[wi])[pos_index(b, v, x_stride, sh)];
+    const R4 x = pos_load<R>(L.xbuf[wi], b, v, x_stride, sh);
     R *d = reinterpret_cast<R *>(L.stage) + (b * n_global + L.int2orig[v]) * 3;
     d[0] = x.x;
     d[1] = x.y;
@@ -1594,10 +1833,9 @@ __global__ void halo_pack_kernel(const Layout L, const int32_t *__restrict__ idx
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int64_t b = blockIdx.y;
-    const int64_t v = pos_index(b, idx[i], x_stride, sh);
     R4 *o = reinterpret_cast<R4 *>(buf) + (b * n + i) * nf;
     const int bb[3] = {b0, b1, b2};
-    for (int k = 0; k < nf; ++k) o[k] = reinterpret_cast<const R4 *>(L.xbuf[bb[k]])[v];
+    for (int k = 0; k < nf; ++k) o[k] = pos_load<R>(L.xbuf[bb[k]], b, idx[i], x_stride, sh);
 }
 
 template <class R>
@@ -1608,10 +1846,9 @@ __global__ void halo_unpack_kernel(const Layout L, const int32_t *__restrict__ i
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int64_t b = blockIdx.y;
-    const int64_t v = pos_index(b, idx[i], x_stride, sh);
     const R4 *o = reinterpret_cast<const R4 *>(buf) + (b * n + i) * nf;
     const int bb[3] = {b0, b1, b2};
-    for (int k = 0; k < nf; ++k) reinterpret_cast<R4 *>(L.xbuf[bb[k]])[v] = o[k];
+    for (int k = 0; k < nf; ++k) pos_store<R>(L.xbuf[bb[k]], b, idx[i], x_stride, sh, o[k]);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1623,7 +1860,7 @@ __global__ void halo_unpack_kernel(const Layout L, const int32_t *__restrict__ i
 // ------------------------------------------------------------------------------------------------
 template <class R>
 __device__ __forceinline__ double3 pos_d(const Layout &L, int work, int64_t b, int64_t v, int64_t xs, int sh) {
-    const typename RT<R>::R4 x = reinterpret_cast<const typename RT<R>::R4 *>(L.xbuf[work])[pos_index(b, v, xs, sh)];
+    const typename RT<R>::R4 x = pos_load<R>(L.xbuf[work], b, v, xs, sh);
     return make_double3(double(x.x), double(x.y), double(x.z));
 }
 __device__ __forceinline__ double3 sub(double3 a, double3 b) { return make_double3(a.x - b.x, a.y - b.y, a.z - b.z); }
@@ -1786,7 +2023,7 @@ __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const
     using R4 = typename RT<R>::R4;
     __shared__ double red_sh[32];
     const int64_t b = blockIdx.y;
-    const R4 *x = reinterpret_cast<const R4 *>(L.xbuf[wi]) + pos_index(b, 0, x_stride, sh);
+    const void *x = L.xbuf[wi];
     const double r_mu = cmu / (cmu + clam);  // mu / lambdahat, independent of E
     double acc = 0.0;
     const int64_t n_items = nt + n_cons + (idt2 > 0.0 ? n_own : 0);
@@ -1794,8 +2031,8 @@ __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const
          item += (int64_t)gridDim.x * blockDim.x) {
         if (item >= nt + n_cons) {  // backward Euler: inertia m_i/(2 dt^2) |x_i - xtilde_i|^2 of owned free nodes
             const int64_t v = item - nt - n_cons;
-            const R4 xv = ld(x + (v << sh));
-            const R4 xt = ld(reinterpret_cast<const R4 *>(L.xtilde) + pos_index(b, v, x_stride, sh));
+            const R4 xv = pos_load<R>(x, b, v, x_stride, sh);
+            const R4 xt = pos_load<R>(L.xtilde, b, v, x_stride, sh);
             const double dx = double(xv.x) - xt.x, dy = double(xv.y) - xt.y, dz = double(xv.z) - xt.z;
             acc += 0.5 * idt2 * double(ld(reinterpret_cast<const R *>(L.mass) + v)) * (dx * dx + dy * dy + dz * dz);
         } else if (item < nt) {
@@ -1803,8 +2040,8 @@ __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const
             const R4 ta = ld(reinterpret_cast<const R4 *>(L.tet_a) + item);
             const R4 tb = ld(reinterpret_cast<const R4 *>(L.tet_b) + item);
             const R4 tc = ld(reinterpret_cast<const R4 *>(L.tet_c) + item);
-            const R4 q0 = ld(x + ((int64_t)id.x << sh)), q1 = ld(x + ((int64_t)id.y << sh)),
-                     q2 = ld(x + ((int64_t)id.z << sh)), q3 = ld(x + ((int64_t)id.w << sh));
+            const R4 q0 = pos_load<R>(x, b, id.x, x_stride, sh), q1 = pos_load<R>(x, b, id.y, x_stride, sh),
+                     q2 = pos_load<R>(x, b, id.z, x_stride, sh), q3 = pos_load<R>(x, b, id.w, x_stride, sh);
             const double Bm[3][3] = {{ta.x, ta.y, ta.z}, {ta.w, tb.x, tb.y}, {tb.z, tb.w, tc.x}};
             const double VE = tc.y, V = tc.z;
             const double d[3][3] = {{double(q1.x) - q0.x, double(q1.y) - q0.y, double(q1.z) - q0.z},
@@ -1860,7 +2097,7 @@ __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const
             double C[3] = {-double(an.x), -double(an.y), -double(an.z)};
             const int nn = ld(L.c_n + c);
             for (int q = 0; q < nn; ++q) {
-                const R4 y = ld(x + ((int64_t)ld(L.c_node + kWcMaxNodes * c + q) << sh));
+                const R4 y = pos_load<R>(x, b, ld(L.c_node + kWcMaxNodes * c + q), x_stride, sh);
                 const double w = ld(reinterpret_cast<const R *>(L.c_w) + kWcMaxNodes * c + q);
                 C[0] += w * y.x; C[1] += w * y.y; C[2] += w * y.z;
             }
@@ -1879,11 +2116,11 @@ template <class R, int MODEL, bool FEXT, bool WC>
 __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, const int64_t n_chunks,
                                                              const int64_t x_stride, const int wi, const double cmu,
                                                              const double clam, const int gr, const int sh,
-                                                             const double idt2) {
+                                                             const double idt2, const bool path) {
     using R4 = typename RT<R>::R4;
     __shared__ double red_sh[32];
     const int64_t b = blockIdx.y;
-    const R4 *x = reinterpret_cast<const R4 *>(L.xbuf[wi]) + pos_index(b, 0, x_stride, sh);
+    const void *x = L.xbuf[wi];
     double acc = 0.0;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_chunks * kChunk;
          t += (int64_t)gridDim.x * blockDim.x) {
@@ -1894,27 +2131,42 @@ __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, con
         const int v = cv.x + lane;
         const int64_t base = L.chunk_off[chunk] + lane;
         const int deg = L.deg[v];
-        const R4 xa4 = x[(int64_t)v << sh];
+        const R4 xa4 = pos_load<R>(x, b, v, x_stride, sh);
         const double xa[3] = {xa4.x, xa4.y, xa4.z};
         double f[3] = {0.0, 0.0, 0.0}, A[6];
         if (FEXT) {
             const R4 fe = reinterpret_cast<const R4 *>(L.fext)[v];
             f[0] = fe.x; f[1] = fe.y; f[2] = fe.z;
         }
-        for (int k = 0; k < deg; ++k) {
+        bool done = false;
+        if constexpr (MODEL == MODEL_NH) {
+            if (path) {  // path records: three slots, one new neighbour per record
+                const int2 p0 = L.path0[v];
+                R4 S0 = xa4, S1 = pos_load<R>(x, b, p0.x, x_stride, sh), S2 = pos_load<R>(x, b, p0.y, x_stride, sh);
+                for (int k = 0; k < deg; ++k) {
+                    Pair<R, MODEL_NH> pr;
+                    const int code = load_path_rec<true>(L, base + (int64_t)k * kChunk, pr);
+                    path_push(S0, S1, S2, pos_load<R>(x, b, code & 0x3fffffff, x_stride, sh), code);
+                    const double d1[3] = {S0.x - xa[0], S0.y - xa[1], S0.z - xa[2]};
+                    const double d2[3] = {S1.x - xa[0], S1.y - xa[1], S1.z - xa[2]};
+                    const double d3[3] = {S2.x - xa[0], S2.y - xa[1], S2.z - xa[2]};
+                    contrib<false>(d1, d2, d3, pr, cmu, clam, f, A);
+                }
+                done = true;
+            }
+        }
+        for (int k = 0; k < deg && !done; ++k) {
             Pair<R, MODEL> pr;
             load_pair<true>(L, base + (int64_t)k * kChunk, pr);
-            const R4 p1 = ld(x + ((int64_t)pr.id.x << sh)), p2 = ld(x + ((int64_t)pr.id.y << sh)),
-                     p3 = ld(x + ((int64_t)pr.id.z << sh));
+            const R4 p1 = pos_load<R>(x, b, pr.id.x, x_stride, sh), p2 = pos_load<R>(x, b, pr.id.y, x_stride, sh),
+                     p3 = pos_load<R>(x, b, pr.id.z, x_stride, sh);
             const double d1[3] = {p1.x - xa[0], p1.y - xa[1], p1.z - xa[2]};
             const double d2[3] = {p2.x - xa[0], p2.y - xa[1], p2.z - xa[2]};
             const double d3[3] = {p3.x - xa[0], p3.y - xa[1], p3.z - xa[2]};
             contrib<false>(d1, d2, d3, pr, cmu, clam, f, A);
         }
-        if (WC) wc_contrib<R, double, false>(L, x, sh, v, xa, f, A);
-        if (idt2 > 0.0)
-            inertia_contrib<R, double>(L, v, ld(reinterpret_cast<const R4 *>(L.xtilde) + pos_index(b, v, x_stride, sh)),
-                                       idt2, xa, f, A);
+        if (WC) wc_contrib_at<R, double, false>(L, x, b, x_stride, sh, v, xa, f, A);
+        if (idt2 > 0.0) inertia_contrib<R, double>(L, v, pos_load<R>(L.xtilde, b, v, x_stride, sh), idt2, xa, f, A);
         acc += f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
     }
     const double s = block_sum(acc, red_sh);
@@ -1942,11 +2194,11 @@ cudaError_t energy_dispatch(const Problem &p, const Layout &L, int wi, cudaStrea
         L, p.n_tets, p.n_cons, p.x_stride, wi, p.cmu, p.clam, p.rho_g[0], p.rho_g[1], p.rho_g[2], p.ge, p.lane_shift, p.n_own, p.inv_dt2);
     dim3 gr(p.gr, p.n_batch);
     if (p.has_fext) {
-        if (p.has_wc) residual_kernel<R, MODEL, true, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2);
-        else residual_kernel<R, MODEL, true, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2);
+        if (p.has_wc) residual_kernel<R, MODEL, true, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2, p.path);
+        else residual_kernel<R, MODEL, true, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2, p.path);
     } else {
-        if (p.has_wc) residual_kernel<R, MODEL, false, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2);
-        else residual_kernel<R, MODEL, false, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2);
+        if (p.has_wc) residual_kernel<R, MODEL, false, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2, p.path);
+        else residual_kernel<R, MODEL, false, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2, p.path);
     }
     reduce_kernel<<<p.n_batch, kRedBlock, 0, st>>>(L, p.ge, p.gr);
     return cudaGetLastError();
