@@ -146,6 +146,7 @@ struct pbng_ctx {
     std::vector<int2> h_rec_id2;   // path-ordered NH records: {id | drop << 30, VE bits} (Problem::path)
     std::vector<int2> h_path0;     // path-ordered NH records: per free vertex the slots S1, S2 before record 0
     bool path_rec = false;
+    size_t wc_cap = 0, vc_cap = 0, deps_cap = 0;  // weak-constraint / pipeline-dependency room in the workspace
     int64_t n_records = 0;         // pair records stored per sweep (path mode: incl. load-only ones)
     std::vector<unsigned char> h_rec_a, h_rec_b, h_rec_c, h_fext, h_wc_d, h_c_w, h_c_anchor, h_c_K, h_tet_a,
         h_tet_b, h_tet_c, h_targets;
@@ -428,6 +429,61 @@ bool use_path_records(const pbng_ctx *c) {
     return sh == 6 || (sh == 0 && problem_split(c) == 1);
 }
 
+// weak constraints held by this context (owned first): distinct nodes with combined weights w0_j - w1_j;
+// per owned free vertex the list of (constraint, w0_i - w1_i) in input order.  Also the fast path of
+// pbng_update_constraints (colouring unchanged: only these arrays are rebuilt and uploaded).
+template <class R>
+void build_constraint_arrays(pbng_ctx *c) {
+    const size_t s = sizeof(R), s4 = 4 * sizeof(R);
+    const int64_t ncl = (int64_t)c->cons_local.size();
+    const int64_t ncap = std::max<int64_t>(ncl, 1);
+    c->h_c_n.assign((size_t)ncap, 0);
+    c->h_c_node.assign((size_t)ncap * kWcMaxNodes, 0);
+    c->h_c_w.assign((size_t)ncap * kWcMaxNodes * s, 0);
+    c->h_c_anchor.assign((size_t)ncap * s4, 0);
+    c->h_c_K.assign((size_t)ncap * kWcMaxNodes * s, 0);
+    std::vector<std::pair<int32_t, int32_t>> by_gid;  // (global id, local id), ascending global id
+    for (int64_t li = 0; li < ncl; ++li) by_gid.push_back({c->cons_local[li], (int32_t)li});
+    std::sort(by_gid.begin(), by_gid.end());
+    std::vector<std::vector<std::pair<int32_t, double>>> per_v((size_t)c->n_free);
+    for (const auto &gl : by_gid) {
+        const int32_t li = gl.second;
+        const pbng_weak_constraint &w = c->wc[gl.first];
+        int32_t nodes[kWcMaxNodes];
+        double wt[kWcMaxNodes];
+        int nn = 0;
+        auto add = [&](int32_t node, double weight) {
+            for (int q = 0; q < nn; ++q)
+                if (nodes[q] == node) { wt[q] += weight; return; }
+            nodes[nn] = node;
+            wt[nn] = weight;
+            ++nn;
+        };
+        for (int q = 0; q < w.n0; ++q) add(w.idx0[q], w.w0[q]);
+        for (int q = 0; q < w.n1; ++q) add(w.idx1[q], -w.w1[q]);
+        c->h_c_n[li] = nn;
+        for (int q = 0; q < nn; ++q) {
+            const int32_t vi = c->orig2int[nodes[q]];
+            c->h_c_node[kWcMaxNodes * li + q] = vi;
+            put1<R>(c->h_c_w, kWcMaxNodes * li + q, wt[q]);
+            if (vi >= 0 && vi < c->n_free) per_v[vi].push_back({li, wt[q]});
+        }
+        if (w.n1 == 0) put4<R>(c->h_c_anchor, li, w.anchor[0], w.anchor[1], w.anchor[2], 0.0);
+        for (int q = 0; q < 6; ++q) put1<R>(c->h_c_K, kWcMaxNodes * li + q, w.K[q]);
+    }
+    c->h_wc_off.assign((size_t)c->n_free + 1, 0);
+    for (int64_t i = 0; i < c->n_free; ++i) c->h_wc_off[i + 1] = c->h_wc_off[i] + (int32_t)per_v[i].size();
+    c->n_vc = c->h_wc_off[c->n_free];
+    c->h_wc_cid.assign((size_t)std::max<int64_t>(c->n_vc, 1), 0);
+    c->h_wc_d.assign((size_t)std::max<int64_t>(c->n_vc, 1) * s, 0);
+    for (int64_t i = 0; i < c->n_free; ++i)
+        for (size_t q = 0; q < per_v[i].size(); ++q) {
+            c->h_wc_cid[c->h_wc_off[i] + q] = per_v[i][q].first;
+            put1<R>(c->h_wc_d, c->h_wc_off[i] + q, per_v[i][q].second);
+        }
+
+}
+
 template <class R>
 void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::vector<int32_t> &vt) {
     const int64_t nv = c->nv, nb = c->nb;
@@ -630,54 +686,7 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
         put1<R>(c->h_mass, i, m);
     }
 
-    // weak constraints held by this context (owned first): distinct nodes with combined weights
-    // w0_j - w1_j; per owned free vertex the list of (constraint, w0_i - w1_i) in input order
-    const int64_t ncl = (int64_t)c->cons_local.size();
-    const int64_t ncap = std::max<int64_t>(ncl, 1);
-    c->h_c_n.assign((size_t)ncap, 0);
-    c->h_c_node.assign((size_t)ncap * kWcMaxNodes, 0);
-    c->h_c_w.assign((size_t)ncap * kWcMaxNodes * s, 0);
-    c->h_c_anchor.assign((size_t)ncap * s4, 0);
-    c->h_c_K.assign((size_t)ncap * kWcMaxNodes * s, 0);
-    std::vector<std::pair<int32_t, int32_t>> by_gid;  // (global id, local id), ascending global id
-    for (int64_t li = 0; li < ncl; ++li) by_gid.push_back({c->cons_local[li], (int32_t)li});
-    std::sort(by_gid.begin(), by_gid.end());
-    std::vector<std::vector<std::pair<int32_t, double>>> per_v((size_t)c->n_free);
-    for (const auto &gl : by_gid) {
-        const int32_t li = gl.second;
-        const pbng_weak_constraint &w = c->wc[gl.first];
-        int32_t nodes[kWcMaxNodes];
-        double wt[kWcMaxNodes];
-        int nn = 0;
-        auto add = [&](int32_t node, double weight) {
-            for (int q = 0; q < nn; ++q)
-                if (nodes[q] == node) { wt[q] += weight; return; }
-            nodes[nn] = node;
-            wt[nn] = weight;
-            ++nn;
-        };
-        for (int q = 0; q < w.n0; ++q) add(w.idx0[q], w.w0[q]);
-        for (int q = 0; q < w.n1; ++q) add(w.idx1[q], -w.w1[q]);
-        c->h_c_n[li] = nn;
-        for (int q = 0; q < nn; ++q) {
-            const int32_t vi = c->orig2int[nodes[q]];
-            c->h_c_node[kWcMaxNodes * li + q] = vi;
-            put1<R>(c->h_c_w, kWcMaxNodes * li + q, wt[q]);
-            if (vi >= 0 && vi < c->n_free) per_v[vi].push_back({li, wt[q]});
-        }
-        if (w.n1 == 0) put4<R>(c->h_c_anchor, li, w.anchor[0], w.anchor[1], w.anchor[2], 0.0);
-        for (int q = 0; q < 6; ++q) put1<R>(c->h_c_K, kWcMaxNodes * li + q, w.K[q]);
-    }
-    c->h_wc_off.assign((size_t)c->n_free + 1, 0);
-    for (int64_t i = 0; i < c->n_free; ++i) c->h_wc_off[i + 1] = c->h_wc_off[i] + (int32_t)per_v[i].size();
-    c->n_vc = c->h_wc_off[c->n_free];
-    c->h_wc_cid.assign((size_t)std::max<int64_t>(c->n_vc, 1), 0);
-    c->h_wc_d.assign((size_t)std::max<int64_t>(c->n_vc, 1) * s, 0);
-    for (int64_t i = 0; i < c->n_free; ++i)
-        for (size_t q = 0; q < per_v[i].size(); ++q) {
-            c->h_wc_cid[c->h_wc_off[i] + q] = per_v[i][q].first;
-            put1<R>(c->h_wc_d, c->h_wc_off[i] + q, per_v[i][q].second);
-        }
+    build_constraint_arrays<R>(c);
 
     // tet records for the energy pass (the tets this context owns)
     const int64_t ntl = (int64_t)c->tet_local.size();
@@ -969,14 +978,20 @@ void plan_workspace(pbng_ctx *c) {
     take(c->r_chunk_v, std::max<size_t>(c->h_chunk_v.size(), 1) * 8);
     take(c->r_deg, std::max<size_t>(c->h_deg.size(), 1) * 4);
     take(c->r_fext, c->h_fext.size());
+    // weak constraints get headroom (pbng_update_constraints' fast path rewrites them in place): room for
+    // a contact at every free boundary vertex (up to 4 free nodes each) on top of twice the current set
+    const size_t ncl = c->h_c_n.size(), nvc = c->h_wc_cid.size();
+    c->wc_cap = std::max<size_t>(2 * ncl, ncl + c->h_sv.size() + 64);
+    c->vc_cap = std::max<size_t>(2 * nvc, nvc + 4 * (c->h_sv.size() + 64));
+    c->deps_cap = 2 * c->h_deps.size() + 1024;
     take(c->r_wc_off, c->h_wc_off.size() * 4);
-    take(c->r_wc_cid, c->h_wc_cid.size() * 4);
-    take(c->r_wc_d, c->h_wc_d.size());
-    take(c->r_c_n, c->h_c_n.size() * 4);
-    take(c->r_c_node, c->h_c_node.size() * 4);
-    take(c->r_c_w, c->h_c_w.size());
-    take(c->r_c_anchor, c->h_c_anchor.size());
-    take(c->r_c_K, c->h_c_K.size());
+    take(c->r_wc_cid, c->vc_cap * 4);
+    take(c->r_wc_d, c->vc_cap * s);
+    take(c->r_c_n, c->wc_cap * 4);
+    take(c->r_c_node, c->wc_cap * kWcMaxNodes * 4);
+    take(c->r_c_w, c->wc_cap * kWcMaxNodes * s);
+    take(c->r_c_anchor, c->wc_cap * s4);
+    take(c->r_c_K, c->wc_cap * kWcMaxNodes * s);
     take(c->r_tet_id, c->h_tet_id.size() * 16);
     take(c->r_tet_a, c->h_tet_a.size());
     take(c->r_tet_b, c->h_tet_b.size());
@@ -996,7 +1011,7 @@ void plan_workspace(pbng_ctx *c) {
     take(c->r_halo_send, std::max<size_t>(c->h_halo_send.size(), 1) * 4);
     take(c->r_halo_recv, std::max<size_t>(c->h_halo_recv.size(), 1) * 4);
     take(c->r_dep_off, c->h_dep_off.size() * 4);
-    take(c->r_deps, std::max<size_t>(c->h_deps.size(), 1) * 4);
+    take(c->r_deps, std::max<size_t>(c->deps_cap, 1) * 4);
     take(c->r_pipe, 8 + (size_t)c->nb * (size_t)std::max<int64_t>(c->n_chunks, 1) * 4);  // counter, flags
     take(c->r_surf, std::max<size_t>(c->h_surf.size(), 1) * 16);
     take(c->r_sv, std::max<size_t>(c->h_sv.size(), 1) * 8);
@@ -2418,6 +2433,114 @@ pbng_status pbng_test_polar(pbng_dtype dtype, const double *F, double *R, int64_
     return PBNG_OK;
 }
 
+}  // extern "C"
+
+// pbng_update_constraints when the incremental recolouring changed no colour: the
+// colour-sorted layout, the pair records and the iterate stay where they are; only the weak-constraint
+// arrays (and, for the pipelined schedule, the chunk dependency lists) are rebuilt on the host and written
+// into their headroom in the workspace.  Positions, acceleration state and the backward-Euler target are
+// kept; new Dirichlet targets are written into the pinned rows (the acceleration state then restarts, as
+// with pbng_set_positions).  PBNG_E_OUT_OF_MEMORY = no headroom left (the caller re-lays out).
+static pbng_status update_constraints_in_place(pbng_ctx *c, const double *pinned_xyz, const pbng_weak_constraint *wc,
+                                               int64_t n_wc) {
+    // a free vertex without tets must keep a constraint; the re-layout reports it
+    std::vector<char> touched((size_t)c->nv, 0);
+    for (int64_t q = 0; q < n_wc; ++q) {
+        for (int a = 0; a < wc[q].n0; ++a) touched[wc[q].idx0[a]] = 1;
+        for (int a = 0; a < wc[q].n1; ++a) touched[wc[q].idx1[a]] = 1;
+    }
+    for (int64_t i = 0; i < c->n_free; ++i)
+        if (c->h_deg[i] == 0 && !touched[c->int2orig[i]]) return fail(PBNG_E_OUT_OF_MEMORY, "update_constraints: re-layout");
+    const std::vector<pbng_weak_constraint> old_wc = c->wc;
+    const std::vector<int32_t> old_local = c->cons_local;
+    const int64_t old_owned = c->n_cons_owned;
+    c->wc.assign(wc, wc + n_wc);
+    c->cons_local.resize((size_t)n_wc);
+    for (int64_t q = 0; q < n_wc; ++q) c->cons_local[q] = (int32_t)q;
+    c->n_cons_owned = n_wc;
+    if (c->dtype == DT_F64) build_constraint_arrays<double>(c);
+    else build_constraint_arrays<float>(c);
+    const bool deps = pipeline_available(c);
+    if (deps) {
+        std::vector<int64_t> vt_off((size_t)c->nv + 1, 0);
+        for (int64_t e = 0; e < c->nt; ++e)
+            for (int a = 0; a < 4; ++a) vt_off[c->tets[4 * e + a] + 1]++;
+        for (int64_t v = 0; v < c->nv; ++v) vt_off[v + 1] += vt_off[v];
+        std::vector<int32_t> vt((size_t)std::max<int64_t>(vt_off[c->nv], 1));
+        std::vector<int64_t> fill(vt_off.begin(), vt_off.end() - 1);
+        for (int64_t e = 0; e < c->nt; ++e)
+            for (int a = 0; a < 4; ++a) vt[fill[c->tets[4 * e + a]]++] = (int32_t)e;
+        build_pipeline(c, vt_off, vt);
+    }
+    if (c->h_c_n.size() > c->wc_cap || c->h_wc_cid.size() > c->vc_cap || (deps && c->h_deps.size() > c->deps_cap)) {
+        c->wc = old_wc;  // no headroom: leave the context as it was for the re-layout
+        c->cons_local = old_local;
+        c->n_cons_owned = old_owned;
+        return fail(PBNG_E_OUT_OF_MEMORY, "update_constraints: re-layout");
+    }
+    const int64_t np = (int64_t)c->pinned.size();
+    if (pinned_xyz) {
+        for (int64_t k = 0; k < np; ++k)
+            for (int64_t b = 0; b < c->nb; ++b)
+                for (int a = 0; a < 3; ++a)
+                    c->targets[3 * (b * np + k) + a] = pinned_xyz[3 * (b * np + c->pin_order[k]) + a];
+        const size_t s4 = c->real4_size();
+        const int64_t npl = (int64_t)c->local_pinned.size();
+        for (int64_t b = 0; b < c->nb; ++b)
+            for (int64_t k = 0; k < npl; ++k) {
+                const double *t = c->targets.data() + 3 * (b * np + c->local_pinned[k]);
+                if (c->dtype == DT_F64) put4<double>(c->h_targets, b * npl + k, t[0], t[1], t[2], 0.0);
+                else put4<float>(c->h_targets, b * npl + k, t[0], t[1], t[2], 0.0);
+            }
+        (void)s4;
+    }
+    Problem &p = c->prob;
+    p.has_wc = c->n_vc > 0;
+    p.n_cons = c->n_cons_owned;
+    const int64_t items = (int64_t)c->tet_local.size() + c->n_cons_owned + c->n_free;
+    const int ge_cap = (int)(c->r_part_e.bytes / (8 * (size_t)c->nb));
+    p.ge = (int)std::max<int64_t>(1, std::min<int64_t>({(items + kRedBlock - 1) / kRedBlock, 1184, (int64_t)ge_cap}));
+    DevGuard g(c->device);
+    char *base = static_cast<char *>(c->ws);
+    auto up = [&](const Region &r, const void *src, size_t n) -> cudaError_t {
+        if (n == 0) return cudaSuccess;
+        return cudaMemcpyAsync(base + r.off, src, n, cudaMemcpyHostToDevice, c->stream);
+    };
+    cudaError_t e = cudaSuccess;
+    auto chk = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
+    chk(up(c->r_wc_off, c->h_wc_off.data(), c->h_wc_off.size() * 4));
+    chk(up(c->r_wc_cid, c->h_wc_cid.data(), c->h_wc_cid.size() * 4));
+    chk(up(c->r_wc_d, c->h_wc_d.data(), c->h_wc_d.size()));
+    chk(up(c->r_c_n, c->h_c_n.data(), c->h_c_n.size() * 4));
+    chk(up(c->r_c_node, c->h_c_node.data(), c->h_c_node.size() * 4));
+    chk(up(c->r_c_w, c->h_c_w.data(), c->h_c_w.size()));
+    chk(up(c->r_c_anchor, c->h_c_anchor.data(), c->h_c_anchor.size()));
+    chk(up(c->r_c_K, c->h_c_K.data(), c->h_c_K.size()));
+    if (deps) {
+        chk(up(c->r_dep_off, c->h_dep_off.data(), c->h_dep_off.size() * 4));
+        chk(up(c->r_deps, c->h_deps.data(), c->h_deps.size() * 4));
+    }
+    if (pinned_xyz) {
+        chk(up(c->r_targets, c->h_targets.data(), c->h_targets.size()));
+        if (c->positions_set) {  // pinned rows <- the new targets, free rows kept (through the stage buffer)
+            chk(launch_get_positions(c->prob, c->L, c->work, c->stream));
+            chk(launch_set_positions(c->prob, c->L, 3, c->stream));
+            c->launches += 2;
+            c->work = 0;
+            c->out = 1;
+            c->hist = 2;
+            c->l = 0;
+            c->hist_valid = true;
+        }
+    }
+    chk(cudaStreamSynchronize(c->stream));  // the host images are rewritten by the next update
+    if (e != cudaSuccess) return cuda_fail(e, "update_constraints: upload");
+    c->cur_accel = -1;
+    return PBNG_OK;
+}
+
+extern "C" {
+
 pbng_status pbng_update_constraints(pbng_ctx *c, const double *pinned_xyz, const pbng_weak_constraint *wc, int64_t n_wc,
                                     int64_t *n_recoloured) {
     if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
@@ -2432,7 +2555,7 @@ pbng_status pbng_update_constraints(pbng_ctx *c, const double *pinned_xyz, const
     pbng_status st = validate_wc(c, wc, n_wc, "update_constraints");
     if (st != PBNG_OK) return st;
     const bool keep = c->bound && c->positions_set;
-    std::vector<unsigned char> saved;
+    std::vector<unsigned char> saved, saved_xt;
     int64_t changed = 0;
     try {
         // "newly added" = node set not present among the previous constraints (removed ones only relax)
@@ -2445,6 +2568,23 @@ pbng_status pbng_update_constraints(pbng_ctx *c, const double *pinned_xyz, const
             is_new[q] = !std::binary_search(old_nodes.begin(), old_nodes.end(), nodes[q]);
         }
         std::vector<int32_t> col = recolour_incremental(c, nodes, is_new, &changed);
+        if (changed == 0 && c->bound) {
+            st = update_constraints_in_place(c, pinned_xyz, wc, n_wc);
+            if (st == PBNG_OK) {
+                if (n_recoloured) *n_recoloured = 0;
+                return PBNG_OK;
+            }
+            if (st != PBNG_E_OUT_OF_MEMORY) return st;  // no headroom left: fall through to the re-layout
+        }
+        const double idt2 = c->prob.inv_dt2;
+        if (keep && idt2 > 0.0) {  // the backward-Euler target, original order (restored with the iterate)
+            DevGuard g(c->device);
+            saved_xt.resize((size_t)c->nb * c->nv * 3 * c->real_size());
+            PBNG_CUDA(launch_get_positions(c->prob, c->L, -1, c->stream), "update_constraints: inertial target");
+            PBNG_CUDA(cudaMemcpyAsync(saved_xt.data(), c->L.stage, saved_xt.size(), cudaMemcpyDeviceToHost, c->stream),
+                      "update_constraints: copy");
+            PBNG_CUDA(cudaStreamSynchronize(c->stream), "update_constraints: synchronize");
+        }
         if (keep) {  // the current iterate, original order (restored after the re-layout)
             saved.resize((size_t)c->nb * c->nv * 3 * c->real_size());
             st = pbng_get_positions(c, saved.data());
@@ -2462,7 +2602,7 @@ pbng_status pbng_update_constraints(pbng_ctx *c, const double *pinned_xyz, const
         st = colour_and_layout(c, &col);
         if (st != PBNG_OK) return st;
         if (n_recoloured) *n_recoloured = changed;
-        c->prob.inv_dt2 = 0.0;  // the backward-Euler target is not carried over (pbng_set_inertia again)
+        c->prob.inv_dt2 = 0.0;
         if (was_bound) {
             if (c->ws_need > ws_bytes)
                 return fail(PBNG_E_OUT_OF_MEMORY, "update_constraints: the new layout needs " + std::to_string(c->ws_need) +
@@ -2470,6 +2610,10 @@ pbng_status pbng_update_constraints(pbng_ctx *c, const double *pinned_xyz, const
             st = pbng_bind_workspace(c, ws, ws_bytes);
             if (st != PBNG_OK) return st;
             if (keep) {
+                if (!saved_xt.empty()) {  // carry the backward-Euler target over to the new layout
+                    st = pbng_set_inertia(c, 1.0 / std::sqrt(idt2), saved_xt.data());
+                    if (st != PBNG_OK) return st;
+                }
                 st = pbng_set_positions(c, saved.data());
                 if (st != PBNG_OK) return st;
                 DevGuard g(c->device);

@@ -1816,7 +1816,7 @@ __global__ void get_positions_kernel(const Layout L, const int64_t nv, const int
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= nv) return;
     const int64_t b = blockIdx.y;
-    const R4 x = pos_load<R>(L.xbuf[wi], b, v, x_stride, sh);
+    const R4 x = pos_load<R>(wi < 0 ? L.xtilde : L.xbuf[wi], b, v, x_stride, sh);  // wi < 0: the inertial target
     R *d = reinterpret_cast<R *>(L.stage) + (b * n_global + L.int2orig[v]) * 3;
     d[0] = x.x;
     d[1] = x.y;

@@ -58,7 +58,11 @@ def test_device_detection_equals_oracle(dtype):
     ctx.close()
 
 
-def test_two_blocks_colliding_backward_euler_matches_oracle():
+@pytest.mark.parametrize("inertia_first", [False, True])
+def test_two_blocks_colliding_backward_euler_matches_oracle(inertia_first):
+    """inertia_first: the backward-Euler target is set BEFORE pbng_update_constraints, which must carry it
+    (and the iterate) over -- in place when the incremental recolouring changes no colour, across the
+    re-layout otherwise; both paths occur in this run."""
     import torch
 
     import oracle.oracle as O
@@ -77,11 +81,15 @@ def test_two_blocks_colliding_backward_euler_matches_oracle():
     xo_prev = s.meta["x_prev"].copy()
     xo = s.x0[0].copy()
     n_contact_steps = 0
+    recoloured = []
     for step in range(1, 9):
         tgt = G.targets_at(s, step)
         wc = ctx.detect_contacts(th, kn)
-        ctx.update_constraints(wc, targets=tgt)
-        ctx.set_inertia(dt, 2 * xg - xg_prev)
+        if inertia_first:
+            ctx.set_inertia(dt, 2 * xg - xg_prev)
+        recoloured.append(ctx.update_constraints(wc, targets=tgt))
+        if not inertia_first:
+            ctx.set_inertia(dt, 2 * xg - xg_prev)
         ctx.iterate(K)
         xg_prev, xg = xg, ctx.get_positions()
         gpu_hist.append(xg.cpu().numpy()[0])
@@ -113,6 +121,7 @@ def test_two_blocks_colliding_backward_euler_matches_oracle():
         err = np.abs(gpu_hist[-1] - xo).max() / s.bbox_diag()
         assert err <= 1e-10, f"step {step}: position error {err:.3e}"
     assert n_contact_steps >= 4  # the blocks met (step 3) and stayed in contact
+    assert any(r == 0 for r in recoloured) and any(r > 0 for r in recoloured), recoloured
     ctx.close()
 
 
