@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <atomic>
+#include <tuple>
 
 #include "pbng_internal.h"
 
@@ -2014,21 +2015,58 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
     return r;  // valid in thread 0
 }
 
-template <class R, int MODEL>
+// Item loops of the energy / residual kernels.  BM = false: one sample per grid row (blockIdx.y), one item
+// per thread.  BM = true (batched layouts, sh >= 5): one group of 32 samples per grid row, lane = sample,
+// one item per WARP -- the item's records are warp-uniform (broadcast) loads and the position loads of a
+// warp are the item's contiguous sample-minor lines.  Both reduce in a fixed order (deterministic).
+template <bool BM>
+__device__ __forceinline__ void item_range(int64_t &b, int64_t &i0, int64_t &step) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (BM) {
+        b = (int64_t)blockIdx.y * 32 + lane;
+        i0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+        step = (int64_t)gridDim.x * (blockDim.x >> 5);
+    } else {
+        b = blockIdx.y;
+        i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        step = (int64_t)gridDim.x * blockDim.x;
+    }
+}
+// the block's partial of sample b: BM sums the block's warps lane by lane (each lane one sample)
+template <bool BM>
+__device__ __forceinline__ void store_partial(double acc, double *part, int64_t b, int g, int32_t n_batch,
+                                              double *red_sh) {
+    if (!BM) {
+        const double s = block_sum(acc, red_sh);
+        if (threadIdx.x == 0) part[b * g + blockIdx.x] = s;
+        return;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    red_sh[warp * 32 + lane] = acc;
+    __syncthreads();
+    if (warp == 0) {
+        double s = 0.0;
+        for (int w = 0; w < nw; ++w) s += red_sh[w * 32 + lane];
+        if (b < n_batch) part[b * g + blockIdx.x] = s;
+    }
+}
+
+template <class R, int MODEL, bool BM>
 __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const int64_t nt, const int64_t n_cons,
                                                            const int64_t x_stride, const int wi, const double cmu,
                                                            const double clam, const double rgx, const double rgy,
                                                            const double rgz, const int ge, const int sh,
-                                                           const int64_t n_own, const double idt2) {
+                                                           const int64_t n_own, const double idt2,
+                                                           const int32_t n_batch) {
     using R4 = typename RT<R>::R4;
-    __shared__ double red_sh[32];
-    const int64_t b = blockIdx.y;
+    __shared__ double red_sh[kRedBlock];
+    int64_t b, i0, istep;
+    item_range<BM>(b, i0, istep);
     const void *x = L.xbuf[wi];
     const double r_mu = cmu / (cmu + clam);  // mu / lambdahat, independent of E
     double acc = 0.0;
     const int64_t n_items = nt + n_cons + (idt2 > 0.0 ? n_own : 0);
-    for (int64_t item = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; item < n_items;
-         item += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t item = i0; item < n_items; item += istep) {
         if (item >= nt + n_cons) {  // backward Euler: inertia m_i/(2 dt^2) |x_i - xtilde_i|^2 of owned free nodes
             const int64_t v = item - nt - n_cons;
             const R4 xv = pos_load<R>(x, b, v, x_stride, sh);
@@ -2108,28 +2146,28 @@ __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const
                           C[2] * (kxz * C[0] + kyz * C[1] + kzz * C[2]));
         }
     }
-    const double s = block_sum(acc, red_sh);
-    if (threadIdx.x == 0) L.part_e[b * ge + blockIdx.x] = s;
+    store_partial<BM>(acc, L.part_e, b, ge, n_batch, red_sh);
 }
 
-template <class R, int MODEL, bool FEXT, bool WC>
+template <class R, int MODEL, bool FEXT, bool WC, bool BM>
 __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, const int64_t n_chunks,
                                                              const int64_t x_stride, const int wi, const double cmu,
                                                              const double clam, const int gr, const int sh,
-                                                             const double idt2, const bool path) {
+                                                             const double idt2, const bool path,
+                                                             const int32_t n_batch) {
     using R4 = typename RT<R>::R4;
-    __shared__ double red_sh[32];
-    const int64_t b = blockIdx.y;
+    __shared__ double red_sh[kRedBlock];
+    int64_t b, i0, istep;
+    item_range<BM>(b, i0, istep);
     const void *x = L.xbuf[wi];
     double acc = 0.0;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_chunks * kChunk;
-         t += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t t = i0; t < n_chunks * kChunk; t += istep) {
         const int64_t chunk = t >> 5;
-        const int lane = (int)(t & 31);
+        const int cl = (int)(t & 31);  // the vertex's lane in its chunk
         const int2 cv = L.chunk_v[chunk];
-        if (lane >= cv.y) continue;
-        const int v = cv.x + lane;
-        const int64_t base = L.chunk_off[chunk] + lane;
+        if (cl >= cv.y) continue;
+        const int v = cv.x + cl;
+        const int64_t base = L.chunk_off[chunk] + cl;
         const int deg = L.deg[v];
         const R4 xa4 = pos_load<R>(x, b, v, x_stride, sh);
         const double xa[3] = {xa4.x, xa4.y, xa4.z};
@@ -2169,8 +2207,7 @@ __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, con
         if (idt2 > 0.0) inertia_contrib<R, double>(L, v, pos_load<R>(L.xtilde, b, v, x_stride, sh), idt2, xa, f, A);
         acc += f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
     }
-    const double s = block_sum(acc, red_sh);
-    if (threadIdx.x == 0) L.part_r[b * gr + blockIdx.x] = s;
+    store_partial<BM>(acc, L.part_r, b, gr, n_batch, red_sh);
 }
 
 __global__ void __launch_bounds__(kRedBlock) reduce_kernel(const Layout L, const int ge, const int gr) {
@@ -2188,20 +2225,34 @@ __global__ void __launch_bounds__(kRedBlock) reduce_kernel(const Layout L, const
     }
 }
 
-template <class R, int MODEL>
-cudaError_t energy_dispatch(const Problem &p, const Layout &L, int wi, cudaStream_t st) {
-    energy_kernel<R, MODEL><<<dim3(p.ge, p.n_batch), kRedBlock, 0, st>>>(
-        L, p.n_tets, p.n_cons, p.x_stride, wi, p.cmu, p.clam, p.rho_g[0], p.rho_g[1], p.rho_g[2], p.ge, p.lane_shift, p.n_own, p.inv_dt2);
-    dim3 gr(p.gr, p.n_batch);
+template <class R, int MODEL, bool BM>
+cudaError_t energy_residual_launch(const Problem &p, const Layout &L, int wi, cudaStream_t st) {
+    const unsigned rows = BM ? (unsigned)((p.n_batch + 31) / 32) : (unsigned)p.n_batch;
+    energy_kernel<R, MODEL, BM><<<dim3(p.ge, rows), kRedBlock, 0, st>>>(
+        L, p.n_tets, p.n_cons, p.x_stride, wi, p.cmu, p.clam, p.rho_g[0], p.rho_g[1], p.rho_g[2], p.ge, p.lane_shift,
+        p.n_own, p.inv_dt2, p.n_batch);
+    dim3 gr(p.gr, rows);
+    const auto a = std::make_tuple(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2, p.path,
+                                   p.n_batch);
+    auto go = [&](auto kern) {
+        std::apply([&](auto... xs) { kern<<<gr, kRedBlock, 0, st>>>(xs...); }, a);
+    };
     if (p.has_fext) {
-        if (p.has_wc) residual_kernel<R, MODEL, true, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2, p.path);
-        else residual_kernel<R, MODEL, true, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2, p.path);
+        if (p.has_wc) go(residual_kernel<R, MODEL, true, true, BM>);
+        else go(residual_kernel<R, MODEL, true, false, BM>);
     } else {
-        if (p.has_wc) residual_kernel<R, MODEL, false, true><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2, p.path);
-        else residual_kernel<R, MODEL, false, false><<<gr, kRedBlock, 0, st>>>(L, p.n_chunks, p.x_stride, wi, p.cmu, p.clam, p.gr, p.lane_shift, p.inv_dt2, p.path);
+        if (p.has_wc) go(residual_kernel<R, MODEL, false, true, BM>);
+        else go(residual_kernel<R, MODEL, false, false, BM>);
     }
     reduce_kernel<<<p.n_batch, kRedBlock, 0, st>>>(L, p.ge, p.gr);
     return cudaGetLastError();
+}
+
+template <class R, int MODEL>
+cudaError_t energy_dispatch(const Problem &p, const Layout &L, int wi, cudaStream_t st) {
+    // batched layouts: a warp covers one item for 32 samples (coalesced sample-minor loads)
+    if (p.lane_shift >= 5) return energy_residual_launch<R, MODEL, true>(p, L, wi, st);
+    return energy_residual_launch<R, MODEL, false>(p, L, wi, st);
 }
 
 // test hook: R(F) of the device polar decomposition for n matrices (pbng_test_polar)

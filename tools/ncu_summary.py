@@ -130,14 +130,16 @@ def main():
                      f"{g('sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active')[0]} | {g('sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active')[0]} | "
                      f"{g('smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio')[0]} |")
     n = max(len(kern), 1)
-    alg = bench["roofline"]["algorithmic_bytes_per_launch"]
+    rf = bench["roofline"]
+    alg = rf["hbm"]["algorithmic_bytes_per_launch"] if "hbm" in rf else rf["algorithmic_bytes_per_launch"]
     lines += ["", f"Mean DRAM traffic per sweep launch (ncu): **{tot_b/n/1e6:.1f} MB**; algorithmic bytes per launch "
               f"(bench.py model, DESIGN.md): **{alg/1e6:.1f} MB** (ratio {tot_b/n/alg:.3f}).",
               f"ncu DRAM bandwidth over the iteration: {tot_b/tot_t/1e3:.0f} GB/s (cold cache, serialised launches).",
               f"FLOP rate over the iteration (SASS add + mul + 2 fma): FP32 {fl['f']/tot_t/1e6:.2f} TFLOP/s, "
-              f"FP64 {fl['d']/tot_t/1e6:.2f} TFLOP/s (derived peaks: FP32 74.4, FP64 37.2 TFLOP/s at 1965 MHz; scalar "
-              "FADD/FMUL/FFMA thread-op counters: the packed FP32x2 FFMA2/FADD2/FMUL2 of the FCR and batched NH kernels have "
-              "no counter in this ncu set, so those kernels are under-counted).", "",
+              f"FP64 {fl['d']/tot_t/1e6:.2f} TFLOP/s from the scalar FADD/FMUL/FFMA counters of this set; the packed "
+              "FFMA2/FADD2/FMUL2 ops are counted by tools/flop_count.py (profiles/sweep_flops.json), and bench.py's ALU "
+              "fraction uses those counts against the measured peaks of profiles/alu_peaks.json (FP32 73.4-74.0, FP64 33.9 "
+              "TFLOP/s).", "",
               "## Launch list (share of GPU time, all launches of the command)", "",
               "| kernel | launches | total us | share |", "|---|---|---|---|"]
     for name, c, t, sh in shares:
