@@ -11,10 +11,14 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
+#include <thread>
 #include <new>
 #include <string>
 #include <utility>
@@ -27,6 +31,19 @@ using namespace pbng;
 namespace {
 
 thread_local std::string g_err = "no error";
+
+// PBNG_TIMING=1: host phase timings of the constraint-update path on stderr (tools/contact_timing.py)
+struct PhaseTimer {
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    PhaseTimer() : on(getenv("PBNG_TIMING") && atoi(getenv("PBNG_TIMING")) != 0), t0(std::chrono::steady_clock::now()) {}
+    void lap(const char *what) {
+        if (!on) return;
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[pbng] %-32s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    }
+};
 
 pbng_status fail(pbng_status s, const std::string &msg) {
     g_err = msg;
@@ -54,6 +71,21 @@ struct DevGuard {
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// fn(lo, hi) over [0, n) in contiguous blocks on up to 16 host threads (independent iterations only; the
+// result must not depend on the split -- every caller writes disjoint outputs per index)
+template <class F>
+void parallel_for(int64_t n, F &&fn, int64_t min_per_thread = 4096) {
+    const int64_t hw = std::max<int64_t>(1, std::min<int64_t>(16, (int64_t)std::thread::hardware_concurrency()));
+    const int64_t nt = std::max<int64_t>(1, std::min<int64_t>(hw, n / std::max<int64_t>(min_per_thread, 1)));
+    if (nt <= 1) {
+        fn((int64_t)0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int64_t k = 0; k < nt; ++k) th.emplace_back([&, k] { fn(n * k / nt, n * (k + 1) / nt); });
+    for (auto &t : th) t.join();
+}
 
 double det3(const double *M) {
     return M[0] * (M[4] * M[8] - M[5] * M[7]) - M[1] * (M[3] * M[8] - M[5] * M[6]) +
@@ -146,6 +178,9 @@ struct pbng_ctx {
     std::vector<int2> h_rec_id2;   // path-ordered NH records: {id | drop << 30, VE bits} (Problem::path)
     std::vector<int2> h_path0;     // path-ordered NH records: per free vertex the slots S1, S2 before record 0
     bool path_rec = false;
+    std::vector<int64_t> inc_off;  // vertex -> incident tets (ascending), mesh-only: built once and kept
+    std::vector<int32_t> inc;
+    void *stage2 = nullptr;  // second staging buffer (device re-layout of pbng_update_constraints)
     size_t wc_cap = 0, vc_cap = 0, deps_cap = 0;  // weak-constraint / pipeline-dependency room in the workspace
     int64_t n_records = 0;         // pair records stored per sweep (path mode: incl. load-only ones)
     std::vector<unsigned char> h_rec_a, h_rec_b, h_rec_c, h_fext, h_wc_d, h_c_w, h_c_anchor, h_c_K, h_tet_a,
@@ -159,7 +194,9 @@ struct pbng_ctx {
     // vertices {vertex, body}, internal ids; tri_orig = the triangles' original vertex ids
     std::vector<int4> h_surf;
     std::vector<int2> h_sv;
-    std::vector<int32_t> surf_orig;
+    std::vector<int32_t> surf_orig;                  // boundary triangles in original ids (mesh-only, cached)
+    std::vector<int32_t> surf_body, surf_verts, surf_vbody;  // per triangle body; boundary vertices and bodies
+    bool surf_cached = false;
     std::vector<int64_t> pin_order;  // caller order of the pinned set -> ascending order (set_constraints)
     uint64_t ws_bytes = 0;           // bytes of the bound workspace
     bool l2_persist = false;         // pbng_set_l2_persistence (re-applied by every bind)
@@ -176,7 +213,7 @@ struct pbng_ctx {
     Region r_rec_id, r_rec_a, r_rec_b, r_rec_c, r_chunk_off, r_chunk_v, r_deg, r_fext, r_wc_off, r_wc_cid, r_wc_d,
         r_c_n, r_c_node, r_c_w, r_c_anchor, r_c_K, r_tet_id, r_tet_a, r_tet_b, r_tet_c, r_int2orig, r_targets,
         r_x[3], r_stage, r_part_e, r_part_r, r_results, r_flag, r_halo_send, r_halo_recv, r_mass, r_xt, r_dep_off,
-        r_deps, r_pipe, r_surf, r_sv, r_chead, r_cnext, r_cres, r_cscal, r_hsend, r_hrecv, r_allred, r_path0;
+        r_deps, r_pipe, r_surf, r_sv, r_chead, r_cnext, r_cres, r_cscal, r_hsend, r_hrecv, r_allred, r_path0, r_stage2;
     size_t ws_need = 0;
     // bound device state
     bool bound = false;
@@ -365,11 +402,41 @@ struct PathRec {
     int drop;
     int32_t slot[3];
 };
-void vertex_path_records(const std::vector<std::array<int32_t, 3>> &tri, uint32_t seed, std::vector<PathRec> &out,
-                         int32_t path0[2]) {
+// Path covers depend only on the link's structure, so they are memoised per thread by a canonical key
+// (vertex labels replaced by order of first appearance); the retry seed is a hash of that key, so the
+// result is a pure function of the structure -- independent of thread count, memo state and vertex id.
+struct PathMemo {
+    std::unordered_map<std::string, std::vector<std::vector<int>>> m;
+};
+void vertex_path_records(const std::vector<std::array<int32_t, 3>> &tri, uint32_t /*unused*/, std::vector<PathRec> &out,
+                         int32_t path0[2], PathMemo *memo = nullptr) {
     out.clear();
+    std::string key;
+    {
+        std::vector<std::pair<int32_t, unsigned char>> seen;
+        key.reserve(3 * tri.size());
+        for (const auto &t : tri)
+            for (int a = 0; a < 3; ++a) {
+                unsigned char id = 0xff;
+                for (const auto &pv : seen)
+                    if (pv.first == t[a]) id = pv.second;
+                if (id == 0xff) {
+                    id = (unsigned char)std::min<size_t>(seen.size(), 0xfe);
+                    seen.push_back({t[a], id});
+                }
+                key.push_back((char)id);
+            }
+    }
+    uint32_t seed = 2166136261u;
+    for (char ch : key) seed = (seed ^ (unsigned char)ch) * 16777619u;
     std::vector<std::vector<int>> paths;
-    link_paths(tri, seed, paths);
+    auto hit = memo && tri.size() <= 250 ? memo->m.find(key) : (memo ? memo->m.end() : decltype(memo->m.end())());
+    if (memo && tri.size() <= 250 && hit != memo->m.end()) {
+        paths = hit->second;
+    } else {
+        link_paths(tri, seed, paths);
+        if (memo && tri.size() <= 250) memo->m.emplace(key, paths);
+    }
     int32_t S[3] = {-1, -1, -1};
     auto push = [&](int tet, int32_t vnew, int drop) {
         if (drop == 2) S[2] = S[1];
@@ -496,9 +563,7 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     c->path_rec = use_path_records(c);
     c->col_chunk.assign(c->ncol + 1, 0);
     c->h_deg.assign(c->n_free, 0);
-    std::vector<std::array<int32_t, 3>> link;
-    std::vector<PathRec> prec;
-    auto vertex_link = [&](int32_t o) {  // the three other vertices of each incident tet, in vt order
+    auto vertex_link = [&](int32_t o, std::vector<std::array<int32_t, 3>> &link) {  // other vertices per incident tet
         link.clear();
         for (int64_t q = vt_off[o]; q < vt_off[o + 1]; ++q) {
             const int32_t *t = c->tets.data() + 4 * vt[q];
@@ -510,18 +575,24 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
         }
     };
     if (c->path_rec) c->h_path0.assign((size_t)std::max<int64_t>(c->n_free, 1), make_int2(0, 0));
-    for (int64_t i = 0; i < c->n_free; ++i) {
-        const int32_t o = c->int2orig[i];
-        if (c->path_rec) {
-            vertex_link(o);
-            int32_t p0[2];
-            vertex_path_records(link, (uint32_t)o, prec, p0);
-            c->h_deg[i] = (int32_t)prec.size();
-            c->h_path0[i] = prec.empty() ? make_int2((int32_t)i, (int32_t)i) : make_int2(c->orig2int[p0[0]], c->orig2int[p0[1]]);
-        } else {
-            c->h_deg[i] = (int32_t)(vt_off[o + 1] - vt_off[o]);
+    parallel_for(c->n_free, [&](int64_t lo, int64_t hi) {
+        std::vector<std::array<int32_t, 3>> link;
+        std::vector<PathRec> prec;
+        PathMemo memo;
+        for (int64_t i = lo; i < hi; ++i) {
+            const int32_t o = c->int2orig[i];
+            if (c->path_rec) {
+                vertex_link(o, link);
+                int32_t p0[2];
+                vertex_path_records(link, (uint32_t)o, prec, p0, &memo);
+                c->h_deg[i] = (int32_t)prec.size();
+                c->h_path0[i] = prec.empty() ? make_int2((int32_t)i, (int32_t)i)
+                                             : make_int2(c->orig2int[p0[0]], c->orig2int[p0[1]]);
+            } else {
+                c->h_deg[i] = (int32_t)(vt_off[o + 1] - vt_off[o]);
+            }
         }
-    }
+    }, 1024);
     c->h_chunk_off.clear();
     c->h_chunk_v.clear();
     c->h_chunk_off.push_back(0);
@@ -566,16 +637,20 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     // rec_c: FCR g3z (+ VE in fp64); NH: VE in fp64, unused in fp32 (VE rides in rec_id.w)
     const size_t rec_c_bytes = nh ? (c->dtype == DT_F64 ? s : 0) : (c->dtype == DT_F64 ? 2 * s : s);
     c->h_rec_c.assign(std::max<size_t>((size_t)ns * rec_c_bytes, s), 0);
-    for (int64_t ch = 0; ch < n_chunks; ++ch) {
+    parallel_for(n_chunks, [&](int64_t ch_lo, int64_t ch_hi) {  // chunks write disjoint record slots
+    std::vector<std::array<int32_t, 3>> link;
+    std::vector<PathRec> prec;
+    PathMemo memo;
+    for (int64_t ch = ch_lo; ch < ch_hi; ++ch) {
         const int2 cv = c->h_chunk_v[ch];
         for (int32_t lane = 0; lane < cv.y; ++lane) {
             const int32_t vi = cv.x + lane, o = c->int2orig[vi];
             if (c->path_rec) {
                 // path-ordered records: slot order (S0, S1, S2) after the push; s'_k and det B' follow the
                 // slots (det B' = sgn(pi) det B keeps J and cof(F) g_i, pbng_kernels.cu "path records")
-                vertex_link(o);
+                vertex_link(o, link);
                 int32_t p0[2];
-                vertex_path_records(link, (uint32_t)o, prec, p0);
+                vertex_path_records(link, (uint32_t)o, prec, p0, &memo);
                 for (size_t k = 0; k < prec.size(); ++k) {
                     const PathRec &pr = prec[k];
                     const int64_t r = c->h_chunk_off[ch] + (int64_t)k * kChunk + lane;
@@ -666,6 +741,8 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
         }
     }
 
+    }, 64);
+
     // body force f^ext_i = sum_e R^0 g V_e / 4, free vertices
     const bool has_fext = c->density > 0 && (c->grav[0] != 0 || c->grav[1] != 0 || c->grav[2] != 0);
     c->h_fext.assign(has_fext ? (size_t)std::max<int64_t>(c->n_free, 1) * s4 : 0, 0);
@@ -751,7 +828,7 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
 void build_pipeline(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::vector<int32_t> &vt) {
     c->h_dep_off.assign((size_t)c->n_chunks + 1, 0);
     c->h_deps.clear();
-    if (c->n_ranks > 1) return;
+    if (c->n_ranks > 1 || c->path_rec) return;  // the pipelined schedule is unavailable (pipeline_available)
     std::vector<int32_t> chunk_of((size_t)std::max<int64_t>(c->n_free, 1), -1), chunk_col((size_t)std::max<int64_t>(c->n_chunks, 1), 0);
     for (int32_t col = 0; col < c->ncol; ++col)
         for (int64_t ch = c->col_chunk[col]; ch < c->col_chunk[col + 1]; ++ch) {
@@ -759,28 +836,37 @@ void build_pipeline(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::
             const int2 cv = c->h_chunk_v[ch];
             for (int32_t q = 0; q < cv.y; ++q) chunk_of[cv.x + q] = (int32_t)ch;
         }
-    std::vector<int32_t> tmp;
-    for (int64_t ch = 0; ch < c->n_chunks; ++ch) {
-        tmp.clear();
-        tmp.push_back((int32_t)ch);
-        const int2 cv = c->h_chunk_v[ch];
-        auto add = [&](int32_t j) {
-            if (j >= 0 && j < c->n_free) tmp.push_back(chunk_of[j]);
-        };
-        for (int32_t q = 0; q < cv.y; ++q) {
-            const int32_t i = cv.x + q, o = c->int2orig[i];
-            for (int64_t k = vt_off[o]; k < vt_off[o + 1]; ++k) {
-                const int32_t *t = c->tets.data() + 4 * vt[k];
-                for (int a = 0; a < 4; ++a) add(c->orig2int[t[a]]);
+    // per chunk in parallel (each thread its own "already listed" stamps), then concatenated in chunk order
+    std::vector<std::vector<int32_t>> lists((size_t)c->n_chunks);
+    parallel_for(c->n_chunks, [&](int64_t lo, int64_t hi) {
+        std::vector<int64_t> stamp((size_t)std::max<int64_t>(c->n_chunks, 1), -1);  // chunk already listed for ch
+        for (int64_t ch = lo; ch < hi; ++ch) {
+            std::vector<int32_t> &tmp = lists[ch];
+            tmp.push_back((int32_t)ch);
+            stamp[ch] = ch;
+            const int2 cv = c->h_chunk_v[ch];
+            auto add = [&](int32_t j) {
+                if (j >= 0 && j < c->n_free && stamp[chunk_of[j]] != ch) {
+                    stamp[chunk_of[j]] = ch;
+                    tmp.push_back(chunk_of[j]);
+                }
+            };
+            for (int32_t q = 0; q < cv.y; ++q) {
+                const int32_t i = cv.x + q, o = c->int2orig[i];
+                for (int64_t k = vt_off[o]; k < vt_off[o + 1]; ++k) {
+                    const int32_t *t = c->tets.data() + 4 * vt[k];
+                    for (int a = 0; a < 4; ++a) add(c->orig2int[t[a]]);
+                }
+                for (int32_t k = c->h_wc_off[i]; k < c->h_wc_off[i + 1]; ++k) {
+                    const int32_t cid = c->h_wc_cid[k];
+                    for (int32_t m = 0; m < c->h_c_n[cid]; ++m) add(c->h_c_node[kWcMaxNodes * cid + m]);
+                }
             }
-            for (int32_t k = c->h_wc_off[i]; k < c->h_wc_off[i + 1]; ++k) {
-                const int32_t cid = c->h_wc_cid[k];
-                for (int32_t m = 0; m < c->h_c_n[cid]; ++m) add(c->h_c_node[kWcMaxNodes * cid + m]);
-            }
+            std::sort(tmp.begin(), tmp.end());
         }
-        std::sort(tmp.begin(), tmp.end());
-        tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-        for (int32_t y : tmp) c->h_deps.push_back((y << 1) | (chunk_col[y] < chunk_col[ch] ? 1 : 0));
+    }, 64);
+    for (int64_t ch = 0; ch < c->n_chunks; ++ch) {
+        for (int32_t y : lists[ch]) c->h_deps.push_back((y << 1) | (chunk_col[y] < chunk_col[ch] ? 1 : 0));
         c->h_dep_off[ch + 1] = (int32_t)c->h_deps.size();
     }
 }
@@ -790,13 +876,41 @@ void build_pipeline(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::
 // (v1 - v0) x (v2 - v0) points towards local vertex k (include/pbng.h pbng_detect_contacts), and bodies
 // = connected components of tets sharing a vertex, labelled by their smallest vertex index.  Only for
 // an undecomposed context.
+void surface_original(pbng_ctx *c);
 void build_surface(pbng_ctx *c) {
     c->h_surf.clear();
     c->h_sv.clear();
-    c->surf_orig.clear();
     c->prob.n_surf = c->prob.n_sv = 0;
     c->prob.n_cbuckets = 1;
     if (c->n_ranks > 1 || c->nt == 0) return;
+#ifdef PBNG_NO_SURF_CACHE
+    c->surf_cached = false;
+#endif
+    if (!c->surf_cached) surface_original(c);  // mesh-only: computed once, re-laid out by id mapping
+    const size_t nf = c->surf_orig.size() / 3;
+    for (size_t f = 0; f < nf; ++f) {
+        const int32_t *v = &c->surf_orig[3 * f];
+        c->h_surf.push_back(make_int4(c->orig2int[v[0]], c->orig2int[v[1]], c->orig2int[v[2]], c->surf_body[f]));
+    }
+    std::vector<char> is_pinned((size_t)c->nv, 0);
+    for (int32_t p : c->pinned) is_pinned[p] = 1;
+    for (size_t k = 0; k < c->surf_verts.size(); ++k) {
+        const int32_t v = c->surf_verts[k];
+        if (!is_pinned[v]) c->h_sv.push_back(make_int2(c->orig2int[v], c->surf_vbody[k]));
+    }
+    c->prob.n_surf = (int64_t)c->h_surf.size();
+    c->prob.n_sv = (int64_t)c->h_sv.size();
+    int64_t nb = 1;
+    while (nb < 16 * std::max<int64_t>(c->prob.n_surf, 1)) nb <<= 1;
+    c->prob.n_cbuckets = nb;
+}
+
+// the boundary of the rest mesh in original ids (surf_orig, surf_body, surf_verts, surf_vbody)
+void surface_original(pbng_ctx *c) {
+    c->surf_orig.clear();
+    c->surf_body.clear();
+    c->surf_verts.clear();
+    c->surf_vbody.clear();
     const int64_t nt = c->nt, nv = c->nv;
     // union-find over vertices
     std::vector<int32_t> par((size_t)nv);
@@ -812,25 +926,48 @@ void build_surface(pbng_ctx *c) {
         }
     std::vector<int32_t> body((size_t)nv);
     for (int64_t v = 0; v < nv; ++v) body[v] = root((int32_t)v);  // the component's minimum vertex
-    // faces keyed by their sorted triple; a face is on the boundary iff its key occurs once
-    std::vector<std::pair<std::array<int32_t, 3>, int64_t>> key((size_t)(4 * nt));
+    // a face is on the boundary iff no other tet has the same vertex triple: faces are bucketed by their
+    // smallest vertex (CSR), and each bucket's few faces are matched on the other two (sorted) vertices
+    auto face_key = [&](int64_t e, int f, int32_t k[3]) {
+        int m = 0;
+        for (int a = 0; a < 4; ++a)
+            if (a != f) k[m++] = c->tets[4 * e + a];
+        std::sort(k, k + 3);
+    };
+    std::vector<int64_t> off((size_t)nv + 1, 0);
     for (int64_t e = 0; e < nt; ++e)
         for (int f = 0; f < 4; ++f) {
-            std::array<int32_t, 3> k;
-            int m = 0;
-            for (int a = 0; a < 4; ++a)
-                if (a != f) k[m++] = c->tets[4 * e + a];
-            std::sort(k.begin(), k.end());
-            key[4 * e + f] = {k, 4 * e + f};
+            int32_t k[3];
+            face_key(e, f, k);
+            off[k[0] + 1]++;
         }
-    std::sort(key.begin(), key.end());
+    for (int64_t v = 0; v < nv; ++v) off[v + 1] += off[v];
+    std::vector<int64_t> fid((size_t)(4 * nt)), fill(off.begin(), off.end() - 1);
+    for (int64_t e = 0; e < nt; ++e)
+        for (int f = 0; f < 4; ++f) {
+            int32_t k[3];
+            face_key(e, f, k);
+            fid[fill[k[0]]++] = 4 * e + f;
+        }
     std::vector<char> boundary((size_t)(4 * nt), 0);
-    for (size_t i = 0; i < key.size();) {
-        size_t j = i + 1;
-        while (j < key.size() && key[j].first == key[i].first) ++j;
-        if (j == i + 1) boundary[key[i].second] = 1;
-        i = j;
-    }
+    parallel_for(nv, [&](int64_t lo, int64_t hi) {
+        std::vector<std::pair<uint64_t, int64_t>> b;
+        for (int64_t v = lo; v < hi; ++v) {
+            b.clear();
+            for (int64_t q = off[v]; q < off[v + 1]; ++q) {
+                int32_t k[3];
+                face_key(fid[q] / 4, (int)(fid[q] % 4), k);
+                b.push_back({(uint64_t)(uint32_t)k[1] << 32 | (uint32_t)k[2], fid[q]});
+            }
+            std::sort(b.begin(), b.end());
+            for (size_t i = 0; i < b.size();) {
+                size_t j = i + 1;
+                while (j < b.size() && b[j].first == b[i].first) ++j;
+                if (j == i + 1) boundary[b[i].second] = 1;
+                i = j;
+            }
+        }
+    });
     std::vector<char> on_surf((size_t)nv, 0);
     for (int64_t e = 0; e < nt; ++e)
         for (int f = 0; f < 4; ++f) {
@@ -849,17 +986,14 @@ void build_surface(pbng_ctx *c) {
                 c->surf_orig.push_back(v[a]);
                 on_surf[v[a]] = 1;
             }
-            c->h_surf.push_back(make_int4(c->orig2int[v[0]], c->orig2int[v[1]], c->orig2int[v[2]], body[v[0]]));
+            c->surf_body.push_back(body[v[0]]);
         }
-    std::vector<char> is_pinned((size_t)nv, 0);
-    for (int32_t p : c->pinned) is_pinned[p] = 1;
     for (int64_t v = 0; v < nv; ++v)
-        if (on_surf[v] && !is_pinned[v]) c->h_sv.push_back(make_int2(c->orig2int[v], body[v]));
-    c->prob.n_surf = (int64_t)c->h_surf.size();
-    c->prob.n_sv = (int64_t)c->h_sv.size();
-    int64_t nb = 1;
-    while (nb < 16 * std::max<int64_t>(c->prob.n_surf, 1)) nb <<= 1;
-    c->prob.n_cbuckets = nb;
+        if (on_surf[v]) {
+            c->surf_verts.push_back((int32_t)v);
+            c->surf_vbody.push_back(body[v]);
+        }
+    c->surf_cached = true;
 }
 
 // Incremental recolouring of pbng_update_constraints: the nodes incident to the new
@@ -878,9 +1012,14 @@ std::vector<int32_t> recolour_incremental(const pbng_ctx *c, const std::vector<s
             if (is_new[q]) extra[v] = 1;
         }
     std::vector<std::vector<int32_t>> vtets((size_t)nv);
-    for (int64_t e = 0; e < nt; ++e)
-        for (int a = 0; a < 4; ++a)
-            if (extra[c->tets[4 * e + a]]) vtets[c->tets[4 * e + a]].push_back((int32_t)e);
+    if (!c->inc_off.empty()) {  // the cached incidence (ascending tet index, as the scan below)
+        for (int64_t v = 0; v < nv; ++v)
+            if (extra[v]) vtets[v].assign(c->inc.begin() + c->inc_off[v], c->inc.begin() + c->inc_off[v + 1]);
+    } else {
+        for (int64_t e = 0; e < nt; ++e)
+            for (int a = 0; a < 4; ++a)
+                if (extra[c->tets[4 * e + a]]) vtets[c->tets[4 * e + a]].push_back((int32_t)e);
+    }
     int32_t ncol = 0;
     for (int32_t k : col) ncol = std::max(ncol, k + 1);
     *changed = 0;
@@ -968,6 +1107,17 @@ void plan_workspace(pbng_ctx *c) {
     };
     const Problem &p = c->prob;
     const size_t s = c->real_size(), s4 = c->real4_size();
+    // position buffers and staging first: their offsets depend only on (n_batch, vertices held, dtype,
+    // layout shift), so a re-layout with the same vertex set (pbng_update_constraints) leaves them in place
+    // and the iterate can be carried over on the device
+    {
+        size_t groups = (size_t)((c->nb + (1 << p.lane_shift) - 1) >> p.lane_shift);
+        if (p.lane_shift == 5) groups += groups & 1;
+        for (int k = 0; k < 3; ++k) take(c->r_x[k], (groups << p.lane_shift) * (size_t)p.x_stride * s4);
+        take(c->r_xt, (groups << p.lane_shift) * (size_t)p.x_stride * s4);
+        take(c->r_stage, (size_t)c->nb * (size_t)c->nv * 3 * s);
+        take(c->r_stage2, (size_t)c->nb * (size_t)c->nv * 3 * s);
+    }
     const int64_t ns = std::max<int64_t>(c->n_slots, 1);
     take(c->r_rec_id, (size_t)ns * (c->path_rec ? 8 : 16));
     take(c->r_path0, c->h_path0.size() * 8);
@@ -998,16 +1148,13 @@ void plan_workspace(pbng_ctx *c) {
     take(c->r_tet_c, c->h_tet_c.size());
     take(c->r_int2orig, (size_t)std::max<int64_t>(c->n_local, 1) * 4);
     take(c->r_targets, c->h_targets.size());
-    size_t groups = (size_t)((c->nb + (1 << p.lane_shift) - 1) >> p.lane_shift);
-    if (p.lane_shift == 5) groups += groups & 1;  // an even number of sample groups (sweep_batched2_kernel)
-    for (int k = 0; k < 3; ++k) take(c->r_x[k], (groups << p.lane_shift) * (size_t)p.x_stride * s4);
-    take(c->r_stage, (size_t)c->nb * (size_t)c->nv * 3 * s);
+
     take(c->r_part_e, (size_t)c->nb * p.ge * 8);
     take(c->r_part_r, (size_t)c->nb * p.gr * 8);
     take(c->r_results, (size_t)c->nb * 2 * 8);
     take(c->r_flag, 4);
     take(c->r_mass, c->h_mass.size());
-    take(c->r_xt, (groups << p.lane_shift) * (size_t)p.x_stride * s4);
+
     take(c->r_halo_send, std::max<size_t>(c->h_halo_send.size(), 1) * 4);
     take(c->r_halo_recv, std::max<size_t>(c->h_halo_recv.size(), 1) * 4);
     take(c->r_dep_off, c->h_dep_off.size() * 4);
@@ -1695,22 +1842,30 @@ pbng_status pbng_set_constraints(pbng_ctx *c, const int32_t *pinned, int64_t n_p
 
 // colouring (greedy, or `given` -- the incremental recolouring of pbng_update_constraints) and the
 // colour-sorted device layout it implies
+// vertex -> incident tets in ascending tet index (CSR), cached in the context (the mesh never changes)
+static void incidence(pbng_ctx *c) {
+    const int64_t nv = c->nv, nt = c->nt;
+    c->inc_off.assign((size_t)nv + 1, 0);
+    for (int64_t e = 0; e < nt; ++e)
+        for (int a = 0; a < 4; ++a) c->inc_off[c->tets[4 * e + a] + 1]++;
+    for (int64_t v = 0; v < nv; ++v) c->inc_off[v + 1] += c->inc_off[v];
+    c->inc.assign((size_t)std::max<int64_t>(c->inc_off[nv], 1), 0);
+    std::vector<int64_t> fill(c->inc_off.begin(), c->inc_off.end() - 1);
+    for (int64_t e = 0; e < nt; ++e)
+        for (int a = 0; a < 4; ++a) c->inc[fill[c->tets[4 * e + a]]++] = (int32_t)e;
+}
+
 static pbng_status colour_and_layout(pbng_ctx *c, const std::vector<int32_t> *given) {
     drop_dd_graph(c);
     c->layout_gen += 1;
+    PhaseTimer T;
     try {
         const int64_t nv = c->nv, nt = c->nt, nwc = (int64_t)c->wc.size();
         // vertex -> incident tets (ascending tet index) and vertex -> stencils (tets, then constraints)
-        std::vector<int64_t> vt_off((size_t)nv + 1, 0), vs_off((size_t)nv + 1, 0);
-        for (int64_t e = 0; e < nt; ++e)
-            for (int a = 0; a < 4; ++a) vt_off[c->tets[4 * e + a] + 1]++;
-        for (int64_t v = 0; v < nv; ++v) vt_off[v + 1] += vt_off[v];
-        std::vector<int32_t> vt((size_t)std::max<int64_t>(vt_off[nv], 1));
-        {
-            std::vector<int64_t> fill(vt_off.begin(), vt_off.end() - 1);
-            for (int64_t e = 0; e < nt; ++e)
-                for (int a = 0; a < 4; ++a) vt[fill[c->tets[4 * e + a]]++] = (int32_t)e;
-        }
+        if (c->inc_off.empty()) incidence(c);
+        const std::vector<int64_t> &vt_off = c->inc_off;
+        const std::vector<int32_t> &vt = c->inc;
+        std::vector<int64_t> vs_off((size_t)nv + 1, 0);
         std::vector<std::vector<int32_t>> cnodes((size_t)nwc);
         for (int64_t q = 0; q < nwc; ++q) {
             const pbng_weak_constraint &w = c->wc[q];
@@ -1737,6 +1892,7 @@ static pbng_status colour_and_layout(pbng_ctx *c, const std::vector<int32_t> *gi
         for (int64_t v = 0; v < nv; ++v)
             if (!is_pinned[v] && vs_off[v + 1] == vs_off[v])
                 return fail(PBNG_E_ISOLATED_VERTEX, "color: free vertex " + std::to_string(v) + " has no element or constraint");
+        T.lap("layout: incidence + stencils");
         if (given) {
             c->colour = *given;
             c->ncol = 0;
@@ -1886,10 +2042,14 @@ static pbng_status colour_and_layout(pbng_ctx *c, const std::vector<int32_t> *gi
         c->h_halo_recv.resize(c->halo_recv_orig.size());
         for (size_t q = 0; q < c->halo_send_orig.size(); ++q) c->h_halo_send[q] = c->orig2int[c->halo_send_orig[q]];
         for (size_t q = 0; q < c->halo_recv_orig.size(); ++q) c->h_halo_recv[q] = c->orig2int[c->halo_recv_orig[q]];
+        T.lap("layout: colouring + ownership + order");
         if (c->dtype == DT_F64) build_layout<double>(c, vt_off, vt);
         else build_layout<float>(c, vt_off, vt);
+        T.lap("layout: records");
         build_pipeline(c, vt_off, vt);
+        T.lap("layout: pipeline dependencies");
         build_surface(c);
+        T.lap("layout: surface");
         plan_workspace(c);
     } catch (const std::bad_alloc &) {
         return fail(PBNG_E_OUT_OF_MEMORY, "color: host allocation");
@@ -1918,13 +2078,12 @@ pbng_status pbng_workspace_bytes(pbng_ctx *c, uint64_t *bytes) {
     return PBNG_OK;
 }
 
-pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
-    pbng_status st = require_device(c);
-    if (st != PBNG_OK) return st;
-    if (!c->colored) return fail(PBNG_E_NOT_COLORED, "bind_workspace: call pbng_color first");
-    if (!dptr || (reinterpret_cast<uintptr_t>(dptr) & 255u) != 0)
-        return fail(PBNG_E_INVALID_ARGUMENT, "bind_workspace: pointer must be non-null and 256-byte aligned");
-    if (bytes < c->ws_need) return fail(PBNG_E_OUT_OF_MEMORY, "bind_workspace: workspace smaller than pbng_workspace_bytes");
+}  // extern "C"
+
+// Upload the host images into the workspace and point the layout at it.  fresh = false (re-layout of
+// pbng_update_constraints): the position, inertial-target and staging regions, which sit first at offsets
+// the re-layout does not change, are left alone, and the iterate state is kept.
+static pbng_status bind_layout(pbng_ctx *c, void *dptr, uint64_t bytes, bool fresh) {
     DevGuard g(c->device);
     char *base = static_cast<char *>(dptr);
     auto at = [&](const Region &r) { return static_cast<void *>(base + r.off); };
@@ -1956,6 +2115,7 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     L.targets = at(c->r_targets);
     for (int k = 0; k < 3; ++k) L.xbuf[k] = at(c->r_x[k]);
     L.stage = at(c->r_stage);
+    c->stage2 = at(c->r_stage2);
     L.part_e = static_cast<double *>(at(c->r_part_e));
     L.part_r = static_cast<double *>(at(c->r_part_r));
     L.results = static_cast<double *>(at(c->r_results));
@@ -2011,10 +2171,12 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     chk(up(c->r_sv, c->h_sv.data(), c->h_sv.size() * 8));
     chk(up(c->r_dep_off, c->h_dep_off.data(), c->h_dep_off.size() * 4));
     chk(up(c->r_deps, c->h_deps.data(), c->h_deps.size() * 4));
-    chk(cudaMemsetAsync(base + c->r_flag.off, 0, 4, c->stream));
-    // position buffers start at zero: padding rows / lanes (x_stride, sample groups) are then finite
-    for (int k = 0; k < 3; ++k) chk(cudaMemsetAsync(base + c->r_x[k].off, 0, c->r_x[k].bytes, c->stream));
-    chk(cudaMemsetAsync(base + c->r_xt.off, 0, c->r_xt.bytes, c->stream));
+    if (fresh) {
+        chk(cudaMemsetAsync(base + c->r_flag.off, 0, 4, c->stream));
+        // position buffers start at zero: padding rows / lanes (x_stride, sample groups) are then finite
+        for (int k = 0; k < 3; ++k) chk(cudaMemsetAsync(base + c->r_x[k].off, 0, c->r_x[k].bytes, c->stream));
+        chk(cudaMemsetAsync(base + c->r_xt.off, 0, c->r_xt.bytes, c->stream));
+    }
     chk(cudaStreamSynchronize(c->stream));
     if (e != cudaSuccess) return cuda_fail(e, "bind_workspace");
     drop_dd_graph(c);  // a captured iterate block holds the old layout and buffers
@@ -2023,9 +2185,21 @@ pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
     c->ws_bytes = bytes;
     c->L = L;
     c->bound = true;
-    c->positions_set = false;
-    if (c->l2_persist) return apply_l2_persistence(c, 1);  // the position buffers may have moved
+    if (fresh) c->positions_set = false;
+    if (c->l2_persist && fresh) return apply_l2_persistence(c, 1);  // the position buffers may have moved
     return PBNG_OK;
+}
+
+extern "C" {
+
+pbng_status pbng_bind_workspace(pbng_ctx *c, void *dptr, uint64_t bytes) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    if (!c->colored) return fail(PBNG_E_NOT_COLORED, "bind_workspace: call pbng_color first");
+    if (!dptr || (reinterpret_cast<uintptr_t>(dptr) & 255u) != 0)
+        return fail(PBNG_E_INVALID_ARGUMENT, "bind_workspace: pointer must be non-null and 256-byte aligned");
+    if (bytes < c->ws_need) return fail(PBNG_E_OUT_OF_MEMORY, "bind_workspace: workspace smaller than pbng_workspace_bytes");
+    return bind_layout(c, dptr, bytes, true);
 }
 
 pbng_status pbng_set_positions(pbng_ctx *c, const void *x) {
@@ -2451,6 +2625,7 @@ static pbng_status update_constraints_in_place(pbng_ctx *c, const double *pinned
     }
     for (int64_t i = 0; i < c->n_free; ++i)
         if (c->h_deg[i] == 0 && !touched[c->int2orig[i]]) return fail(PBNG_E_OUT_OF_MEMORY, "update_constraints: re-layout");
+    PhaseTimer T;
     const std::vector<pbng_weak_constraint> old_wc = c->wc;
     const std::vector<int32_t> old_local = c->cons_local;
     const int64_t old_owned = c->n_cons_owned;
@@ -2460,17 +2635,12 @@ static pbng_status update_constraints_in_place(pbng_ctx *c, const double *pinned
     c->n_cons_owned = n_wc;
     if (c->dtype == DT_F64) build_constraint_arrays<double>(c);
     else build_constraint_arrays<float>(c);
+    T.lap("in place: constraint arrays");
     const bool deps = pipeline_available(c);
     if (deps) {
-        std::vector<int64_t> vt_off((size_t)c->nv + 1, 0);
-        for (int64_t e = 0; e < c->nt; ++e)
-            for (int a = 0; a < 4; ++a) vt_off[c->tets[4 * e + a] + 1]++;
-        for (int64_t v = 0; v < c->nv; ++v) vt_off[v + 1] += vt_off[v];
-        std::vector<int32_t> vt((size_t)std::max<int64_t>(vt_off[c->nv], 1));
-        std::vector<int64_t> fill(vt_off.begin(), vt_off.end() - 1);
-        for (int64_t e = 0; e < c->nt; ++e)
-            for (int a = 0; a < 4; ++a) vt[fill[c->tets[4 * e + a]]++] = (int32_t)e;
-        build_pipeline(c, vt_off, vt);
+        if (c->inc_off.empty()) incidence(c);
+        build_pipeline(c, c->inc_off, c->inc);
+        T.lap("in place: pipeline dependencies");
     }
     if (c->h_c_n.size() > c->wc_cap || c->h_wc_cid.size() > c->vc_cap || (deps && c->h_deps.size() > c->deps_cap)) {
         c->wc = old_wc;  // no headroom: leave the context as it was for the re-layout
@@ -2534,6 +2704,7 @@ static pbng_status update_constraints_in_place(pbng_ctx *c, const double *pinned
         }
     }
     chk(cudaStreamSynchronize(c->stream));  // the host images are rewritten by the next update
+    T.lap("in place: upload");
     if (e != cudaSuccess) return cuda_fail(e, "update_constraints: upload");
     c->cur_accel = -1;
     return PBNG_OK;
@@ -2552,10 +2723,10 @@ pbng_status pbng_update_constraints(pbng_ctx *c, const double *pinned_xyz, const
     if (pinned_xyz)
         for (int64_t k = 0; k < (int64_t)c->nb * np * 3; ++k)
             if (!std::isfinite(pinned_xyz[k])) return fail(PBNG_E_INVALID_ARGUMENT, "update_constraints: non-finite target");
+    PhaseTimer T;
     pbng_status st = validate_wc(c, wc, n_wc, "update_constraints");
     if (st != PBNG_OK) return st;
     const bool keep = c->bound && c->positions_set;
-    std::vector<unsigned char> saved, saved_xt;
     int64_t changed = 0;
     try {
         // "newly added" = node set not present among the previous constraints (removed ones only relax)
@@ -2567,28 +2738,33 @@ pbng_status pbng_update_constraints(pbng_ctx *c, const double *pinned_xyz, const
             nodes[q] = distinct_nodes(wc[q]);
             is_new[q] = !std::binary_search(old_nodes.begin(), old_nodes.end(), nodes[q]);
         }
+        T.lap("update: new-constraint sets");
         std::vector<int32_t> col = recolour_incremental(c, nodes, is_new, &changed);
+        T.lap("update: incremental recolouring");
         if (changed == 0 && c->bound) {
             st = update_constraints_in_place(c, pinned_xyz, wc, n_wc);
+            T.lap("update: in place");
             if (st == PBNG_OK) {
                 if (n_recoloured) *n_recoloured = 0;
                 return PBNG_OK;
             }
             if (st != PBNG_E_OUT_OF_MEMORY) return st;  // no headroom left: fall through to the re-layout
         }
+        // re-layout.  The position, inertial-target and staging regions sit first in the workspace at offsets
+        // the re-layout keeps, so the iterate (stage) and the backward-Euler target (stage2) are carried
+        // over on the device in original vertex order; nothing goes through the host.
         const double idt2 = c->prob.inv_dt2;
-        if (keep && idt2 > 0.0) {  // the backward-Euler target, original order (restored with the iterate)
+        const bool was_bound = c->bound;
+        void *ws = c->ws;
+        const uint64_t ws_bytes = c->ws_bytes;
+        const size_t fixed_end = c->r_stage2.off + c->r_stage2.bytes;
+        if (keep) {
             DevGuard g(c->device);
-            saved_xt.resize((size_t)c->nb * c->nv * 3 * c->real_size());
-            PBNG_CUDA(launch_get_positions(c->prob, c->L, -1, c->stream), "update_constraints: inertial target");
-            PBNG_CUDA(cudaMemcpyAsync(saved_xt.data(), c->L.stage, saved_xt.size(), cudaMemcpyDeviceToHost, c->stream),
-                      "update_constraints: copy");
-            PBNG_CUDA(cudaStreamSynchronize(c->stream), "update_constraints: synchronize");
-        }
-        if (keep) {  // the current iterate, original order (restored after the re-layout)
-            saved.resize((size_t)c->nb * c->nv * 3 * c->real_size());
-            st = pbng_get_positions(c, saved.data());
-            if (st != PBNG_OK) return st;
+            Layout L2 = c->L;
+            L2.stage = c->stage2;
+            if (idt2 > 0.0) PBNG_CUDA(launch_get_positions(c->prob, L2, -1, c->stream), "update_constraints: inertial target");
+            PBNG_CUDA(launch_get_positions(c->prob, c->L, c->work, c->stream), "update_constraints: iterate");
+            c->launches += idt2 > 0.0 ? 2 : 1;
         }
         c->wc.assign(wc, wc + n_wc);
         if (pinned_xyz)
@@ -2596,29 +2772,45 @@ pbng_status pbng_update_constraints(pbng_ctx *c, const double *pinned_xyz, const
                 for (int64_t b = 0; b < c->nb; ++b)
                     for (int a = 0; a < 3; ++a)
                         c->targets[3 * (b * np + k) + a] = pinned_xyz[3 * (b * np + c->pin_order[k]) + a];
-        const bool was_bound = c->bound;
-        void *ws = c->ws;
-        const uint64_t ws_bytes = c->ws_bytes;
+        T.lap("update: save iterate (device)");
         st = colour_and_layout(c, &col);
+        T.lap("update: re-layout (host)");
         if (st != PBNG_OK) return st;
         if (n_recoloured) *n_recoloured = changed;
-        c->prob.inv_dt2 = 0.0;
         if (was_bound) {
-            if (c->ws_need > ws_bytes)
+            if (c->ws_need > ws_bytes) {
+                c->prob.inv_dt2 = 0.0;
                 return fail(PBNG_E_OUT_OF_MEMORY, "update_constraints: the new layout needs " + std::to_string(c->ws_need) +
                                                       " workspace bytes; bind a larger workspace and set positions");
-            st = pbng_bind_workspace(c, ws, ws_bytes);
+            }
+            if (c->r_stage2.off + c->r_stage2.bytes != fixed_end)
+                return fail(PBNG_E_INVALID_ARGUMENT, "update_constraints: position regions moved (internal error)");
+            st = bind_layout(c, ws, ws_bytes, !keep);
             if (st != PBNG_OK) return st;
             if (keep) {
-                if (!saved_xt.empty()) {  // carry the backward-Euler target over to the new layout
-                    st = pbng_set_inertia(c, 1.0 / std::sqrt(idt2), saved_xt.data());
-                    if (st != PBNG_OK) return st;
-                }
-                st = pbng_set_positions(c, saved.data());
-                if (st != PBNG_OK) return st;
                 DevGuard g(c->device);
+                c->prob.inv_dt2 = idt2;  // carried over: the target is restored from stage2 below
+                if (idt2 > 0.0) {
+                    Layout L2 = c->L;
+                    L2.stage = c->stage2;
+                    PBNG_CUDA(launch_set_positions(c->prob, L2, -1, c->stream), "update_constraints: inertial target");
+                }
+                PBNG_CUDA(launch_set_positions(c->prob, c->L, 3, c->stream), "update_constraints: iterate");
+                c->launches += idt2 > 0.0 ? 2 : 1;
+                c->work = 0;
+                c->out = 1;
+                c->hist = 2;
+                c->l = 0;
+                c->hist_valid = true;
+                c->positions_set = true;
+                c->cur_accel = -1;
                 PBNG_CUDA(cudaStreamSynchronize(c->stream), "update_constraints: synchronize");
+                T.lap("update: upload + restore (device)");
+            } else {
+                c->prob.inv_dt2 = 0.0;
             }
+        } else {
+            c->prob.inv_dt2 = 0.0;
         }
     } catch (const std::bad_alloc &) {
         return fail(PBNG_E_OUT_OF_MEMORY, "update_constraints: host allocation");
