@@ -333,6 +333,17 @@ __device__ __forceinline__ void polar_newton(const float (&F)[3][3], const float
 // Jacobi routine; fp64 -> Jacobi (7 sweeps).  C = cof F and J = det F are passed in.
 template <class R>
 __device__ __forceinline__ void polar_fcr(const R (&F)[3][3], const R (&C)[3][3], R J, R (&Rm)[3][3]) {
+#ifdef PBNG_POLAR_F64  // experiment: the fp32 path with an fp64 polar factor (isolates the polar's share of fp32 drift)
+    if (sizeof(R) == 4) {
+        double Fd[3][3], Rd[3][3];
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) Fd[a][b] = double(F[a][b]);
+        polar_rotation(Fd, Rd);
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) Rm[a][b] = R(Rd[a][b]);
+        return;
+    }
+#endif
     if (sizeof(R) == 4) {
         R fro = R(0);
 #pragma unroll
