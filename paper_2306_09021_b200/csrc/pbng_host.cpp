@@ -1259,6 +1259,19 @@ cudaError_t timed_sweep(pbng_ctx *c, const SweepLaunch &s) {
     return timed_launch(c, [&] { return launch_sweep(c->prob, c->L, s, c->stream); });
 }
 
+// the windowed persistent schedule of the batched fp32 NH layout (sh 6, undecomposed, <= 32 colours,
+// colour launches not forced).  PBNG_B2_WINDOW = group pairs per window, read per call; default 0 = colour
+// launches: measured on config 4 the windowed schedule is bitwise identical but slower (window 4 / 8 / 16:
+// 1.72 / 1.345 / 1.33 ms per iteration against 1.147 for the colour launches)
+int b2_window_size() {
+    const char *e = getenv("PBNG_B2_WINDOW");
+    return e ? atoi(e) : 0;
+}
+bool b2_window_schedule(const pbng_ctx *c) {
+    return c->prob.lane_shift == 6 && c->n_ranks == 1 && c->ncol <= kB2MaxColours && b2_window_size() > 0 &&
+           c->schedule != PBNG_SCHEDULE_COLOUR_LAUNCHES;
+}
+
 pbng_status check_iterate(pbng_ctx *c, pbng_accel accel, double omega, double rho, double gamma, const char *who) {
     pbng_status st = require_device(c);
     if (st != PBNG_OK) return st;
@@ -2290,6 +2303,36 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
                     gamma, &sweeps, "iterate: decomposed iterations");
         if (st != PBNG_OK) return st;
         span_launches += sweeps;
+    } else if (b2_window_schedule(c)) {
+        // batched fp32 NH (sh 6): windowed persistent launches, one per kPipeMaxIter iterations
+        for (int32_t it = 0; it < n_iterations; it += kPipeMaxIter) {
+            B2Window W;
+            W.n_iter = std::min<int32_t>(kPipeMaxIter, n_iterations - it);
+            W.ncol = c->ncol;
+            W.window = b2_window_size();
+            W.work = c->work;
+            W.out = c->out;
+            W.hist = c->hist;
+            W.gamma = accel == PBNG_ACCEL_CHEBYSHEV ? gamma : 1.0;
+            for (int j = 0; j < W.n_iter; ++j)
+                W.omega[j] = accel == PBNG_ACCEL_SOR ? omega
+                             : accel == PBNG_ACCEL_CHEBYSHEV ? chebyshev_weight(c->l + j + 1, rho) : 1.0;
+            constexpr int WPB = kSweepBlock / 32;
+            W.blk_off[0] = 0;
+            for (int32_t col = 0; col < c->ncol; ++col) {
+                W.v_begin[col] = c->col_vbegin[col];
+                W.n_v[col] = c->col_nfree[col];
+                W.chunk_begin[col] = c->col_chunk[col];
+                W.blk_off[col + 1] = W.blk_off[col] + (c->col_nfree[col] + WPB - 1) / WPB;
+            }
+            const size_t n_gp = (size_t)((c->nb + 63) / 64);
+            PBNG_CUDA(cudaMemsetAsync(c->L.pipe_counter, 0, 8 + n_gp * (size_t)c->ncol * 4, c->stream), "iterate: window reset");
+            PBNG_CUDA(timed_launch(c, [&] { return launch_b2_window(c->prob, c->L, W, (int)accel, c->stream); }),
+                      "iterate: windowed batched sweep");
+            c->launches += 1;
+            span_launches += 1;
+            for (int j = 0; j < W.n_iter; ++j) end_iteration_impl(c, accel);
+        }
     } else if (effective_schedule(c) == 2) {
         // pipelined: one persistent launch per kPipeMaxIter iterations, no barrier between colours
         for (int32_t it = 0; it < n_iterations; it += kPipeMaxIter) {

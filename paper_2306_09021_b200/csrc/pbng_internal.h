@@ -135,7 +135,22 @@ struct PipeLaunch {
     double omega[kPipeMaxIter] = {};
 };
 
+// one launch of the windowed persistent schedule of the batched fp32 NH layout (sh 6): n_iter <= kPipeMaxIter
+// whole iterations over windows of `window` sample-group pairs; per colour c its vertex range, first chunk
+// and block offsets (blocks of kSweepBlock / 32 vertices; blk_off[ncol] = blocks per group pair)
+constexpr int kB2MaxColours = 32;
+struct B2Window {
+    int n_iter = 0, ncol = 0, window = 4;
+    int work = 0, out = 1, hist = 2;
+    double gamma = 1;
+    double omega[kPipeMaxIter] = {};
+    int32_t v_begin[kB2MaxColours] = {}, n_v[kB2MaxColours] = {};
+    int64_t chunk_begin[kB2MaxColours] = {};
+    int32_t blk_off[kB2MaxColours + 1] = {};
+};
+
 // launchers (pbng_kernels.cu); return cudaGetLastError()
+cudaError_t launch_b2_window(const Problem &p, const Layout &L, const B2Window &w, int accel, cudaStream_t st);
 // pipelined sweep: the caller zeroes pipe_flags and pipe_counter before each launch
 cudaError_t launch_sweep_pipe(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st);
 cudaError_t launch_sweep(const Problem &p, const Layout &L, const SweepLaunch &s, cudaStream_t st);

@@ -1481,9 +1481,10 @@ __device__ __forceinline__ void pf_l1(const void *p) { asm volatile("prefetch.gl
 struct P6 {
     float2 x, y, z;
 };
+template <bool COH = false>
 __device__ __forceinline__ P6 ld_p6(const float *p) {
-    const float4 a = ld(reinterpret_cast<const float4 *>(p));
-    const float2 b = ld(reinterpret_cast<const float2 *>(p + 4));
+    const float4 a = COH ? *reinterpret_cast<const float4 *>(p) : ld(reinterpret_cast<const float4 *>(p));
+    const float2 b = COH ? *reinterpret_cast<const float2 *>(p + 4) : ld(reinterpret_cast<const float2 *>(p + 4));
     return {make_float2(a.x, a.y), make_float2(a.z, a.w), b};
 }
 
@@ -1506,28 +1507,23 @@ __device__ __forceinline__ void chol_solve3(const float (&A)[6], const float (&f
 // ((gp * x_stride + u) << 8) + 8 lane and holds {x0 x1 y0 y1 | z0 z1 . .} -- the packed operands of its
 // two samples, loaded with one LDG.128 + one LDG.64 (no repacking moves).  The warp's records are staged
 // in shared memory (lane k stores record k) and read back as warp-broadcast LDS.128 pairs.
-template <int ACCEL, bool FEXT, bool WC>
-__global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_kernel(const Layout L, const int32_t v_begin,
-                                                                     const int32_t n_v, const int64_t chunk_begin,
-                                                                     const int64_t x_stride, const int32_t n_batch,
-                                                                     const int wi, const int oi, const int hi,
-                                                                     const float cmu, const float clam,
-                                                                     const float omega, const float gamma,
-                                                                     const float idt2, const int reverse) {
-    constexpr int WPB = kSweepBlock / 32;
-    __shared__ int2 s_id[WPB][32];
-    __shared__ float4 s_sd[WPB][32];
-    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    const int t = blockIdx.x * WPB + wq;  // vertex index within the colour
-    if (t >= n_v) return;                  // warp-uniform (only warp-level synchronisation below)
+// One vertex (index t of its colour) for the 64 samples of group pair gp, by one warp (COH: positions are
+// written by other CTAs of the same launch -- the windowed persistent kernel -- so they are read with
+// plain loads after an acquire instead of the read-only path).
+template <int ACCEL, bool FEXT, bool WC, bool COH>
+__device__ __forceinline__ void b2_vertex(const Layout &L, const int t, const int32_t v_begin, const int64_t chunk_begin,
+                                          const int64_t gp, const int64_t x_stride, const int32_t n_batch, const int wi,
+                                          const int oi, const int hi, const float cmu, const float clam,
+                                          const float omega, const float gamma, const float idt2, int2 (&s_id)[32],
+                                          float4 (&s_sd)[32]) {
+    const int lane = threadIdx.x & 31;
     const int v = v_begin + t;
     const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
     const int deg = ld(L.deg + v);
-    const int64_t gp = reverse ? gridDim.y - 1 - blockIdx.y : blockIdx.y;
     const int64_t slot = ((gp * x_stride) << 8) + 8 * lane;  // this lane's float offset at vertex 0
     const float *__restrict__ wk = reinterpret_cast<const float *>(L.xbuf[wi]) + slot;
     const int64_t vo = (int64_t)v << 8;
-    const float4 a01 = *reinterpret_cast<const float4 *>(wk + vo);
+    const float4 a01 = *reinterpret_cast<const float4 *>(wk + vo);  // own row: written only by this warp
     const float2 a2 = *reinterpret_cast<const float2 *>(wk + vo + 4);
     const float2 xa[3] = {make_float2(a01.x, a01.y), make_float2(a01.z, a01.w), a2};
     float2 f[3] = {bc(0.f), bc(0.f), bc(0.f)};
@@ -1544,28 +1540,28 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_kern
     {
         const int2 p0 = ld(L.path0 + v);
         S0 = {bc(0.f), bc(0.f), bc(0.f)};
-        S1 = diff(ld_p6(wk + ((int64_t)p0.x << 8)));
-        S2 = diff(ld_p6(wk + ((int64_t)p0.y << 8)));
+        S1 = diff(ld_p6<COH>(wk + ((int64_t)p0.x << 8)));
+        S2 = diff(ld_p6<COH>(wk + ((int64_t)p0.y << 8)));
     }
     for (int k0 = 0; k0 < deg; k0 += 32) {
         if (k0 + lane < deg) {
             const int64_t r = base + (int64_t)(k0 + lane) * kChunk;
-            s_id[wq][lane] = ld(reinterpret_cast<const int2 *>(L.rec_id) + r);
-            s_sd[wq][lane] = ld(reinterpret_cast<const float4 *>(L.rec_a) + r);
-            PBNG_CHECK(r < L.n_slots && (s_id[wq][lane].x & 0x3fffffff) < L.n_vertices);
+            s_id[lane] = ld(reinterpret_cast<const int2 *>(L.rec_id) + r);
+            s_sd[lane] = ld(reinterpret_cast<const float4 *>(L.rec_a) + r);
+            PBNG_CHECK(r < L.n_slots && (s_id[lane].x & 0x3fffffff) < L.n_vertices);
         }
         __syncwarp();
         const int n = min(32, deg - k0);
 #pragma unroll kB2Unroll
         for (int j = 0; j < n; ++j) {
             if (kB2Prefetch > 0 && j + kB2Prefetch < n)  // the gather of record j + PF: L2 -> L1 now
-                pf_l1(wk + ((int64_t)(s_id[wq][j + kB2Prefetch].x & 0x3fffffff) << 8));
-            const int2 id = s_id[wq][j];
-            const float4 sd = s_sd[wq][j];
+                pf_l1(wk + ((int64_t)(s_id[j + kB2Prefetch].x & 0x3fffffff) << 8));
+            const int2 id = s_id[j];
+            const float4 sd = s_sd[j];
             Pair<float, MODEL_NH> pr;
             pr.s[0] = sd.x; pr.s[1] = sd.y; pr.s[2] = sd.z; pr.detB = sd.w;
             pr.VE = __int_as_float(id.y);
-            const P6 nw = diff(ld_p6(wk + ((int64_t)(id.x & 0x3fffffff) << 8)));
+            const P6 nw = diff(ld_p6<COH>(wk + ((int64_t)(id.x & 0x3fffffff) << 8)));
             path_push(S0, S1, S2, nw, id.x);
             const float2 d1[3] = {S0.x, S0.y, S0.z};
             const float2 d2[3] = {S1.x, S1.y, S1.z};
@@ -1623,6 +1619,87 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_kern
         float *hw = reinterpret_cast<float *>(L.xbuf[hi]) + slot + vo;
         *reinterpret_cast<float4 *>(hw) = a01;
         *reinterpret_cast<float2 *>(hw + 4) = a2;
+    }
+}
+
+template <int ACCEL, bool FEXT, bool WC>
+__global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_kernel(const Layout L, const int32_t v_begin,
+                                                                     const int32_t n_v, const int64_t chunk_begin,
+                                                                     const int64_t x_stride, const int32_t n_batch,
+                                                                     const int wi, const int oi, const int hi,
+                                                                     const float cmu, const float clam,
+                                                                     const float omega, const float gamma,
+                                                                     const float idt2, const int reverse) {
+    constexpr int WPB = kSweepBlock / 32;
+    __shared__ int2 s_id[WPB][32];
+    __shared__ float4 s_sd[WPB][32];
+    const int wq = threadIdx.x >> 5;
+    const int t = blockIdx.x * WPB + wq;  // vertex index within the colour
+    if (t >= n_v) return;                  // warp-uniform (only warp-level synchronisation below)
+    const int64_t gp = reverse ? gridDim.y - 1 - blockIdx.y : blockIdx.y;
+    b2_vertex<ACCEL, FEXT, WC, false>(L, t, v_begin, chunk_begin, gp, x_stride, n_batch, wi, oi, hi, cmu, clam, omega,
+                                      gamma, idt2, s_id[wq], s_sd[wq]);
+}
+
+// Windowed persistent schedule for the batched fp32 Neo-Hookean layout (sh 6).  The sample-group pairs are
+// independent problems, so a colour pass of one group pair needs only the previous colour pass of the SAME
+// group pair.  Items (iteration, window of W group pairs, colour, group pair, block of WPB vertices) are
+// taken in that order from a global counter; an item waits (acquire) until its group pair's previous colour
+// pass has released all its blocks.  A window's positions (W x 3 buffers x ~5 MB) stay in L2 through its 8
+// colour passes, instead of every colour launch re-reading all 4096 samples from DRAM.  Every vertex reads
+// exactly what the colour launches give it -> bitwise-identical iterates.
+template <int ACCEL, bool FEXT, bool WC>
+__global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_window_kernel(
+    const Layout L, const B2Window P, const int64_t x_stride, const int32_t n_batch, const float cmu, const float clam,
+    const float idt2) {
+    constexpr int WPB = kSweepBlock / 32;
+    __shared__ int2 s_id[WPB][32];
+    __shared__ float4 s_sd[WPB][32];
+    __shared__ int64_t item_sh;
+    const int wq = threadIdx.x >> 5;
+    const int64_t n_gp = (n_batch + 63) / 64;
+    const int64_t per_gp = P.blk_off[P.ncol];  // blocks of one group pair in one iteration
+    const int64_t per_iter = n_gp * per_gp;
+    const int64_t n_items = per_iter * P.n_iter;
+    int32_t *done = L.pipe_flags;  // [n_gp][ncol] blocks finished (all iterations of this launch)
+    for (;;) {
+        if (threadIdx.x == 0) item_sh = (int64_t)atomicAdd(reinterpret_cast<unsigned long long *>(L.pipe_counter), 1ull);
+        __syncthreads();
+        const int64_t q = item_sh;
+        __syncthreads();
+        if (q >= n_items) return;
+        const int it = (int)(q / per_iter);
+        int64_t r = q - (int64_t)it * per_iter;
+        const int64_t wsz = (int64_t)P.window * per_gp;
+        const int64_t w = r / wsz;
+        r -= w * wsz;
+        const int64_t gp0 = w * P.window;
+        const int64_t W = min((int64_t)P.window, n_gp - gp0);  // group pairs in this window
+        int c = 0;
+        while (c + 1 < P.ncol && r >= W * P.blk_off[c + 1]) ++c;
+        r -= W * P.blk_off[c];
+        const int nblk = P.blk_off[c + 1] - P.blk_off[c];
+        const int64_t gp = gp0 + r / nblk;
+        const int blk = (int)(r % nblk);
+        if (threadIdx.x == 0) {  // the group pair's previous colour pass (previous iteration for colour 0)
+            const int pc = c > 0 ? c - 1 : P.ncol - 1;
+            const int target = (c > 0 ? it + 1 : it) * (P.blk_off[pc + 1] - P.blk_off[pc]);
+            const int32_t *fl = done + gp * P.ncol + pc;
+            while (ld_acquire(fl) < target) __nanosleep(32);
+        }
+        __syncthreads();
+        __threadfence();
+        const int wi = (ACCEL != ACCEL_NONE && (it & 1)) ? P.out : P.work;
+        const int oi = (ACCEL != ACCEL_NONE && (it & 1)) ? P.work : P.out;
+        const int t = blk * WPB + wq;
+        if (t < P.n_v[c])
+            b2_vertex<ACCEL, FEXT, WC, true>(L, t, P.v_begin[c], P.chunk_begin[c], gp, x_stride, n_batch, wi, oi, P.hist,
+                                             cmu, clam, float(P.omega[it]), float(P.gamma), idt2, s_id[wq], s_sd[wq]);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(done + gp * P.ncol + c, 1);
+        }
     }
 }
 
@@ -2301,8 +2378,40 @@ template <class R, int MODEL>
 cudaError_t energy_entry(const Problem &p, const Layout &L, int work, cudaStream_t st);
 template <class R, int MODEL>
 cudaError_t pipe_entry(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st);
+template <class R, int MODEL>
+cudaError_t b2win_entry(const Problem &p, const Layout &L, const B2Window &w, int accel, cudaStream_t st);
 
 #if defined(PBNG_TU_R)
+template <class R, int MODEL>
+cudaError_t b2win_entry(const Problem &p, const Layout &L, const B2Window &w, int accel, cudaStream_t st) {
+    if constexpr (sizeof(R) == 4 && MODEL == MODEL_NH) {
+        // persistent grid: every SM filled to the instance's occupancy (items are taken in order by running
+        // CTAs and only wait for earlier items, so a larger grid could not deadlock either)
+        const bool fe = p.has_fext, wcn = p.has_wc;
+        auto go = [&](auto kern) -> cudaError_t {
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSweepBlock, 0);
+            const int blocks = std::max(1, (p.sm_count > 0 ? p.sm_count : 148) * std::max(1, per_sm));
+            kern<<<(unsigned)blocks, kSweepBlock, 0, st>>>(L, w, p.x_stride, p.n_batch, float(p.cmu), float(p.clam),
+                                                          float(p.inv_dt2));
+            return cudaGetLastError();
+        };
+#define PBNG_B2W(A)                                                                   \
+    if (fe && wcn) return go(sweep_batched2_window_kernel<A, true, true>);          \
+    if (fe) return go(sweep_batched2_window_kernel<A, true, false>);                \
+    if (wcn) return go(sweep_batched2_window_kernel<A, false, true>);               \
+    return go(sweep_batched2_window_kernel<A, false, false>);
+        if (accel == ACCEL_SOR) { PBNG_B2W(ACCEL_SOR) }
+        if (accel == ACCEL_CHEB) { PBNG_B2W(ACCEL_CHEB) }
+        PBNG_B2W(ACCEL_NONE)
+#undef PBNG_B2W
+    } else {
+        (void)p; (void)L; (void)w; (void)accel; (void)st;
+        return cudaErrorInvalidValue;
+    }
+}
+template cudaError_t b2win_entry<PBNG_TU_R, PBNG_TU_MODEL>(const Problem &, const Layout &, const B2Window &, int,
+                                                           cudaStream_t);
 template <class R, int MODEL>
 cudaError_t pipe_entry(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st) {
     return pipe_dispatch2<R, MODEL>(p, L, s, st);
@@ -2321,6 +2430,11 @@ template cudaError_t sweep_entry<PBNG_TU_R, PBNG_TU_MODEL>(const Problem &, cons
                                                            cudaStream_t);
 template cudaError_t energy_entry<PBNG_TU_R, PBNG_TU_MODEL>(const Problem &, const Layout &, int, cudaStream_t);
 #else
+
+cudaError_t launch_b2_window(const Problem &p, const Layout &L, const B2Window &w, int accel, cudaStream_t st) {
+    if (w.n_iter <= 0 || p.n_chunks <= 0) return cudaSuccess;
+    return b2win_entry<float, MODEL_NH>(p, L, w, accel, st);
+}
 
 cudaError_t launch_sweep_pipe(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st) {
     if (s.n_iter <= 0 || p.n_chunks <= 0) return cudaSuccess;

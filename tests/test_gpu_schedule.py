@@ -97,3 +97,51 @@ def test_full_config3_pipelined_bitwise():
     p = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, PBNG_PATH="0"), capture_output=True,
                        text=True, timeout=900)
     assert p.returncode == 0 and "bitwise" in p.stdout, p.stderr[-2000:]
+
+
+def _batched_c5(n_samples):
+    # config 5 (small) as a batch of NH problems: gravity (f^ext), springs + plane contacts (weak
+    # constraints); every sample with its own noise
+    s = G.make_config(5, "small")
+    s.model = "nh"
+    rng = np.random.default_rng(5)
+    x0 = np.repeat(s.x0, n_samples, axis=0)
+    free = np.setdiff1d(np.arange(s.n_vertices), s.pinned)
+    x0[:, free] += rng.uniform(-0.02, 0.02, (n_samples, free.size, 3)) * s.h
+    s.x0 = x0
+    s.targets = np.repeat(s.targets, n_samples, axis=0)
+    return s
+
+
+@pytest.mark.parametrize("case", ["cheb100", "sor70", "c5_gravity_constraints", "c5_backward_euler"])
+def test_batched_window_schedule_equals_colour_launches_bitwise(case):
+    """The windowed persistent schedule of the batched fp32 NH layout (sample-group pairs advance through the
+    colours independently, an item waits only for its own group pair's previous colour pass) gives exactly
+    the colour launches' iterates: ragged sample counts, > 64 iterations (two launches), SOR / Chebyshev /
+    none, body force, weak constraints, backward Euler."""
+    from paper_2306_09021_b200 import context_from_scene
+    if case == "cheb100":
+        s, parts, acc = G.config4_batched(n_samples=100, n=5, iterations=70), [70, 3], None
+    elif case == "sor70":
+        s, parts, acc = G.config4_batched(n_samples=65, n=4, iterations=70), [66, 4], "sor"
+        s.accel, s.omega = "sor", 1.5
+    else:
+        s, parts, acc = _batched_c5(72), [12], None
+    import os
+    out = []
+    for sched in ("colour_launches", "auto"):
+        os.environ["PBNG_B2_WINDOW"] = "8" if sched == "auto" else "0"  # read by every pbng_iterate call
+        ctx = context_from_scene(s, device=0, dtype="f32")
+        assert ctx.query()["n_batch"] == s.n_batch
+        ctx.set_schedule(sched)
+        if case == "c5_backward_euler":
+            ctx.set_inertia(1e-2, np.asarray(s.x0))
+        for k in parts:
+            ctx.iterate(k, s.accel, s.omega, s.rho, s.gamma)
+        E, r = ctx.energy_residual()
+        out.append((ctx.get_positions().cpu().numpy(), E, r, ctx.query()["kernel_launches"]))
+        ctx.close()
+    del os.environ["PBNG_B2_WINDOW"]
+    assert np.array_equal(out[0][0], out[1][0]), np.abs(out[0][0] - out[1][0]).max()
+    assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
+    assert out[1][3] < out[0][3]  # the windowed schedule: one launch per <= 64 iterations
