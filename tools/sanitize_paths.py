@@ -71,6 +71,17 @@ def main():
         for c in ctxs:
             c.close()
         print(f"dd config {cfg}", flush=True)
+    # path-ordered NH records: config 3 at a size where one warp per chunk is chosen (sweep_kernel path
+    # mode), the batched sh-6 layout (path records), its windowed persistent schedule, a disconnected link
+    s = G.config3_hetero_cube(n=80)
+    run(s, "f32", iters=2)
+    run(s, "f64", iters=1)
+    s = G.config4_batched(n_samples=70, n=4, iterations=5)
+    run(s, "f32")
+    os.environ["PBNG_B2_WINDOW"] = "2"
+    run(s, "f32", iters=66)
+    del os.environ["PBNG_B2_WINDOW"]
+    print("path records + window", flush=True)
     # contact detection + incremental recolouring
     s = G.two_blocks_colliding(n=3, gap=0.01)
     ctx = context_from_scene(s, device=0, dtype="f64")
