@@ -1260,15 +1260,19 @@ cudaError_t timed_sweep(pbng_ctx *c, const SweepLaunch &s) {
 }
 
 // the windowed persistent schedule of the batched fp32 NH layout (sh 6, undecomposed, <= 32 colours,
-// colour launches not forced).  PBNG_B2_WINDOW = group pairs per window, read per call; default 0 = colour
-// launches: measured on config 4 the windowed schedule is bitwise identical but slower (window 4 / 8 / 16:
-// 1.72 / 1.345 / 1.33 ms per iteration against 1.147 for the colour launches)
-int b2_window_size() {
+// colour launches not forced).  Auto: one window holding every sample-group pair when there are at most 8
+// (n_batch <= 512 -- the per-GPU shard of config 4 at 8 GPUs), where the colour launches are short and
+// their tails and launch gaps dominate (512 samples: 0.173 vs 0.202 ms per iteration); colour launches
+// otherwise (4096 samples: windows of 4 / 8 / 16 take 1.72 / 1.345 / 1.33 ms against 1.147, DESIGN.md
+// section 7).  PBNG_B2_WINDOW (read per call) overrides: group pairs per window, 0 = colour launches.
+int b2_window_size(const pbng_ctx *c) {
     const char *e = getenv("PBNG_B2_WINDOW");
-    return e ? atoi(e) : 0;
+    if (e) return atoi(e);
+    const int n_gp = (c->nb + 63) / 64;
+    return n_gp <= 8 ? n_gp : 0;
 }
 bool b2_window_schedule(const pbng_ctx *c) {
-    return c->prob.lane_shift == 6 && c->n_ranks == 1 && c->ncol <= kB2MaxColours && b2_window_size() > 0 &&
+    return c->prob.lane_shift == 6 && c->n_ranks == 1 && c->ncol <= kB2MaxColours && b2_window_size(c) > 0 &&
            c->schedule != PBNG_SCHEDULE_COLOUR_LAUNCHES;
 }
 
@@ -2309,7 +2313,7 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
             B2Window W;
             W.n_iter = std::min<int32_t>(kPipeMaxIter, n_iterations - it);
             W.ncol = c->ncol;
-            W.window = b2_window_size();
+            W.window = b2_window_size(c);
             W.work = c->work;
             W.out = c->out;
             W.hist = c->hist;
