@@ -2329,6 +2329,19 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
                 W.chunk_begin[col] = c->col_chunk[col];
                 W.blk_off[col + 1] = W.blk_off[col] + (c->col_nfree[col] + WPB - 1) / WPB;
             }
+            // an empty colour has no items: each colour waits for the previous colour WITH vertices (so the
+            // chain of waits still orders every colour pass of a group pair)
+            for (int32_t col = 0; col < c->ncol; ++col) {
+                int32_t pc = col;
+                for (int k = 1; k <= c->ncol; ++k) {
+                    const int32_t q = (col - k + c->ncol) % c->ncol;
+                    if (W.blk_off[q + 1] > W.blk_off[q]) {
+                        pc = q;
+                        break;
+                    }
+                }
+                W.prev[col] = pc;
+            }
             const size_t n_gp = (size_t)((c->nb + 63) / 64);
             PBNG_CUDA(cudaMemsetAsync(c->L.pipe_counter, 0, 8 + n_gp * (size_t)c->ncol * 4, c->stream), "iterate: window reset");
             PBNG_CUDA(timed_launch(c, [&] { return launch_b2_window(c->prob, c->L, W, (int)accel, c->stream); }),

@@ -147,6 +147,7 @@ struct B2Window {
     int32_t v_begin[kB2MaxColours] = {}, n_v[kB2MaxColours] = {};
     int64_t chunk_begin[kB2MaxColours] = {};
     int32_t blk_off[kB2MaxColours + 1] = {};
+    int32_t prev[kB2MaxColours] = {};  // the previous colour with vertices (cyclic; may be the colour itself)
 };
 
 // launchers (pbng_kernels.cu); return cudaGetLastError()

@@ -1681,9 +1681,9 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_wind
         const int nblk = P.blk_off[c + 1] - P.blk_off[c];
         const int64_t gp = gp0 + r / nblk;
         const int blk = (int)(r % nblk);
-        if (threadIdx.x == 0) {  // the group pair's previous colour pass (previous iteration for colour 0)
-            const int pc = c > 0 ? c - 1 : P.ncol - 1;
-            const int target = (c > 0 ? it + 1 : it) * (P.blk_off[pc + 1] - P.blk_off[pc]);
+        if (threadIdx.x == 0) {  // the group pair's previous (non-empty) colour pass, this or the previous iteration
+            const int pc = P.prev[c];
+            const int target = (pc < c ? it + 1 : it) * (P.blk_off[pc + 1] - P.blk_off[pc]);
             const int32_t *fl = done + gp * P.ncol + pc;
             while (ld_acquire(fl) < target) __nanosleep(32);
         }
@@ -2103,33 +2103,37 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
     return r;  // valid in thread 0
 }
 
-// Item loops of the energy / residual kernels.  BM = false: one sample per grid row (blockIdx.y), one item
-// per thread.  BM = true (batched layouts, sh >= 5): one group of 32 samples per grid row, lane = sample,
-// one item per WARP -- the item's records are warp-uniform (broadcast) loads and the position loads of a
-// warp are the item's contiguous sample-minor lines.  Both reduce in a fixed order (deterministic).
-template <bool BM>
-__device__ __forceinline__ void item_range(int64_t &b, int64_t &i0, int64_t &step) {
+// Item loops of the energy / residual kernels.  NS = 0: one sample per grid row (blockIdx.y), one item per
+// thread.  NS = 1 (sample-minor sh 5): one group of 32 samples per grid row, lane = sample, one item per
+// WARP.  NS = 2 (two-sample sh 6): one group pair of 64 samples per grid row, lane = its two samples (the
+// two halves of one 32 B slot), one item per warp.  In the warp modes the item's records are warp-uniform
+// (broadcast) loads and the position loads of a warp are the item's contiguous sample-minor lines.  All
+// reduce in a fixed order (deterministic).
+template <int NS>
+__device__ __forceinline__ void item_range(int64_t (&b)[2], int64_t &i0, int64_t &step) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (BM) {
-        b = (int64_t)blockIdx.y * 32 + lane;
+    if (NS > 0) {
+        b[0] = (int64_t)blockIdx.y * (32 * NS) + lane;
+        b[1] = b[0] + 32;
         i0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
         step = (int64_t)gridDim.x * (blockDim.x >> 5);
     } else {
-        b = blockIdx.y;
+        b[0] = b[1] = blockIdx.y;
         i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
         step = (int64_t)gridDim.x * blockDim.x;
     }
 }
-// the block's partial of sample b: BM sums the block's warps lane by lane (each lane one sample)
-template <bool BM>
+// the block's partial of sample b: the warp modes sum the block's warps lane by lane (lane = sample)
+template <int NS>
 __device__ __forceinline__ void store_partial(double acc, double *part, int64_t b, int g, int32_t n_batch,
                                               double *red_sh) {
-    if (!BM) {
+    if (NS == 0) {
         const double s = block_sum(acc, red_sh);
         if (threadIdx.x == 0) part[b * g + blockIdx.x] = s;
         return;
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();  // red_sh may still be read by a previous call
     red_sh[warp * 32 + lane] = acc;
     __syncthreads();
     if (warp == 0) {
@@ -2139,7 +2143,7 @@ __device__ __forceinline__ void store_partial(double acc, double *part, int64_t 
     }
 }
 
-template <class R, int MODEL, bool BM>
+template <class R, int MODEL, int NS>
 __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const int64_t nt, const int64_t n_cons,
                                                            const int64_t x_stride, const int wi, const double cmu,
                                                            const double clam, const double rgx, const double rgy,
@@ -2148,13 +2152,18 @@ __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const
                                                            const int32_t n_batch) {
     using R4 = typename RT<R>::R4;
     __shared__ double red_sh[kRedBlock];
-    int64_t b, i0, istep;
-    item_range<BM>(b, i0, istep);
+    int64_t bq[2], i0, istep;
+    item_range<NS>(bq, i0, istep);
+    constexpr int NQ = NS == 2 ? 2 : 1;
     const void *x = L.xbuf[wi];
     const double r_mu = cmu / (cmu + clam);  // mu / lambdahat, independent of E
-    double acc = 0.0;
+    double accq[2] = {0.0, 0.0};
     const int64_t n_items = nt + n_cons + (idt2 > 0.0 ? n_own : 0);
-    for (int64_t item = i0; item < n_items; item += istep) {
+    for (int64_t item = i0; item < n_items; item += istep)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int64_t b = bq[q];
+        double &acc = accq[q];
         if (item >= nt + n_cons) {  // backward Euler: inertia m_i/(2 dt^2) |x_i - xtilde_i|^2 of owned free nodes
             const int64_t v = item - nt - n_cons;
             const R4 xv = pos_load<R>(x, b, v, x_stride, sh);
@@ -2234,10 +2243,11 @@ __global__ void __launch_bounds__(kRedBlock) energy_kernel(const Layout L, const
                           C[2] * (kxz * C[0] + kyz * C[1] + kzz * C[2]));
         }
     }
-    store_partial<BM>(acc, L.part_e, b, ge, n_batch, red_sh);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) store_partial<NS>(accq[q], L.part_e, bq[q], ge, n_batch, red_sh);
 }
 
-template <class R, int MODEL, bool FEXT, bool WC, bool BM>
+template <class R, int MODEL, bool FEXT, bool WC, int NS>
 __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, const int64_t n_chunks,
                                                              const int64_t x_stride, const int wi, const double cmu,
                                                              const double clam, const int gr, const int sh,
@@ -2245,11 +2255,16 @@ __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, con
                                                              const int32_t n_batch) {
     using R4 = typename RT<R>::R4;
     __shared__ double red_sh[kRedBlock];
-    int64_t b, i0, istep;
-    item_range<BM>(b, i0, istep);
+    int64_t bq[2], i0, istep;
+    item_range<NS>(bq, i0, istep);
+    constexpr int NQ = NS == 2 ? 2 : 1;
     const void *x = L.xbuf[wi];
-    double acc = 0.0;
-    for (int64_t t = i0; t < n_chunks * kChunk; t += istep) {
+    double accq[2] = {0.0, 0.0};
+    for (int64_t t = i0; t < n_chunks * kChunk; t += istep)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int64_t b = bq[q];
+        double &acc = accq[q];
         const int64_t chunk = t >> 5;
         const int cl = (int)(t & 31);  // the vertex's lane in its chunk
         const int2 cv = L.chunk_v[chunk];
@@ -2295,7 +2310,8 @@ __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, con
         if (idt2 > 0.0) inertia_contrib<R, double>(L, v, pos_load<R>(L.xtilde, b, v, x_stride, sh), idt2, xa, f, A);
         acc += f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
     }
-    store_partial<BM>(acc, L.part_r, b, gr, n_batch, red_sh);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) store_partial<NS>(accq[q], L.part_r, bq[q], gr, n_batch, red_sh);
 }
 
 __global__ void __launch_bounds__(kRedBlock) reduce_kernel(const Layout L, const int ge, const int gr) {
@@ -2313,10 +2329,10 @@ __global__ void __launch_bounds__(kRedBlock) reduce_kernel(const Layout L, const
     }
 }
 
-template <class R, int MODEL, bool BM>
+template <class R, int MODEL, int NS>
 cudaError_t energy_residual_launch(const Problem &p, const Layout &L, int wi, cudaStream_t st) {
-    const unsigned rows = BM ? (unsigned)((p.n_batch + 31) / 32) : (unsigned)p.n_batch;
-    energy_kernel<R, MODEL, BM><<<dim3(p.ge, rows), kRedBlock, 0, st>>>(
+    const unsigned rows = NS > 0 ? (unsigned)((p.n_batch + 32 * NS - 1) / (32 * NS)) : (unsigned)p.n_batch;
+    energy_kernel<R, MODEL, NS><<<dim3(p.ge, rows), kRedBlock, 0, st>>>(
         L, p.n_tets, p.n_cons, p.x_stride, wi, p.cmu, p.clam, p.rho_g[0], p.rho_g[1], p.rho_g[2], p.ge, p.lane_shift,
         p.n_own, p.inv_dt2, p.n_batch);
     dim3 gr(p.gr, rows);
@@ -2326,11 +2342,11 @@ cudaError_t energy_residual_launch(const Problem &p, const Layout &L, int wi, cu
         std::apply([&](auto... xs) { kern<<<gr, kRedBlock, 0, st>>>(xs...); }, a);
     };
     if (p.has_fext) {
-        if (p.has_wc) go(residual_kernel<R, MODEL, true, true, BM>);
-        else go(residual_kernel<R, MODEL, true, false, BM>);
+        if (p.has_wc) go(residual_kernel<R, MODEL, true, true, NS>);
+        else go(residual_kernel<R, MODEL, true, false, NS>);
     } else {
-        if (p.has_wc) go(residual_kernel<R, MODEL, false, true, BM>);
-        else go(residual_kernel<R, MODEL, false, false, BM>);
+        if (p.has_wc) go(residual_kernel<R, MODEL, false, true, NS>);
+        else go(residual_kernel<R, MODEL, false, false, NS>);
     }
     reduce_kernel<<<p.n_batch, kRedBlock, 0, st>>>(L, p.ge, p.gr);
     return cudaGetLastError();
@@ -2338,9 +2354,10 @@ cudaError_t energy_residual_launch(const Problem &p, const Layout &L, int wi, cu
 
 template <class R, int MODEL>
 cudaError_t energy_dispatch(const Problem &p, const Layout &L, int wi, cudaStream_t st) {
-    // batched layouts: a warp covers one item for 32 samples (coalesced sample-minor loads)
-    if (p.lane_shift >= 5) return energy_residual_launch<R, MODEL, true>(p, L, wi, st);
-    return energy_residual_launch<R, MODEL, false>(p, L, wi, st);
+    // batched layouts: a warp covers one item for 32 (sh 5) or 64 (sh 6) samples
+    if (p.lane_shift == 6) return energy_residual_launch<R, MODEL, 2>(p, L, wi, st);
+    if (p.lane_shift == 5) return energy_residual_launch<R, MODEL, 1>(p, L, wi, st);
+    return energy_residual_launch<R, MODEL, 0>(p, L, wi, st);
 }
 
 // test hook: R(F) of the device polar decomposition for n matrices (pbng_test_polar)

@@ -113,7 +113,7 @@ def _batched_c5(n_samples):
     return s
 
 
-@pytest.mark.parametrize("case", ["cheb100", "sor70", "c5_gravity_constraints", "c5_backward_euler"])
+@pytest.mark.parametrize("case", ["cheb100", "sor70", "c5_gravity_constraints", "c5_backward_euler", "empty_colours"])
 def test_batched_window_schedule_equals_colour_launches_bitwise(case):
     """The windowed persistent schedule of the batched fp32 NH layout (sample-group pairs advance through the
     colours independently, an item waits only for its own group pair's previous colour pass) gives exactly
@@ -125,6 +125,13 @@ def test_batched_window_schedule_equals_colour_launches_bitwise(case):
     elif case == "sor70":
         s, parts, acc = G.config4_batched(n_samples=65, n=4, iterations=70), [66, 4], "sor"
         s.accel, s.omega = "sor", 1.5
+    elif case == "empty_colours":  # colours without free vertices: the waits chain over the non-empty ones
+        from test_gpu_path_records import batch_of
+        X = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [-1, 0, 0], [0, -1, 0], [0, 0, -1],
+                      [0.4, 0.4, -0.8]], float)
+        T = np.array([[0, 1, 2, 3], [0, 1, 2, 7], [0, 4, 5, 6]], np.int32)
+        load = np.array([[0.1, 0, 0], [0, 0.1, 0], [-0.1, 0, 0], [0, -0.1, 0], [0, 0, -0.1]])
+        s, parts, acc = batch_of(X, T, [1, 2, 4, 5, 6], 64, 0.05, 3, 25, load=load), [25], None
     else:
         s, parts, acc = _batched_c5(72), [12], None
     import os
