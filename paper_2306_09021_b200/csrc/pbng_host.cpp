@@ -828,7 +828,7 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
 void build_pipeline(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::vector<int32_t> &vt) {
     c->h_dep_off.assign((size_t)c->n_chunks + 1, 0);
     c->h_deps.clear();
-    if (c->n_ranks > 1 || c->path_rec) return;  // the pipelined schedule is unavailable (pipeline_available)
+    if (c->n_ranks > 1) return;  // the pipelined schedule is unavailable (pipeline_available)
     std::vector<int32_t> chunk_of((size_t)std::max<int64_t>(c->n_free, 1), -1), chunk_col((size_t)std::max<int64_t>(c->n_chunks, 1), 0);
     for (int32_t col = 0; col < c->ncol; ++col)
         for (int64_t ch = c->col_chunk[col]; ch < c->col_chunk[col + 1]; ++ch) {
@@ -1073,7 +1073,8 @@ std::vector<int32_t> distinct_nodes(const pbng_weak_constraint &w) {
 }
 
 bool pipeline_available(const pbng_ctx *c) {
-    return c->n_ranks == 1 && c->prob.lane_shift == 0 && c->n_chunks > 0 && !c->path_rec;
+    // path-ordered records are walked by one warp per chunk: the pipelined kernel then runs one-warp items
+    return c->n_ranks == 1 && c->prob.lane_shift == 0 && c->n_chunks > 0 && (!c->path_rec || problem_split(c) == 1);
 }
 
 int problem_split(const pbng_ctx *c);

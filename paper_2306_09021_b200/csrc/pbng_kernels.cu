@@ -1196,7 +1196,7 @@ template <class R, int SPLIT> struct SplitMinBlocks {
 // sweep_kernel; SPLIT > 1: the partial sums and fixed-order combination of sweep_split_kernel), so the
 // per-vertex summation order -- and the result -- is that of the colour-launch schedule with the same
 // split (pbng_host.cpp problem_split).
-template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int SPLIT>
+template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int SPLIT, bool PATH = false>
 __global__ void __launch_bounds__(SplitBlock<SPLIT>::n, (MODEL == MODEL_FCR && SPLIT == 8) ? 3 : PBNG_SWEEP_MINB)
     sweep_pipe_kernel(const Layout L, const PipeLaunch P,
                                                                  const int64_t x_stride, const int32_t n_batch,
@@ -1257,9 +1257,14 @@ __global__ void __launch_bounds__(SplitBlock<SPLIT>::n, (MODEL == MODEL_FCR && S
         R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
         const int64_t base = ld(L.chunk_off + X) + lane;
         if (SPLIT == 1) {
-            if (valid)
-                update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_COHERENT>(L, work, xs, v, base, ld(L.deg + v), oi,
-                                                                          P.hist, cmu, clam, omega, gamma, idt2);
+            if (valid) {
+                if constexpr (PATH && MODEL == MODEL_NH)
+                    update_vertex_path<R, ACCEL, FEXT, WC, GATHER_COHERENT>(L, work, xs, v, base, ld(L.deg + v), oi,
+                                                                            P.hist, cmu, clam, omega, gamma, idt2);
+                else
+                    update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_COHERENT>(L, work, xs, v, base, ld(L.deg + v), oi,
+                                                                              P.hist, cmu, clam, omega, gamma, idt2);
+            }
         } else {
             R f[3] = {R(0), R(0), R(0)};
             R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
@@ -1807,13 +1812,13 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
 
 // persistent grid: every SM filled to the kernel's occupancy (queried once per instantiation and device;
 // racing threads compute and store the same value)
-template <class R, int MODEL, int ACCEL, bool FE, bool W, int SPLIT>
+template <class R, int MODEL, int ACCEL, bool FE, bool W, int SPLIT, bool PATH = false>
 cudaError_t pipe_launch(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st) {
     static std::atomic<int> cache[kMaxDevices];
     int blocks = cache[p.device % kMaxDevices].load(std::memory_order_acquire);
     if (blocks == 0) {
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_pipe_kernel<R, MODEL, ACCEL, FE, W, SPLIT>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_pipe_kernel<R, MODEL, ACCEL, FE, W, SPLIT, PATH>,
                                                       SplitBlock<SPLIT>::n, 0);
         blocks = std::max(1, (p.sm_count > 0 ? p.sm_count : 148) * std::max(1, per_sm));
         cache[p.device % kMaxDevices].store(blocks, std::memory_order_release);
@@ -1822,7 +1827,7 @@ cudaError_t pipe_launch(const Problem &p, const Layout &L, const PipeLaunch &s, 
     const int64_t items = p.n_chunks * p.n_batch * s.n_iter;
     const int64_t g = std::min<int64_t>(blocks, (items + GROUPS - 1) / GROUPS);
     if (g <= 0) return cudaSuccess;
-    sweep_pipe_kernel<R, MODEL, ACCEL, FE, W, SPLIT><<<(unsigned)g, SplitBlock<SPLIT>::n, 0, st>>>(
+    sweep_pipe_kernel<R, MODEL, ACCEL, FE, W, SPLIT, PATH><<<(unsigned)g, SplitBlock<SPLIT>::n, 0, st>>>(
         L, s, p.x_stride, p.n_batch, p.n_chunks, R(p.cmu), R(p.clam), R(p.inv_dt2));
     return cudaGetLastError();
 }
@@ -1832,6 +1837,9 @@ cudaError_t pipe_dispatch4(const Problem &p, const Layout &L, const PipeLaunch &
     if (s.split == 2) return pipe_launch<R, MODEL, ACCEL, FE, W, 2>(p, L, s, st);
     if (s.split == 4) return pipe_launch<R, MODEL, ACCEL, FE, W, 4>(p, L, s, st);
     if (s.split == 8) return pipe_launch<R, MODEL, ACCEL, FE, W, 8>(p, L, s, st);
+    if constexpr (MODEL == MODEL_NH) {
+        if (p.path) return pipe_launch<R, MODEL, ACCEL, FE, W, 1, true>(p, L, s, st);
+    }
     return pipe_launch<R, MODEL, ACCEL, FE, W, 1>(p, L, s, st);
 }
 

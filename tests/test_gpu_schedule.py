@@ -152,3 +152,13 @@ def test_batched_window_schedule_equals_colour_launches_bitwise(case):
     assert np.array_equal(out[0][0], out[1][0]), np.abs(out[0][0] - out[1][0]).max()
     assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
     assert out[1][3] < out[0][3]  # the windowed schedule: one launch per <= 64 iterations
+
+
+def test_full_config3_pipelined_path_records_bitwise():
+    """Path-ordered records under the pipelined schedule (one-warp items walking the same records) give the
+    colour launches' bits (measured slower on config 3, so auto keeps the colour launches)."""
+    s = G.make_config(3, "full")
+    xa, Ea, _, qa = run(s, "f32", "colour_launches", [2])
+    xb, Eb, _, qb = run(s, "f32", "pipelined", [2])
+    assert qa["schedule"] == 1 and qb["schedule"] == 2
+    assert np.array_equal(xa, xb) and np.array_equal(Ea, Eb)
