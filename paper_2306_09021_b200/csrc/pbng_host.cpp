@@ -178,6 +178,11 @@ struct pbng_ctx {
     std::vector<int2> h_rec_id2;   // path-ordered NH records: {id | drop << 30, VE bits} (Problem::path)
     std::vector<int2> h_path0;     // path-ordered NH records: per free vertex the slots S1, S2 before record 0
     bool path_rec = false;
+    // rest-recompute path records (SURVEY.md §8(d) lower-byte variant (i)): {id | drop, E_e/6} only, the
+    // kernels rebuild s'_j, det B' and V_e from the rest positions h_rest (Real4 [n_local], internal ids)
+    bool rest_rec = false;
+    int records = 0;  // pbng_records requested (0 auto, 1 stored rest data, 2 rest recompute)
+    std::vector<unsigned char> h_rest;
     std::vector<int64_t> inc_off;  // vertex -> incident tets (ascending), mesh-only: built once and kept
     std::vector<int32_t> inc;
     void *stage2 = nullptr;  // second staging buffer (device re-layout of pbng_update_constraints)
@@ -213,7 +218,8 @@ struct pbng_ctx {
     Region r_rec_id, r_rec_a, r_rec_b, r_rec_c, r_chunk_off, r_chunk_v, r_deg, r_fext, r_wc_off, r_wc_cid, r_wc_d,
         r_c_n, r_c_node, r_c_w, r_c_anchor, r_c_K, r_tet_id, r_tet_a, r_tet_b, r_tet_c, r_int2orig, r_targets,
         r_x[3], r_stage, r_part_e, r_part_r, r_results, r_flag, r_halo_send, r_halo_recv, r_mass, r_xt, r_dep_off,
-        r_deps, r_pipe, r_surf, r_sv, r_chead, r_cnext, r_cres, r_cscal, r_hsend, r_hrecv, r_allred, r_path0, r_stage2;
+        r_deps, r_pipe, r_surf, r_sv, r_chead, r_cnext, r_cres, r_cscal, r_hsend, r_hrecv, r_allred, r_path0, r_stage2,
+        r_rest;
     size_t ws_need = 0;
     // bound device state
     bool bound = false;
@@ -496,6 +502,19 @@ bool use_path_records(const pbng_ctx *c) {
     return sh == 6 || (sh == 0 && problem_split(c) == 1);
 }
 
+// rest-recompute records (pbng_records; PBNG_RECORDS=1|2 overrides auto for experiments): path records of
+// the one-thread-per-vertex sweep only (sh 0).  The batched kernel shares each record across 64 samples
+// of a warp, so its records cost no HBM per sample and recomputing them per lane would only add ALU work.
+bool use_rest_records(const pbng_ctx *c) {
+    static const int env = [] {
+        const char *e = getenv("PBNG_RECORDS");
+        return e ? atoi(e) : 0;
+    }();
+    if (!c->path_rec || layout_lane_shift(c) != 0) return false;
+    const int want = c->records != 0 ? c->records : env;
+    return want == 2;
+}
+
 // weak constraints held by this context (owned first): distinct nodes with combined weights w0_j - w1_j;
 // per owned free vertex the list of (constraint, w0_i - w1_i) in input order.  Also the fast path of
 // pbng_update_constraints (colouring unchanged: only these arrays are rebuilt and uploaded).
@@ -561,6 +580,7 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
 
     // chunks and degrees (path-ordered NH records: records per vertex incl. load-only ones)
     c->path_rec = use_path_records(c);
+    c->rest_rec = use_rest_records(c);
     c->col_chunk.assign(c->ncol + 1, 0);
     c->h_deg.assign(c->n_free, 0);
     auto vertex_link = [&](int32_t o, std::vector<std::array<int32_t, 3>> &link) {  // other vertices per incident tet
@@ -631,11 +651,18 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     const int64_t ns = std::max<int64_t>(c->n_slots, 1);
     c->h_rec_id.assign(c->path_rec ? 1 : (size_t)ns, make_int4(0, 0, 0, 0));
     c->h_rec_id2.assign(c->path_rec ? (size_t)ns : 1, make_int2(0, 0));
-    c->h_rec_a.assign((size_t)ns * s4, 0);
+    c->h_rec_a.assign(c->rest_rec ? s4 : (size_t)ns * s4, 0);  // rest-recompute records: unused
     const bool nh = c->model == MODEL_NH;
     c->h_rec_b.assign(nh ? s4 : (size_t)ns * s4, 0);  // NH: unused
     // rec_c: FCR g3z (+ VE in fp64); NH: VE in fp64, unused in fp32 (VE rides in rec_id.w)
+    // rest-recompute records: rec_c holds E_e/6 in fp64 (fp32: in rec_id.y)
     const size_t rec_c_bytes = nh ? (c->dtype == DT_F64 ? s : 0) : (c->dtype == DT_F64 ? 2 * s : s);
+    c->h_rest.assign(c->rest_rec ? (size_t)std::max<int64_t>(c->n_local, 1) * s4 : 0, 0);
+    if (c->rest_rec)
+        for (int64_t i = 0; i < c->n_local; ++i) {
+            const double *X = c->X.data() + 3 * (size_t)c->int2orig[i];
+            put4<R>(c->h_rest, i, X[0], X[1], X[2], 0.0);
+        }
     c->h_rec_c.assign(std::max<size_t>((size_t)ns * rec_c_bytes, s), 0);
     parallel_for(n_chunks, [&](int64_t ch_lo, int64_t ch_hi) {  // chunks write disjoint record slots
     std::vector<std::array<int32_t, 3>> link;
@@ -657,11 +684,23 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
                     const int32_t code = c->orig2int[pr.vnew] | (pr.drop << 30);
                     if (pr.tet < 0) {  // load-only: VE = 0 and zero rest data contribute exactly 0
                         c->h_rec_id2[r] = make_int2(code, 0);
-                        put4<R>(c->h_rec_a, r, 0.0, 0.0, 0.0, 0.0);
+                        if (!c->rest_rec) put4<R>(c->h_rec_a, r, 0.0, 0.0, 0.0, 0.0);
                         if (c->dtype == DT_F64) put1<R>(c->h_rec_c, r, 0.0);
                         continue;
                     }
                     const int64_t e = vt[vt_off[o] + pr.tet];
+                    if (c->rest_rec) {  // E_e / 6: V_e E_e = |det Dm'| E_e / 6 with Dm' rebuilt in slot order
+                        const double E6 = Ee(e) / 6.0;
+                        int2 id = make_int2(code, 0);
+                        if (c->dtype == DT_F32) {
+                            const float ef = (float)E6;
+                            std::memcpy(&id.y, &ef, 4);
+                        } else {
+                            put1<R>(c->h_rec_c, r, E6);
+                        }
+                        c->h_rec_id2[r] = id;
+                        continue;
+                    }
                     const int32_t *t = c->tets.data() + 4 * e;
                     int a = 0;
                     while (t[a] != o) ++a;
@@ -808,6 +847,7 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     // sweep_batched2_kernel (sh 6), otherwise sample-minor groups of 32 (sh 5)
     p.lane_shift = layout_lane_shift(c);
     p.path = c->path_rec;
+    p.rest = c->rest_rec;
     p.cmu = cmu;
     p.clam = clam;
     for (int k = 0; k < 3; ++k) p.rho_g[k] = c->density * c->grav[k];
@@ -1122,7 +1162,8 @@ void plan_workspace(pbng_ctx *c) {
     const int64_t ns = std::max<int64_t>(c->n_slots, 1);
     take(c->r_rec_id, (size_t)ns * (c->path_rec ? 8 : 16));
     take(c->r_path0, c->h_path0.size() * 8);
-    take(c->r_rec_a, (size_t)ns * s4);
+    take(c->r_rec_a, c->h_rec_a.size());
+    take(c->r_rest, c->h_rest.size());
     take(c->r_rec_b, c->h_rec_b.size());
     take(c->r_rec_c, c->h_rec_c.size());
     take(c->r_chunk_off, c->h_chunk_off.size() * 8);
@@ -1183,13 +1224,17 @@ double sweep_bytes_model(const pbng_ctx *c) {
     const double s = (double)c->real_size();
     // path-ordered NH records: {id | drop, VE} + {s'_0..2, det B'} = 24 B (fp32) / 48 B (fp64) per record
     // (load-only ones included) + the per-vertex first slots (8 B)
-    const double rec = c->path_rec ? (c->dtype == DT_F64 ? 48.0 : 24.0)
+    // rest-recompute records: {id | drop, E_e/6} = 8 B (fp32) / 16 B (fp64), plus every held vertex's rest
+    // position read once (below)
+    const double rec = c->rest_rec ? (c->dtype == DT_F64 ? 16.0 : 8.0)
+                       : c->path_rec ? (c->dtype == DT_F64 ? 48.0 : 24.0)
                        : c->model == MODEL_NH ? (c->dtype == DT_F64 ? 56.0 : 32.0) : (c->dtype == DT_F64 ? 96.0 : 52.0);
     double b = (double)(c->path_rec ? c->n_records : c->n_pairs) * rec + (double)(c->n_chunks + 1) * 8.0 +
                (double)c->n_free * (c->path_rec ? 12.0 : 4.0);
     double per_v = 3 * s;  // write x_PBNG
     per_v += (c->prob.has_fext ? 3 * s : 0);
     b += (double)c->nb * ((double)c->n_free * per_v + (double)c->n_local * 3 * s);
+    if (c->rest_rec) b += (double)c->n_local * 3 * s;
     return b;
 }
 
@@ -1216,6 +1261,8 @@ int problem_split(const pbng_ctx *c) {
         return e ? atoi(e) : 0;
     }();
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
+    // rest-recompute records requested explicitly: they exist only as path records, walked by one warp per chunk
+    if (c->records == PBNG_RECORDS_REST && c->model == MODEL_NH && !batched_layout(c)) return 1;
     int64_t gfree = 0;  // free vertices of the whole mesh (all ranks)
     for (int64_t k : c->gcol_nfree) gfree += k;
     const int64_t chunks_per_colour = gfree * c->nb / kChunk / std::max(c->ncol, 1);
@@ -2113,6 +2160,7 @@ static pbng_status bind_layout(pbng_ctx *c, void *dptr, uint64_t bytes, bool fre
     L.rec_a = at(c->r_rec_a);
     L.rec_b = at(c->r_rec_b);
     L.rec_c = at(c->r_rec_c);
+    L.rest = c->rest_rec ? at(c->r_rest) : nullptr;
     L.chunk_off = static_cast<const int64_t *>(at(c->r_chunk_off));
     L.chunk_v = static_cast<const int2 *>(at(c->r_chunk_v));
     L.deg = static_cast<const int32_t *>(at(c->r_deg));
@@ -2162,6 +2210,7 @@ static pbng_status bind_layout(pbng_ctx *c, void *dptr, uint64_t bytes, bool fre
     else chk(up(c->r_rec_id, c->h_rec_id.data(), c->h_rec_id.size() * 16));
     chk(up(c->r_path0, c->h_path0.data(), c->h_path0.size() * 8));
     chk(up(c->r_rec_a, c->h_rec_a.data(), c->h_rec_a.size()));
+    chk(up(c->r_rest, c->h_rest.data(), c->h_rest.size()));
     chk(up(c->r_rec_b, c->h_rec_b.data(), c->h_rec_b.size()));
     chk(up(c->r_rec_c, c->h_rec_c.data(), c->h_rec_c.size()));
     chk(up(c->r_chunk_off, c->h_chunk_off.data(), c->h_chunk_off.size() * 8));
@@ -2595,6 +2644,16 @@ pbng_status pbng_query(pbng_ctx *c, pbng_info *info) {
         info->schedule = effective_schedule(c);
     }
     info->graph_replays = (int32_t)c->dd_graph_replays;
+    info->records = !c->colored ? 0 : c->rest_rec ? 2 : 1;
+    return PBNG_OK;
+}
+
+pbng_status pbng_set_records(pbng_ctx *c, pbng_records records) {
+    if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
+    if (records != PBNG_RECORDS_AUTO && records != PBNG_RECORDS_STORED && records != PBNG_RECORDS_REST)
+        return fail(PBNG_E_INVALID_ARGUMENT, "set_records: unknown record layout");
+    if (c->colored) return fail(PBNG_E_BAD_ORDER, "set_records: the record layout is built by pbng_color; call it before");
+    c->records = (int)records;
     return PBNG_OK;
 }
 

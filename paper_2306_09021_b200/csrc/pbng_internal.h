@@ -48,6 +48,7 @@ struct Layout {
     const int2 *chunk_v = nullptr;       // [n_chunks] {first internal vertex, vertices in chunk}
     const int32_t *deg = nullptr;        // [n_free] records per vertex
     const int2 *path0 = nullptr;         // [n_free] path mode: slots S1, S2 before the vertex's first record
+    const void *rest = nullptr;          // Real4 [n_vertices] rest positions (rest-recompute records) or null
     const void *fext = nullptr;          // Real4 [n_free] or null (no body force)
     // weak constraints: per free vertex CSR of (constraint id, w0_i - w1_i) in input order
     const int32_t *wc_off = nullptr;     // [n_free + 1]
@@ -108,6 +109,7 @@ struct Problem {
     int64_t n_surf = 0, n_sv = 0, n_cbuckets = 1;  // contact detection sizes
     int device = 0, sm_count = 0;  // the context's CUDA device and its SM count (queried at bind)
     bool path = false;  // Neo-Hookean pair records in path order (pbng_kernels.cu "path records")
+    bool rest = false;  // path records without rest data: rebuilt from Layout::rest (pbng_kernels.cu "rest-recompute")
 };
 
 constexpr int kMaxDevices = 64;  // per-device launch caches (pbng_kernels.cu) are indexed by ordinal

@@ -654,6 +654,59 @@ __device__ __forceinline__ void prefetch_path(const Layout &L, int64_t r) {
     pf_l2(reinterpret_cast<const typename RT<R>::R4 *>(L.rec_a) + r);
 }
 
+// ------------------------------------------------------------------------------------------------
+// Rest-recompute path records (Problem::rest, pbng_set_records; SURVEY.md §8(d) lower-byte variant (i)).
+// A record keeps only the new neighbour {id | drop << 30} and E_e/6 (fp32: rec_id.y bits, 8 B; fp64: rec_c,
+// 16 B); the rest data is rebuilt from three REST slots T_0..2 pushed exactly like the position slots,
+// from the rest positions X, in slot order:
+//   a_k = X_{T_k} - X_i,  Dm' = [a_0 a_1 a_2],  c_0 = a_1 x a_2, c_1 = a_2 x a_0, c_2 = a_0 x a_1,
+//   det Dm' = a_0 . c_0;  the rows of B' = Dm'^{-1} are g_k = c_k / det Dm', and g_i = -(g_0 + g_1 + g_2)
+//   = -N / det Dm' with N = c_0 + c_1 + c_2, so
+//   s'_k = g_k . g_i = -(c_k . N) / det^2,   det B' = 1 / det Dm',   V_e E_e = |det Dm'| E_e / 6.
+// These are the stored record's quantities by definition (the slot relabelling is built in), computed in
+// the compute dtype instead of fp64.  Load-only records (E_e/6 = 0) take 1/det := 0 and so contribute
+// exactly 0 whatever their slots hold.
+// ------------------------------------------------------------------------------------------------
+template <bool STREAM>
+__device__ __forceinline__ int load_rest_rec(const Layout &L, int64_t r, float &E6) {
+    const int2 *ip = reinterpret_cast<const int2 *>(L.rec_id) + r;
+    const int2 id = STREAM ? lds(ip) : ld(ip);
+    E6 = __int_as_float(id.y);
+    PBNG_CHECK(r >= 0 && r < L.n_slots && (id.x & 0x3fffffff) < L.n_vertices);
+    return id.x;
+}
+template <bool STREAM>
+__device__ __forceinline__ int load_rest_rec(const Layout &L, int64_t r, double &E6) {
+    const int2 *ip = reinterpret_cast<const int2 *>(L.rec_id) + r;
+    const int2 id = STREAM ? lds(ip) : ld(ip);
+    E6 = ld(reinterpret_cast<const double *>(L.rec_c) + r);
+    PBNG_CHECK(r >= 0 && r < L.n_slots && (id.x & 0x3fffffff) < L.n_vertices);
+    return id.x;
+}
+template <class R>
+__device__ __forceinline__ typename RT<R>::R4 rest_at(const Layout &L, int i) {
+    return ld(reinterpret_cast<const typename RT<R>::R4 *>(L.rest) + i);
+}
+template <class R, class R4>
+__device__ __forceinline__ void rest_pair(const R4 &T0, const R4 &T1, const R4 &T2, const R (&Xi)[3], const R E6,
+                                          Pair<R, MODEL_NH> &p) {
+    const R a0[3] = {T0.x - Xi[0], T0.y - Xi[1], T0.z - Xi[2]};
+    const R a1[3] = {T1.x - Xi[0], T1.y - Xi[1], T1.z - Xi[2]};
+    const R a2[3] = {T2.x - Xi[0], T2.y - Xi[1], T2.z - Xi[2]};
+    const R c0[3] = {a1[1] * a2[2] - a1[2] * a2[1], a1[2] * a2[0] - a1[0] * a2[2], a1[0] * a2[1] - a1[1] * a2[0]};
+    const R c1[3] = {a2[1] * a0[2] - a2[2] * a0[1], a2[2] * a0[0] - a2[0] * a0[2], a2[0] * a0[1] - a2[1] * a0[0]};
+    const R c2[3] = {a0[1] * a1[2] - a0[2] * a1[1], a0[2] * a1[0] - a0[0] * a1[2], a0[0] * a1[1] - a0[1] * a1[0]};
+    const R det = a0[0] * c0[0] + a0[1] * c0[1] + a0[2] * c0[2];
+    const R N[3] = {c0[0] + c1[0] + c2[0], c0[1] + c1[1] + c2[1], c0[2] + c1[2] + c2[2]};
+    const R inv = E6 != R(0) ? R(1) / det : R(0);
+    const R q = -inv * inv;
+    p.s[0] = q * (c0[0] * N[0] + c0[1] * N[1] + c0[2] * N[2]);
+    p.s[1] = q * (c1[0] * N[0] + c1[1] * N[1] + c1[2] * N[2]);
+    p.s[2] = q * (c2[0] * N[0] + c2[1] * N[1] + c2[2] * N[2]);
+    p.detB = inv;
+    p.VE = E6 * fabs(det);
+}
+
 template <class R, int MODEL>
 __device__ __forceinline__ void prefetch_pair(const Layout &L, int64_t r) {
     pf_l2(L.rec_id + r);
@@ -980,7 +1033,8 @@ __device__ __forceinline__ void update_vertex(const Layout &L, typename RT<R>::R
 }
 
 // update_vertex for path records (Neo-Hookean, Problem::path): one neighbour gather per record
-template <class R, int ACCEL, bool FEXT, bool WC, int G>
+// (REST: rest-recompute records, one more gather of the neighbour's rest position per record)
+template <class R, int ACCEL, bool FEXT, bool WC, int G, bool REST = false>
 __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<R>::R4 *__restrict__ work,
                                                    const int64_t xs, const int v, const int64_t base, const int deg,
                                                    const int oi, const int hi, const R cmu, const R clam,
@@ -996,13 +1050,35 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
     R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
     const int2 p0 = ld(L.path0 + v);
     R4 S0 = xa4, S1 = gather<G>(work + p0.x), S2 = gather<G>(work + p0.y);
+    R4 T0, T1, T2;  // REST: the slots' rest positions
+    R Xi[3];
+    if constexpr (REST) {
+        T0 = rest_at<R>(L, v);
+        T1 = rest_at<R>(L, p0.x);
+        T2 = rest_at<R>(L, p0.y);
+        Xi[0] = T0.x; Xi[1] = T0.y; Xi[2] = T0.z;
+    }
 #pragma unroll kSweepUnroll
     for (int k = 0; k < deg; ++k) {
-        if (kSweepPrefetch > 0 && k + kSweepPrefetch < deg) prefetch_path<R>(L, base + (int64_t)(k + kSweepPrefetch) * kChunk);
         Pair<R, MODEL_NH> pr;
-        const int code = load_path_rec<true>(L, base + (int64_t)k * kChunk, pr);
-        const R4 nw = gather<G>(work + (code & 0x3fffffff));
-        path_push(S0, S1, S2, nw, code);
+        int code;
+        if constexpr (REST) {
+            if (kSweepPrefetch > 0 && k + kSweepPrefetch < deg)
+                pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + base + (int64_t)(k + kSweepPrefetch) * kChunk);
+            R E6;
+            code = load_rest_rec<true>(L, base + (int64_t)k * kChunk, E6);
+            const int j = code & 0x3fffffff;
+            const R4 nw = gather<G>(work + j), nr = rest_at<R>(L, j);
+            path_push(S0, S1, S2, nw, code);
+            path_push(T0, T1, T2, nr, code);
+            rest_pair<R>(T0, T1, T2, Xi, E6, pr);
+        } else {
+            if (kSweepPrefetch > 0 && k + kSweepPrefetch < deg)
+                prefetch_path<R>(L, base + (int64_t)(k + kSweepPrefetch) * kChunk);
+            code = load_path_rec<true>(L, base + (int64_t)k * kChunk, pr);
+            const R4 nw = gather<G>(work + (code & 0x3fffffff));
+            path_push(S0, S1, S2, nw, code);
+        }
         R d1[3], d2[3], d3[3];
         sub3<R>(S0, xa, d1);
         sub3<R>(S1, xa, d2);
@@ -1048,7 +1124,7 @@ template <class R, int MODEL> struct StageSmem {  // per warp: [ring][kGroups mb
 // (TMA), one mbarrier per group: HBM latency is hidden without holding registers, and the lanes only
 // gather their neighbour positions (through L1; they belong to other colours, read-only in this
 // launch).  The per-vertex summation order is ascending tet index, as in the oracle.
-template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, bool ONE_WAVE = false, bool PATH = false>
+template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, bool ONE_WAVE = false, int PATH = 0>
 __global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : SweepMinBlocks<R>::n)) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
                                                             const int64_t chunk_begin, const int64_t x_stride,
                                                             const int wi, const int oi, const int hi, const R cmu,
@@ -1066,7 +1142,8 @@ __global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : 
         const int deg = ld(L.deg + v);
         if (kPdl) {
             for (int k = 0; k < kSweepPrefetch && k < deg; ++k) {
-                if constexpr (PATH) prefetch_path<R>(L, base + (int64_t)k * kChunk);
+                if constexpr (PATH == 2) pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + base + (int64_t)k * kChunk);
+                else if constexpr (PATH) prefetch_path<R>(L, base + (int64_t)k * kChunk);
                 else prefetch_pair<R, MODEL>(L, base + (int64_t)k * kChunk);
             }
             asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1074,8 +1151,8 @@ __global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : 
         const int64_t xs = (int64_t)blockIdx.y * x_stride;
         R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
         if constexpr (PATH && MODEL == MODEL_NH)
-            update_vertex_path<R, ACCEL, FEXT, WC, GATHER_NC>(L, work, xs, v, base, deg, oi, hi, cmu, clam, omega,
-                                                              gamma, idt2);
+            update_vertex_path<R, ACCEL, FEXT, WC, GATHER_NC, PATH == 2>(L, work, xs, v, base, deg, oi, hi, cmu, clam,
+                                                                         omega, gamma, idt2);
         else
             update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_NC>(L, work, xs, v, base, deg, oi, hi, cmu, clam, omega,
                                                                 gamma, idt2);
@@ -1196,7 +1273,7 @@ template <class R, int SPLIT> struct SplitMinBlocks {
 // sweep_kernel; SPLIT > 1: the partial sums and fixed-order combination of sweep_split_kernel), so the
 // per-vertex summation order -- and the result -- is that of the colour-launch schedule with the same
 // split (pbng_host.cpp problem_split).
-template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int SPLIT, bool PATH = false>
+template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, int SPLIT, int PATH = 0>
 __global__ void __launch_bounds__(SplitBlock<SPLIT>::n, (MODEL == MODEL_FCR && SPLIT == 8) ? 3 : PBNG_SWEEP_MINB)
     sweep_pipe_kernel(const Layout L, const PipeLaunch P,
                                                                  const int64_t x_stride, const int32_t n_batch,
@@ -1259,8 +1336,8 @@ __global__ void __launch_bounds__(SplitBlock<SPLIT>::n, (MODEL == MODEL_FCR && S
         if (SPLIT == 1) {
             if (valid) {
                 if constexpr (PATH && MODEL == MODEL_NH)
-                    update_vertex_path<R, ACCEL, FEXT, WC, GATHER_COHERENT>(L, work, xs, v, base, ld(L.deg + v), oi,
-                                                                            P.hist, cmu, clam, omega, gamma, idt2);
+                    update_vertex_path<R, ACCEL, FEXT, WC, GATHER_COHERENT, PATH == 2>(
+                        L, work, xs, v, base, ld(L.deg + v), oi, P.hist, cmu, clam, omega, gamma, idt2);
                 else
                     update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_COHERENT>(L, work, xs, v, base, ld(L.deg + v), oi,
                                                                               P.hist, cmu, clam, omega, gamma, idt2);
@@ -1790,12 +1867,20 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
         const bool one_wave = kOneWave && sizeof(R) == 4 && !kSweepTma && blocks > (int64_t)sms * 6 &&
                               blocks <= (int64_t)sms * (1024 / kSweepBlock);
         if constexpr (MODEL == MODEL_NH) {
-            if (p.path) {
+            if (p.path && p.rest) {
                 if (one_wave)
-                    return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, true, true>, L, s.v_begin,
+                    return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, true, 2>, L, s.v_begin,
                                               s.n_v, s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga,
                                               idt2);
-                return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, false, true>, L, s.v_begin, s.n_v,
+                return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, false, 2>, L, s.v_begin, s.n_v,
+                                          s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga, idt2);
+            }
+            if (p.path) {
+                if (one_wave)
+                    return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, true, 1>, L, s.v_begin,
+                                              s.n_v, s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga,
+                                              idt2);
+                return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, false, 1>, L, s.v_begin, s.n_v,
                                           s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga, idt2);
             }
         }
@@ -1812,7 +1897,7 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
 
 // persistent grid: every SM filled to the kernel's occupancy (queried once per instantiation and device;
 // racing threads compute and store the same value)
-template <class R, int MODEL, int ACCEL, bool FE, bool W, int SPLIT, bool PATH = false>
+template <class R, int MODEL, int ACCEL, bool FE, bool W, int SPLIT, int PATH = 0>
 cudaError_t pipe_launch(const Problem &p, const Layout &L, const PipeLaunch &s, cudaStream_t st) {
     static std::atomic<int> cache[kMaxDevices];
     int blocks = cache[p.device % kMaxDevices].load(std::memory_order_acquire);
@@ -1838,7 +1923,8 @@ cudaError_t pipe_dispatch4(const Problem &p, const Layout &L, const PipeLaunch &
     if (s.split == 4) return pipe_launch<R, MODEL, ACCEL, FE, W, 4>(p, L, s, st);
     if (s.split == 8) return pipe_launch<R, MODEL, ACCEL, FE, W, 8>(p, L, s, st);
     if constexpr (MODEL == MODEL_NH) {
-        if (p.path) return pipe_launch<R, MODEL, ACCEL, FE, W, 1, true>(p, L, s, st);
+        if (p.path && p.rest) return pipe_launch<R, MODEL, ACCEL, FE, W, 1, 2>(p, L, s, st);
+        if (p.path) return pipe_launch<R, MODEL, ACCEL, FE, W, 1, 1>(p, L, s, st);
     }
     return pipe_launch<R, MODEL, ACCEL, FE, W, 1>(p, L, s, st);
 }
@@ -2292,9 +2378,26 @@ __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, con
             if (path) {  // path records: three slots, one new neighbour per record
                 const int2 p0 = L.path0[v];
                 R4 S0 = xa4, S1 = pos_load<R>(x, b, p0.x, x_stride, sh), S2 = pos_load<R>(x, b, p0.y, x_stride, sh);
+                const bool rest = L.rest != nullptr;  // rest-recompute records: the sweep's own rebuild
+                R4 T0 = xa4, T1 = xa4, T2 = xa4;
+                R Xi[3] = {R(0), R(0), R(0)};
+                if (rest) {
+                    T0 = rest_at<R>(L, v);
+                    T1 = rest_at<R>(L, p0.x);
+                    T2 = rest_at<R>(L, p0.y);
+                    Xi[0] = T0.x; Xi[1] = T0.y; Xi[2] = T0.z;
+                }
                 for (int k = 0; k < deg; ++k) {
                     Pair<R, MODEL_NH> pr;
-                    const int code = load_path_rec<true>(L, base + (int64_t)k * kChunk, pr);
+                    int code;
+                    if (rest) {
+                        R E6;
+                        code = load_rest_rec<true>(L, base + (int64_t)k * kChunk, E6);
+                        path_push(T0, T1, T2, rest_at<R>(L, code & 0x3fffffff), code);
+                        rest_pair<R>(T0, T1, T2, Xi, E6, pr);
+                    } else {
+                        code = load_path_rec<true>(L, base + (int64_t)k * kChunk, pr);
+                    }
                     path_push(S0, S1, S2, pos_load<R>(x, b, code & 0x3fffffff, x_stride, sh), code);
                     const double d1[3] = {S0.x - xa[0], S0.y - xa[1], S0.z - xa[2]};
                     const double d2[3] = {S1.x - xa[0], S1.y - xa[1], S1.z - xa[2]};

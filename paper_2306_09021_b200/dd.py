@@ -86,10 +86,11 @@ def combine_energy_residual(parts):
     return E, R
 
 
-def loopback_contexts(scene, n_ranks: int, device: int = 0, dtype: Optional[str] = None, owner=None):
+def loopback_contexts(scene, n_ranks: int, device: int = 0, dtype: Optional[str] = None, owner=None,
+                      records: str = "auto"):
     """One rank-local context per rank of a slab partition, all on one device (emulation)."""
     owner = slab_partition(scene.X, n_ranks) if owner is None else owner
-    return [context_from_scene(scene, device=device, dtype=dtype, partition=(owner, r, n_ranks))
+    return [context_from_scene(scene, device=device, dtype=dtype, partition=(owner, r, n_ranks), records=records)
             for r in range(n_ranks)], owner
 
 

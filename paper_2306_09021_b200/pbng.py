@@ -23,6 +23,7 @@ DTYPE = {"f32": 0, "f64": 1}
 MODEL = {"nh": 0, "fcr": 1, "snh": 2}
 ACCEL = {"none": 0, "sor": 1, "chebyshev": 2}
 SCHEDULE = {"auto": 0, "colour_launches": 1, "pipelined": 2}
+RECORDS = {"auto": 0, "stored": 1, "rest": 2}
 EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbng_color", "pbng_workspace_bytes",
            "pbng_bind_workspace", "pbng_set_positions", "pbng_get_positions", "pbng_iterate", "pbng_energy_residual",
            "pbng_synchronize", "pbng_query", "pbng_profile_enable", "pbng_profile_read", "pbng_destroy",
@@ -30,7 +31,8 @@ EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbn
            "pbng_halo_counts", "pbng_halo_vertices", "pbng_halo_pack", "pbng_halo_unpack", "pbng_test_polar",
            "pbng_set_inertia", "pbng_set_schedule", "pbng_detect_contacts", "pbng_update_constraints",
            "pbng_get_colours", "pbng_set_l2_persistence", "pbng_sweep_colour_part", "pbng_set_stream",
-           "pbng_nccl_unique_id", "pbng_partition", "pbng_group_create", "pbng_group_iterate", "pbng_group_destroy")
+           "pbng_nccl_unique_id", "pbng_partition", "pbng_group_create", "pbng_group_iterate", "pbng_group_destroy",
+           "pbng_set_records")
 
 WC_DTYPE = np.dtype([("n0", "<i4"), ("n1", "<i4"), ("idx0", "<i4", 4), ("idx1", "<i4", 4), ("w0", "<f8", 4),
                      ("w1", "<f8", 4), ("anchor", "<f8", 3), ("K", "<f8", 6)])
@@ -50,7 +52,7 @@ class Info(C.Structure):
                 ("iteration", C.c_int64), ("kernel_launches", C.c_int64), ("sweep_bytes", C.c_double),
                 ("accel_bytes", C.c_double), ("sweep_flops", C.c_double), ("n_local_vertices", C.c_int64),
                 ("n_ghosts", C.c_int64), ("rank", C.c_int32), ("n_ranks", C.c_int32), ("schedule", C.c_int32),
-                ("graph_replays", C.c_int32)]
+                ("graph_replays", C.c_int32), ("records", C.c_int32)]
 
 
 _lib = None
@@ -92,6 +94,7 @@ def lib():
     L.pbng_test_polar.argtypes = [C.c_int, vp, vp, i64, C.c_int]
     L.pbng_set_inertia.argtypes = [vp, d, vp]
     L.pbng_set_schedule.argtypes = [vp, C.c_int]
+    L.pbng_set_records.argtypes = [vp, C.c_int]
     L.pbng_detect_contacts.argtypes = [vp, i32, d, d, d, vp, i64, C.POINTER(i64)]
     L.pbng_update_constraints.argtypes = [vp, vp, vp, i64, C.POINTER(i64)]
     L.pbng_get_colours.argtypes = [vp, vp, C.POINTER(i32)]
@@ -233,6 +236,7 @@ class Context:
         torch = self._torch
         if dt == 0 or xtilde is None:
             _check(lib().pbng_set_inertia(self._h, float(dt), None))
+            self._inertia_dt = 0.0
             return
         if isinstance(xtilde, np.ndarray):
             xtilde = torch.from_numpy(_np(xtilde, self.np_dtype))
@@ -240,6 +244,7 @@ class Context:
             xtilde = xtilde.to(self.torch_dtype).contiguous()
         self._xt_keep = xtilde
         _check(lib().pbng_set_inertia(self._h, float(dt), xtilde.data_ptr()))
+        self._inertia_dt = float(dt)
 
     def get_positions(self, out=None):
         torch = self._torch
@@ -260,6 +265,11 @@ class Context:
     def set_schedule(self, schedule: str = "auto"):
         """'colour_launches' (one launch per colour pass), 'pipelined' (persistent dataflow launch) or 'auto'."""
         _check(lib().pbng_set_schedule(self._h, SCHEDULE[schedule]))
+
+    def set_records(self, records: str = "auto"):
+        """Pair-record layout built by color(): 'stored' rest data, 'rest' (recomputed from rest positions) or
+        'auto' (pbng_set_records; call before color())."""
+        _check(lib().pbng_set_records(self._h, RECORDS[records]))
 
     # ---- dynamic weak constraints ----------------------------------------------------------------
     def detect_contacts(self, thickness: float, k_n: float, k_t: float = 0.0, sample: int = 0) -> np.ndarray:
@@ -297,6 +307,10 @@ class Context:
             self.bind_workspace(self._torch.empty(int(nbytes * 1.25) + 256, dtype=self._torch.uint8,
                                                   device=f"cuda:{self.device}"))
             self.set_positions(saved)
+            # the library carries the backward-Euler target over a re-layout, but not across this re-bind:
+            # set it again from the last set_inertia
+            if getattr(self, "_inertia_dt", 0.0) > 0.0:
+                _check(lib().pbng_set_inertia(self._h, self._inertia_dt, self._xt_keep.data_ptr()))
             self.colours, self.n_colours = self.get_colours()
             return n.value
         _check(st)
@@ -439,15 +453,19 @@ def test_polar(F, dtype: str = "f32", device: int = 0) -> np.ndarray:
 
 
 def context_from_scene(scene, device=0, dtype: Optional[str] = None, stream=None, bind: bool = True,
-                       set_positions: bool = True, partition=None, l2_persist: bool = True) -> Context:
+                       set_positions: bool = True, partition=None, l2_persist: bool = True,
+                       records: str = "auto") -> Context:
     """Build, colour, bind and initialise a Context for a scenes.Scene (all samples of its batch).
     partition = (owner, rank, n_ranks) builds the rank-local context of a domain decomposition (driven by
     a Group or the colour-by-colour calls); (owner, rank, n_ranks, nccl_id) attaches the library's NCCL
     halo transport (pbng_partition);
-    l2_persist keeps the gathered position buffers L2-resident (pbng_set_l2_persistence)."""
+    l2_persist keeps the gathered position buffers L2-resident (pbng_set_l2_persistence);
+    records chooses the pair-record layout (pbng_set_records)."""
     ctx = Context(scene.X, scene.tets, n_batch=scene.n_batch, dtype=dtype or scene.dtype, device=device, stream=stream)
     ctx.set_material(scene.model, scene.E, scene.nu, scene.density, scene.gravity)
     ctx.set_constraints(scene.pinned, scene.targets, scene.wc)
+    if records != "auto":
+        ctx.set_records(records)
     if partition is not None:
         if len(partition) == 4:
             ctx.partition(*partition)

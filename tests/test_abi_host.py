@@ -145,3 +145,33 @@ def test_schedule_selection():
     with pytest.raises(P.PBNGError) as e:
         d.set_schedule("pipelined")
     assert e.value.status == 1
+
+
+def test_record_layout_selection():
+    """pbng_set_records (lower-byte variant (i)): rest-recompute records only for the
+    unbatched Neo-Hookean path layout; chosen before pbng_color; the algorithmic byte model shrinks."""
+    def make(s, records, nb=1, dtype="f32"):
+        c = P.Context(s.X, s.tets, n_batch=nb, dtype=dtype, device=-1)
+        c.set_material(s.model, s.E, s.nu, s.density, s.gravity)
+        c.set_constraints(s.pinned, np.repeat(s.targets[:1], nb, axis=0), s.wc)
+        if records is not None:
+            c.set_records(records)
+        c.color()
+        return c
+    s = G.make_config(3, "small")
+    q_st, q_re, q_au = make(s, "stored").query(), make(s, "rest").query(), make(s, None).query()
+    assert (q_st["records"], q_re["records"]) == (1, 2)
+    assert q_au["records"] in (1, 2)
+    # 8 B per record (+ path0, + the rest positions once) against 32 B per stored three-id record
+    assert q_re["sweep_bytes"] < 0.5 * q_st["sweep_bytes"]
+    # fp64: 48 B -> 16 B per record
+    assert make(s, "rest", dtype="f64").query()["sweep_bytes"] < make(s, "stored", dtype="f64").query()["sweep_bytes"]
+    # fixed-corotated and batched contexts keep stored rest data
+    assert make(G.make_config(5, "small"), "rest").query()["records"] == 1
+    assert make(s, "rest", nb=32).query()["records"] == 1
+    c = make(s, None)
+    with pytest.raises(P.PBNGError) as e:
+        c.set_records("rest")  # after pbng_color
+    assert e.value.status == 5
+    with pytest.raises(KeyError):
+        c.set_records("bogus")

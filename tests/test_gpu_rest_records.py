@@ -1,0 +1,125 @@
+"""Rest-recompute records (pbng_set_records(PBNG_RECORDS_REST); SURVEY.md §8(d) lower-byte variant (i)):
+Neo-Hookean path records that carry only the new neighbour and E_e/6, the sweep rebuilding Dm', g_j, s'_j,
+det B' and V_e from the rest positions in the compute dtype.  The iterates must
+match the fp64 oracle within north_star's tolerances (fp64 1e-10 x bbox diagonal / 1e-10 relative energy;
+fp32 1e-4 / 1e-5) exactly as the stored-record layout does; the schedules and the domain decomposition
+stay bitwise equal among themselves (same per-vertex arithmetic); load-only records (a vertex whose link
+falls into several paths) add exactly nothing although their three slots need not span a tet."""
+import numpy as np
+import pytest
+
+from scenes import generators as G
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": (1e-10, 1e-10), "f32": (1e-4, 1e-5)}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def run(s, dtype, records, schedule="auto"):
+    from paper_2306_09021_b200 import context_from_scene
+    ctx = context_from_scene(s, device=0, dtype=dtype, records=records)
+    info = ctx.query()
+    ctx.set_schedule(schedule)
+    ctx.iterate(s.iterations, s.accel, s.omega, s.rho, s.gamma)
+    E, R = ctx.energy_residual()
+    x = ctx.get_positions().cpu().numpy().astype(np.float64)
+    ctx.close()
+    return x, E, R, info
+
+
+def oracle_check(s, dtype, x, E, b=0):
+    from oracle import Oracle
+    o = Oracle(s, b)
+    xo, _ = o.iterate(s.x0[b], s.x0[b], 0, s.iterations, s.accel, s.omega, s.rho, s.gamma)
+    Eo = o.energy(xo)
+    err = np.abs(x[b] - xo).max() / s.bbox_diag()
+    erel = abs(E[b] - Eo) / max(abs(Eo), 1e-30)
+    tx, te = TOL[dtype]
+    assert err <= tx and erel <= te, (dtype, err, erel)
+    return err, erel
+
+
+@pytest.mark.parametrize("cfg,dtype", [(1, "f64"), (1, "f32"), (3, "f32"), (3, "f64")])
+def test_rest_records_match_oracle(cfg, dtype):
+    s = G.make_config(cfg, "small")
+    if cfg == 1:
+        s.iterations = 60
+    x, E, _, info = run(s, dtype, "rest")
+    assert info["records"] == 2
+    oracle_check(s, dtype, x, E)
+
+
+def test_rest_records_agree_with_stored_records_and_residual():
+    # the two layouts hold the same quantities (stored: fp64-derived, rounded to fp32; rest: derived in
+    # fp32): iterates agree to fp32 drift and the fp64 residual evaluations agree to fp32 data accuracy
+    s = G.make_config(3, "small")
+    xs, Es, Rs, i1 = run(s, "f32", "stored")
+    xr, Er, Rr, i2 = run(s, "f32", "rest")
+    assert i1["records"] == 1 and i2["records"] == 2
+    assert i2["sweep_bytes"] < i1["sweep_bytes"]
+    assert np.abs(xs - xr).max() / s.bbox_diag() < 1e-5
+    np.testing.assert_allclose(Er, Es, rtol=1e-6)
+    np.testing.assert_allclose(Rr, Rs, rtol=1e-3)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_rest_records_pipelined_equals_colour_launches_bitwise(dtype):
+    s = G.make_config(3, "small")
+    x1, E1, R1, _ = run(s, dtype, "rest", "colour_launches")
+    x2, E2, R2, info = run(s, dtype, "rest", "pipelined")
+    assert np.array_equal(x1, x2), np.abs(x1 - x2).max()
+    assert np.array_equal(E1, E2) and np.array_equal(R1, R2)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_rest_records_loopback_decomposition_is_bitwise(dtype):
+    from paper_2306_09021_b200 import dd
+    s = G.make_config(3, "small")
+    x1, E1, _, _ = run(s, dtype, "rest")
+    ctxs, owner = dd.loopback_contexts(s, 3, dtype=dtype, records="rest")
+    assert all(c.query()["records"] == 2 for c in ctxs)
+    grp = dd.Group(ctxs)
+    grp.iterate(s.iterations, s.accel, s.omega, s.rho, s.gamma)
+    E, _ = dd.combine_energy_residual([c.energy_residual() for c in ctxs])
+    pinned = np.zeros(s.n_vertices, bool)
+    pinned[s.pinned] = True
+    xs = [c.get_positions().cpu().numpy().astype(np.float64) for c in ctxs]
+    x = xs[0].copy()
+    for r in range(3):
+        rows = (owner == r) & ~pinned
+        x[:, rows] = xs[r][:, rows]
+    grp.close()
+    for c in ctxs:
+        c.close()
+    assert np.array_equal(x1, x), np.abs(x1 - x).max()
+    np.testing.assert_allclose(E, E1, rtol=1e-12)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_rest_records_disconnected_link_load_only(dtype):
+    # vertex 0: tets (0,1,2,3) and (0,1,2,7) form one path; (0,4,5,6) meets them only at vertex 0, so a
+    # second path starts with load-only records whose slots {x_7 or x_3, x_4, ...} need not span a tet
+    X = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [-1, 0, 0], [0, -1, 0], [0, 0, -1],
+                  [0.4, 0.4, -0.8]], float)
+    T = np.array([[0, 1, 2, 3], [0, 1, 2, 7], [0, 4, 5, 6]], np.int32)
+    pinned = np.array([1, 2, 4, 5, 6], np.int32)
+    load = np.array([[0.1, 0, 0], [0, 0.1, 0], [-0.1, 0, 0], [0, -0.1, 0], [0, 0, -0.1]])
+    rng = np.random.default_rng(3)
+    x0 = X.copy()[None]
+    free = np.setdiff1d(np.arange(8), pinned)
+    x0[0, free] += rng.uniform(-0.05, 0.05, (free.size, 3))
+    targets = (X[pinned] + load)[None]
+    x0[0, pinned] = targets[0]
+    s = G._finish("disconnected", X, T, "nh", 1e5, 0.3, 0.0, (0.0, 0.0, 0.0), pinned, targets, x0,
+                  iterations=25, accel="none", omega=1.0, dtype=dtype, h=1.0)
+    x, E, _, info = run(s, dtype, "rest")
+    assert info["records"] == 2
+    assert np.isfinite(x).all()
+    oracle_check(s, dtype, x, E)

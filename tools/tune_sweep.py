@@ -24,9 +24,10 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--dtype", default=None)
+    ap.add_argument("--records", default="auto", help="pair-record layout: auto | stored | rest")
     args = ap.parse_args()
     s = G.make_config(args.config, "full")
-    ctx = context_from_scene(s, device=0, dtype=args.dtype)
+    ctx = context_from_scene(s, device=0, dtype=args.dtype, records=args.records)
     if os.environ.get("PBNG_L2PERSIST", "1") == "0":
         ctx.set_l2_persistence(False)
     q = ctx.query()
@@ -46,6 +47,7 @@ def main():
     ms = float(np.median(times))
     byts = q["sweep_bytes"] + (q["accel_bytes"] if s.accel != "none" else 0)
     print(json.dumps({"pipe": os.environ.get("PBNG_SWEEP_PIPE", "default"), "config": args.config,
+                      "records": q["records"],
                       "dtype": ctx.dtype, "ms_per_iter": ms, "min_ms": float(min(times)),
                       "vupd_per_s": q["n_free"] * q["n_batch"] / (ms / 1e3),
                       "GBps": byts / (ms / 1e3) / 1e9, "energy": float(E[0]), "residual": float(R[0])}))
