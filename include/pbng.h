@@ -96,7 +96,7 @@ typedef struct {
     int32_t rank, n_ranks;
     int32_t schedule;         /* pbng_schedule pbng_iterate uses now (1 colour launches, 2 pipelined) */
     int32_t graph_replays;    /* CUDA-graph replays of decomposed iterate blocks owned by this context */
-    int32_t records;          /* pair-record layout built by pbng_color: 1 rest data stored, 2 rest recompute */
+    int32_t records;          /* pair-record layout built by pbng_color: 1 stored, 2 rest recompute, 3 table */
 } pbng_info;
 
 /* How pbng_iterate orders the colour passes (PAPER.md:693-705 fixes only the ORDER: colour after colour,
@@ -113,17 +113,28 @@ typedef enum { PBNG_SCHEDULE_AUTO = 0, PBNG_SCHEDULE_COLOUR_LAUNCHES = 1, PBNG_S
 
 /* Where the per-(vertex, tet) rest-shape data of the sweep comes from (Dm^{-1} and V^0_e
  * are functions of the rest positions X alone; PAPER.md:570-575 weighs storing per-element data against
- * recomputing it).  Results agree within rounding, not bitwise.
+ * recomputing it).
  * PBNG_RECORDS_STORED: every record carries its rest data precomputed in fp64 (Neo-Hookean path records:
  *   s'_1..3 = g_j . g_i and det B' in slot order, V_e E_e: 24 B fp32 / 48 B fp64).
  * PBNG_RECORDS_REST: Neo-Hookean path records of an unbatched (n_batch < 32) context carry only the new
  *   neighbour and E_e/6 (8 B fp32 / 16 B fp64); the sweep rebuilds Dm' = [X_a - X_i, X_b - X_i, X_c - X_i]
  *   (slot order) from the rest positions, kept as Real4 in the workspace, and derives g_j, s'_j, det B' and
- *   V_e = |det Dm'|/6 in the compute dtype.  Path records are walked by one warp per 32-vertex chunk, so
- *   REST also selects that sweep for problems that would otherwise split a chunk's records over several
- *   warps (small problems).  Other contexts (fixed-corotated, batched) keep STORED.
- * PBNG_RECORDS_AUTO (default): STORED (DESIGN.md section 7 has the measurements behind the choice). */
-typedef enum { PBNG_RECORDS_AUTO = 0, PBNG_RECORDS_STORED = 1, PBNG_RECORDS_REST = 2 } pbng_records;
+ *   V_e = |det Dm'|/6 in the compute dtype.  Results agree with STORED within rounding, not bitwise.
+ * PBNG_RECORDS_TABLE: the same contexts, when the mesh has at most 256 distinct {s'_1..3, det B'} tuples
+ *   (bitwise, in the compute dtype: regular meshes repeat a few element shapes) and fewer than 2^22
+ *   vertices: the tuples live in a table in the workspace and each record carries its entry index next to
+ *   the neighbour id, plus V_e E_e (8 B fp32 / 16 B fp64).  The sweep reads exactly the values STORED holds,
+ *   so the results are bitwise those of STORED.  Falls back to STORED when the table would overflow.
+ * REST and TABLE walk path records with one warp per 32-vertex chunk, so requesting them also selects that
+ * sweep for problems that would otherwise split a chunk's records over several warps (small problems).
+ * Other contexts (fixed-corotated, batched) keep STORED.
+ * PBNG_RECORDS_AUTO (default): TABLE where it applies (measured fastest), else STORED. */
+typedef enum {
+    PBNG_RECORDS_AUTO = 0,
+    PBNG_RECORDS_STORED = 1,
+    PBNG_RECORDS_REST = 2,
+    PBNG_RECORDS_TABLE = 3
+} pbng_records;
 
 /* Create a mesh context: rest positions X (n_vertices*3 doubles), tets (n_tets*4
  * int32, any orientation), n_batch >= 1 independent samples sharing mesh, material and colouring

@@ -181,7 +181,10 @@ struct pbng_ctx {
     // rest-recompute path records (SURVEY.md §8(d) lower-byte variant (i)): {id | drop, E_e/6} only, the
     // kernels rebuild s'_j, det B' and V_e from the rest positions h_rest (Real4 [n_local], internal ids)
     bool rest_rec = false;
-    int records = 0;  // pbng_records requested (0 auto, 1 stored rest data, 2 rest recompute)
+    // table path records: h_rec_a holds the n_tab distinct {s'_0..2, det B'} tuples, record codes index them
+    bool tab_rec = false;
+    int64_t n_tab = 0;
+    int records = 0;  // pbng_records requested (0 auto, 1 stored rest data, 2 rest recompute, 3 table)
     std::vector<unsigned char> h_rest;
     std::vector<int64_t> inc_off;  // vertex -> incident tets (ascending), mesh-only: built once and kept
     std::vector<int32_t> inc;
@@ -515,6 +518,105 @@ bool use_rest_records(const pbng_ctx *c) {
     return want == 2;
 }
 
+// table records: wanted when requested (pbng_records 3 / PBNG_RECORDS=3) or by auto, for the same contexts
+// as the rest-recompute ones and ids below 2^22 (bits 22..29 of the code carry the table index); whether the
+// mesh has few enough distinct rest tuples is only known once the records exist (build_rest_table)
+bool want_table_records(const pbng_ctx *c) {
+    static const int env = [] {
+        const char *e = getenv("PBNG_RECORDS");
+        return e ? atoi(e) : 0;
+    }();
+    if (!c->path_rec || layout_lane_shift(c) != 0 || c->n_local >= (1 << 22)) return false;
+    const int want = c->records != 0 ? c->records : env;
+    return want == 3 || want == 0;
+}
+
+// Table records are regrouped so that a lane's records come in groups of kRecGroup consecutive slots
+// (pbng_kernels.cu update_vertex_path, mode 3): record k of lane `lane` of chunk ch sits at
+//     chunk_off[ch] + (k / 4) * 128 + 4 * lane + k % 4,
+// chunk widths rounded up to a multiple of 4 (padding slots: code 0, VE 0, never read), so one lane loads
+// four 8-byte records with two 16-byte loads and has four neighbour gathers in flight at once.
+template <class R>
+void group_table_records(pbng_ctx *c) {
+    const int64_t nch = c->n_chunks;
+    std::vector<int64_t> off((size_t)nch + 1, 0);
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        const int64_t w = (c->h_chunk_off[ch + 1] - c->h_chunk_off[ch]) / kChunk;
+        off[ch + 1] = off[ch] + (w + kRecGroup - 1) / kRecGroup * kRecGroup * kChunk;
+    }
+    const bool f64 = c->dtype == DT_F64;
+    std::vector<int2> id2((size_t)std::max<int64_t>(off[nch], 1), make_int2(0, 0));
+    std::vector<unsigned char> rc(f64 ? (size_t)std::max<int64_t>(off[nch], 1) * 8 : c->h_rec_c.size(), 0);
+    parallel_for(nch, [&](int64_t lo, int64_t hi) {
+        for (int64_t ch = lo; ch < hi; ++ch) {
+            const int64_t w = (c->h_chunk_off[ch + 1] - c->h_chunk_off[ch]) / kChunk;
+            for (int64_t k = 0; k < w; ++k)
+                for (int lane = 0; lane < kChunk; ++lane) {
+                    const int64_t r = c->h_chunk_off[ch] + k * kChunk + lane;
+                    const int64_t r2 = off[ch] + (k / kRecGroup) * (kRecGroup * kChunk) + kRecGroup * lane + k % kRecGroup;
+                    id2[r2] = c->h_rec_id2[r];
+                    if (f64) std::memcpy(rc.data() + r2 * 8, c->h_rec_c.data() + r * 8, 8);
+                }
+        }
+    }, 256);
+    c->h_rec_id2.swap(id2);
+    if (f64) c->h_rec_c.swap(rc);
+    c->h_chunk_off.swap(off);
+    c->n_slots = c->h_chunk_off.back();
+}
+
+// Deduplicate the stored path records' rest data {s'_0..2, det B'} (compared bit for bit in the compute
+// dtype) into a table of at most 256 entries; on success h_rec_a becomes the table and each record's code
+// carries its entry in bits 22..29, so the kernels read exactly the values the stored layout holds.
+// Regular meshes (the configs' Kuhn grids, the paper's 5-tet grids) repeat a few element shapes; an
+// irregular mesh overflows the table and keeps the stored layout.
+template <class R>
+bool build_rest_table(pbng_ctx *c) {
+    constexpr size_t K = 4 * sizeof(R);
+    struct Key {
+        unsigned char b[K];
+        bool operator==(const Key &o) const { return std::memcmp(b, o.b, K) == 0; }
+    };
+    struct Hash {
+        size_t operator()(const Key &k) const {
+            uint64_t h = 1469598103934665603ull;
+            for (size_t q = 0; q < K; ++q) h = (h ^ k.b[q]) * 1099511628211ull;
+            return (size_t)h;
+        }
+    };
+    const int64_t ns = c->n_slots;
+    if (ns <= 0) return false;
+    auto key_at = [&](int64_t r) {
+        Key k;
+        std::memcpy(k.b, c->h_rec_a.data() + (size_t)r * K, K);
+        return k;
+    };
+    std::unordered_map<Key, int32_t, Hash> table;
+    std::mutex mu;
+    bool overflow = false;
+    parallel_for(ns, [&](int64_t lo, int64_t hi) {
+        std::unordered_map<Key, int32_t, Hash> local;
+        for (int64_t r = lo; r < hi && local.size() <= 256; ++r) local.emplace(key_at(r), 0);
+        std::lock_guard<std::mutex> lk(mu);
+        for (const auto &kv : local) table.emplace(kv.first, 0);
+        if (local.size() > 256 || table.size() > 256) overflow = true;
+    }, 1 << 16);
+    if (overflow || table.size() > 256) return false;
+    std::vector<Key> keys;
+    for (const auto &kv : table) keys.push_back(kv.first);
+    std::sort(keys.begin(), keys.end(), [](const Key &a, const Key &b) { return std::memcmp(a.b, b.b, K) < 0; });
+    for (size_t q = 0; q < keys.size(); ++q) table[keys[q]] = (int32_t)q;
+    parallel_for(ns, [&](int64_t lo, int64_t hi) {
+        for (int64_t r = lo; r < hi; ++r)
+            c->h_rec_id2[r].x = (int32_t)((uint32_t)c->h_rec_id2[r].x | ((uint32_t)table.at(key_at(r)) << 22));
+    }, 1 << 16);
+    c->n_tab = (int64_t)keys.size();
+    c->h_rec_a.assign(keys.size() * K, 0);
+    for (size_t q = 0; q < keys.size(); ++q) std::memcpy(c->h_rec_a.data() + q * K, keys[q].b, K);
+    group_table_records<R>(c);
+    return true;
+}
+
 // weak constraints held by this context (owned first): distinct nodes with combined weights w0_j - w1_j;
 // per owned free vertex the list of (constraint, w0_i - w1_i) in input order.  Also the fast path of
 // pbng_update_constraints (colouring unchanged: only these arrays are rebuilt and uploaded).
@@ -781,6 +883,9 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     }
 
     }, 64);
+    c->tab_rec = false;
+    c->n_tab = 0;
+    if (!c->rest_rec && want_table_records(c)) c->tab_rec = build_rest_table<R>(c);
 
     // body force f^ext_i = sum_e R^0 g V_e / 4, free vertices
     const bool has_fext = c->density > 0 && (c->grav[0] != 0 || c->grav[1] != 0 || c->grav[2] != 0);
@@ -847,7 +952,7 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     // sweep_batched2_kernel (sh 6), otherwise sample-minor groups of 32 (sh 5)
     p.lane_shift = layout_lane_shift(c);
     p.path = c->path_rec;
-    p.rest = c->rest_rec;
+    p.path_mode = !c->path_rec ? 0 : c->rest_rec ? 2 : c->tab_rec ? 3 : 1;
     p.cmu = cmu;
     p.clam = clam;
     for (int k = 0; k < 3; ++k) p.rho_g[k] = c->density * c->grav[k];
@@ -1226,7 +1331,8 @@ double sweep_bytes_model(const pbng_ctx *c) {
     // (load-only ones included) + the per-vertex first slots (8 B)
     // rest-recompute records: {id | drop, E_e/6} = 8 B (fp32) / 16 B (fp64), plus every held vertex's rest
     // position read once (below)
-    const double rec = c->rest_rec ? (c->dtype == DT_F64 ? 16.0 : 8.0)
+    // table records: {id | entry | drop, VE} (+ VE in fp64) = 8 B / 16 B, the table itself is <= 8 KB
+    const double rec = (c->rest_rec || c->tab_rec) ? (c->dtype == DT_F64 ? 16.0 : 8.0)
                        : c->path_rec ? (c->dtype == DT_F64 ? 48.0 : 24.0)
                        : c->model == MODEL_NH ? (c->dtype == DT_F64 ? 56.0 : 32.0) : (c->dtype == DT_F64 ? 96.0 : 52.0);
     double b = (double)(c->path_rec ? c->n_records : c->n_pairs) * rec + (double)(c->n_chunks + 1) * 8.0 +
@@ -1262,7 +1368,9 @@ int problem_split(const pbng_ctx *c) {
     }();
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8) return forced;
     // rest-recompute records requested explicitly: they exist only as path records, walked by one warp per chunk
-    if (c->records == PBNG_RECORDS_REST && c->model == MODEL_NH && !batched_layout(c)) return 1;
+    if ((c->records == PBNG_RECORDS_REST || c->records == PBNG_RECORDS_TABLE) && c->model == MODEL_NH &&
+        !batched_layout(c))
+        return 1;
     int64_t gfree = 0;  // free vertices of the whole mesh (all ranks)
     for (int64_t k : c->gcol_nfree) gfree += k;
     const int64_t chunks_per_colour = gfree * c->nb / kChunk / std::max(c->ncol, 1);
@@ -2161,6 +2269,7 @@ static pbng_status bind_layout(pbng_ctx *c, void *dptr, uint64_t bytes, bool fre
     L.rec_b = at(c->r_rec_b);
     L.rec_c = at(c->r_rec_c);
     L.rest = c->rest_rec ? at(c->r_rest) : nullptr;
+    L.path_mode = c->prob.path_mode;
     L.chunk_off = static_cast<const int64_t *>(at(c->r_chunk_off));
     L.chunk_v = static_cast<const int2 *>(at(c->r_chunk_v));
     L.deg = static_cast<const int32_t *>(at(c->r_deg));
@@ -2644,13 +2753,14 @@ pbng_status pbng_query(pbng_ctx *c, pbng_info *info) {
         info->schedule = effective_schedule(c);
     }
     info->graph_replays = (int32_t)c->dd_graph_replays;
-    info->records = !c->colored ? 0 : c->rest_rec ? 2 : 1;
+    info->records = !c->colored ? 0 : c->rest_rec ? 2 : c->tab_rec ? 3 : 1;
     return PBNG_OK;
 }
 
 pbng_status pbng_set_records(pbng_ctx *c, pbng_records records) {
     if (!c) return fail(PBNG_E_INVALID_ARGUMENT, "null context");
-    if (records != PBNG_RECORDS_AUTO && records != PBNG_RECORDS_STORED && records != PBNG_RECORDS_REST)
+    if (records != PBNG_RECORDS_AUTO && records != PBNG_RECORDS_STORED && records != PBNG_RECORDS_REST &&
+        records != PBNG_RECORDS_TABLE)
         return fail(PBNG_E_INVALID_ARGUMENT, "set_records: unknown record layout");
     if (c->colored) return fail(PBNG_E_BAD_ORDER, "set_records: the record layout is built by pbng_color; call it before");
     c->records = (int)records;

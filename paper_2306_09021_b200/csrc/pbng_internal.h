@@ -20,6 +20,7 @@ constexpr int kChunk = 32;        // vertices per SELL chunk == one warp
 #endif
 constexpr int kSweepBlock = PBNG_SWEEP_BLOCK;  // threads per sweep CTA (a multiple of the 32-vertex chunk)
 constexpr int kWcMaxNodes = 8;    // distinct nodes per weak constraint
+constexpr int kRecGroup = 4;      // table path records: consecutive slots per lane (pbng_host.cpp group_table_records)
 constexpr int kRedBlock = 256;    // threads per reduction CTA
 
 // Pair-record layout (SELL-32, one record per (free vertex i, incident tet e), vertex-major within a
@@ -49,6 +50,7 @@ struct Layout {
     const int32_t *deg = nullptr;        // [n_free] records per vertex
     const int2 *path0 = nullptr;         // [n_free] path mode: slots S1, S2 before the vertex's first record
     const void *rest = nullptr;          // Real4 [n_vertices] rest positions (rest-recompute records) or null
+    int path_mode = 0;                   // NH path records: 0 none, 1 stored, 2 rest recompute, 3 table
     const void *fext = nullptr;          // Real4 [n_free] or null (no body force)
     // weak constraints: per free vertex CSR of (constraint id, w0_i - w1_i) in input order
     const int32_t *wc_off = nullptr;     // [n_free + 1]
@@ -109,7 +111,8 @@ struct Problem {
     int64_t n_surf = 0, n_sv = 0, n_cbuckets = 1;  // contact detection sizes
     int device = 0, sm_count = 0;  // the context's CUDA device and its SM count (queried at bind)
     bool path = false;  // Neo-Hookean pair records in path order (pbng_kernels.cu "path records")
-    bool rest = false;  // path records without rest data: rebuilt from Layout::rest (pbng_kernels.cu "rest-recompute")
+    int path_mode = 0;  // 1 stored rest data, 2 rebuilt from Layout::rest ("rest-recompute"), 3 table of
+                        // distinct rest tuples indexed from the record (pbng_kernels.cu load_path_rec)
 };
 
 constexpr int kMaxDevices = 64;  // per-device launch caches (pbng_kernels.cu) are indexed by ordinal

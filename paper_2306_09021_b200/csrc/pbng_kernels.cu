@@ -619,28 +619,68 @@ __device__ __forceinline__ void pf_l2(const void *p) { asm volatile("prefetch.gl
 // exactly 0.  fp32: rec_id = int2 {id | drop << 30, VE bits}, rec_a float4 {s'_0 s'_1 s'_2 det B'} = 24 B;
 // fp64: int2 {id | drop << 30, 0}, double4, rec_c VE = 48 B.
 // ------------------------------------------------------------------------------------------------
-template <bool STREAM>
+// TAB (table records, Problem::path_mode 3): rec_a holds the mesh's DISTINCT {s'_0..2, det B'} tuples and
+// bits 22..29 of the record's code index them (ids < 2^22); the code returned has those bits cleared.
+template <bool STREAM, bool TAB = false>
 __device__ __forceinline__ int load_path_rec(const Layout &L, int64_t r, Pair<float, MODEL_NH> &p) {
     const int2 *ip = reinterpret_cast<const int2 *>(L.rec_id) + r;
-    const float4 *a = reinterpret_cast<const float4 *>(L.rec_a) + r;
     const int2 id = STREAM ? lds(ip) : ld(ip);
-    const float4 x = STREAM ? lds(a) : ld(a);
+    const float4 x = TAB ? ld(reinterpret_cast<const float4 *>(L.rec_a) + (((unsigned)id.x >> 22) & 0xffu))
+                         : STREAM ? lds(reinterpret_cast<const float4 *>(L.rec_a) + r)
+                                  : ld(reinterpret_cast<const float4 *>(L.rec_a) + r);
     p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
     p.VE = __int_as_float(id.y);
-    PBNG_CHECK(r >= 0 && r < L.n_slots && (id.x & 0x3fffffff) < L.n_vertices);
-    return id.x;
+    const int code = TAB ? (int)((unsigned)id.x & ~(0xffu << 22)) : id.x;
+    PBNG_CHECK(r >= 0 && r < L.n_slots && (code & 0x3fffffff) < L.n_vertices);
+    return code;
 }
-template <bool STREAM>
+template <bool STREAM, bool TAB = false>
 __device__ __forceinline__ int load_path_rec(const Layout &L, int64_t r, Pair<double, MODEL_NH> &p) {
     const int2 *ip = reinterpret_cast<const int2 *>(L.rec_id) + r;
-    const double4 *a = reinterpret_cast<const double4 *>(L.rec_a) + r;
     const int2 id = STREAM ? lds(ip) : ld(ip);
-    const double4 x = STREAM ? lds(a) : ld(a);
+    const double4 x = TAB ? ld(reinterpret_cast<const double4 *>(L.rec_a) + (((unsigned)id.x >> 22) & 0xffu))
+                          : STREAM ? lds(reinterpret_cast<const double4 *>(L.rec_a) + r)
+                                   : ld(reinterpret_cast<const double4 *>(L.rec_a) + r);
     p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
     p.VE = ld(reinterpret_cast<const double *>(L.rec_c) + r);
-    PBNG_CHECK(r >= 0 && r < L.n_slots && (id.x & 0x3fffffff) < L.n_vertices);
-    return id.x;
+    const int code = TAB ? (int)((unsigned)id.x & ~(0xffu << 22)) : id.x;
+    PBNG_CHECK(r >= 0 && r < L.n_slots && (code & 0x3fffffff) < L.n_vertices);
+    return code;
 }
+// table records in groups of kRecGroup = 4 slots per lane (pbng_host.cpp group_table_records): the first slot
+// of lane `lane`'s group g is chunk_off + g * 128 + 4 * lane = base + 3 * lane + g * 128 with base = chunk_off
+// + lane (chunk_off is a multiple of 128).  One group = two 16-byte loads of {code, VE bits} pairs (fp32;
+// fp64 VE: two more 16-byte loads from rec_c).
+__device__ __forceinline__ int64_t group_base(int64_t base) { return base + 3 * (base & 31); }
+template <class R> struct RecGroup {
+    int code[4];
+    R VE[4];
+};
+__device__ __forceinline__ void load_group(const Layout &L, int64_t r, RecGroup<float> &g) {
+    const int4 *p = reinterpret_cast<const int4 *>(reinterpret_cast<const int2 *>(L.rec_id) + r);
+    const int4 a = lds(p), b = lds(p + 1);
+    g.code[0] = a.x; g.code[1] = a.z; g.code[2] = b.x; g.code[3] = b.z;
+    g.VE[0] = __int_as_float(a.y); g.VE[1] = __int_as_float(a.w);
+    g.VE[2] = __int_as_float(b.y); g.VE[3] = __int_as_float(b.w);
+    PBNG_CHECK(r >= 0 && r + 3 < L.n_slots && (r & 3) == 0);
+}
+__device__ __forceinline__ void load_group(const Layout &L, int64_t r, RecGroup<double> &g) {
+    const int4 *p = reinterpret_cast<const int4 *>(reinterpret_cast<const int2 *>(L.rec_id) + r);
+    const int4 a = lds(p), b = lds(p + 1);
+    g.code[0] = a.x; g.code[1] = a.z; g.code[2] = b.x; g.code[3] = b.z;
+    const double4 v = lds(reinterpret_cast<const double4 *>(L.rec_c) + (r >> 2));
+    g.VE[0] = v.x; g.VE[1] = v.y; g.VE[2] = v.z; g.VE[3] = v.w;
+    PBNG_CHECK(r >= 0 && r + 3 < L.n_slots && (r & 3) == 0);
+}
+// the table entry {s'_0..2, det B'} of a table-record code; returns the code without the entry bits
+template <class R>
+__device__ __forceinline__ int table_pair(const Layout &L, const int code, const R VE, Pair<R, MODEL_NH> &p) {
+    const typename RT<R>::R4 x = ld(reinterpret_cast<const typename RT<R>::R4 *>(L.rec_a) + (((unsigned)code >> 22) & 0xffu));
+    p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
+    p.VE = VE;
+    return (int)((unsigned)code & ~(0xffu << 22));
+}
+
 template <class T>
 __device__ __forceinline__ void path_push(T &S0, T &S1, T &S2, const T &nw, const int code) {
     const int drop = (int)((unsigned)code >> 30);
@@ -1033,8 +1073,9 @@ __device__ __forceinline__ void update_vertex(const Layout &L, typename RT<R>::R
 }
 
 // update_vertex for path records (Neo-Hookean, Problem::path): one neighbour gather per record
-// (REST: rest-recompute records, one more gather of the neighbour's rest position per record)
-template <class R, int ACCEL, bool FEXT, bool WC, int G, bool REST = false>
+// (MODE 1: stored records; 2: rest-recompute records, one more gather of the neighbour's rest position per
+// record; 3: table records, the rest data read from the small table of distinct tuples)
+template <class R, int ACCEL, bool FEXT, bool WC, int G, int MODE = 1>
 __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<R>::R4 *__restrict__ work,
                                                    const int64_t xs, const int v, const int64_t base, const int deg,
                                                    const int oi, const int hi, const R cmu, const R clam,
@@ -1050,6 +1091,7 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
     R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
     const int2 p0 = ld(L.path0 + v);
     R4 S0 = xa4, S1 = gather<G>(work + p0.x), S2 = gather<G>(work + p0.y);
+    constexpr bool REST = MODE == 2;
     R4 T0, T1, T2;  // REST: the slots' rest positions
     R Xi[3];
     if constexpr (REST) {
@@ -1058,6 +1100,33 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
         T2 = rest_at<R>(L, p0.y);
         Xi[0] = T0.x; Xi[1] = T0.y; Xi[2] = T0.z;
     }
+    if constexpr (MODE == 3) {
+        // table records: four records per step, their four neighbour gathers issued together
+        const int64_t b4 = group_base(base);
+        for (int k = 0; k < deg; k += 4) {
+            if (kSweepPrefetch > 0 && k + 4 * kSweepPrefetch < deg)
+                pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + b4 + (int64_t)(k + 4 * kSweepPrefetch) * kChunk);
+            RecGroup<R> g;
+            load_group(L, b4 + (int64_t)k * kChunk, g);
+            R4 nw[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) nw[q] = gather<G>(work + (g.code[q] & 0x3fffff));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (k + q < deg) {
+                    Pair<R, MODEL_NH> pr;
+                    const int code = table_pair<R>(L, g.code[q], g.VE[q], pr);
+                    PBNG_CHECK((code & 0x3fffffff) < L.n_vertices);
+                    path_push(S0, S1, S2, nw[q], code);
+                    R d1[3], d2[3], d3[3];
+                    sub3<R>(S0, xa, d1);
+                    sub3<R>(S1, xa, d2);
+                    sub3<R>(S2, xa, d3);
+                    contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
+                }
+            }
+        }
+    } else {
 #pragma unroll kSweepUnroll
     for (int k = 0; k < deg; ++k) {
         Pair<R, MODEL_NH> pr;
@@ -1073,9 +1142,11 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
             path_push(T0, T1, T2, nr, code);
             rest_pair<R>(T0, T1, T2, Xi, E6, pr);
         } else {
-            if (kSweepPrefetch > 0 && k + kSweepPrefetch < deg)
-                prefetch_path<R>(L, base + (int64_t)(k + kSweepPrefetch) * kChunk);
-            code = load_path_rec<true>(L, base + (int64_t)k * kChunk, pr);
+            if (kSweepPrefetch > 0 && k + kSweepPrefetch < deg) {
+                if constexpr (MODE == 3) pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + base + (int64_t)(k + kSweepPrefetch) * kChunk);
+                else prefetch_path<R>(L, base + (int64_t)(k + kSweepPrefetch) * kChunk);
+            }
+            code = load_path_rec<true, MODE == 3>(L, base + (int64_t)k * kChunk, pr);
             const R4 nw = gather<G>(work + (code & 0x3fffffff));
             path_push(S0, S1, S2, nw, code);
         }
@@ -1084,6 +1155,7 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
         sub3<R>(S1, xa, d2);
         sub3<R>(S2, xa, d3);
         contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
+    }
     }
     if (WC) wc_contrib<R, R, true, G>(L, work, 0, v, xa, f, A);
     if (idt2 > R(0)) inertia_contrib<R, R>(L, v, ld(reinterpret_cast<const R4 *>(L.xtilde) + xs + v), idt2, xa, f, A);
@@ -1142,7 +1214,10 @@ __global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : 
         const int deg = ld(L.deg + v);
         if (kPdl) {
             for (int k = 0; k < kSweepPrefetch && k < deg; ++k) {
-                if constexpr (PATH == 2) pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + base + (int64_t)k * kChunk);
+                if constexpr (PATH == 3) {
+                    if (4 * k < deg) pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + group_base(base) + (int64_t)(4 * k) * kChunk);
+                }
+                else if constexpr (PATH == 2) pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + base + (int64_t)k * kChunk);
                 else if constexpr (PATH) prefetch_path<R>(L, base + (int64_t)k * kChunk);
                 else prefetch_pair<R, MODEL>(L, base + (int64_t)k * kChunk);
             }
@@ -1151,7 +1226,7 @@ __global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : 
         const int64_t xs = (int64_t)blockIdx.y * x_stride;
         R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
         if constexpr (PATH && MODEL == MODEL_NH)
-            update_vertex_path<R, ACCEL, FEXT, WC, GATHER_NC, PATH == 2>(L, work, xs, v, base, deg, oi, hi, cmu, clam,
+            update_vertex_path<R, ACCEL, FEXT, WC, GATHER_NC, PATH>(L, work, xs, v, base, deg, oi, hi, cmu, clam,
                                                                          omega, gamma, idt2);
         else
             update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_NC>(L, work, xs, v, base, deg, oi, hi, cmu, clam, omega,
@@ -1336,7 +1411,7 @@ __global__ void __launch_bounds__(SplitBlock<SPLIT>::n, (MODEL == MODEL_FCR && S
         if (SPLIT == 1) {
             if (valid) {
                 if constexpr (PATH && MODEL == MODEL_NH)
-                    update_vertex_path<R, ACCEL, FEXT, WC, GATHER_COHERENT, PATH == 2>(
+                    update_vertex_path<R, ACCEL, FEXT, WC, GATHER_COHERENT, PATH>(
                         L, work, xs, v, base, ld(L.deg + v), oi, P.hist, cmu, clam, omega, gamma, idt2);
                 else
                     update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_COHERENT>(L, work, xs, v, base, ld(L.deg + v), oi,
@@ -1867,7 +1942,15 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
         const bool one_wave = kOneWave && sizeof(R) == 4 && !kSweepTma && blocks > (int64_t)sms * 6 &&
                               blocks <= (int64_t)sms * (1024 / kSweepBlock);
         if constexpr (MODEL == MODEL_NH) {
-            if (p.path && p.rest) {
+            if (p.path && p.path_mode == 3) {
+                if (one_wave)
+                    return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, true, 3>, L, s.v_begin,
+                                              s.n_v, s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga,
+                                              idt2);
+                return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, false, 3>, L, s.v_begin, s.n_v,
+                                          s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga, idt2);
+            }
+            if (p.path && p.path_mode == 2) {
                 if (one_wave)
                     return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, true, 2>, L, s.v_begin,
                                               s.n_v, s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga,
@@ -1923,7 +2006,8 @@ cudaError_t pipe_dispatch4(const Problem &p, const Layout &L, const PipeLaunch &
     if (s.split == 4) return pipe_launch<R, MODEL, ACCEL, FE, W, 4>(p, L, s, st);
     if (s.split == 8) return pipe_launch<R, MODEL, ACCEL, FE, W, 8>(p, L, s, st);
     if constexpr (MODEL == MODEL_NH) {
-        if (p.path && p.rest) return pipe_launch<R, MODEL, ACCEL, FE, W, 1, 2>(p, L, s, st);
+        if (p.path && p.path_mode == 3) return pipe_launch<R, MODEL, ACCEL, FE, W, 1, 3>(p, L, s, st);
+        if (p.path && p.path_mode == 2) return pipe_launch<R, MODEL, ACCEL, FE, W, 1, 2>(p, L, s, st);
         if (p.path) return pipe_launch<R, MODEL, ACCEL, FE, W, 1, 1>(p, L, s, st);
     }
     return pipe_launch<R, MODEL, ACCEL, FE, W, 1>(p, L, s, st);
@@ -2378,7 +2462,7 @@ __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, con
             if (path) {  // path records: three slots, one new neighbour per record
                 const int2 p0 = L.path0[v];
                 R4 S0 = xa4, S1 = pos_load<R>(x, b, p0.x, x_stride, sh), S2 = pos_load<R>(x, b, p0.y, x_stride, sh);
-                const bool rest = L.rest != nullptr;  // rest-recompute records: the sweep's own rebuild
+                const bool rest = L.path_mode == 2;  // rest-recompute records: the sweep's own rebuild
                 R4 T0 = xa4, T1 = xa4, T2 = xa4;
                 R Xi[3] = {R(0), R(0), R(0)};
                 if (rest) {
@@ -2395,6 +2479,9 @@ __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, con
                         code = load_rest_rec<true>(L, base + (int64_t)k * kChunk, E6);
                         path_push(T0, T1, T2, rest_at<R>(L, code & 0x3fffffff), code);
                         rest_pair<R>(T0, T1, T2, Xi, E6, pr);
+                    } else if (L.path_mode == 3) {
+                        const int64_t r = group_base(base) + (int64_t)(k & ~3) * kChunk + (k & 3);
+                        code = load_path_rec<true, true>(L, r, pr);
                     } else {
                         code = load_path_rec<true>(L, base + (int64_t)k * kChunk, pr);
                     }

@@ -23,7 +23,7 @@ DTYPE = {"f32": 0, "f64": 1}
 MODEL = {"nh": 0, "fcr": 1, "snh": 2}
 ACCEL = {"none": 0, "sor": 1, "chebyshev": 2}
 SCHEDULE = {"auto": 0, "colour_launches": 1, "pipelined": 2}
-RECORDS = {"auto": 0, "stored": 1, "rest": 2}
+RECORDS = {"auto": 0, "stored": 1, "rest": 2, "table": 3}
 EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbng_color", "pbng_workspace_bytes",
            "pbng_bind_workspace", "pbng_set_positions", "pbng_get_positions", "pbng_iterate", "pbng_energy_residual",
            "pbng_synchronize", "pbng_query", "pbng_profile_enable", "pbng_profile_read", "pbng_destroy",
@@ -267,8 +267,8 @@ class Context:
         _check(lib().pbng_set_schedule(self._h, SCHEDULE[schedule]))
 
     def set_records(self, records: str = "auto"):
-        """Pair-record layout built by color(): 'stored' rest data, 'rest' (recomputed from rest positions) or
-        'auto' (pbng_set_records; call before color())."""
+        """Pair-record layout built by color(): 'stored' rest data, 'rest' (recomputed from rest positions),
+        'table' (distinct rest tuples in a table) or 'auto' (pbng_set_records; call before color())."""
         _check(lib().pbng_set_records(self._h, RECORDS[records]))
 
     # ---- dynamic weak constraints ----------------------------------------------------------------

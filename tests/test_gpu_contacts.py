@@ -58,12 +58,13 @@ def test_device_detection_equals_oracle(dtype):
     ctx.close()
 
 
-@pytest.mark.parametrize("inertia_first,records", [(False, "stored"), (True, "stored"), (True, "rest")])
+@pytest.mark.parametrize("inertia_first,records", [(False, "stored"), (True, "stored"), (True, "rest"),
+                                                   (False, "table")])
 def test_two_blocks_colliding_backward_euler_matches_oracle(inertia_first, records):
     """inertia_first: the backward-Euler target is set BEFORE pbng_update_constraints, which must carry it
     (and the iterate) over -- in place when the incremental recolouring changes no colour, across the
-    re-layout otherwise; both paths occur in this run.  records = "rest": rest-recompute records
-    (pbng_set_records), which every re-layout must rebuild with the rest positions."""
+    re-layout otherwise; both paths occur in this run.  records = "rest" / "table": the lower-byte record
+    layouts (pbng_set_records), which every re-layout must rebuild."""
     import torch
 
     import oracle.oracle as O
@@ -73,7 +74,7 @@ def test_two_blocks_colliding_backward_euler_matches_oracle(inertia_first, recor
     free = _free(s)
     # --- GPU: detect -> update (incremental recolour) -> inertia -> iterate, every step
     ctx = context_from_scene(s, device=0, dtype="f64", records=records)
-    assert ctx.query()["records"] == (2 if records == "rest" else 1)
+    assert ctx.query()["records"] == {"stored": 1, "rest": 2, "table": 3}[records]
     xg_prev = torch.tensor(s.meta["x_prev"][None], dtype=torch.float64, device="cuda:0")
     xg = torch.tensor(s.x0, dtype=torch.float64, device="cuda:0")
     gpu_hist, gpu_wcs = [], []

@@ -1,10 +1,12 @@
-"""Rest-recompute records (pbng_set_records(PBNG_RECORDS_REST); SURVEY.md §8(d) lower-byte variant (i)):
-Neo-Hookean path records that carry only the new neighbour and E_e/6, the sweep rebuilding Dm', g_j, s'_j,
-det B' and V_e from the rest positions in the compute dtype.  The iterates must
-match the fp64 oracle within north_star's tolerances (fp64 1e-10 x bbox diagonal / 1e-10 relative energy;
-fp32 1e-4 / 1e-5) exactly as the stored-record layout does; the schedules and the domain decomposition
-stay bitwise equal among themselves (same per-vertex arithmetic); load-only records (a vertex whose link
-falls into several paths) add exactly nothing although their three slots need not span a tet."""
+"""Lower-byte Neo-Hookean path records (pbng_set_records; SURVEY.md §8(d) lower-byte variants):
+* "rest" (variant (i)): records carry only the new neighbour and E_e/6, the sweep rebuilding Dm', g_j, s'_j,
+  det B' and V_e from the rest positions in the compute dtype;
+* "table": the distinct {s'_j, det B'} tuples of a regular mesh in a table, each record carrying its entry
+  index, so the sweep reads exactly the stored layout's values (bitwise equal to "stored").
+The iterates must match the fp64 oracle within north_star's tolerances (fp64 1e-10 x bbox diagonal / 1e-10
+relative energy; fp32 1e-4 / 1e-5) exactly as the stored-record layout does; the schedules and the domain
+decomposition stay bitwise equal among themselves (same per-vertex arithmetic); load-only records (a vertex
+whose link falls into several paths) add exactly nothing although their three slots need not span a tet."""
 import numpy as np
 import pytest
 
@@ -46,13 +48,24 @@ def oracle_check(s, dtype, x, E, b=0):
     return err, erel
 
 
+CODE = {"rest": 2, "table": 3}
+
+
+def small(cfg):
+    # config 3 on a 16^3 grid: h = 1/16 keeps the rest positions exact in binary, so the fp64 rest tuples of
+    # congruent elements are bitwise equal and fit the table (at h = 1/14 they differ in the last bits and
+    # "table" falls back to "stored" in fp64, tests/test_abi_host.py)
+    return G.config3_hetero_cube(n=16) if cfg == 3 else G.make_config(cfg, "small")
+
+
+@pytest.mark.parametrize("records", ["rest", "table"])
 @pytest.mark.parametrize("cfg,dtype", [(1, "f64"), (1, "f32"), (3, "f32"), (3, "f64")])
-def test_rest_records_match_oracle(cfg, dtype):
-    s = G.make_config(cfg, "small")
+def test_rest_records_match_oracle(cfg, dtype, records):
+    s = small(cfg)
     if cfg == 1:
         s.iterations = 60
-    x, E, _, info = run(s, dtype, "rest")
-    assert info["records"] == 2
+    x, E, _, info = run(s, dtype, records)
+    assert info["records"] == CODE[records]
     oracle_check(s, dtype, x, E)
 
 
@@ -69,22 +82,24 @@ def test_rest_records_agree_with_stored_records_and_residual():
     np.testing.assert_allclose(Rr, Rs, rtol=1e-3)
 
 
+@pytest.mark.parametrize("records", ["rest", "table"])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-def test_rest_records_pipelined_equals_colour_launches_bitwise(dtype):
-    s = G.make_config(3, "small")
-    x1, E1, R1, _ = run(s, dtype, "rest", "colour_launches")
-    x2, E2, R2, info = run(s, dtype, "rest", "pipelined")
+def test_rest_records_pipelined_equals_colour_launches_bitwise(dtype, records):
+    s = small(3)
+    x1, E1, R1, _ = run(s, dtype, records, "colour_launches")
+    x2, E2, R2, info = run(s, dtype, records, "pipelined")
     assert np.array_equal(x1, x2), np.abs(x1 - x2).max()
     assert np.array_equal(E1, E2) and np.array_equal(R1, R2)
 
 
+@pytest.mark.parametrize("records", ["rest", "table"])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-def test_rest_records_loopback_decomposition_is_bitwise(dtype):
+def test_rest_records_loopback_decomposition_is_bitwise(dtype, records):
     from paper_2306_09021_b200 import dd
-    s = G.make_config(3, "small")
-    x1, E1, _, _ = run(s, dtype, "rest")
-    ctxs, owner = dd.loopback_contexts(s, 3, dtype=dtype, records="rest")
-    assert all(c.query()["records"] == 2 for c in ctxs)
+    s = small(3)
+    x1, E1, _, _ = run(s, dtype, records)
+    ctxs, owner = dd.loopback_contexts(s, 3, dtype=dtype, records=records)
+    assert all(c.query()["records"] == CODE[records] for c in ctxs)
     grp = dd.Group(ctxs)
     grp.iterate(s.iterations, s.accel, s.omega, s.rho, s.gamma)
     E, _ = dd.combine_energy_residual([c.energy_residual() for c in ctxs])
@@ -102,8 +117,9 @@ def test_rest_records_loopback_decomposition_is_bitwise(dtype):
     np.testing.assert_allclose(E, E1, rtol=1e-12)
 
 
+@pytest.mark.parametrize("records", ["rest", "table"])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-def test_rest_records_disconnected_link_load_only(dtype):
+def test_rest_records_disconnected_link_load_only(dtype, records):
     # vertex 0: tets (0,1,2,3) and (0,1,2,7) form one path; (0,4,5,6) meets them only at vertex 0, so a
     # second path starts with load-only records whose slots {x_7 or x_3, x_4, ...} need not span a tet
     X = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [-1, 0, 0], [0, -1, 0], [0, 0, -1],
@@ -119,7 +135,21 @@ def test_rest_records_disconnected_link_load_only(dtype):
     x0[0, pinned] = targets[0]
     s = G._finish("disconnected", X, T, "nh", 1e5, 0.3, 0.0, (0.0, 0.0, 0.0), pinned, targets, x0,
                   iterations=25, accel="none", omega=1.0, dtype=dtype, h=1.0)
-    x, E, _, info = run(s, dtype, "rest")
-    assert info["records"] == 2
+    x, E, _, info = run(s, dtype, records)
+    assert info["records"] == CODE[records]
     assert np.isfinite(x).all()
     oracle_check(s, dtype, x, E)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_full_config3_table_records_bitwise_equal_stored(dtype):
+    # full config 3 in bench.py's launch configuration: auto picks the table layout (the Kuhn grid has few
+    # distinct element shapes) and it reproduces the stored layout's iterates bit for bit
+    s = G.make_config(3, "full")
+    s.iterations = 4
+    xa, Ea, Ra, ia = run(s, dtype, "auto")
+    xs, Es, Rs, is_ = run(s, dtype, "stored")
+    assert ia["records"] == 3 and is_["records"] == 1
+    assert ia["sweep_bytes"] < 0.45 * is_["sweep_bytes"]
+    assert np.array_equal(xa, xs), np.abs(xa - xs).max()
+    assert np.array_equal(Ea, Es) and np.array_equal(Ra, Rs)
