@@ -1012,6 +1012,10 @@ constexpr int kSweepUnroll = PBNG_SWEEP_UNROLL;  // pair-loop unroll (loads of r
 #define PBNG_SWEEP_PREFETCH 4
 #endif
 constexpr int kSweepPrefetch = PBNG_SWEEP_PREFETCH;  // L2 prefetch distance of the record stream (0: off)
+#ifndef PBNG_TAB_PREFETCH
+#define PBNG_TAB_PREFETCH 2
+#endif
+constexpr int kTabPrefetch = PBNG_TAB_PREFETCH;  // table records: L2 prefetch distance in 4-record groups (2 best, 4: +1.3%)
 #ifndef PBNG_SWEEP_MINB
 #define PBNG_SWEEP_MINB 1
 #endif
@@ -1037,6 +1041,17 @@ __device__ __forceinline__ void split_partial(const Layout &L, const typename RT
 #define PBNG_SWEEP_MINB_F64 1
 #endif
 template <class R> struct SweepMinBlocks { static constexpr int n = sizeof(R) == 4 ? PBNG_SWEEP_MINB : PBNG_SWEEP_MINB_F64; };
+// table records (8 B, no rest data streamed through L1): more resident warps pay, unlike the stored layouts
+// (fp32 64 registers / 32 warps per SM measured best)
+#ifndef PBNG_SWEEP_MINB_TAB
+#define PBNG_SWEEP_MINB_TAB 8
+#endif
+#ifndef PBNG_SWEEP_MINB_TAB64
+#define PBNG_SWEEP_MINB_TAB64 1
+#endif
+template <class R, int PATH> struct SweepMinBlocksP {
+    static constexpr int n = PATH != 3 ? SweepMinBlocks<R>::n : sizeof(R) == 4 ? PBNG_SWEEP_MINB_TAB : PBNG_SWEEP_MINB_TAB64;
+};
 
 // One free vertex's PBNG update: accumulate over its records in ascending tet order,
 // weak constraints, inertia, then solve + blend + store (finish_vertex).
@@ -1104,8 +1119,8 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
         // table records: four records per step, their four neighbour gathers issued together
         const int64_t b4 = group_base(base);
         for (int k = 0; k < deg; k += 4) {
-            if (kSweepPrefetch > 0 && k + 4 * kSweepPrefetch < deg)
-                pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + b4 + (int64_t)(k + 4 * kSweepPrefetch) * kChunk);
+            if (kTabPrefetch > 0 && k + 4 * kTabPrefetch < deg)
+                pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + b4 + (int64_t)(k + 4 * kTabPrefetch) * kChunk);
             RecGroup<R> g;
             load_group(L, b4 + (int64_t)k * kChunk, g);
             R4 nw[4];
@@ -1197,7 +1212,7 @@ template <class R, int MODEL> struct StageSmem {  // per warp: [ring][kGroups mb
 // gather their neighbour positions (through L1; they belong to other colours, read-only in this
 // launch).  The per-vertex summation order is ascending tet index, as in the oracle.
 template <class R, int MODEL, int ACCEL, bool FEXT, bool WC, bool ONE_WAVE = false, int PATH = 0>
-__global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : SweepMinBlocks<R>::n)) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
+__global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : SweepMinBlocksP<R, PATH>::n)) sweep_kernel(const Layout L, const int32_t v_begin, const int32_t n_v,
                                                             const int64_t chunk_begin, const int64_t x_stride,
                                                             const int wi, const int oi, const int hi, const R cmu,
                                                             const R clam, const R omega, const R gamma, const R idt2) {
@@ -1215,7 +1230,8 @@ __global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : 
         if (kPdl) {
             for (int k = 0; k < kSweepPrefetch && k < deg; ++k) {
                 if constexpr (PATH == 3) {
-                    if (4 * k < deg) pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + group_base(base) + (int64_t)(4 * k) * kChunk);
+                    if (k < kTabPrefetch && 4 * k < deg)
+                        pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + group_base(base) + (int64_t)(4 * k) * kChunk);
                 }
                 else if constexpr (PATH == 2) pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + base + (int64_t)k * kChunk);
                 else if constexpr (PATH) prefetch_path<R>(L, base + (int64_t)k * kChunk);
