@@ -1015,6 +1015,10 @@ constexpr int kSweepPrefetch = PBNG_SWEEP_PREFETCH;  // L2 prefetch distance of 
 #ifndef PBNG_TAB_PREFETCH
 #define PBNG_TAB_PREFETCH 2
 #endif
+#ifndef PBNG_TAB_UNROLL
+#define PBNG_TAB_UNROLL 1
+#endif
+constexpr int kTabUnroll = PBNG_TAB_UNROLL;  // table records: unroll of the 4-record group loop
 constexpr int kTabPrefetch = PBNG_TAB_PREFETCH;  // table records: L2 prefetch distance in 4-record groups (2 best, 4: +1.3%)
 #ifndef PBNG_SWEEP_MINB
 #define PBNG_SWEEP_MINB 1
@@ -1118,6 +1122,7 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
     if constexpr (MODE == 3) {
         // table records: four records per step, their four neighbour gathers issued together
         const int64_t b4 = group_base(base);
+#pragma unroll kTabUnroll
         for (int k = 0; k < deg; k += 4) {
             if (kTabPrefetch > 0 && k + 4 * kTabPrefetch < deg)
                 pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + b4 + (int64_t)(k + 4 * kTabPrefetch) * kChunk);
