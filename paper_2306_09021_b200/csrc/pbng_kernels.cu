@@ -1109,7 +1109,10 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
     }
     R A[6] = {R(0), R(0), R(0), R(0), R(0), R(0)};
     const int2 p0 = ld(L.path0 + v);
-    R4 S0 = xa4, S1 = gather<G>(work + p0.x), S2 = gather<G>(work + p0.y);
+    // difference slots: S_k holds d = x_k - x_i, computed once when the neighbour is pushed (the same
+    // subtraction the contribution would repeat for every record that keeps the neighbour: bitwise equal)
+    auto dif = [&](const R4 &q) { return mk4<R>(q.x - xa[0], q.y - xa[1], q.z - xa[2]); };
+    R4 S0 = mk4<R>(R(0), R(0), R(0)), S1 = dif(gather<G>(work + p0.x)), S2 = dif(gather<G>(work + p0.y));
     constexpr bool REST = MODE == 2;
     R4 T0, T1, T2;  // REST: the slots' rest positions
     R Xi[3];
@@ -1132,16 +1135,15 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
 #pragma unroll
             for (int q = 0; q < 4; ++q) nw[q] = gather<G>(work + (g.code[q] & 0x3fffff));
 #pragma unroll
+            for (int q = 0; q < 4; ++q) nw[q] = dif(nw[q]);
+#pragma unroll
             for (int q = 0; q < 4; ++q) {
                 if (k + q < deg) {
                     Pair<R, MODEL_NH> pr;
                     const int code = table_pair<R>(L, g.code[q], g.VE[q], pr);
                     PBNG_CHECK((code & 0x3fffffff) < L.n_vertices);
                     path_push(S0, S1, S2, nw[q], code);
-                    R d1[3], d2[3], d3[3];
-                    sub3<R>(S0, xa, d1);
-                    sub3<R>(S1, xa, d2);
-                    sub3<R>(S2, xa, d3);
+                    const R d1[3] = {S0.x, S0.y, S0.z}, d2[3] = {S1.x, S1.y, S1.z}, d3[3] = {S2.x, S2.y, S2.z};
                     contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
                 }
             }
@@ -1157,7 +1159,7 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
             R E6;
             code = load_rest_rec<true>(L, base + (int64_t)k * kChunk, E6);
             const int j = code & 0x3fffffff;
-            const R4 nw = gather<G>(work + j), nr = rest_at<R>(L, j);
+            const R4 nw = dif(gather<G>(work + j)), nr = rest_at<R>(L, j);
             path_push(S0, S1, S2, nw, code);
             path_push(T0, T1, T2, nr, code);
             rest_pair<R>(T0, T1, T2, Xi, E6, pr);
@@ -1167,13 +1169,10 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
                 else prefetch_path<R>(L, base + (int64_t)(k + kSweepPrefetch) * kChunk);
             }
             code = load_path_rec<true, MODE == 3>(L, base + (int64_t)k * kChunk, pr);
-            const R4 nw = gather<G>(work + (code & 0x3fffffff));
+            const R4 nw = dif(gather<G>(work + (code & 0x3fffffff)));
             path_push(S0, S1, S2, nw, code);
         }
-        R d1[3], d2[3], d3[3];
-        sub3<R>(S0, xa, d1);
-        sub3<R>(S1, xa, d2);
-        sub3<R>(S2, xa, d3);
+        const R d1[3] = {S0.x, S0.y, S0.z}, d2[3] = {S1.x, S1.y, S1.z}, d3[3] = {S2.x, S2.y, S2.z};
         contrib<true>(d1, d2, d3, pr, cmu, clam, f, A);
     }
     }
