@@ -1643,16 +1643,16 @@ __device__ __forceinline__ void contrib_nh2(const float2 (&d1)[3], const float2 
 }
 
 #ifndef PBNG_B2_MINB
-#define PBNG_B2_MINB 5  // path records + difference slots: 96 registers / 20 warps per SM measured best (1.153 ms per config-4 iteration; 1: 1.179, 4: 1.208)
+#define PBNG_B2_MINB 5  // 96 registers / 20 warps per SM measured best (config 4: 0.970 ms per iteration; 4: 1.158, 6: 1.068 with unroll 6)
 #endif
 #ifndef PBNG_B2_UNROLL
-#define PBNG_B2_UNROLL 2
+#define PBNG_B2_UNROLL 12
 #endif
 constexpr int kB2Unroll = PBNG_B2_UNROLL;
 #ifndef PBNG_B2_PF
-#define PBNG_B2_PF 4
+#define PBNG_B2_PF 0
 #endif
-constexpr int kB2Prefetch = PBNG_B2_PF;  // records ahead whose neighbour slot is prefetched into L1 (0: off)
+constexpr int kB2Prefetch = PBNG_B2_PF;  // records ahead whose neighbour slot is prefetched into L1 (0: off; 4: 7% slower)
 __device__ __forceinline__ void pf_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 // the packed positions of a lane's two samples at one vertex (sh 6 slot {x0 x1 y0 y1 | z0 z1 . .})
 struct P6 {
