@@ -755,7 +755,10 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
     c->h_rec_id2.assign(c->path_rec ? (size_t)ns : 1, make_int2(0, 0));
     c->h_rec_a.assign(c->rest_rec ? s4 : (size_t)ns * s4, 0);  // rest-recompute records: unused
     const bool nh = c->model == MODEL_NH;
-    c->h_rec_b.assign(nh ? s4 : (size_t)ns * s4, 0);  // NH: unused
+    // NH: unused, except the batched sh-6 path records' precomputed material scalars {V mu, V lambda,
+    // V (mu + lambda), 2 V mu |g_i|^2} (pbng_kernels.cu contrib_nh2v)
+    const bool b2v = nh && c->path_rec && layout_lane_shift(c) == 6;
+    c->h_rec_b.assign(nh && !b2v ? s4 : (size_t)ns * s4, 0);
     // rec_c: FCR g3z (+ VE in fp64); NH: VE in fp64, unused in fp32 (VE rides in rec_id.w)
     // rest-recompute records: rec_c holds E_e/6 in fp64 (fp32: in rec_id.y)
     const size_t rec_c_bytes = nh ? (c->dtype == DT_F64 ? s : 0) : (c->dtype == DT_F64 ? 2 * s : s);
@@ -833,6 +836,10 @@ void build_layout(pbng_ctx *c, const std::vector<int64_t> &vt_off, const std::ve
                     }
                     c->h_rec_id2[r] = id;
                     put4<R>(c->h_rec_a, r, sj[pi[0]], sj[pi[1]], sj[pi[2]], sgn * det3(Bp));
+                    if (b2v) {
+                        const double Vmu = VE * cmu, Vlam = VE * clam;
+                        put4<R>(c->h_rec_b, r, Vmu, Vlam, Vmu + Vlam, -2.0 * Vmu * (sj[0] + sj[1] + sj[2]));
+                    }
                     if (c->dtype == DT_F64) put1<R>(c->h_rec_c, r, VE);
                 }
                 continue;

@@ -1642,6 +1642,34 @@ __device__ __forceinline__ void contrib_nh2(const float2 (&d1)[3], const float2 
     A[5] = fma2(t0, w[2], A[5]);
 }
 
+// contrib_nh2 with the record's material scalars precomputed on the host (batched sh-6 records, rec_b:
+// {V mu, V lambda, V (mu + lambda), 2 V mu |g_i|^2} in fp64, rounded): the same terms without the ~10 scalar
+// instructions per record that derive them from VE
+__device__ __forceinline__ void contrib_nh2v(const float2 (&d1)[3], const float2 (&d2)[3], const float2 (&d3)[3],
+                                             const float4 sd, const float4 vv, float2 (&f)[3], float2 (&A)[6]) {
+    const float2 e1[3] = {sub2(d2[0], d1[0]), sub2(d2[1], d1[1]), sub2(d2[2], d1[2])};
+    const float2 e2[3] = {sub2(d3[0], d1[0]), sub2(d3[1], d1[1]), sub2(d3[2], d1[2])};
+    const float2 n[3] = {fma2(e1[1], e2[2], ng(mul2(e1[2], e2[1]))), fma2(e1[2], e2[0], ng(mul2(e1[0], e2[2]))),
+                         fma2(e1[0], e2[1], ng(mul2(e1[1], e2[0])))};
+    const float2 J = mul2(fma2(d1[0], n[0], fma2(d1[1], n[1], mul2(d1[2], n[2]))), bc(sd.w));
+    const float Vmu = vv.x, Vlam = vv.y, lh = vv.z;
+    const float2 sc = fma2(bc(lh), J, bc(-lh - Vmu));  // lamhat (J - 1) - mu, times V
+    float2 w[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        w[r] = mul2(bc(-sd.w), n[r]);
+        const float2 Fg = fma2(bc(sd.z), d3[r], fma2(bc(sd.y), d2[r], mul2(bc(sd.x), d1[r])));
+        f[r] = fma2(ng(sc), w[r], fma2(bc(-Vmu), Fg, f[r]));
+    }
+    const float2 t0 = mul2(bc(Vlam), w[0]), t1 = mul2(bc(Vlam), w[1]), t2 = mul2(bc(Vlam), w[2]);
+    A[0] = fma2(t0, w[0], add2(A[0], bc(vv.w)));
+    A[1] = fma2(t1, w[1], add2(A[1], bc(vv.w)));
+    A[2] = fma2(t2, w[2], add2(A[2], bc(vv.w)));
+    A[3] = fma2(t0, w[1], A[3]);
+    A[4] = fma2(t1, w[2], A[4]);
+    A[5] = fma2(t0, w[2], A[5]);
+}
+
 #ifndef PBNG_B2_MINB
 #define PBNG_B2_MINB 5  // 96 registers / 20 warps per SM measured best (config 4: 0.970 ms per iteration; 4: 1.158, 6: 1.068 with unroll 6)
 #endif
@@ -1692,7 +1720,7 @@ __device__ __forceinline__ void b2_vertex(const Layout &L, const int t, const in
                                           const int64_t gp, const int64_t x_stride, const int32_t n_batch, const int wi,
                                           const int oi, const int hi, const float cmu, const float clam,
                                           const float omega, const float gamma, const float idt2, int2 (&s_id)[32],
-                                          float4 (&s_sd)[32]) {
+                                          float4 (&s_sd)[32], float4 (&s_vv)[32]) {
     const int lane = threadIdx.x & 31;
     const int v = v_begin + t;
     const int64_t base = ld(L.chunk_off + chunk_begin + (t >> 5)) + (t & 31);
@@ -1725,6 +1753,7 @@ __device__ __forceinline__ void b2_vertex(const Layout &L, const int t, const in
             const int64_t r = base + (int64_t)(k0 + lane) * kChunk;
             s_id[lane] = ld(reinterpret_cast<const int2 *>(L.rec_id) + r);
             s_sd[lane] = ld(reinterpret_cast<const float4 *>(L.rec_a) + r);
+            s_vv[lane] = ld(reinterpret_cast<const float4 *>(L.rec_b) + r);
             PBNG_CHECK(r < L.n_slots && (s_id[lane].x & 0x3fffffff) < L.n_vertices);
         }
         __syncwarp();
@@ -1734,16 +1763,12 @@ __device__ __forceinline__ void b2_vertex(const Layout &L, const int t, const in
             if (kB2Prefetch > 0 && j + kB2Prefetch < n)  // the gather of record j + PF: L2 -> L1 now
                 pf_l1(wk + ((int64_t)(s_id[j + kB2Prefetch].x & 0x3fffffff) << 8));
             const int2 id = s_id[j];
-            const float4 sd = s_sd[j];
-            Pair<float, MODEL_NH> pr;
-            pr.s[0] = sd.x; pr.s[1] = sd.y; pr.s[2] = sd.z; pr.detB = sd.w;
-            pr.VE = __int_as_float(id.y);
             const P6 nw = diff(ld_p6<COH>(wk + ((int64_t)(id.x & 0x3fffffff) << 8)));
             path_push(S0, S1, S2, nw, id.x);
             const float2 d1[3] = {S0.x, S0.y, S0.z};
             const float2 d2[3] = {S1.x, S1.y, S1.z};
             const float2 d3[3] = {S2.x, S2.y, S2.z};
-            contrib_nh2(d1, d2, d3, pr, cmu, clam, f, A);
+            contrib_nh2v(d1, d2, d3, s_sd[j], s_vv[j], f, A);
         }
         __syncwarp();
     }
@@ -1810,12 +1835,13 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_kern
     constexpr int WPB = kSweepBlock / 32;
     __shared__ int2 s_id[WPB][32];
     __shared__ float4 s_sd[WPB][32];
+    __shared__ float4 s_vv[WPB][32];
     const int wq = threadIdx.x >> 5;
     const int t = blockIdx.x * WPB + wq;  // vertex index within the colour
     if (t >= n_v) return;                  // warp-uniform (only warp-level synchronisation below)
     const int64_t gp = reverse ? gridDim.y - 1 - blockIdx.y : blockIdx.y;
     b2_vertex<ACCEL, FEXT, WC, false>(L, t, v_begin, chunk_begin, gp, x_stride, n_batch, wi, oi, hi, cmu, clam, omega,
-                                      gamma, idt2, s_id[wq], s_sd[wq]);
+                                      gamma, idt2, s_id[wq], s_sd[wq], s_vv[wq]);
 }
 
 // Windowed persistent schedule for the batched fp32 Neo-Hookean layout (sh 6).  The sample-group pairs are
@@ -1832,6 +1858,7 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_wind
     constexpr int WPB = kSweepBlock / 32;
     __shared__ int2 s_id[WPB][32];
     __shared__ float4 s_sd[WPB][32];
+    __shared__ float4 s_vv[WPB][32];
     __shared__ int64_t item_sh;
     const int wq = threadIdx.x >> 5;
     const int64_t n_gp = (n_batch + 63) / 64;
@@ -1871,7 +1898,8 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_wind
         const int t = blk * WPB + wq;
         if (t < P.n_v[c])
             b2_vertex<ACCEL, FEXT, WC, true>(L, t, P.v_begin[c], P.chunk_begin[c], gp, x_stride, n_batch, wi, oi, P.hist,
-                                             cmu, clam, float(P.omega[it]), float(P.gamma), idt2, s_id[wq], s_sd[wq]);
+                                             cmu, clam, float(P.omega[it]), float(P.gamma), idt2, s_id[wq], s_sd[wq],
+                                             s_vv[wq]);
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
