@@ -1024,12 +1024,23 @@ constexpr int kTabPrefetch = PBNG_TAB_PREFETCH;  // table records: L2 prefetch d
 #define PBNG_SWEEP_MINB 1
 #endif
 
+#ifndef PBNG_SPLIT_PREFETCH
+#define PBNG_SPLIT_PREFETCH 0
+#endif
+#ifndef PBNG_SPLIT_UNROLL
+#define PBNG_SPLIT_UNROLL 1
+#endif
+constexpr int kSplitPrefetch = PBNG_SPLIT_PREFETCH;  // split warps: L2 prefetch distance in own records (0: off)
+constexpr int kSplitUnroll = PBNG_SPLIT_UNROLL;
 // partial sums of warp `sub` of a SPLIT-warp group over records k = sub, sub + SPLIT, ... (ascending)
 template <class R, int MODEL, int G, int SPLIT>
 __device__ __forceinline__ void split_partial(const Layout &L, const typename RT<R>::R4 *work, const R (&xa)[3],
                                               const int64_t base, const int deg, const int sub, const R cmu,
                                               const R clam, R (&f)[3], R (&A)[6]) {
+#pragma unroll kSplitUnroll
     for (int k = sub; k < deg; k += SPLIT) {
+        if (kSplitPrefetch > 0 && k + SPLIT * kSplitPrefetch < deg)
+            prefetch_pair<R, MODEL>(L, base + (int64_t)(k + SPLIT * kSplitPrefetch) * kChunk);
         Pair<R, MODEL> pr;
         load_pair<true>(L, base + (int64_t)k * kChunk, pr);
         R d1[3], d2[3], d3[3];
