@@ -1025,12 +1025,12 @@ constexpr int kTabPrefetch = PBNG_TAB_PREFETCH;  // table records: L2 prefetch d
 #endif
 
 #ifndef PBNG_SPLIT_PREFETCH
-#define PBNG_SPLIT_PREFETCH 0
+#define PBNG_SPLIT_PREFETCH 2
 #endif
 #ifndef PBNG_SPLIT_UNROLL
 #define PBNG_SPLIT_UNROLL 1
 #endif
-constexpr int kSplitPrefetch = PBNG_SPLIT_PREFETCH;  // split warps: L2 prefetch distance in own records (0: off)
+constexpr int kSplitPrefetch = PBNG_SPLIT_PREFETCH;  // split warps: L2 prefetch distance in own records (2: config 5 -1.5%, config 2 -3%)
 constexpr int kSplitUnroll = PBNG_SPLIT_UNROLL;
 // partial sums of warp `sub` of a SPLIT-warp group over records k = sub, sub + SPLIT, ... (ascending)
 template <class R, int MODEL, int G, int SPLIT>

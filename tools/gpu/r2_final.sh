@@ -12,7 +12,7 @@ python bench.py --config 3 --dtype f64 --no-cpu-baseline > gpurun_out/fb_c3f64.j
 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/fb_ref_c3.json 2> gpurun_out/fb_ref_c3.err
 bash tools/ncu_sweep.sh r2fc3 3
 else
-bash tools/ncu_sweep.sh r2fc3d 3 --dtype f64
-bash tools/ncu_sweep.sh r2fc4 4
+NCU_DROP_REP=1 bash tools/ncu_sweep.sh r2fc3d 3 --dtype f64
+NCU_DROP_REP=1 bash tools/ncu_sweep.sh r2fc4 4
 fi
 echo done

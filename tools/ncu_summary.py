@@ -36,7 +36,13 @@ METRICS = [
 
 
 def ncu_raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # the raw page exported on the GPU box (<tag>_raw.csv, tools/ncu_sweep.sh) when the report itself was
+    # dropped to keep gpurun_out/ small; otherwise read the report
+    raw = rep.replace("_sweep.ncu-rep", "_raw.csv")
+    if os.path.exists(raw):
+        out = open(raw).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     res = []
