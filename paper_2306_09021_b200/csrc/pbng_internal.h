@@ -20,7 +20,10 @@ constexpr int kChunk = 32;        // vertices per SELL chunk == one warp
 #endif
 constexpr int kSweepBlock = PBNG_SWEEP_BLOCK;  // threads per sweep CTA (a multiple of the 32-vertex chunk)
 constexpr int kWcMaxNodes = 8;    // distinct nodes per weak constraint
-constexpr int kRecGroup = 4;      // table path records: consecutive slots per lane (pbng_host.cpp group_table_records)
+#ifndef PBNG_REC_GROUP
+#define PBNG_REC_GROUP 4
+#endif
+constexpr int kRecGroup = PBNG_REC_GROUP;  // table path records: consecutive slots per lane (4 or 8; group_table_records)
 constexpr int kRedBlock = 256;    // threads per reduction CTA
 
 // Pair-record layout (SELL-32, one record per (free vertex i, incident tet e), vertex-major within a

@@ -647,30 +647,39 @@ __device__ __forceinline__ int load_path_rec(const Layout &L, int64_t r, Pair<do
     PBNG_CHECK(r >= 0 && r < L.n_slots && (code & 0x3fffffff) < L.n_vertices);
     return code;
 }
-// table records in groups of kRecGroup = 4 slots per lane (pbng_host.cpp group_table_records): the first slot
-// of lane `lane`'s group g is chunk_off + g * 128 + 4 * lane = base + 3 * lane + g * 128 with base = chunk_off
-// + lane (chunk_off is a multiple of 128).  One group = two 16-byte loads of {code, VE bits} pairs (fp32;
-// fp64 VE: two more 16-byte loads from rec_c).
-__device__ __forceinline__ int64_t group_base(int64_t base) { return base + 3 * (base & 31); }
+// table records in groups of kRecGroup (RG = 4) slots per lane (pbng_host.cpp group_table_records): the first
+// slot of lane `lane`'s group g is chunk_off + g * 32 RG + RG lane = base + (RG - 1) lane + g * 32 RG with
+// base = chunk_off + lane (chunk_off is a multiple of 32 RG).  One group = RG/2 16-byte loads of
+// {code, VE bits} pairs (fp32; fp64 VE: RG/4 more 32-byte loads from rec_c).
+constexpr int RG = kRecGroup;
+__device__ __forceinline__ int64_t group_base(int64_t base) { return base + (RG - 1) * (base & 31); }
 template <class R> struct RecGroup {
-    int code[4];
-    R VE[4];
+    int code[RG];
+    R VE[RG];
 };
 __device__ __forceinline__ void load_group(const Layout &L, int64_t r, RecGroup<float> &g) {
     const int4 *p = reinterpret_cast<const int4 *>(reinterpret_cast<const int2 *>(L.rec_id) + r);
-    const int4 a = lds(p), b = lds(p + 1);
-    g.code[0] = a.x; g.code[1] = a.z; g.code[2] = b.x; g.code[3] = b.z;
-    g.VE[0] = __int_as_float(a.y); g.VE[1] = __int_as_float(a.w);
-    g.VE[2] = __int_as_float(b.y); g.VE[3] = __int_as_float(b.w);
-    PBNG_CHECK(r >= 0 && r + 3 < L.n_slots && (r & 3) == 0);
+#pragma unroll
+    for (int h = 0; h < RG / 2; ++h) {
+        const int4 a = lds(p + h);
+        g.code[2 * h] = a.x; g.code[2 * h + 1] = a.z;
+        g.VE[2 * h] = __int_as_float(a.y); g.VE[2 * h + 1] = __int_as_float(a.w);
+    }
+    PBNG_CHECK(r >= 0 && r + RG - 1 < L.n_slots && (r % RG) == 0);
 }
 __device__ __forceinline__ void load_group(const Layout &L, int64_t r, RecGroup<double> &g) {
     const int4 *p = reinterpret_cast<const int4 *>(reinterpret_cast<const int2 *>(L.rec_id) + r);
-    const int4 a = lds(p), b = lds(p + 1);
-    g.code[0] = a.x; g.code[1] = a.z; g.code[2] = b.x; g.code[3] = b.z;
-    const double4 v = lds(reinterpret_cast<const double4 *>(L.rec_c) + (r >> 2));
-    g.VE[0] = v.x; g.VE[1] = v.y; g.VE[2] = v.z; g.VE[3] = v.w;
-    PBNG_CHECK(r >= 0 && r + 3 < L.n_slots && (r & 3) == 0);
+#pragma unroll
+    for (int h = 0; h < RG / 2; ++h) {
+        const int4 a = lds(p + h);
+        g.code[2 * h] = a.x; g.code[2 * h + 1] = a.z;
+    }
+#pragma unroll
+    for (int h = 0; h < RG / 4; ++h) {
+        const double4 v = lds(reinterpret_cast<const double4 *>(L.rec_c) + (r >> 2) + h);
+        g.VE[4 * h] = v.x; g.VE[4 * h + 1] = v.y; g.VE[4 * h + 2] = v.z; g.VE[4 * h + 3] = v.w;
+    }
+    PBNG_CHECK(r >= 0 && r + RG - 1 < L.n_slots && (r % RG) == 0);
 }
 // the table entry {s'_0..2, det B'} of a table-record code; returns the code without the entry bits
 template <class R>
@@ -1134,21 +1143,21 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
         Xi[0] = T0.x; Xi[1] = T0.y; Xi[2] = T0.z;
     }
     if constexpr (MODE == 3) {
-        // table records: four records per step, their four neighbour gathers issued together
+        // table records: RG records per step, their RG neighbour gathers issued together
         const int64_t b4 = group_base(base);
 #pragma unroll kTabUnroll
-        for (int k = 0; k < deg; k += 4) {
-            if (kTabPrefetch > 0 && k + 4 * kTabPrefetch < deg)
-                pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + b4 + (int64_t)(k + 4 * kTabPrefetch) * kChunk);
+        for (int k = 0; k < deg; k += RG) {
+            if (kTabPrefetch > 0 && k + RG * kTabPrefetch < deg)
+                pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + b4 + (int64_t)(k + RG * kTabPrefetch) * kChunk);
             RecGroup<R> g;
             load_group(L, b4 + (int64_t)k * kChunk, g);
-            R4 nw[4];
+            R4 nw[RG];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) nw[q] = gather<G>(work + (g.code[q] & 0x3fffff));
+            for (int q = 0; q < RG; ++q) nw[q] = gather<G>(work + (g.code[q] & 0x3fffff));
 #pragma unroll
-            for (int q = 0; q < 4; ++q) nw[q] = dif(nw[q]);
+            for (int q = 0; q < RG; ++q) nw[q] = dif(nw[q]);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < RG; ++q) {
                 if (k + q < deg) {
                     Pair<R, MODEL_NH> pr;
                     const int code = table_pair<R>(L, g.code[q], g.VE[q], pr);
@@ -1245,8 +1254,8 @@ __global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : 
         if (kPdl) {
             for (int k = 0; k < kSweepPrefetch && k < deg; ++k) {
                 if constexpr (PATH == 3) {
-                    if (k < kTabPrefetch && 4 * k < deg)
-                        pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + group_base(base) + (int64_t)(4 * k) * kChunk);
+                    if (k < kTabPrefetch && RG * k < deg)
+                        pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + group_base(base) + (int64_t)(RG * k) * kChunk);
                 }
                 else if constexpr (PATH == 2) pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + base + (int64_t)k * kChunk);
                 else if constexpr (PATH) prefetch_path<R>(L, base + (int64_t)k * kChunk);
@@ -2539,7 +2548,7 @@ __global__ void __launch_bounds__(kRedBlock) residual_kernel(const Layout L, con
                         path_push(T0, T1, T2, rest_at<R>(L, code & 0x3fffffff), code);
                         rest_pair<R>(T0, T1, T2, Xi, E6, pr);
                     } else if (L.path_mode == 3) {
-                        const int64_t r = group_base(base) + (int64_t)(k & ~3) * kChunk + (k & 3);
+                        const int64_t r = group_base(base) + (int64_t)(k - k % RG) * kChunk + k % RG;
                         code = load_path_rec<true, true>(L, r, pr);
                     } else {
                         code = load_path_rec<true>(L, base + (int64_t)k * kChunk, pr);
