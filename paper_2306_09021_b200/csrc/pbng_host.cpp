@@ -2277,6 +2277,7 @@ static pbng_status bind_layout(pbng_ctx *c, void *dptr, uint64_t bytes, bool fre
     L.rec_c = at(c->r_rec_c);
     L.rest = c->rest_rec ? at(c->r_rest) : nullptr;
     L.path_mode = c->prob.path_mode;
+    L.n_tab = c->prob.path_mode == 3 ? (int32_t)c->n_tab : 0;
     L.chunk_off = static_cast<const int64_t *>(at(c->r_chunk_off));
     L.chunk_v = static_cast<const int2 *>(at(c->r_chunk_v));
     L.deg = static_cast<const int32_t *>(at(c->r_deg));
@@ -2487,7 +2488,7 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
             for (int j = 0; j < W.n_iter; ++j)
                 W.omega[j] = accel == PBNG_ACCEL_SOR ? omega
                              : accel == PBNG_ACCEL_CHEBYSHEV ? chebyshev_weight(c->l + j + 1, rho) : 1.0;
-            constexpr int WPB = kSweepBlock / 32;
+            constexpr int WPB = kSweepBlock / 32 * kB2WinVpw;  // vertices per item
             W.blk_off[0] = 0;
             for (int32_t col = 0; col < c->ncol; ++col) {
                 W.v_begin[col] = c->col_vbegin[col];

@@ -54,6 +54,7 @@ struct Layout {
     const int2 *path0 = nullptr;         // [n_free] path mode: slots S1, S2 before the vertex's first record
     const void *rest = nullptr;          // Real4 [n_vertices] rest positions (rest-recompute records) or null
     int path_mode = 0;                   // NH path records: 0 none, 1 stored, 2 rest recompute, 3 table
+    int32_t n_tab = 0;                   // table records: distinct rest tuples in rec_a
     const void *fext = nullptr;          // Real4 [n_free] or null (no body force)
     // weak constraints: per free vertex CSR of (constraint id, w0_i - w1_i) in input order
     const int32_t *wc_off = nullptr;     // [n_free + 1]
@@ -147,6 +148,11 @@ struct PipeLaunch {
 // whole iterations over windows of `window` sample-group pairs; per colour c its vertex range, first chunk
 // and block offsets (blocks of kSweepBlock / 32 vertices; blk_off[ncol] = blocks per group pair)
 constexpr int kB2MaxColours = 32;
+// windowed batched schedule: vertices per warp in one item (an item = kSweepBlock / 32 * kB2WinVpw vertices)
+#ifndef PBNG_B2_WIN_VPW
+#define PBNG_B2_WIN_VPW 1
+#endif
+constexpr int kB2WinVpw = PBNG_B2_WIN_VPW;
 struct B2Window {
     int n_iter = 0, ncol = 0, window = 4;
     int work = 0, out = 1, hist = 2;

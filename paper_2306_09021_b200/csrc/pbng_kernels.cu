@@ -607,6 +607,7 @@ __device__ __forceinline__ void load_pair(const Layout &L, int64_t r, Pair<doubl
 
 // L2 prefetch of a later record of the stream (no registers held while it is in flight)
 __device__ __forceinline__ void pf_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void pf_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 // ------------------------------------------------------------------------------------------------
 // Path records (Problem::path, Neo-Hookean; host: vertex_path_records).  A vertex's records follow paths
 // in the dual graph of its link, so consecutive records share two of their three neighbours.  The kernels
@@ -685,6 +686,14 @@ __device__ __forceinline__ void load_group(const Layout &L, int64_t r, RecGroup<
 template <class R>
 __device__ __forceinline__ int table_pair(const Layout &L, const int code, const R VE, Pair<R, MODEL_NH> &p) {
     const typename RT<R>::R4 x = ld(reinterpret_cast<const typename RT<R>::R4 *>(L.rec_a) + (((unsigned)code >> 22) & 0xffu));
+    p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
+    p.VE = VE;
+    return (int)((unsigned)code & ~(0xffu << 22));
+}
+template <class R>
+__device__ __forceinline__ int table_pair_smem(const typename RT<R>::R4 *stab, const int code, const R VE,
+                                               Pair<R, MODEL_NH> &p) {
+    const typename RT<R>::R4 x = stab[((unsigned)code >> 22) & 0xffu];
     p.s[0] = x.x; p.s[1] = x.y; p.s[2] = x.z; p.detB = x.w;
     p.VE = VE;
     return (int)((unsigned)code & ~(0xffu << 22));
@@ -1029,6 +1038,31 @@ constexpr int kSweepPrefetch = PBNG_SWEEP_PREFETCH;  // L2 prefetch distance of 
 #endif
 constexpr int kTabUnroll = PBNG_TAB_UNROLL;  // table records: unroll of the 4-record group loop
 constexpr int kTabPrefetch = PBNG_TAB_PREFETCH;  // table records: L2 prefetch distance in 4-record groups (2 best, 4: +1.3%)
+// table records: the group tail (slots k + q >= deg) is processed without a branch.  Those slots are padding
+// {code 0, VE 0} (pbng_host.cpp group_table_records / SELL padding): V E = 0 makes Vmu = Vlam = 0, so the
+// slot adds exactly zero to f and A (finite table entry, finite positions), and the pushes it makes into
+// the position slots happen after the vertex's last record.
+#ifndef PBNG_TAB_NOBRANCH
+#define PBNG_TAB_NOBRANCH 0
+#endif
+constexpr bool kTabNoBranch = PBNG_TAB_NOBRANCH;
+// table records: the colour-launch sweep copies the n_tab table entries into shared memory once per CTA
+// (before waiting on the previous colour) and reads them with LDS instead of L1-cached LDG
+#ifndef PBNG_TAB_SMEM
+#define PBNG_TAB_SMEM 0
+#endif
+constexpr bool kTabSmem = PBNG_TAB_SMEM;
+// table records: L1 prefetch of the lane's next record group (its 32-B sector) one group ahead, so the
+// group load hits L1 instead of waiting on L2 (PBNG_TAB_L1PF); register double-buffering of the next
+// group's record load instead (PBNG_TAB_PIPE)
+#ifndef PBNG_TAB_L1PF
+#define PBNG_TAB_L1PF 0
+#endif
+constexpr bool kTabL1Pf = PBNG_TAB_L1PF;
+#ifndef PBNG_TAB_PIPE
+#define PBNG_TAB_PIPE 0
+#endif
+constexpr bool kTabPipe = PBNG_TAB_PIPE;
 #ifndef PBNG_SWEEP_MINB
 #define PBNG_SWEEP_MINB 1
 #endif
@@ -1114,11 +1148,12 @@ __device__ __forceinline__ void update_vertex(const Layout &L, typename RT<R>::R
 // update_vertex for path records (Neo-Hookean, Problem::path): one neighbour gather per record
 // (MODE 1: stored records; 2: rest-recompute records, one more gather of the neighbour's rest position per
 // record; 3: table records, the rest data read from the small table of distinct tuples)
-template <class R, int ACCEL, bool FEXT, bool WC, int G, int MODE = 1>
+template <class R, int ACCEL, bool FEXT, bool WC, int G, int MODE = 1, bool TS = false>
 __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<R>::R4 *__restrict__ work,
                                                    const int64_t xs, const int v, const int64_t base, const int deg,
                                                    const int oi, const int hi, const R cmu, const R clam,
-                                                   const R omega, const R gamma, const R idt2) {
+                                                   const R omega, const R gamma, const R idt2,
+                                                   const typename RT<R>::R4 *stab = nullptr) {
     using R4 = typename RT<R>::R4;
     const R4 xa4 = work[v];
     const R xa[3] = {xa4.x, xa4.y, xa4.z};
@@ -1145,12 +1180,20 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
     if constexpr (MODE == 3) {
         // table records: RG records per step, their RG neighbour gathers issued together
         const int64_t b4 = group_base(base);
+        RecGroup<R> gn;
+        if (kTabPipe && deg > 0) load_group(L, b4, gn);
 #pragma unroll kTabUnroll
         for (int k = 0; k < deg; k += RG) {
             if (kTabPrefetch > 0 && k + RG * kTabPrefetch < deg)
                 pf_l2(reinterpret_cast<const int2 *>(L.rec_id) + b4 + (int64_t)(k + RG * kTabPrefetch) * kChunk);
+            if (kTabL1Pf && k + RG < deg) pf_l1(reinterpret_cast<const int2 *>(L.rec_id) + b4 + (int64_t)(k + RG) * kChunk);
             RecGroup<R> g;
-            load_group(L, b4 + (int64_t)k * kChunk, g);
+            if (kTabPipe) {
+                g = gn;
+                if (k + RG < deg) load_group(L, b4 + (int64_t)(k + RG) * kChunk, gn);
+            } else {
+                load_group(L, b4 + (int64_t)k * kChunk, g);
+            }
             R4 nw[RG];
 #pragma unroll
             for (int q = 0; q < RG; ++q) nw[q] = gather<G>(work + (g.code[q] & 0x3fffff));
@@ -1158,9 +1201,10 @@ __device__ __forceinline__ void update_vertex_path(const Layout &L, typename RT<
             for (int q = 0; q < RG; ++q) nw[q] = dif(nw[q]);
 #pragma unroll
             for (int q = 0; q < RG; ++q) {
-                if (k + q < deg) {
+                if (kTabNoBranch || k + q < deg) {
                     Pair<R, MODEL_NH> pr;
-                    const int code = table_pair<R>(L, g.code[q], g.VE[q], pr);
+                    const int code = TS ? table_pair_smem<R>(stab, g.code[q], g.VE[q], pr)
+                                        : table_pair<R>(L, g.code[q], g.VE[q], pr);
                     PBNG_CHECK((code & 0x3fffffff) < L.n_vertices);
                     path_push(S0, S1, S2, nw[q], code);
                     const R d1[3] = {S0.x, S0.y, S0.z}, d2[3] = {S1.x, S1.y, S1.z}, d3[3] = {S2.x, S2.y, S2.z};
@@ -1246,6 +1290,12 @@ __global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : 
         // waiting for the previous colour they touch only static data (offsets, degree) and prefetch their
         // first records into L2 (the record stream does not depend on any position)
         if (kPdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        extern __shared__ __align__(128) unsigned char tsm[];
+        R4 *stab = reinterpret_cast<R4 *>(tsm);
+        if constexpr (PATH == 3 && kTabSmem) {  // static table: copied before the wait on the previous colour
+            for (int q = threadIdx.x; q < L.n_tab; q += kSweepBlock) stab[q] = ld(reinterpret_cast<const R4 *>(L.rec_a) + q);
+            __syncthreads();
+        }
         const int t = blockIdx.x * kSweepBlock + threadIdx.x;
         if (t >= n_v) return;
         const int v = v_begin + t;
@@ -1266,8 +1316,8 @@ __global__ void __launch_bounds__(kSweepBlock, (ONE_WAVE ? 1024 / kSweepBlock : 
         const int64_t xs = (int64_t)blockIdx.y * x_stride;
         R4 *__restrict__ work = reinterpret_cast<R4 *>(L.xbuf[wi]) + xs;
         if constexpr (PATH && MODEL == MODEL_NH)
-            update_vertex_path<R, ACCEL, FEXT, WC, GATHER_NC, PATH>(L, work, xs, v, base, deg, oi, hi, cmu, clam,
-                                                                         omega, gamma, idt2);
+            update_vertex_path<R, ACCEL, FEXT, WC, GATHER_NC, PATH, PATH == 3 && kTabSmem>(
+                L, work, xs, v, base, deg, oi, hi, cmu, clam, omega, gamma, idt2, stab);
         else
             update_vertex<R, MODEL, ACCEL, FEXT, WC, GATHER_NC>(L, work, xs, v, base, deg, oi, hi, cmu, clam, omega,
                                                                 gamma, idt2);
@@ -1365,6 +1415,21 @@ __device__ __forceinline__ int ld_acquire(const int32_t *p) {
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int32_t *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_release_add(int32_t *p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// windowed batched schedule: relaxed polling + one acquire fence per item, release reduction (1), or
+// acquire polling + __threadfence in every thread (0)
+#ifndef PBNG_B2_LIGHTSYNC
+#define PBNG_B2_LIGHTSYNC 1
+#endif
+constexpr bool kB2LightSync = PBNG_B2_LIGHTSYNC;
 __device__ __forceinline__ void st_release(int32_t *p, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -1701,7 +1766,6 @@ constexpr int kB2Unroll = PBNG_B2_UNROLL;
 #define PBNG_B2_PF 0
 #endif
 constexpr int kB2Prefetch = PBNG_B2_PF;  // records ahead whose neighbour slot is prefetched into L1 (0: off; 4: 7% slower)
-__device__ __forceinline__ void pf_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 // the packed positions of a lane's two samples at one vertex (sh 6 slot {x0 x1 y0 y1 | z0 z1 . .})
 struct P6 {
     float2 x, y, z;
@@ -1909,21 +1973,36 @@ __global__ void __launch_bounds__(kSweepBlock, PBNG_B2_MINB) sweep_batched2_wind
             const int pc = P.prev[c];
             const int target = (pc < c ? it + 1 : it) * (P.blk_off[pc + 1] - P.blk_off[pc]);
             const int32_t *fl = done + gp * P.ncol + pc;
-            while (ld_acquire(fl) < target) __nanosleep(32);
+            if (kB2LightSync) {
+                // relaxed polling, then ONE acquire fence: every acquire invalidates the SM's whole L1
+                // (CCTL.IVALL), so acquiring per poll and fencing in every thread wiped the gathers that
+                // the other resident warps had cached
+                while (ld_relaxed(fl) < target) __nanosleep(32);
+                fence_acq_rel_gpu();
+            } else {
+                while (ld_acquire(fl) < target) __nanosleep(32);
+            }
         }
-        __syncthreads();
-        __threadfence();
+        __syncthreads();  // the CTA's loads below are ordered after thread 0's acquire
+        if (!kB2LightSync) __threadfence();
         const int wi = (ACCEL != ACCEL_NONE && (it & 1)) ? P.out : P.work;
         const int oi = (ACCEL != ACCEL_NONE && (it & 1)) ? P.work : P.out;
-        const int t = blk * WPB + wq;
-        if (t < P.n_v[c])
-            b2_vertex<ACCEL, FEXT, WC, true>(L, t, P.v_begin[c], P.chunk_begin[c], gp, x_stride, n_batch, wi, oi, P.hist,
-                                             cmu, clam, float(P.omega[it]), float(P.gamma), idt2, s_id[wq], s_sd[wq],
-                                             s_vv[wq]);
+#pragma unroll 1
+        for (int u = 0; u < kB2WinVpw; ++u) {
+            const int t = (blk * kB2WinVpw + u) * WPB + wq;
+            if (t < P.n_v[c])
+                b2_vertex<ACCEL, FEXT, WC, true>(L, t, P.v_begin[c], P.chunk_begin[c], gp, x_stride, n_batch, wi, oi,
+                                                 P.hist, cmu, clam, float(P.omega[it]), float(P.gamma), idt2, s_id[wq],
+                                                 s_sd[wq], s_vv[wq]);
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(done + gp * P.ncol + c, 1);
+            if (kB2LightSync) {
+                red_release_add(done + gp * P.ncol + c, 1);  // cumulative over the CTA's stores (bar.sync above)
+            } else {
+                __threadfence();
+                atomicAdd(done + gp * P.ncol + c, 1);
+            }
         }
     }
 }
@@ -2011,6 +2090,7 @@ cudaError_t sweep_dispatch4(const Problem &p, const Layout &L, const SweepLaunch
                               blocks <= (int64_t)sms * (1024 / kSweepBlock);
         if constexpr (MODEL == MODEL_NH) {
             if (p.path && p.path_mode == 3) {
+                if (kTabSmem) cfg.dynamicSmemBytes = (size_t)L.n_tab * sizeof(typename RT<R>::R4);
                 if (one_wave)
                     return cudaLaunchKernelEx(&cfg, sweep_kernel<R, MODEL, ACCEL, FE, W, true, 3>, L, s.v_begin,
                                               s.n_v, s.chunk_begin, p.x_stride, s.work, s.out, s.hist, cmu, clam, om, ga,
