@@ -270,12 +270,31 @@ pbng_status pbng_halo_unpack(pbng_ctx *ctx, int32_t colour, int32_t peer, int32_
  *   schedule as the NCCL path for all ranks in turn on ctxs[0]'s stream, the exchange being device-to-device
  *   copies between the ranks' halo buffers.  No kernel ever waits for another rank's kernel.  The group
  *   borrows the contexts (destroy the group first).
- * Halo buffers live in the bound workspace (pbng_workspace_bytes counts them). */
+ * Halo buffers live in the bound workspace (pbng_workspace_bytes counts them).
+ *
+ * Peer-store transport (NVLink / NVSwitch peer memory instead of NCCL copies; same iterates bit for bit):
+ * pbng_enable_peer_halo(ctx, 1) (collective over pbng_partition's communicator; after pbng_color and
+ *   pbng_bind_workspace, again after any re-bind or re-layout -- pbng_iterate returns PBNG_E_BAD_ORDER
+ *   otherwise): every rank exports its workspace allocation and a few flag words with cudaIpcGetMemHandle,
+ *   the handles and each neighbour's ghost-row lists travel once over NCCL, and the neighbours' memory is
+ *   mapped with cudaIpcOpenMemHandle (the workspace must come from cudaMalloc, e.g. PyTorch's default
+ *   allocator; the GPUs need peer access).  pbng_iterate then runs, per colour pass E:
+ *   wait until the neighbours' rows of pass E-1 have landed -> part 1 -> per neighbour, on the side stream,
+ *   ONE kernel { wait until that neighbour has finished pass E-1; store this rank's boundary rows straight
+ *   into its ghost rows; raise its `pushed` flag } while part 2 runs -> raise the neighbours' `done` flag.
+ *   No pack / unpack kernels, no NCCL call per colour (one all-reduce barrier per pbng_iterate call).
+ *   A signal that does not arrive within PBNG_PEER_TIMEOUT_MS (environment, default 20000) makes the next
+ *   synchronising call return PBNG_E_CUDA instead of hanging.  enable = 0 returns to NCCL send / receive.
+ * pbng_group_set_transport(group, 1): the same kernels and flag protocol in the one-GPU loopback group
+ *   (the "peer" pointers are the other contexts' buffers; every wait is already satisfied in stream order,
+ *   so no kernel spins); 0 = staged copies (default). */
 typedef struct pbng_group pbng_group;
 pbng_status pbng_nccl_unique_id(void *id_out);
 pbng_status pbng_partition(pbng_ctx *ctx, const int32_t *owner_rank, int32_t rank, int32_t n_ranks,
                            const void *nccl_unique_id);
+pbng_status pbng_enable_peer_halo(pbng_ctx *ctx, int32_t enable);
 pbng_status pbng_group_create(pbng_ctx *const *ctxs, int32_t n_ranks, pbng_group **out);
+pbng_status pbng_group_set_transport(pbng_group *group, int32_t transport);
 pbng_status pbng_group_iterate(pbng_group *group, int32_t n_iterations, pbng_accel accel, double omega, double rho,
                                double gamma);
 pbng_status pbng_group_destroy(pbng_group *group);

@@ -256,6 +256,24 @@ struct pbng_ctx {
         }
     } dd_key;
     uint64_t layout_gen = 0;  // bumped by every re-layout / bind: captured launches bake the layout in
+    // peer-store halo transport (pbng_enable_peer_halo / pbng_group_set_transport): the neighbours' position
+    // buffers and flag words through peer mappings, this rank's own flag words and the neighbours' ghost rows
+    struct PeerState {
+        bool enabled = false;
+        uint64_t gen = 0;          // layout_gen and workspace the mappings were made for
+        const void *ws = nullptr;
+        uint32_t *flags = nullptr;  // own allocation: pushed[n_ranks] | done[n_ranks] | counter[n_ranks] | scratch[4]
+        int32_t *rows = nullptr;    // [halo_send_off.back()] the send vertices' ghost rows on their receiver
+        std::vector<int> nbr;       // ranks this one exchanges any row with
+        struct Peer {
+            void *x[3] = {nullptr, nullptr, nullptr};
+            int64_t stride = 0;
+            int sh = 0;
+            uint32_t *flags = nullptr;
+            void *ipc_ws = nullptr, *ipc_flags = nullptr;  // cudaIpcOpenMemHandle results (multi-process)
+        };
+        std::vector<Peer> peer;  // [n_ranks]
+    } peer;
     cudaGraphExec_t dd_graph = nullptr;
     int64_t dd_graph_launches = 0;   // kernels one replay of dd_graph runs
     int64_t dd_graph_sweeps = 0;     // sweep launches one replay of dd_graph runs
@@ -1561,6 +1579,7 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
     bool ok = false;
     std::string why;
@@ -1596,6 +1615,7 @@ const NcclApi &nccl() {
         sym(api.GroupStart, "ncclGroupStart");
         sym(api.GroupEnd, "ncclGroupEnd");
         sym(api.AllReduce, "ncclAllReduce");
+        sym(api.AllGather, "ncclAllGather");
         sym(api.GetErrorString, "ncclGetErrorString");
         api.ok = all;
     });
@@ -1633,12 +1653,288 @@ void drop_dd_graph(pbng_ctx *c) {
     c->dd_key = pbng_ctx::GraphKey();
 }
 
+// ---- peer-store halo transport: set-up (kernels: pbng_kernels.cu "Peer-store halo transport") ----
+
+void peer_release(pbng_ctx *c) {
+    pbng_ctx::PeerState &P = c->peer;
+    for (auto &q : P.peer) {
+        if (q.ipc_ws) cudaIpcCloseMemHandle(q.ipc_ws);
+        if (q.ipc_flags) cudaIpcCloseMemHandle(q.ipc_flags);
+    }
+    P.peer.clear();
+    P.nbr.clear();
+    if (P.flags) cudaFree(P.flags);
+    if (P.rows) cudaFree(P.rows);
+    P.flags = nullptr;
+    P.rows = nullptr;
+    P.enabled = false;
+}
+
+bool peer_stale(const pbng_ctx *c) { return !c->peer.enabled || c->peer.gen != c->layout_gen || c->peer.ws != c->ws; }
+
+// own allocations and the neighbour list (ranks with a non-empty send or receive list in some colour)
+cudaError_t peer_alloc(pbng_ctx *c) {
+    peer_release(c);
+    pbng_ctx::PeerState &P = c->peer;
+    const int n_ranks = c->n_ranks;
+    P.peer.assign(n_ranks, pbng_ctx::PeerState::Peer());
+    for (int q = 0; q < n_ranks; ++q) {
+        if (q == c->rank) continue;
+        bool any = false;
+        for (int32_t col = 0; col < c->ncol && !any; ++col) {
+            const size_t seg = (size_t)col * n_ranks + q;
+            any = halo_n_send(c, seg) > 0 || halo_n_recv(c, seg) > 0;
+        }
+        if (any) P.nbr.push_back(q);
+    }
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(&P.flags), (size_t)(3 * n_ranks + 4) * 4);
+    if (e == cudaSuccess) e = cudaMemset(P.flags, 0, (size_t)(3 * n_ranks + 4) * 4);
+    const size_t n_send = c->halo_send_off.empty() ? 0 : (size_t)c->halo_send_off.back();
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void **>(&P.rows), std::max<size_t>(n_send, 1) * 4);
+    return e;
+}
+
+// loopback group: the "peer mappings" are the other contexts' own device pointers
+pbng_status peer_setup_group(const std::vector<pbng_ctx *> &ranks) {
+    for (pbng_ctx *c : ranks) {
+        PBNG_CUDA(peer_alloc(c), "peer halo: allocation");
+        const int n_ranks = c->n_ranks;
+        const size_t n_send = (size_t)c->halo_send_off.back();
+        std::vector<int32_t> rows(std::max<size_t>(n_send, 1), 0);
+        for (int q : c->peer.nbr) {
+            const pbng_ctx *d = ranks[q];
+            for (int32_t col = 0; col < c->ncol; ++col) {
+                const size_t sseg = (size_t)col * n_ranks + q, rseg = (size_t)col * n_ranks + c->rank;
+                const int64_t n = halo_n_send(c, sseg);
+                if (n != halo_n_recv(d, rseg))
+                    return fail(PBNG_E_INVALID_ARGUMENT, "peer halo: send and receive lists of two ranks differ in length");
+                for (int64_t k = 0; k < n; ++k) {
+                    // the k-th vertex rank c sends is the k-th vertex rank q receives (both ascending original id)
+                    if (c->halo_send_orig[c->halo_send_off[sseg] + k] != d->halo_recv_orig[d->halo_recv_off[rseg] + k])
+                        return fail(PBNG_E_INVALID_ARGUMENT, "peer halo: send and receive lists of two ranks differ");
+                    rows[c->halo_send_off[sseg] + k] = d->h_halo_recv[d->halo_recv_off[rseg] + k];
+                }
+            }
+        }
+        PBNG_CUDA(cudaMemcpy(c->peer.rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice), "peer halo: rows");
+    }
+    for (pbng_ctx *c : ranks) {
+        for (int q : c->peer.nbr) {
+            pbng_ctx *d = ranks[q];
+            pbng_ctx::PeerState::Peer &P = c->peer.peer[q];
+            for (int k = 0; k < 3; ++k) P.x[k] = d->L.xbuf[k];
+            P.stride = d->prob.x_stride;
+            P.sh = d->prob.lane_shift;
+            P.flags = d->peer.flags;
+        }
+        c->peer.enabled = true;
+        c->peer.gen = c->layout_gen;
+        c->peer.ws = c->ws;
+    }
+    return PBNG_OK;
+}
+
+// what a rank tells the others about its memory (all-gathered through the communicator)
+struct PeerHello {
+    cudaIpcMemHandle_t ws, flags;
+    uint64_t ws_off;     // the workspace's offset inside the allocation the handle names
+    uint64_t x_off[3];   // position buffers, bytes from the workspace base
+    int64_t x_stride;
+    int32_t sh, nbr;     // nbr: this rank exchanges rows with the receiving rank (filled per reader)
+};
+
+// one process per GPU: IPC handles of the workspace allocation and the flag words, and the neighbours'
+// ghost rows, exchanged over the context's NCCL communicator (collective)
+pbng_status peer_setup_comm(pbng_ctx *c) {
+    const NcclApi &A = nccl();
+    PBNG_CUDA(peer_alloc(c), "peer halo: allocation");
+    const int n_ranks = c->n_ranks;
+    PeerHello me;
+    std::memset(&me, 0, sizeof(me));
+    // the bound workspace is usually a slice of a caching allocator's block: the handle names the whole
+    // cudaMalloc allocation, the slice is found by its offset (cuMemGetAddressRange through the runtime)
+    typedef int (*GetRange)(unsigned long long *, size_t *, unsigned long long);
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    PBNG_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &qr), "peer halo: driver entry point");
+    if (!fn || qr != cudaDriverEntryPointSuccess) return fail(PBNG_E_CUDA, "peer halo: cuMemGetAddressRange not available");
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (reinterpret_cast<GetRange>(fn)(&base, &size, (unsigned long long)(uintptr_t)c->ws) != 0)
+        return fail(PBNG_E_CUDA, "peer halo: the workspace is not a device allocation");
+    PBNG_CUDA(cudaIpcGetMemHandle(&me.ws, reinterpret_cast<void *>((uintptr_t)base)),
+              "peer halo: cudaIpcGetMemHandle(workspace) -- allocate the workspace with cudaMalloc (PyTorch: not "
+              "expandable_segments)");
+    PBNG_CUDA(cudaIpcGetMemHandle(&me.flags, c->peer.flags), "peer halo: cudaIpcGetMemHandle(flags)");
+    me.ws_off = (uint64_t)((uintptr_t)c->ws - (uintptr_t)base);
+    for (int k = 0; k < 3; ++k) me.x_off[k] = (uint64_t)(static_cast<char *>(c->L.xbuf[k]) - static_cast<char *>(c->ws));
+    me.x_stride = c->prob.x_stride;
+    me.sh = c->prob.lane_shift;
+    PeerHello *d_all = nullptr;
+    PBNG_CUDA(cudaMalloc(reinterpret_cast<void **>(&d_all), sizeof(PeerHello) * (size_t)n_ranks), "peer halo: allocation");
+    std::vector<PeerHello> all(n_ranks);
+    pbng_status st = PBNG_OK;
+    do {
+        cudaError_t e = cudaMemcpyAsync(d_all + c->rank, &me, sizeof(me), cudaMemcpyHostToDevice, c->stream);
+        if (e != cudaSuccess) { st = cuda_fail(e, "peer halo: copy"); break; }
+        ncclResult_t r = A.AllGather(d_all + c->rank, d_all, sizeof(PeerHello), ncclUint8, c->comm, c->stream);
+        if (r != ncclSuccess) { st = nccl_fail(r, "peer halo: all-gather"); break; }
+        // the neighbours' ghost rows: rank q's receive list (colour, this rank) is this rank's row list (colour, q)
+        r = A.GroupStart();
+        for (int q : c->peer.nbr)
+            for (int32_t col = 0; col < c->ncol && r == ncclSuccess; ++col) {
+                const size_t seg = (size_t)col * n_ranks + q;
+                const int64_t ns = halo_n_send(c, seg), nr = halo_n_recv(c, seg);
+                if (nr > 0) r = A.Send(c->L.halo_recv + c->halo_recv_off[seg], (size_t)nr * 4, ncclUint8, q, c->comm, c->stream);
+                if (r == ncclSuccess && ns > 0)
+                    r = A.Recv(c->peer.rows + c->halo_send_off[seg], (size_t)ns * 4, ncclUint8, q, c->comm, c->stream);
+            }
+        ncclResult_t r2 = A.GroupEnd();
+        if (r == ncclSuccess) r = r2;
+        if (r != ncclSuccess) { st = nccl_fail(r, "peer halo: row exchange"); break; }
+        e = cudaMemcpyAsync(all.data(), d_all, sizeof(PeerHello) * (size_t)n_ranks, cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) { st = cuda_fail(e, "peer halo: exchange"); break; }
+    } while (false);
+    cudaFree(d_all);
+    if (st != PBNG_OK) return st;
+    for (int q : c->peer.nbr) {
+        pbng_ctx::PeerState::Peer &P = c->peer.peer[q];
+        PBNG_CUDA(cudaIpcOpenMemHandle(&P.ipc_ws, all[q].ws, cudaIpcMemLazyEnablePeerAccess),
+                  "peer halo: cudaIpcOpenMemHandle(workspace) -- the ranks' GPUs need peer access (NVLink / NVSwitch)");
+        PBNG_CUDA(cudaIpcOpenMemHandle(&P.ipc_flags, all[q].flags, cudaIpcMemLazyEnablePeerAccess),
+                  "peer halo: cudaIpcOpenMemHandle(flags)");
+        char *ws = static_cast<char *>(P.ipc_ws) + all[q].ws_off;
+        for (int k = 0; k < 3; ++k) P.x[k] = ws + all[q].x_off[k];
+        P.stride = all[q].x_stride;
+        P.sh = all[q].sh;
+        P.flags = static_cast<uint32_t *>(P.ipc_flags);
+    }
+    c->peer.enabled = true;
+    c->peer.gen = c->layout_gen;
+    c->peer.ws = c->ws;
+    return PBNG_OK;
+}
+
 // The exchange step of one colour, on stream `side`, after every rank's part-1 vertices of the colour
 // are final: pack each (rank, peer) send list, move the buffers, unpack each receive list.  `ranks` are
 // the rank contexts this process drives (one with NCCL, all of them in the loopback group).
 struct Exchange {
     std::vector<pbng_ctx *> ranks;
     bool loopback = false;
+    bool peer = false;  // peer-store transport: rows stored straight into the neighbours' ghost rows
+
+    static uint64_t peer_timeout_ns() {
+        const char *e = getenv("PBNG_PEER_TIMEOUT_MS");
+        const long ms = e ? atol(e) : 20000;
+        return (uint64_t)(ms > 0 ? ms : 20000) * 1000000ull;
+    }
+    // flag words of a rank: pushed[q] at q, done[q] at n_ranks + q, block counter of the push to q at 2 n_ranks + q
+    // start of an iterate block: zero the flag words; between processes a barrier keeps a fast neighbour's
+    // first signal from landing before the zeroing
+    cudaError_t peer_begin(cudaStream_t main) {
+        for (pbng_ctx *c : ranks) {
+            cudaError_t e = cudaMemsetAsync(c->peer.flags, 0, (size_t)(3 * c->n_ranks + 4) * 4, main);
+            if (e != cudaSuccess) return e;
+        }
+        if (!loopback) {
+            pbng_ctx *c = ranks[0];
+            uint32_t *scratch = c->peer.flags + 3 * c->n_ranks;
+            ncclResult_t r = nccl().AllReduce(scratch, scratch, 1, ncclInt32, ncclSum, c->comm, main);
+            if (r != ncclSuccess) {
+                status = nccl_fail(r, "iterate: peer-halo barrier");
+                return cudaErrorUnknown;
+            }
+        }
+        return cudaSuccess;
+    }
+    // end of pass E (colour col; both parts and the pushes are in stream order before this), ONE launch per
+    // rank: tell every neighbour this rank is done reading pass E, then wait for the rows the neighbours
+    // stored during pass E -- pass E + 1 reads them
+    cudaError_t peer_sync(int32_t col, uint32_t E, cudaStream_t main) {
+        for (pbng_ctx *c : ranks) {
+            PeerSignal S;
+            S.val = E;
+            for (int q : c->peer.nbr) S.flag[S.n++] = c->peer.peer[q].flags + c->n_ranks + c->rank;
+            PeerWait W;
+            W.flags = c->peer.flags;
+            W.want = E;
+            W.timeout_ns = peer_timeout_ns();
+            for (int q : c->peer.nbr)
+                if (halo_n_recv(c, (size_t)col * c->n_ranks + q) > 0) W.slot[W.n++] = q;
+            if (S.n == 0 && W.n == 0) continue;
+            cudaError_t e = launch_halo_sync(c->L, S, W, main);
+            if (e != cudaSuccess) return e;
+            ++launches;
+        }
+        return cudaSuccess;
+    }
+    // the exchange of pass E (colour col) on `side`: per neighbour ONE kernel { wait done >= E - 1; store rows;
+    // pushed = E }
+    cudaError_t run_peer(int32_t col, int nf, uint32_t E, cudaStream_t side) {
+        for (pbng_ctx *c : ranks) {
+            const int n_ranks = c->n_ranks;
+            for (int q : c->peer.nbr) {
+                const size_t seg = (size_t)col * n_ranks + q;
+                const int64_t n = halo_n_send(c, seg);
+                if (n == 0) continue;
+                const pbng_ctx::PeerState::Peer &P = c->peer.peer[q];
+                PeerPush A;
+                A.idx = c->L.halo_send + c->halo_send_off[seg];
+                A.rows = c->peer.rows + c->halo_send_off[seg];
+                A.n = n;
+                A.nf = nf;
+                A.buf[0] = c->work;
+                A.buf[1] = c->out;
+                A.buf[2] = c->hist;
+                A.x_stride = c->prob.x_stride;
+                A.sh = c->prob.lane_shift;
+                for (int k = 0; k < 3; ++k) A.peer_x[k] = P.x[k];
+                A.peer_stride = P.stride;
+                A.peer_sh = P.sh;
+                A.wait_flag = c->peer.flags + n_ranks + q;
+                A.wait_val = E - 1;
+                A.sig_flag = P.flags + c->rank;
+                A.sig_val = E;
+                A.counter = c->peer.flags + 2 * n_ranks + q;
+                A.timeout_ns = peer_timeout_ns();
+                cudaError_t e = launch_halo_push(c->prob, c->L, A, side);
+                if (e != cudaSuccess) return e;
+                ++launches;
+            }
+        }
+        return cudaSuccess;
+    }
+    // after pass E (both parts and the pushes): tell every neighbour this rank is done reading pass E
+    cudaError_t peer_signal_done(uint32_t E, cudaStream_t main) {
+        for (pbng_ctx *c : ranks) {
+            PeerSignal S;
+            S.val = E;
+            for (int q : c->peer.nbr) S.flag[S.n++] = c->peer.peer[q].flags + c->n_ranks + c->rank;
+            if (S.n == 0) continue;
+            cudaError_t e = launch_halo_signal(S, main);
+            if (e != cudaSuccess) return e;
+            ++launches;
+        }
+        return cudaSuccess;
+    }
+    // end of the block: every neighbour is through its last pass (its rows of that pass landed before its
+    // done signal), so nothing more is stored here
+    cudaError_t peer_end(uint32_t E_last, cudaStream_t main) {
+        if (E_last == 0) return cudaSuccess;
+        for (pbng_ctx *c : ranks) {
+            PeerWait W;
+            W.flags = c->peer.flags;
+            W.want = E_last;
+            W.timeout_ns = peer_timeout_ns();
+            for (int q : c->peer.nbr) W.slot[W.n++] = c->n_ranks + q;
+            if (W.n == 0) continue;
+            cudaError_t e = launch_halo_wait(c->L, W, main);
+            if (e != cudaSuccess) return e;
+            ++launches;
+        }
+        return cudaSuccess;
+    }
     int64_t launches = 0;
     pbng_status status = PBNG_OK;
 
@@ -1723,15 +2019,21 @@ cudaError_t dd_iterations(Exchange &X, cudaStream_t main, cudaStream_t side, cud
                           int32_t n, pbng_accel accel, double omega, double rho, double gamma, int64_t *sweeps) {
     const int nf = accel == PBNG_ACCEL_NONE ? 1 : 3;
     const int32_t ncol = X.ranks[0]->ncol;
+    if (X.peer) {
+        cudaError_t e = X.peer_begin(main);
+        if (e != cudaSuccess) return e;
+    }
+    uint32_t E = 0;  // pass epoch of the peer-store flags: 1 + pass index within this block
     for (int32_t it = 0; it < n; ++it) {
         for (int32_t col = 0; col < ncol; ++col) {
+            ++E;
             for (pbng_ctx *c : X.ranks) {
                 cudaError_t e = sweep_colour_impl(c, col, accel, omega, rho, gamma, sweeps, 1);
                 if (e != cudaSuccess) return e;
             }
             cudaError_t e = cudaEventRecord(ev_a, main);
             if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_a, 0);
-            if (e == cudaSuccess) e = X.run(col, nf, side);
+            if (e == cudaSuccess) e = X.peer ? X.run_peer(col, nf, E, side) : X.run(col, nf, side);
             if (e == cudaSuccess) e = cudaEventRecord(ev_b, side);
             if (e != cudaSuccess) return e;
             for (pbng_ctx *c : X.ranks) {
@@ -1739,10 +2041,15 @@ cudaError_t dd_iterations(Exchange &X, cudaStream_t main, cudaStream_t side, cud
                 if (e != cudaSuccess) return e;
             }
             e = cudaStreamWaitEvent(main, ev_b, 0);
+            // the block's last pass signals first and waits in a second round (peer_end): in the one-GPU
+            // loopback group a rank's wait must not precede, in stream order, the signal it waits for
+            if (e == cudaSuccess && X.peer)
+                e = (it == n - 1 && col == ncol - 1) ? X.peer_signal_done(E, main) : X.peer_sync(col, E, main);
             if (e != cudaSuccess) return e;
         }
         for (pbng_ctx *c : X.ranks) end_iteration_impl(c, accel);
     }
+    if (X.peer) return X.peer_end(E, main);
     return cudaSuccess;
 }
 
@@ -1777,6 +2084,7 @@ pbng_status dd_run(pbng_ctx *owner, Exchange &X, cudaStream_t main, cudaStream_t
         key.gens.push_back(reinterpret_cast<uintptr_t>(c->ws));
         key.gens.push_back((uint64_t)c->work | (uint64_t)c->l << 8);
     }
+    key.gens.push_back(X.peer ? 1 : 0);
     const bool use_graph = dd_graphs_enabled() && owner->profiling != 1 && n > 0;
     if (use_graph && owner->dd_graph && owner->dd_key == key) {
         PBNG_CUDA(cudaGraphLaunch(owner->dd_graph, main), who);
@@ -2469,6 +2777,12 @@ pbng_status pbng_iterate(pbng_ctx *c, int32_t n_iterations, pbng_accel accel, do
         PBNG_CUDA(ensure_dd_streams(c), "iterate: side stream");
         Exchange X;
         X.ranks = {c};
+        if (c->peer.enabled) {
+            if (peer_stale(c))
+                return fail(PBNG_E_BAD_ORDER, "iterate: the layout or workspace changed since pbng_enable_peer_halo; "
+                                              "call it again on every rank");
+            X.peer = true;
+        }
         int64_t sweeps = 0;
         st = dd_run(c, X, c->stream, c->dd_side, c->dd_cap, c->dd_ev_a, c->dd_ev_b, n_iterations, accel, omega, rho,
                     gamma, &sweeps, "iterate: decomposed iterations");
@@ -2695,6 +3009,7 @@ pbng_status pbng_synchronize(pbng_ctx *c) {
     if (c->bound) {
         int32_t flag = 0;
         PBNG_CUDA(cudaMemcpy(&flag, c->L.flag, 4, cudaMemcpyDeviceToHost), "synchronize: flag");
+        if (flag & 2) return fail(PBNG_E_CUDA, "peer halo: a neighbour rank's signal did not arrive in time");
         if (flag) return fail(PBNG_E_NONFINITE, "a non-finite position was produced");
     }
     return PBNG_OK;
@@ -2729,6 +3044,7 @@ pbng_status pbng_energy_residual(pbng_ctx *c, double *energy_out, double *residu
         if (energy_out) energy_out[b] = res[2 * b];
         if (residual_out) residual_out[b] = res[2 * b + 1];
     }
+    if (flag & 2) return fail(PBNG_E_CUDA, "peer halo: a neighbour rank's signal did not arrive in time");
     if (flag) return fail(PBNG_E_NONFINITE, "a non-finite position was produced");
     return PBNG_OK;
 }
@@ -3141,6 +3457,7 @@ pbng_status pbng_partition(pbng_ctx *c, const int32_t *owner, int32_t rank, int3
     if (st != PBNG_OK) return st;
     DevGuard g(c->device);
     drop_dd_graph(c);
+    peer_release(c);
     if (c->comm) {
         nccl().CommDestroy(c->comm);
         c->comm = nullptr;
@@ -3159,6 +3476,7 @@ pbng_status pbng_partition(pbng_ctx *c, const int32_t *owner, int32_t rank, int3
 
 struct pbng_group {
     std::vector<pbng_ctx *> ranks;
+    int transport = 0;  // 0: staged device-to-device copies, 1: peer stores
     cudaStream_t side = nullptr, cap = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
 };
@@ -3224,6 +3542,19 @@ pbng_status pbng_group_iterate(pbng_group *g, int32_t n_iterations, pbng_accel a
     Exchange X;
     X.ranks = g->ranks;
     X.loopback = true;
+    if (g->transport == 1) {
+        bool stale = false;
+        for (pbng_ctx *c : g->ranks) stale = stale || peer_stale(c);
+        if (stale) {
+            drop_dd_graph(c0);
+            pbng_status ps = peer_setup_group(g->ranks);
+            if (ps != PBNG_OK) {
+                for (size_t k = 0; k < g->ranks.size(); ++k) g->ranks[k]->stream = saved[k];
+                return ps;
+            }
+        }
+        X.peer = true;
+    }
     int64_t sweeps = 0;
     pbng_status st = dd_run(c0, X, main, g->side, g->cap, g->ev_a, g->ev_b, n_iterations, accel, omega, rho, gamma,
                             &sweeps, "group_iterate");
@@ -3237,11 +3568,49 @@ pbng_status pbng_group_iterate(pbng_group *g, int32_t n_iterations, pbng_accel a
     return st;
 }
 
+pbng_status pbng_group_set_transport(pbng_group *g, int32_t transport) {
+    if (!g) return fail(PBNG_E_INVALID_ARGUMENT, "group_set_transport: null group");
+    if (transport != 0 && transport != 1) return fail(PBNG_E_INVALID_ARGUMENT, "group_set_transport: 0 (copies) or 1 (peer stores)");
+    DevGuard dg(g->ranks[0]->device);
+    drop_dd_graph(g->ranks[0]);
+    if (transport == 0)
+        for (pbng_ctx *c : g->ranks) {
+            cudaStreamSynchronize(c->stream);
+            peer_release(c);
+        }
+    g->transport = transport;
+    return PBNG_OK;
+}
+
+pbng_status pbng_enable_peer_halo(pbng_ctx *c, int32_t enable) {
+    pbng_status st = require_device(c);
+    if (st != PBNG_OK) return st;
+    if (c->n_ranks < 2 || !c->comm)
+        return fail(PBNG_E_BAD_ORDER, "enable_peer_halo: needs a decomposed context with pbng_partition's communicator");
+    if (!c->colored || !c->bound) return fail(PBNG_E_BAD_ORDER, "enable_peer_halo: colour and bind first");
+    if (c->n_ranks > kMaxPeers) return fail(PBNG_E_INVALID_ARGUMENT, "enable_peer_halo: at most 64 ranks");
+    DevGuard g(c->device);
+    PBNG_CUDA(cudaStreamSynchronize(c->stream), "enable_peer_halo: synchronize");
+    drop_dd_graph(c);
+    if (!enable) {
+        peer_release(c);
+        return PBNG_OK;
+    }
+    if (!nccl().AllGather) return fail(PBNG_E_NCCL, "enable_peer_halo: ncclAllGather not available");
+    st = peer_setup_comm(c);
+    if (st != PBNG_OK) peer_release(c);
+    return st;
+}
+
 pbng_status pbng_group_destroy(pbng_group *g) {
     if (!g) return PBNG_OK;
     if (!g->ranks.empty()) {
         DevGuard dg(g->ranks[0]->device);
         if (g->side) cudaStreamSynchronize(g->side);
+        for (pbng_ctx *c : g->ranks) {
+            cudaStreamSynchronize(c->stream);
+            peer_release(c);
+        }
         drop_dd_graph(g->ranks[0]);
         if (g->side) cudaStreamDestroy(g->side);
         if (g->cap) cudaStreamDestroy(g->cap);
@@ -3259,6 +3628,7 @@ pbng_status pbng_destroy(pbng_ctx *c) {
         cudaStreamSynchronize(c->stream);
         clear_l2_persistence(c);  // restore the caller's stream window and the device's persisting limit
         drop_dd_graph(c);
+        peer_release(c);
         if (c->comm) nccl().CommDestroy(c->comm);
         if (c->dd_side) cudaStreamDestroy(c->dd_side);
         if (c->dd_cap) cudaStreamDestroy(c->dd_cap);

@@ -177,6 +177,43 @@ cudaError_t launch_halo_pack(const Problem &p, const Layout &L, const int32_t *i
                              const int (&bufs)[3], void *buf, cudaStream_t st);
 cudaError_t launch_halo_unpack(const Problem &p, const Layout &L, const int32_t *idx, int64_t n, int n_fields,
                                const int (&bufs)[3], const void *buf, cudaStream_t st);
+// peer-store halo transport (pbng_kernels.cu "Peer-store halo transport"): one neighbour's rows of one colour,
+// stored straight into the neighbour's position buffers
+constexpr int kMaxPeers = 64;  // ranks of one decomposition (pbng_group_create's bound)
+struct PeerPush {
+    const int32_t *idx = nullptr;   // this rank's send rows (internal ids), device
+    const int32_t *rows = nullptr;  // the same vertices' ghost rows on the neighbour (its internal ids), device
+    int64_t n = 0;
+    int nf = 1;                     // fields: work (, out, hist)
+    int buf[3] = {0, 1, 2};         // buffer indices of the fields (the ranks rotate their buffers in lockstep)
+    int64_t x_stride = 0;
+    int sh = 0;
+    void *peer_x[3] = {nullptr, nullptr, nullptr};  // the neighbour's xbuf[0..2] through the peer mapping
+    int64_t peer_stride = 0;
+    int peer_sh = 0;
+    const uint32_t *wait_flag = nullptr;  // own done[q] (null: ordering by the stream alone)
+    uint32_t wait_val = 0;
+    uint32_t *sig_flag = nullptr;         // the neighbour's pushed[this rank] (null: none)
+    uint32_t sig_val = 0;
+    uint32_t *counter = nullptr;          // own scratch word, zero between launches
+    uint64_t timeout_ns = 0;
+};
+struct PeerWait {
+    const uint32_t *flags = nullptr;
+    int n = 0;
+    int slot[kMaxPeers] = {};
+    uint32_t want = 0;
+    uint64_t timeout_ns = 0;
+};
+struct PeerSignal {
+    int n = 0;
+    uint32_t *flag[kMaxPeers] = {};
+    uint32_t val = 0;
+};
+cudaError_t launch_halo_push(const Problem &p, const Layout &L, const PeerPush &P, cudaStream_t st);
+cudaError_t launch_halo_wait(const Layout &L, const PeerWait &W, cudaStream_t st);
+cudaError_t launch_halo_signal(const PeerSignal &S, cudaStream_t st);
+cudaError_t launch_halo_sync(const Layout &L, const PeerSignal &S, const PeerWait &W, cudaStream_t st);
 int kernels_per_energy_residual();
 // contact detection at the positions of buffer `work`, sample `sample`: per free boundary vertex the closest
 // boundary triangle of another body within `thickness` (L.c_res); fp64 arithmetic

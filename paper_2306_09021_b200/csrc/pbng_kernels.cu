@@ -2267,6 +2267,107 @@ __global__ void halo_unpack_kernel(const Layout L, const int32_t *__restrict__ i
 }
 
 // ------------------------------------------------------------------------------------------------
+// Peer-store halo transport (pbng_enable_peer_halo / pbng_group_set_transport; PAPER.md:693-705 colour
+// order): after a colour's part-1 vertices are final, ONE kernel per neighbour rank reads
+// this rank's send rows and stores them straight into the neighbour's ghost rows through a peer mapping
+// (NVLink P2P between processes, plain device pointers in the one-GPU loopback group) -- no pack buffer,
+// no library copy, no unpack.  Ordering between ranks is carried by two epoch flags per neighbour pair in
+// the receiver's memory, E = 1 + pass index within the pbng_iterate call (pass = iteration * colours + colour):
+//   pushed[q] = E   rank q's rows of pass E have landed here            (written by q's push kernel)
+//   done[q]   = E   rank q has finished every read of pass E            (written by q's signal kernel)
+// Rank r's pass E: wait pushed[q] >= E-1 (all neighbours) -> part 1 -> per neighbour q on the side stream
+// { wait done[q] >= E-1 ; store rows ; pushed_on_q[r] = E } || part 2 -> signal done_on_q[r] = E.
+// Every wait refers to pass E-1 of a neighbour, so by induction on E there is no cycle.
+// ------------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t global_timer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// bounded spin: a neighbour that never signals (a rank died, mismatched iterate calls) raises bit 1 of
+// the context's flag word instead of hanging the GPU; the host reports it as PBNG_E_CUDA
+__device__ __forceinline__ void peer_wait(const uint32_t *flag, uint32_t want, int32_t *err, uint64_t timeout_ns) {
+    if ((int32_t)(ld_acquire_sys(flag) - want) >= 0) return;
+    if (*reinterpret_cast<volatile int32_t *>(err) & 2) return;  // an earlier wait already timed out: fail fast
+    const uint64_t t0 = global_timer_ns();
+    while ((int32_t)(ld_acquire_sys(flag) - want) < 0) {
+        __nanosleep(200);
+        if (global_timer_ns() - t0 > timeout_ns) {
+            atomicOr(err, 2);
+            return;
+        }
+    }
+}
+
+template <class R>
+__global__ void __launch_bounds__(256) halo_push_kernel(const Layout L, const PeerPush P) {
+    using R4 = typename RT<R>::R4;
+    if (P.wait_flag) {  // the neighbour must be done reading pass E-1 before its ghost rows change
+        if (threadIdx.x == 0) peer_wait(P.wait_flag, P.wait_val, L.flag, P.timeout_ns);
+        __syncthreads();
+    }
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t b = blockIdx.y;
+    if (i < P.n) {
+        const int32_t src = P.idx[i], dst = P.rows[i];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (k < P.nf) {
+                const R4 x = pos_load<R>(L.xbuf[P.buf[k]], b, src, P.x_stride, P.sh);
+                pos_store<R>(P.peer_x[P.buf[k]], b, dst, P.peer_stride, P.peer_sh, x);
+            }
+    }
+    if (P.sig_flag) {
+        __threadfence_system();  // this thread's peer stores are performed before the block is counted
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned total = gridDim.x * gridDim.y;
+            if (atomicAdd(P.counter, 1u) == total - 1) {  // last block: every block's rows have landed
+                *P.counter = 0;
+                __threadfence_system();
+                st_release_sys(P.sig_flag, P.sig_val);
+            }
+        }
+    }
+}
+
+// end of pass E on the main stream, one launch: publish done = E in every neighbour's flag words, then wait
+// for the rows the neighbours stored in pass E (their pushed flags) before the next pass starts
+__global__ void halo_sync_kernel(const PeerSignal S, const PeerWait W, int32_t *err) {
+    const int t = threadIdx.x;
+    if (t < S.n) {
+        __threadfence_system();
+        st_release_sys(S.flag[t], S.val);
+    }
+    if (t < W.n) peer_wait(W.flags + W.slot[t], W.want, err, W.timeout_ns);
+}
+
+// one thread per neighbour: wait until flags[slot[t]] >= want (pushed / done epochs of the neighbours)
+__global__ void halo_wait_kernel(const PeerWait W, int32_t *err) {
+    const int t = threadIdx.x;
+    if (t < W.n) peer_wait(W.flags + W.slot[t], W.want, err, W.timeout_ns);
+}
+
+// one thread per neighbour: publish `val` in the neighbour's flag word (all earlier work of the stream,
+// this rank's reads of pass E included, is complete at the kernel boundary)
+__global__ void halo_signal_kernel(const PeerSignal S) {
+    const int t = threadIdx.x;
+    if (t < S.n) {
+        __threadfence_system();
+        st_release_sys(S.flag[t], S.val);
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
 // contact detection (pbng_detect_contacts): a uniform hash grid of the boundary
 // triangles (cell size = largest triangle extent + 2 thickness, so a triangle's thickness-inflated box
 // covers at most 2 cells per axis), then one thread per free boundary vertex walks its cell's bucket and
@@ -2863,6 +2964,34 @@ cudaError_t launch_halo_unpack(const Problem &p, const Layout &L, const int32_t 
         halo_unpack_kernel<double><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf, p.lane_shift);
     else
         halo_unpack_kernel<float><<<grid, 256, 0, st>>>(L, idx, n, n_fields, p.x_stride, bufs[0], bufs[1], bufs[2], buf, p.lane_shift);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_push(const Problem &p, const Layout &L, const PeerPush &P, cudaStream_t st) {
+    if (P.n <= 0 && !P.sig_flag) return cudaSuccess;
+    dim3 grid((unsigned)std::max<int64_t>((P.n + 255) / 256, 1), (unsigned)p.n_batch);
+    if (p.dtype == DT_F64)
+        halo_push_kernel<double><<<grid, 256, 0, st>>>(L, P);
+    else
+        halo_push_kernel<float><<<grid, 256, 0, st>>>(L, P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_wait(const Layout &L, const PeerWait &W, cudaStream_t st) {
+    if (W.n <= 0) return cudaSuccess;
+    halo_wait_kernel<<<1, 64, 0, st>>>(W, L.flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_sync(const Layout &L, const PeerSignal &S, const PeerWait &W, cudaStream_t st) {
+    if (S.n <= 0 && W.n <= 0) return cudaSuccess;
+    halo_sync_kernel<<<1, 64, 0, st>>>(S, W, L.flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_halo_signal(const PeerSignal &S, cudaStream_t st) {
+    if (S.n <= 0) return cudaSuccess;
+    halo_signal_kernel<<<1, 64, 0, st>>>(S);
     return cudaGetLastError();
 }
 

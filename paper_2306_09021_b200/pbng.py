@@ -32,7 +32,7 @@ EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbn
            "pbng_set_inertia", "pbng_set_schedule", "pbng_detect_contacts", "pbng_update_constraints",
            "pbng_get_colours", "pbng_set_l2_persistence", "pbng_sweep_colour_part", "pbng_set_stream",
            "pbng_nccl_unique_id", "pbng_partition", "pbng_group_create", "pbng_group_iterate", "pbng_group_destroy",
-           "pbng_set_records")
+           "pbng_set_records", "pbng_enable_peer_halo", "pbng_group_set_transport")
 
 WC_DTYPE = np.dtype([("n0", "<i4"), ("n1", "<i4"), ("idx0", "<i4", 4), ("idx1", "<i4", 4), ("w0", "<f8", 4),
                      ("w1", "<f8", 4), ("anchor", "<f8", 3), ("K", "<f8", 6)])
@@ -106,6 +106,8 @@ def lib():
     L.pbng_group_create.argtypes = [C.POINTER(vp), i32, C.POINTER(vp)]
     L.pbng_group_iterate.argtypes = [vp, i32, C.c_int, d, d, d]
     L.pbng_group_destroy.argtypes = [vp]
+    L.pbng_group_set_transport.argtypes = [vp, i32]
+    L.pbng_enable_peer_halo.argtypes = [vp, i32]
     L.pbng_last_error.restype = C.c_char_p
     L.pbng_version.restype = i32
     for name in EXPORTS:
@@ -380,6 +382,11 @@ class Context:
         idb = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
         _check(lib().pbng_partition(self._h, _ptr(owner) if owner is not None else None, int(rank), int(n_ranks), idb))
 
+    def enable_peer_halo(self, enable: bool = True):
+        """pbng_enable_peer_halo: halo rows stored straight into the neighbours' ghost rows over peer memory
+        (collective over the partition's communicator; after color + bind)."""
+        _check(lib().pbng_enable_peer_halo(self._h, 1 if enable else 0))
+
     def halo_counts(self, colour: int, peer: int):
         ns, nr = C.c_int64(), C.c_int64()
         _check(lib().pbng_halo_counts(self._h, int(colour), int(peer), C.byref(ns), C.byref(nr)))
@@ -427,6 +434,10 @@ class Group:
         h = C.c_void_p()
         _check(lib().pbng_group_create(arr, len(self.ctxs), C.byref(h)))
         self._h = h
+
+    def set_transport(self, transport: str):
+        """pbng_group_set_transport: "copies" (staged device-to-device copies) or "peer" (peer stores + flags)."""
+        _check(lib().pbng_group_set_transport(self._h, {"copies": 0, "peer": 1}[transport]))
 
     def iterate(self, n: int, accel: str = "none", omega: float = 1.0, rho: float = 0.0, gamma: float = 1.0):
         _check(lib().pbng_group_iterate(self._h, int(n), ACCEL[accel], float(omega), float(rho), float(gamma)))

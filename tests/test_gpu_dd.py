@@ -43,11 +43,13 @@ def gather(scene, ctxs, owner):
     return x
 
 
-def decomposed(scene, dtype, world, mode="group", split=None):
+def decomposed(scene, dtype, world, mode="group", split=None, transport="copies"):
     from paper_2306_09021_b200 import dd
     ctxs, owner = dd.loopback_contexts(scene, world, dtype=dtype)
     parts = [scene.iterations] if split is None else split
     grp = dd.Group(ctxs) if mode == "group" else None
+    if grp is not None and transport != "copies":
+        grp.set_transport(transport)
     for k in parts:
         if mode == "group":
             grp.iterate(k, scene.accel, scene.omega, scene.rho, scene.gamma)
@@ -146,3 +148,86 @@ def test_full_config5_eight_ranks_graph_replay_bitwise_and_host_submission():
     assert np.array_equal(x1, xd)
     assert replays >= 1
     assert host_s < 0.5 * gpu_s
+
+
+@pytest.mark.parametrize("cfg,world,dtype", [(5, 2, "f64"), (5, 3, "f32"), (3, 3, "f32"), (2, 2, "f32"),
+                                             (4, 2, "f32"), (1, 2, "f64")])
+def test_peer_store_transport_is_bitwise(cfg, world, dtype):
+    """pbng_group_set_transport(1): boundary rows stored straight into the neighbours' ghost rows by ONE kernel
+    per neighbour, ordered by the pushed / done epoch flags (include/pbng.h "Peer-store transport") -- the
+    iterates equal the undecomposed ones bit for bit, and no wait times out (PBNG_E_CUDA otherwise)."""
+    s = G.make_config(cfg, "small")
+    if cfg == 1:
+        s.accel, s.omega, s.iterations = "sor", 1.5, 40
+    x1, E1, R1 = single(s, dtype)
+    xd, Ed, Rd, infos = decomposed(s, dtype, world, transport="peer")
+    assert sum(i["n_ghosts"] for i in infos) > 0
+    assert np.array_equal(x1, xd), np.abs(x1 - xd).max()
+    np.testing.assert_allclose(Ed, E1, rtol=1e-12, atol=0)
+
+
+def test_peer_store_transport_split_calls_graph_and_direct():
+    """Calls that continue the state (flag epochs restart per call), with CUDA graphs and with direct launches,
+    and switching the transport back and forth on one group."""
+    from paper_2306_09021_b200 import dd
+    s = G.make_config(5, "small")
+    xs, Es, _, _ = decomposed(s, "f32", 3, mode="serial", split=[3, 2, 4])
+    xg, Eg, _, _ = decomposed(s, "f32", 3, split=[3, 2, 4], transport="peer")
+    os.environ["PBNG_DD_GRAPH"] = "0"
+    try:
+        xe, Ee, _, _ = decomposed(s, "f32", 3, split=[3, 2, 4], transport="peer")
+    finally:
+        del os.environ["PBNG_DD_GRAPH"]
+    assert np.array_equal(xs, xg) and np.array_equal(xs, xe)
+    assert np.array_equal(Es, Eg) and np.array_equal(Es, Ee)
+    ctxs, owner = dd.loopback_contexts(s, 3, dtype="f32")
+    grp = dd.Group(ctxs)
+    for k, tr in zip([3, 2, 4], ["peer", "copies", "peer"]):
+        grp.set_transport(tr)
+        grp.iterate(k, s.accel, s.omega, s.rho, s.gamma)
+    xm = gather(s, ctxs, owner)
+    grp.close()
+    for c in ctxs:
+        c.close()
+    assert np.array_equal(xs, xm)
+
+
+def test_batched_sample_minor_peer_store_is_bitwise():
+    s = G.config4_batched(n_samples=40, n=4, iterations=12)
+    x1, E1, R1 = single(s, "f32")
+    xd, Ed, Rd, infos = decomposed(s, "f32", 2, transport="peer")
+    assert np.array_equal(x1, xd), np.abs(x1 - xd).max()
+
+
+def test_full_config5_eight_ranks_peer_store_bitwise_and_timing():
+    """Config 5 at full size over 8 loopback ranks with peer stores: bitwise equal to one context, the graph is
+    replayed, and the GPU time per iteration is printed next to the staged-copy transport's."""
+    import torch
+    from paper_2306_09021_b200 import dd
+    s = G.config5_muscle_stack()
+    s.iterations = 6
+    x1, E1, _ = single(s, "f32")
+    ctxs, owner = dd.loopback_contexts(s, 8, dtype="f32")
+    grp = dd.Group(ctxs)
+    x0 = np.asarray(s.x0)
+    times = {}
+    for tr in ("copies", "peer"):
+        grp.set_transport(tr)
+        for rep in range(3):
+            for c in ctxs:
+                c.set_positions(x0)
+            torch.cuda.synchronize()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(ctxs[0].stream)
+            grp.iterate(s.iterations, s.accel)
+            ev1.record(ctxs[0].stream)
+            torch.cuda.synchronize()
+            times[tr] = ev0.elapsed_time(ev1) * 1e3 / s.iterations
+        xd = gather(s, ctxs, owner)
+        assert np.array_equal(x1, xd), tr
+    launches = ctxs[0].query()["kernel_launches"]
+    print(f"config5 8 loopback ranks, GPU us/iteration: copies {times['copies']:.1f}, peer stores {times['peer']:.1f}")
+    grp.close()
+    for c in ctxs:
+        c.close()
+    assert launches > 0
