@@ -294,7 +294,7 @@ def run_reference(args):
 class Solver:
     """One rank's solve of a scene through the public API (context_from_scene / iterate / energy_residual)."""
 
-    def __init__(self, scene, config, local, dev, stream, world, rank, decomposed, dtype, pg):
+    def __init__(self, scene, config, local, dev, stream, world, rank, decomposed, dtype, pg, halo="nccl"):
         import torch
         from paper_2306_09021_b200 import context_from_scene, dd
         self.scene, self.dev, self.stream, self.pg = scene, dev, stream, pg
@@ -306,6 +306,9 @@ class Solver:
                 part = (owner, rank, world, dd.nccl_unique_id(pg, rank))
             self.ctx = context_from_scene(scene, device=local, stream=stream, set_positions=False, partition=part,
                                           dtype=dtype)
+            if decomposed and halo == "peer":
+                # rows stored straight into the neighbours' ghost rows over NVLink peer memory (collective)
+                self.ctx.enable_peer_halo(True)
             nd = self.ctx.np_dtype
             self.x0_dev = torch.from_numpy(np.ascontiguousarray(scene.x0, dtype=nd)).to(dev)
             self.x0_host = torch.from_numpy(np.ascontiguousarray(scene.x0, dtype=nd)).pin_memory()
@@ -435,7 +438,7 @@ def run_ours(args):
             torch.cuda.empty_cache()
         barrier()
 
-    S = Solver(scene, config, local, dev, stream, world, rank, decomposed, args.dtype, pg)
+    S = Solver(scene, config, local, dev, stream, world, rank, decomposed, args.dtype, pg, args.halo)
     ctx, q = S.ctx, S.q
     for _ in range(args.warmup):
         S.step()
@@ -482,7 +485,7 @@ def run_ours(args):
                 "step": "set_positions(x0, device) + iterate + energy_residual",
                 "l2": "inputs larger than L2: %.2f GB of algorithmic bytes per iteration vs 126 MB L2" % (
                     (q["sweep_bytes"] + q["accel_bytes"]) / 1e9),
-                "parallelism": (f"domain decomposition over {world} GPUs (slabs), NCCL halo exchange after every colour"
+                "parallelism": ((f"domain decomposition over {world} GPUs (slabs), " + ("peer-store halo rows over NVLink (pbng_enable_peer_halo)" if args.halo == "peer" else "NCCL halo exchange") + " after every colour")
                                 if decomposed else f"samples sharded over {world} GPUs (no collective)" if config == 4
                                 else f"replicas x{world} (independent problems, no collective)"),
             },
@@ -521,6 +524,9 @@ def main():
     ap.add_argument("--dtype", default=None, choices=["f32", "f64"],
                     help="override the config's compute dtype (e.g. config 3 in fp64: the FP64 measurement variant)")
     ap.add_argument("--dd", action="store_true", help="N > 1: domain-decompose one mesh (z slabs) instead of replicas")
+    ap.add_argument("--halo", default=os.environ.get("PBNG_BENCH_HALO", "nccl"), choices=["nccl", "peer"],
+                    help="decomposed runs: per-colour halo by NCCL send/receive (default) or by peer stores "
+                         "(pbng_enable_peer_halo: one kernel per neighbour writes its ghost rows over NVLink)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("bench.py: warmup raised to 3 (timing rule)", file=sys.stderr)

@@ -2275,9 +2275,12 @@ __global__ void halo_unpack_kernel(const Layout L, const int32_t *__restrict__ i
 // the receiver's memory, E = 1 + pass index within the pbng_iterate call (pass = iteration * colours + colour):
 //   pushed[q] = E   rank q's rows of pass E have landed here            (written by q's push kernel)
 //   done[q]   = E   rank q has finished every read of pass E            (written by q's signal kernel)
-// Rank r's pass E: wait pushed[q] >= E-1 (all neighbours) -> part 1 -> per neighbour q on the side stream
-// { wait done[q] >= E-1 ; store rows ; pushed_on_q[r] = E } || part 2 -> signal done_on_q[r] = E.
-// Every wait refers to pass E-1 of a neighbour, so by induction on E there is no cycle.
+// Rank r's pass E: part 1 -> per neighbour q on the side stream { wait done[q] >= E-1 ; store rows ;
+// pushed_on_q[r] = E } || part 2 -> join -> ONE sync kernel { done_on_q[r] = E ; wait pushed[q] >= E for the
+// neighbours that send rows of this colour }.  The block's last pass signals, then waits done[q] >= E.
+// A wait of pass E refers to what a neighbour does in passes <= E before its own wait of pass E, so by
+// induction on E there is no cycle; tests/test_peer_protocol.py model-checks the rules under random rank
+// speeds (and shows that dropping either wait breaks the serial colour order).
 // ------------------------------------------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
@@ -2343,6 +2346,9 @@ __global__ void __launch_bounds__(256) halo_push_kernel(const Layout L, const Pe
 // end of pass E on the main stream, one launch: publish done = E in every neighbour's flag words, then wait
 // for the rows the neighbours stored in pass E (their pushed flags) before the next pass starts
 __global__ void halo_sync_kernel(const PeerSignal S, const PeerWait W, int32_t *err) {
+    // the next pass's part-1 sweep is a programmatic dependent launch: its CTAs may start now, prefetch their
+    // records (static data) and block in griddepcontrol.wait until this kernel -- i.e. the flag wait -- is done
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int t = threadIdx.x;
     if (t < S.n) {
         __threadfence_system();
