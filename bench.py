@@ -294,7 +294,7 @@ def run_reference(args):
 class Solver:
     """One rank's solve of a scene through the public API (context_from_scene / iterate / energy_residual)."""
 
-    def __init__(self, scene, config, local, dev, stream, world, rank, decomposed, dtype, pg, halo="nccl"):
+    def __init__(self, scene, config, local, dev, stream, world, rank, decomposed, dtype, pg, halo="nccl", colours=None):
         import torch
         from paper_2306_09021_b200 import context_from_scene, dd
         self.scene, self.dev, self.stream, self.pg = scene, dev, stream, pg
@@ -305,7 +305,7 @@ class Solver:
                 owner = dd.slab_partition(scene.X, world)
                 part = (owner, rank, world, dd.nccl_unique_id(pg, rank))
             self.ctx = context_from_scene(scene, device=local, stream=stream, set_positions=False, partition=part,
-                                          dtype=dtype)
+                                          dtype=dtype, colours=colours)
             if decomposed and halo == "peer":
                 # rows stored straight into the neighbours' ghost rows over NVLink peer memory (collective)
                 self.ctx.enable_peer_halo(True)
@@ -348,7 +348,7 @@ def timed(fn, steps, stream, dev, barrier):
     return ev0.elapsed_time(ev1), out
 
 
-def roofline_block(config, dtype_key, q, sweep_ms, sweep_launches, t_ms, iters, steps, scene_accel):
+def roofline_block(config, dtype_key, q, sweep_ms, sweep_launches, t_ms, iters, steps, scene_accel, colouring="greedy"):
     """Roofline of the dominant kernel: HBM for the Neo-Hookean colour sweep (config
     3), FP32 ALU for the fixed-corotated and batched kernels (configs 2, 4, 5) against the measured
     CUDA-core peak; both fractions are reported for every config, `bound` names the one that binds."""
@@ -363,7 +363,7 @@ def roofline_block(config, dtype_key, q, sweep_ms, sweep_launches, t_ms, iters, 
     key = f"config{config}" + ("" if dtype_key is None else f"_{dtype_key}")
     hbm_block = {"achieved": achieved_bw, "peak": hbm, "unit": "GB/s", "frac": achieved_bw / hbm,
                  "peak_source": peak_kind, "algorithmic_bytes_per_launch": bytes_per_launch,
-                 "traffic": ncu_traffic(key)}
+                 "traffic": ncu_traffic(key if colouring == "greedy" else f"{key}_{colouring}")}
     fl = sweep_flops(key)
     ap = alu_peaks()
     alu_block = None
@@ -438,7 +438,13 @@ def run_ours(args):
             torch.cuda.empty_cache()
         barrier()
 
-    S = Solver(scene, config, local, dev, stream, world, rank, decomposed, args.dtype, pg, args.halo)
+    colours = None
+    if args.colouring == "kuhn4":
+        if config != 3:
+            raise SystemExit("--colouring kuhn4 applies to config 3 (one Kuhn grid)")
+        from scenes import generators as G
+        colours = G.kuhn_grid_colouring(128, 128, 128)
+    S = Solver(scene, config, local, dev, stream, world, rank, decomposed, args.dtype, pg, args.halo, colours)
     ctx, q = S.ctx, S.q
     for _ in range(args.warmup):
         S.step()
@@ -481,6 +487,8 @@ def run_ours(args):
                              .replace("fp64 fp64", "fp64")),
                 "free_vertices_per_gpu": q["n_free"] * q["n_batch"], "iterations_per_step": iters,
                 "pairs_per_iteration": q["n_pairs"], "colours": q["n_colours"],
+                "colouring": ("greedy (PAPER.md:702-705)" if args.colouring == "greedy" else
+                              "caller-supplied (i+j+k) mod 4 of the Kuhn grid (pbng_color_given)"),
                 "samples_on_rank0": q["n_batch"],
                 "step": "set_positions(x0, device) + iterate + energy_residual",
                 "l2": "inputs larger than L2: %.2f GB of algorithmic bytes per iteration vs 126 MB L2" % (
@@ -490,7 +498,7 @@ def run_ours(args):
                                 else f"replicas x{world} (independent problems, no collective)"),
             },
             "roofline": roofline_block(config, args.dtype, q, sweep_ms, sweep_launches, t_ms, iters, args.steps,
-                                       scene.accel),
+                                       scene.accel, args.colouring),
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
@@ -524,6 +532,9 @@ def main():
     ap.add_argument("--dtype", default=None, choices=["f32", "f64"],
                     help="override the config's compute dtype (e.g. config 3 in fp64: the FP64 measurement variant)")
     ap.add_argument("--dd", action="store_true", help="N > 1: domain-decompose one mesh (z slabs) instead of replicas")
+    ap.add_argument("--colouring", default="greedy", choices=["greedy", "kuhn4"],
+                    help="config 3: the paper's greedy colouring (default, 8 colours) or the caller-supplied "
+                         "4-colouring (i + j + k) mod 4 of the Kuhn grid through pbng_color_given")
     ap.add_argument("--halo", default=os.environ.get("PBNG_BENCH_HALO", "nccl"), choices=["nccl", "peer"],
                     help="decomposed runs: per-colour halo by NCCL send/receive (default) or by peer stores "
                          "(pbng_enable_peer_halo: one kernel per neighbour writes its ghost rows over NVLink)")

@@ -163,6 +163,14 @@ pbng_status pbng_set_constraints(pbng_ctx *ctx, const int32_t *pinned, int64_t n
  * Fails with PBNG_E_ISOLATED_VERTEX for a free vertex with no incident stencil. */
 pbng_status pbng_color(pbng_ctx *ctx, int32_t *colour_out, int32_t *n_colours_out);
 
+/* The same layout from a colouring the caller supplies instead of the greedy one (colours[n_vertices], every
+ * vertex, pinned ones included): any node colouring in the sense of PAPER.md:702 -- nodes of one colour share
+ * no element and no weak constraint -- gives a valid colour-parallel Gauss-Seidel order,
+ * and fewer colours mean fewer, larger colour passes; e.g. (i + j + k) mod 4 on a Kuhn grid,
+ * where greedy colouring in index order takes 8.  Validated: PBNG_E_INVALID_ARGUMENT with *bad_index (optional)
+ * = the offending vertex, tet, or n_tets + constraint index.  Replaces pbng_color in the call order. */
+pbng_status pbng_color_given(pbng_ctx *ctx, const int32_t *colours, int32_t *n_colours_out, int64_t *bad_index);
+
 /* Device bytes the caller must allocate for pbng_bind_workspace (256-byte aligned). */
 pbng_status pbng_workspace_bytes(pbng_ctx *ctx, uint64_t *bytes);
 

@@ -2559,6 +2559,47 @@ pbng_status pbng_color(pbng_ctx *c, int32_t *colour_out, int32_t *n_colours_out)
     return PBNG_OK;
 }
 
+pbng_status pbng_color_given(pbng_ctx *c, const int32_t *colours, int32_t *n_colours_out, int64_t *bad_index) {
+    if (bad_index) *bad_index = -1;
+    if (!c || !colours) return fail(PBNG_E_INVALID_ARGUMENT, "color_given: null argument");
+    if (!c->has_material || !c->has_constraints)
+        return fail(PBNG_E_BAD_ORDER, "color_given: set_material and set_constraints must come first");
+    // a node colouring in the sense of PAPER.md:702: nodes of one colour share no element and no weak constraint
+    for (int64_t v = 0; v < c->nv; ++v)
+        if (colours[v] < 0 || colours[v] >= 65536) {
+            if (bad_index) *bad_index = v;
+            return fail(PBNG_E_INVALID_ARGUMENT, "color_given: colour of vertex " + std::to_string(v) + " outside [0, 65536)");
+        }
+    for (int64_t e = 0; e < c->nt; ++e) {
+        const int32_t *t = c->tets.data() + 4 * e;
+        for (int a = 0; a < 4; ++a)
+            for (int b = a + 1; b < 4; ++b)
+                if (t[a] != t[b] && colours[t[a]] == colours[t[b]]) {
+                    if (bad_index) *bad_index = e;
+                    return fail(PBNG_E_INVALID_ARGUMENT, "color_given: two vertices of tet " + std::to_string(e) + " share a colour");
+                }
+    }
+    for (size_t q = 0; q < c->wc.size(); ++q) {
+        const pbng_weak_constraint &w = c->wc[q];
+        std::vector<int32_t> nodes;
+        for (int a = 0; a < w.n0; ++a) nodes.push_back(w.idx0[a]);
+        for (int a = 0; a < w.n1; ++a) nodes.push_back(w.idx1[a]);
+        std::sort(nodes.begin(), nodes.end());
+        nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
+        for (size_t a = 0; a < nodes.size(); ++a)
+            for (size_t b = a + 1; b < nodes.size(); ++b)
+                if (colours[nodes[a]] == colours[nodes[b]]) {
+                    if (bad_index) *bad_index = c->nt + (int64_t)q;
+                    return fail(PBNG_E_INVALID_ARGUMENT, "color_given: two nodes of weak constraint " + std::to_string(q) + " share a colour");
+                }
+    }
+    const std::vector<int32_t> given(colours, colours + c->nv);
+    pbng_status st = colour_and_layout(c, &given);
+    if (st != PBNG_OK) return st;
+    if (n_colours_out) *n_colours_out = c->ncol;
+    return PBNG_OK;
+}
+
 pbng_status pbng_workspace_bytes(pbng_ctx *c, uint64_t *bytes) {
     if (!c || !bytes) return fail(PBNG_E_INVALID_ARGUMENT, "null argument");
     if (!c->colored) return fail(PBNG_E_NOT_COLORED, "workspace_bytes: call pbng_color first");

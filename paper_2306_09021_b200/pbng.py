@@ -32,7 +32,7 @@ EXPORTS = ("pbng_create_mesh", "pbng_set_material", "pbng_set_constraints", "pbn
            "pbng_set_inertia", "pbng_set_schedule", "pbng_detect_contacts", "pbng_update_constraints",
            "pbng_get_colours", "pbng_set_l2_persistence", "pbng_sweep_colour_part", "pbng_set_stream",
            "pbng_nccl_unique_id", "pbng_partition", "pbng_group_create", "pbng_group_iterate", "pbng_group_destroy",
-           "pbng_set_records", "pbng_enable_peer_halo", "pbng_group_set_transport")
+           "pbng_set_records", "pbng_enable_peer_halo", "pbng_group_set_transport", "pbng_color_given")
 
 WC_DTYPE = np.dtype([("n0", "<i4"), ("n1", "<i4"), ("idx0", "<i4", 4), ("idx1", "<i4", 4), ("w0", "<f8", 4),
                      ("w1", "<f8", 4), ("anchor", "<f8", 3), ("K", "<f8", 6)])
@@ -108,6 +108,7 @@ def lib():
     L.pbng_group_destroy.argtypes = [vp]
     L.pbng_group_set_transport.argtypes = [vp, i32]
     L.pbng_enable_peer_halo.argtypes = [vp, i32]
+    L.pbng_color_given.argtypes = [vp, vp, C.POINTER(i32), C.POINTER(i64)]
     L.pbng_last_error.restype = C.c_char_p
     L.pbng_version.restype = i32
     for name in EXPORTS:
@@ -194,9 +195,18 @@ class Context:
                                           _ptr(targets) if targets.size else None, _ptr(w) if w.size else None,
                                           w.size))
 
-    def color(self):
-        out = np.empty(self.n_vertices, np.int32)
+    def color(self, colours=None):
+        """pbng_color (greedy), or pbng_color_given with the caller's node colouring."""
         n = C.c_int32()
+        if colours is not None:
+            out = _np(colours, np.int32).reshape(-1).copy()
+            if out.shape[0] != self.n_vertices:
+                raise ValueError("colours: one entry per vertex")
+            bad = C.c_int64(-1)
+            _check(lib().pbng_color_given(self._h, _ptr(out), C.byref(n), C.byref(bad)))
+            self.colours, self.n_colours = out, n.value
+            return out, n.value
+        out = np.empty(self.n_vertices, np.int32)
         _check(lib().pbng_color(self._h, _ptr(out), C.byref(n)))
         self.colours, self.n_colours = out, n.value
         return out, n.value
@@ -465,7 +475,7 @@ def test_polar(F, dtype: str = "f32", device: int = 0) -> np.ndarray:
 
 def context_from_scene(scene, device=0, dtype: Optional[str] = None, stream=None, bind: bool = True,
                        set_positions: bool = True, partition=None, l2_persist: bool = True,
-                       records: str = "auto") -> Context:
+                       records: str = "auto", colours=None) -> Context:
     """Build, colour, bind and initialise a Context for a scenes.Scene (all samples of its batch).
     partition = (owner, rank, n_ranks) builds the rank-local context of a domain decomposition (driven by
     a Group or the colour-by-colour calls); (owner, rank, n_ranks, nccl_id) attaches the library's NCCL
@@ -482,7 +492,7 @@ def context_from_scene(scene, device=0, dtype: Optional[str] = None, stream=None
             ctx.partition(*partition)
         else:
             ctx.set_partition(*partition)
-    ctx.colours, ctx.n_colours = ctx.color()
+    ctx.colours, ctx.n_colours = ctx.color(colours)
     if bind and ctx.device >= 0:
         ctx.bind_workspace()
         if l2_persist:

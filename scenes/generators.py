@@ -135,6 +135,15 @@ def kuhn_grid(nx: int, ny: int, nz: int, h: float, origin=(0.0, 0.0, 0.0), verte
     return X, tets
 
 
+def kuhn_grid_colouring(nx: int, ny: int, nz: int) -> np.ndarray:
+    """An input for pbng_color_given / the oracle's set_colours: colour (i + j + k) mod 4 of grid vertex
+    (i, j, k) of kuhn_grid(nx, ny, nz).  Two vertices of one Kuhn tet differ by a non-zero offset in {0,1}^3,
+    so their index sums differ by 1, 2 or 3: no two vertices of a tet share a colour."""
+    i, j, k = np.meshgrid(np.arange(nx + 1), np.arange(ny + 1), np.arange(nz + 1), indexing="ij")
+    col = (i + j + k) % 4
+    return np.ascontiguousarray(col.transpose(2, 1, 0).reshape(-1).astype(np.int32))  # v = i + (nx+1)(j + (ny+1) k)
+
+
 def five_tet_grid(n: int, h: float = 1.0):
     """Alternating 5-tet split of an n^3-VERTEX grid ((n-1)^3 cells); the mesh family whose sizes match
     PAPER.md Table 1 (32K vertices / 150K elements = 32^3 / 31^3*5).  Cells with even

@@ -46,6 +46,8 @@ def oracle_run(key, scene):
         from oracle import Oracle, threads
         threads(_host_threads())
         o = Oracle(scene, omp=True)
+        if getattr(scene, "given_colours", None) is not None:
+            o.set_colours(scene.given_colours)  # both sides visit the caller's colouring (pbng_color_given)
         x0 = scene.x0[0]
         t = time.perf_counter()
         x, _ = o.iterate(x0, x0, 0, scene.iterations, scene.accel, scene.omega, scene.rho, scene.gamma)
@@ -55,7 +57,7 @@ def oracle_run(key, scene):
 
 def gpu_run(scene, dtype):
     from paper_2306_09021_b200 import context_from_scene
-    ctx = context_from_scene(scene, device=0, dtype=dtype)
+    ctx = context_from_scene(scene, device=0, dtype=dtype, colours=getattr(scene, "given_colours", None))
     ctx.iterate(scene.iterations, scene.accel, scene.omega, scene.rho, scene.gamma)
     E, r = ctx.energy_residual()
     x = ctx.get_positions().cpu().numpy().astype(np.float64)[0]
@@ -91,6 +93,14 @@ def check(name, scene, dtype, key):
 def test_full_config3_all_iterations(dtype):
     s = G.config3_hetero_cube()  # 128^3, 12.6M tets, NH, per-tet lognormal E, SOR 1.5, 50 iterations
     check("config3_all_iterations", s, dtype, "c3")
+
+
+def test_full_config3_given_4_colouring_all_iterations():
+    """Config 3 at full size on the caller-supplied 4-colouring of the Kuhn grid (pbng_color_given): the
+    CUDA path against the oracle visiting the same colouring, all 50 iterations."""
+    s = G.config3_hetero_cube()
+    s.given_colours = G.kuhn_grid_colouring(128, 128, 128)
+    check("config3_kuhn4_all_iterations", s, "f32", "c3k4")
 
 
 @pytest.mark.parametrize("noise_seed", [0, 1, 2, 3])

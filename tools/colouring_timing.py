@@ -1,0 +1,58 @@
+"""Config 3 (full size) with the greedy colouring (8 colours) against a caller-supplied 4-colouring of the Kuhn
+grid (pbng_color_given, scenes.kuhn_grid_colouring): ms per iteration of the colour sweeps, vertex-updates/s,
+and energy / Newton residual after the config's 50 iterations (both orders are valid PBNG).
+
+    python tools/colouring_timing.py [--dtype f32] [--n 128] [--reps 5]
+One JSON line per colouring."""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+    from paper_2306_09021_b200 import context_from_scene
+    from scenes import generators as G
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--n", type=int, default=128)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--iters", type=int, default=10)
+    args = ap.parse_args()
+    s = G.config3_hetero_cube(n=args.n)
+    acc = (s.accel, s.omega, s.rho, s.gamma)
+    for name, col in (("greedy", None), ("kuhn4", G.kuhn_grid_colouring(args.n, args.n, args.n))):
+        ctx = context_from_scene(s, device=0, dtype=args.dtype, colours=col)
+        q = ctx.query()
+        ctx.iterate(3, *acc)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(args.reps):
+            ctx.set_positions(np.asarray(s.x0))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ctx.iterate(args.iters, *acc)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / args.iters)
+        ctx.set_positions(np.asarray(s.x0))
+        E0, R0 = ctx.energy_residual()
+        ctx.iterate(s.iterations, *acc)
+        E, R = ctx.energy_residual()
+        ms = float(np.median(times))
+        print(json.dumps({"colouring": name, "n_colours": int(ctx.n_colours), "dtype": ctx.dtype, "records": q["records"],
+                          "ms_per_iter": ms, "min_ms": float(min(times)),
+                          "vupd_per_s": q["n_free"] / (ms / 1e3), "iterations": s.iterations,
+                          "energy_x0": float(E0[0]), "residual_x0": float(R0[0]),
+                          "energy": float(E[0]), "residual": float(R[0])}), flush=True)
+        ctx.close()
+
+
+if __name__ == "__main__":
+    main()
