@@ -24,8 +24,13 @@ def main():
     ap.add_argument("--n", type=int, default=128)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--config", type=int, default=3, choices=[3, 4], help="3: one n^3 cube; 4: 4096 samples of a 16^3 cube")
     args = ap.parse_args()
-    s = G.config3_hetero_cube(n=args.n)
+    if args.config == 4:
+        args.n = 16
+        s = G.config4_batched()
+    else:
+        s = G.config3_hetero_cube(n=args.n)
     acc = (s.accel, s.omega, s.rho, s.gamma)
     for name, col in (("greedy", None), ("kuhn4", G.kuhn_grid_colouring(args.n, args.n, args.n))):
         ctx = context_from_scene(s, device=0, dtype=args.dtype, colours=col)
@@ -48,9 +53,10 @@ def main():
         ms = float(np.median(times))
         print(json.dumps({"colouring": name, "n_colours": int(ctx.n_colours), "dtype": ctx.dtype, "records": q["records"],
                           "ms_per_iter": ms, "min_ms": float(min(times)),
-                          "vupd_per_s": q["n_free"] / (ms / 1e3), "iterations": s.iterations,
+                          "config": args.config, "vupd_per_s": q["n_free"] * q["n_batch"] / (ms / 1e3), "iterations": s.iterations,
                           "energy_x0": float(E0[0]), "residual_x0": float(R0[0]),
-                          "energy": float(E[0]), "residual": float(R[0])}), flush=True)
+                          "energy": float(E[0]), "residual": float(R[0]),
+                          "residual_mean_over_samples": float(np.mean(R))}), flush=True)
         ctx.close()
 
 
