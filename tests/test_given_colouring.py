@@ -137,3 +137,38 @@ def test_gpu_given_colouring_schedules_agree_bitwise_and_record_layouts_agree():
     assert np.array_equal(xs[("table", "colour_launches")], xs[("table", "pipelined")])
     d = np.abs(xs[("table", "colour_launches")].astype(np.float64) - xs[("stored", "colour_launches")])
     assert d.max() <= 1e-5 * s.bbox_diag()
+
+
+def _stack_colouring(n_blocks, n):
+    # block b coloured (i + j + k + b) mod 4: a binding spring joins (i, j, n) of block b to (i, j, 0) of block
+    # b + 1, colours (i + j + n + b) and (i + j + b + 1) mod 4, distinct while (n - 1) mod 4 != 0
+    one = G.kuhn_grid_colouring(n, n, n)
+    return np.concatenate([(one + b) % 4 for b in range(n_blocks)]).astype(np.int32)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,dtype", [(2, "f64"), (2, "f32"), (5, "f64"), (5, "f32")])
+def test_gpu_equals_oracle_on_given_colourings_fixed_corotated(cfg, dtype):
+    """Fixed-corotated configs (twisted bar with Chebyshev; stacked blocks with springs and contacts) on
+    4-colourings: the split / pipelined kernels against the oracle visiting the same colouring."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from oracle import Oracle
+    from paper_2306_09021_b200 import context_from_scene
+    s = G.make_config(cfg, "small")
+    col = G.kuhn_grid_colouring(6, 6, 24) if cfg == 2 else _stack_colouring(3, 7)
+    s.iterations = 12
+    o = Oracle(s)
+    o.set_colours(col)
+    x0 = s.x0[0]
+    xo, _ = o.iterate(x0, x0, 0, s.iterations, s.accel, s.omega, s.rho, s.gamma)
+    ctx = context_from_scene(s, device=0, dtype=dtype, colours=col)
+    assert ctx.n_colours == 4
+    ctx.iterate(s.iterations, s.accel, s.omega, s.rho, s.gamma)
+    E, _ = ctx.energy_residual()
+    xg = ctx.get_positions().cpu().numpy().astype(np.float64)[0]
+    ctx.close()
+    tx, te = TOL[dtype]
+    assert np.abs(xg - xo).max() / s.bbox_diag() <= tx
+    assert abs(float(E[0]) - o.energy(xo)) / abs(o.energy(xo)) <= te

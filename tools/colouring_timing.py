@@ -24,15 +24,27 @@ def main():
     ap.add_argument("--n", type=int, default=128)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--iters", type=int, default=10)
-    ap.add_argument("--config", type=int, default=3, choices=[3, 4], help="3: one n^3 cube; 4: 4096 samples of a 16^3 cube")
+    ap.add_argument("--config", type=int, default=3, choices=[2, 3, 4, 5],
+                    help="2: twisted bar; 3: one n^3 cube; 4: 4096 samples of a 16^3 cube; 5: 8 stacked blocks")
     args = ap.parse_args()
     if args.config == 4:
         args.n = 16
         s = G.config4_batched()
+        k4 = G.kuhn_grid_colouring(16, 16, 16)
+    elif args.config == 2:
+        s = G.config2_twisted_bar()
+        k4 = G.kuhn_grid_colouring(32, 32, 128)
+    elif args.config == 5:
+        # block b is coloured (i + j + k + b) mod 4: the binding springs join the top face of block b to the
+        # bottom face of block b + 1 at the same (i, j), colours (i + j + 48 + b) and (i + j + b + 1) mod 4
+        s = G.config5_muscle_stack()
+        one = G.kuhn_grid_colouring(48, 48, 48)
+        k4 = np.concatenate([(one + b) % 4 for b in range(8)]).astype(np.int32)
     else:
         s = G.config3_hetero_cube(n=args.n)
+        k4 = G.kuhn_grid_colouring(args.n, args.n, args.n)
     acc = (s.accel, s.omega, s.rho, s.gamma)
-    for name, col in (("greedy", None), ("kuhn4", G.kuhn_grid_colouring(args.n, args.n, args.n))):
+    for name, col in (("greedy", None), ("kuhn4", k4)):
         ctx = context_from_scene(s, device=0, dtype=args.dtype, colours=col)
         q = ctx.query()
         ctx.iterate(3, *acc)
