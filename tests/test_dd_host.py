@@ -173,3 +173,16 @@ def test_nccl_unique_id_bootstrap_over_process_group(world):
     uids = [g[0] for g in got]
     assert all(len(u) == 128 for u in uids) and all(u == uids[0] for u in uids)
     assert all(g[1] == 11 for g in got)  # PBNG_E_NO_DEVICE
+
+
+def test_peer_halo_needs_a_device_context_with_a_communicator():
+    """pbng_enable_peer_halo (include/pbng.h "Peer-store transport") on host-only contexts: a device is required
+    (PBNG_E_NO_DEVICE) whether or not the context is partitioned; nothing is allocated or mapped."""
+    from paper_2306_09021_b200 import PBNGError, context_from_scene, dd
+    s = _scene("stack")
+    for part in (None, (dd.slab_partition(s.X, 2), 0, 2)):
+        ctx = context_from_scene(s, device=-1, dtype="f64", partition=part)
+        with pytest.raises(PBNGError) as e:
+            ctx.enable_peer_halo(True)
+        assert e.value.status == 11  # PBNG_E_NO_DEVICE
+        ctx.close()

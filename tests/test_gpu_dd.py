@@ -231,3 +231,22 @@ def test_full_config5_eight_ranks_peer_store_bitwise_and_timing():
     for c in ctxs:
         c.close()
     assert launches > 0
+
+
+def test_enable_peer_halo_without_a_communicator_is_refused():
+    """pbng_enable_peer_halo is collective over pbng_partition's communicator: a device context without one
+    (undecomposed, or a loopback rank context) gets PBNG_E_BAD_ORDER and keeps working."""
+    from paper_2306_09021_b200 import PBNGError, context_from_scene, dd
+    s = G.make_config(3, "small")
+    ctx = context_from_scene(s, device=0, dtype="f32")
+    with pytest.raises(PBNGError) as e:
+        ctx.enable_peer_halo(True)
+    assert e.value.status == 5
+    ctx.iterate(2, s.accel, s.omega, s.rho, s.gamma)
+    ctx.close()
+    ctxs, _ = dd.loopback_contexts(s, 2, dtype="f32")
+    with pytest.raises(PBNGError) as e:
+        ctxs[0].enable_peer_halo(True)
+    assert e.value.status == 5
+    for c in ctxs:
+        c.close()
