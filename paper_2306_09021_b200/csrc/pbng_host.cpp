@@ -269,6 +269,7 @@ struct pbng_ctx {
             void *x[3] = {nullptr, nullptr, nullptr};
             int64_t stride = 0;
             int sh = 0;
+            int64_t n_local = 0;  // vertices the neighbour holds
             uint32_t *flags = nullptr;
             void *ipc_ws = nullptr, *ipc_flags = nullptr;  // cudaIpcOpenMemHandle results (multi-process)
         };
@@ -1725,6 +1726,7 @@ pbng_status peer_setup_group(const std::vector<pbng_ctx *> &ranks) {
             for (int k = 0; k < 3; ++k) P.x[k] = d->L.xbuf[k];
             P.stride = d->prob.x_stride;
             P.sh = d->prob.lane_shift;
+            P.n_local = d->n_local;
             P.flags = d->peer.flags;
         }
         c->peer.enabled = true;
@@ -1740,7 +1742,8 @@ struct PeerHello {
     uint64_t ws_off;     // the workspace's offset inside the allocation the handle names
     uint64_t x_off[3];   // position buffers, bytes from the workspace base
     int64_t x_stride;
-    int32_t sh, nbr;     // nbr: this rank exchanges rows with the receiving rank (filled per reader)
+    int32_t sh, pad;
+    int64_t n_local;     // vertices this rank holds
 };
 
 // one process per GPU: IPC handles of the workspace allocation and the flag words, and the neighbours'
@@ -1770,6 +1773,7 @@ pbng_status peer_setup_comm(pbng_ctx *c) {
     for (int k = 0; k < 3; ++k) me.x_off[k] = (uint64_t)(static_cast<char *>(c->L.xbuf[k]) - static_cast<char *>(c->ws));
     me.x_stride = c->prob.x_stride;
     me.sh = c->prob.lane_shift;
+    me.n_local = c->n_local;
     PeerHello *d_all = nullptr;
     PBNG_CUDA(cudaMalloc(reinterpret_cast<void **>(&d_all), sizeof(PeerHello) * (size_t)n_ranks), "peer halo: allocation");
     std::vector<PeerHello> all(n_ranks);
@@ -1808,6 +1812,7 @@ pbng_status peer_setup_comm(pbng_ctx *c) {
         for (int k = 0; k < 3; ++k) P.x[k] = ws + all[q].x_off[k];
         P.stride = all[q].x_stride;
         P.sh = all[q].sh;
+        P.n_local = all[q].n_local;
         P.flags = static_cast<uint32_t *>(P.ipc_flags);
     }
     c->peer.enabled = true;
@@ -1892,6 +1897,7 @@ struct Exchange {
                 for (int k = 0; k < 3; ++k) A.peer_x[k] = P.x[k];
                 A.peer_stride = P.stride;
                 A.peer_sh = P.sh;
+                A.peer_n_vertices = P.n_local;
                 A.wait_flag = c->peer.flags + n_ranks + q;
                 A.wait_val = E - 1;
                 A.sig_flag = P.flags + c->rank;

@@ -191,6 +191,7 @@ struct PeerPush {
     void *peer_x[3] = {nullptr, nullptr, nullptr};  // the neighbour's xbuf[0..2] through the peer mapping
     int64_t peer_stride = 0;
     int peer_sh = 0;
+    int64_t peer_n_vertices = 0;    // vertices the neighbour holds (PBNG_DEBUG bound of `rows`)
     const uint32_t *wait_flag = nullptr;  // own done[q] (null: ordering by the stream alone)
     uint32_t wait_val = 0;
     uint32_t *sig_flag = nullptr;         // the neighbour's pushed[this rank] (null: none)

@@ -2322,6 +2322,8 @@ __global__ void __launch_bounds__(256) halo_push_kernel(const Layout L, const Pe
     const int64_t b = blockIdx.y;
     if (i < P.n) {
         const int32_t src = P.idx[i], dst = P.rows[i];
+        PBNG_CHECK(src >= 0 && src < L.n_vertices);          // an owned row of this rank
+        PBNG_CHECK(dst >= 0 && dst < P.peer_n_vertices);     // a row the neighbour holds (its ghost)
 #pragma unroll
         for (int k = 0; k < 3; ++k)
             if (k < P.nf) {

@@ -5,7 +5,7 @@ allows it (`compute-sanitizer --tool memcheck python tools/sanitize_paths.py`; t
 Paths: colour launches (thread-per-vertex, split 2/4/8) and the pipelined schedule for Neo-Hookean,
 fixed-corotated and stable Neo-Hookean in fp32 and fp64 with no / SOR / Chebyshev acceleration; the
 sample-minor batched kernels (scalar and packed two-group); backward Euler; weak constraints; the
-domain-decomposition halo pack / unpack (loopback, overlapped); contact detection + incremental
+domain-decomposition halo pack / unpack and peer-store push (loopback, overlapped); contact detection + incremental
 recolouring; energy / residual; positions in / out."""
 import os
 import sys
@@ -66,11 +66,28 @@ def main():
         ctxs, _ = dd.loopback_contexts(s, 2, dtype="f32")
         grp = dd.Group(ctxs)
         grp.iterate(2, s.accel, s.omega, s.rho, s.gamma)
+        # the peer-store transport: rows stored straight into the other rank's ghost rows (bounds asserted)
+        grp.set_transport("peer")
+        grp.iterate(2, s.accel, s.omega, s.rho, s.gamma)
+        for c in ctxs:
+            E, R = c.energy_residual()
+            assert np.all(np.isfinite(E)) and np.all(np.isfinite(R))
         grp.close()
         torch.cuda.synchronize()
         for c in ctxs:
             c.close()
-        print(f"dd config {cfg}", flush=True)
+        print(f"dd config {cfg} (copies + peer stores)", flush=True)
+    s = G.config4_batched(n_samples=40, n=4, iterations=4)
+    ctxs, _ = dd.loopback_contexts(s, 3, dtype="f32")
+    grp = dd.Group(ctxs)
+    grp.set_transport("peer")
+    grp.iterate(3, s.accel, s.omega, s.rho, s.gamma)
+    for c in ctxs:
+        c.energy_residual()
+    grp.close()
+    for c in ctxs:
+        c.close()
+    print("dd batched sample-minor layout, 3 ranks, peer stores", flush=True)
     # path-ordered NH records: config 3 at a size where one warp per chunk is chosen (sweep_kernel path
     # mode), the batched sh-6 layout (path records), its windowed persistent schedule, a disconnected link
     s = G.config3_hetero_cube(n=80)
