@@ -434,11 +434,25 @@ def run_ours(args):
         pg.all_reduce(t)
         return float(t.item())
 
+    colours = None
+    if args.colouring == "kuhn4":
+        from scenes import generators as G
+        if config == 3:
+            colours = G.kuhn_grid_colouring(128, 128, 128)
+        elif config == 4:
+            colours = G.kuhn_grid_colouring(16, 16, 16)
+        elif config == 5:
+            # block b shifted by b so that the binding springs' end nodes (top of b, bottom of b + 1) differ
+            one = G.kuhn_grid_colouring(48, 48, 48)
+            colours = np.concatenate([(one + b) % 4 for b in range(8)]).astype(np.int32)
+        else:
+            raise SystemExit("--colouring kuhn4: configs 3, 4 and 5 (config 2 diverges on it under its Chebyshev "
+                             "blend, in the oracle too: DESIGN.md section 7)")
     # ---- same-invocation 1-GPU anchor of the sharded config: rank 0 solves the whole batch alone ----
     anchor = None
     if world > 1 and config == 4:
         if rank == 0:
-            a = Solver(full, config, local, dev, stream, 1, 0, False, args.dtype, None)
+            a = Solver(full, config, local, dev, stream, 1, 0, False, args.dtype, None, colours=colours)
             for _ in range(args.warmup):
                 a.step()
             ta, _ = timed(a.step, args.steps, stream, dev, lambda: None)
@@ -449,12 +463,6 @@ def run_ours(args):
             torch.cuda.empty_cache()
         barrier()
 
-    colours = None
-    if args.colouring == "kuhn4":
-        if config != 3:
-            raise SystemExit("--colouring kuhn4 applies to config 3 (one Kuhn grid)")
-        from scenes import generators as G
-        colours = G.kuhn_grid_colouring(128, 128, 128)
     S = Solver(scene, config, local, dev, stream, world, rank, decomposed, args.dtype, pg, args.halo, colours)
     ctx, q = S.ctx, S.q
     for _ in range(args.warmup):
@@ -544,8 +552,8 @@ def main():
                     help="override the config's compute dtype (e.g. config 3 in fp64: the FP64 measurement variant)")
     ap.add_argument("--dd", action="store_true", help="N > 1: domain-decompose one mesh (z slabs) instead of replicas")
     ap.add_argument("--colouring", default="greedy", choices=["greedy", "kuhn4"],
-                    help="config 3: the paper's greedy colouring (default, 8 colours) or the caller-supplied "
-                         "4-colouring (i + j + k) mod 4 of the Kuhn grid through pbng_color_given")
+                    help="the paper's greedy colouring (default, 8 colours) or, configs 3-5, the caller-supplied "
+                         "4-colouring (i + j + k) mod 4 of the Kuhn grid(s) through pbng_color_given")
     ap.add_argument("--halo", default=os.environ.get("PBNG_BENCH_HALO", "nccl"), choices=["nccl", "peer"],
                     help="decomposed runs: per-colour halo by NCCL send/receive (default) or by peer stores "
                          "(pbng_enable_peer_halo: one kernel per neighbour writes its ghost rows over NVLink)")
