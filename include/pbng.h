@@ -287,9 +287,10 @@ pbng_status pbng_halo_unpack(pbng_ctx *ctx, int32_t colour, int32_t peer, int32_
  *   the handles and each neighbour's ghost-row lists travel once over NCCL, and the neighbours' memory is
  *   mapped with cudaIpcOpenMemHandle (the workspace must come from cudaMalloc, e.g. PyTorch's default
  *   allocator; the GPUs need peer access).  pbng_iterate then runs, per colour pass E:
- *   wait until the neighbours' rows of pass E-1 have landed -> part 1 -> per neighbour, on the side stream,
- *   ONE kernel { wait until that neighbour has finished pass E-1; store this rank's boundary rows straight
- *   into its ghost rows; raise its `pushed` flag } while part 2 runs -> raise the neighbours' `done` flag.
+ *   part 1 -> per neighbour, on the side stream, ONE kernel { wait until that neighbour has finished pass
+ *   E-1 (its `done` flag here); store this rank's boundary rows straight into its ghost rows; raise the
+ *   `pushed` flag there } while part 2 runs -> ONE sync kernel { raise the neighbours' `done` flags; wait
+ *   until the rows the neighbours store in pass E have landed (their `pushed` flags here) }.
  *   No pack / unpack kernels, no NCCL call per colour (one all-reduce barrier per pbng_iterate call).
  *   A signal that does not arrive within PBNG_PEER_TIMEOUT_MS (environment, default 20000) makes the next
  *   synchronising call return PBNG_E_CUDA instead of hanging.  enable = 0 returns to NCCL send / receive.
