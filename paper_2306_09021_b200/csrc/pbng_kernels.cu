@@ -2332,13 +2332,20 @@ __global__ void __launch_bounds__(256) halo_push_kernel(const Layout L, const Pe
             }
     }
     if (P.sig_flag) {
-        __threadfence_system();  // this thread's peer stores are performed before the block is counted
+        // the CTA barrier orders every thread's peer stores before thread 0's system-scope fence (fences are
+        // cumulative over what the barrier made visible to thread 0), so ONE fence.sys per CTA -- not one per
+        // thread -- puts the block's rows before its count; the last block's release store then publishes all
         __syncthreads();
         if (threadIdx.x == 0) {
             const unsigned total = gridDim.x * gridDim.y;
+            if (total == 1) {  // one CTA (the usual halo size): the release store alone publishes its rows
+                st_release_sys(P.sig_flag, P.sig_val);
+                return;
+            }
+            __threadfence_system();
             if (atomicAdd(P.counter, 1u) == total - 1) {  // last block: every block's rows have landed
                 *P.counter = 0;
-                __threadfence_system();
+                __threadfence_system();  // pairs with the other blocks' fences through the counter
                 st_release_sys(P.sig_flag, P.sig_val);
             }
         }
@@ -2352,10 +2359,7 @@ __global__ void halo_sync_kernel(const PeerSignal S, const PeerWait W, int32_t *
     // records (static data) and block in griddepcontrol.wait until this kernel -- i.e. the flag wait -- is done
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int t = threadIdx.x;
-    if (t < S.n) {
-        __threadfence_system();
-        st_release_sys(S.flag[t], S.val);
-    }
+    if (t < S.n) st_release_sys(S.flag[t], S.val);  // release: after everything earlier in the stream
     if (t < W.n) peer_wait(W.flags + W.slot[t], W.want, err, W.timeout_ns);
 }
 
